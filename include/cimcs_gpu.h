@@ -1,0 +1,169 @@
+/*
+ * cimcs_gpu.h -- C ABI of the B200 MFZ-CIM L0RBCS hot path (libcimcs_gpu.so).
+ *
+ * The reference (arXiv 2405.00366, /root/reference/proj) is CPU-only C++;
+ * its solver seams are C++ (std::function closures, Eigen vectors).  This
+ * header is the thin C layer the reference's solver API calls into so the
+ * GPU path is a drop-in.  Every entry point names the reference interface it
+ * replaces (paths relative to /root/reference/proj).  Plain pointers and
+ * sizes only; all host buffers are caller-owned; every call is synchronous
+ * on return.  Host vectors are trajectory-major: element (b, r, i) of a
+ * B x R x N array is at ((b * R) + r) * N + i, where b = instance,
+ * r = replica, i = spin.
+ *
+ * Status codes mirror the reference's exception types (types.hpp:16-33):
+ *   0 ok, 1 input_error, 2 config_error, 3 divergence_error, 4 cuda error.
+ * The message of the last failing call on this thread: cimcs_last_error().
+ */
+#ifndef CIMCS_GPU_H
+#define CIMCS_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CIMCS_ABI_VERSION 1
+
+enum { CIMCS_OK = 0, CIMCS_INPUT_ERROR = 1, CIMCS_CONFIG_ERROR = 2,
+       CIMCS_DIVERGENCE = 3, CIMCS_CUDA_ERROR = 4 };
+enum { CIMCS_F32 = 0, CIMCS_F64 = 1 };
+/* == Backend {MfzCN, MfzBN, PositiveP}, orchestrator.hpp:28 (PositiveP: not on this path) */
+enum { CIMCS_MFZ_CN = 0, CIMCS_MFZ_BN = 1, CIMCS_PP = 2 };
+/* == CdpMethod {Jacobi, ConjugateGradient}, cdp.hpp:60 */
+enum { CIMCS_CDP_JACOBI = 0, CIMCS_CDP_CG = 1 };
+enum { CIMCS_PUMP_SIGMOID = 0, CIMCS_PUMP_LINEAR = 1 };
+
+/* HyperParams, types.hpp:77-96, plus the two BASELINE-config extensions
+ * (linear pump ramp).  Field order is part of the ABI. */
+typedef struct cimcs_hyper {
+    double g2, j, K, beta, tau, dt;
+    int32_t n_steps;
+    double p_thr, d, eta_init, eta_end;
+    int32_t velo;
+    double dt_c;
+    int32_t jacobi_iters, cg_max_iters;
+    double cg_tol, gamma;
+    int32_t mfz_loss_minus_j;
+    double mu_abort;
+    int32_t pump_kind;   /* CIMCS_PUMP_SIGMOID (reference, orchestrator.cpp:12-14) or LINEAR */
+    double pump_end;     /* LINEAR: p(t) = (pump_end * t) / (n_steps * dt) */
+} cimcs_hyper;
+
+/* AlternationRecord, orchestrator.hpp:100-111 (seconds omitted; support added) */
+typedef struct cimcs_record {
+    int32_t i, support;
+    double eta, hamiltonian, rmse, hamming, min_e, median_e;
+} cimcs_record;
+
+/* Device-side timing of the last solve/run_cim, CUDA events on the context
+ * stream; launches = number of this library's kernels launched. */
+typedef struct cimcs_timing {
+    double total_ms;      /* whole call, device time */
+    double gram_ms;       /* K1 builder */
+    double cim_ms;        /* K2 fused Euler steps (all alternations) */
+    double refit_ms;      /* K3 masked Jacobi refit */
+    double score_ms;      /* K4 scorer + median */
+    double h2d_ms, d2h_ms;
+    int64_t step_launches, refit_launches, other_launches;
+    double step_bytes;    /* algorithmic bytes of one step launch (G share, dense) */
+    double step_flops;    /* algorithmic flops of one step launch (2 N^2 R B) */
+} cimcs_timing;
+
+typedef struct cimcs_ctx cimcs_ctx;
+
+/* ---------------------------------------------------------- utilities */
+int cimcs_abi_version(void);
+const char* cimcs_last_error(void);
+/* types.hpp:77-96 / :98-106 */
+void cimcs_hyper_default(cimcs_hyper* h);
+int cimcs_hyper_validate(const cimcs_hyper* h);
+/* splitmix64 seed mixing, tools/main.cpp:263-268 */
+uint64_t cimcs_mix_seed(uint64_t base, uint64_t salt);
+/* The fixed summation order of every G*v contraction (fp64 path is bitwise
+ * reproducible against the oracle's ORC_CANON mode with these values). */
+int cimcs_gemv_order(int dtype, int32_t* nseg, int32_t* gran);
+
+/* Host instance generator: gen_instance, datagen.cpp:15-55 (same seeded
+ * stream and draw order; std::mt19937_64 + Box-Muller as rng.hpp:21-64).
+ * A is M x N column-major (ProblemInstance::A layout). */
+int cimcs_gen_dims(int32_t N, double alpha, double a, int32_t* M, int32_t* K);
+int cimcs_gen_instance(int32_t N, double alpha, double a, double nu, uint64_t seed,
+                       double* A, double* y, double* x_true, int32_t* xi_true);
+/* Batch of instances on `threads` host threads (instance_grid/run_jobs,
+ * tools/main.cpp:305-344).  Arrays of per-instance pointers. */
+int cimcs_gen_instances(int32_t B, int32_t N, const double* alpha, const double* a,
+                        const double* nu, const uint64_t* seeds, double* const* A,
+                        double* const* y, double* const* x_true, int32_t* const* xi_true,
+                        int32_t threads);
+
+/* ------------------------------------------------------------ context */
+/* One per host thread; owns device buffers, one CUDA stream and graphs. */
+int cimcs_create(int32_t device, int32_t dtype, cimcs_ctx** out);
+void cimcs_destroy(cimcs_ctx* ctx);
+/* key: "host_threads" (c0 generator pool), "use_graphs" (0/1), "sparse_skip" (0/1). */
+int cimcs_set_option(cimcs_ctx* ctx, const char* key, int64_t value);
+
+/* B problems of equal N (make_problem(inst), orchestrator.cpp:80-99).
+ * A[b]: M[b] x N column-major, y[b]: M[b].  x_true/xi_true may be NULL
+ * (metrics then NaN, as SolverProblem::rmse_at, orchestrator.cpp:70-78). */
+int cimcs_set_problems(cimcs_ctx* ctx, int32_t B, int32_t N, const int32_t* M,
+                       const double* const* A, const double* const* y,
+                       const double* const* x_true, const int32_t* const* xi_true);
+/* K1: G = A^T A (gram, full diagonal), hz = A^T y, D = diag(G), device
+ * resident.  Replaces coupling_from_observation (model.cpp:54-63) and the
+ * per-step matrix-free A^T(A w) (orchestrator.cpp:86-88): J w = D∘w - G w. */
+int cimcs_build_coupling(cimcs_ctx* ctx);
+/* Copy instance b's coupling back (fp64 host buffers; N*N, N, N).  Test aid. */
+int cimcs_get_coupling(cimcs_ctx* ctx, int32_t b, double* G, double* hz, double* D);
+
+/* One Euler step for all B x R trajectories from given (c, e):
+ * local_field_{continuous,binarized} (solver_mfz.cpp:33-59) + mfz_step
+ * (:61-88).  h_out (optional) receives the local field.  fail_index[b*R+r]
+ * = first non-finite spin or -1.  Returns 3 if any trajectory diverged. */
+int cimcs_mfz_step(cimcs_ctx* ctx, int32_t R, int32_t backend, const cimcs_hyper* hp,
+                   double eta, double p, const double* Rsig, const double* c,
+                   const double* e, double* c_out, double* e_out, double* h_out,
+                   int32_t* fail_index);
+
+/* One CIM call for all B x R trajectories: run_cim / run_mfz
+ * (orchestrator.cpp:140-161, solver_mfz.cpp:90-124).  c0 = the initial
+ * amplitudes (0.01 * gauss from each trajectory's stream, init_mfz
+ * solver_mfz.cpp:24-31); per-trajectory divergence freezes that
+ * trajectory only (fail_index >= 0) and the call returns 3. */
+int cimcs_run_cim(cimcs_ctx* ctx, int32_t R, int32_t backend, const cimcs_hyper* hp,
+                  double eta, const double* Rsig, const double* c0, double* c_out,
+                  double* e_out, int32_t* sigma_out, double* min_e, int32_t* fail_index);
+
+/* Masked refit on each trajectory's support: cdp_minimize with damped
+ * Jacobi (cdp.cpp:48-64, 132-139).  Entries with sigma = 0 are returned
+ * bitwise untouched.  Singular active diagonal -> input_error. */
+int cimcs_refit(cimcs_ctx* ctx, int32_t R, const int32_t* sigma, const double* R_prev,
+                double* R_out, const cimcs_hyper* hp);
+
+/* K4 scorer: objective_at (orchestrator.cpp:57-62), rmse / hamming_loss
+ * (model.cpp:128-153).  Outputs are B x R. */
+int cimcs_score(cimcs_ctx* ctx, int32_t R, const double* Rsig, const int32_t* sigma,
+                double lambda, double* objective, double* rmse, double* hamming);
+
+/* The whole alternating loop for all B x R trajectories:
+ * alternating_minimize (orchestrator.cpp:170-235) with R_init = hz
+ * (default_r_init, :138) unless R_init != NULL.  seeds[b*R + r] seeds
+ * trajectory (b, r)'s std::mt19937_64 stream (the reference's Rng), which
+ * supplies N normals per alternation for c0.  hist holds (velo+1)*B*R
+ * records, trajectory-major; n_hist[b*R+r] = recorded alternations;
+ * fail_alt = alternation that diverged or -1 (AlternatingResult::failed,
+ * orchestrator.hpp:113-124).  cdp must be CIMCS_CDP_JACOBI. */
+int cimcs_solve(cimcs_ctx* ctx, int32_t R, int32_t backend, const cimcs_hyper* hp,
+                int32_t cdp, const uint64_t* seeds, const double* R_init,
+                int32_t track_best, double* R_out, int32_t* sigma_out,
+                cimcs_record* hist, int32_t* n_hist, int32_t* fail_alt,
+                int32_t* fail_index);
+
+int cimcs_get_timing(const cimcs_ctx* ctx, cimcs_timing* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,576 @@
+// kernels.cuh -- sm_100a kernels of the MFZ-CIM L0RBCS hot path.
+//
+// Compiled with -fmad=false: every elementwise expression keeps the
+// reference's association and rounding (solver_mfz.cpp:61-88, cdp.cpp:60-61);
+// the only fused multiply-adds are the explicit fma() of the G*v contraction
+// and of the Gram build, whose order is the documented canonical order that
+// the oracle's ORC_CANON mode restates.
+//
+// Device layout (per context, B instances, ldN = round_up(N, 32), NR =
+// replica slots, a power of two <= 16):
+//   G   [B][ldN][ldN]  gram A^T A (symmetric, full diagonal), zero padded
+//   D   [B][ldN]       diag(G)          hz [B][ldN]  A^T y
+//   Rs, C, E, W0, W1   [B][ldN][NR]     signal, amplitude, error, contraction input
+// A trajectory (b, r) owns column r of every [B][ldN][NR] array.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cimcs {
+
+constexpr int kSeg = 8;            // consumer warps = canonical segments
+constexpr int kGran = 8;           // consecutive j per warp per chunk
+constexpr int kChunk = kSeg * kGran;  // j per pipeline stage
+constexpr int kThreads = (kSeg + 1) * 32;  // + 1 producer warp
+constexpr int kFreeTraj = 0x7fffffff;      // fail_gstep of a healthy trajectory
+constexpr int kInactiveTraj = -2;          // padded replica slot
+
+template <typename T> struct Cfg;
+template <> struct Cfg<float> {
+    static constexpr int RPL = 4;     // rows per lane
+    static constexpr int kStages = 3;
+    static constexpr int kMinBlocks = 2;
+};
+template <> struct Cfg<double> {
+    static constexpr int RPL = 2;
+    static constexpr int kStages = 3;
+    static constexpr int kMinBlocks = 1;
+};
+
+template <typename T> __host__ __device__ constexpr int row_block() { return 32 * Cfg<T>::RPL; }
+template <typename T> __host__ __device__ constexpr int red_pitch() { return row_block<T>() + 2; }
+
+template <typename T, int NR>
+__host__ __device__ constexpr size_t stage_bytes() {
+    return (size_t)kChunk * row_block<T>() * sizeof(T) + (size_t)kChunk * NR * sizeof(T);
+}
+template <typename T, int NR>
+__host__ __device__ constexpr size_t gemv_smem_bytes() {
+    size_t pipe = Cfg<T>::kStages * stage_bytes<T, NR>();
+    size_t red = (size_t)kSeg * NR * red_pitch<T>() * sizeof(T);
+    size_t body = pipe > red ? pipe : red;
+    return body + 1024;  // + mbarriers
+}
+
+// Mode of the fused epilogue that follows the G*v contraction.
+enum : int { EPI_STEP_BN = 1, EPI_STEP_CN = 0, EPI_JACOBI = 2, EPI_SCORE = 3 };
+
+// Per-call scalars (host-computed in fp64 exactly as the reference does).
+struct StepScalars {
+    double dt, half_rt, rt, tau, nbeta, Kj, loss_off, minus_j;  // loss = (-1+p) [- j]
+    double one_minus_dtc, dt_c;
+    int n_steps;
+};
+
+// Per-alternation values read by graph-captured kernels from device memory.
+struct AltParams {
+    double thresh;     // ((eta*eta)/4.0)*rt
+    double lambda;     // (eta*eta)/2.0
+    double eta;
+    int alt;           // alternation index
+    int gstep_base;    // alt * n_steps
+};
+
+struct GemvArgs {
+    const void* G;       // [B][ldN][ldN]
+    const void* D;       // [B][ldN]
+    const void* hz;      // [B][ldN]
+    const void* Win;     // [B][ldN][NR]
+    void* Wout;
+    void* Rs;            // signal (in/out for Jacobi)
+    void* C;
+    void* E;
+    void* Hdbg;          // optional local-field dump [B][ldN][NR]
+    const int8_t* sigma; // [B][ldN][NR]  (Jacobi / score)
+    int* fail_gstep;     // [B*NR]
+    int* fail_idx;       // [B*NR]
+    unsigned long long* minE;  // [B*NR] order-preserving encoding
+    double* part;        // score partials [B][nRB][NR][4]
+    const double* pump;  // [n_steps] (step mode; NULL -> p_scalar)
+    const AltParams* alt;
+    const double* xtrue; // [B][ldN]  (score; may be NULL)
+    const int8_t* xitrue;
+    int* err;            // singular-diagonal report (Jacobi)
+    double p_scalar;
+    int step;            // step index inside the alternation
+    int N, ldN, B;
+    StepScalars s;
+};
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+        "[%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void consumer_bar() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kSeg * 32) : "memory");
+}
+
+// Order-preserving integer image of a float / double (for atomicMin).
+__device__ __forceinline__ unsigned long long ord_key(double v) {
+    unsigned long long u = (unsigned long long)__double_as_longlong(v);
+    return (u & 0x8000000000000000ULL) ? ~u : (u | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ unsigned long long ord_key(float v) {
+    return ord_key((double)v);  // exact widening keeps the order
+}
+__host__ __device__ inline double ord_val(unsigned long long k) {
+    unsigned long long u = (k & 0x8000000000000000ULL) ? (k & 0x7fffffffffffffffULL) : ~k;
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double((long long)u);
+#else
+    double d;
+    memcpy(&d, &u, 8);
+    return d;
+#endif
+}
+
+__device__ __forceinline__ bool finite_(double v) { return isfinite(v); }
+__device__ __forceinline__ bool finite_(float v) { return isfinite(v); }
+
+template <typename T>
+__device__ __forceinline__ T fma_(T a, T b, T c);
+template <>
+__device__ __forceinline__ float fma_<float>(float a, float b, float c) {
+    return __fmaf_rn(a, b, c);
+}
+template <>
+__device__ __forceinline__ double fma_<double>(double a, double b, double c) {
+    return __fma_rn(a, b, c);
+}
+
+// -------------------------------------------------------- contraction core
+// One CTA = (instance b, RB rows).  Warps 0..7 consume; warp 8 produces.
+// Chunk c covers j in [64c, 64c + 64); consumer warp w handles
+// j in [64c + 8w, 64c + 8w + 8) with a sequential fma chain into its own
+// accumulators (canonical segment w); the 8 segment partials are then added
+// left to right.  G is read through its symmetry: the G tile of chunk c is
+// rows j of G restricted to the CTA's columns [i0, i0 + RB) -- contiguous,
+// one bulk copy per row.
+template <typename T, int NR, int MODE>
+__global__ void __launch_bounds__(kThreads, Cfg<T>::kMinBlocks) gemv_fused_kernel(GemvArgs a) {
+    constexpr int RPL = Cfg<T>::RPL;
+    constexpr int RB = row_block<T>();
+    constexpr int S = Cfg<T>::kStages;
+    constexpr int RBP = red_pitch<T>();
+    extern __shared__ __align__(1024) unsigned char smem[];
+
+    const int b = blockIdx.y;
+    const int i0 = blockIdx.x * RB;
+    const int N = a.N, ldN = a.ldN;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // stage s: G tile [kChunk][RB] followed by the W chunk [kChunk][NR]
+    auto stageG = [&](int s) { return reinterpret_cast<T*>(smem + s * stage_bytes<T, NR>()); };
+    auto stageW = [&](int s) { return stageG(s) + kChunk * RB; };
+    size_t body = S * stage_bytes<T, NR>();
+    const size_t red_b = (size_t)kSeg * NR * RBP * sizeof(T);
+    if (red_b > body) body = red_b;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + body);
+    uint64_t* empty = full + S;
+    __shared__ unsigned long long s_min[kSeg][NR];
+    __shared__ int s_frozen[NR];
+
+    const size_t gbase = (size_t)b * ldN * ldN;
+    const T* Gb = static_cast<const T*>(a.G) + gbase;
+    const T* Wb = static_cast<const T*>(a.Win) + (size_t)b * ldN * NR;
+    const int nchunks = (N + kChunk - 1) / kChunk;
+    const int ncols = min(RB, ldN - i0);  // valid (padded) columns of the tile
+    const uint32_t row_bytes = (uint32_t)ncols * sizeof(T);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kSeg);
+        }
+        mbar_fence_init();
+    }
+    if (threadIdx.x < NR) {
+        const int g = a.fail_gstep ? a.fail_gstep[b * NR + threadIdx.x] : kFreeTraj;
+        int frozen;
+        if (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN)
+            frozen = g < a.alt->gstep_base + a.step;  // failed at an earlier step
+        else
+            frozen = g != kFreeTraj;
+        s_frozen[threadIdx.x] = frozen;
+    }
+    __syncthreads();
+
+    if (warp == kSeg) {
+        // ---------------- producer warp: bulk copies G rows + W chunk
+        for (int c = 0; c < nchunks; ++c) {
+            const int s = c % S;
+            if (c >= S) mbar_wait(&empty[s], ((c / S) - 1) & 1);
+            const int j0 = c * kChunk;
+            const int nj = min(kChunk, N - j0);
+            const int njw = min(kChunk, ldN - j0);  // W rows (zero padded to ldN)
+            const uint32_t wbytes = (uint32_t)njw * NR * sizeof(T);
+            if (lane == 0) mbar_arrive_expect_tx(&full[s], nj * row_bytes + wbytes);
+            __syncwarp();
+            for (int r = lane; r < nj; r += 32)
+                bulk_g2s(stageG(s) + r * RB, Gb + (size_t)(j0 + r) * ldN + i0, row_bytes,
+                         &full[s]);
+            if (lane == 0) bulk_g2s(stageW(s), Wb + (size_t)j0 * NR, wbytes, &full[s]);
+        }
+        return;
+    }
+
+    // -------------------- consumer warps: segmented fma chains
+    T acc[RPL][NR];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r)
+#pragma unroll
+        for (int q = 0; q < NR; ++q) acc[r][q] = T(0);
+
+    for (int c = 0; c < nchunks; ++c) {
+        const int s = c % S;
+        mbar_wait(&full[s], (c / S) & 1);
+        const int jw = c * kChunk + warp * kGran;
+        const int nv = min(kGran, N - jw);
+        const T* gs = stageG(s) + (warp * kGran) * RB + lane * RPL;
+        const T* ws = stageW(s) + (warp * kGran) * NR;
+#pragma unroll
+        for (int jj = 0; jj < kGran; ++jj) {
+            if (jj < nv) {
+                T g[RPL];
+                if constexpr (sizeof(T) == 4) {
+                    const float4 v = *reinterpret_cast<const float4*>(gs + jj * RB);
+                    g[0] = v.x; g[1] = v.y; g[2] = v.z; g[3] = v.w;
+                } else {
+                    const double2 v = *reinterpret_cast<const double2*>(gs + jj * RB);
+                    g[0] = v.x; g[1] = v.y;
+                }
+                T w[NR];
+                if constexpr (sizeof(T) == 4 && NR % 4 == 0) {
+#pragma unroll
+                    for (int q = 0; q < NR / 4; ++q) {
+                        const float4 v = *reinterpret_cast<const float4*>(ws + jj * NR + 4 * q);
+                        w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+                    }
+                } else if constexpr (sizeof(T) == 8 && NR % 2 == 0) {
+#pragma unroll
+                    for (int q = 0; q < NR / 2; ++q) {
+                        const double2 v = *reinterpret_cast<const double2*>(ws + jj * NR + 2 * q);
+                        w[2 * q] = v.x; w[2 * q + 1] = v.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < NR; ++q) w[q] = ws[jj * NR + q];
+                }
+#pragma unroll
+                for (int r = 0; r < RPL; ++r)
+#pragma unroll
+                    for (int q = 0; q < NR; ++q) acc[r][q] = fma_<T>(g[r], w[q], acc[r][q]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+
+    // ----------------------------------------- segment partials -> smem
+    consumer_bar();  // every stage consumed before the buffer is reused
+    T* red = reinterpret_cast<T*>(smem);
+#pragma unroll
+    for (int q = 0; q < NR; ++q)
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) red[(warp * NR + q) * RBP + lane * RPL + r] = acc[r][q];
+    consumer_bar();
+
+    // ------------------------------------------------- fused epilogue
+    const int t = threadIdx.x;  // 0 .. 255
+    const int q = t % NR;       // every output of this thread has replica q
+    const bool frozen = s_frozen[q];
+    T local_min = T(INFINITY);
+    double sA = 0.0, sB = 0.0, sC = 0.0;  // score partials
+    const StepScalars& sc = a.s;
+    for (int o = t; o < RB * NR; o += kSeg * 32) {
+        const int row = o / NR;
+        const int i = i0 + row;
+        if (i >= N) break;
+        T gw = red[(0 * NR + q) * RBP + row];
+#pragma unroll
+        for (int w = 1; w < kSeg; ++w) gw = gw + red[(w * NR + q) * RBP + row];
+        const size_t vi = ((size_t)b * ldN + i) * NR + q;
+        const size_t si = (size_t)b * ldN + i;
+        if (frozen) continue;
+        if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
+            const T* Cp = static_cast<const T*>(a.C);
+            const T* Ep = static_cast<const T*>(a.E);
+            const T wv = static_cast<const T*>(a.Win)[vi];
+            const T Dv = static_cast<const T*>(a.D)[si];
+            const T hzv = static_cast<const T*>(a.hz)[si];
+            const T Rv = static_cast<const T*>(a.Rs)[vi];
+            const T c = Cp[vi];
+            const T e = Ep[vi];
+            const T Jw = Dv * wv - gw;  // apply_coupling: gram_diag∘w - G w
+            const T half_rt = (T)sc.half_rt;
+            T h;
+            if constexpr (MODE == EPI_STEP_BN)
+                h = half_rt * (Jw + hzv);
+            else
+                h = Jw + half_rt * hzv;
+            if (a.Hdbg) static_cast<T*>(a.Hdbg)[vi] = h;
+            const double pd = a.pump ? a.pump[a.step] : a.p_scalar;
+            const T loss = sc.minus_j != 0.0 ? (T)((-1.0 + pd) - sc.minus_j) : (T)(-1.0 + pd);
+            const T thresh = (T)a.alt->thresh;
+            const T inj = ((T)sc.Kj * e) * (Rv * h - thresh);
+            const T cn = c + (T)sc.dt * ((loss - c * c) * c + inj);
+            const T en = e + (T)sc.dt * (((T)sc.nbeta * (c * c - (T)sc.tau)) * e);
+            if (!finite_(cn) || !finite_(en)) {
+                const int traj = b * NR + q;
+                atomicMin(&a.fail_gstep[traj], a.alt->gstep_base + a.step);
+                atomicMin(&a.fail_idx[traj], i);
+                continue;
+            }
+            static_cast<T*>(a.C)[vi] = cn;
+            static_cast<T*>(a.E)[vi] = en;
+            T wn;
+            if constexpr (MODE == EPI_STEP_BN)
+                wn = Rv * (cn > T(0) ? T(1) : T(0));
+            else
+                wn = (Rv * T(0.25)) * (cn + (T)sc.rt);
+            static_cast<T*>(a.Wout)[vi] = wn;
+            local_min = en < local_min ? en : local_min;
+        } else if constexpr (MODE == EPI_JACOBI) {
+            // cdp.cpp:60-61: offdiag = G R - D∘R; R = (1-dt_c) R + dt_c (b - offdiag) / D
+            T* Rp = static_cast<T*>(a.Rs);
+            const T Rv = Rp[vi];
+            const bool on = a.sigma[vi] != 0;
+            T rn = Rv;
+            if (on) {
+                const T Dv = static_cast<const T*>(a.D)[si];
+                if (Dv == T(0)) {
+                    atomicMin(a.err, i);
+                    continue;
+                }
+                const T off = gw - Dv * Rv;
+                const T bv = static_cast<const T*>(a.hz)[si];
+                rn = (T)sc.one_minus_dtc * Rv + (T)sc.dt_c * ((bv - off) / Dv);
+                Rp[vi] = rn;
+            }
+            static_cast<T*>(a.Wout)[vi] = rn * (on ? T(1) : T(0));
+        } else {  // EPI_SCORE: w = R∘sigma is Win; partial sums of w.Gw, hz.w, rmse
+            const T wv = static_cast<const T*>(a.Win)[vi];
+            const T hzv = static_cast<const T*>(a.hz)[si];
+            sA = sA + (double)wv * (double)gw;
+            sB = sB + (double)hzv * (double)wv;
+            if (a.xtrue) {
+                const double xt = a.xitrue[si] ? a.xtrue[si] : 0.0;
+                const double d = (double)wv - xt;
+                sC = sC + d * d;
+            }
+        }
+    }
+
+    if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
+        // per-replica min of e over this CTA, then one atomic per replica
+        unsigned long long k = ord_key(local_min);
+#pragma unroll
+        for (int off = 16; off >= NR; off >>= 1)
+            k = min(k, __shfl_xor_sync(0xffffffffu, k, off));
+        if (lane < NR) s_min[warp][lane] = k;
+        consumer_bar();
+        if (t < NR && !s_frozen[t]) {
+            unsigned long long m = s_min[0][t];
+#pragma unroll
+            for (int w = 1; w < kSeg; ++w) m = min(m, s_min[w][t]);
+            if (m != ord_key(T(INFINITY))) atomicMin(&a.minE[b * NR + t], m);
+        }
+    } else if constexpr (MODE == EPI_SCORE) {
+        // deterministic CTA reduction: lanes with equal q, then warps in order
+#pragma unroll
+        for (int off = 16; off >= NR; off >>= 1) {
+            sA = sA + __shfl_xor_sync(0xffffffffu, sA, off);
+            sB = sB + __shfl_xor_sync(0xffffffffu, sB, off);
+            sC = sC + __shfl_xor_sync(0xffffffffu, sC, off);
+        }
+        double* sred = reinterpret_cast<double*>(smem);  // red no longer needed
+        consumer_bar();
+        if (lane < NR) {
+            sred[(warp * NR + lane) * 3 + 0] = sA;
+            sred[(warp * NR + lane) * 3 + 1] = sB;
+            sred[(warp * NR + lane) * 3 + 2] = sC;
+        }
+        consumer_bar();
+        if (t < NR) {
+            double A_ = 0.0, B_ = 0.0, C_ = 0.0;
+            for (int w = 0; w < kSeg; ++w) {
+                A_ = A_ + sred[(w * NR + t) * 3 + 0];
+                B_ = B_ + sred[(w * NR + t) * 3 + 1];
+                C_ = C_ + sred[(w * NR + t) * 3 + 2];
+            }
+            double* p = a.part + (((size_t)b * gridDim.x + blockIdx.x) * NR + t) * 4;
+            p[0] = A_;
+            p[1] = B_;
+            p[2] = C_;
+        }
+    }
+}
+
+// ---------------------------------------------------------- Gram builder
+// K1: G = A^T A on fp64 CUDA cores.  Each G entry is ONE sequential fma
+// chain over k = 0..M-1 (canonical; restated by the oracle's fma_chain).
+// 64x64 tiles over the upper triangle, mirrored; A is M x N column-major.
+constexpr int kGT = 64, kGK = 16;
+__global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ A, int M, int N,
+                                                   int ldN, size_t a_stride, double* G) {
+    const int b = blockIdx.z;
+    const int bi = blockIdx.y, bj = blockIdx.x;
+    if (bj < bi) return;
+    const double* Ab = A + (size_t)b * a_stride;
+    double* Gb = G + (size_t)b * ldN * ldN;
+    __shared__ double As[kGK][kGT + 2];
+    __shared__ double Bs[kGK][kGT + 2];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int i0 = bi * kGT, j0 = bj * kGT;
+    double acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+    const int lc = threadIdx.x / 4, lk = (threadIdx.x % 4) * 4;  // loader: column, k quad
+    for (int k0 = 0; k0 < M; k0 += kGK) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int k = k0 + lk + u;
+            const int ci = i0 + lc, cj = j0 + lc;
+            As[lk + u][lc] = (k < M && ci < N) ? Ab[(size_t)ci * M + k] : 0.0;
+            Bs[lk + u][lc] = (k < M && cj < N) ? Ab[(size_t)cj * M + k] : 0.0;
+        }
+        __syncthreads();
+        const int kn = min(kGK, M - k0);
+        for (int kk = 0; kk < kn; ++kk) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) av[r] = As[kk][ty * 4 + r];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) bv[c] = Bs[kk][tx * 4 + c];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[r][c] = __fma_rn(av[r], bv[c], acc[r][c]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int i = i0 + ty * 4 + r, j = j0 + tx * 4 + c;
+            if (i < N && j < N) {
+                Gb[(size_t)i * ldN + j] = acc[r][c];
+                Gb[(size_t)j * ldN + i] = acc[r][c];
+            }
+        }
+}
+
+// hz = A^T y (sequential fma chain per column), D = diag(G).
+__global__ void hz_diag_kernel(const double* __restrict__ A, const double* __restrict__ y,
+                               const int* __restrict__ Ms, int N, int ldN, size_t a_stride,
+                               int y_stride, const double* __restrict__ G, double* hz,
+                               double* D, int B) {
+    const int b = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N || b >= B) return;
+    const int M = Ms[b];
+    const double* col = A + (size_t)b * a_stride + (size_t)i * M;
+    const double* yb = y + (size_t)b * y_stride;
+    double acc = 0.0;
+    for (int k = 0; k < M; ++k) acc = __fma_rn(col[k], yb[k], acc);
+    hz[(size_t)b * ldN + i] = acc;
+    D[(size_t)b * ldN + i] = G[(size_t)b * ldN * ldN + (size_t)i * ldN + i];
+}
+
+template <typename T>
+__global__ void convert_kernel(const double* __restrict__ src, T* __restrict__ dst, size_t n) {
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
+         k += (size_t)gridDim.x * blockDim.x)
+        dst[k] = (T)src[k];
+}
+
+// ------------------------------------------------------- state kernels
+// init_mfz (solver_mfz.cpp:24-31) + first contraction input.  c0 host
+// layout [b][r][i] (fp64); device [b][i][r].
+template <typename T, int NR, int BN>
+__global__ void init_state_kernel(const double* __restrict__ c0, int Rreal, int N, int ldN,
+                                  int B, const T* __restrict__ Rs, T* C, T* E, T* W,
+                                  const int* fail_gstep, unsigned long long* minE, double rt,
+                                  const double* __restrict__ e0) {
+    const size_t total = (size_t)B * ldN * NR;
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < total;
+         k += (size_t)gridDim.x * blockDim.x) {
+        const int q = k % NR;
+        const size_t bi = k / NR;
+        const int i = bi % ldN;
+        const int b = bi / ldN;
+        const int traj = b * NR + q;
+        if (i == 0) minE[traj] = ord_key(T(1));
+        if (fail_gstep[traj] != kFreeTraj) continue;
+        if (i >= N || q >= Rreal) {
+            C[k] = T(0);
+            E[k] = T(1);
+            W[k] = T(0);
+            continue;
+        }
+        const size_t hk = ((size_t)b * Rreal + q) * N + i;
+        const T c = (T)c0[hk];
+        C[k] = c;
+        E[k] = e0 ? (T)e0[hk] : T(1);
+        const T R = Rs[k];
+        W[k] = BN ? R * (c > T(0) ? T(1) : T(0)) : (R * T(0.25)) * (c + (T)rt);
+    }
+}
+
+// sigma = [c > 0] (extract_support, orchestrator.cpp:22-27) and the masked
+// refit input V = R∘sigma.  Frozen trajectories keep their last sigma.
+template <typename T, int NR>
+__global__ void support_kernel(const T* __restrict__ C, const T* __restrict__ Rs, int8_t* sig,
+                               T* V, const int* fail_gstep, int N, int ldN, int B) {
+    const size_t total = (size_t)B * ldN * NR;
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < total;
+         k += (size_t)gridDim.x * blockDim.x) {
+        const int q = k % NR;
+        const size_t bi = k / NR;
+        const int i = bi % ldN;
+        const int b = bi / ldN;
+        if (fail_gstep[b * NR + q] != kFreeTraj) continue;
+        const int8_t s = (i < N && C[k] > T(0)) ? 1 : 0;
+        sig[k] = s;
+        V[k] = Rs[k] * (s ? T(1) : T(0));
+    }
+}
+
+}  // namespace cimcs

@@ -1,0 +1,1481 @@
+// runtime.cu -- host runtime + C ABI of libcimcs_gpu.so (see include/cimcs_gpu.h).
+//
+// The alternation driver restates alternating_minimize
+// (orchestrator.cpp:170-235) for B instances x R replicas at once: per
+// alternation one CUDA graph runs init -> n_steps fused Euler steps (K2),
+// one graph runs the support extraction + damped Jacobi refit (K3), one graph
+// runs the scorer (K4).  c0 for the next alternation is drawn on a host
+// thread pool from each trajectory's std::mt19937_64 stream while the GPU
+// runs the current one.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/cimcs_gpu.h"
+#include "host_rng.hpp"
+#include "kernels.cuh"
+
+using namespace cimcs;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Status {
+    int code;
+};
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(x)                                                                          \
+    do {                                                                               \
+        cudaError_t e_ = (x);                                                          \
+        if (e_ != cudaSuccess)                                                         \
+            return fail(CIMCS_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+int pow2_slots(int R) {
+    int n = 1;
+    while (n < R) n <<= 1;
+    return n;
+}
+
+// ------------------------------------------------------------- aux kernels
+template <typename T, int NR>
+__global__ void traj_to_dev(const double* __restrict__ h, T* __restrict__ d, int Rreal, int N,
+                            int ldN, int B, T pad) {
+    const size_t total = (size_t)B * ldN * NR;
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < total;
+         k += (size_t)gridDim.x * blockDim.x) {
+        const int q = k % NR;
+        const size_t bi = k / NR;
+        const int i = bi % ldN;
+        const int b = bi / ldN;
+        d[k] = (i < N && q < Rreal) ? (T)h[((size_t)b * Rreal + q) * N + i] : pad;
+    }
+}
+
+template <typename T, int NR>
+__global__ void dev_to_traj(const T* __restrict__ d, double* __restrict__ h, int Rreal, int N,
+                            int ldN, int B) {
+    const size_t total = (size_t)B * Rreal * N;
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < total;
+         k += (size_t)gridDim.x * blockDim.x) {
+        const int i = k % N;
+        const size_t bq = k / N;
+        const int q = bq % Rreal;
+        const int b = bq / Rreal;
+        h[k] = (double)d[((size_t)b * ldN + i) * NR + q];
+    }
+}
+
+template <int NR>
+__global__ void sig_to_dev(const int32_t* __restrict__ h, int8_t* d, int Rreal, int N, int ldN,
+                           int B) {
+    const size_t total = (size_t)B * ldN * NR;
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < total;
+         k += (size_t)gridDim.x * blockDim.x) {
+        const int q = k % NR;
+        const size_t bi = k / NR;
+        const int i = bi % ldN;
+        const int b = bi / ldN;
+        d[k] = (i < N && q < Rreal) ? (int8_t)h[((size_t)b * Rreal + q) * N + i] : (int8_t)0;
+    }
+}
+
+template <int NR>
+__global__ void sig_to_traj(const int8_t* __restrict__ d, int32_t* h, int Rreal, int N, int ldN,
+                            int B) {
+    const size_t total = (size_t)B * Rreal * N;
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < total;
+         k += (size_t)gridDim.x * blockDim.x) {
+        const int i = k % N;
+        const size_t bq = k / N;
+        const int q = bq % Rreal;
+        const int b = bq / Rreal;
+        h[k] = d[((size_t)b * ldN + i) * NR + q];
+    }
+}
+
+// R_init = hz (default_r_init, orchestrator.cpp:138) for every replica
+template <typename T, int NR>
+__global__ void rinit_hz_kernel(const T* __restrict__ hz, T* Rs, int Rreal, int N, int ldN,
+                                int B) {
+    const size_t total = (size_t)B * ldN * NR;
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < total;
+         k += (size_t)gridDim.x * blockDim.x) {
+        const int q = k % NR;
+        const size_t bi = k / NR;
+        const int i = bi % ldN;
+        Rs[k] = (i < N && q < Rreal) ? hz[bi] : T(0);
+    }
+}
+
+template <typename T, int NR>
+__global__ void mask_kernel(const T* __restrict__ Rs, const int8_t* __restrict__ sig, T* V,
+                            size_t total) {
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < total;
+         k += (size_t)gridDim.x * blockDim.x)
+        V[k] = Rs[k] * (sig[k] ? T(1) : T(0));
+}
+
+__global__ void traj_flags_kernel(int* fail_gstep, int* fail_idx, int Rreal, int NR, int B) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= B * NR) return;
+    fail_gstep[k] = (k % NR) < Rreal ? kFreeTraj : kInactiveTraj;
+    fail_idx[k] = INT_MAX;
+}
+
+struct DevRecord {
+    int i, support;
+    double eta, hamiltonian, rmse, hamming, min_e, median_e;
+};
+
+// Per trajectory: combine score partials (row blocks in order), count the
+// support and the Hamming mismatches, write the history record, track best.
+template <int NR>
+__global__ void finalize_kernel(const double* __restrict__ part, int nRB,
+                                const int8_t* __restrict__ sig, const int8_t* __restrict__ xi,
+                                const unsigned long long* __restrict__ minE,
+                                const int* __restrict__ fail_gstep, const AltParams* alt, int N,
+                                int ldN, int has_truth, DevRecord* hist_alt, int* n_hist,
+                                double* best_obj, int* improved, double* obj_out,
+                                double* rmse_out, double* ham_out) {
+    const int traj = blockIdx.x;
+    const int b = traj / NR, q = traj % NR;
+    __shared__ long long s_sup[256], s_ham[256];
+    long long sup = 0, ham = 0;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        const int s = sig[((size_t)b * ldN + i) * NR + q];
+        sup += s;
+        if (has_truth) ham += abs(s - (int)xi[(size_t)b * ldN + i]);
+    }
+    s_sup[threadIdx.x] = sup;
+    s_ham[threadIdx.x] = ham;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            s_sup[threadIdx.x] += s_sup[threadIdx.x + w];
+            s_ham[threadIdx.x] += s_ham[threadIdx.x + w];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    if (improved) improved[traj] = 0;
+    if (fail_gstep[traj] != kFreeTraj) return;
+    double A = 0.0, Bv = 0.0, Cv = 0.0;
+    for (int r = 0; r < nRB; ++r) {
+        const double* p = part + (((size_t)b * nRB + r) * NR + q) * 4;
+        A = A + p[0];
+        Bv = Bv + p[1];
+        Cv = Cv + p[2];
+    }
+    const double lam = alt->lambda;
+    // objective_at: 0.5 w.(G w) - hz.w + lambda |sigma|  (orchestrator.cpp:57-62)
+    const double obj = 0.5 * A - Bv + lam * (double)s_sup[0];
+    const double rm = has_truth ? sqrt(Cv / (double)N) : NAN;
+    const double hm = has_truth ? (double)s_ham[0] / (double)N : NAN;
+    if (obj_out) obj_out[traj] = obj;
+    if (rmse_out) rmse_out[traj] = rm;
+    if (ham_out) ham_out[traj] = hm;
+    if (hist_alt) {
+        DevRecord& rec = hist_alt[traj];
+        rec.i = alt->alt;
+        rec.support = (int)s_sup[0];
+        rec.eta = alt->eta;
+        rec.hamiltonian = obj;
+        rec.rmse = rm;
+        rec.hamming = hm;
+        rec.min_e = ord_val(minE[traj]);
+        n_hist[traj] += 1;
+    }
+    if (best_obj && obj < best_obj[traj]) {
+        best_obj[traj] = obj;
+        improved[traj] = 1;
+    }
+}
+
+// median(e_final) (orchestrator.cpp:163-168): bitonic sort in shared memory.
+template <typename T, int NR>
+__global__ void median_kernel(const T* __restrict__ E, const int* __restrict__ fail_gstep, int N,
+                              int ldN, int P, DevRecord* hist_alt) {
+    extern __shared__ __align__(16) unsigned char msm[];
+    T* v = reinterpret_cast<T*>(msm);
+    const int traj = blockIdx.x;
+    if (fail_gstep[traj] != kFreeTraj) return;
+    const int b = traj / NR, q = traj % NR;
+    for (int i = threadIdx.x; i < P; i += blockDim.x)
+        v[i] = i < N ? E[((size_t)b * ldN + i) * NR + q] : T(INFINITY);
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const bool up = (i & k) == 0;
+                    const T a = v[i], c = v[l];
+                    if ((a > c) == up) {
+                        v[i] = c;
+                        v[l] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    if (threadIdx.x == 0)
+        hist_alt[traj].median_e = N % 2 == 1 ? (double)v[N / 2]
+                                             : 0.5 * ((double)v[N / 2 - 1] + (double)v[N / 2]);
+}
+
+template <typename T, int NR>
+__global__ void best_update_kernel(const int* __restrict__ improved, const T* __restrict__ Rs,
+                                   const int8_t* __restrict__ sig, T* bestR, int8_t* bestS, int ldN,
+                                   int B) {
+    const size_t total = (size_t)B * ldN * NR;
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < total;
+         k += (size_t)gridDim.x * blockDim.x) {
+        const int q = k % NR;
+        const int b = (int)((k / NR) / ldN);
+        if (improved[b * NR + q]) {
+            bestR[k] = Rs[k];
+            bestS[k] = sig[k];
+        }
+    }
+}
+
+int grid_for(size_t n) {
+    size_t g = (n + 255) / 256;
+    return (int)std::min<size_t>(std::max<size_t>(g, 1), 148 * 16);
+}
+
+}  // namespace
+
+// ======================================================================= ctx
+struct cimcs_ctx {
+    int device = 0, dtype = CIMCS_F32;
+    cudaStream_t stream = nullptr;
+    int host_threads = 0;
+    bool use_graphs = true;
+    // problems
+    int B = 0, N = 0, ldN = 0, Mmax = 0;
+    std::vector<int> M;
+    bool has_truth = false, built = false;
+    double *dA = nullptr, *dy = nullptr;
+    int* dM = nullptr;
+    double* dG64 = nullptr;  // fp64 gram (the G of the fp64 path)
+    float* dG32 = nullptr;
+    void *dD = nullptr, *dhz = nullptr;
+    double* dx = nullptr;
+    int8_t* dxi = nullptr;
+    // trajectory state (NR slots)
+    int NR = 0;
+    void *Rs = nullptr, *C = nullptr, *E = nullptr, *W0 = nullptr, *W1 = nullptr,
+         *Hdbg = nullptr, *bestR = nullptr;
+    int8_t *sig = nullptr, *bestS = nullptr;
+    int *fail_gstep = nullptr, *fail_idx = nullptr, *n_hist = nullptr, *improved = nullptr,
+        *err = nullptr;
+    unsigned long long* minE = nullptr;
+    double *part = nullptr, *best_obj = nullptr, *stage = nullptr, *obj = nullptr,
+           *rmse = nullptr, *ham = nullptr;
+    int32_t* stage_i = nullptr;
+    size_t stage_elems = 0;
+    AltParams* alt = nullptr;
+    double* pump = nullptr;
+    int pump_cap = 0;
+    DevRecord* hist = nullptr;
+    int hist_cap = 0;
+    cimcs_timing timing{};
+
+    size_t elt() const { return dtype == CIMCS_F64 ? 8 : 4; }
+    const void* G() const { return dtype == CIMCS_F64 ? (const void*)dG64 : (const void*)dG32; }
+    size_t state_elems() const { return (size_t)B * ldN * NR; }
+};
+
+namespace {
+
+void free_state(cimcs_ctx* c) {
+    void* ptrs[] = {c->Rs,  c->C,        c->E,          c->W0,  c->W1,       c->Hdbg,
+                    c->bestR, c->sig,    c->bestS,      c->fail_gstep, c->fail_idx, c->n_hist,
+                    c->improved, c->minE, c->part,      c->best_obj, c->obj, c->rmse, c->ham};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    c->Rs = c->C = c->E = c->W0 = c->W1 = c->Hdbg = c->bestR = nullptr;
+    c->sig = c->bestS = nullptr;
+    c->fail_gstep = c->fail_idx = c->n_hist = c->improved = nullptr;
+    c->minE = nullptr;
+    c->part = c->best_obj = c->obj = c->rmse = c->ham = nullptr;
+    c->NR = 0;
+}
+
+void free_problems(cimcs_ctx* c) {
+    free_state(c);
+    void* ptrs[] = {c->dA, c->dy, c->dM, c->dG64, c->dG32, c->dD, c->dhz, c->dx, c->dxi};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    c->dA = c->dy = nullptr;
+    c->dM = nullptr;
+    c->dG64 = nullptr;
+    c->dG32 = nullptr;
+    c->dD = c->dhz = nullptr;
+    c->dx = nullptr;
+    c->dxi = nullptr;
+    c->B = c->N = c->ldN = 0;
+    c->built = false;
+}
+
+template <typename P>
+int dalloc(P** p, size_t bytes) {
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(bytes, 16));
+    if (e != cudaSuccess)
+        return fail(CIMCS_CUDA_ERROR, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    cudaMemset(*p, 0, std::max<size_t>(bytes, 16));
+    return 0;
+}
+
+int ensure_stage(cimcs_ctx* c, size_t elems) {
+    if (c->stage_elems >= elems) return 0;
+    if (c->stage) cudaFree(c->stage);
+    if (c->stage_i) cudaFree(c->stage_i);
+    c->stage = nullptr;
+    c->stage_i = nullptr;
+    c->stage_elems = 0;
+    if (int rc = dalloc(&c->stage, elems * 8)) return rc;
+    if (int rc = dalloc(&c->stage_i, elems * 4)) return rc;
+    c->stage_elems = elems;
+    return 0;
+}
+
+int ensure_state(cimcs_ctx* c, int NR) {
+    if (c->NR == NR && c->Rs) return 0;
+    free_state(c);
+    c->NR = NR;
+    const size_t n = c->state_elems(), es = c->elt();
+    const int nT = c->B * NR;
+    const int nRB = (c->N + (c->dtype == CIMCS_F64 ? row_block<double>() : row_block<float>()) - 1) /
+                    (c->dtype == CIMCS_F64 ? row_block<double>() : row_block<float>());
+    int rc = 0;
+    if ((rc = dalloc(&c->Rs, n * es)) || (rc = dalloc(&c->C, n * es)) ||
+        (rc = dalloc(&c->E, n * es)) || (rc = dalloc(&c->W0, n * es)) ||
+        (rc = dalloc(&c->W1, n * es)) || (rc = dalloc(&c->Hdbg, n * es)) ||
+        (rc = dalloc(&c->bestR, n * es)) || (rc = dalloc(&c->sig, n)) ||
+        (rc = dalloc(&c->bestS, n)) || (rc = dalloc(&c->fail_gstep, nT * 4)) ||
+        (rc = dalloc(&c->fail_idx, nT * 4)) || (rc = dalloc(&c->n_hist, nT * 4)) ||
+        (rc = dalloc(&c->improved, nT * 4)) || (rc = dalloc(&c->minE, nT * 8)) ||
+        (rc = dalloc(&c->part, (size_t)c->B * nRB * NR * 4 * 8)) ||
+        (rc = dalloc(&c->best_obj, nT * 8)) || (rc = dalloc(&c->obj, nT * 8)) ||
+        (rc = dalloc(&c->rmse, nT * 8)) || (rc = dalloc(&c->ham, nT * 8)))
+        return rc;
+    return 0;
+}
+
+StepScalars make_scalars(const cimcs_hyper* hp) {
+    StepScalars s{};
+    s.dt = hp->dt;
+    s.rt = std::sqrt(hp->tau);
+    s.half_rt = s.rt / 2.0;
+    s.tau = hp->tau;
+    s.nbeta = -hp->beta;
+    s.Kj = hp->K * hp->j;
+    s.minus_j = hp->mfz_loss_minus_j ? hp->j : 0.0;
+    s.one_minus_dtc = 1.0 - hp->dt_c;
+    s.dt_c = hp->dt_c;
+    s.n_steps = hp->n_steps;
+    return s;
+}
+
+AltParams make_alt(const cimcs_hyper* hp, double eta, int alt) {
+    AltParams a{};
+    const double rt = std::sqrt(hp->tau);
+    a.thresh = eta * eta / 4.0 * rt;  // solver_mfz.cpp:69
+    a.lambda = eta * eta / 2.0;       // orchestrator.cpp:189
+    a.eta = eta;
+    a.alt = alt;
+    a.gstep_base = alt * hp->n_steps;
+    return a;
+}
+
+double eta_schedule(int i, double eta_init, double eta_end, int velo) {
+    const double linear = eta_init * (1.0 - static_cast<double>(i) / velo);
+    return std::max(linear, eta_end);
+}
+
+std::vector<double> pump_table(const cimcs_hyper* hp) {
+    std::vector<double> p(hp->n_steps);
+    double t = 0.0;
+    const double T = static_cast<double>(hp->n_steps) * hp->dt;
+    for (int k = 0; k < hp->n_steps; ++k) {
+        p[k] = hp->pump_kind == CIMCS_PUMP_LINEAR
+                   ? hp->pump_end * t / T
+                   : (hp->p_thr - hp->d) + 2.0 * hp->d / (1.0 + std::exp(-(t - 4.0) / 2.0));
+        t = t + hp->dt;
+    }
+    return p;
+}
+
+// ----------------------------------------------------- typed dispatch
+template <typename T, int NR, int MODE>
+int launch_gemv_t(cimcs_ctx* c, const GemvArgs& a) {
+    auto kern = gemv_fused_kernel<T, NR, MODE>;
+    constexpr size_t smem = gemv_smem_bytes<T, NR>();
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    dim3 grid((c->N + row_block<T>() - 1) / row_block<T>(), c->B);
+    kern<<<grid, kThreads, smem, c->stream>>>(a);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+template <typename T, int NR>
+int launch_gemv_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
+    switch (mode) {
+        case EPI_STEP_BN: return launch_gemv_t<T, NR, EPI_STEP_BN>(c, a);
+        case EPI_STEP_CN: return launch_gemv_t<T, NR, EPI_STEP_CN>(c, a);
+        case EPI_JACOBI: return launch_gemv_t<T, NR, EPI_JACOBI>(c, a);
+        default: return launch_gemv_t<T, NR, EPI_SCORE>(c, a);
+    }
+}
+
+template <typename T>
+int launch_gemv_T(cimcs_ctx* c, int mode, const GemvArgs& a) {
+    switch (c->NR) {
+        case 1: return launch_gemv_nr<T, 1>(c, mode, a);
+        case 2: return launch_gemv_nr<T, 2>(c, mode, a);
+        case 4: return launch_gemv_nr<T, 4>(c, mode, a);
+        case 8: return launch_gemv_nr<T, 8>(c, mode, a);
+        default: return launch_gemv_nr<T, 16>(c, mode, a);
+    }
+}
+
+int launch_gemv(cimcs_ctx* c, int mode, const GemvArgs& a) {
+    return c->dtype == CIMCS_F64 ? launch_gemv_T<double>(c, mode, a)
+                                 : launch_gemv_T<float>(c, mode, a);
+}
+
+// Generic NR/T dispatch for the small state kernels.
+#define DISPATCH_NR(NRV, ...)                                               \
+    switch (NRV) {                                                          \
+        case 1: { constexpr int NR_ = 1; __VA_ARGS__; } break;              \
+        case 2: { constexpr int NR_ = 2; __VA_ARGS__; } break;              \
+        case 4: { constexpr int NR_ = 4; __VA_ARGS__; } break;              \
+        case 8: { constexpr int NR_ = 8; __VA_ARGS__; } break;              \
+        default: { constexpr int NR_ = 16; __VA_ARGS__; } break;            \
+    }
+
+template <typename T>
+int run_init_T(cimcs_ctx* c, int Rreal, int bn, const double* dc0, const double* de0, double rt) {
+    const int g = grid_for(c->state_elems());
+    T* W = static_cast<T*>(c->W0);
+    DISPATCH_NR(c->NR, {
+        if (bn)
+            init_state_kernel<T, NR_, 1><<<g, 256, 0, c->stream>>>(
+                dc0, Rreal, c->N, c->ldN, c->B, static_cast<const T*>(c->Rs),
+                static_cast<T*>(c->C), static_cast<T*>(c->E), W, c->fail_gstep, c->minE, rt,
+                de0);
+        else
+            init_state_kernel<T, NR_, 0><<<g, 256, 0, c->stream>>>(
+                dc0, Rreal, c->N, c->ldN, c->B, static_cast<const T*>(c->Rs),
+                static_cast<T*>(c->C), static_cast<T*>(c->E), W, c->fail_gstep, c->minE, rt,
+                de0);
+    });
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int run_init(cimcs_ctx* c, int Rreal, int bn, const double* dc0, const double* de0, double rt) {
+    return c->dtype == CIMCS_F64 ? run_init_T<double>(c, Rreal, bn, dc0, de0, rt)
+                                 : run_init_T<float>(c, Rreal, bn, dc0, de0, rt);
+}
+
+template <typename T>
+int run_support_T(cimcs_ctx* c) {
+    const int g = grid_for(c->state_elems());
+    DISPATCH_NR(c->NR, {
+        support_kernel<T, NR_><<<g, 256, 0, c->stream>>>(
+            static_cast<const T*>(c->C), static_cast<const T*>(c->Rs), c->sig,
+            static_cast<T*>(c->W0), c->fail_gstep, c->N, c->ldN, c->B);
+    });
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int run_support(cimcs_ctx* c) {
+    return c->dtype == CIMCS_F64 ? run_support_T<double>(c) : run_support_T<float>(c);
+}
+
+template <typename T>
+int upload_traj_T(cimcs_ctx* c, const double* h, void* d, int Rreal, T pad) {
+    const size_t n = (size_t)c->B * Rreal * c->N;
+    if (int rc = ensure_stage(c, std::max(n, c->state_elems()))) return rc;
+    CK(cudaMemcpyAsync(c->stage, h, n * 8, cudaMemcpyHostToDevice, c->stream));
+    const int g = grid_for(c->state_elems());
+    DISPATCH_NR(c->NR, {
+        traj_to_dev<T, NR_><<<g, 256, 0, c->stream>>>(c->stage, static_cast<T*>(d), Rreal, c->N,
+                                                      c->ldN, c->B, pad);
+    });
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int upload_traj(cimcs_ctx* c, const double* h, void* d, int Rreal, double pad = 0.0) {
+    return c->dtype == CIMCS_F64 ? upload_traj_T<double>(c, h, d, Rreal, pad)
+                                 : upload_traj_T<float>(c, h, d, Rreal, (float)pad);
+}
+
+template <typename T>
+int download_traj_T(cimcs_ctx* c, const void* d, double* h, int Rreal) {
+    const size_t n = (size_t)c->B * Rreal * c->N;
+    if (int rc = ensure_stage(c, std::max(n, c->state_elems()))) return rc;
+    const int g = grid_for(n);
+    DISPATCH_NR(c->NR, {
+        dev_to_traj<T, NR_><<<g, 256, 0, c->stream>>>(static_cast<const T*>(d), c->stage, Rreal,
+                                                      c->N, c->ldN, c->B);
+    });
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h, c->stage, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    return 0;
+}
+
+int download_traj(cimcs_ctx* c, const void* d, double* h, int Rreal) {
+    return c->dtype == CIMCS_F64 ? download_traj_T<double>(c, d, h, Rreal)
+                                 : download_traj_T<float>(c, d, h, Rreal);
+}
+
+int upload_sig(cimcs_ctx* c, const int32_t* h, int8_t* d, int Rreal) {
+    const size_t n = (size_t)c->B * Rreal * c->N;
+    if (int rc = ensure_stage(c, std::max(n, c->state_elems()))) return rc;
+    for (size_t k = 0; k < n; ++k)
+        if (h[k] != 0 && h[k] != 1) return fail(CIMCS_INPUT_ERROR, "sigma must be 0/1");
+    CK(cudaMemcpyAsync(c->stage_i, h, n * 4, cudaMemcpyHostToDevice, c->stream));
+    const int g = grid_for(c->state_elems());
+    DISPATCH_NR(c->NR, {
+        sig_to_dev<NR_><<<g, 256, 0, c->stream>>>(c->stage_i, d, Rreal, c->N, c->ldN, c->B);
+    });
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int download_sig(cimcs_ctx* c, const int8_t* d, int32_t* h, int Rreal) {
+    const size_t n = (size_t)c->B * Rreal * c->N;
+    if (int rc = ensure_stage(c, std::max(n, c->state_elems()))) return rc;
+    const int g = grid_for(n);
+    DISPATCH_NR(c->NR, {
+        sig_to_traj<NR_><<<g, 256, 0, c->stream>>>(d, c->stage_i, Rreal, c->N, c->ldN, c->B);
+    });
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h, c->stage_i, n * 4, cudaMemcpyDeviceToHost, c->stream));
+    return 0;
+}
+
+template <typename T>
+int rinit_hz_T(cimcs_ctx* c, int Rreal) {
+    const int g = grid_for(c->state_elems());
+    DISPATCH_NR(c->NR, {
+        rinit_hz_kernel<T, NR_><<<g, 256, 0, c->stream>>>(static_cast<const T*>(c->dhz),
+                                                          static_cast<T*>(c->Rs), Rreal, c->N,
+                                                          c->ldN, c->B);
+    });
+    CK(cudaGetLastError());
+    return 0;
+}
+
+template <typename T>
+int mask_T(cimcs_ctx* c, void* V) {
+    const int g = grid_for(c->state_elems());
+    DISPATCH_NR(c->NR, {
+        mask_kernel<T, NR_><<<g, 256, 0, c->stream>>>(static_cast<const T*>(c->Rs), c->sig,
+                                                      static_cast<T*>(V), c->state_elems());
+    });
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int reset_flags(cimcs_ctx* c, int Rreal) {
+    const int nT = c->B * c->NR;
+    traj_flags_kernel<<<(nT + 255) / 256, 256, 0, c->stream>>>(c->fail_gstep, c->fail_idx, Rreal,
+                                                              c->NR, c->B);
+    CK(cudaGetLastError());
+    CK(cudaMemsetAsync(c->n_hist, 0, nT * 4, c->stream));
+    CK(cudaMemsetAsync(c->err, 0x7f, 4, c->stream));
+    return 0;
+}
+
+GemvArgs base_args(cimcs_ctx* c, const StepScalars& s) {
+    GemvArgs a{};
+    a.G = c->G();
+    a.D = c->dD;
+    a.hz = c->dhz;
+    a.Rs = c->Rs;
+    a.C = c->C;
+    a.E = c->E;
+    a.sigma = c->sig;
+    a.fail_gstep = c->fail_gstep;
+    a.fail_idx = c->fail_idx;
+    a.minE = c->minE;
+    a.part = c->part;
+    a.alt = c->alt;
+    a.xtrue = c->has_truth ? c->dx : nullptr;
+    a.xitrue = c->dxi;
+    a.err = c->err;
+    a.N = c->N;
+    a.ldN = c->ldN;
+    a.B = c->B;
+    a.s = s;
+    return a;
+}
+
+int nRB_of(const cimcs_ctx* c) {
+    const int rb = c->dtype == CIMCS_F64 ? row_block<double>() : row_block<float>();
+    return (c->N + rb - 1) / rb;
+}
+
+// Enqueue the n_steps fused Euler steps of one CIM call (graph-capturable).
+int enqueue_steps(cimcs_ctx* c, int bn, const StepScalars& s, int n_steps) {
+    GemvArgs a = base_args(c, s);
+    a.pump = c->pump;
+    a.Hdbg = nullptr;
+    for (int k = 0; k < n_steps; ++k) {
+        a.step = k;
+        a.Win = (k & 1) ? c->W1 : c->W0;
+        a.Wout = (k & 1) ? c->W0 : c->W1;
+        if (int rc = launch_gemv(c, bn ? EPI_STEP_BN : EPI_STEP_CN, a)) return rc;
+    }
+    return 0;
+}
+
+// support + masked Jacobi sweeps (graph-capturable).  Final V in W[iters&1].
+int enqueue_refit(cimcs_ctx* c, const StepScalars& s, int iters, bool do_support) {
+    if (do_support) {
+        if (int rc = run_support(c)) return rc;
+    }
+    GemvArgs a = base_args(c, s);
+    for (int it = 0; it < iters; ++it) {
+        a.Win = (it & 1) ? c->W1 : c->W0;
+        a.Wout = (it & 1) ? c->W0 : c->W1;
+        if (int rc = launch_gemv(c, EPI_JACOBI, a)) return rc;
+    }
+    return 0;
+}
+
+template <typename T>
+int enqueue_median_T(cimcs_ctx* c, DevRecord* hist_alt) {
+    int P = 1;
+    while (P < c->N) P <<= 1;
+    const size_t smem = (size_t)P * sizeof(T);
+    if (smem > 200 * 1024) return 0;  // median left as NaN beyond 25k/51k spins
+    DISPATCH_NR(c->NR, {
+        auto k = median_kernel<T, NR_>;
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k<<<c->B * c->NR, 1024, smem, c->stream>>>(static_cast<const T*>(c->E), c->fail_gstep,
+                                                  c->N, c->ldN, P, hist_alt);
+    });
+    CK(cudaGetLastError());
+    return 0;
+}
+
+// scorer on V = W[v_slot]: score GEMV + finalize (+ history, + best tracking)
+int enqueue_score(cimcs_ctx* c, const StepScalars& s, int v_slot, DevRecord* hist_alt,
+                  bool track_best) {
+    GemvArgs a = base_args(c, s);
+    a.Win = v_slot ? c->W1 : c->W0;
+    a.Wout = nullptr;
+    if (int rc = launch_gemv(c, EPI_SCORE, a)) return rc;
+    DISPATCH_NR(c->NR, {
+        finalize_kernel<NR_><<<c->B * c->NR, 256, 0, c->stream>>>(
+            c->part, nRB_of(c), c->sig, c->dxi, c->minE, c->fail_gstep, c->alt, c->N, c->ldN,
+            c->has_truth ? 1 : 0, hist_alt, c->n_hist, track_best ? c->best_obj : nullptr,
+            c->improved, c->obj, c->rmse, c->ham);
+    });
+    CK(cudaGetLastError());
+    if (hist_alt) {
+        if (int rc = c->dtype == CIMCS_F64 ? enqueue_median_T<double>(c, hist_alt)
+                                           : enqueue_median_T<float>(c, hist_alt))
+            return rc;
+    }
+    if (track_best) {
+        const int g = grid_for(c->state_elems());
+        if (c->dtype == CIMCS_F64) {
+            DISPATCH_NR(c->NR, {
+                best_update_kernel<double, NR_><<<g, 256, 0, c->stream>>>(
+                    c->improved, static_cast<const double*>(c->Rs), c->sig,
+                    static_cast<double*>(c->bestR), c->bestS, c->ldN, c->B);
+            });
+        } else {
+            DISPATCH_NR(c->NR, {
+                best_update_kernel<float, NR_><<<g, 256, 0, c->stream>>>(
+                    c->improved, static_cast<const float*>(c->Rs), c->sig,
+                    static_cast<float*>(c->bestR), c->bestS, c->ldN, c->B);
+            });
+        }
+        CK(cudaGetLastError());
+    }
+    return 0;
+}
+
+int check_ready(cimcs_ctx* c, int R) {
+    if (!c) return fail(CIMCS_INPUT_ERROR, "null context");
+    if (!c->built) return fail(CIMCS_INPUT_ERROR, "coupling not built (cimcs_build_coupling)");
+    if (R < 1 || R > 16) return fail(CIMCS_INPUT_ERROR, "R must be in [1, 16]");
+    return 0;
+}
+
+int validate(const cimcs_hyper* h) {
+    if (!h) return fail(CIMCS_CONFIG_ERROR, "null hyper-parameters");
+    if (!(h->dt > 0)) return fail(CIMCS_CONFIG_ERROR, "dt must be > 0");
+    if (h->n_steps < 1) return fail(CIMCS_CONFIG_ERROR, "n_steps must be >= 1");
+    if (!(h->tau > 0)) return fail(CIMCS_CONFIG_ERROR, "tau must be > 0");
+    if (h->g2 < 0) return fail(CIMCS_CONFIG_ERROR, "g2 must be >= 0");
+    if (h->eta_init < h->eta_end || h->eta_end < 0)
+        return fail(CIMCS_CONFIG_ERROR, "need eta_init >= eta_end >= 0");
+    if (h->velo < 1) return fail(CIMCS_CONFIG_ERROR, "velo must be >= 1");
+    if (h->pump_kind != CIMCS_PUMP_SIGMOID && h->pump_kind != CIMCS_PUMP_LINEAR)
+        return fail(CIMCS_CONFIG_ERROR, "pump_kind must be sigmoid or linear");
+    return 0;
+}
+
+int upload_pump(cimcs_ctx* c, const cimcs_hyper* hp) {
+    const std::vector<double> p = pump_table(hp);
+    for (double v : p)
+        if (!std::isfinite(v)) return fail(CIMCS_INPUT_ERROR, "mfz_step: non-finite pump");
+    if (c->pump_cap < hp->n_steps) {
+        if (c->pump) cudaFree(c->pump);
+        c->pump = nullptr;
+        if (int rc = dalloc(&c->pump, (size_t)hp->n_steps * 8)) return rc;
+        c->pump_cap = hp->n_steps;
+    }
+    CK(cudaMemcpy(c->pump, p.data(), (size_t)hp->n_steps * 8, cudaMemcpyHostToDevice));
+    return 0;
+}
+
+int set_alt(cimcs_ctx* c, const AltParams& ap) {
+    CK(cudaMemcpyAsync(c->alt, &ap, sizeof(AltParams), cudaMemcpyHostToDevice, c->stream));
+    return 0;
+}
+
+// Host c0 generator pool: trajectory streams split contiguously over threads.
+void gen_c0(std::vector<HostRng>& rngs, int N, double* out, int threads) {
+    const int nt = (int)rngs.size();
+    threads = std::max(1, std::min(threads, nt));
+    auto work = [&](int t0, int t1) {
+        for (int t = t0; t < t1; ++t) {
+            double* o = out + (size_t)t * N;
+            for (int i = 0; i < N; ++i) o[i] = 0.01 * rngs[t].gauss();  // init_mfz :27
+        }
+    };
+    if (threads == 1) {
+        work(0, nt);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const int per = (nt + threads - 1) / threads;
+    for (int k = 0; k < threads; ++k) {
+        const int t0 = k * per, t1 = std::min(nt, t0 + per);
+        if (t0 < t1) pool.emplace_back(work, t0, t1);
+    }
+    for (auto& th : pool) th.join();
+}
+
+struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    ~Graph() {
+        if (exec) cudaGraphExecDestroy(exec);
+    }
+};
+
+template <typename F>
+int capture(cimcs_ctx* c, Graph& g, F&& body) {
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const int rc = body();
+    cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+    if (rc) {
+        if (e == cudaSuccess) cudaGraphDestroy(graph);
+        return rc;
+    }
+    CK(e);
+    CK(cudaGraphInstantiate(&g.exec, graph, 0));
+    cudaGraphDestroy(graph);
+    return 0;
+}
+
+struct Events {
+    std::vector<cudaEvent_t> ev;
+    explicit Events(size_t n) : ev(n, nullptr) {
+        for (auto& e : ev) cudaEventCreate(&e);
+    }
+    ~Events() {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+    float ms(size_t a, size_t b) const {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, ev[a], ev[b]);
+        return t;
+    }
+};
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+int cimcs_abi_version(void) { return CIMCS_ABI_VERSION; }
+const char* cimcs_last_error(void) { return g_err.c_str(); }
+
+void cimcs_hyper_default(cimcs_hyper* h) {
+    h->g2 = 1e-7;
+    h->j = 1.0;
+    h->K = 1.0;
+    h->beta = 0.2;
+    h->tau = 1.0;
+    h->dt = 0.02;
+    h->n_steps = 1000;
+    h->p_thr = 1.0;
+    h->d = 0.4;
+    h->eta_init = 0.8;
+    h->eta_end = 0.18;
+    h->velo = 51;
+    h->dt_c = 0.1;
+    h->jacobi_iters = 100;
+    h->cg_max_iters = 10000;
+    h->cg_tol = 1e-10;
+    h->gamma = 1e-4;
+    h->mfz_loss_minus_j = 0;
+    h->mu_abort = 100.0;
+    h->pump_kind = CIMCS_PUMP_SIGMOID;
+    h->pump_end = 1.2;
+}
+
+int cimcs_hyper_validate(const cimcs_hyper* h) { return validate(h); }
+uint64_t cimcs_mix_seed(uint64_t base, uint64_t salt) { return mix_seed(base, salt); }
+
+int cimcs_gemv_order(int dtype, int32_t* nseg, int32_t* gran) {
+    (void)dtype;
+    if (nseg) *nseg = kSeg;
+    if (gran) *gran = kGran;
+    return 0;
+}
+
+int cimcs_gen_dims(int32_t N, double alpha, double a, int32_t* M, int32_t* K) {
+    int m = 0, k = 0;
+    if (gen_dims(N, alpha, a, &m, &k)) return fail(CIMCS_INPUT_ERROR, "gen_instance: bad dims");
+    if (M) *M = m;
+    if (K) *K = k;
+    return 0;
+}
+
+int cimcs_gen_instance(int32_t N, double alpha, double a, double nu, uint64_t seed, double* A,
+                       double* y, double* x_true, int32_t* xi_true) {
+    if (gen_instance(N, alpha, a, nu, seed, A, y, x_true, xi_true))
+        return fail(CIMCS_INPUT_ERROR, "gen_instance: bad arguments");
+    return 0;
+}
+
+int cimcs_gen_instances(int32_t B, int32_t N, const double* alpha, const double* a,
+                        const double* nu, const uint64_t* seeds, double* const* A,
+                        double* const* y, double* const* x_true, int32_t* const* xi_true,
+                        int32_t threads) {
+    std::atomic<int> next{0}, bad{0};
+    auto work = [&] {
+        for (int b = next.fetch_add(1); b < B; b = next.fetch_add(1))
+            if (gen_instance(N, alpha[b], a[b], nu[b], seeds[b], A[b], y[b], x_true[b],
+                             xi_true[b]))
+                bad = 1;
+    };
+    if (threads <= 0) threads = (int)std::thread::hardware_concurrency();
+    threads = std::max(1, std::min<int>(threads, B));
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) pool.emplace_back(work);
+    for (auto& th : pool) th.join();
+    return bad ? fail(CIMCS_INPUT_ERROR, "gen_instance: bad arguments") : 0;
+}
+
+int cimcs_create(int32_t device, int32_t dtype, cimcs_ctx** out) {
+    if (!out) return fail(CIMCS_INPUT_ERROR, "null out");
+    if (dtype != CIMCS_F32 && dtype != CIMCS_F64) return fail(CIMCS_CONFIG_ERROR, "bad dtype");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(CIMCS_CONFIG_ERROR, "bad device");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(CIMCS_CUDA_ERROR, "libcimcs_gpu is built for sm_100a (B200) only");
+    auto* c = new cimcs_ctx();
+    c->device = device;
+    c->dtype = dtype;
+    c->host_threads = std::max(1u, std::thread::hardware_concurrency());
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return fail(CIMCS_CUDA_ERROR, "stream create failed");
+    }
+    if (dalloc(&c->alt, sizeof(AltParams)) || dalloc(&c->err, 16)) {
+        delete c;
+        return CIMCS_CUDA_ERROR;
+    }
+    *out = c;
+    return 0;
+}
+
+void cimcs_destroy(cimcs_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    free_problems(c);
+    if (c->stage) cudaFree(c->stage);
+    if (c->stage_i) cudaFree(c->stage_i);
+    if (c->alt) cudaFree(c->alt);
+    if (c->err) cudaFree(c->err);
+    if (c->pump) cudaFree(c->pump);
+    if (c->hist) cudaFree(c->hist);
+    cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
+    if (!c || !key) return fail(CIMCS_INPUT_ERROR, "null argument");
+    const std::string k(key);
+    if (k == "host_threads") c->host_threads = (int)std::max<int64_t>(1, v);
+    else if (k == "use_graphs") c->use_graphs = v != 0;
+    else return fail(CIMCS_CONFIG_ERROR, "unknown option " + k);
+    return 0;
+}
+
+int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
+                       const double* const* A, const double* const* y,
+                       const double* const* x_true, const int32_t* const* xi_true) {
+    if (!c) return fail(CIMCS_INPUT_ERROR, "null context");
+    if (B < 1 || N < 1) return fail(CIMCS_INPUT_ERROR, "need B >= 1 and N >= 1");
+    for (int b = 0; b < B; ++b)
+        if (M[b] < 1 || !A[b] || !y[b]) return fail(CIMCS_INPUT_ERROR, "empty A");
+    CK(cudaSetDevice(c->device));
+    free_problems(c);
+    c->B = B;
+    c->N = N;
+    c->ldN = (N + 31) / 32 * 32;
+    c->M.assign(M, M + B);
+    c->Mmax = *std::max_element(c->M.begin(), c->M.end());
+    c->has_truth = x_true != nullptr && xi_true != nullptr;
+    const size_t astride = (size_t)c->Mmax * N;
+    int rc;
+    if ((rc = dalloc(&c->dA, (size_t)B * astride * 8)) ||
+        (rc = dalloc(&c->dy, (size_t)B * c->Mmax * 8)) || (rc = dalloc(&c->dM, (size_t)B * 4)))
+        return rc;
+    for (int b = 0; b < B; ++b) {
+        CK(cudaMemcpyAsync(c->dA + (size_t)b * astride, A[b], (size_t)M[b] * N * 8,
+                           cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->dy + (size_t)b * c->Mmax, y[b], (size_t)M[b] * 8,
+                           cudaMemcpyHostToDevice, c->stream));
+    }
+    CK(cudaMemcpyAsync(c->dM, M, (size_t)B * 4, cudaMemcpyHostToDevice, c->stream));
+    if (c->has_truth) {
+        if ((rc = dalloc(&c->dx, (size_t)B * c->ldN * 8)) ||
+            (rc = dalloc(&c->dxi, (size_t)B * c->ldN)))
+            return rc;
+        std::vector<int8_t> xi8((size_t)B * c->ldN, 0);
+        for (int b = 0; b < B; ++b) {
+            CK(cudaMemcpyAsync(c->dx + (size_t)b * c->ldN, x_true[b], (size_t)N * 8,
+                               cudaMemcpyHostToDevice, c->stream));
+            for (int i = 0; i < N; ++i) {
+                if (xi_true[b][i] != 0 && xi_true[b][i] != 1)
+                    return fail(CIMCS_INPUT_ERROR, "xi_true must be 0/1");
+                xi8[(size_t)b * c->ldN + i] = (int8_t)xi_true[b][i];
+            }
+        }
+        CK(cudaMemcpyAsync(c->dxi, xi8.data(), xi8.size(), cudaMemcpyHostToDevice, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int cimcs_build_coupling(cimcs_ctx* c) {
+    if (!c || c->B < 1) return fail(CIMCS_INPUT_ERROR, "no problems set");
+    CK(cudaSetDevice(c->device));
+    const size_t nG = (size_t)c->B * c->ldN * c->ldN;
+    const size_t nv = (size_t)c->B * c->ldN;
+    int rc;
+    if (!c->dG64 && (rc = dalloc(&c->dG64, nG * 8))) return rc;
+    double *hz64 = nullptr, *D64 = nullptr;
+    if ((rc = dalloc(&hz64, nv * 8)) || (rc = dalloc(&D64, nv * 8))) return rc;
+    Events ev(2);
+    cudaEventRecord(ev.ev[0], c->stream);
+    CK(cudaMemsetAsync(c->dG64, 0, nG * 8, c->stream));
+    const int nt = (c->N + kGT - 1) / kGT;
+    const size_t astride = (size_t)c->Mmax * c->N;
+    // one launch per distinct M (instances of a phase grid differ in M)
+    for (int b = 0; b < c->B;) {
+        int e = b;
+        while (e < c->B && c->M[e] == c->M[b]) ++e;
+        gram_kernel<<<dim3(nt, nt, e - b), 256, 0, c->stream>>>(
+            c->dA + (size_t)b * astride, c->M[b], c->N, c->ldN, astride,
+            c->dG64 + (size_t)b * c->ldN * c->ldN);
+        CK(cudaGetLastError());
+        b = e;
+    }
+    hz_diag_kernel<<<dim3((c->N + 127) / 128, c->B), 128, 0, c->stream>>>(
+        c->dA, c->dy, c->dM, c->N, c->ldN, astride, c->Mmax, c->dG64, hz64, D64, c->B);
+    CK(cudaGetLastError());
+    c->timing.other_launches += 2;
+    if (c->dtype == CIMCS_F64) {
+        c->dhz = hz64;
+        c->dD = D64;
+    } else {
+        float *G32 = nullptr, *hz32 = nullptr, *D32 = nullptr;
+        if ((rc = dalloc(&G32, nG * 4)) || (rc = dalloc(&hz32, nv * 4)) ||
+            (rc = dalloc(&D32, nv * 4)))
+            return rc;
+        convert_kernel<float><<<148 * 8, 256, 0, c->stream>>>(c->dG64, G32, nG);
+        convert_kernel<float><<<grid_for(nv), 256, 0, c->stream>>>(hz64, hz32, nv);
+        convert_kernel<float><<<grid_for(nv), 256, 0, c->stream>>>(D64, D32, nv);
+        CK(cudaGetLastError());
+        c->dG32 = G32;
+        c->dhz = hz32;
+        c->dD = D32;
+        CK(cudaStreamSynchronize(c->stream));
+        cudaFree(hz64);
+        cudaFree(D64);
+        // the fp64 gram is kept for cimcs_get_coupling only when small
+        if (nG * 8 > (size_t)1 << 30) {
+            cudaFree(c->dG64);
+            c->dG64 = nullptr;
+        }
+    }
+    cudaEventRecord(ev.ev[1], c->stream);
+    CK(cudaStreamSynchronize(c->stream));
+    c->timing.gram_ms = ev.ms(0, 1);
+    c->built = true;
+    return 0;
+}
+
+int cimcs_get_coupling(cimcs_ctx* c, int32_t b, double* G, double* hz, double* D) {
+    if (!c || !c->built || b < 0 || b >= c->B) return fail(CIMCS_INPUT_ERROR, "bad instance");
+    const int N = c->N, ld = c->ldN;
+    std::vector<double> row(ld);
+    if (G) {
+        if (c->dtype == CIMCS_F64 || c->dG64) {
+            for (int i = 0; i < N; ++i)
+                CK(cudaMemcpy(G + (size_t)i * N, c->dG64 + ((size_t)b * ld + i) * ld, N * 8,
+                              cudaMemcpyDeviceToHost));
+        } else {
+            std::vector<float> rf(N);
+            for (int i = 0; i < N; ++i) {
+                CK(cudaMemcpy(rf.data(), c->dG32 + ((size_t)b * ld + i) * ld, N * 4,
+                              cudaMemcpyDeviceToHost));
+                for (int j = 0; j < N; ++j) G[(size_t)i * N + j] = rf[j];
+            }
+        }
+    }
+    auto vec = [&](const void* d, double* h) -> int {
+        if (!h) return 0;
+        if (c->dtype == CIMCS_F64) {
+            CK(cudaMemcpy(h, static_cast<const double*>(d) + (size_t)b * ld, N * 8,
+                          cudaMemcpyDeviceToHost));
+        } else {
+            std::vector<float> f(N);
+            CK(cudaMemcpy(f.data(), static_cast<const float*>(d) + (size_t)b * ld, N * 4,
+                          cudaMemcpyDeviceToHost));
+            for (int i = 0; i < N; ++i) h[i] = f[i];
+        }
+        return 0;
+    };
+    if (int rc = vec(c->dhz, hz)) return rc;
+    return vec(c->dD, D);
+}
+
+int cimcs_mfz_step(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp, double eta,
+                   double p, const double* Rsig, const double* cin, const double* ein,
+                   double* c_out, double* e_out, double* h_out, int32_t* fail_index) {
+    if (int rc = check_ready(c, R)) return rc;
+    if (int rc = validate(hp)) return rc;
+    if (!std::isfinite(p)) return fail(CIMCS_INPUT_ERROR, "mfz_step: non-finite pump");
+    if (backend != CIMCS_MFZ_BN && backend != CIMCS_MFZ_CN)
+        return fail(CIMCS_CONFIG_ERROR, "backend must be mfz-bn or mfz-cn");
+    CK(cudaSetDevice(c->device));
+    if (int rc = ensure_state(c, pow2_slots(R))) return rc;
+    const size_t n = (size_t)c->B * R * c->N;
+    if (int rc = reset_flags(c, R)) return rc;
+    if (int rc = set_alt(c, make_alt(hp, eta, 0))) return rc;
+    if (int rc = upload_traj(c, Rsig, c->Rs, R)) return rc;
+    // c and e go through a second staging area (the init kernel reads host layout)
+    double* dce = nullptr;
+    if (int rc = dalloc(&dce, 2 * n * 8)) return rc;
+    CK(cudaMemcpyAsync(dce, cin, n * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dce + n, ein, n * 8, cudaMemcpyHostToDevice, c->stream));
+    const StepScalars s = make_scalars(hp);
+    int rc = run_init(c, R, backend == CIMCS_MFZ_BN, dce, dce + n, s.rt);
+    if (!rc) {
+        GemvArgs a = base_args(c, s);
+        a.pump = nullptr;
+        a.p_scalar = p;
+        a.step = 0;
+        a.Win = c->W0;
+        a.Wout = c->W1;
+        a.Hdbg = c->Hdbg;
+        rc = launch_gemv(c, backend == CIMCS_MFZ_BN ? EPI_STEP_BN : EPI_STEP_CN, a);
+    }
+    if (!rc && c_out) rc = download_traj(c, c->C, c_out, R);
+    if (!rc && e_out) rc = download_traj(c, c->E, e_out, R);
+    if (!rc && h_out) rc = download_traj(c, c->Hdbg, h_out, R);
+    std::vector<int> fi(c->B * c->NR);
+    if (!rc)
+        if (cudaMemcpyAsync(fi.data(), c->fail_idx, fi.size() * 4, cudaMemcpyDeviceToHost,
+                            c->stream) != cudaSuccess)
+            rc = fail(CIMCS_CUDA_ERROR, "copy");
+    cudaStreamSynchronize(c->stream);
+    cudaFree(dce);
+    if (rc) return rc;
+    bool div = false;
+    for (int b = 0; b < c->B; ++b)
+        for (int r = 0; r < R; ++r) {
+            const int v = fi[b * c->NR + r];
+            if (fail_index) fail_index[b * R + r] = v == INT_MAX ? -1 : v;
+            div |= v != INT_MAX;
+        }
+    return div ? fail(CIMCS_DIVERGENCE, "mfz_step: non-finite amplitude") : 0;
+}
+
+int cimcs_run_cim(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp, double eta,
+                  const double* Rsig, const double* c0, double* c_out, double* e_out,
+                  int32_t* sigma_out, double* min_e, int32_t* fail_index) {
+    if (int rc = check_ready(c, R)) return rc;
+    if (int rc = validate(hp)) return rc;
+    if (backend != CIMCS_MFZ_BN && backend != CIMCS_MFZ_CN)
+        return fail(CIMCS_CONFIG_ERROR, "backend must be mfz-bn or mfz-cn");
+    CK(cudaSetDevice(c->device));
+    if (int rc = ensure_state(c, pow2_slots(R))) return rc;
+    if (int rc = upload_pump(c, hp)) return rc;
+    const size_t n = (size_t)c->B * R * c->N;
+    if (int rc = reset_flags(c, R)) return rc;
+    if (int rc = set_alt(c, make_alt(hp, eta, 0))) return rc;
+    if (int rc = upload_traj(c, Rsig, c->Rs, R)) return rc;
+    double* dc0 = nullptr;
+    if (int rc = dalloc(&dc0, n * 8)) return rc;
+    CK(cudaMemcpyAsync(dc0, c0, n * 8, cudaMemcpyHostToDevice, c->stream));
+    const StepScalars s = make_scalars(hp);
+    Events ev(2);
+    cudaEventRecord(ev.ev[0], c->stream);
+    int rc = run_init(c, R, backend == CIMCS_MFZ_BN, dc0, nullptr, s.rt);
+    if (!rc) rc = enqueue_steps(c, backend == CIMCS_MFZ_BN, s, hp->n_steps);
+    cudaEventRecord(ev.ev[1], c->stream);
+    if (!rc) rc = run_support(c);
+    if (!rc && c_out) rc = download_traj(c, c->C, c_out, R);
+    if (!rc && e_out) rc = download_traj(c, c->E, e_out, R);
+    if (!rc && sigma_out) rc = download_sig(c, c->sig, sigma_out, R);
+    std::vector<int> fi(c->B * c->NR);
+    std::vector<unsigned long long> me(c->B * c->NR);
+    if (!rc) {
+        cudaMemcpyAsync(fi.data(), c->fail_idx, fi.size() * 4, cudaMemcpyDeviceToHost, c->stream);
+        cudaMemcpyAsync(me.data(), c->minE, me.size() * 8, cudaMemcpyDeviceToHost, c->stream);
+    }
+    cudaError_t se = cudaStreamSynchronize(c->stream);
+    cudaFree(dc0);
+    if (rc) return rc;
+    if (se != cudaSuccess) return fail(CIMCS_CUDA_ERROR, cudaGetErrorString(se));
+    c->timing.cim_ms = ev.ms(0, 1);
+    c->timing.step_launches = hp->n_steps;
+    bool div = false;
+    for (int b = 0; b < c->B; ++b)
+        for (int r = 0; r < R; ++r) {
+            const int v = fi[b * c->NR + r];
+            if (fail_index) fail_index[b * R + r] = v == INT_MAX ? -1 : v;
+            if (min_e) min_e[b * R + r] = ord_val(me[b * c->NR + r]);
+            div |= v != INT_MAX;
+        }
+    return div ? fail(CIMCS_DIVERGENCE, "mfz_step: non-finite amplitude") : 0;
+}
+
+int cimcs_refit(cimcs_ctx* c, int32_t R, const int32_t* sigma, const double* R_prev,
+                double* R_out, const cimcs_hyper* hp) {
+    if (int rc = check_ready(c, R)) return rc;
+    if (!hp) return fail(CIMCS_CONFIG_ERROR, "null hyper-parameters");
+    CK(cudaSetDevice(c->device));
+    if (int rc = ensure_state(c, pow2_slots(R))) return rc;
+    if (int rc = reset_flags(c, R)) return rc;
+    if (int rc = upload_traj(c, R_prev, c->Rs, R)) return rc;
+    if (int rc = upload_sig(c, sigma, c->sig, R)) return rc;
+    const StepScalars s = make_scalars(hp);
+    int rc = c->dtype == CIMCS_F64 ? mask_T<double>(c, c->W0) : mask_T<float>(c, c->W0);
+    Events ev(2);
+    cudaEventRecord(ev.ev[0], c->stream);
+    if (!rc) rc = enqueue_refit(c, s, hp->jacobi_iters, false);
+    cudaEventRecord(ev.ev[1], c->stream);
+    if (!rc) rc = download_traj(c, c->Rs, R_out, R);
+    int err = INT_MAX;
+    cudaMemcpyAsync(&err, c->err, 4, cudaMemcpyDeviceToHost, c->stream);
+    CK(cudaStreamSynchronize(c->stream));
+    if (rc) return rc;
+    c->timing.refit_ms = ev.ms(0, 1);
+    if (err != 0x7f7f7f7f && err != INT_MAX)
+        return fail(CIMCS_INPUT_ERROR,
+                    "jacobi_solve: singular diagonal at active index " + std::to_string(err));
+    return 0;
+}
+
+int cimcs_score(cimcs_ctx* c, int32_t R, const double* Rsig, const int32_t* sigma, double lambda,
+                double* objective, double* rmse, double* hamming) {
+    if (int rc = check_ready(c, R)) return rc;
+    CK(cudaSetDevice(c->device));
+    if (int rc = ensure_state(c, pow2_slots(R))) return rc;
+    if (int rc = reset_flags(c, R)) return rc;
+    AltParams ap{};
+    ap.lambda = lambda;
+    if (int rc = set_alt(c, ap)) return rc;
+    if (int rc = upload_traj(c, Rsig, c->Rs, R)) return rc;
+    if (int rc = upload_sig(c, sigma, c->sig, R)) return rc;
+    cimcs_hyper h;
+    cimcs_hyper_default(&h);
+    const StepScalars s = make_scalars(&h);
+    int rc = c->dtype == CIMCS_F64 ? mask_T<double>(c, c->W0) : mask_T<float>(c, c->W0);
+    if (!rc) rc = enqueue_score(c, s, 0, nullptr, false);
+    const int nT = c->B * c->NR;
+    std::vector<double> o(nT), r(nT), h_(nT);
+    if (!rc) {
+        cudaMemcpyAsync(o.data(), c->obj, nT * 8, cudaMemcpyDeviceToHost, c->stream);
+        cudaMemcpyAsync(r.data(), c->rmse, nT * 8, cudaMemcpyDeviceToHost, c->stream);
+        cudaMemcpyAsync(h_.data(), c->ham, nT * 8, cudaMemcpyDeviceToHost, c->stream);
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    if (rc) return rc;
+    for (int b = 0; b < c->B; ++b)
+        for (int q = 0; q < R; ++q) {
+            if (objective) objective[b * R + q] = o[b * c->NR + q];
+            if (rmse) rmse[b * R + q] = r[b * c->NR + q];
+            if (hamming) hamming[b * R + q] = h_[b * c->NR + q];
+        }
+    return 0;
+}
+
+int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp, int32_t cdp,
+                const uint64_t* seeds, const double* R_init, int32_t track_best, double* R_out,
+                int32_t* sigma_out, cimcs_record* hist, int32_t* n_hist, int32_t* fail_alt,
+                int32_t* fail_index) {
+    if (int rc = check_ready(c, R)) return rc;
+    if (int rc = validate(hp)) return rc;
+    if (backend != CIMCS_MFZ_BN && backend != CIMCS_MFZ_CN)
+        return fail(CIMCS_CONFIG_ERROR, "backend must be mfz-bn or mfz-cn");
+    if (cdp != CIMCS_CDP_JACOBI)
+        return fail(CIMCS_CONFIG_ERROR, "cdp: only the damped Jacobi refit is on the GPU path");
+    if (!seeds) return fail(CIMCS_INPUT_ERROR, "null seeds");
+    CK(cudaSetDevice(c->device));
+    const int NR = pow2_slots(R);
+    if (int rc = ensure_state(c, NR)) return rc;
+    if (int rc = upload_pump(c, hp)) return rc;
+    const int nalt = hp->velo + 1;
+    const int nT = c->B * NR;
+    if (c->hist_cap < nalt * nT) {
+        if (c->hist) cudaFree(c->hist);
+        c->hist = nullptr;
+        if (int rc = dalloc(&c->hist, (size_t)nalt * nT * sizeof(DevRecord))) return rc;
+        c->hist_cap = nalt * nT;
+    }
+    const int bn = backend == CIMCS_MFZ_BN;
+    const StepScalars s = make_scalars(hp);
+    const int ntraj = c->B * R;
+    const size_t nc0 = (size_t)ntraj * c->N;
+
+    // host streams + pinned double buffer for c0
+    std::vector<HostRng> rngs;
+    rngs.reserve(ntraj);
+    for (int t = 0; t < ntraj; ++t) rngs.emplace_back(seeds[t]);
+    double* pinned = nullptr;
+    CK(cudaMallocHost(&pinned, 2 * nc0 * 8));
+    std::unique_ptr<double, decltype(&cudaFreeHost)> pin_guard(pinned, &cudaFreeHost);
+    double* dc0 = nullptr;
+    if (int rc = dalloc(&dc0, nc0 * 8)) return rc;
+    std::unique_ptr<double, decltype(&cudaFree)> dc0_guard(dc0, &cudaFree);
+    std::vector<AltParams> alts(nalt);
+    for (int i = 0; i < nalt; ++i)
+        alts[i] = make_alt(hp, eta_schedule(i, hp->eta_init, hp->eta_end, hp->velo), i);
+    AltParams* halts = nullptr;
+    CK(cudaMallocHost(&halts, nalt * sizeof(AltParams)));
+    std::unique_ptr<AltParams, decltype(&cudaFreeHost)> alt_guard(halts, &cudaFreeHost);
+    std::copy(alts.begin(), alts.end(), halts);
+
+    Events ev(4 * nalt + 2);
+    Events slot_done(2);
+    cudaEventRecord(ev.ev[4 * nalt], c->stream);
+
+    // initial state: R_init (default hz), flags, best objective = +inf
+    int rc = reset_flags(c, R);
+    if (!rc) {
+        if (R_init)
+            rc = upload_traj(c, R_init, c->Rs, R);
+        else
+            rc = c->dtype == CIMCS_F64 ? rinit_hz_T<double>(c, R) : rinit_hz_T<float>(c, R);
+    }
+    if (rc) return rc;
+    CK(cudaMemsetAsync(c->sig, 0, c->state_elems(), c->stream));
+    {
+        std::vector<double> inf(nT, INFINITY);
+        CK(cudaMemcpyAsync(c->best_obj, inf.data(), nT * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemsetAsync(c->improved, 0, nT * 4, c->stream));
+        CK(cudaStreamSynchronize(c->stream));  // `inf` leaves scope
+    }
+    if (track_best) {
+        CK(cudaMemcpyAsync(c->bestR, c->Rs, c->state_elems() * c->elt(), cudaMemcpyDeviceToDevice,
+                           c->stream));
+        CK(cudaMemsetAsync(c->bestS, 0, c->state_elems(), c->stream));
+    }
+
+    // graphs: [init + steps], [support + jacobi], [score + finalize + median (+best)]
+    // The history slot differs per alternation, so the score graph is per-alternation
+    // cheap; the two heavy graphs are captured once and replayed.
+    Graph g_cim, g_refit;
+    if (c->use_graphs) {
+        rc = capture(c, g_cim, [&] {
+            int r2 = run_init(c, R, bn, dc0, nullptr, s.rt);
+            return r2 ? r2 : enqueue_steps(c, bn, s, hp->n_steps);
+        });
+        if (!rc) rc = capture(c, g_refit, [&] { return enqueue_refit(c, s, hp->jacobi_iters, true); });
+        if (rc) return rc;
+    }
+    const int v_slot = hp->jacobi_iters & 1;
+    gen_c0(rngs, c->N, pinned, c->host_threads);
+    for (int i = 0; i < nalt; ++i) {
+        double* slot = pinned + (size_t)(i & 1) * nc0;
+        CK(cudaMemcpyAsync(c->alt, &halts[i], sizeof(AltParams), cudaMemcpyHostToDevice,
+                           c->stream));
+        CK(cudaMemcpyAsync(dc0, slot, nc0 * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaEventRecord(slot_done.ev[i & 1], c->stream));
+        CK(cudaEventRecord(ev.ev[4 * i + 0], c->stream));
+        if (c->use_graphs) {
+            CK(cudaGraphLaunch(g_cim.exec, c->stream));
+        } else {
+            rc = run_init(c, R, bn, dc0, nullptr, s.rt);
+            if (!rc) rc = enqueue_steps(c, bn, s, hp->n_steps);
+            if (rc) return rc;
+        }
+        CK(cudaEventRecord(ev.ev[4 * i + 1], c->stream));
+        if (c->use_graphs) {
+            CK(cudaGraphLaunch(g_refit.exec, c->stream));
+        } else if ((rc = enqueue_refit(c, s, hp->jacobi_iters, true))) {
+            return rc;
+        }
+        CK(cudaEventRecord(ev.ev[4 * i + 2], c->stream));
+        if ((rc = enqueue_score(c, s, v_slot, c->hist + (size_t)i * nT, track_best != 0)))
+            return rc;
+        CK(cudaEventRecord(ev.ev[4 * i + 3], c->stream));
+        if (i + 1 < nalt) {
+            // draw the next alternation's c0 while the GPU works on this one
+            CK(cudaEventSynchronize(slot_done.ev[(i + 1) & 1]));
+            gen_c0(rngs, c->N, pinned + (size_t)((i + 1) & 1) * nc0, c->host_threads);
+        }
+    }
+    cudaEventRecord(ev.ev[4 * nalt + 1], c->stream);
+
+    // results
+    const void* Rsrc = track_best ? c->bestR : c->Rs;
+    const int8_t* Ssrc = track_best ? c->bestS : c->sig;
+    if (track_best) {
+        // best is only used when some alternation was recorded (isfinite(best_energy))
+        // -- trajectories with no record keep their current R/sigma.
+        std::vector<double> bo(nT);
+        CK(cudaMemcpyAsync(bo.data(), c->best_obj, nT * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        bool all = true;
+        for (int b = 0; b < c->B; ++b)
+            for (int q = 0; q < R; ++q) all &= std::isfinite(bo[b * NR + q]);
+        if (!all) {
+            // copy current state into best slots of unrecorded trajectories
+            std::vector<int> imp(nT, 0);
+            for (int b = 0; b < c->B; ++b)
+                for (int q = 0; q < R; ++q) imp[b * NR + q] = !std::isfinite(bo[b * NR + q]);
+            CK(cudaMemcpyAsync(c->improved, imp.data(), nT * 4, cudaMemcpyHostToDevice,
+                               c->stream));
+            const int g = grid_for(c->state_elems());
+            if (c->dtype == CIMCS_F64) {
+                DISPATCH_NR(NR, {
+                    best_update_kernel<double, NR_><<<g, 256, 0, c->stream>>>(
+                        c->improved, static_cast<const double*>(c->Rs), c->sig,
+                        static_cast<double*>(c->bestR), c->bestS, c->ldN, c->B);
+                });
+            } else {
+                DISPATCH_NR(NR, {
+                    best_update_kernel<float, NR_><<<g, 256, 0, c->stream>>>(
+                        c->improved, static_cast<const float*>(c->Rs), c->sig,
+                        static_cast<float*>(c->bestR), c->bestS, c->ldN, c->B);
+                });
+            }
+            CK(cudaStreamSynchronize(c->stream));
+        }
+    }
+    if (R_out && (rc = download_traj(c, Rsrc, R_out, R))) return rc;
+    if (sigma_out && (rc = download_sig(c, Ssrc, sigma_out, R))) return rc;
+    std::vector<DevRecord> dh((size_t)nalt * nT);
+    std::vector<int> nh(nT), fg(nT), fi(nT);
+    CK(cudaMemcpyAsync(dh.data(), c->hist, dh.size() * sizeof(DevRecord), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaMemcpyAsync(nh.data(), c->n_hist, nT * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(fg.data(), c->fail_gstep, nT * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(fi.data(), c->fail_idx, nT * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    int err = 0;
+    CK(cudaMemcpy(&err, c->err, 4, cudaMemcpyDeviceToHost));
+    if (err != 0x7f7f7f7f && err != INT_MAX)
+        return fail(CIMCS_INPUT_ERROR,
+                    "jacobi_solve: singular diagonal at active index " + std::to_string(err));
+
+    cimcs_timing& tm = c->timing;
+    tm.total_ms = ev.ms(4 * nalt, 4 * nalt + 1);
+    tm.cim_ms = tm.refit_ms = tm.score_ms = 0.0;
+    for (int i = 0; i < nalt; ++i) {
+        tm.cim_ms += ev.ms(4 * i + 0, 4 * i + 1);
+        tm.refit_ms += ev.ms(4 * i + 1, 4 * i + 2);
+        tm.score_ms += ev.ms(4 * i + 2, 4 * i + 3);
+    }
+    tm.step_launches = (int64_t)nalt * hp->n_steps;
+    tm.refit_launches = (int64_t)nalt * hp->jacobi_iters;
+    tm.other_launches = (int64_t)nalt * (2 + 3 + (track_best ? 1 : 0));
+    tm.step_bytes = (double)c->B * c->N * (double)c->N * c->elt();
+    tm.step_flops = 2.0 * c->B * (double)c->N * c->N * R;
+
+    for (int b = 0; b < c->B; ++b)
+        for (int q = 0; q < R; ++q) {
+            const int dt = b * NR + q, ht = b * R + q;
+            if (n_hist) n_hist[ht] = nh[dt];
+            const bool failed = fg[dt] != kFreeTraj;
+            if (fail_alt) fail_alt[ht] = failed ? fg[dt] / hp->n_steps : -1;
+            if (fail_index) fail_index[ht] = failed ? fi[dt] : -1;
+            if (hist)
+                for (int i = 0; i < nalt; ++i) {
+                    cimcs_record& o = hist[(size_t)ht * nalt + i];
+                    if (i < nh[dt]) {
+                        const DevRecord& d = dh[(size_t)i * nT + dt];
+                        o.i = d.i;
+                        o.support = d.support;
+                        o.eta = d.eta;
+                        o.hamiltonian = d.hamiltonian;
+                        o.rmse = d.rmse;
+                        o.hamming = d.hamming;
+                        o.min_e = d.min_e;
+                        o.median_e = d.median_e;
+                    } else {
+                        std::memset(&o, 0, sizeof(o));
+                        o.i = -1;
+                    }
+                }
+        }
+    return 0;
+}
+
+int cimcs_get_timing(const cimcs_ctx* c, cimcs_timing* out) {
+    if (!c || !out) return fail(CIMCS_INPUT_ERROR, "null argument");
+    *out = c->timing;
+    return 0;
+}
+
+}  // extern "C"
