@@ -244,7 +244,8 @@ class Context:
             raise InputError("all instances of a context must share N")
         As = [np.asfortranarray(i.A, np.float64) for i in instances]
         ys = [np.ascontiguousarray(i.y, np.float64) for i in instances]
-        truth = all(i.has_truth() for i in instances)
+        truth = all(getattr(i, "x_true", None) is not None and
+                    getattr(i, "xi_true", None) is not None for i in instances)
         xs = [np.ascontiguousarray(i.x_true, np.float64) for i in instances] if truth else None
         xis = [np.ascontiguousarray(i.xi_true, np.int32) for i in instances] if truth else None
         Ms = np.array([i.M for i in instances], np.int32)

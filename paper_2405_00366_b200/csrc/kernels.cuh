@@ -7,8 +7,12 @@
 // the oracle's ORC_CANON mode restates.
 //
 // Device layout (per context, B instances, ldN = round_up(N, 32), NR =
-// replica slots, a power of two <= 16):
-//   G   [B][ldN][ldN]  gram A^T A (symmetric, full diagonal), zero padded
+// replica slots, a power of two <= 16, RB = rows per CTA, nRB = ceil(N/RB),
+// ldJ = round_up(N, 64)):
+//   G   [B][nRB][ldJ][RB]  gram A^T A (symmetric, full diagonal) stored as
+//                          row-block panels: panel(rb)[j][r] = G[rb*RB + r][j],
+//                          so one pipeline stage (64 consecutive j of one
+//                          panel) is ONE contiguous bulk copy; zero padded
 //   D   [B][ldN]       diag(G)          hz [B][ldN]  A^T y
 //   Rs, C, E, W0, W1   [B][ldN][NR]     signal, amplitude, error, contraction input
 // A trajectory (b, r) owns column r of every [B][ldN][NR] array.
@@ -73,7 +77,7 @@ struct AltParams {
 };
 
 struct GemvArgs {
-    const void* G;       // [B][ldN][ldN]
+    const void* G;       // [B][nRB][ldJ][RB] panels
     const void* D;       // [B][ldN]
     const void* hz;      // [B][ldN]
     const void* Win;     // [B][ldN][NR]
@@ -94,7 +98,7 @@ struct GemvArgs {
     int* err;            // singular-diagonal report (Jacobi)
     double p_scalar;
     int step;            // step index inside the alternation
-    int N, ldN, B;
+    int N, ldN, B, ldJ;
     StepScalars s;
 };
 
@@ -204,12 +208,11 @@ __global__ void __launch_bounds__(kThreads, Cfg<T>::kMinBlocks) gemv_fused_kerne
     __shared__ unsigned long long s_min[kSeg][NR];
     __shared__ int s_frozen[NR];
 
-    const size_t gbase = (size_t)b * ldN * ldN;
-    const T* Gb = static_cast<const T*>(a.G) + gbase;
+    const T* Pb = static_cast<const T*>(a.G) + ((size_t)b * gridDim.x + blockIdx.x) *
+                                                    (size_t)a.ldJ * RB;
     const T* Wb = static_cast<const T*>(a.Win) + (size_t)b * ldN * NR;
     const int nchunks = (N + kChunk - 1) / kChunk;
-    const int ncols = min(RB, ldN - i0);  // valid (padded) columns of the tile
-    const uint32_t row_bytes = (uint32_t)ncols * sizeof(T);
+    constexpr uint32_t row_bytes = RB * sizeof(T);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -238,12 +241,12 @@ __global__ void __launch_bounds__(kThreads, Cfg<T>::kMinBlocks) gemv_fused_kerne
             const int nj = min(kChunk, N - j0);
             const int njw = min(kChunk, ldN - j0);  // W rows (zero padded to ldN)
             const uint32_t wbytes = (uint32_t)njw * NR * sizeof(T);
-            if (lane == 0) mbar_arrive_expect_tx(&full[s], nj * row_bytes + wbytes);
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&full[s], nj * row_bytes + wbytes);
+                bulk_g2s(stageG(s), Pb + (size_t)j0 * RB, nj * row_bytes, &full[s]);
+                bulk_g2s(stageW(s), Wb + (size_t)j0 * NR, wbytes, &full[s]);
+            }
             __syncwarp();
-            for (int r = lane; r < nj; r += 32)
-                bulk_g2s(stageG(s) + r * RB, Gb + (size_t)(j0 + r) * ldN + i0, row_bytes,
-                         &full[s]);
-            if (lane == 0) bulk_g2s(stageW(s), Wb + (size_t)j0 * NR, wbytes, &full[s]);
         }
         return;
     }
@@ -445,13 +448,14 @@ __global__ void __launch_bounds__(kThreads, Cfg<T>::kMinBlocks) gemv_fused_kerne
 // chain over k = 0..M-1 (canonical; restated by the oracle's fma_chain).
 // 64x64 tiles over the upper triangle, mirrored; A is M x N column-major.
 constexpr int kGT = 64, kGK = 16;
+template <typename T, int RB>
 __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ A, int M, int N,
-                                                   int ldN, size_t a_stride, double* G) {
+                                                   int ldJ, size_t a_stride, T* G, int nRB) {
     const int b = blockIdx.z;
     const int bi = blockIdx.y, bj = blockIdx.x;
     if (bj < bi) return;
     const double* Ab = A + (size_t)b * a_stride;
-    double* Gb = G + (size_t)b * ldN * ldN;
+    T* Gb = G + (size_t)b * nRB * ldJ * RB;
     __shared__ double As[kGK][kGT + 2];
     __shared__ double Bs[kGK][kGT + 2];
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -485,33 +489,40 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ A,
         }
         __syncthreads();
     }
+    // G[i][j] -> panel(i / RB)[j][i % RB] and, by symmetry, panel(j / RB)[i][j % RB]
 #pragma unroll
     for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const int i = i0 + ty * 4 + r, j = j0 + tx * 4 + c;
             if (i < N && j < N) {
-                Gb[(size_t)i * ldN + j] = acc[r][c];
-                Gb[(size_t)j * ldN + i] = acc[r][c];
+                const T v = (T)acc[r][c];
+                Gb[((size_t)(i / RB) * ldJ + j) * RB + (i % RB)] = v;
+                Gb[((size_t)(j / RB) * ldJ + i) * RB + (j % RB)] = v;
             }
         }
 }
 
-// hz = A^T y (sequential fma chain per column), D = diag(G).
+// hz = A^T y and D = diag(G) = ||A_i||^2, each one sequential fma chain
+// (D_i is therefore bit-identical to the gram's diagonal entry).
+template <typename T>
 __global__ void hz_diag_kernel(const double* __restrict__ A, const double* __restrict__ y,
                                const int* __restrict__ Ms, int N, int ldN, size_t a_stride,
-                               int y_stride, const double* __restrict__ G, double* hz,
-                               double* D, int B) {
+                               int y_stride, T* hz, T* D, int B) {
     const int b = blockIdx.y;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N || b >= B) return;
     const int M = Ms[b];
     const double* col = A + (size_t)b * a_stride + (size_t)i * M;
     const double* yb = y + (size_t)b * y_stride;
-    double acc = 0.0;
-    for (int k = 0; k < M; ++k) acc = __fma_rn(col[k], yb[k], acc);
-    hz[(size_t)b * ldN + i] = acc;
-    D[(size_t)b * ldN + i] = G[(size_t)b * ldN * ldN + (size_t)i * ldN + i];
+    double acc = 0.0, dd = 0.0;
+    for (int k = 0; k < M; ++k) {
+        const double v = col[k];
+        acc = __fma_rn(v, yb[k], acc);
+        dd = __fma_rn(v, v, dd);
+    }
+    hz[(size_t)b * ldN + i] = (T)acc;
+    D[(size_t)b * ldN + i] = (T)dd;
 }
 
 template <typename T>

@@ -274,8 +274,8 @@ struct cimcs_ctx {
     bool has_truth = false, built = false;
     double *dA = nullptr, *dy = nullptr;
     int* dM = nullptr;
-    double* dG64 = nullptr;  // fp64 gram (the G of the fp64 path)
-    float* dG32 = nullptr;
+    void* dG = nullptr;      // gram panels [B][nRB][ldJ][RB] in the path's dtype
+    int ldJ = 0, nRB = 0, RB = 0;
     void *dD = nullptr, *dhz = nullptr;
     double* dx = nullptr;
     int8_t* dxi = nullptr;
@@ -299,7 +299,7 @@ struct cimcs_ctx {
     cimcs_timing timing{};
 
     size_t elt() const { return dtype == CIMCS_F64 ? 8 : 4; }
-    const void* G() const { return dtype == CIMCS_F64 ? (const void*)dG64 : (const void*)dG32; }
+    const void* G() const { return dG; }
     size_t state_elems() const { return (size_t)B * ldN * NR; }
 };
 
@@ -321,13 +321,12 @@ void free_state(cimcs_ctx* c) {
 
 void free_problems(cimcs_ctx* c) {
     free_state(c);
-    void* ptrs[] = {c->dA, c->dy, c->dM, c->dG64, c->dG32, c->dD, c->dhz, c->dx, c->dxi};
+    void* ptrs[] = {c->dA, c->dy, c->dM, c->dG, c->dD, c->dhz, c->dx, c->dxi};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     c->dA = c->dy = nullptr;
     c->dM = nullptr;
-    c->dG64 = nullptr;
-    c->dG32 = nullptr;
+    c->dG = nullptr;
     c->dD = c->dhz = nullptr;
     c->dx = nullptr;
     c->dxi = nullptr;
@@ -633,15 +632,13 @@ GemvArgs base_args(cimcs_ctx* c, const StepScalars& s) {
     a.err = c->err;
     a.N = c->N;
     a.ldN = c->ldN;
+    a.ldJ = c->ldJ;
     a.B = c->B;
     a.s = s;
     return a;
 }
 
-int nRB_of(const cimcs_ctx* c) {
-    const int rb = c->dtype == CIMCS_F64 ? row_block<double>() : row_block<float>();
-    return (c->N + rb - 1) / rb;
-}
+int nRB_of(const cimcs_ctx* c) { return c->nRB; }
 
 // Enqueue the n_steps fused Euler steps of one CIM call (graph-capturable).
 int enqueue_steps(cimcs_ctx* c, int bn, const StepScalars& s, int n_steps) {
@@ -967,6 +964,9 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
     c->B = B;
     c->N = N;
     c->ldN = (N + 31) / 32 * 32;
+    c->ldJ = (N + kChunk - 1) / kChunk * kChunk;
+    c->RB = c->dtype == CIMCS_F64 ? row_block<double>() : row_block<float>();
+    c->nRB = (N + c->RB - 1) / c->RB;
     c->M.assign(M, M + B);
     c->Mmax = *std::max_element(c->M.begin(), c->M.end());
     c->has_truth = x_true != nullptr && xi_true != nullptr;
@@ -1005,95 +1005,86 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
 int cimcs_build_coupling(cimcs_ctx* c) {
     if (!c || c->B < 1) return fail(CIMCS_INPUT_ERROR, "no problems set");
     CK(cudaSetDevice(c->device));
-    const size_t nG = (size_t)c->B * c->ldN * c->ldN;
+    const size_t nG = (size_t)c->B * c->nRB * c->ldJ * c->RB;
     const size_t nv = (size_t)c->B * c->ldN;
+    const size_t es = c->elt();
     int rc;
-    if (!c->dG64 && (rc = dalloc(&c->dG64, nG * 8))) return rc;
-    double *hz64 = nullptr, *D64 = nullptr;
-    if ((rc = dalloc(&hz64, nv * 8)) || (rc = dalloc(&D64, nv * 8))) return rc;
+    if (!c->dG && (rc = dalloc(&c->dG, nG * es))) return rc;
+    if (!c->dhz && (rc = dalloc(&c->dhz, nv * es))) return rc;
+    if (!c->dD && (rc = dalloc(&c->dD, nv * es))) return rc;
     Events ev(2);
     cudaEventRecord(ev.ev[0], c->stream);
-    CK(cudaMemsetAsync(c->dG64, 0, nG * 8, c->stream));
+    CK(cudaMemsetAsync(c->dG, 0, nG * es, c->stream));
     const int nt = (c->N + kGT - 1) / kGT;
     const size_t astride = (size_t)c->Mmax * c->N;
-    // one launch per distinct M (instances of a phase grid differ in M)
+    const size_t gstride = (size_t)c->nRB * c->ldJ * c->RB;
+    // one launch per run of equal M (instances of a phase grid differ in M)
     for (int b = 0; b < c->B;) {
         int e = b;
         while (e < c->B && c->M[e] == c->M[b]) ++e;
-        gram_kernel<<<dim3(nt, nt, e - b), 256, 0, c->stream>>>(
-            c->dA + (size_t)b * astride, c->M[b], c->N, c->ldN, astride,
-            c->dG64 + (size_t)b * c->ldN * c->ldN);
+        const dim3 grid(nt, nt, e - b);
+        if (c->dtype == CIMCS_F64)
+            gram_kernel<double, row_block<double>()><<<grid, 256, 0, c->stream>>>(
+                c->dA + (size_t)b * astride, c->M[b], c->N, c->ldJ, astride,
+                static_cast<double*>(c->dG) + (size_t)b * gstride, c->nRB);
+        else
+            gram_kernel<float, row_block<float>()><<<grid, 256, 0, c->stream>>>(
+                c->dA + (size_t)b * astride, c->M[b], c->N, c->ldJ, astride,
+                static_cast<float*>(c->dG) + (size_t)b * gstride, c->nRB);
         CK(cudaGetLastError());
         b = e;
     }
-    hz_diag_kernel<<<dim3((c->N + 127) / 128, c->B), 128, 0, c->stream>>>(
-        c->dA, c->dy, c->dM, c->N, c->ldN, astride, c->Mmax, c->dG64, hz64, D64, c->B);
+    const dim3 g2((c->N + 127) / 128, c->B);
+    if (c->dtype == CIMCS_F64)
+        hz_diag_kernel<double><<<g2, 128, 0, c->stream>>>(
+            c->dA, c->dy, c->dM, c->N, c->ldN, astride, c->Mmax, static_cast<double*>(c->dhz),
+            static_cast<double*>(c->dD), c->B);
+    else
+        hz_diag_kernel<float><<<g2, 128, 0, c->stream>>>(
+            c->dA, c->dy, c->dM, c->N, c->ldN, astride, c->Mmax, static_cast<float*>(c->dhz),
+            static_cast<float*>(c->dD), c->B);
     CK(cudaGetLastError());
-    c->timing.other_launches += 2;
-    if (c->dtype == CIMCS_F64) {
-        c->dhz = hz64;
-        c->dD = D64;
-    } else {
-        float *G32 = nullptr, *hz32 = nullptr, *D32 = nullptr;
-        if ((rc = dalloc(&G32, nG * 4)) || (rc = dalloc(&hz32, nv * 4)) ||
-            (rc = dalloc(&D32, nv * 4)))
-            return rc;
-        convert_kernel<float><<<148 * 8, 256, 0, c->stream>>>(c->dG64, G32, nG);
-        convert_kernel<float><<<grid_for(nv), 256, 0, c->stream>>>(hz64, hz32, nv);
-        convert_kernel<float><<<grid_for(nv), 256, 0, c->stream>>>(D64, D32, nv);
-        CK(cudaGetLastError());
-        c->dG32 = G32;
-        c->dhz = hz32;
-        c->dD = D32;
-        CK(cudaStreamSynchronize(c->stream));
-        cudaFree(hz64);
-        cudaFree(D64);
-        // the fp64 gram is kept for cimcs_get_coupling only when small
-        if (nG * 8 > (size_t)1 << 30) {
-            cudaFree(c->dG64);
-            c->dG64 = nullptr;
-        }
-    }
     cudaEventRecord(ev.ev[1], c->stream);
     CK(cudaStreamSynchronize(c->stream));
     c->timing.gram_ms = ev.ms(0, 1);
+    c->timing.other_launches += 2;
     c->built = true;
     return 0;
 }
 
 int cimcs_get_coupling(cimcs_ctx* c, int32_t b, double* G, double* hz, double* D) {
     if (!c || !c->built || b < 0 || b >= c->B) return fail(CIMCS_INPUT_ERROR, "bad instance");
-    const int N = c->N, ld = c->ldN;
-    std::vector<double> row(ld);
-    if (G) {
-        if (c->dtype == CIMCS_F64 || c->dG64) {
-            for (int i = 0; i < N; ++i)
-                CK(cudaMemcpy(G + (size_t)i * N, c->dG64 + ((size_t)b * ld + i) * ld, N * 8,
-                              cudaMemcpyDeviceToHost));
-        } else {
-            std::vector<float> rf(N);
-            for (int i = 0; i < N; ++i) {
-                CK(cudaMemcpy(rf.data(), c->dG32 + ((size_t)b * ld + i) * ld, N * 4,
-                              cudaMemcpyDeviceToHost));
-                for (int j = 0; j < N; ++j) G[(size_t)i * N + j] = rf[j];
-            }
-        }
-    }
-    auto vec = [&](const void* d, double* h) -> int {
-        if (!h) return 0;
+    const int N = c->N, ld = c->ldN, RB = c->RB, ldJ = c->ldJ;
+    const size_t gstride = (size_t)c->nRB * ldJ * RB;
+    auto fetch = [&](const void* d, size_t off, size_t n, std::vector<double>& h) -> int {
+        h.resize(n);
         if (c->dtype == CIMCS_F64) {
-            CK(cudaMemcpy(h, static_cast<const double*>(d) + (size_t)b * ld, N * 8,
+            CK(cudaMemcpy(h.data(), static_cast<const double*>(d) + off, n * 8,
                           cudaMemcpyDeviceToHost));
         } else {
-            std::vector<float> f(N);
-            CK(cudaMemcpy(f.data(), static_cast<const float*>(d) + (size_t)b * ld, N * 4,
+            std::vector<float> f(n);
+            CK(cudaMemcpy(f.data(), static_cast<const float*>(d) + off, n * 4,
                           cudaMemcpyDeviceToHost));
-            for (int i = 0; i < N; ++i) h[i] = f[i];
+            for (size_t k = 0; k < n; ++k) h[k] = f[k];
         }
         return 0;
     };
-    if (int rc = vec(c->dhz, hz)) return rc;
-    return vec(c->dD, D);
+    std::vector<double> h;
+    if (G) {
+        if (int rc = fetch(c->dG, (size_t)b * gstride, gstride, h)) return rc;
+        for (int i = 0; i < N; ++i)
+            for (int j = 0; j < N; ++j)
+                G[(size_t)i * N + j] = h[((size_t)(i / RB) * ldJ + j) * RB + (i % RB)];
+    }
+    if (hz) {
+        if (int rc = fetch(c->dhz, (size_t)b * ld, N, h)) return rc;
+        std::copy(h.begin(), h.end(), hz);
+    }
+    if (D) {
+        if (int rc = fetch(c->dD, (size_t)b * ld, N, h)) return rc;
+        std::copy(h.begin(), h.end(), D);
+    }
+    return 0;
 }
 
 int cimcs_mfz_step(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp, double eta,
@@ -1440,7 +1431,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
     tm.step_launches = (int64_t)nalt * hp->n_steps;
     tm.refit_launches = (int64_t)nalt * hp->jacobi_iters;
     tm.other_launches = (int64_t)nalt * (2 + 3 + (track_best ? 1 : 0));
-    tm.step_bytes = (double)c->B * c->N * (double)c->N * c->elt();
+    tm.step_bytes = (double)c->B * c->N * (double)c->N * c->elt();  // dense G share
     tm.step_flops = 2.0 * c->B * (double)c->N * c->N * R;
 
     for (int b = 0; b < c->B; ++b)
