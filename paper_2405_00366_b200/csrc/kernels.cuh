@@ -176,6 +176,46 @@ __device__ __forceinline__ double fma_<double>(double a, double b, double c) {
     return __fma_rn(a, b, c);
 }
 
+// Operands of one j: the lane's RPL entries of G row j and the NR entries
+// of W row j (a warp-wide broadcast).
+template <typename T, int RPL, int NR>
+struct Ops {
+    T g[RPL];
+    T w[NR];
+    __device__ __forceinline__ void load(const T* gp, const T* wp) {
+        if constexpr (sizeof(T) == 4) {
+            const float4 v = *reinterpret_cast<const float4*>(gp);
+            g[0] = v.x; g[1] = v.y; g[2] = v.z; g[3] = v.w;
+        } else {
+            const double2 v = *reinterpret_cast<const double2*>(gp);
+            g[0] = v.x; g[1] = v.y;
+        }
+        if constexpr (sizeof(T) == 4 && NR % 4 == 0) {
+#pragma unroll
+            for (int q = 0; q < NR / 4; ++q) {
+                const float4 v = *reinterpret_cast<const float4*>(wp + 4 * q);
+                w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+            }
+        } else if constexpr (sizeof(T) == 8 && NR % 2 == 0) {
+#pragma unroll
+            for (int q = 0; q < NR / 2; ++q) {
+                const double2 v = *reinterpret_cast<const double2*>(wp + 2 * q);
+                w[2 * q] = v.x; w[2 * q + 1] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < NR; ++q) w[q] = wp[q];
+        }
+    }
+    // acc[r][q] = fma(G[j][i_r], W[j][q], acc[r][q]) -- the canonical chain step
+    __device__ __forceinline__ void fma_into(T (&acc)[RPL][NR]) const {
+#pragma unroll
+        for (int r = 0; r < RPL; ++r)
+#pragma unroll
+            for (int q = 0; q < NR; ++q) acc[r][q] = fma_<T>(g[r], w[q], acc[r][q]);
+    }
+};
+
 // -------------------------------------------------------- contraction core
 // One CTA = (instance b, RB rows).  Warps 0..7 consume; warp 8 produces.
 // Chunk c covers j in [64c, 64c + 64); consumer warp w handles
@@ -265,38 +305,21 @@ __global__ void __launch_bounds__(kThreads, Cfg<T>::kMinBlocks) gemv_fused_kerne
         const int nv = min(kGran, N - jw);
         const T* gs = stageG(s) + (warp * kGran) * RB + lane * RPL;
         const T* ws = stageW(s) + (warp * kGran) * NR;
+        if (nv == kGran) {
+            // software pipelined: operands of j+1 are in flight while j's fmas issue
+            Ops<T, RPL, NR> cur, nxt;
+            cur.load(gs, ws);
 #pragma unroll
-        for (int jj = 0; jj < kGran; ++jj) {
-            if (jj < nv) {
-                T g[RPL];
-                if constexpr (sizeof(T) == 4) {
-                    const float4 v = *reinterpret_cast<const float4*>(gs + jj * RB);
-                    g[0] = v.x; g[1] = v.y; g[2] = v.z; g[3] = v.w;
-                } else {
-                    const double2 v = *reinterpret_cast<const double2*>(gs + jj * RB);
-                    g[0] = v.x; g[1] = v.y;
-                }
-                T w[NR];
-                if constexpr (sizeof(T) == 4 && NR % 4 == 0) {
-#pragma unroll
-                    for (int q = 0; q < NR / 4; ++q) {
-                        const float4 v = *reinterpret_cast<const float4*>(ws + jj * NR + 4 * q);
-                        w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
-                    }
-                } else if constexpr (sizeof(T) == 8 && NR % 2 == 0) {
-#pragma unroll
-                    for (int q = 0; q < NR / 2; ++q) {
-                        const double2 v = *reinterpret_cast<const double2*>(ws + jj * NR + 2 * q);
-                        w[2 * q] = v.x; w[2 * q + 1] = v.y;
-                    }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < NR; ++q) w[q] = ws[jj * NR + q];
-                }
-#pragma unroll
-                for (int r = 0; r < RPL; ++r)
-#pragma unroll
-                    for (int q = 0; q < NR; ++q) acc[r][q] = fma_<T>(g[r], w[q], acc[r][q]);
+            for (int jj = 0; jj < kGran; ++jj) {
+                if (jj + 1 < kGran) nxt.load(gs + (jj + 1) * RB, ws + (jj + 1) * NR);
+                cur.fma_into(acc);
+                if (jj + 1 < kGran) cur = nxt;
+            }
+        } else {
+            for (int jj = 0; jj < nv; ++jj) {
+                Ops<T, RPL, NR> cur;
+                cur.load(gs + jj * RB, ws + jj * NR);
+                cur.fma_into(acc);
             }
         }
         __syncwarp();
@@ -313,82 +336,135 @@ __global__ void __launch_bounds__(kThreads, Cfg<T>::kMinBlocks) gemv_fused_kerne
     consumer_bar();
 
     // ------------------------------------------------- fused epilogue
+    // Each consumer thread owns OPT outputs (row, replica q); all its global
+    // loads are issued before any arithmetic so their latencies overlap.
+    constexpr int OPT = (RB * NR + kSeg * 32 - 1) / (kSeg * 32);
     const int t = threadIdx.x;  // 0 .. 255
     const int q = t % NR;       // every output of this thread has replica q
     const bool frozen = s_frozen[q];
     T local_min = T(INFINITY);
     double sA = 0.0, sB = 0.0, sC = 0.0;  // score partials
     const StepScalars& sc = a.s;
-    for (int o = t; o < RB * NR; o += kSeg * 32) {
-        const int row = o / NR;
-        const int i = i0 + row;
-        if (i >= N) break;
-        T gw = red[(0 * NR + q) * RBP + row];
+    T gwv[OPT];
+    bool ok[OPT];
+    int iv[OPT];
 #pragma unroll
-        for (int w = 1; w < kSeg; ++w) gw = gw + red[(w * NR + q) * RBP + row];
-        const size_t vi = ((size_t)b * ldN + i) * NR + q;
-        const size_t si = (size_t)b * ldN + i;
-        if (frozen) continue;
-        if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
-            const T* Cp = static_cast<const T*>(a.C);
-            const T* Ep = static_cast<const T*>(a.E);
-            const T wv = static_cast<const T*>(a.Win)[vi];
-            const T Dv = static_cast<const T*>(a.D)[si];
-            const T hzv = static_cast<const T*>(a.hz)[si];
-            const T Rv = static_cast<const T*>(a.Rs)[vi];
-            const T c = Cp[vi];
-            const T e = Ep[vi];
-            const T Jw = Dv * wv - gw;  // apply_coupling: gram_diag∘w - G w
-            const T half_rt = (T)sc.half_rt;
+    for (int k = 0; k < OPT; ++k) {
+        const int o = t + k * kSeg * 32;
+        const int row = o / NR;
+        iv[k] = i0 + row;
+        ok[k] = o < RB * NR && iv[k] < N && !frozen;
+        T gw = T(0);
+        if (ok[k]) {
+            gw = red[(0 * NR + q) * RBP + row];
+#pragma unroll
+            for (int w = 1; w < kSeg; ++w) gw = gw + red[(w * NR + q) * RBP + row];
+        }
+        gwv[k] = gw;
+    }
+    if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
+        const T* __restrict__ Wp = static_cast<const T*>(a.Win);
+        const T* __restrict__ Dp = static_cast<const T*>(a.D);
+        const T* __restrict__ Hp = static_cast<const T*>(a.hz);
+        const T* __restrict__ Rp = static_cast<const T*>(a.Rs);
+        T* __restrict__ Cp = static_cast<T*>(a.C);
+        T* __restrict__ Ep = static_cast<T*>(a.E);
+        T* __restrict__ Wo = static_cast<T*>(a.Wout);
+        T wv[OPT], Dv[OPT], hzv[OPT], Rv[OPT], cv[OPT], ev[OPT];
+#pragma unroll
+        for (int k = 0; k < OPT; ++k) {
+            if (ok[k]) {
+                const size_t vi = ((size_t)b * ldN + iv[k]) * NR + q;
+                const size_t si = (size_t)b * ldN + iv[k];
+                wv[k] = __ldg(Wp + vi);
+                Dv[k] = __ldg(Dp + si);
+                hzv[k] = __ldg(Hp + si);
+                Rv[k] = __ldg(Rp + vi);
+                cv[k] = Cp[vi];
+                ev[k] = Ep[vi];
+            }
+        }
+        const T half_rt = (T)sc.half_rt, rt = (T)sc.rt, dt = (T)sc.dt, Kj = (T)sc.Kj;
+        const T nbeta = (T)sc.nbeta, tau = (T)sc.tau;
+        const double pd = a.pump ? a.pump[a.step] : a.p_scalar;
+        const T loss = sc.minus_j != 0.0 ? (T)((-1.0 + pd) - sc.minus_j) : (T)(-1.0 + pd);
+        const T thresh = (T)a.alt->thresh;
+#pragma unroll
+        for (int k = 0; k < OPT; ++k) {
+            if (!ok[k]) continue;
+            const size_t vi = ((size_t)b * ldN + iv[k]) * NR + q;
+            const T c = cv[k], e = ev[k];
+            const T Jw = Dv[k] * wv[k] - gwv[k];  // apply_coupling: gram_diag∘w - G w
             T h;
             if constexpr (MODE == EPI_STEP_BN)
-                h = half_rt * (Jw + hzv);
+                h = half_rt * (Jw + hzv[k]);
             else
-                h = Jw + half_rt * hzv;
+                h = Jw + half_rt * hzv[k];
             if (a.Hdbg) static_cast<T*>(a.Hdbg)[vi] = h;
-            const double pd = a.pump ? a.pump[a.step] : a.p_scalar;
-            const T loss = sc.minus_j != 0.0 ? (T)((-1.0 + pd) - sc.minus_j) : (T)(-1.0 + pd);
-            const T thresh = (T)a.alt->thresh;
-            const T inj = ((T)sc.Kj * e) * (Rv * h - thresh);
-            const T cn = c + (T)sc.dt * ((loss - c * c) * c + inj);
-            const T en = e + (T)sc.dt * (((T)sc.nbeta * (c * c - (T)sc.tau)) * e);
+            const T inj = (Kj * e) * (Rv[k] * h - thresh);
+            const T cn = c + dt * ((loss - c * c) * c + inj);
+            const T en = e + dt * ((nbeta * (c * c - tau)) * e);
             if (!finite_(cn) || !finite_(en)) {
                 const int traj = b * NR + q;
                 atomicMin(&a.fail_gstep[traj], a.alt->gstep_base + a.step);
-                atomicMin(&a.fail_idx[traj], i);
+                atomicMin(&a.fail_idx[traj], iv[k]);
                 continue;
             }
-            static_cast<T*>(a.C)[vi] = cn;
-            static_cast<T*>(a.E)[vi] = en;
+            Cp[vi] = cn;
+            Ep[vi] = en;
             T wn;
             if constexpr (MODE == EPI_STEP_BN)
-                wn = Rv * (cn > T(0) ? T(1) : T(0));
+                wn = Rv[k] * (cn > T(0) ? T(1) : T(0));
             else
-                wn = (Rv * T(0.25)) * (cn + (T)sc.rt);
-            static_cast<T*>(a.Wout)[vi] = wn;
+                wn = (Rv[k] * T(0.25)) * (cn + rt);
+            Wo[vi] = wn;
             local_min = en < local_min ? en : local_min;
-        } else if constexpr (MODE == EPI_JACOBI) {
-            // cdp.cpp:60-61: offdiag = G R - D∘R; R = (1-dt_c) R + dt_c (b - offdiag) / D
-            T* Rp = static_cast<T*>(a.Rs);
-            const T Rv = Rp[vi];
-            const bool on = a.sigma[vi] != 0;
-            T rn = Rv;
-            if (on) {
-                const T Dv = static_cast<const T*>(a.D)[si];
-                if (Dv == T(0)) {
-                    atomicMin(a.err, i);
+        }
+    } else if constexpr (MODE == EPI_JACOBI) {
+        // cdp.cpp:60-61: offdiag = G R - D∘R; R = (1-dt_c) R + dt_c (b - offdiag) / D
+        T* __restrict__ Rp = static_cast<T*>(a.Rs);
+        const T* __restrict__ Dp = static_cast<const T*>(a.D);
+        const T* __restrict__ Hp = static_cast<const T*>(a.hz);
+        T* __restrict__ Wo = static_cast<T*>(a.Wout);
+        T Rv[OPT], Dv[OPT], bv[OPT];
+        bool on[OPT];
+#pragma unroll
+        for (int k = 0; k < OPT; ++k) {
+            if (ok[k]) {
+                const size_t vi = ((size_t)b * ldN + iv[k]) * NR + q;
+                const size_t si = (size_t)b * ldN + iv[k];
+                Rv[k] = Rp[vi];
+                on[k] = a.sigma[vi] != 0;
+                Dv[k] = __ldg(Dp + si);
+                bv[k] = __ldg(Hp + si);
+            }
+        }
+        const T omd = (T)sc.one_minus_dtc, dtc = (T)sc.dt_c;
+#pragma unroll
+        for (int k = 0; k < OPT; ++k) {
+            if (!ok[k]) continue;
+            const size_t vi = ((size_t)b * ldN + iv[k]) * NR + q;
+            T rn = Rv[k];
+            if (on[k]) {
+                if (Dv[k] == T(0)) {
+                    atomicMin(a.err, iv[k]);
                     continue;
                 }
-                const T off = gw - Dv * Rv;
-                const T bv = static_cast<const T*>(a.hz)[si];
-                rn = (T)sc.one_minus_dtc * Rv + (T)sc.dt_c * ((bv - off) / Dv);
+                const T off = gwv[k] - Dv[k] * Rv[k];
+                rn = omd * Rv[k] + dtc * ((bv[k] - off) / Dv[k]);
                 Rp[vi] = rn;
             }
-            static_cast<T*>(a.Wout)[vi] = rn * (on ? T(1) : T(0));
-        } else {  // EPI_SCORE: w = R∘sigma is Win; partial sums of w.Gw, hz.w, rmse
+            Wo[vi] = rn * (on[k] ? T(1) : T(0));
+        }
+    } else {  // EPI_SCORE: w = R∘sigma is Win; partial sums of w.Gw, hz.w, rmse
+#pragma unroll
+        for (int k = 0; k < OPT; ++k) {
+            if (!ok[k]) continue;
+            const size_t vi = ((size_t)b * ldN + iv[k]) * NR + q;
+            const size_t si = (size_t)b * ldN + iv[k];
             const T wv = static_cast<const T*>(a.Win)[vi];
             const T hzv = static_cast<const T*>(a.hz)[si];
-            sA = sA + (double)wv * (double)gw;
+            sA = sA + (double)wv * (double)gwv[k];
             sB = sB + (double)hzv * (double)wv;
             if (a.xtrue) {
                 const double xt = a.xitrue[si] ? a.xtrue[si] : 0.0;
