@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""Headline benchmark: MF-CIM spin-steps/s on BASELINE.json config 1.
+
+Workload (one "step" of this script = one full pass of the hot path over the
+batch): 64 seeded gen_instance(N=2000, alpha=0.5, a=0.1, nu=0.01) instances x
+16 replicas, K1 gram build, 20 alternations (velo=19) x 1000 fused Euler
+steps (dt 0.01, linear pump 0 -> 1.2) + damped-Jacobi refit (100 sweeps) +
+scoring.  Inputs (A, y) are resident in HBM when the timed region starts;
+the 1 GB gram (fp32) is larger than L2, so no flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--dtype f32|f64]
+
+Multi-GPU (torchrun, one rank per GPU): every rank solves its own 64-instance
+batch (seeds offset by rank) -- weak scaling, no data-path collective; the
+step time is the max over ranks.  ``--impl reference`` times the CPU
+restatement of the reference path (oracle/, matrix-free A^T(A w), no FMA,
+one trajectory per host thread as the reference's run_jobs pool) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+CFG = dict(N=2000, alpha=0.5, a=0.1, nu=0.01, B=64, R=16, velo=19, n_steps=1000)
+METRIC = "MF-CIM spin-steps/s"
+UNIT = "spin-steps/s"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """Per-launch DRAM traffic of the step kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_step_summary.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 2 + k and s[2 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def make_instances(rank):
+    import paper_2405_00366_b200 as P
+    seeds = [1 + rank * CFG["B"] + s for s in range(CFG["B"])]
+    return P.gen_instances(CFG["N"], [(CFG["alpha"], CFG["a"], CFG["nu"], s) for s in seeds])
+
+
+def cpu_sample(insts, nthreads, alt_limit=1):
+    """Bounded CPU sample: one trajectory per host thread, first alt_limit
+    alternations (1000 Euler steps each + refit + scoring), reference-literal
+    coupling (A^T(A w), orchestrator.cpp:86-88)."""
+    from oracle import oracle as O
+    hp = O.baseline_params(velo=CFG["velo"], n_steps=CFG["n_steps"])
+    n = nthreads
+    sel = [insts[k % len(insts)] for k in range(n)]
+    oinst = [O.Instance(i.A, i.y, i.x_true, i.xi_true) for i in sel]
+    seeds = np.array([O.mix_seed(i.seed, 1 + 3 * (k // len(insts)))
+                      for k, i in enumerate(sel)], np.uint64)
+    wall, _, _ = O.solve_batch_limited(oinst, seeds, hp, nthreads, alt_limit=alt_limit,
+                                       backend=O.MFZ_BN, mode=O.LITERAL)
+    spin_steps = n * CFG["N"] * CFG["n_steps"] * alt_limit
+    return spin_steps / wall, wall, n
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    insts = make_instances(0)
+    nthreads = os.cpu_count() or 1
+    vals, walls = [], []
+    for k in range(args.warmup + args.steps):
+        v, wall, n = cpu_sample(insts, nthreads)
+        if k >= args.warmup:
+            vals.append(v)
+            walls.append(wall)
+    v = statistics.median(vals)
+    sample = (f"{nthreads} trajectories (1 per host thread) of config-1 instances, each 1 "
+              f"alternation = {CFG['n_steps']} Euler steps + 100-sweep Jacobi refit + scoring, "
+              "fp64 matrix-free A^T(A w) as orchestrator.cpp:86-88")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(walls),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded gen_instance, datagen.cpp:15-55)",
+        "config": {"workload": "BASELINE config 1: N=2000 M=1000 K=200, 64 inst x 16 rep, "
+                               "20 x 1000 steps", "sample": "bounded CPU sample"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthreads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+    import paper_2405_00366_b200 as P
+
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    insts = make_instances(rank)
+    hp = P.baseline_params(velo=CFG["velo"], n_steps=CFG["n_steps"])
+    R = CFG["R"]
+    seeds = P.replica_seeds(insts, R, "mfz-bn")
+    nalt = CFG["velo"] + 1
+    units = CFG["B"] * R * CFG["N"] * CFG["n_steps"] * nalt  # spin-steps per rank per step
+
+    ctx = P.Context(local, args.dtype)
+    ctx.set_problems(insts)
+
+    def one_step():
+        ctx.build_coupling()
+        res = ctx.solve(R, "mfz-bn", hp, seeds)
+        tm = ctx.timing()
+        return res, tm
+
+    for _ in range(args.warmup):
+        one_step()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    dev_ms, step_ms_list, launches = [], [], 0
+    gram_ms, cim_ms, refit_ms, score_ms = [], [], [], []
+    barrier()
+    with ClockSampler(local) as clocks:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            res, tm = one_step()
+            dev_ms.append(tm["gram_ms"] + tm["total_ms"])
+            gram_ms.append(tm["gram_ms"])
+            cim_ms.append(tm["cim_ms"])
+            refit_ms.append(tm["refit_ms"])
+            score_ms.append(tm["score_ms"])
+            step_ms_list.append(tm["cim_ms"] / (nalt * CFG["n_steps"]))
+            launches += int(tm["step_launches"] + tm["refit_launches"] + tm["other_launches"]) + 2
+        barrier()
+        wall = time.perf_counter() - t0
+    total_dev_ms = sum(dev_ms)
+    if dist is not None:
+        t = torch.tensor([total_dev_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_dev_ms = float(t.item())
+    ms_per_step = total_dev_ms / args.steps
+    value = ws * units / (ms_per_step * 1e-3)
+
+    # roofline of the dominant kernel (the fused Euler step)
+    es = 4 if args.dtype == "f32" else 8
+    step_bytes = CFG["B"] * CFG["N"] * CFG["N"] * es  # algorithmic: the dense G share
+    step_s = statistics.median(step_ms_list) * 1e-3
+    peak, peak_kind = measured_peaks()
+    achieved = step_bytes / step_s / 1e9
+
+    # e2e: public API with HOST buffers, H2D of the instances and D2H of results inside
+    e2e_val, h2d, d2h = None, 0, 0
+    if not args.no_e2e:
+        ctx2 = P.Context(local, args.dtype)
+        barrier()
+        e2e_times = []
+        for _ in range(max(1, min(args.steps, 2))):
+            t1 = time.perf_counter()
+            ctx2.set_problems(insts)
+            ctx2.build_coupling()
+            r2 = ctx2.solve(R, "mfz-bn", hp, seeds)
+            torch.cuda.synchronize()
+            e2e_times.append(time.perf_counter() - t1)
+        ctx2.close()
+        e2e_s = max(e2e_times)
+        if dist is not None:
+            t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e_val = ws * units / e2e_s
+        h2d = sum(i.A.nbytes + i.y.nbytes + i.x_true.nbytes + i.xi_true.nbytes for i in insts)
+        h2d += CFG["B"] * R * CFG["N"] * 8 * nalt  # host-drawn c0 streams
+        d2h = r2["R"].nbytes + r2["sigma"].nbytes + r2["history"].nbytes
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        nthreads = os.cpu_count() or 1
+        v, wall_c, n = cpu_sample(insts, nthreads)
+        cpu = {"value": v, "unit": UNIT, "cores": nthreads, "kind": "port",
+               "sample": f"{n} trajectories (1/host thread) x 1 alternation x "
+                         f"{CFG['n_steps']} Euler steps + refit, fp64 A^T(A w) "
+                         f"restatement, {wall_c:.1f}s wall"}
+    ctx.close()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+            "data": "synthetic (seeded gen_instance, datagen.cpp:15-55)",
+            "config": {"workload": "BASELINE config 1: N=2000 M=1000 K=200 (alpha 0.5, a 0.1, "
+                                   "nu 0.01), 64 instances x 16 replicas, 20 alternations x "
+                                   "1000 Euler steps, dt 0.01, linear pump 0->1.2, Jacobi refit",
+                       "per_rank_instances": CFG["B"], "replicas": R,
+                       "step": "gram build + full alternating solve",
+                       "l2": "inputs larger than L2 (gram 1.02 GB fp32)"},
+            "instances_per_s": ws * CFG["B"] / (ms_per_step * 1e-3),
+            "breakdown_ms": {"gram": statistics.median(gram_ms), "cim": statistics.median(cim_ms),
+                             "refit": statistics.median(refit_ms),
+                             "score": statistics.median(score_ms)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(),
+                         "kernel": "gemv_fused_kernel (fused Euler step)",
+                         "bytes_per_launch": step_bytes, "peak_kind": peak_kind},
+            "e2e": None if e2e_val is None else {
+                "value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "wall_s": wall,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()
