@@ -102,6 +102,39 @@ struct GemvArgs {
     StepScalars s;
 };
 
+// fp32 tensor-core path: a contraction input W is stored as the concatenated
+// UMMA B operand [W | W_lo] (2*NR rows, K-major, canonical no-swizzle layout)
+// where W_lo = W - trunc_tf32(W) is its tf32 residue (see tc_kernels.cuh).
+constexpr int kTcChunkJ = 64;
+__host__ __device__ inline size_t tc_wofs(int ldJ, int NR, int b, int j, int r) {
+    const int NC = 2 * NR, c = j / kTcChunkJ, jl = j % kTcChunkJ;
+    return (size_t)b * ldJ * NC + (size_t)c * kTcChunkJ * NC + (jl / 4) * 4 * NC + (r / 8) * 32 +
+           (r % 8) * 4 + (jl % 4);
+}
+__host__ __device__ inline float trunc_tf32(float x) {
+#ifdef __CUDA_ARCH__
+    return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+#else
+    uint32_t u;
+    memcpy(&u, &x, 4);
+    u &= 0xFFFFE000u;
+    memcpy(&x, &u, 4);
+    return x;
+#endif
+}
+// Store one contraction input value: standard [b][i][r] layout, or (tc) the
+// canonical concatenated operand with its tf32 residue.
+template <typename T>
+__device__ __forceinline__ void put_w(T* W, int tc, int ldN, int ldJ, int NR, int b, int i, int r,
+                                      T v) {
+    if (tc) {
+        W[tc_wofs(ldJ, NR, b, i, r)] = v;
+        W[tc_wofs(ldJ, NR, b, i, NR + r)] = (T)((float)v - trunc_tf32((float)v));
+    } else {
+        W[((size_t)b * ldN + i) * NR + r] = v;
+    }
+}
+
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -615,7 +648,7 @@ template <typename T, int NR, int BN>
 __global__ void init_state_kernel(const double* __restrict__ c0, int Rreal, int N, int ldN,
                                   int B, const T* __restrict__ Rs, T* C, T* E, T* W,
                                   const int* fail_gstep, unsigned long long* minE, double rt,
-                                  const double* __restrict__ e0) {
+                                  const double* __restrict__ e0, int tc, int ldJ) {
     const size_t total = (size_t)B * ldN * NR;
     for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < total;
          k += (size_t)gridDim.x * blockDim.x) {
@@ -629,7 +662,8 @@ __global__ void init_state_kernel(const double* __restrict__ c0, int Rreal, int 
         if (i >= N || q >= Rreal) {
             C[k] = T(0);
             E[k] = T(1);
-            W[k] = T(0);
+            if (i < N) put_w<T>(W, tc, ldN, ldJ, NR, b, i, q, T(0));
+            else if (!tc) W[k] = T(0);
             continue;
         }
         const size_t hk = ((size_t)b * Rreal + q) * N + i;
@@ -637,7 +671,8 @@ __global__ void init_state_kernel(const double* __restrict__ c0, int Rreal, int 
         C[k] = c;
         E[k] = e0 ? (T)e0[hk] : T(1);
         const T R = Rs[k];
-        W[k] = BN ? R * (c > T(0) ? T(1) : T(0)) : (R * T(0.25)) * (c + (T)rt);
+        put_w<T>(W, tc, ldN, ldJ, NR, b, i, q,
+                 BN ? R * (c > T(0) ? T(1) : T(0)) : (R * T(0.25)) * (c + (T)rt));
     }
 }
 
@@ -645,7 +680,8 @@ __global__ void init_state_kernel(const double* __restrict__ c0, int Rreal, int 
 // refit input V = R∘sigma.  Frozen trajectories keep their last sigma.
 template <typename T, int NR>
 __global__ void support_kernel(const T* __restrict__ C, const T* __restrict__ Rs, int8_t* sig,
-                               T* V, const int* fail_gstep, int N, int ldN, int B) {
+                               T* V, const int* fail_gstep, int N, int ldN, int B, int tc,
+                               int ldJ) {
     const size_t total = (size_t)B * ldN * NR;
     for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < total;
          k += (size_t)gridDim.x * blockDim.x) {
@@ -656,7 +692,8 @@ __global__ void support_kernel(const T* __restrict__ C, const T* __restrict__ Rs
         if (fail_gstep[b * NR + q] != kFreeTraj) continue;
         const int8_t s = (i < N && C[k] > T(0)) ? 1 : 0;
         sig[k] = s;
-        V[k] = Rs[k] * (s ? T(1) : T(0));
+        if (i < N) put_w<T>(V, tc, ldN, ldJ, NR, b, i, q, Rs[k] * (s ? T(1) : T(0)));
+        else if (!tc) V[k] = T(0);
     }
 }
 

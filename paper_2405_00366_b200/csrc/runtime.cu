@@ -23,6 +23,7 @@
 #include "../../include/cimcs_gpu.h"
 #include "host_rng.hpp"
 #include "kernels.cuh"
+#include "tc_kernels.cuh"
 
 using namespace cimcs;
 
@@ -125,10 +126,16 @@ __global__ void rinit_hz_kernel(const T* __restrict__ hz, T* Rs, int Rreal, int 
 
 template <typename T, int NR>
 __global__ void mask_kernel(const T* __restrict__ Rs, const int8_t* __restrict__ sig, T* V,
-                            size_t total) {
+                            size_t total, int N, int ldN, int ldJ, int tc) {
     for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < total;
-         k += (size_t)gridDim.x * blockDim.x)
-        V[k] = Rs[k] * (sig[k] ? T(1) : T(0));
+         k += (size_t)gridDim.x * blockDim.x) {
+        const int q = k % NR;
+        const size_t bi = k / NR;
+        const int i = bi % ldN;
+        const int b = bi / ldN;
+        if (i < N) put_w<T>(V, tc, ldN, ldJ, NR, b, i, q, Rs[k] * (sig[k] ? T(1) : T(0)));
+        else if (!tc) V[k] = T(0);
+    }
 }
 
 __global__ void traj_flags_kernel(int* fail_gstep, int* fail_idx, int Rreal, int NR, int B) {
@@ -268,6 +275,10 @@ struct cimcs_ctx {
     cudaStream_t stream = nullptr;
     int host_threads = 0;
     bool use_graphs = true;
+    bool want_tc = true;  // fp32 contraction on tcgen05 (3xTF32)
+    bool tc = false;      // active for the current problem set
+    int nch = 0;
+    int num_sms = 148;
     // problems
     int B = 0, N = 0, ldN = 0, Mmax = 0;
     std::vector<int> M;
@@ -301,6 +312,8 @@ struct cimcs_ctx {
     size_t elt() const { return dtype == CIMCS_F64 ? 8 : 4; }
     const void* G() const { return dG; }
     size_t state_elems() const { return (size_t)B * ldN * NR; }
+    // contraction-input arrays: [b][i][r], or (tc) [W | W_lo] canonical, 2*NR rows
+    size_t w_elems() const { return (size_t)B * (ldJ > ldN ? ldJ : ldN) * NR * (tc ? 2 : 1); }
 };
 
 namespace {
@@ -365,9 +378,10 @@ int ensure_state(cimcs_ctx* c, int NR) {
     const int nRB = (c->N + (c->dtype == CIMCS_F64 ? row_block<double>() : row_block<float>()) - 1) /
                     (c->dtype == CIMCS_F64 ? row_block<double>() : row_block<float>());
     int rc = 0;
+    const size_t nw = c->w_elems();
     if ((rc = dalloc(&c->Rs, n * es)) || (rc = dalloc(&c->C, n * es)) ||
-        (rc = dalloc(&c->E, n * es)) || (rc = dalloc(&c->W0, n * es)) ||
-        (rc = dalloc(&c->W1, n * es)) || (rc = dalloc(&c->Hdbg, n * es)) ||
+        (rc = dalloc(&c->E, n * es)) || (rc = dalloc(&c->W0, nw * es)) ||
+        (rc = dalloc(&c->W1, nw * es)) || (rc = dalloc(&c->Hdbg, n * es)) ||
         (rc = dalloc(&c->bestR, n * es)) || (rc = dalloc(&c->sig, n)) ||
         (rc = dalloc(&c->bestS, n)) || (rc = dalloc(&c->fail_gstep, nT * 4)) ||
         (rc = dalloc(&c->fail_idx, nT * 4)) || (rc = dalloc(&c->n_hist, nT * 4)) ||
@@ -460,9 +474,71 @@ int launch_gemv_T(cimcs_ctx* c, int mode, const GemvArgs& a) {
     }
 }
 
+template <int NR, int MODE>
+int launch_tc_t(cimcs_ctx* c, const GemvArgs& g) {
+    TcArgs a{};
+    a.G = static_cast<const float*>(g.G);
+    a.D = static_cast<const float*>(g.D);
+    a.hz = static_cast<const float*>(g.hz);
+    a.Win = static_cast<const float*>(g.Win);
+    a.Wout = static_cast<float*>(g.Wout);
+    a.Rs = static_cast<float*>(g.Rs);
+    a.C = static_cast<float*>(g.C);
+    a.E = static_cast<float*>(g.E);
+    a.Hdbg = static_cast<float*>(g.Hdbg);
+    a.sigma = g.sigma;
+    a.fail_gstep = g.fail_gstep;
+    a.fail_idx = g.fail_idx;
+    a.minE = g.minE;
+    a.part = g.part;
+    a.pump = g.pump;
+    a.alt = g.alt;
+    a.xtrue = g.xtrue;
+    a.xitrue = g.xitrue;
+    a.err = g.err;
+    a.p_scalar = g.p_scalar;
+    a.step = g.step;
+    a.N = c->N;
+    a.ldN = c->ldN;
+    a.ldJ = c->ldJ;
+    a.B = c->B;
+    a.nRB = c->nRB;
+    a.nch = c->nch;
+    a.ntiles = c->B * c->nRB;
+    a.s = g.s;
+    auto kern = tc_step_kernel<NR, MODE>;
+    constexpr size_t smem = tc_smem_bytes(NR);
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const int grid = std::min(a.ntiles, c->num_sms);
+    kern<<<grid, kTcThreads, smem, c->stream>>>(a);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+template <int NR>
+int launch_tc_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
+    switch (mode) {
+        case EPI_STEP_BN: return launch_tc_t<NR, EPI_STEP_BN>(c, a);
+        case EPI_STEP_CN: return launch_tc_t<NR, EPI_STEP_CN>(c, a);
+        case EPI_JACOBI: return launch_tc_t<NR, EPI_JACOBI>(c, a);
+        default: return launch_tc_t<NR, EPI_SCORE>(c, a);
+    }
+}
+
 int launch_gemv(cimcs_ctx* c, int mode, const GemvArgs& a) {
+    if (c->tc) return c->NR == 8 ? launch_tc_nr<8>(c, mode, a) : launch_tc_nr<16>(c, mode, a);
     return c->dtype == CIMCS_F64 ? launch_gemv_T<double>(c, mode, a)
                                  : launch_gemv_T<float>(c, mode, a);
+}
+
+// replica slots: a power of two; the tensor-core path needs MMA N in {8, 16}
+int slots_for(const cimcs_ctx* c, int R) {
+    const int p = pow2_slots(R);
+    return c->tc ? std::max(8, p) : p;
 }
 
 // Generic NR/T dispatch for the small state kernels.
@@ -484,12 +560,12 @@ int run_init_T(cimcs_ctx* c, int Rreal, int bn, const double* dc0, const double*
             init_state_kernel<T, NR_, 1><<<g, 256, 0, c->stream>>>(
                 dc0, Rreal, c->N, c->ldN, c->B, static_cast<const T*>(c->Rs),
                 static_cast<T*>(c->C), static_cast<T*>(c->E), W, c->fail_gstep, c->minE, rt,
-                de0);
+                de0, c->tc ? 1 : 0, c->ldJ);
         else
             init_state_kernel<T, NR_, 0><<<g, 256, 0, c->stream>>>(
                 dc0, Rreal, c->N, c->ldN, c->B, static_cast<const T*>(c->Rs),
                 static_cast<T*>(c->C), static_cast<T*>(c->E), W, c->fail_gstep, c->minE, rt,
-                de0);
+                de0, c->tc ? 1 : 0, c->ldJ);
     });
     CK(cudaGetLastError());
     return 0;
@@ -506,7 +582,7 @@ int run_support_T(cimcs_ctx* c) {
     DISPATCH_NR(c->NR, {
         support_kernel<T, NR_><<<g, 256, 0, c->stream>>>(
             static_cast<const T*>(c->C), static_cast<const T*>(c->Rs), c->sig,
-            static_cast<T*>(c->W0), c->fail_gstep, c->N, c->ldN, c->B);
+            static_cast<T*>(c->W0), c->fail_gstep, c->N, c->ldN, c->B, c->tc ? 1 : 0, c->ldJ);
     });
     CK(cudaGetLastError());
     return 0;
@@ -597,7 +673,8 @@ int mask_T(cimcs_ctx* c, void* V) {
     const int g = grid_for(c->state_elems());
     DISPATCH_NR(c->NR, {
         mask_kernel<T, NR_><<<g, 256, 0, c->stream>>>(static_cast<const T*>(c->Rs), c->sig,
-                                                      static_cast<T*>(V), c->state_elems());
+                                                      static_cast<T*>(V), c->state_elems(), c->N,
+                                                      c->ldN, c->ldJ, c->tc ? 1 : 0);
     });
     CK(cudaGetLastError());
     return 0;
@@ -913,6 +990,7 @@ int cimcs_create(int32_t device, int32_t dtype, cimcs_ctx** out) {
     if (prop.major != 10)
         return fail(CIMCS_CUDA_ERROR, "libcimcs_gpu is built for sm_100a (B200) only");
     auto* c = new cimcs_ctx();
+    c->num_sms = prop.multiProcessorCount;
     c->device = device;
     c->dtype = dtype;
     c->host_threads = std::max(1u, std::thread::hardware_concurrency());
@@ -948,6 +1026,10 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
     const std::string k(key);
     if (k == "host_threads") c->host_threads = (int)std::max<int64_t>(1, v);
     else if (k == "use_graphs") c->use_graphs = v != 0;
+    else if (k == "tensor_cores") {
+        if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set tensor_cores before set_problems");
+        c->want_tc = v != 0;
+    }
     else return fail(CIMCS_CONFIG_ERROR, "unknown option " + k);
     return 0;
 }
@@ -965,8 +1047,10 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
     c->N = N;
     c->ldN = (N + 31) / 32 * 32;
     c->ldJ = (N + kChunk - 1) / kChunk * kChunk;
-    c->RB = c->dtype == CIMCS_F64 ? row_block<double>() : row_block<float>();
+    c->tc = c->dtype == CIMCS_F32 && c->want_tc;
+    c->RB = c->dtype == CIMCS_F64 ? row_block<double>() : (c->tc ? kTcRows : row_block<float>());
     c->nRB = (N + c->RB - 1) / c->RB;
+    c->nch = c->ldJ / kTcChunk;
     c->M.assign(M, M + B);
     c->Mmax = *std::max_element(c->M.begin(), c->M.end());
     c->has_truth = x_true != nullptr && xi_true != nullptr;
@@ -1005,7 +1089,8 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
 int cimcs_build_coupling(cimcs_ctx* c) {
     if (!c || c->B < 1) return fail(CIMCS_INPUT_ERROR, "no problems set");
     CK(cudaSetDevice(c->device));
-    const size_t nG = (size_t)c->B * c->nRB * c->ldJ * c->RB;
+    const size_t nG = c->tc ? (size_t)c->B * c->nRB * c->nch * kTcTileFloats
+                            : (size_t)c->B * c->nRB * c->ldJ * c->RB;
     const size_t nv = (size_t)c->B * c->ldN;
     const size_t es = c->elt();
     int rc;
@@ -1023,7 +1108,12 @@ int cimcs_build_coupling(cimcs_ctx* c) {
         int e = b;
         while (e < c->B && c->M[e] == c->M[b]) ++e;
         const dim3 grid(nt, nt, e - b);
-        if (c->dtype == CIMCS_F64)
+        if (c->tc)
+            tc_gram_kernel<<<grid, 256, 0, c->stream>>>(
+                c->dA + (size_t)b * astride, c->M[b], c->N, astride,
+                static_cast<float*>(c->dG) + (size_t)b * c->nRB * c->nch * kTcTileFloats, c->nRB,
+                c->nch);
+        else if (c->dtype == CIMCS_F64)
             gram_kernel<double, row_block<double>()><<<grid, 256, 0, c->stream>>>(
                 c->dA + (size_t)b * astride, c->M[b], c->N, c->ldJ, astride,
                 static_cast<double*>(c->dG) + (size_t)b * gstride, c->nRB);
@@ -1070,7 +1160,12 @@ int cimcs_get_coupling(cimcs_ctx* c, int32_t b, double* G, double* hz, double* D
         return 0;
     };
     std::vector<double> h;
-    if (G) {
+    if (G && c->tc) {
+        const size_t ts = (size_t)c->nRB * c->nch * kTcTileFloats;
+        if (int rc = fetch(c->dG, (size_t)b * ts, ts, h)) return rc;
+        for (int i = 0; i < N; ++i)
+            for (int j = 0; j < N; ++j) G[(size_t)i * N + j] = h[tc_gofs(c->nRB, c->nch, 0, i, j)];
+    } else if (G) {
         if (int rc = fetch(c->dG, (size_t)b * gstride, gstride, h)) return rc;
         for (int i = 0; i < N; ++i)
             for (int j = 0; j < N; ++j)
@@ -1096,7 +1191,7 @@ int cimcs_mfz_step(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* 
     if (backend != CIMCS_MFZ_BN && backend != CIMCS_MFZ_CN)
         return fail(CIMCS_CONFIG_ERROR, "backend must be mfz-bn or mfz-cn");
     CK(cudaSetDevice(c->device));
-    if (int rc = ensure_state(c, pow2_slots(R))) return rc;
+    if (int rc = ensure_state(c, slots_for(c, R))) return rc;
     const size_t n = (size_t)c->B * R * c->N;
     if (int rc = reset_flags(c, R)) return rc;
     if (int rc = set_alt(c, make_alt(hp, eta, 0))) return rc;
@@ -1147,7 +1242,7 @@ int cimcs_run_cim(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* h
     if (backend != CIMCS_MFZ_BN && backend != CIMCS_MFZ_CN)
         return fail(CIMCS_CONFIG_ERROR, "backend must be mfz-bn or mfz-cn");
     CK(cudaSetDevice(c->device));
-    if (int rc = ensure_state(c, pow2_slots(R))) return rc;
+    if (int rc = ensure_state(c, slots_for(c, R))) return rc;
     if (int rc = upload_pump(c, hp)) return rc;
     const size_t n = (size_t)c->B * R * c->N;
     if (int rc = reset_flags(c, R)) return rc;
@@ -1194,7 +1289,7 @@ int cimcs_refit(cimcs_ctx* c, int32_t R, const int32_t* sigma, const double* R_p
     if (int rc = check_ready(c, R)) return rc;
     if (!hp) return fail(CIMCS_CONFIG_ERROR, "null hyper-parameters");
     CK(cudaSetDevice(c->device));
-    if (int rc = ensure_state(c, pow2_slots(R))) return rc;
+    if (int rc = ensure_state(c, slots_for(c, R))) return rc;
     if (int rc = reset_flags(c, R)) return rc;
     if (int rc = upload_traj(c, R_prev, c->Rs, R)) return rc;
     if (int rc = upload_sig(c, sigma, c->sig, R)) return rc;
@@ -1220,7 +1315,7 @@ int cimcs_score(cimcs_ctx* c, int32_t R, const double* Rsig, const int32_t* sigm
                 double* objective, double* rmse, double* hamming) {
     if (int rc = check_ready(c, R)) return rc;
     CK(cudaSetDevice(c->device));
-    if (int rc = ensure_state(c, pow2_slots(R))) return rc;
+    if (int rc = ensure_state(c, slots_for(c, R))) return rc;
     if (int rc = reset_flags(c, R)) return rc;
     AltParams ap{};
     ap.lambda = lambda;
@@ -1262,7 +1357,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
         return fail(CIMCS_CONFIG_ERROR, "cdp: only the damped Jacobi refit is on the GPU path");
     if (!seeds) return fail(CIMCS_INPUT_ERROR, "null seeds");
     CK(cudaSetDevice(c->device));
-    const int NR = pow2_slots(R);
+    const int NR = slots_for(c, R);
     if (int rc = ensure_state(c, NR)) return rc;
     if (int rc = upload_pump(c, hp)) return rc;
     const int nalt = hp->velo + 1;

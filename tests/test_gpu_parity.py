@@ -283,3 +283,87 @@ def test_fp32_path_tolerance(gpu, O):
     assert same >= 0.9 * len(insts)
     assert np.mean(rel) <= 5e-2
     ctx.close()
+
+
+# ------------------------------------------------ fp32 tensor-core (tcgen05) path
+
+def _ctx_opts(P, insts, dtype, **opts):
+    ctx = P.Context(0, dtype)
+    for k, v in opts.items():
+        ctx.set_option(k, v)
+    ctx.set_problems(insts)
+    ctx.build_coupling()
+    return ctx
+
+
+@pytest.mark.parametrize("backend", ["mfz-bn", "mfz-cn"])
+@pytest.mark.parametrize("R", [3, 8, 16])
+def test_tc_step_field_accuracy(gpu, O, backend, R):
+    """3xTF32 tcgen05 contraction: local field within 2e-5 (relative to the
+    field's scale) of the fp64 oracle; CUDA-core fp32 shown for scale."""
+    insts = [O.gen_instance(300, 0.6, 0.2, 0.01, 3), O.gen_instance(300, 0.4, 0.1, 0.01, 4)]
+    probs = _probs(O, insts)
+    B, N = 2, 300
+    rng = np.random.default_rng(R)
+    Rs = rng.normal(size=(B, R, N))
+    c = rng.normal(scale=0.5, size=(B, R, N))
+    e = np.abs(rng.normal(size=(B, R, N))) + 0.1
+    hp = gpu.baseline_params()
+    out = {}
+    for tc in (1, 0):
+        ctx = _ctx_opts(gpu, insts, "f32", tensor_cores=tc)
+        out[tc] = ctx.mfz_step(R, backend, hp, 0.37, 0.83, Rs, c, e)
+        ctx.close()
+    ohp = O.baseline_params()
+    for b in range(B):
+        for r in range(R):
+            if backend == "mfz-bn":
+                h = probs[b].local_field_bn(Rs[b, r], (c[b, r] > 0).astype(np.int32), ohp.tau)
+            else:
+                h = probs[b].local_field_cn(Rs[b, r], c[b, r], ohp.tau)
+            scale = np.max(np.abs(h))
+            err_tc = np.max(np.abs(out[1]["h"][b, r] - h)) / scale
+            err_cc = np.max(np.abs(out[0]["h"][b, r] - h)) / scale
+            assert err_tc < 2e-5, (err_tc, err_cc)
+
+
+def test_tc_refit_and_score_accuracy(gpu, O):
+    insts = [O.gen_instance(300, 0.6, 0.2, 0.01, 7)]
+    p = _probs(O, insts)[0]
+    R = 16
+    rng = np.random.default_rng(2)
+    sigma = (rng.random((1, R, 300)) < 0.3).astype(np.int32)
+    Rp = rng.normal(size=(1, R, 300))
+    ctx = _ctx_opts(gpu, insts, "f32", tensor_cores=1)
+    out = ctx.refit(R, sigma, Rp, gpu.HyperParams())
+    sc = ctx.score(R, Rp, sigma, 0.05)
+    ctx.close()
+    for r in range(R):
+        ref = p.cdp(sigma[0, r], Rp[0, r], O.CDP_JACOBI, O.HyperParams())
+        assert np.max(np.abs(out[0, r] - ref)) < 1e-4 * max(1.0, np.max(np.abs(ref)))
+        keep = sigma[0, r] == 0  # untouched (fp32-rounded on upload)
+        assert np.array_equal(out[0, r][keep], Rp[0, r][keep].astype(np.float32))
+        obj = p.objective_at(Rp[0, r], sigma[0, r], 0.05)
+        assert math.isclose(sc["objective"][0, r], obj, rel_tol=1e-5, abs_tol=1e-6)
+
+
+def test_tc_solve_matches_fp64_supports(gpu, O):
+    """fp32 tensor-core solve vs the fp64 oracle (stated fp32 tolerance:
+    >= 90% identical supports, mean |dRMSE|/RMSE <= 5e-2)."""
+    insts = [O.gen_instance(256, 0.5, 0.1, 0.01, s) for s in range(1, 5)]
+    R = 4
+    hp = O.baseline_params(velo=9)
+    seeds = np.array([[O.mix_seed(i.seed, 1 + 3 * r) for r in range(R)] for i in insts],
+                     np.uint64)
+    ctx = _ctx_opts(gpu, insts, "f32", tensor_cores=1)
+    res = ctx.solve(R, "mfz-bn", gpu.baseline_params(velo=9), seeds)
+    ctx.close()
+    same, rel = 0, []
+    for b, inst in enumerate(insts):
+        for r in range(R):
+            ref = _oracle_solve(O, inst, O.MFZ_BN, hp, int(seeds[b, r]))
+            same += np.array_equal(res["sigma"][b, r], ref["sigma"])
+            g = O.rmse(res["R"][b, r], res["sigma"][b, r], inst.x_true, inst.xi_true)
+            rel.append(abs(g - ref["final_rmse"]) / ref["final_rmse"])
+    assert same >= 0.9 * len(insts) * R, same
+    assert np.mean(rel) <= 5e-2
