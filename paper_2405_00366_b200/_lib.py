@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcimcs_gpu.so")
+LIB_PATH = os.environ.get("CIMCS_GPU_LIB") or os.path.join(HERE, "libcimcs_gpu.so")
 
 OK, INPUT_ERROR, CONFIG_ERROR, DIVERGENCE, CUDA_ERROR = 0, 1, 2, 3, 4
 F32, F64 = 0, 1
