@@ -40,7 +40,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
     return d;
 }
 
-__global__ void probe(const float* A, const float* B, float* D, int passes, int km, int sanity) {
+__global__ void probe(const float* A, const float* B, float* D, int passes, int km, int sanity, int amn, int bmn, int swap) {
     __shared__ __align__(1024) unsigned char sA[M * K * 4];
     __shared__ __align__(1024) unsigned char sB[K * N * 4];
     __shared__ __align__(8) uint64_t bar;
@@ -48,11 +48,11 @@ __global__ void probe(const float* A, const float* B, float* D, int passes, int 
     const int t = threadIdx.x;
     for (int e = t; e < M * K; e += blockDim.x) {
         const int m = e / K, k = e % K;
-        *reinterpret_cast<float*>(sA + offA(m, k, km)) = A[m * K + k];
+        *reinterpret_cast<float*>(sA + offA(m, k, amn ? 0 : 1)) = A[m * K + k];
     }
     for (int e = t; e < K * N; e += blockDim.x) {
         const int k = e / N, n = e % N;
-        *reinterpret_cast<float*>(sB + offB(k, n, km)) = B[k * N + n];
+        *reinterpret_cast<float*>(sB + offB(k, n, bmn ? 0 : 1)) = B[k * N + n];
     }
     if (t == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
@@ -68,8 +68,7 @@ __global__ void probe(const float* A, const float* B, float* D, int passes, int 
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tbase;
     // idesc: F32 accum, A/B TF32, both MN-major, N>>3, M>>4
-    const uint32_t mj = km ? 0u : 1u;
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (mj << 15) | (mj << 16) |
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)amn << 15) | ((uint32_t)bmn << 16) |
                            ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
     if (sanity) {
         const int w = t / 32;
@@ -85,10 +84,14 @@ __global__ void probe(const float* A, const float* B, float* D, int passes, int 
             for (int kb = 0; kb < K / 8; ++kb) {
                 // MN-major: SBO = MN-group stride (128), LBO = K-group stride
                 // K-major : SBO = MN 8-row group stride (128), LBO = K 4-col group stride
-                const uint64_t da = km ? sdesc(su32(sA) + kb * 2 * (M / 8) * 128, (M / 8) * 128, 128)
-                                       : sdesc(su32(sA) + kb * (M / 4) * 128, (M / 4) * 128, 128);
-                const uint64_t db = km ? sdesc(su32(sB) + kb * 2 * (N / 8) * 128, (N / 8) * 128, 128)
-                                       : sdesc(su32(sB) + kb * (N / 4) * 128, (N / 4) * 128, 128);
+                uint32_t la = amn ? (M / 4) * 128 : (M / 8) * 128, sa = 128;
+                uint32_t lb = bmn ? (N / 4) * 128 : (N / 8) * 128, sb = 128;
+                if (swap & 1) { uint32_t t = la; la = sa; sa = t; }
+                if (swap & 2) { uint32_t t = lb; lb = sb; sb = t; }
+                const uint64_t da = amn ? sdesc(su32(sA) + kb * (M / 4) * 128, la, sa)
+                                        : sdesc(su32(sA) + kb * 2 * (M / 8) * 128, la, sa);
+                const uint64_t db = bmn ? sdesc(su32(sB) + kb * (N / 4) * 128, lb, sb)
+                                        : sdesc(su32(sB) + kb * 2 * (N / 8) * 128, lb, sb);
                 const uint32_t acc = (p | kb) ? 1u : 0u;
                 asm volatile(
                     "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -128,11 +131,11 @@ static float trunc_tf32(float x) {
 }
 
 static double run(float* dA, float* dB, float* dD, std::vector<float>& A, std::vector<float>& B,
-                  std::vector<float>& D, int km, int sanity) {
+                  std::vector<float>& D, int amn, int bmn, int swap, int sanity) {
     cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
     cudaMemset(dD, 0, D.size() * 4);
-    probe<<<1, 128>>>(dA, dB, dD, 1, km, sanity);
+    probe<<<1, 128>>>(dA, dB, dD, 1, 0, sanity, amn, bmn, swap);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("CUDA error %s\n", cudaGetErrorString(e)); exit(1); }
     cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
@@ -147,7 +150,9 @@ static double run(float* dA, float* dB, float* dD, std::vector<float>& A, std::v
     return maxerr;
 }
 
-int main() {
+int main(int argc, char** argv) {
+    const int amn = argc > 1 ? atoi(argv[1]) : 0, bmn = argc > 2 ? atoi(argv[2]) : 0,
+              swap = argc > 3 ? atoi(argv[3]) : 0;
     std::vector<float> A(M * K), B(K * N), D(M * N);
     srand(1);
     for (auto& v : A) v = trunc_tf32((float)rand() / RAND_MAX - 0.5f);
@@ -156,14 +161,7 @@ int main() {
     cudaMalloc(&dA, A.size() * 4);
     cudaMalloc(&dB, B.size() * 4);
     cudaMalloc(&dD, D.size() * 4);
-    printf("tmem st/ld sanity err: %.3e\n", run(dA, dB, dD, A, B, D, 0, 1));
-    printf("MN-major gemm err: %.3e  D[0]=%f D[17]=%f\n", run(dA, dB, dD, A, B, D, 0, 0), D[0], D[17]);
-    printf("K-major  gemm err: %.3e  D[0]=%f D[17]=%f\n", run(dA, dB, dD, A, B, D, 1, 0), D[0], D[17]);
-    for (int km = 0; km < 2; ++km) {
-        std::vector<float> A2(M * K, 1.0f + 3.0f / 4096.0f), B2(K * N, 0.0f);
-        B2[0] = 1.0f;
-        run(dA, dB, dD, A2, B2, D, km, 0);
-        printf("conversion probe km=%d: D = %.10f (trunc 1.0, rn 1.0009765625, exact %.10f)\n", km, D[0], 1.0 + 3.0 / 4096.0);
-    }
+    double e = run(dA, dB, dD, A, B, D, amn, bmn, swap, 0);
+    printf("A %s B %s swap %d : err %.3e  D[1]=%f\n", amn ? "MN" : "K ", bmn ? "MN" : "K ", swap, e, D[1]);
     return 0;
 }
