@@ -367,3 +367,20 @@ def test_tc_solve_matches_fp64_supports(gpu, O):
             rel.append(abs(g - ref["final_rmse"]) / ref["final_rmse"])
     assert same >= 0.9 * len(insts) * R, same
     assert np.mean(rel) <= 5e-2
+
+
+def test_solve_matches_reference_literal_order(gpu, O):
+    """fp64 GPU solve vs the oracle in the reference's own coupling form
+    (matrix-free A^T(A w), orchestrator.cpp:86-88): identical supports and
+    RMSE within 1e-12 relative on config-0 instances (4 seeds)."""
+    for s in range(4):
+        inst = O.gen_instance(500, 0.6, 0.2, 0.01, s)
+        hp = O.baseline_params()
+        seed = O.mix_seed(s, 1)
+        ref = O.Problem(inst, O.LITERAL).alternating_minimize(O.MFZ_BN, hp, O.Rng(seed))
+        ctx = _ctx(gpu, [inst])
+        res = ctx.solve(1, "mfz-bn", gpu.baseline_params(), [seed])
+        ctx.close()
+        assert np.array_equal(res["sigma"][0, 0], ref["sigma"])
+        g = O.rmse(res["R"][0, 0], res["sigma"][0, 0], inst.x_true, inst.xi_true)
+        assert math.isclose(g, ref["final_rmse"], rel_tol=1e-12)
