@@ -612,6 +612,87 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ A,
         }
 }
 
+// K1 v2: 128x128 tiles over the upper triangle, 256 threads x (8x8) outputs,
+// k in chunks of 8 staged through shared memory.  Each G entry is still ONE
+// sequential fma chain over k = 0..M-1 (the canonical order); zero padding
+// beyond M / N contributes fma(0, 0, acc) = acc exactly.
+constexpr int kG2T = 128, kG2K = 8;
+template <typename Out>
+__global__ void __launch_bounds__(256) gram128_kernel(const double* __restrict__ A, int M, int N,
+                                                      size_t a_stride, Out out) {
+    const int b = blockIdx.z;
+    const int bi = blockIdx.y, bj = blockIdx.x;
+    if (bj < bi) return;
+    const double* Ab = A + (size_t)b * a_stride;
+    __shared__ __align__(16) double As[kG2K][kG2T];
+    __shared__ __align__(16) double Bs[kG2K][kG2T];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int i0 = bi * kG2T, j0 = bj * kG2T;
+    double acc[8][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[r][c] = 0.0;
+    // loader: thread t fills column (t % 128) of As (t < 128) or Bs, 8 k values
+    const int lc = threadIdx.x % 128;
+    const bool lA = threadIdx.x < 128;
+    const int gcol = (lA ? i0 : j0) + lc;
+    const double* src = Ab + (size_t)gcol * M;
+    double (*dst)[kG2T] = lA ? As : Bs;
+    for (int k0 = 0; k0 < M; k0 += kG2K) {
+        double v[kG2K];
+#pragma unroll
+        for (int u = 0; u < kG2K; ++u)
+            v[u] = (gcol < N && k0 + u < M) ? __ldg(src + k0 + u) : 0.0;
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < kG2K; ++u) dst[u][lc] = v[u];
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < kG2K; ++kk) {
+            double av[8], bv[8];
+            const double2 a0 = *reinterpret_cast<const double2*>(&As[kk][ty * 4]);
+            const double2 a1 = *reinterpret_cast<const double2*>(&As[kk][ty * 4 + 2]);
+            const double2 a2 = *reinterpret_cast<const double2*>(&As[kk][64 + ty * 4]);
+            const double2 a3 = *reinterpret_cast<const double2*>(&As[kk][64 + ty * 4 + 2]);
+            const double2 b0 = *reinterpret_cast<const double2*>(&Bs[kk][tx * 4]);
+            const double2 b1 = *reinterpret_cast<const double2*>(&Bs[kk][tx * 4 + 2]);
+            const double2 b2 = *reinterpret_cast<const double2*>(&Bs[kk][64 + tx * 4]);
+            const double2 b3 = *reinterpret_cast<const double2*>(&Bs[kk][64 + tx * 4 + 2]);
+            av[0] = a0.x; av[1] = a0.y; av[2] = a1.x; av[3] = a1.y;
+            av[4] = a2.x; av[5] = a2.y; av[6] = a3.x; av[7] = a3.y;
+            bv[0] = b0.x; bv[1] = b0.y; bv[2] = b1.x; bv[3] = b1.y;
+            bv[4] = b2.x; bv[5] = b2.y; bv[6] = b3.x; bv[7] = b3.y;
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc[r][c] = __fma_rn(av[r], bv[c], acc[r][c]);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const int i = i0 + (r < 4 ? ty * 4 + r : 64 + ty * 4 + r - 4);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int j = j0 + (c < 4 ? tx * 4 + c : 64 + tx * 4 + c - 4);
+            if (i < N && j < N) {
+                out.store(b, i, j, acc[r][c]);
+                if (bi != bj) out.store(b, j, i, acc[r][c]);
+            }
+        }
+    }
+}
+
+// panel output of the CUDA-core contraction: panel(i / RB)[j][i % RB]
+template <typename T, int RB>
+struct PanelOut {
+    T* G;
+    int ldJ, nRB;
+    __device__ __forceinline__ void store(int b, int i, int j, double v) const {
+        G[(((size_t)b * nRB + i / RB) * ldJ + j) * RB + (i % RB)] = (T)v;
+    }
+};
+
 // hz = A^T y and D = diag(G) = ||A_i||^2, each one sequential fma chain
 // (D_i is therefore bit-identical to the gram's diagonal entry).
 template <typename T>

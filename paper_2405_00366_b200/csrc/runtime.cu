@@ -1100,27 +1100,27 @@ int cimcs_build_coupling(cimcs_ctx* c) {
     Events ev(2);
     cudaEventRecord(ev.ev[0], c->stream);
     CK(cudaMemsetAsync(c->dG, 0, nG * es, c->stream));
-    const int nt = (c->N + kGT - 1) / kGT;
+    const int nt = (c->N + kG2T - 1) / kG2T;
     const size_t astride = (size_t)c->Mmax * c->N;
-    const size_t gstride = (size_t)c->nRB * c->ldJ * c->RB;
     // one launch per run of equal M (instances of a phase grid differ in M)
     for (int b = 0; b < c->B;) {
         int e = b;
         while (e < c->B && c->M[e] == c->M[b]) ++e;
         const dim3 grid(nt, nt, e - b);
-        if (c->tc)
-            tc_gram_kernel<<<grid, 256, 0, c->stream>>>(
-                c->dA + (size_t)b * astride, c->M[b], c->N, astride,
-                static_cast<float*>(c->dG) + (size_t)b * c->nRB * c->nch * kTcTileFloats, c->nRB,
-                c->nch);
-        else if (c->dtype == CIMCS_F64)
-            gram_kernel<double, row_block<double>()><<<grid, 256, 0, c->stream>>>(
-                c->dA + (size_t)b * astride, c->M[b], c->N, c->ldJ, astride,
-                static_cast<double*>(c->dG) + (size_t)b * gstride, c->nRB);
-        else
-            gram_kernel<float, row_block<float>()><<<grid, 256, 0, c->stream>>>(
-                c->dA + (size_t)b * astride, c->M[b], c->N, c->ldJ, astride,
-                static_cast<float*>(c->dG) + (size_t)b * gstride, c->nRB);
+        const double* Ab = c->dA + (size_t)b * astride;
+        if (c->tc) {
+            TcPanelOut o{static_cast<float*>(c->dG) + (size_t)b * c->nRB * c->nch * kTcTileFloats,
+                         c->nRB, c->nch};
+            gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o);
+        } else if (c->dtype == CIMCS_F64) {
+            PanelOut<double, row_block<double>()> o{
+                static_cast<double*>(c->dG) + (size_t)b * c->nRB * c->ldJ * c->RB, c->ldJ, c->nRB};
+            gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o);
+        } else {
+            PanelOut<float, row_block<float>()> o{
+                static_cast<float*>(c->dG) + (size_t)b * c->nRB * c->ldJ * c->RB, c->ldJ, c->nRB};
+            gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o);
+        }
         CK(cudaGetLastError());
         b = e;
     }

@@ -461,6 +461,15 @@ constexpr size_t tc_smem_bytes(int NR) {
     return (size_t)kTcStages * (kTcTileFloats * 4 + 2 * kTcChunk * NR * 4) + 16 * 8 + 64;
 }
 
+// canonical tcgen05 A-operand output of the gram builder (fp32)
+struct TcPanelOut {
+    float* G;
+    int nRB, nch;
+    __device__ __forceinline__ void store(int b, int i, int j, double v) const {
+        G[tc_gofs(nRB, nch, b, i, j)] = (float)v;
+    }
+};
+
 // G panels in the canonical A layout, fp32 (gram rounded from the fp64 chain)
 __global__ void __launch_bounds__(256) tc_gram_kernel(const double* __restrict__ A, int M, int N,
                                                       size_t a_stride, float* G, int nRB,
