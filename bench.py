@@ -35,6 +35,15 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 CFG = dict(N=2000, alpha=0.5, a=0.1, nu=0.01, B=64, R=16, velo=19, n_steps=1000)
+WORKLOADS = {
+    0: "BASELINE config 0: N=500 M=300 K=100, 1 instance x 1 replica, fp64, 20 x 1000 steps",
+    1: "BASELINE config 1: N=2000 M=1000 K=200 (alpha 0.5, a 0.1, nu 0.01), 64 instances x 16 "
+       "replicas, 20 alternations x 1000 Euler steps, dt 0.01, linear pump 0->1.2, Jacobi refit",
+    2: "BASELINE config 2: phase sweep N=2000, alpha 0.3..0.9 x a 0.05..0.3 x 32 trials = 1344 "
+       "instances x 8 replicas, 20 x 1000 steps",
+    3: "BASELINE config 3: MRI-shaped synthetic, N=16384 (3-level Haar of a 128x128 ellipse "
+       "phantom), M=6554 random DCT rows, 1 instance x 16 replicas, 20 x 1000 steps",
+}
 METRIC = "MF-CIM spin-steps/s"
 UNIT = "spin-steps/s"
 
@@ -113,18 +122,25 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def make_instances(rank):
-    import paper_2405_00366_b200 as P
-    seeds = [1 + rank * CFG["B"] + s for s in range(CFG["B"])]
-    return P.gen_instances(CFG["N"], [(CFG["alpha"], CFG["a"], CFG["nu"], s) for s in seeds])
+def make_instances(rank, config=1):
+    """(instances, replicas, hyper-params, default dtype) of a BASELINE config."""
+    from paper_2405_00366_b200 import workloads as W
+    if config == 0:
+        return W.config0()
+    if config == 2:
+        return W.config2()
+    if config == 3:
+        return W.config3()
+    return W.config1(rank, CFG["B"])
 
 
-def cpu_sample(insts, nthreads, alt_limit=1):
+def cpu_sample(insts, nthreads, alt_limit=1, n_steps=None):
     """Bounded CPU sample: one trajectory per host thread, first alt_limit
-    alternations (1000 Euler steps each + refit + scoring), reference-literal
+    alternations (n_steps Euler steps each + refit + scoring), reference-literal
     coupling (A^T(A w), orchestrator.cpp:86-88)."""
     from oracle import oracle as O
-    hp = O.baseline_params(velo=CFG["velo"], n_steps=CFG["n_steps"])
+    n_steps = n_steps or CFG["n_steps"]
+    hp = O.baseline_params(velo=CFG["velo"], n_steps=n_steps)
     n = nthreads
     sel = [insts[k % len(insts)] for k in range(n)]
     oinst = [O.Instance(i.A, i.y, i.x_true, i.xi_true) for i in sel]
@@ -132,14 +148,14 @@ def cpu_sample(insts, nthreads, alt_limit=1):
                       for k, i in enumerate(sel)], np.uint64)
     wall, _, _ = O.solve_batch_limited(oinst, seeds, hp, nthreads, alt_limit=alt_limit,
                                        backend=O.MFZ_BN, mode=O.LITERAL)
-    spin_steps = n * CFG["N"] * CFG["n_steps"] * alt_limit
+    spin_steps = n * insts[0].N * n_steps * alt_limit
     return spin_steps / wall, wall, n
 
 
 def run_reference(args, ws, rank):
     if rank != 0:
         return
-    insts = make_instances(0)
+    insts, _, _, _ = make_instances(0, args.config)
     nthreads = os.cpu_count() or 1
     vals, walls = [], []
     for k in range(args.warmup + args.steps):
@@ -156,8 +172,7 @@ def run_reference(args, ws, rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(walls),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded gen_instance, datagen.cpp:15-55)",
-        "config": {"workload": "BASELINE config 1: N=2000 M=1000 K=200, 64 inst x 16 rep, "
-                               "20 x 1000 steps", "sample": "bounded CPU sample"},
+        "config": {"workload": WORKLOADS[args.config], "sample": "bounded CPU sample"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthreads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -174,12 +189,13 @@ def run_ours(args, ws, rank, local):
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl")
-    insts = make_instances(rank)
-    hp = P.baseline_params(velo=CFG["velo"], n_steps=CFG["n_steps"])
-    R = CFG["R"]
+    insts, R, hp, wdtype = make_instances(rank, args.config)
+    if args.dtype is None:
+        args.dtype = wdtype
     seeds = P.replica_seeds(insts, R, "mfz-bn")
-    nalt = CFG["velo"] + 1
-    units = CFG["B"] * R * CFG["N"] * CFG["n_steps"] * nalt  # spin-steps per rank per step
+    nalt = hp.velo + 1
+    Bn, Nn = len(insts), insts[0].N
+    units = Bn * R * Nn * hp.n_steps * nalt  # spin-steps per rank per step
 
     ctx = P.Context(local, args.dtype)
     ctx.set_problems(insts)
@@ -210,7 +226,7 @@ def run_ours(args, ws, rank, local):
             cim_ms.append(tm["cim_ms"])
             refit_ms.append(tm["refit_ms"])
             score_ms.append(tm["score_ms"])
-            step_ms_list.append(tm["cim_ms"] / (nalt * CFG["n_steps"]))
+            step_ms_list.append(tm["cim_ms"] / (nalt * hp.n_steps))
             launches += int(tm["step_launches"] + tm["refit_launches"] + tm["other_launches"]) + 2
         barrier()
         wall = time.perf_counter() - t0
@@ -224,7 +240,7 @@ def run_ours(args, ws, rank, local):
 
     # roofline of the dominant kernel (the fused Euler step)
     es = 4 if args.dtype == "f32" else 8
-    step_bytes = CFG["B"] * CFG["N"] * CFG["N"] * es  # algorithmic: the dense G share
+    step_bytes = Bn * Nn * Nn * es  # algorithmic: the dense G share
     step_s = statistics.median(step_ms_list) * 1e-3
     peak, peak_kind = measured_peaks()
     achieved = step_bytes / step_s / 1e9
@@ -250,20 +266,21 @@ def run_ours(args, ws, rank, local):
             e2e_s = float(t.item())
         e2e_val = ws * units / e2e_s
         h2d = sum(i.A.nbytes + i.y.nbytes + i.x_true.nbytes + i.xi_true.nbytes for i in insts)
-        h2d += CFG["B"] * R * CFG["N"] * 8 * nalt  # host-drawn c0 streams
+        h2d += Bn * R * Nn * 8 * nalt  # host-drawn c0 streams
         d2h = r2["R"].nbytes + r2["sigma"].nbytes + r2["history"].nbytes
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         nthreads = os.cpu_count() or 1
-        v, wall_c, n = cpu_sample(insts, nthreads)
+        cs = 100 if args.config == 3 else hp.n_steps  # config 3: 100-step sample
+        v, wall_c, n = cpu_sample(insts, nthreads, n_steps=cs)
         cpu = {"value": v, "unit": UNIT, "cores": nthreads, "kind": "port",
                "sample": f"{n} trajectories (1/host thread) x 1 alternation x "
-                         f"{CFG['n_steps']} Euler steps + refit, fp64 A^T(A w) "
+                         f"{cs} Euler steps + refit, fp64 A^T(A w) "
                          f"restatement, {wall_c:.1f}s wall"}
     ctx.close()
     fp64 = None
-    if args.dtype == "f32" and not args.no_fp64:
+    if args.dtype == "f32" and not args.no_fp64 and args.config == 1:
         c64 = P.Context(local, "f64")
         c64.set_problems(insts)
         c64.build_coupling()
@@ -274,7 +291,7 @@ def run_ours(args, ws, rank, local):
         t64 = c64.timing()
         c64.close()
         ms64 = t64["gram_ms"] + t64["total_ms"]
-        st64 = t64["cim_ms"] / (nalt * CFG["n_steps"]) * 1e-3
+        st64 = t64["cim_ms"] / (nalt * hp.n_steps) * 1e-3
         ach64 = 2 * step_bytes / st64 / 1e9 if args.dtype == "f32" else None
         fp64 = {"value": ws * units / (ms64 * 1e-3), "unit": UNIT, "ms_per_step": ms64,
                 "steps": 1, "warmup": 1,
@@ -287,21 +304,21 @@ def run_ours(args, ws, rank, local):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (seeded gen_instance, datagen.cpp:15-55)",
-            "config": {"workload": "BASELINE config 1: N=2000 M=1000 K=200 (alpha 0.5, a 0.1, "
-                                   "nu 0.01), 64 instances x 16 replicas, 20 alternations x "
-                                   "1000 Euler steps, dt 0.01, linear pump 0->1.2, Jacobi refit",
-                       "per_rank_instances": CFG["B"], "replicas": R,
+            "config": {"workload": WORKLOADS[args.config],
+                       "per_rank_instances": Bn, "replicas": R,
                        "step": "gram build + full alternating solve",
-                       "l2": "inputs larger than L2 (gram 1.02 GB fp32)"},
-            "instances_per_s": ws * CFG["B"] / (ms_per_step * 1e-3),
+                       "l2": ("inputs larger than L2 (gram %.2f GB)" % (step_bytes / 1e9)
+                              if step_bytes > 126e6 else "gram fits in L2 (no flush)")},
+            "instances_per_s": ws * Bn / (ms_per_step * 1e-3),
             "breakdown_ms": {"gram": statistics.median(gram_ms), "cim": statistics.median(cim_ms),
                              "refit": statistics.median(refit_ms),
                              "score": statistics.median(score_ms)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(),
+                         "frac": achieved / peak,
+                         "traffic": ncu_traffic() if args.config == 1 and args.dtype == "f32" else None,
                          "kernel": ("tc_step_kernel<16,BN> (fused Euler step, tcgen05 3xTF32)"
                                     if args.dtype == "f32" else
-                                    "gemv_fused_kernel<double,16,BN> (fused Euler step)"),
+                                    "gemv_fused_kernel<double> (fused Euler step, fp64 DFMA)"),
                          "bytes_per_launch": step_bytes, "peak_kind": peak_kind},
             "e2e": None if e2e_val is None else {
                 "value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
@@ -326,7 +343,9 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--dtype", default=None, choices=["f32", "f64"],
+                    help="default: the config's (f32 for 1-3, f64 for 0)")
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fp64", action="store_true", help="skip the fp64 secondary line")
