@@ -101,8 +101,18 @@ int cimcs_gen_instances(int32_t B, int32_t N, const double* alpha, const double*
 /* ------------------------------------------------------------ context */
 /* One per host thread; owns device buffers, one CUDA stream and graphs. */
 int cimcs_create(int32_t device, int32_t dtype, cimcs_ctx** out);
+/* Row-sharded context (one process per GPU, config 4): rank owns whole
+ * 128-spin row blocks [rank*per, (rank+1)*per) of every instance's gram and
+ * the state of those spins; the contraction input is all-gathered (NCCL)
+ * after every Euler step and Jacobi sweep inside the CUDA graphs.  No C ABI
+ * call changes meaning; every rank receives full result vectors.
+ * cimcs_nccl_unique_id fills 128 bytes on one rank, to be broadcast. */
+int cimcs_nccl_unique_id(uint8_t* out, int32_t nbytes);
+int cimcs_create_sharded(int32_t device, int32_t dtype, int32_t world, int32_t rank,
+                         const uint8_t* nccl_id, cimcs_ctx** out);
 void cimcs_destroy(cimcs_ctx* ctx);
-/* key: "host_threads" (c0 generator pool), "use_graphs" (0/1), "sparse_skip" (0/1). */
+/* key: "host_threads" (c0 generator pool), "use_graphs" (0/1), "tensor_cores" (0/1,
+ * fp32 contexts, before cimcs_set_problems). */
 int cimcs_set_option(cimcs_ctx* ctx, const char* key, int64_t value);
 
 /* B problems of equal N (make_problem(inst), orchestrator.cpp:80-99).

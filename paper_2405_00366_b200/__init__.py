@@ -6,5 +6,5 @@ this package is the Python mirror of the reference's ``cimcs`` module.
 from .cimcs import (  # noqa: F401
     BACKENDS, ConfigError, Context, CudaError, DivergenceError, HyperParams, InputError,
     Instance, baseline_params, eta_schedule, gemv_order, gen_dims, gen_instance,
-    gen_instances, mix_seed, pump_schedule, replica_seeds, solve, solve_batch,
+    gen_instances, mix_seed, nccl_unique_id, pump_schedule, replica_seeds, solve, solve_batch,
 )

@@ -25,6 +25,7 @@ EXPORTS = (
     "cimcs_gen_instances", "cimcs_create", "cimcs_destroy", "cimcs_set_option",
     "cimcs_set_problems", "cimcs_build_coupling", "cimcs_get_coupling", "cimcs_mfz_step",
     "cimcs_run_cim", "cimcs_refit", "cimcs_score", "cimcs_solve", "cimcs_get_timing",
+    "cimcs_nccl_unique_id", "cimcs_create_sharded",
 )
 
 
@@ -92,6 +93,8 @@ def load() -> C.CDLL:
     L.cimcs_score.argtypes = [vp, i32, vp, vp, d, vp, vp, vp]
     L.cimcs_solve.argtypes = [vp, i32, i32, vp, i32, vp, vp, i32, vp, vp, vp, vp, vp, vp]
     L.cimcs_get_timing.argtypes = [vp, vp]
+    L.cimcs_nccl_unique_id.argtypes = [vp, i32]
+    L.cimcs_create_sharded.argtypes = [i32, i32, i32, i32, vp, vp]
     _lib = L
     return L
 

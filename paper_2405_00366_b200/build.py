@@ -15,6 +15,7 @@ LIB = os.path.join(HERE, "libcimcs_gpu.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("runtime.cu",)]
 DEPS = SOURCES + [
     os.path.join(HERE, "csrc", "kernels.cuh"),
+    os.path.join(HERE, "csrc", "tc_kernels.cuh"),
     os.path.join(HERE, "csrc", "host_rng.hpp"),
     os.path.join(ROOT, "include", "cimcs_gpu.h"),
 ]
@@ -23,6 +24,7 @@ FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
     "-fmad=false", "-Xcompiler", "-fPIC,-O3", "-shared", "-cudart", "static",
 ]
+LIBS = ["-lnccl"]
 
 
 def stale() -> bool:
@@ -34,7 +36,7 @@ def stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
-        cmd = [NVCC, *FLAGS, "-o", LIB, *SOURCES]
+        cmd = [NVCC, *FLAGS, "-o", LIB, *SOURCES, *LIBS]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)

@@ -121,6 +121,13 @@ def eta_schedule(i: int, eta_init: float, eta_end: float, velo: int) -> float:
     return eta_end if linear < eta_end else linear
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL id for cimcs_create_sharded (broadcast it to all ranks)."""
+    buf = (C.c_uint8 * 128)()
+    _check(load().cimcs_nccl_unique_id(buf, 128))
+    return bytes(buf)
+
+
 def mix_seed(base: int, salt: int) -> int:
     return load().cimcs_mix_seed(base, salt)
 
@@ -207,11 +214,18 @@ def _traj(a, B, R, N, dtype=np.float64):
 class Context:
     """One device context: B problems of equal N, device-resident coupling."""
 
-    def __init__(self, device: int = 0, dtype: str = "f32"):
+    def __init__(self, device: int = 0, dtype: str = "f32", shard=None):
+        """shard = (world, rank, nccl_id_bytes) for a row-sharded context."""
         self._lib = load()
         self.dtype = dtype
         self._ctx = C.c_void_p()
-        _check(self._lib.cimcs_create(device, DTYPES[dtype], C.byref(self._ctx)))
+        if shard is None:
+            _check(self._lib.cimcs_create(device, DTYPES[dtype], C.byref(self._ctx)))
+        else:
+            world, rank, nid = shard
+            buf = (C.c_uint8 * 128).from_buffer_copy(bytes(nid))
+            _check(self._lib.cimcs_create_sharded(device, DTYPES[dtype], world, rank, buf,
+                                                  C.byref(self._ctx)))
         self.B = self.N = 0
         self._keep = None
 

@@ -99,6 +99,7 @@ struct GemvArgs {
     double p_scalar;
     int step;            // step index inside the alternation
     int N, ldN, B, ldJ;
+    int rb0;             // first (global) row block of this rank (row sharding)
     StepScalars s;
 };
 
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<T>::kMinBlocks) gemv_fused_kerne
     extern __shared__ __align__(1024) unsigned char smem[];
 
     const int b = blockIdx.y;
-    const int i0 = blockIdx.x * RB;
+    const int i0 = (a.rb0 + blockIdx.x) * RB;  // panels are local, rows global
     const int N = a.N, ldN = a.ldN;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -619,10 +620,13 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ A,
 constexpr int kG2T = 128, kG2K = 8;
 template <typename Out>
 __global__ void __launch_bounds__(256) gram128_kernel(const double* __restrict__ A, int M, int N,
-                                                      size_t a_stride, Out out) {
+                                                      size_t a_stride, Out out, int bi0,
+                                                      int mirror) {
+    // mirror: upper-triangle tiles, each stored twice (single rank);
+    // otherwise: row tiles bi0 + blockIdx.y, all column tiles (row sharding)
     const int b = blockIdx.z;
-    const int bi = blockIdx.y, bj = blockIdx.x;
-    if (bj < bi) return;
+    const int bi = bi0 + blockIdx.y, bj = blockIdx.x;
+    if (mirror && bj < bi) return;
     const double* Ab = A + (size_t)b * a_stride;
     __shared__ __align__(16) double As[kG2K][kG2T];
     __shared__ __align__(16) double Bs[kG2K][kG2T];
@@ -677,7 +681,7 @@ __global__ void __launch_bounds__(256) gram128_kernel(const double* __restrict__
             const int j = j0 + (c < 4 ? tx * 4 + c : 64 + tx * 4 + c - 4);
             if (i < N && j < N) {
                 out.store(b, i, j, acc[r][c]);
-                if (bi != bj) out.store(b, j, i, acc[r][c]);
+                if (mirror && bi != bj) out.store(b, j, i, acc[r][c]);
             }
         }
     }
@@ -687,9 +691,10 @@ __global__ void __launch_bounds__(256) gram128_kernel(const double* __restrict__
 template <typename T, int RB>
 struct PanelOut {
     T* G;
-    int ldJ, nRB;
+    int ldJ, nRB, row0;  // nRB: local row blocks; row0: first local row
     __device__ __forceinline__ void store(int b, int i, int j, double v) const {
-        G[(((size_t)b * nRB + i / RB) * ldJ + j) * RB + (i % RB)] = (T)v;
+        const int il = i - row0;
+        G[(((size_t)b * nRB + il / RB) * ldJ + j) * RB + (il % RB)] = (T)v;
     }
 };
 

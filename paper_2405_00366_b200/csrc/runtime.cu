@@ -8,6 +8,7 @@
 // thread pool from each trajectory's std::mt19937_64 stream while the GPU
 // runs the current one.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -150,21 +151,19 @@ struct DevRecord {
     double eta, hamiltonian, rmse, hamming, min_e, median_e;
 };
 
-// Per trajectory: combine score partials (row blocks in order), count the
-// support and the Hamming mismatches, write the history record, track best.
+// Per trajectory: combine the score partials of this rank's row blocks (in
+// order) and count the support / Hamming mismatches over this rank's rows:
+// tp[traj] = {w.Gw, hz.w, sum (w - x xi)^2, |sigma|, hamming}.  Row-sharded
+// contexts all-reduce tp across ranks before finalize_kernel.
 template <int NR>
-__global__ void finalize_kernel(const double* __restrict__ part, int nRB,
-                                const int8_t* __restrict__ sig, const int8_t* __restrict__ xi,
-                                const unsigned long long* __restrict__ minE,
-                                const int* __restrict__ fail_gstep, const AltParams* alt, int N,
-                                int ldN, int has_truth, DevRecord* hist_alt, int* n_hist,
-                                double* best_obj, int* improved, double* obj_out,
-                                double* rmse_out, double* ham_out) {
+__global__ void tp_kernel(const double* __restrict__ part, int nRB,
+                          const int8_t* __restrict__ sig, const int8_t* __restrict__ xi,
+                          int row0, int row1, int ldN, int has_truth, double* tp) {
     const int traj = blockIdx.x;
     const int b = traj / NR, q = traj % NR;
     __shared__ long long s_sup[256], s_ham[256];
     long long sup = 0, ham = 0;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
         const int s = sig[((size_t)b * ldN + i) * NR + q];
         sup += s;
         if (has_truth) ham += abs(s - (int)xi[(size_t)b * ldN + i]);
@@ -180,8 +179,6 @@ __global__ void finalize_kernel(const double* __restrict__ part, int nRB,
         __syncthreads();
     }
     if (threadIdx.x != 0) return;
-    if (improved) improved[traj] = 0;
-    if (fail_gstep[traj] != kFreeTraj) return;
     double A = 0.0, Bv = 0.0, Cv = 0.0;
     for (int r = 0; r < nRB; ++r) {
         const double* p = part + (((size_t)b * nRB + r) * NR + q) * 4;
@@ -189,18 +186,38 @@ __global__ void finalize_kernel(const double* __restrict__ part, int nRB,
         Bv = Bv + p[1];
         Cv = Cv + p[2];
     }
+    double* o = tp + (size_t)traj * 5;
+    o[0] = A;
+    o[1] = Bv;
+    o[2] = Cv;
+    o[3] = (double)s_sup[0];
+    o[4] = (double)s_ham[0];
+}
+
+// Per trajectory: objective / rmse / hamming, the history record, best tracking.
+__global__ void finalize_kernel(const double* __restrict__ tp, int ntraj,
+                                const unsigned long long* __restrict__ minE,
+                                const int* __restrict__ fail_gstep, const AltParams* alt, int N,
+                                int has_truth, DevRecord* hist_alt, int* n_hist,
+                                double* best_obj, int* improved, double* obj_out,
+                                double* rmse_out, double* ham_out) {
+    const int traj = blockIdx.x * blockDim.x + threadIdx.x;
+    if (traj >= ntraj) return;
+    if (improved) improved[traj] = 0;
+    if (fail_gstep[traj] != kFreeTraj) return;
+    const double* t = tp + (size_t)traj * 5;
     const double lam = alt->lambda;
     // objective_at: 0.5 w.(G w) - hz.w + lambda |sigma|  (orchestrator.cpp:57-62)
-    const double obj = 0.5 * A - Bv + lam * (double)s_sup[0];
-    const double rm = has_truth ? sqrt(Cv / (double)N) : NAN;
-    const double hm = has_truth ? (double)s_ham[0] / (double)N : NAN;
+    const double obj = 0.5 * t[0] - t[1] + lam * t[3];
+    const double rm = has_truth ? sqrt(t[2] / (double)N) : NAN;
+    const double hm = has_truth ? t[4] / (double)N : NAN;
     if (obj_out) obj_out[traj] = obj;
     if (rmse_out) rmse_out[traj] = rm;
     if (ham_out) ham_out[traj] = hm;
     if (hist_alt) {
         DevRecord& rec = hist_alt[traj];
         rec.i = alt->alt;
-        rec.support = (int)s_sup[0];
+        rec.support = (int)t[3];
         rec.eta = alt->eta;
         rec.hamiltonian = obj;
         rec.rmse = rm;
@@ -212,6 +229,14 @@ __global__ void finalize_kernel(const double* __restrict__ part, int nRB,
         best_obj[traj] = obj;
         improved[traj] = 1;
     }
+}
+
+// After the failing step is agreed across ranks (MIN over fail_gstep), only
+// ranks that saw that step keep their offending index candidate.
+__global__ void fail_fix_kernel(const int* __restrict__ local_gstep, const int* __restrict__ gstep,
+                                int* fail_idx, int n) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n && local_gstep[k] != gstep[k]) fail_idx[k] = INT_MAX;
 }
 
 // median(e_final) (orchestrator.cpp:163-168): bitonic sort in shared memory.
@@ -276,6 +301,13 @@ struct cimcs_ctx {
     int host_threads = 0;
     bool use_graphs = true;
     bool want_tc = true;  // fp32 contraction on tcgen05 (3xTF32)
+    // row sharding (one rank per GPU): this rank owns spin rows [row0, row1)
+    int world = 1, rank = 0;
+    bool sharded = false;  // created by cimcs_create_sharded (padded row layout)
+    ncclComm_t comm = nullptr;
+    int row0 = 0, row1 = 0, rb0 = 0;
+    double* tp = nullptr;        // per-trajectory score partials [B*NR][5]
+    int* fail_tmp = nullptr;     // local fail_gstep before the cross-rank MIN
     bool tc = false;      // active for the current problem set
     int nch = 0;
     int num_sms = 148;
@@ -286,7 +318,7 @@ struct cimcs_ctx {
     double *dA = nullptr, *dy = nullptr;
     int* dM = nullptr;
     void* dG = nullptr;      // gram panels [B][nRB][ldJ][RB] in the path's dtype
-    int ldJ = 0, nRB = 0, RB = 0;
+    int ldJ = 0, nRB = 0, RB = 0;  // nRB: row blocks held by this rank
     void *dD = nullptr, *dhz = nullptr;
     double* dx = nullptr;
     int8_t* dxi = nullptr;
@@ -321,7 +353,8 @@ namespace {
 void free_state(cimcs_ctx* c) {
     void* ptrs[] = {c->Rs,  c->C,        c->E,          c->W0,  c->W1,       c->Hdbg,
                     c->bestR, c->sig,    c->bestS,      c->fail_gstep, c->fail_idx, c->n_hist,
-                    c->improved, c->minE, c->part,      c->best_obj, c->obj, c->rmse, c->ham};
+                    c->improved, c->minE, c->part,      c->best_obj, c->obj, c->rmse, c->ham,
+                    c->tp, c->fail_tmp};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     c->Rs = c->C = c->E = c->W0 = c->W1 = c->Hdbg = c->bestR = nullptr;
@@ -329,6 +362,8 @@ void free_state(cimcs_ctx* c) {
     c->fail_gstep = c->fail_idx = c->n_hist = c->improved = nullptr;
     c->minE = nullptr;
     c->part = c->best_obj = c->obj = c->rmse = c->ham = nullptr;
+    c->tp = nullptr;
+    c->fail_tmp = nullptr;
     c->NR = 0;
 }
 
@@ -375,8 +410,7 @@ int ensure_state(cimcs_ctx* c, int NR) {
     c->NR = NR;
     const size_t n = c->state_elems(), es = c->elt();
     const int nT = c->B * NR;
-    const int nRB = (c->N + (c->dtype == CIMCS_F64 ? row_block<double>() : row_block<float>()) - 1) /
-                    (c->dtype == CIMCS_F64 ? row_block<double>() : row_block<float>());
+    const int nRB = std::max(c->nRB, 1);
     int rc = 0;
     const size_t nw = c->w_elems();
     if ((rc = dalloc(&c->Rs, n * es)) || (rc = dalloc(&c->C, n * es)) ||
@@ -388,7 +422,8 @@ int ensure_state(cimcs_ctx* c, int NR) {
         (rc = dalloc(&c->improved, nT * 4)) || (rc = dalloc(&c->minE, nT * 8)) ||
         (rc = dalloc(&c->part, (size_t)c->B * nRB * NR * 4 * 8)) ||
         (rc = dalloc(&c->best_obj, nT * 8)) || (rc = dalloc(&c->obj, nT * 8)) ||
-        (rc = dalloc(&c->rmse, nT * 8)) || (rc = dalloc(&c->ham, nT * 8)))
+        (rc = dalloc(&c->rmse, nT * 8)) || (rc = dalloc(&c->ham, nT * 8)) ||
+        (rc = dalloc(&c->tp, (size_t)nT * 5 * 8)) || (rc = dalloc(&c->fail_tmp, nT * 4)))
         return rc;
     return 0;
 }
@@ -447,7 +482,8 @@ int launch_gemv_t(cimcs_ctx* c, const GemvArgs& a) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    dim3 grid((c->N + row_block<T>() - 1) / row_block<T>(), c->B);
+    if (c->nRB == 0) return 0;  // this rank holds no rows
+    dim3 grid(c->nRB, c->B);
     kern<<<grid, kThreads, smem, c->stream>>>(a);
     CK(cudaGetLastError());
     return 0;
@@ -505,7 +541,9 @@ int launch_tc_t(cimcs_ctx* c, const GemvArgs& g) {
     a.nRB = c->nRB;
     a.nch = c->nch;
     a.ntiles = c->B * c->nRB;
+    a.rb0 = c->rb0;
     a.s = g.s;
+    if (a.ntiles == 0) return 0;
     auto kern = tc_step_kernel<NR, MODE>;
     constexpr size_t smem = tc_smem_bytes(NR);
     static bool attr = false;
@@ -711,11 +749,68 @@ GemvArgs base_args(cimcs_ctx* c, const StepScalars& s) {
     a.ldN = c->ldN;
     a.ldJ = c->ldJ;
     a.B = c->B;
+    a.rb0 = c->rb0;
     a.s = s;
     return a;
 }
 
 int nRB_of(const cimcs_ctx* c) { return c->nRB; }
+
+// ------------------------------------------------ row-sharding collectives
+#define NK(x)                                                                           \
+    do {                                                                                \
+        ncclResult_t r_ = (x);                                                          \
+        if (r_ != ncclSuccess)                                                          \
+            return fail(CIMCS_CUDA_ERROR, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+ncclDataType_t nccl_t(const cimcs_ctx* c) {
+    return c->dtype == CIMCS_F64 ? ncclFloat64 : ncclFloat32;
+}
+
+// All-gather this rank's rows of a per-instance array X[b][rows][row_elems]
+// (rows padded to world * per): in place, one call per instance, grouped.
+int allgather_rows(cimcs_ctx* c, void* X, size_t row_elems, size_t inst_elems,
+                   ncclDataType_t t, size_t esize) {
+    if (c->world == 1) return 0;
+    const size_t per = (size_t)(c->ldN / c->world);
+    NK(ncclGroupStart());
+    for (int b = 0; b < c->B; ++b) {
+        char* base = static_cast<char*>(X) + (size_t)b * inst_elems * esize;
+        NK(ncclAllGather(base + (size_t)c->rank * per * row_elems * esize, base, per * row_elems, t,
+                         c->comm, c->stream));
+    }
+    NK(ncclGroupEnd());
+    return 0;
+}
+
+// contraction input (w or the refit's V): the tc layout is chunk-major in j,
+// so a rank's rows are one contiguous slice per instance as well
+int allgather_w(cimcs_ctx* c, void* W) {
+    if (c->tc) return allgather_rows(c, W, 2 * c->NR, (size_t)c->ldJ * 2 * c->NR, ncclFloat32, 4);
+    return allgather_rows(c, W, c->NR, (size_t)c->ldN * c->NR, nccl_t(c), c->elt());
+}
+int allgather_state(cimcs_ctx* c, void* X) {
+    return allgather_rows(c, X, c->NR, (size_t)c->ldN * c->NR, nccl_t(c), c->elt());
+}
+int allgather_sig(cimcs_ctx* c, int8_t* S) {
+    return allgather_rows(c, S, c->NR, (size_t)c->ldN * c->NR, ncclInt8, 1);
+}
+
+// After a CIM call: agree on divergence (first step, then first spin of that
+// step) and on min_e across ranks.
+int reconcile_cim(cimcs_ctx* c) {
+    if (c->world == 1) return 0;
+    const int nT = c->B * c->NR;
+    CK(cudaMemcpyAsync(c->fail_tmp, c->fail_gstep, nT * 4, cudaMemcpyDeviceToDevice, c->stream));
+    NK(ncclAllReduce(c->fail_gstep, c->fail_gstep, nT, ncclInt32, ncclMin, c->comm, c->stream));
+    fail_fix_kernel<<<(nT + 255) / 256, 256, 0, c->stream>>>(c->fail_tmp, c->fail_gstep,
+                                                             c->fail_idx, nT);
+    CK(cudaGetLastError());
+    NK(ncclAllReduce(c->fail_idx, c->fail_idx, nT, ncclInt32, ncclMin, c->comm, c->stream));
+    NK(ncclAllReduce(c->minE, c->minE, nT, ncclUint64, ncclMin, c->comm, c->stream));
+    return 0;
+}
 
 // Enqueue the n_steps fused Euler steps of one CIM call (graph-capturable).
 int enqueue_steps(cimcs_ctx* c, int bn, const StepScalars& s, int n_steps) {
@@ -727,8 +822,9 @@ int enqueue_steps(cimcs_ctx* c, int bn, const StepScalars& s, int n_steps) {
         a.Win = (k & 1) ? c->W1 : c->W0;
         a.Wout = (k & 1) ? c->W0 : c->W1;
         if (int rc = launch_gemv(c, bn ? EPI_STEP_BN : EPI_STEP_CN, a)) return rc;
+        if (int rc = allgather_w(c, a.Wout)) return rc;  // row sharding: exchange w
     }
-    return 0;
+    return reconcile_cim(c);
 }
 
 // support + masked Jacobi sweeps (graph-capturable).  Final V in W[iters&1].
@@ -736,11 +832,17 @@ int enqueue_refit(cimcs_ctx* c, const StepScalars& s, int iters, bool do_support
     if (do_support) {
         if (int rc = run_support(c)) return rc;
     }
+    if (int rc = allgather_w(c, c->W0)) return rc;
     GemvArgs a = base_args(c, s);
     for (int it = 0; it < iters; ++it) {
         a.Win = (it & 1) ? c->W1 : c->W0;
         a.Wout = (it & 1) ? c->W0 : c->W1;
         if (int rc = launch_gemv(c, EPI_JACOBI, a)) return rc;
+        if (int rc = allgather_w(c, a.Wout)) return rc;
+    }
+    if (c->world > 1) {
+        if (int rc = allgather_state(c, c->Rs)) return rc;
+        NK(ncclAllReduce(c->err, c->err, 1, ncclInt32, ncclMin, c->comm, c->stream));
     }
     return 0;
 }
@@ -768,13 +870,21 @@ int enqueue_score(cimcs_ctx* c, const StepScalars& s, int v_slot, DevRecord* his
     a.Win = v_slot ? c->W1 : c->W0;
     a.Wout = nullptr;
     if (int rc = launch_gemv(c, EPI_SCORE, a)) return rc;
+    const int nT = c->B * c->NR;
     DISPATCH_NR(c->NR, {
-        finalize_kernel<NR_><<<c->B * c->NR, 256, 0, c->stream>>>(
-            c->part, nRB_of(c), c->sig, c->dxi, c->minE, c->fail_gstep, c->alt, c->N, c->ldN,
-            c->has_truth ? 1 : 0, hist_alt, c->n_hist, track_best ? c->best_obj : nullptr,
-            c->improved, c->obj, c->rmse, c->ham);
+        tp_kernel<NR_><<<nT, 256, 0, c->stream>>>(c->part, nRB_of(c), c->sig, c->dxi, c->row0,
+                                                  c->row1, c->ldN, c->has_truth ? 1 : 0, c->tp);
     });
     CK(cudaGetLastError());
+    if (c->world > 1)
+        NK(ncclAllReduce(c->tp, c->tp, (size_t)nT * 5, ncclFloat64, ncclSum, c->comm, c->stream));
+    finalize_kernel<<<(nT + 127) / 128, 128, 0, c->stream>>>(
+        c->tp, nT, c->minE, c->fail_gstep, c->alt, c->N, c->has_truth ? 1 : 0, hist_alt,
+        c->n_hist, track_best ? c->best_obj : nullptr, c->improved, c->obj, c->rmse, c->ham);
+    CK(cudaGetLastError());
+    if (hist_alt && c->world > 1) {
+        if (int rc = allgather_state(c, c->E)) return rc;
+    }
     if (hist_alt) {
         if (int rc = c->dtype == CIMCS_F64 ? enqueue_median_T<double>(c, hist_alt)
                                            : enqueue_median_T<float>(c, hist_alt))
@@ -1006,6 +1116,37 @@ int cimcs_create(int32_t device, int32_t dtype, cimcs_ctx** out) {
     return 0;
 }
 
+int cimcs_nccl_unique_id(uint8_t* out, int32_t nbytes) {
+    if (!out || nbytes < (int32_t)sizeof(ncclUniqueId))
+        return fail(CIMCS_INPUT_ERROR, "need a 128-byte buffer");
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+    return 0;
+}
+
+int cimcs_create_sharded(int32_t device, int32_t dtype, int32_t world, int32_t rank,
+                         const uint8_t* nccl_id, cimcs_ctx** out) {
+    if (world < 1 || rank < 0 || rank >= world || !nccl_id)
+        return fail(CIMCS_CONFIG_ERROR, "bad world/rank/id");
+    if (int rc = cimcs_create(device, dtype, out)) return rc;
+    cimcs_ctx* c = *out;
+    c->world = world;
+    c->rank = rank;
+    c->sharded = true;
+    if (world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        const ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+        if (r != ncclSuccess) {
+            cimcs_destroy(c);
+            *out = nullptr;
+            return fail(CIMCS_CUDA_ERROR, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        }
+    }
+    return 0;
+}
+
 void cimcs_destroy(cimcs_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
@@ -1017,6 +1158,7 @@ void cimcs_destroy(cimcs_ctx* c) {
     if (c->err) cudaFree(c->err);
     if (c->pump) cudaFree(c->pump);
     if (c->hist) cudaFree(c->hist);
+    if (c->comm) ncclCommDestroy(c->comm);
     cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -1049,7 +1191,19 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
     c->ldJ = (N + kChunk - 1) / kChunk * kChunk;
     c->tc = c->dtype == CIMCS_F32 && c->want_tc;
     c->RB = c->dtype == CIMCS_F64 ? row_block<double>() : (c->tc ? kTcRows : row_block<float>());
+    c->row0 = 0;
+    c->row1 = N;
+    c->rb0 = 0;
     c->nRB = (N + c->RB - 1) / c->RB;
+    if (c->sharded) {
+        // row sharding: equal slices of whole 128-row tiles (sharding.row_shard)
+        const int per = (N + c->world * 128 - 1) / (c->world * 128) * 128;
+        c->ldN = c->ldJ = per * c->world;
+        c->row0 = std::min(N, c->rank * per);
+        c->row1 = std::min(N, c->row0 + per);
+        c->rb0 = c->row0 / c->RB;
+        c->nRB = c->row1 > c->row0 ? (c->row1 - c->row0 + c->RB - 1) / c->RB : 0;
+    }
     c->nch = c->ldJ / kTcChunk;
     c->M.assign(M, M + B);
     c->Mmax = *std::max_element(c->M.begin(), c->M.end());
@@ -1101,25 +1255,34 @@ int cimcs_build_coupling(cimcs_ctx* c) {
     cudaEventRecord(ev.ev[0], c->stream);
     CK(cudaMemsetAsync(c->dG, 0, nG * es, c->stream));
     const int nt = (c->N + kG2T - 1) / kG2T;
+    const int bi0 = c->row0 / kG2T;
+    const int nti = c->world == 1 ? nt : (c->row1 - c->row0 + kG2T - 1) / kG2T;
+    const int mirror = c->world == 1 ? 1 : 0;
     const size_t astride = (size_t)c->Mmax * c->N;
     // one launch per run of equal M (instances of a phase grid differ in M)
     for (int b = 0; b < c->B;) {
         int e = b;
         while (e < c->B && c->M[e] == c->M[b]) ++e;
-        const dim3 grid(nt, nt, e - b);
+        const dim3 grid(nt, nti, e - b);
         const double* Ab = c->dA + (size_t)b * astride;
+        if (nti == 0) {
+            b = e;
+            continue;
+        }
         if (c->tc) {
             TcPanelOut o{static_cast<float*>(c->dG) + (size_t)b * c->nRB * c->nch * kTcTileFloats,
-                         c->nRB, c->nch};
-            gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o);
+                         c->nRB, c->nch, c->row0};
+            gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o, bi0, mirror);
         } else if (c->dtype == CIMCS_F64) {
             PanelOut<double, row_block<double>()> o{
-                static_cast<double*>(c->dG) + (size_t)b * c->nRB * c->ldJ * c->RB, c->ldJ, c->nRB};
-            gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o);
+                static_cast<double*>(c->dG) + (size_t)b * c->nRB * c->ldJ * c->RB, c->ldJ, c->nRB,
+                c->row0};
+            gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o, bi0, mirror);
         } else {
             PanelOut<float, row_block<float>()> o{
-                static_cast<float*>(c->dG) + (size_t)b * c->nRB * c->ldJ * c->RB, c->ldJ, c->nRB};
-            gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o);
+                static_cast<float*>(c->dG) + (size_t)b * c->nRB * c->ldJ * c->RB, c->ldJ, c->nRB,
+                c->row0};
+            gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o, bi0, mirror);
         }
         CK(cudaGetLastError());
         b = e;
@@ -1144,6 +1307,7 @@ int cimcs_build_coupling(cimcs_ctx* c) {
 
 int cimcs_get_coupling(cimcs_ctx* c, int32_t b, double* G, double* hz, double* D) {
     if (!c || !c->built || b < 0 || b >= c->B) return fail(CIMCS_INPUT_ERROR, "bad instance");
+    if (c->world > 1) return fail(CIMCS_CONFIG_ERROR, "get_coupling: not on a row-sharded context");
     const int N = c->N, ld = c->ldN, RB = c->RB, ldJ = c->ldJ;
     const size_t gstride = (size_t)c->nRB * ldJ * RB;
     auto fetch = [&](const void* d, size_t off, size_t n, std::vector<double>& h) -> int {
@@ -1212,6 +1376,12 @@ int cimcs_mfz_step(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* 
         a.Wout = c->W1;
         a.Hdbg = c->Hdbg;
         rc = launch_gemv(c, backend == CIMCS_MFZ_BN ? EPI_STEP_BN : EPI_STEP_CN, a);
+        if (!rc) rc = reconcile_cim(c);
+        if (!rc && c->world > 1) {
+            rc = allgather_state(c, c->C);
+            if (!rc) rc = allgather_state(c, c->E);
+            if (!rc) rc = allgather_state(c, c->Hdbg);
+        }
     }
     if (!rc && c_out) rc = download_traj(c, c->C, c_out, R);
     if (!rc && e_out) rc = download_traj(c, c->E, e_out, R);
@@ -1258,6 +1428,11 @@ int cimcs_run_cim(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* h
     if (!rc) rc = enqueue_steps(c, backend == CIMCS_MFZ_BN, s, hp->n_steps);
     cudaEventRecord(ev.ev[1], c->stream);
     if (!rc) rc = run_support(c);
+    if (!rc && c->world > 1) {
+        rc = allgather_state(c, c->C);
+        if (!rc) rc = allgather_state(c, c->E);
+        if (!rc) rc = allgather_sig(c, c->sig);
+    }
     if (!rc && c_out) rc = download_traj(c, c->C, c_out, R);
     if (!rc && e_out) rc = download_traj(c, c->E, e_out, R);
     if (!rc && sigma_out) rc = download_sig(c, c->sig, sigma_out, R);
@@ -1464,6 +1639,10 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
     cudaEventRecord(ev.ev[4 * nalt + 1], c->stream);
 
     // results
+    if (c->world > 1) {  // every rank returns the full vectors
+        if ((rc = allgather_sig(c, c->sig))) return rc;
+        if (track_best && (rc = allgather_sig(c, c->bestS))) return rc;
+    }
     const void* Rsrc = track_best ? c->bestR : c->Rs;
     const int8_t* Ssrc = track_best ? c->bestS : c->sig;
     if (track_best) {

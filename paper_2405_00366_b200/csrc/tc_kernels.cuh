@@ -145,7 +145,8 @@ struct TcArgs {
     int* err;
     double p_scalar;
     int step;
-    int N, ldN, ldJ, B, nRB, nch, ntiles;
+    int N, ldN, ldJ, B, nRB, nch, ntiles;  // nRB: LOCAL row blocks per instance
+    int rb0;                               // first global row block of this rank
     StepScalars s;
 };
 
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(TcArgs a) {
         for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++tt) {
             const int acc = tt & 1;
             const int b = tile / a.nRB, rb = tile % a.nRB;
-            const int i = rb * kTcRows + row;
+            const int i = (a.rb0 + rb) * kTcRows + row;
             mbar_wait(&tm_full[acc], (tt / 2) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             float gw[NR];
@@ -464,9 +465,9 @@ constexpr size_t tc_smem_bytes(int NR) {
 // canonical tcgen05 A-operand output of the gram builder (fp32)
 struct TcPanelOut {
     float* G;
-    int nRB, nch;
+    int nRB, nch, row0;  // nRB: local row blocks; row0: first local row
     __device__ __forceinline__ void store(int b, int i, int j, double v) const {
-        G[tc_gofs(nRB, nch, b, i, j)] = (float)v;
+        G[tc_gofs(nRB, nch, b, i - row0, j)] = (float)v;
     }
 };
 

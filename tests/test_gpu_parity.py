@@ -384,3 +384,26 @@ def test_solve_matches_reference_literal_order(gpu, O):
         assert np.array_equal(res["sigma"][0, 0], ref["sigma"])
         g = O.rmse(res["R"][0, 0], res["sigma"][0, 0], inst.x_true, inst.xi_true)
         assert math.isclose(g, ref["final_rmse"], rel_tol=1e-12)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_row_sharded_context_world1(gpu, O, dtype):
+    """The row-sharded context (padded 128-row slices, NCCL communicator) at
+    world size 1 reproduces the plain context: bitwise in fp64."""
+    insts = [O.gen_instance(300, 0.6, 0.2, 0.01, s) for s in (5, 6)]
+    R = 3
+    hp = gpu.baseline_params(velo=3, n_steps=300)
+    seeds = np.array([[O.mix_seed(i.seed, 1 + 3 * r) for r in range(R)] for i in insts],
+                     np.uint64)
+    plain = _ctx(gpu, insts, dtype)
+    a = plain.solve(R, "mfz-bn", hp, seeds)
+    plain.close()
+    sh = gpu.Context(0, dtype, shard=(1, 0, gpu.nccl_unique_id()))
+    sh.set_problems(insts)
+    sh.build_coupling()
+    b = sh.solve(R, "mfz-bn", hp, seeds)
+    sh.close()
+    if dtype == "f64":
+        assert np.array_equal(a["R"], b["R"]) and np.array_equal(a["sigma"], b["sigma"])
+    else:
+        assert (a["sigma"] == b["sigma"]).mean() > 0.99
