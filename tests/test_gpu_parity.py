@@ -407,3 +407,43 @@ def test_row_sharded_context_world1(gpu, O, dtype):
         assert np.array_equal(a["R"], b["R"]) and np.array_equal(a["sigma"], b["sigma"])
     else:
         assert (a["sigma"] == b["sigma"]).mean() > 0.99
+
+
+def test_phase_grid_mixed_M_bitwise(gpu, O):
+    """Config-2 style batch: instances of different M (alpha) in one context,
+    seeded in instance_grid order; every trajectory bitwise equal to its own
+    fp64 oracle trial."""
+    from paper_2405_00366_b200 import workloads as W
+    grid = [g for g in W.config2_grid(trials=1)][::7][:4]  # 4 cells, alphas differ
+    insts = [O.gen_instance(128, al, a, nu, s) for al, a, nu, s in grid]
+    assert len({i.M for i in insts}) > 1
+    R = 2
+    hp = O.baseline_params(velo=2, n_steps=250)
+    seeds = np.array([[O.mix_seed(i.seed, 1 + 3 * r) for r in range(R)] for i in insts],
+                     np.uint64)
+    ctx = _ctx(gpu, insts)
+    res = ctx.solve(R, "mfz-bn", gpu.baseline_params(velo=2, n_steps=250), seeds)
+    ctx.close()
+    for b, inst in enumerate(insts):
+        for r in range(R):
+            ref = _oracle_solve(O, inst, O.MFZ_BN, hp, int(seeds[b, r]))
+            assert np.array_equal(res["R"][b, r], ref["R"])
+            assert np.array_equal(res["sigma"][b, r], ref["sigma"])
+
+
+def test_tc_cn_mode_and_track_best(gpu, O):
+    """fp32 tensor-core path, continuous-field mode with track_best."""
+    insts = [O.gen_instance(256, 0.5, 0.1, 0.01, s) for s in (11, 12)]
+    R = 4
+    hp = O.baseline_params(velo=5)
+    seeds = np.array([[O.mix_seed(i.seed, 0 + 3 * r) for r in range(R)] for i in insts],
+                     np.uint64)
+    ctx = _ctx_opts(gpu, insts, "f32", tensor_cores=1)
+    res = ctx.solve(R, "mfz-cn", gpu.baseline_params(velo=5), seeds, track_best=True)
+    ctx.close()
+    same = 0
+    for b, inst in enumerate(insts):
+        for r in range(R):
+            ref = _oracle_solve(O, inst, O.MFZ_CN, hp, int(seeds[b, r]), track_best=True)
+            same += np.array_equal(res["sigma"][b, r], ref["sigma"])
+    assert same >= 0.9 * len(insts) * R
