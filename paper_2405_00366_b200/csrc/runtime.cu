@@ -301,6 +301,7 @@ struct cimcs_ctx {
     int host_threads = 0;
     bool use_graphs = true;
     bool want_tc = true;  // fp32 contraction on tcgen05 (3xTF32)
+    bool tc_requested = true;  // want_tc when the resident problems were set
     // row sharding (one rank per GPU): this rank owns spin rows [row0, row1)
     int world = 1, rank = 0;
     bool sharded = false;  // created by cimcs_create_sharded (padded row layout)
@@ -335,6 +336,15 @@ struct cimcs_ctx {
     int32_t* stage_i = nullptr;
     size_t stage_elems = 0;
     AltParams* alt = nullptr;
+    // reusable host/device buffers and the instantiated solve graphs
+    double* pin = nullptr;        // pinned staging for uploads (2 slots)
+    size_t pin_bytes = 0;         // per slot
+    double* pin_c0 = nullptr;     // pinned c0 double buffer
+    size_t pin_c0_elems = 0;
+    double* dc0 = nullptr;        // device c0 of the current alternation
+    size_t dc0_elems = 0;
+    cudaGraphExec_t g_cim = nullptr, g_refit = nullptr;
+    std::vector<long long> graph_key;
     double* pump = nullptr;
     int pump_cap = 0;
     DevRecord* hist = nullptr;
@@ -350,7 +360,15 @@ struct cimcs_ctx {
 
 namespace {
 
+void drop_graphs(cimcs_ctx* c) {
+    if (c->g_cim) cudaGraphExecDestroy(c->g_cim);
+    if (c->g_refit) cudaGraphExecDestroy(c->g_refit);
+    c->g_cim = c->g_refit = nullptr;
+    c->graph_key.clear();
+}
+
 void free_state(cimcs_ctx* c) {
+    drop_graphs(c);
     void* ptrs[] = {c->Rs,  c->C,        c->E,          c->W0,  c->W1,       c->Hdbg,
                     c->bestR, c->sig,    c->bestS,      c->fail_gstep, c->fail_idx, c->n_hist,
                     c->improved, c->minE, c->part,      c->best_obj, c->obj, c->rmse, c->ham,
@@ -973,6 +991,58 @@ void gen_c0(std::vector<HostRng>& rngs, int N, double* out, int threads) {
     for (auto& th : pool) th.join();
 }
 
+// Host -> device upload of B variable-size pieces through two pinned slots:
+// host threads pack a slot while the DMA engine drains the other.
+template <class SizeF, class SrcF, class DstF>
+int staged_upload(cimcs_ctx* c, int B, SizeF size_of, SrcF src_of, DstF dst_of) {
+    const size_t slot = (size_t)64 << 20;
+    if (c->pin_bytes < slot) {
+        if (c->pin) cudaFreeHost(c->pin);
+        c->pin = nullptr;
+        CK(cudaMallocHost(&c->pin, 2 * slot));
+        c->pin_bytes = slot;
+    }
+    cudaEvent_t done[2];
+    CK(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+    std::unique_ptr<cudaEvent_t[], void (*)(cudaEvent_t*)> guard(done, [](cudaEvent_t* e) {
+        cudaEventDestroy(e[0]);
+        cudaEventDestroy(e[1]);
+    });
+    const int threads = std::max(1, std::min(c->host_threads, 16));
+    int k = 0;
+    char* base = reinterpret_cast<char*>(c->pin);
+    for (int b = 0; b < B; ++b) {
+        const size_t n = size_of(b);
+        const char* src = src_of(b);
+        char* dst = dst_of(b);
+        for (size_t off = 0; off < n; off += slot, ++k) {
+            const size_t len = std::min(slot, n - off);
+            char* buf = base + (size_t)(k & 1) * slot;
+            if (k >= 2) CK(cudaEventSynchronize(done[k & 1]));
+            const int nt = len >= ((size_t)8 << 20) ? threads : 1;
+            if (nt == 1) {
+                std::memcpy(buf, src + off, len);
+            } else {
+                std::vector<std::thread> pool;
+                const size_t per = (len + nt - 1) / nt;
+                for (int t = 0; t < nt; ++t) {
+                    const size_t o = (size_t)t * per;
+                    if (o >= len) break;
+                    pool.emplace_back([=] { std::memcpy(buf + o, src + off + o, std::min(per, len - o)); });
+                }
+                for (auto& th : pool) th.join();
+            }
+            CK(cudaMemcpyAsync(dst + off, buf, len, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaEventRecord(done[k & 1], c->stream));
+        }
+    }
+    // the slots are reused by the next upload: drain them before returning
+    if (k >= 1) CK(cudaEventSynchronize(done[(k - 1) & 1]));
+    if (k >= 2) CK(cudaEventSynchronize(done[k & 1]));
+    return 0;
+}
+
 struct Graph {
     cudaGraphExec_t exec = nullptr;
     ~Graph() {
@@ -1158,6 +1228,10 @@ void cimcs_destroy(cimcs_ctx* c) {
     if (c->err) cudaFree(c->err);
     if (c->pump) cudaFree(c->pump);
     if (c->hist) cudaFree(c->hist);
+    if (c->pin) cudaFreeHost(c->pin);
+    if (c->pin_c0) cudaFreeHost(c->pin_c0);
+    if (c->dc0) cudaFree(c->dc0);
+    drop_graphs(c);
     if (c->comm) ncclCommDestroy(c->comm);
     cudaStreamDestroy(c->stream);
     delete c;
@@ -1184,7 +1258,14 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
     for (int b = 0; b < B; ++b)
         if (M[b] < 1 || !A[b] || !y[b]) return fail(CIMCS_INPUT_ERROR, "empty A");
     CK(cudaSetDevice(c->device));
-    free_problems(c);
+    const bool truth = x_true != nullptr && xi_true != nullptr;
+    // same shapes as the resident problem set: keep every device allocation
+    const bool reuse = c->dA && c->B == B && c->N == N && c->has_truth == truth &&
+                       std::equal(c->M.begin(), c->M.end(), M) && (int)c->M.size() == B &&
+                       c->want_tc == c->tc_requested;
+    if (!reuse) free_problems(c);
+    c->built = false;
+    c->tc_requested = c->want_tc;
     c->B = B;
     c->N = N;
     c->ldN = (N + 31) / 32 * 32;
@@ -1207,22 +1288,27 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
     c->nch = c->ldJ / kTcChunk;
     c->M.assign(M, M + B);
     c->Mmax = *std::max_element(c->M.begin(), c->M.end());
-    c->has_truth = x_true != nullptr && xi_true != nullptr;
+    c->has_truth = truth;
     const size_t astride = (size_t)c->Mmax * N;
     int rc;
-    if ((rc = dalloc(&c->dA, (size_t)B * astride * 8)) ||
-        (rc = dalloc(&c->dy, (size_t)B * c->Mmax * 8)) || (rc = dalloc(&c->dM, (size_t)B * 4)))
+    if (!reuse && ((rc = dalloc(&c->dA, (size_t)B * astride * 8)) ||
+                   (rc = dalloc(&c->dy, (size_t)B * c->Mmax * 8)) ||
+                   (rc = dalloc(&c->dM, (size_t)B * 4))))
         return rc;
-    for (int b = 0; b < B; ++b) {
-        CK(cudaMemcpyAsync(c->dA + (size_t)b * astride, A[b], (size_t)M[b] * N * 8,
-                           cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->dy + (size_t)b * c->Mmax, y[b], (size_t)M[b] * 8,
-                           cudaMemcpyHostToDevice, c->stream));
-    }
+    // A and y go through a pinned double buffer filled by host threads
+    // (pageable cudaMemcpy runs at a fraction of the link rate)
+    if (int rc2 = staged_upload(c, B, [&](int b) { return (size_t)M[b] * N * 8; },
+                                [&](int b) { return reinterpret_cast<const char*>(A[b]); },
+                                [&](int b) { return reinterpret_cast<char*>(c->dA + (size_t)b * astride); }))
+        return rc2;
+    if (int rc2 = staged_upload(c, B, [&](int b) { return (size_t)M[b] * 8; },
+                                [&](int b) { return reinterpret_cast<const char*>(y[b]); },
+                                [&](int b) { return reinterpret_cast<char*>(c->dy + (size_t)b * c->Mmax); }))
+        return rc2;
     CK(cudaMemcpyAsync(c->dM, M, (size_t)B * 4, cudaMemcpyHostToDevice, c->stream));
     if (c->has_truth) {
-        if ((rc = dalloc(&c->dx, (size_t)B * c->ldN * 8)) ||
-            (rc = dalloc(&c->dxi, (size_t)B * c->ldN)))
+        if (!reuse && ((rc = dalloc(&c->dx, (size_t)B * c->ldN * 8)) ||
+                       (rc = dalloc(&c->dxi, (size_t)B * c->ldN))))
             return rc;
         std::vector<int8_t> xi8((size_t)B * c->ldN, 0);
         for (int b = 0; b < B; ++b) {
@@ -1552,12 +1638,21 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
     std::vector<HostRng> rngs;
     rngs.reserve(ntraj);
     for (int t = 0; t < ntraj; ++t) rngs.emplace_back(seeds[t]);
-    double* pinned = nullptr;
-    CK(cudaMallocHost(&pinned, 2 * nc0 * 8));
-    std::unique_ptr<double, decltype(&cudaFreeHost)> pin_guard(pinned, &cudaFreeHost);
-    double* dc0 = nullptr;
-    if (int rc = dalloc(&dc0, nc0 * 8)) return rc;
-    std::unique_ptr<double, decltype(&cudaFree)> dc0_guard(dc0, &cudaFree);
+    if (c->pin_c0_elems < nc0) {
+        if (c->pin_c0) cudaFreeHost(c->pin_c0);
+        c->pin_c0 = nullptr;
+        CK(cudaMallocHost(&c->pin_c0, 2 * nc0 * 8));
+        c->pin_c0_elems = nc0;
+    }
+    if (c->dc0_elems < nc0) {
+        if (c->dc0) cudaFree(c->dc0);
+        c->dc0 = nullptr;
+        drop_graphs(c);  // the CIM graph reads dc0
+        if (int rc = dalloc(&c->dc0, nc0 * 8)) return rc;
+        c->dc0_elems = nc0;
+    }
+    double* pinned = c->pin_c0;
+    double* dc0 = c->dc0;
     std::vector<AltParams> alts(nalt);
     for (int i = 0; i < nalt; ++i)
         alts[i] = make_alt(hp, eta_schedule(i, hp->eta_init, hp->eta_end, hp->velo), i);
@@ -1595,14 +1690,32 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
     // graphs: [init + steps], [support + jacobi], [score + finalize + median (+best)]
     // The history slot differs per alternation, so the score graph is per-alternation
     // cheap; the two heavy graphs are captured once and replayed.
-    Graph g_cim, g_refit;
+    // the two heavy graphs are cached across solves with the same shape and
+    // schedule (the scalars they bake in are part of the key)
     if (c->use_graphs) {
-        rc = capture(c, g_cim, [&] {
-            int r2 = run_init(c, R, bn, dc0, nullptr, s.rt);
-            return r2 ? r2 : enqueue_steps(c, bn, s, hp->n_steps);
-        });
-        if (!rc) rc = capture(c, g_refit, [&] { return enqueue_refit(c, s, hp->jacobi_iters, true); });
-        if (rc) return rc;
+        auto bits = [](double v) {
+            long long u;
+            std::memcpy(&u, &v, 8);
+            return u;
+        };
+        const std::vector<long long> key = {R, NR, bn, hp->n_steps, hp->jacobi_iters,
+                                            (long long)(uintptr_t)dc0, bits(s.dt), bits(s.rt),
+                                            bits(s.nbeta), bits(s.Kj), bits(s.minus_j),
+                                            bits(s.dt_c), c->B, c->N};
+        if (key != c->graph_key || !c->g_cim || !c->g_refit) {
+            drop_graphs(c);
+            Graph gc, gr;
+            rc = capture(c, gc, [&] {
+                int r2 = run_init(c, R, bn, dc0, nullptr, s.rt);
+                return r2 ? r2 : enqueue_steps(c, bn, s, hp->n_steps);
+            });
+            if (!rc) rc = capture(c, gr, [&] { return enqueue_refit(c, s, hp->jacobi_iters, true); });
+            if (rc) return rc;
+            c->g_cim = gc.exec;
+            c->g_refit = gr.exec;
+            gc.exec = gr.exec = nullptr;
+            c->graph_key = key;
+        }
     }
     const int v_slot = hp->jacobi_iters & 1;
     gen_c0(rngs, c->N, pinned, c->host_threads);
@@ -1614,7 +1727,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
         CK(cudaEventRecord(slot_done.ev[i & 1], c->stream));
         CK(cudaEventRecord(ev.ev[4 * i + 0], c->stream));
         if (c->use_graphs) {
-            CK(cudaGraphLaunch(g_cim.exec, c->stream));
+            CK(cudaGraphLaunch(c->g_cim, c->stream));
         } else {
             rc = run_init(c, R, bn, dc0, nullptr, s.rt);
             if (!rc) rc = enqueue_steps(c, bn, s, hp->n_steps);
@@ -1622,7 +1735,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
         }
         CK(cudaEventRecord(ev.ev[4 * i + 1], c->stream));
         if (c->use_graphs) {
-            CK(cudaGraphLaunch(g_refit.exec, c->stream));
+            CK(cudaGraphLaunch(c->g_refit, c->stream));
         } else if ((rc = enqueue_refit(c, s, hp->jacobi_iters, true))) {
             return rc;
         }
