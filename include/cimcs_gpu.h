@@ -152,6 +152,16 @@ int cimcs_run_cim(cimcs_ctx* ctx, int32_t R, int32_t backend, const cimcs_hyper*
 int cimcs_refit(cimcs_ctx* ctx, int32_t R, const int32_t* sigma, const double* R_prev,
                 double* R_out, const cimcs_hyper* hp);
 
+/* cdp_minimize(inst, sigma, R_prev, method, params) (cdp.cpp:132-139) for all
+ * B x R trajectories: method CIMCS_CDP_JACOBI (jacobi_solve, cdp.cpp:48-64;
+ * same as cimcs_refit) or CIMCS_CDP_CG (cg_solve, cdp.cpp:66-105: stops at
+ * |r| <= cg_tol*|b| or cg_max_iters, breakdown when p.Gp <= 0).  iterations
+ * (optional, B x R) receives CgInfo::iterations (jacobi_iters for Jacobi).
+ * CG is not available on row-sharded contexts (config_error). */
+int cimcs_cdp_minimize(cimcs_ctx* ctx, int32_t R, const int32_t* sigma, const double* R_prev,
+                       int32_t method, const cimcs_hyper* hp, double* R_out,
+                       int32_t* iterations);
+
 /* K4 scorer: objective_at (orchestrator.cpp:57-62), rmse / hamming_loss
  * (model.cpp:128-153).  Outputs are B x R. */
 int cimcs_score(cimcs_ctx* ctx, int32_t R, const double* Rsig, const int32_t* sigma,
@@ -164,7 +174,7 @@ int cimcs_score(cimcs_ctx* ctx, int32_t R, const double* Rsig, const int32_t* si
  * supplies N normals per alternation for c0.  hist holds (velo+1)*B*R
  * records, trajectory-major; n_hist[b*R+r] = recorded alternations;
  * fail_alt = alternation that diverged or -1 (AlternatingResult::failed,
- * orchestrator.hpp:113-124).  cdp must be CIMCS_CDP_JACOBI. */
+ * orchestrator.hpp:113-124).  cdp: CIMCS_CDP_JACOBI or CIMCS_CDP_CG. */
 int cimcs_solve(cimcs_ctx* ctx, int32_t R, int32_t backend, const cimcs_hyper* hp,
                 int32_t cdp, const uint64_t* seeds, const double* R_init,
                 int32_t track_best, double* R_out, int32_t* sigma_out,

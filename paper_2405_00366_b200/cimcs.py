@@ -310,16 +310,23 @@ class Context:
             _check(rc)
         return dict(c=co, e=eo, sigma=so, min_e=me, fail_index=fi)
 
-    def refit(self, R: int, sigma, R_prev, hp: HyperParams | None = None):
+    def refit(self, R: int, sigma, R_prev, hp: HyperParams | None = None,
+              cdp: str = "jacobi", return_iterations: bool = False):
+        """cdp_minimize (cdp.cpp:132-139) of every trajectory on its support:
+        the damped Jacobi refit or (cdp="cg") conjugate gradient."""
+        if cdp not in ("jacobi", "cg"):
+            raise ConfigError("cdp must be 'jacobi' or 'cg'")
         hp = hp or HyperParams()
         B, N = self.B, self.N
         s = _traj(sigma, B, R, N, np.int32)
         rp = _traj(R_prev, B, R, N)
         out = np.zeros((B, R, N))
+        its = np.zeros((B, R), np.int32)
         h = hp.to_c()
-        _check(self._lib.cimcs_refit(self._ctx, R, s.ctypes.data, rp.ctypes.data,
-                                     out.ctypes.data, C.byref(h)))
-        return out
+        method = _lib.CDP_JACOBI if cdp == "jacobi" else _lib.CDP_CG
+        _check(self._lib.cimcs_cdp_minimize(self._ctx, R, s.ctypes.data, rp.ctypes.data, method,
+                                            C.byref(h), out.ctypes.data, its.ctypes.data))
+        return (out, its) if return_iterations else out
 
     def score(self, R: int, Rsig, sigma, lam: float):
         B, N = self.B, self.N

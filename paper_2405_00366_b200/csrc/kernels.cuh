@@ -58,7 +58,7 @@ __host__ __device__ constexpr size_t gemv_smem_bytes() {
 }
 
 // Mode of the fused epilogue that follows the G*v contraction.
-enum : int { EPI_STEP_BN = 1, EPI_STEP_CN = 0, EPI_JACOBI = 2, EPI_SCORE = 3 };
+enum : int { EPI_STEP_BN = 1, EPI_STEP_CN = 0, EPI_JACOBI = 2, EPI_SCORE = 3, EPI_MATVEC = 4 };
 
 // Per-call scalars (host-computed in fp64 exactly as the reference does).
 struct StepScalars {
@@ -86,6 +86,7 @@ struct GemvArgs {
     void* C;
     void* E;
     void* Hdbg;          // optional local-field dump [B][ldN][NR]
+    double* Mv;          // EPI_MATVEC output G*v [B][ldN][NR] (CG refit)
     const int8_t* sigma; // [B][ldN][NR]  (Jacobi / score)
     int* fail_gstep;     // [B*NR]
     int* fail_idx;       // [B*NR]
@@ -490,6 +491,10 @@ __global__ void __launch_bounds__(kThreads, Cfg<T>::kMinBlocks) gemv_fused_kerne
             }
             Wo[vi] = rn * (on[k] ? T(1) : T(0));
         }
+    } else if constexpr (MODE == EPI_MATVEC) {  // plain G*v for the CG refit
+#pragma unroll
+        for (int k = 0; k < OPT; ++k)
+            if (ok[k]) a.Mv[((size_t)b * ldN + iv[k]) * NR + q] = (double)gwv[k];
     } else {  // EPI_SCORE: w = R∘sigma is Win; partial sums of w.Gw, hz.w, rmse
 #pragma unroll
         for (int k = 0; k < OPT; ++k) {

@@ -25,6 +25,7 @@
 #include "host_rng.hpp"
 #include "kernels.cuh"
 #include "tc_kernels.cuh"
+#include "cg_kernels.cuh"
 
 using namespace cimcs;
 
@@ -349,6 +350,12 @@ struct cimcs_ctx {
     int pump_cap = 0;
     DevRecord* hist = nullptr;
     int hist_cap = 0;
+    // conjugate-gradient refit state (allocated on first use)
+    double *cgX = nullptr, *cgR = nullptr, *cgP = nullptr, *cgGp = nullptr;
+    int* cg_act = nullptr;
+    void* cg_st = nullptr;        // CgTraj[B*NR]
+    int* cg_live = nullptr;       // [0] live counter, [1] last value
+    cudaStream_t side = nullptr;  // captures the CG loop body
     cimcs_timing timing{};
 
     size_t elt() const { return dtype == CIMCS_F64 ? 8 : 4; }
@@ -372,9 +379,13 @@ void free_state(cimcs_ctx* c) {
     void* ptrs[] = {c->Rs,  c->C,        c->E,          c->W0,  c->W1,       c->Hdbg,
                     c->bestR, c->sig,    c->bestS,      c->fail_gstep, c->fail_idx, c->n_hist,
                     c->improved, c->minE, c->part,      c->best_obj, c->obj, c->rmse, c->ham,
-                    c->tp, c->fail_tmp};
+                    c->tp, c->fail_tmp, c->cgX, c->cgR, c->cgP, c->cgGp, c->cg_act,
+                    c->cg_st, c->cg_live};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    c->cgX = c->cgR = c->cgP = c->cgGp = nullptr;
+    c->cg_act = c->cg_live = nullptr;
+    c->cg_st = nullptr;
     c->Rs = c->C = c->E = c->W0 = c->W1 = c->Hdbg = c->bestR = nullptr;
     c->sig = c->bestS = nullptr;
     c->fail_gstep = c->fail_idx = c->n_hist = c->improved = nullptr;
@@ -513,6 +524,7 @@ int launch_gemv_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
         case EPI_STEP_BN: return launch_gemv_t<T, NR, EPI_STEP_BN>(c, a);
         case EPI_STEP_CN: return launch_gemv_t<T, NR, EPI_STEP_CN>(c, a);
         case EPI_JACOBI: return launch_gemv_t<T, NR, EPI_JACOBI>(c, a);
+        case EPI_MATVEC: return launch_gemv_t<T, NR, EPI_MATVEC>(c, a);
         default: return launch_gemv_t<T, NR, EPI_SCORE>(c, a);
     }
 }
@@ -540,6 +552,7 @@ int launch_tc_t(cimcs_ctx* c, const GemvArgs& g) {
     a.C = static_cast<float*>(g.C);
     a.E = static_cast<float*>(g.E);
     a.Hdbg = static_cast<float*>(g.Hdbg);
+    a.Mv = g.Mv;
     a.sigma = g.sigma;
     a.fail_gstep = g.fail_gstep;
     a.fail_idx = g.fail_idx;
@@ -581,6 +594,7 @@ int launch_tc_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
         case EPI_STEP_BN: return launch_tc_t<NR, EPI_STEP_BN>(c, a);
         case EPI_STEP_CN: return launch_tc_t<NR, EPI_STEP_CN>(c, a);
         case EPI_JACOBI: return launch_tc_t<NR, EPI_JACOBI>(c, a);
+        case EPI_MATVEC: return launch_tc_t<NR, EPI_MATVEC>(c, a);
         default: return launch_tc_t<NR, EPI_SCORE>(c, a);
     }
 }
@@ -863,6 +877,137 @@ int enqueue_refit(cimcs_ctx* c, const StepScalars& s, int iters, bool do_support
         NK(ncclAllReduce(c->err, c->err, 1, ncclInt32, ncclMin, c->comm, c->stream));
     }
     return 0;
+}
+
+// ---------------------------------------------------- CG refit (cdp="cg")
+int ensure_cg(cimcs_ctx* c) {  // outside any capture: allocates
+    if (c->cgX) return 0;
+    const size_t n = c->state_elems();
+    for (double** p : {&c->cgX, &c->cgR, &c->cgP, &c->cgGp})
+        if (int rc = dalloc(p, n * 8)) return rc;
+    if (int rc = dalloc(&c->cg_act, n * 4)) return rc;
+    if (int rc = dalloc(&c->cg_st, (size_t)c->B * c->NR * sizeof(CgTraj))) return rc;
+    if (int rc = dalloc(&c->cg_live, 2 * 4)) return rc;
+    if (!c->side) CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    return 0;
+}
+
+CgArgs cg_args(cimcs_ctx* c, const cimcs_hyper* hp) {
+    CgArgs a{};
+    a.Rs = c->Rs;
+    a.sig = c->sig;
+    a.hz = c->dhz;
+    a.X = c->cgX;
+    a.Rr = c->cgR;
+    a.P = c->cgP;
+    a.Gp = c->cgGp;
+    a.act = c->cg_act;
+    a.st = static_cast<CgTraj*>(c->cg_st);
+    a.fail_gstep = c->fail_gstep;
+    a.W = c->W0;
+    a.n_live = c->cg_live;
+    a.tc = c->tc ? 1 : 0;
+    a.ldJ = c->ldJ;
+    a.N = c->N;
+    a.ldN = c->ldN;
+    a.max_iters = hp->cg_max_iters;
+    a.tol = hp->cg_tol;
+    return a;
+}
+
+template <typename T>
+int cg_launch(cimcs_ctx* c, int which, const CgArgs& a) {
+    const int nT = c->B * c->NR;
+    DISPATCH_NR(c->NR, {
+        if (which == 0) cg_init_kernel<T, NR_><<<nT, kCgThreads, 0, c->stream>>>(a);
+        else if (which == 1) cg_iter_kernel<T, NR_><<<nT, kCgThreads, 0, c->stream>>>(a);
+        else cg_final_kernel<T, NR_><<<nT, kCgThreads, 0, c->stream>>>(a);
+    });
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int cg_kernel(cimcs_ctx* c, int which, const CgArgs& a) {
+    return c->dtype == CIMCS_F64 ? cg_launch<double>(c, which, a) : cg_launch<float>(c, which, a);
+}
+
+// G p for every trajectory (the EPI_MATVEC contraction of W0 into cgGp)
+int cg_matvec(cimcs_ctx* c, const StepScalars& s) {
+    GemvArgs g = base_args(c, s);
+    g.Win = c->W0;
+    g.Wout = nullptr;
+    g.Mv = c->cgGp;
+    return launch_gemv(c, EPI_MATVEC, g);
+}
+
+int cg_cond(cimcs_ctx* c, cudaGraphConditionalHandle h, int use) {
+    cg_cond_kernel<<<1, 1, 0, c->stream>>>(c->cg_live, c->cg_live + 1, h, use);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+// The whole masked CG refit of every trajectory on its current support
+// (sig), Rs in/out; afterwards W0 = Rs∘sig for the scorer.  Inside a stream
+// capture the data-dependent loop is a conditional WHILE node (the body is
+// captured on the side stream), so the refit stays one graph launch; outside
+// a capture the host polls the live count after every iteration.
+int enqueue_cg(cimcs_ctx* c, const StepScalars& s, const cimcs_hyper* hp) {
+    if (c->world > 1) return fail(CIMCS_CONFIG_ERROR, "cdp=cg is not supported on row-sharded contexts");
+    if (int rc = ensure_cg(c)) return rc;
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t cgraph = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    CK(cudaStreamGetCaptureInfo(c->stream, &cs, nullptr, &cgraph, &deps, &ndeps));
+    const bool in_graph = cs == cudaStreamCaptureStatusActive;
+    cudaGraphConditionalHandle h{};
+    if (in_graph) CK(cudaGraphConditionalHandleCreate(&h, cgraph, 0, 0));
+    const CgArgs a = cg_args(c, hp);
+    int rc = c->dtype == CIMCS_F64 ? mask_T<double>(c, c->W0) : mask_T<float>(c, c->W0);
+    if (!rc) rc = cg_matvec(c, s);  // G x0
+    if (!rc) rc = cg_kernel(c, 0, a);
+    if (!rc) rc = cg_cond(c, h, in_graph ? 1 : 0);
+    if (rc) return rc;
+    if (in_graph) {
+        CK(cudaStreamGetCaptureInfo(c->stream, &cs, nullptr, &cgraph, &deps, &ndeps));
+        cudaGraphNodeParams np{};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = h;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        cudaGraphNode_t node;
+        CK(cudaGraphAddNode(&node, cgraph, deps, ndeps, &np));
+        cudaGraph_t body = np.conditional.phGraph_out[0];
+        CK(cudaStreamUpdateCaptureDependencies(c->stream, &node, 1,
+                                               cudaStreamSetCaptureDependencies));
+        cudaStream_t main = c->stream;
+        c->stream = c->side;
+        cudaError_t e = cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0,
+                                                      cudaStreamCaptureModeThreadLocal);
+        if (e == cudaSuccess) {
+            rc = cg_matvec(c, s);
+            if (!rc) rc = cg_kernel(c, 1, a);
+            if (!rc) rc = cg_cond(c, h, 1);
+            cudaGraph_t out;
+            e = cudaStreamEndCapture(c->stream, &out);
+        }
+        c->stream = main;
+        if (rc) return rc;
+        CK(e);
+    } else {
+        int live = 0;
+        CK(cudaMemcpyAsync(&live, c->cg_live + 1, 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        while (live > 0) {
+            if ((rc = cg_matvec(c, s)) || (rc = cg_kernel(c, 1, a)) || (rc = cg_cond(c, h, 0)))
+                return rc;
+            CK(cudaMemcpyAsync(&live, c->cg_live + 1, 4, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        }
+    }
+    rc = cg_kernel(c, 2, a);
+    if (!rc) rc = c->dtype == CIMCS_F64 ? mask_T<double>(c, c->W0) : mask_T<float>(c, c->W0);
+    return rc;
 }
 
 template <typename T>
@@ -1233,6 +1378,7 @@ void cimcs_destroy(cimcs_ctx* c) {
     if (c->dc0) cudaFree(c->dc0);
     drop_graphs(c);
     if (c->comm) ncclCommDestroy(c->comm);
+    if (c->side) cudaStreamDestroy(c->side);
     cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -1545,12 +1691,19 @@ int cimcs_run_cim(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* h
     return div ? fail(CIMCS_DIVERGENCE, "mfz_step: non-finite amplitude") : 0;
 }
 
-int cimcs_refit(cimcs_ctx* c, int32_t R, const int32_t* sigma, const double* R_prev,
-                double* R_out, const cimcs_hyper* hp) {
+int cimcs_cdp_minimize(cimcs_ctx* c, int32_t R, const int32_t* sigma, const double* R_prev,
+                       int32_t method, const cimcs_hyper* hp, double* R_out,
+                       int32_t* iterations) {
     if (int rc = check_ready(c, R)) return rc;
     if (!hp) return fail(CIMCS_CONFIG_ERROR, "null hyper-parameters");
+    if (method != CIMCS_CDP_JACOBI && method != CIMCS_CDP_CG)
+        return fail(CIMCS_CONFIG_ERROR, "cdp method must be jacobi or cg");
+    if (method == CIMCS_CDP_CG && c->world > 1)
+        return fail(CIMCS_CONFIG_ERROR, "cdp=cg is not supported on row-sharded contexts");
     CK(cudaSetDevice(c->device));
     if (int rc = ensure_state(c, slots_for(c, R))) return rc;
+    if (method == CIMCS_CDP_CG)
+        if (int rc = ensure_cg(c)) return rc;
     if (int rc = reset_flags(c, R)) return rc;
     if (int rc = upload_traj(c, R_prev, c->Rs, R)) return rc;
     if (int rc = upload_sig(c, sigma, c->sig, R)) return rc;
@@ -1558,18 +1711,34 @@ int cimcs_refit(cimcs_ctx* c, int32_t R, const int32_t* sigma, const double* R_p
     int rc = c->dtype == CIMCS_F64 ? mask_T<double>(c, c->W0) : mask_T<float>(c, c->W0);
     Events ev(2);
     cudaEventRecord(ev.ev[0], c->stream);
-    if (!rc) rc = enqueue_refit(c, s, hp->jacobi_iters, false);
+    if (!rc)
+        rc = method == CIMCS_CDP_JACOBI ? enqueue_refit(c, s, hp->jacobi_iters, false)
+                                        : enqueue_cg(c, s, hp);
     cudaEventRecord(ev.ev[1], c->stream);
     if (!rc) rc = download_traj(c, c->Rs, R_out, R);
     int err = INT_MAX;
+    std::vector<CgTraj> st(method == CIMCS_CDP_CG ? c->B * c->NR : 0);
     cudaMemcpyAsync(&err, c->err, 4, cudaMemcpyDeviceToHost, c->stream);
+    if (!rc && !st.empty())
+        cudaMemcpyAsync(st.data(), c->cg_st, st.size() * sizeof(CgTraj), cudaMemcpyDeviceToHost,
+                        c->stream);
     CK(cudaStreamSynchronize(c->stream));
     if (rc) return rc;
     c->timing.refit_ms = ev.ms(0, 1);
-    if (err != 0x7f7f7f7f && err != INT_MAX)
+    if (iterations)
+        for (int b = 0; b < c->B; ++b)
+            for (int q = 0; q < R; ++q)
+                iterations[b * R + q] =
+                    method == CIMCS_CDP_CG ? st[b * c->NR + q].it : hp->jacobi_iters;
+    if (method == CIMCS_CDP_JACOBI && err != 0x7f7f7f7f && err != INT_MAX)
         return fail(CIMCS_INPUT_ERROR,
                     "jacobi_solve: singular diagonal at active index " + std::to_string(err));
     return 0;
+}
+
+int cimcs_refit(cimcs_ctx* c, int32_t R, const int32_t* sigma, const double* R_prev,
+                double* R_out, const cimcs_hyper* hp) {
+    return cimcs_cdp_minimize(c, R, sigma, R_prev, CIMCS_CDP_JACOBI, hp, R_out, nullptr);
 }
 
 int cimcs_score(cimcs_ctx* c, int32_t R, const double* Rsig, const int32_t* sigma, double lambda,
@@ -1614,12 +1783,16 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
     if (int rc = validate(hp)) return rc;
     if (backend != CIMCS_MFZ_BN && backend != CIMCS_MFZ_CN)
         return fail(CIMCS_CONFIG_ERROR, "backend must be mfz-bn or mfz-cn");
-    if (cdp != CIMCS_CDP_JACOBI)
-        return fail(CIMCS_CONFIG_ERROR, "cdp: only the damped Jacobi refit is on the GPU path");
+    if (cdp != CIMCS_CDP_JACOBI && cdp != CIMCS_CDP_CG)
+        return fail(CIMCS_CONFIG_ERROR, "cdp must be jacobi or cg");
+    if (cdp == CIMCS_CDP_CG && c->world > 1)
+        return fail(CIMCS_CONFIG_ERROR, "cdp=cg is not supported on row-sharded contexts");
     if (!seeds) return fail(CIMCS_INPUT_ERROR, "null seeds");
     CK(cudaSetDevice(c->device));
     const int NR = slots_for(c, R);
     if (int rc = ensure_state(c, NR)) return rc;
+    if (cdp == CIMCS_CDP_CG)
+        if (int rc = ensure_cg(c)) return rc;
     if (int rc = upload_pump(c, hp)) return rc;
     const int nalt = hp->velo + 1;
     const int nT = c->B * NR;
@@ -1701,7 +1874,8 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
         const std::vector<long long> key = {R, NR, bn, hp->n_steps, hp->jacobi_iters,
                                             (long long)(uintptr_t)dc0, bits(s.dt), bits(s.rt),
                                             bits(s.nbeta), bits(s.Kj), bits(s.minus_j),
-                                            bits(s.dt_c), c->B, c->N};
+                                            bits(s.dt_c), c->B, c->N, cdp, hp->cg_max_iters,
+                                            bits(hp->cg_tol)};
         if (key != c->graph_key || !c->g_cim || !c->g_refit) {
             drop_graphs(c);
             Graph gc, gr;
@@ -1709,7 +1883,14 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
                 int r2 = run_init(c, R, bn, dc0, nullptr, s.rt);
                 return r2 ? r2 : enqueue_steps(c, bn, s, hp->n_steps);
             });
-            if (!rc) rc = capture(c, gr, [&] { return enqueue_refit(c, s, hp->jacobi_iters, true); });
+            if (!rc)
+                rc = capture(c, gr, [&] {
+                    if (cdp == CIMCS_CDP_CG) {
+                        int r2 = run_support(c);
+                        return r2 ? r2 : enqueue_cg(c, s, hp);
+                    }
+                    return enqueue_refit(c, s, hp->jacobi_iters, true);
+                });
             if (rc) return rc;
             c->g_cim = gc.exec;
             c->g_refit = gr.exec;
@@ -1717,7 +1898,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
             c->graph_key = key;
         }
     }
-    const int v_slot = hp->jacobi_iters & 1;
+    const int v_slot = cdp == CIMCS_CDP_CG ? 0 : hp->jacobi_iters & 1;
     gen_c0(rngs, c->N, pinned, c->host_threads);
     for (int i = 0; i < nalt; ++i) {
         double* slot = pinned + (size_t)(i & 1) * nc0;
@@ -1736,6 +1917,8 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
         CK(cudaEventRecord(ev.ev[4 * i + 1], c->stream));
         if (c->use_graphs) {
             CK(cudaGraphLaunch(c->g_refit, c->stream));
+        } else if (cdp == CIMCS_CDP_CG) {
+            if ((rc = run_support(c)) || (rc = enqueue_cg(c, s, hp))) return rc;
         } else if ((rc = enqueue_refit(c, s, hp->jacobi_iters, true))) {
             return rc;
         }

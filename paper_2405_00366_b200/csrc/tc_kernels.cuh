@@ -133,6 +133,7 @@ struct TcArgs {
     float* C;
     float* E;
     float* Hdbg;
+    double* Mv;            // EPI_MATVEC output [B][ldN][NR]
     const int8_t* sigma;   // [B][ldN][NR]
     int* fail_gstep;
     int* fail_idx;
@@ -407,6 +408,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(TcArgs a) {
                         a.Wout[tc_wofs(a.ldJ, NR, b, i, q)] = wn;
                         a.Wout[tc_wofs(a.ldJ, NR, b, i, NR + q)] = wn - trunc_tf32(wn);
                     }
+                }
+            } else if constexpr (MODE == EPI_MATVEC) {
+                if (valid) {
+#pragma unroll
+                    for (int q = 0; q < NR; ++q)
+                        if (!fz[q]) a.Mv[vi0 + q] = (double)gw[q];
                 }
             } else {  // EPI_SCORE
                 double pa[NR], pb[NR], pc[NR];
