@@ -26,6 +26,7 @@
 #include "kernels.cuh"
 #include "tc_kernels.cuh"
 #include "cg_kernels.cuh"
+#include "cluster_kernels.cuh"
 
 using namespace cimcs;
 
@@ -301,6 +302,7 @@ struct cimcs_ctx {
     cudaStream_t stream = nullptr;
     int host_threads = 0;
     bool use_graphs = true;
+    bool use_cluster = true;  // small N: whole CIM call / refit in one cluster launch
     bool want_tc = true;  // fp32 contraction on tcgen05 (3xTF32)
     bool tc_requested = true;  // want_tc when the resident problems were set
     // row sharding (one rank per GPU): this rank owns spin rows [row0, row1)
@@ -845,10 +847,79 @@ int reconcile_cim(cimcs_ctx* c) {
 }
 
 // Enqueue the n_steps fused Euler steps of one CIM call (graph-capturable).
+// ------------------------------------------ small-N cluster loop (N <= 512)
+// Replica slots the register-resident G slice leaves room for.
+int cluster_max_nr(const cimcs_ctx* c) { return c->dtype == CIMCS_F64 ? 4 : 8; }
+
+bool cluster_ok(const cimcs_ctx* c) {
+    return c->use_cluster && c->world == 1 && !c->sharded && c->N <= kClMaxN &&
+           c->NR <= cluster_max_nr(c);
+}
+
+template <typename T, int NR, int MODE>
+int launch_cluster_t(cimcs_ctx* c, GemvArgs a, int n_iters) {
+    auto kern = cluster_loop_kernel<T, NR, MODE>;
+    constexpr size_t smem = cluster_smem_bytes<T, NR>();
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr = true;
+    }
+    a.tc_in = c->tc ? 1 : 0;
+    const unsigned cs = (unsigned)((c->N + kClRows - 1) / kClRows);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(c->B * cs);
+    cfg.blockDim = dim3(kClThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kern, a, c->nRB, c->nch, n_iters));
+    return 0;
+}
+
+template <typename T, int NR>
+int launch_cluster_nr(cimcs_ctx* c, int mode, const GemvArgs& a, int n_iters) {
+    switch (mode) {
+        case EPI_STEP_BN: return launch_cluster_t<T, NR, EPI_STEP_BN>(c, a, n_iters);
+        case EPI_STEP_CN: return launch_cluster_t<T, NR, EPI_STEP_CN>(c, a, n_iters);
+        default: return launch_cluster_t<T, NR, EPI_JACOBI>(c, a, n_iters);
+    }
+}
+
+template <typename T>
+int launch_cluster_T(cimcs_ctx* c, int mode, const GemvArgs& a, int n_iters) {
+    switch (c->NR) {
+        case 1: return launch_cluster_nr<T, 1>(c, mode, a, n_iters);
+        case 2: return launch_cluster_nr<T, 2>(c, mode, a, n_iters);
+        case 4: return launch_cluster_nr<T, 4>(c, mode, a, n_iters);
+        default:
+            if constexpr (sizeof(T) == 4) return launch_cluster_nr<T, 8>(c, mode, a, n_iters);
+            return fail(CIMCS_CONFIG_ERROR, "cluster loop: too many replica slots");
+    }
+}
+
+int launch_cluster(cimcs_ctx* c, int mode, const GemvArgs& a, int n_iters) {
+    return c->dtype == CIMCS_F64 ? launch_cluster_T<double>(c, mode, a, n_iters)
+                                 : launch_cluster_T<float>(c, mode, a, n_iters);
+}
+
 int enqueue_steps(cimcs_ctx* c, int bn, const StepScalars& s, int n_steps) {
     GemvArgs a = base_args(c, s);
     a.pump = c->pump;
     a.Hdbg = nullptr;
+    if (cluster_ok(c)) {  // all n_steps in one launch; final w in W[n_steps & 1]
+        a.step = 0;
+        a.Win = c->W0;
+        a.Wout = (n_steps & 1) ? c->W1 : c->W0;
+        return launch_cluster(c, bn ? EPI_STEP_BN : EPI_STEP_CN, a, n_steps);
+    }
     for (int k = 0; k < n_steps; ++k) {
         a.step = k;
         a.Win = (k & 1) ? c->W1 : c->W0;
@@ -866,6 +937,11 @@ int enqueue_refit(cimcs_ctx* c, const StepScalars& s, int iters, bool do_support
     }
     if (int rc = allgather_w(c, c->W0)) return rc;
     GemvArgs a = base_args(c, s);
+    if (cluster_ok(c) && iters > 0) {  // all sweeps in one launch; final V in W[iters & 1]
+        a.Win = c->W0;
+        a.Wout = (iters & 1) ? c->W1 : c->W0;
+        return launch_cluster(c, EPI_JACOBI, a, iters);
+    }
     for (int it = 0; it < iters; ++it) {
         a.Win = (it & 1) ? c->W1 : c->W0;
         a.Wout = (it & 1) ? c->W0 : c->W1;
@@ -1388,6 +1464,10 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
     const std::string k(key);
     if (k == "host_threads") c->host_threads = (int)std::max<int64_t>(1, v);
     else if (k == "use_graphs") c->use_graphs = v != 0;
+    else if (k == "cluster_loop") {
+        c->use_cluster = v != 0;
+        drop_graphs(c);
+    }
     else if (k == "tensor_cores") {
         if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set tensor_cores before set_problems");
         c->want_tc = v != 0;

@@ -347,15 +347,17 @@ def test_tc_refit_and_score_accuracy(gpu, O):
         assert math.isclose(sc["objective"][0, r], obj, rel_tol=1e-5, abs_tol=1e-6)
 
 
-def test_tc_solve_matches_fp64_supports(gpu, O):
+@pytest.mark.parametrize("cluster", [0, 1])
+def test_tc_solve_matches_fp64_supports(gpu, O, cluster):
     """fp32 tensor-core solve vs the fp64 oracle (stated fp32 tolerance:
-    >= 90% identical supports, mean |dRMSE|/RMSE <= 5e-2)."""
+    >= 90% identical supports, mean |dRMSE|/RMSE <= 5e-2).  cluster=0 forces
+    the tcgen05 grid kernel (N=256 is otherwise run by the small-N cluster loop)."""
     insts = [O.gen_instance(256, 0.5, 0.1, 0.01, s) for s in range(1, 5)]
     R = 4
     hp = O.baseline_params(velo=9)
     seeds = np.array([[O.mix_seed(i.seed, 1 + 3 * r) for r in range(R)] for i in insts],
                      np.uint64)
-    ctx = _ctx_opts(gpu, insts, "f32", tensor_cores=1)
+    ctx = _ctx_opts(gpu, insts, "f32", tensor_cores=1, cluster_loop=cluster)
     res = ctx.solve(R, "mfz-bn", gpu.baseline_params(velo=9), seeds)
     ctx.close()
     same, rel = 0, []
@@ -431,14 +433,15 @@ def test_phase_grid_mixed_M_bitwise(gpu, O):
             assert np.array_equal(res["sigma"][b, r], ref["sigma"])
 
 
-def test_tc_cn_mode_and_track_best(gpu, O):
+@pytest.mark.parametrize("cluster", [0, 1])
+def test_tc_cn_mode_and_track_best(gpu, O, cluster):
     """fp32 tensor-core path, continuous-field mode with track_best."""
     insts = [O.gen_instance(256, 0.5, 0.1, 0.01, s) for s in (11, 12)]
     R = 4
     hp = O.baseline_params(velo=5)
     seeds = np.array([[O.mix_seed(i.seed, 0 + 3 * r) for r in range(R)] for i in insts],
                      np.uint64)
-    ctx = _ctx_opts(gpu, insts, "f32", tensor_cores=1)
+    ctx = _ctx_opts(gpu, insts, "f32", tensor_cores=1, cluster_loop=cluster)
     res = ctx.solve(R, "mfz-cn", gpu.baseline_params(velo=5), seeds, track_best=True)
     ctx.close()
     same = 0
