@@ -122,6 +122,26 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def ctx_nr(R, dtype):
+    """Replica slots of a context: a power of two (>= 8 on the tensor-core path)."""
+    p = 1
+    while p < R:
+        p *= 2
+    return max(8, p) if dtype == "f32" else p
+
+
+def kernel_label(N, NR, dtype):
+    """The dominant kernel of the run (runtime.cu dispatch: cluster_ok / launch_gemv)."""
+    if N <= 512 and NR <= (4 if dtype == "f64" else 8):
+        t = "double" if dtype == "f64" else "float"
+        return (f"cluster_loop_kernel<{t},{NR},BN> (whole 1000-step CIM call per launch, G "
+                "register-resident, w over DSMEM; bound by the per-step FMA chain + DSMEM "
+                "round trip, so the HBM fraction is an HBM-equivalent figure)")
+    if dtype == "f32":
+        return f"tc_step_kernel<{NR},BN> (fused Euler step, tcgen05 3xTF32)"
+    return f"gemv_fused_kernel<double,{NR},BN> (fused Euler step, fp64 DFMA)"
+
+
 def make_instances(rank, config=1, ws=1):
     """(instances, replicas, hyper-params, default dtype) of a BASELINE config.
     Config 1 is weak-scaled (each rank its own 64 instances); config 2's fixed
@@ -260,17 +280,23 @@ def run_ours(args, ws, rank, local):
     e2e_val, h2d, d2h = None, 0, 0
     if not args.no_e2e:
         ctx2 = P.Context(local, args.dtype)
-        barrier()
-        e2e_times = []
-        for _ in range(max(1, min(args.steps, 2))):
-            t1 = time.perf_counter()
+
+        def e2e_once():
             ctx2.set_problems(insts)
             ctx2.build_coupling()
-            r2 = ctx2.solve(R, "mfz-bn", hp, seeds)
+            out = ctx2.solve(R, "mfz-bn", hp, seeds)
             torch.cuda.synchronize()
+            return out
+
+        e2e_once()  # untimed: first-use allocations and graph capture of the context
+        barrier()
+        e2e_times = []
+        for _ in range(max(1, min(args.steps, 3))):
+            t1 = time.perf_counter()
+            r2 = e2e_once()
             e2e_times.append(time.perf_counter() - t1)
         ctx2.close()
-        e2e_s = max(e2e_times)
+        e2e_s = statistics.median(e2e_times)
         if dist is not None:
             t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -328,9 +354,7 @@ def run_ours(args, ws, rank, local):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": ncu_traffic() if args.config == 1 and args.dtype == "f32" else None,
-                         "kernel": ("tc_step_kernel<16,BN> (fused Euler step, tcgen05 3xTF32)"
-                                    if args.dtype == "f32" else
-                                    "gemv_fused_kernel<double> (fused Euler step, fp64 DFMA)"),
+                         "kernel": kernel_label(Nn, ctx_nr(R, args.dtype), args.dtype),
                          "bytes_per_launch": step_bytes, "peak_kind": peak_kind},
             "e2e": None if e2e_val is None else {
                 "value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,

@@ -2078,9 +2078,21 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
         tm.refit_ms += ev.ms(4 * i + 1, 4 * i + 2);
         tm.score_ms += ev.ms(4 * i + 2, 4 * i + 3);
     }
-    tm.step_launches = (int64_t)nalt * hp->n_steps;
-    tm.refit_launches = (int64_t)nalt * hp->jacobi_iters;
-    tm.other_launches = (int64_t)nalt * (2 + 3 + (track_best ? 1 : 0));
+    // kernels of this library per alternation: init + steps | support + sweeps |
+    // score contraction, tp, finalize, median (+ best).  The small-N cluster loop
+    // runs a whole CIM call / refit in one launch; CG counts its last iteration total.
+    const bool cl = cluster_ok(c);
+    tm.step_launches = (int64_t)nalt * (cl ? 1 : hp->n_steps);
+    if (cdp == CIMCS_CDP_CG) {
+        std::vector<CgTraj> st(nT);
+        cudaMemcpy(st.data(), c->cg_st, nT * sizeof(CgTraj), cudaMemcpyDeviceToHost);
+        int mx = 0;
+        for (const CgTraj& t : st) mx = std::max(mx, t.it);
+        tm.refit_launches = (int64_t)nalt * (6 + 3 * (int64_t)mx);
+    } else {
+        tm.refit_launches = (int64_t)nalt * (cl ? 1 : hp->jacobi_iters);
+    }
+    tm.other_launches = (int64_t)nalt * (2 + 4 + (track_best ? 1 : 0));
     tm.step_bytes = (double)c->B * c->N * (double)c->N * c->elt();  // dense G share
     tm.step_flops = 2.0 * c->B * (double)c->N * c->N * R;
 
