@@ -27,6 +27,7 @@
 #include "tc_kernels.cuh"
 #include "cg_kernels.cuh"
 #include "cluster_kernels.cuh"
+#include "sym_kernels.cuh"
 
 using namespace cimcs;
 
@@ -313,6 +314,16 @@ struct cimcs_ctx {
     double* tp = nullptr;        // per-trajectory score partials [B*NR][5]
     int* fail_tmp = nullptr;     // local fail_gstep before the cross-rank MIN
     bool tc = false;      // active for the current problem set
+    bool want_sym = true;  // fp32 tensor-core contexts: symmetric-tile gram (sym_kernels.cuh)
+    bool sym = false;      // active for the current problem set
+    bool sym_requested = true;
+    int ntri = 0;          // upper-triangle tiles per instance
+    short2* dTri = nullptr;
+    int* dSg = nullptr;    // per-instance gram scale exponent
+    float* dSpart = nullptr;  // partial products [B][nRB][nRB][128][NR]
+    __half *WB0 = nullptr, *WB1 = nullptr;  // fp16 B tiles of W0 / W1 [B][nRB][2NR x 128]
+    int *WS0 = nullptr, *WS1 = nullptr;     // their scale exponents [B][nRB][NR]
+    size_t spart_elems = 0;
     int nch = 0;
     int num_sms = 148;
     // problems
@@ -382,10 +393,12 @@ void free_state(cimcs_ctx* c) {
                     c->bestR, c->sig,    c->bestS,      c->fail_gstep, c->fail_idx, c->n_hist,
                     c->improved, c->minE, c->part,      c->best_obj, c->obj, c->rmse, c->ham,
                     c->tp, c->fail_tmp, c->cgX, c->cgR, c->cgP, c->cgGp, c->cg_act,
-                    c->cg_st, c->cg_live};
+                    c->cg_st, c->cg_live, c->WB0, c->WB1, c->WS0, c->WS1};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     c->cgX = c->cgR = c->cgP = c->cgGp = nullptr;
+    c->WB0 = c->WB1 = nullptr;
+    c->WS0 = c->WS1 = nullptr;
     c->cg_act = c->cg_live = nullptr;
     c->cg_st = nullptr;
     c->Rs = c->C = c->E = c->W0 = c->W1 = c->Hdbg = c->bestR = nullptr;
@@ -400,9 +413,14 @@ void free_state(cimcs_ctx* c) {
 
 void free_problems(cimcs_ctx* c) {
     free_state(c);
-    void* ptrs[] = {c->dA, c->dy, c->dM, c->dG, c->dD, c->dhz, c->dx, c->dxi};
+    void* ptrs[] = {c->dA, c->dy, c->dM, c->dG, c->dD, c->dhz, c->dx, c->dxi,
+                    c->dTri, c->dSg, c->dSpart};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    c->dTri = nullptr;
+    c->dSg = nullptr;
+    c->dSpart = nullptr;
+    c->spart_elems = 0;
     c->dA = c->dy = nullptr;
     c->dM = nullptr;
     c->dG = nullptr;
@@ -456,6 +474,20 @@ int ensure_state(cimcs_ctx* c, int NR) {
         (rc = dalloc(&c->rmse, nT * 8)) || (rc = dalloc(&c->ham, nT * 8)) ||
         (rc = dalloc(&c->tp, (size_t)nT * 5 * 8)) || (rc = dalloc(&c->fail_tmp, nT * 4)))
         return rc;
+    if (c->sym) {  // fp16 B tiles of W0/W1 and the partial products of the symmetric kernel
+        const size_t nb = (size_t)c->B * c->nRB * 2 * NR * kSyT, ns = (size_t)c->B * c->nRB * NR;
+        if ((rc = dalloc(&c->WB0, nb * 2)) || (rc = dalloc(&c->WB1, nb * 2)) ||
+            (rc = dalloc(&c->WS0, ns * 4)) || (rc = dalloc(&c->WS1, ns * 4)))
+            return rc;
+        const size_t ne = (size_t)c->B * c->nRB * c->nRB * kSyT * NR;
+        if (c->spart_elems < ne) {
+            if (c->dSpart) cudaFree(c->dSpart);
+            c->dSpart = nullptr;
+            c->spart_elems = 0;
+            if ((rc = dalloc(&c->dSpart, ne * 4))) return rc;
+            c->spart_elems = ne;
+        }
+    }
     return 0;
 }
 
@@ -542,8 +574,7 @@ int launch_gemv_T(cimcs_ctx* c, int mode, const GemvArgs& a) {
     }
 }
 
-template <int NR, int MODE>
-int launch_tc_t(cimcs_ctx* c, const GemvArgs& g) {
+TcArgs tc_args(const cimcs_ctx* c, const GemvArgs& g) {
     TcArgs a{};
     a.G = static_cast<const float*>(g.G);
     a.D = static_cast<const float*>(g.D);
@@ -576,6 +607,12 @@ int launch_tc_t(cimcs_ctx* c, const GemvArgs& g) {
     a.ntiles = c->B * c->nRB;
     a.rb0 = c->rb0;
     a.s = g.s;
+    return a;
+}
+
+template <int NR, int MODE>
+int launch_tc_t(cimcs_ctx* c, const GemvArgs& g) {
+    const TcArgs a = tc_args(c, g);
     if (a.ntiles == 0) return 0;
     auto kern = tc_step_kernel<NR, MODE>;
     constexpr size_t smem = tc_smem_bytes(NR);
@@ -590,6 +627,48 @@ int launch_tc_t(cimcs_ctx* c, const GemvArgs& g) {
     return 0;
 }
 
+// symmetric-tile variant (sym_kernels.cuh): half the gram bytes per step
+template <int NR, int MODE>
+int launch_sym_t(cimcs_ctx* c, const GemvArgs& g) {
+    SymArgs sa{};
+    sa.t = tc_args(c, g);
+    sa.Gs = static_cast<const __half*>(c->dG);
+    sa.sg = c->dSg;
+    sa.WBin = g.Win == c->W0 ? c->WB0 : c->WB1;
+    sa.WSin = g.Win == c->W0 ? c->WS0 : c->WS1;
+    sa.WBout = g.Wout == c->W0 ? c->WB0 : c->WB1;
+    sa.WSout = g.Wout == c->W0 ? c->WS0 : c->WS1;
+    sa.spart = c->dSpart;
+    sa.tri = c->dTri;
+    sa.ntri = c->ntri;
+    sa.ntiles = c->B * c->ntri;
+    if (sa.ntiles == 0) return 0;
+    auto kern = sym_step_kernel<NR, MODE>;
+    constexpr size_t smem = sy_smem_bytes<NR>();
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const int grid = std::min(sa.ntiles, c->num_sms);
+    kern<<<grid, kSyThreads, smem, c->stream>>>(sa);
+    CK(cudaGetLastError());
+    sym_finish_kernel<NR, MODE><<<dim3(c->nRB, c->B), 256, 0, c->stream>>>(sa);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+template <int NR>
+int launch_sym_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
+    switch (mode) {
+        case EPI_STEP_BN: return launch_sym_t<NR, EPI_STEP_BN>(c, a);
+        case EPI_STEP_CN: return launch_sym_t<NR, EPI_STEP_CN>(c, a);
+        case EPI_JACOBI: return launch_sym_t<NR, EPI_JACOBI>(c, a);
+        case EPI_MATVEC: return launch_sym_t<NR, EPI_MATVEC>(c, a);
+        default: return launch_sym_t<NR, EPI_SCORE>(c, a);
+    }
+}
+
 template <int NR>
 int launch_tc_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
     switch (mode) {
@@ -602,9 +681,29 @@ int launch_tc_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
 }
 
 int launch_gemv(cimcs_ctx* c, int mode, const GemvArgs& a) {
+    if (c->sym) return c->NR == 8 ? launch_sym_nr<8>(c, mode, a) : launch_sym_nr<16>(c, mode, a);
     if (c->tc) return c->NR == 8 ? launch_tc_nr<8>(c, mode, a) : launch_tc_nr<16>(c, mode, a);
     return c->dtype == CIMCS_F64 ? launch_gemv_T<double>(c, mode, a)
                                  : launch_gemv_T<float>(c, mode, a);
+}
+
+#define DISPATCH_NR_TC(NRV, ...)                                            \
+    if ((NRV) == 8) { constexpr int NR_ = 8; __VA_ARGS__; }                 \
+    else { constexpr int NR_ = 16; __VA_ARGS__; }
+
+// symmetric path: refresh the fp16 B tiles of W (W0 or W1) after a writer
+// other than the symmetric kernel itself
+int sym_sync_w(cimcs_ctx* c, const void* W) {
+    if (!c->sym) return 0;
+    const bool w0 = W == c->W0;
+    const dim3 g(c->nRB, c->B);
+    DISPATCH_NR_TC(c->NR, {
+        sym_wconvert_kernel<NR_><<<g, 128, 0, c->stream>>>(
+            static_cast<const float*>(W), c->N, c->ldJ, c->nRB, w0 ? c->WB0 : c->WB1,
+            w0 ? c->WS0 : c->WS1);
+    });
+    CK(cudaGetLastError());
+    return 0;
 }
 
 // replica slots: a power of two; the tensor-core path needs MMA N in {8, 16}
@@ -640,7 +739,7 @@ int run_init_T(cimcs_ctx* c, int Rreal, int bn, const double* dc0, const double*
                 de0, c->tc ? 1 : 0, c->ldJ);
     });
     CK(cudaGetLastError());
-    return 0;
+    return sym_sync_w(c, c->W0);
 }
 
 int run_init(cimcs_ctx* c, int Rreal, int bn, const double* dc0, const double* de0, double rt) {
@@ -657,7 +756,7 @@ int run_support_T(cimcs_ctx* c) {
             static_cast<T*>(c->W0), c->fail_gstep, c->N, c->ldN, c->B, c->tc ? 1 : 0, c->ldJ);
     });
     CK(cudaGetLastError());
-    return 0;
+    return sym_sync_w(c, c->W0);
 }
 
 int run_support(cimcs_ctx* c) {
@@ -749,7 +848,7 @@ int mask_T(cimcs_ctx* c, void* V) {
                                                       c->ldN, c->ldJ, c->tc ? 1 : 0);
     });
     CK(cudaGetLastError());
-    return 0;
+    return sym_sync_w(c, V);
 }
 
 int reset_flags(cimcs_ctx* c, int Rreal) {
@@ -1042,6 +1141,7 @@ int enqueue_cg(cimcs_ctx* c, const StepScalars& s, const cimcs_hyper* hp) {
     int rc = c->dtype == CIMCS_F64 ? mask_T<double>(c, c->W0) : mask_T<float>(c, c->W0);
     if (!rc) rc = cg_matvec(c, s);  // G x0
     if (!rc) rc = cg_kernel(c, 0, a);
+    if (!rc) rc = sym_sync_w(c, c->W0);
     if (!rc) rc = cg_cond(c, h, in_graph ? 1 : 0);
     if (rc) return rc;
     if (in_graph) {
@@ -1063,6 +1163,7 @@ int enqueue_cg(cimcs_ctx* c, const StepScalars& s, const cimcs_hyper* hp) {
         if (e == cudaSuccess) {
             rc = cg_matvec(c, s);
             if (!rc) rc = cg_kernel(c, 1, a);
+            if (!rc) rc = sym_sync_w(c, c->W0);
             if (!rc) rc = cg_cond(c, h, 1);
             cudaGraph_t out;
             e = cudaStreamEndCapture(c->stream, &out);
@@ -1075,7 +1176,8 @@ int enqueue_cg(cimcs_ctx* c, const StepScalars& s, const cimcs_hyper* hp) {
         CK(cudaMemcpyAsync(&live, c->cg_live + 1, 4, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         while (live > 0) {
-            if ((rc = cg_matvec(c, s)) || (rc = cg_kernel(c, 1, a)) || (rc = cg_cond(c, h, 0)))
+            if ((rc = cg_matvec(c, s)) || (rc = cg_kernel(c, 1, a)) ||
+                (rc = sym_sync_w(c, c->W0)) || (rc = cg_cond(c, h, 0)))
                 return rc;
             CK(cudaMemcpyAsync(&live, c->cg_live + 1, 4, cudaMemcpyDeviceToHost, c->stream));
             CK(cudaStreamSynchronize(c->stream));
@@ -1464,7 +1566,10 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
     const std::string k(key);
     if (k == "host_threads") c->host_threads = (int)std::max<int64_t>(1, v);
     else if (k == "use_graphs") c->use_graphs = v != 0;
-    else if (k == "cluster_loop") {
+    else if (k == "symmetric") {
+        if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set symmetric before set_problems");
+        c->want_sym = v != 0;
+    } else if (k == "cluster_loop") {
         c->use_cluster = v != 0;
         drop_graphs(c);
     }
@@ -1488,10 +1593,11 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
     // same shapes as the resident problem set: keep every device allocation
     const bool reuse = c->dA && c->B == B && c->N == N && c->has_truth == truth &&
                        std::equal(c->M.begin(), c->M.end(), M) && (int)c->M.size() == B &&
-                       c->want_tc == c->tc_requested;
+                       c->want_tc == c->tc_requested && c->want_sym == c->sym_requested;
     if (!reuse) free_problems(c);
     c->built = false;
     c->tc_requested = c->want_tc;
+    c->sym_requested = c->want_sym;
     c->B = B;
     c->N = N;
     c->ldN = (N + 31) / 32 * 32;
@@ -1512,6 +1618,10 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
         c->nRB = c->row1 > c->row0 ? (c->row1 - c->row0 + c->RB - 1) / c->RB : 0;
     }
     c->nch = c->ldJ / kTcChunk;
+    // symmetric-tile gram for the streaming regime (the small-N cluster loop
+    // reads the canonical panels; row-sharded contexts stream their own rows)
+    c->sym = c->tc && c->want_sym && c->world == 1 && !c->sharded && N > kClMaxN;
+    c->ntri = c->sym ? c->nRB * (c->nRB + 1) / 2 : 0;
     c->M.assign(M, M + B);
     c->Mmax = *std::max_element(c->M.begin(), c->M.end());
     c->has_truth = truth;
@@ -1555,22 +1665,48 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
 int cimcs_build_coupling(cimcs_ctx* c) {
     if (!c || c->B < 1) return fail(CIMCS_INPUT_ERROR, "no problems set");
     CK(cudaSetDevice(c->device));
-    const size_t nG = c->tc ? (size_t)c->B * c->nRB * c->nch * kTcTileFloats
-                            : (size_t)c->B * c->nRB * c->ldJ * c->RB;
-    const size_t nv = (size_t)c->B * c->ldN;
     const size_t es = c->elt();
+    // gram bytes: symmetric fp16 hi/lo tiles, canonical tf32 panels, or CUDA-core panels
+    const size_t gbytes = c->sym ? (size_t)c->B * c->ntri * 2 * kSyPlaneBytes
+                          : c->tc ? (size_t)c->B * c->nRB * c->nch * kTcTileFloats * es
+                                  : (size_t)c->B * c->nRB * c->ldJ * c->RB * es;
+    const size_t nv = (size_t)c->B * c->ldN;
     int rc;
-    if (!c->dG && (rc = dalloc(&c->dG, nG * es))) return rc;
+    if (!c->dG && (rc = dalloc(&c->dG, gbytes))) return rc;
     if (!c->dhz && (rc = dalloc(&c->dhz, nv * es))) return rc;
     if (!c->dD && (rc = dalloc(&c->dD, nv * es))) return rc;
+    if (c->sym && !c->dTri) {
+        std::vector<short2> tab(c->ntri);
+        for (int I = 0; I < c->nRB; ++I)
+            for (int J = I; J < c->nRB; ++J) tab[sy_tri(I, J, c->nRB)] = make_short2(I, J);
+        if ((rc = dalloc(&c->dTri, c->ntri * sizeof(short2))) || (rc = dalloc(&c->dSg, c->B * 4)))
+            return rc;
+        CK(cudaMemcpy(c->dTri, tab.data(), tab.size() * sizeof(short2), cudaMemcpyHostToDevice));
+    }
     Events ev(2);
     cudaEventRecord(ev.ev[0], c->stream);
-    CK(cudaMemsetAsync(c->dG, 0, nG * es, c->stream));
+    CK(cudaMemsetAsync(c->dG, 0, gbytes, c->stream));
     const int nt = (c->N + kG2T - 1) / kG2T;
     const int bi0 = c->row0 / kG2T;
     const int nti = c->world == 1 ? nt : (c->row1 - c->row0 + kG2T - 1) / kG2T;
     const int mirror = c->world == 1 ? 1 : 0;
     const size_t astride = (size_t)c->Mmax * c->N;
+    // hz = A^T y, D = diag(G) first: the symmetric tiles are scaled by max D
+    const dim3 g2((c->N + 127) / 128, c->B);
+    if (c->dtype == CIMCS_F64)
+        hz_diag_kernel<double><<<g2, 128, 0, c->stream>>>(
+            c->dA, c->dy, c->dM, c->N, c->ldN, astride, c->Mmax, static_cast<double*>(c->dhz),
+            static_cast<double*>(c->dD), c->B);
+    else
+        hz_diag_kernel<float><<<g2, 128, 0, c->stream>>>(
+            c->dA, c->dy, c->dM, c->N, c->ldN, astride, c->Mmax, static_cast<float*>(c->dhz),
+            static_cast<float*>(c->dD), c->B);
+    CK(cudaGetLastError());
+    if (c->sym) {
+        sym_scale_kernel<<<c->B, 256, 0, c->stream>>>(static_cast<const float*>(c->dD), c->N,
+                                                     c->ldN, c->dSg);
+        CK(cudaGetLastError());
+    }
     // one launch per run of equal M (instances of a phase grid differ in M)
     for (int b = 0; b < c->B;) {
         int e = b;
@@ -1581,7 +1717,11 @@ int cimcs_build_coupling(cimcs_ctx* c) {
             b = e;
             continue;
         }
-        if (c->tc) {
+        if (c->sym) {
+            SymOut o{static_cast<__half*>(c->dG) + (size_t)b * c->ntri * 2 * kSyPlaneHalfs,
+                     c->dSg + b, c->nRB, c->ntri};
+            gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o, bi0, mirror);
+        } else if (c->tc) {
             TcPanelOut o{static_cast<float*>(c->dG) + (size_t)b * c->nRB * c->nch * kTcTileFloats,
                          c->nRB, c->nch, c->row0};
             gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o, bi0, mirror);
@@ -1599,16 +1739,6 @@ int cimcs_build_coupling(cimcs_ctx* c) {
         CK(cudaGetLastError());
         b = e;
     }
-    const dim3 g2((c->N + 127) / 128, c->B);
-    if (c->dtype == CIMCS_F64)
-        hz_diag_kernel<double><<<g2, 128, 0, c->stream>>>(
-            c->dA, c->dy, c->dM, c->N, c->ldN, astride, c->Mmax, static_cast<double*>(c->dhz),
-            static_cast<double*>(c->dD), c->B);
-    else
-        hz_diag_kernel<float><<<g2, 128, 0, c->stream>>>(
-            c->dA, c->dy, c->dM, c->N, c->ldN, astride, c->Mmax, static_cast<float*>(c->dhz),
-            static_cast<float*>(c->dD), c->B);
-    CK(cudaGetLastError());
     cudaEventRecord(ev.ev[1], c->stream);
     CK(cudaStreamSynchronize(c->stream));
     c->timing.gram_ms = ev.ms(0, 1);
@@ -1636,7 +1766,23 @@ int cimcs_get_coupling(cimcs_ctx* c, int32_t b, double* G, double* hz, double* D
         return 0;
     };
     std::vector<double> h;
-    if (G && c->tc) {
+    if (G && c->sym) {
+        const size_t nh = (size_t)c->ntri * 2 * kSyPlaneHalfs;
+        std::vector<__half> t(nh);
+        int sg = 0;
+        CK(cudaMemcpy(t.data(), static_cast<const __half*>(c->dG) + (size_t)b * nh, nh * 2,
+                      cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&sg, c->dSg + b, 4, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < N; ++i)
+            for (int j = 0; j < N; ++j) {
+                int r = i, q = j;  // stored upper triangle: G[i][j] = G[j][i]
+                if (r / kSyT > q / kSyT) std::swap(r, q);
+                const size_t o = (size_t)sy_tri(r / kSyT, q / kSyT, c->nRB) * 2 * kSyPlaneHalfs +
+                                 sy_offk(r % kSyT, q % kSyT, kSyT) / 2;
+                const double v = (double)__half2float(t[o]) + (double)__half2float(t[o + kSyPlaneHalfs]);
+                G[(size_t)i * N + j] = std::ldexp(v, -sg);
+            }
+    } else if (G && c->tc) {
         const size_t ts = (size_t)c->nRB * c->nch * kTcTileFloats;
         if (int rc = fetch(c->dG, (size_t)b * ts, ts, h)) return rc;
         for (int i = 0; i < N; ++i)

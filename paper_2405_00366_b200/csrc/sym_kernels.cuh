@@ -1,0 +1,428 @@
+// sym_kernels.cuh -- fp32 fused MFZ step that reads each gram entry ONCE per
+// step by exploiting G = G^T (tcgen05 kind::f16, fp16 hi/lo split).
+//
+// The streaming kernel (tc_kernels.cuh) is bound by HBM bytes: every step
+// reads the whole N x N gram.  Here only the upper-triangle 128 x 128 tiles
+// (I <= J) are stored, and one tile in shared memory feeds TWO products:
+//     use 1:  out[I] += G[I,J]   * w[J]     A = tile, K-major
+//     use 2:  out[J] += G[I,J]^T * w[I]     A = the same bytes as an MN-major
+//                                           operand (tools/tc_probe_f16.cu)
+// which halves the gram bytes per step.  The transposed view needs a 16-bit
+// MMA kind (tf32 is K-major only), so fp32 accuracy is kept with a split
+//     x ~= hi + lo,  hi = fp16(x * 2^s), lo = fp16(x * 2^s - hi)   (~22 bits)
+// with exact power-of-two scales: s_G per instance (max |G| = max diag in
+// [2^14, 2^15)) and s_w per (128-row block, replica) computed on the fly, so
+// no value leaves fp16's normal range.  G w ~= G_hi [w_hi | w_lo] + G_lo w_hi,
+// accumulated in fp32 in TMEM, and unscaled exactly.
+//
+// A row block K receives nRB partial products (one per tile touching it),
+// written to [B][nRB][slot][128][NR].  A second, evenly spread kernel
+// (sym_finish_kernel, one CTA per block) sums the slots in a FIXED order and
+// runs the fused Euler / Jacobi / score / matvec update (tc_row_update, shared
+// with the streaming kernel): deterministic, and no CTA waits for another.
+// (A fused variant with owner-CTA finisher warps and an L2-resident ring of
+// partials was measured slower: each finish is a chain of dependent L2 round
+// trips, and 7 of them per CTA behind the tile stream left a long tail.)
+//
+// The contraction input w is kept, next to the fp32 [W | W_lo] array the other
+// kernels use, as per-block fp16 B tiles [w_hi | w_lo] (2NR x 128, canonical
+// K-major) with one scale exponent per (block, replica): written once per
+// block by the finisher that produces w (or by sym_wconvert_kernel after any
+// other writer), so a tile only bulk-copies them.
+//
+// Persistent, warp-specialised CTA (one per SM, 6 warps):
+//   warp 0      producer: per tile bulk copies of G_hi, G_lo (32 KB each) and
+//               the two 8 KB B tiles
+//   warp 1      MMA issuer: 8 k-steps x (2 + 2) MMAs, double-buffered TMEM
+//   warps 2-5   tile epilogue: TMEM -> unscaled partial products
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include "tc_kernels.cuh"
+
+namespace cimcs {
+
+constexpr int kSyT = 128;                              // tile edge
+constexpr int kSyStages = 2;
+constexpr int kSyPlaneHalfs = kSyT * kSyT;             // 16384
+constexpr uint32_t kSyPlaneBytes = kSyPlaneHalfs * 2;  // 32 KB
+constexpr int kSyThreads = 6 * 32;
+constexpr int kSyTmemCols = 128;
+
+// byte offset of element (mn, k) of an fp16 operand in the canonical no-swizzle
+// K-major layout (core matrix = 8 MN rows x 8 K = 16 bytes per row)
+__host__ __device__ inline int sy_offk(int mn, int k, int MN) {
+    return (k / 8) * (MN / 8) * 128 + (mn / 8) * 128 + (mn % 8) * 16 + (k % 8) * 2;
+}
+// index of tile (I, J), I <= J, in the row-major upper triangle of nRB x nRB
+__host__ __device__ inline int sy_tri(int I, int J, int nRB) {
+    return I * nRB - I * (I - 1) / 2 + (J - I);
+}
+
+// gram builder output: tile (i/128, j/128) of the upper triangle, planes hi|lo
+struct SymOut {
+    __half* G;
+    const int* sg;  // per-instance scale exponent
+    int nRB, ntri;
+    __device__ __forceinline__ void store(int b, int i, int j, double v) const {
+        const int I = i / kSyT, J = j / kSyT;
+        if (I > J) return;
+        __half* t = G + ((size_t)b * ntri + sy_tri(I, J, nRB)) * 2 * kSyPlaneHalfs;
+        const int o = sy_offk(i % kSyT, j % kSyT, kSyT) / 2;
+        const double gs = ldexp(v, sg[b]);
+        const __half hi = __double2half(gs);
+        t[o] = hi;
+        t[kSyPlaneHalfs + o] = __double2half(gs - (double)__half2float(hi));
+    }
+};
+
+// e such that m * 2^e is in [2^14, 2^15) (0 for m = 0 / non-finite / subnormal),
+// clamped to [-100, 100]
+__host__ __device__ inline int sy_exp14(float m) {
+    if (!(m > 0.f) || !(m < INFINITY)) return 0;
+    int u;
+    memcpy(&u, &m, 4);
+    const int ex = (u >> 23) & 0xff;  // biased exponent
+    const int e = ex == 0 ? 0 : 14 - (ex - 127);
+    return e < -100 ? -100 : (e > 100 ? 100 : e);  // 2^-(s_G + s_w) stays representable
+}
+// exact 2^e as a float, |e| <= 126
+__device__ __forceinline__ float sy_pow2(int e) { return __int_as_float((127 + e) << 23); }
+
+// s_G[b]: max |G| (= max diag) * 2^s_G in [2^14, 2^15)
+__global__ void sym_scale_kernel(const float* __restrict__ D, int N, int ldN, int* sg) {
+    const int b = blockIdx.x;
+    float m = 0.f;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) m = fmaxf(m, fabsf(D[(size_t)b * ldN + i]));
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    __shared__ float s[32];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, s[w]);
+        m = fmaxf(m, s[0]);
+        sg[b] = sy_exp14(m);
+    }
+}
+
+__host__ __device__ constexpr uint32_t sy_idesc(int n, int amn) {
+    return (1u << 4) | ((uint32_t)amn << 15) | ((uint32_t)(n >> 3) << 17) |
+           ((uint32_t)(kSyT >> 4) << 24);  // F32 accumulate, A = B = F16
+}
+__device__ __forceinline__ void sy_mma(uint32_t d, uint64_t da, uint64_t db, uint32_t idesc,
+                                       uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ uint64_t sy_policy_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t sy_policy_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// bulk copy global -> shared with an L2 eviction-priority hint
+__device__ __forceinline__ void sy_bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+        "[%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void sy_st_last(float4* p, float4 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
+                 "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+                 : "memory");
+}
+
+struct SymArgs {
+    TcArgs t;              // state, scalars, fp32 W (other kernels), outputs
+    const __half* Gs;      // [B][ntri][hi | lo][128 x 128]
+    const int* sg;         // [B]
+    const __half* WBin;    // [B][nRB][2NR x 128] fp16 B tiles of the input w
+    const int* WSin;       // [B][nRB][NR] their scale exponents
+    __half* WBout;         // same for the output w (step / Jacobi modes)
+    int* WSout;
+    float* spart;          // [B][nRB][nRB][128][NR]
+    const short2* tri;     // [ntri] -> (I, J)
+    int ntri, ntiles;      // tiles per instance, B * ntri
+};
+
+template <int NR>
+__host__ __device__ constexpr size_t sy_bbytes() { return (size_t)2 * NR * kSyT * 2; }
+template <int NR>
+__host__ __device__ constexpr size_t sy_stage_bytes() {
+    return 2 * (size_t)kSyPlaneBytes + 2 * sy_bbytes<NR>();
+}
+template <int NR>
+__host__ __device__ constexpr size_t sy_smem_bytes() {
+    return kSyStages * sy_stage_bytes<NR>() + 16 * 8 + 64;
+}
+
+// fp16 B tile + scales of one 128-row block from the values w[q] of row k
+// (called by all 128 threads of a group synchronised on named barrier `bar`).
+template <int NR>
+__device__ __forceinline__ void sy_emit_block(const float (&w)[NR], int k, int lane, int wq,
+                                              unsigned (*s_max)[NR], __half* WB, int* WS,
+                                              int bar) {
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+        const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(w[q])));
+        if (lane == 0) s_max[wq][q] = m;
+    }
+    asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+        const unsigned m = max(max(s_max[0][q], s_max[1][q]), max(s_max[2][q], s_max[3][q]));
+        const int e = sy_exp14(__uint_as_float(m));
+        const float ws = w[q] * sy_pow2(e);
+        const __half hi = __float2half_rn(ws);
+        const __half lo = __float2half_rn(ws - __half2float(hi));
+        unsigned char* B = reinterpret_cast<unsigned char*>(WB);
+        *reinterpret_cast<__half*>(B + sy_offk(q, k, 2 * NR)) = hi;
+        *reinterpret_cast<__half*>(B + sy_offk(NR + q, k, 2 * NR)) = lo;
+        if (k == q) WS[q] = e;
+    }
+    asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");  // s_max reusable
+}
+
+// B tiles of a whole fp32 W array ([W | W_lo] canonical) -- after any writer of
+// W other than the symmetric kernel (init, support, mask, CG).
+template <int NR>
+__global__ void __launch_bounds__(128) sym_wconvert_kernel(const float* __restrict__ W, int N,
+                                                           int ldJ, int nRB, __half* WB, int* WS) {
+    __shared__ unsigned s_max[4][NR];
+    const int X = blockIdx.x, b = blockIdx.y, k = threadIdx.x;
+    const int j = X * kSyT + k;
+    float w[NR];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) w[q] = j < N ? W[tc_wofs(ldJ, NR, b, j, q)] : 0.f;
+    sy_emit_block<NR>(w, k, k & 31, k >> 5, s_max,
+                      WB + ((size_t)b * nRB + X) * (2 * NR * kSyT),
+                      WS + ((size_t)b * nRB + X) * NR, 1);
+}
+
+template <int NR, int MODE>
+__global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const TcArgs& a = sa.t;
+    constexpr uint32_t kBB = (uint32_t)sy_bbytes<NR>();
+    constexpr uint32_t kStage = (uint32_t)sy_stage_bytes<NR>();
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSyStages * kStage);
+    uint64_t* full = bars;                    // [2] G planes + B tiles landed
+    uint64_t* empty = full + kSyStages;       // [2] MMAs of the stage retired
+    uint64_t* tm_full = empty + kSyStages;    // [2] accumulators complete
+    uint64_t* tm_empty = tm_full + 2;         // [2] accumulators drained
+    __shared__ uint32_t s_tmem;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nRB = a.nRB;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kSyStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int k = 0; k < 2; ++k) {
+            mbar_init(&tm_full[k], 1);
+            mbar_init(&tm_empty[k], 4);
+        }
+        mbar_fence_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&s_tmem)),
+                     "n"(kSyTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = s_tmem;
+
+    if (warp == 0) {
+        // ------------------------------------------------------ producer
+        if (lane == 0) {
+            const uint64_t pG = sy_policy_first(), pW = sy_policy_last();
+            int tt = 0;
+            for (int tile = blockIdx.x; tile < sa.ntiles; tile += gridDim.x, ++tt) {
+                const int s = tt % kSyStages;
+                const int b = tile / sa.ntri;
+                const short2 ij = sa.tri[tile % sa.ntri];
+                if (tt >= kSyStages) mbar_wait(&empty[s], ((tt / kSyStages) - 1) & 1);
+                const __half* src = sa.Gs + (size_t)tile * 2 * kSyPlaneHalfs;
+                const __half* wb = sa.WBin + (size_t)b * nRB * (2 * NR * kSyT);
+                unsigned char* st = smem + s * kStage;
+                const bool off = ij.x != ij.y;
+                mbar_arrive_expect_tx(&full[s], 2 * kSyPlaneBytes + (off ? 2 : 1) * kBB);
+                // the gram streams through L2 once per step; w tiles are re-read
+                sy_bulk_g2s(st, src, kSyPlaneBytes, &full[s], pG);
+                sy_bulk_g2s(st + kSyPlaneBytes, src + kSyPlaneHalfs, kSyPlaneBytes, &full[s], pG);
+                sy_bulk_g2s(st + 2 * kSyPlaneBytes, wb + (size_t)ij.y * (2 * NR * kSyT), kBB,
+                            &full[s], pW);
+                if (off)
+                    sy_bulk_g2s(st + 2 * kSyPlaneBytes + kBB, wb + (size_t)ij.x * (2 * NR * kSyT),
+                                kBB, &full[s], pW);
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t id_cat = sy_idesc(2 * NR, 0), id_hi = sy_idesc(NR, 0);
+            constexpr uint32_t id_catT = sy_idesc(2 * NR, 1), id_hiT = sy_idesc(NR, 1);
+            constexpr uint32_t kstr = (kSyT / 8) * 128;   // K-group stride of the tile (2 KB)
+            constexpr uint32_t lboB = (2 * NR / 8) * 128;  // K-group stride of a B tile
+            int tt = 0;
+            for (int tile = blockIdx.x; tile < sa.ntiles; tile += gridDim.x, ++tt) {
+                const int s = tt % kSyStages, acc = tt & 1;
+                const short2 ij = sa.tri[tile % sa.ntri];
+                const bool off = ij.x != ij.y;
+                if (tt >= 2) mbar_wait(&tm_empty[acc], ((tt / 2) - 1) & 1);
+                mbar_wait(&full[s], (tt / kSyStages) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t aHi = smem_u32(smem + s * kStage), aLo = aHi + kSyPlaneBytes;
+                const uint32_t bJ = aHi + 2 * kSyPlaneBytes, bI = bJ + kBB;
+                const uint32_t d1 = tmem + acc * 4 * NR, d2 = d1 + 2 * NR;
+#pragma unroll
+                for (int kb = 0; kb < kSyT / 16; ++kb) {
+                    const uint32_t first = kb ? 1u : 0u;
+                    const uint64_t dBJ = umma_desc(bJ + kb * 2 * lboB, lboB, 128);
+                    sy_mma(d1, umma_desc(aHi + kb * 2 * kstr, kstr, 128), dBJ, id_cat, first);
+                    sy_mma(d1, umma_desc(aLo + kb * 2 * kstr, kstr, 128), dBJ, id_hi, 1u);
+                    if (off) {  // transposed view: K' = tile rows, 16 per k-step = 256 B
+                        const uint64_t dBI = umma_desc(bI + kb * 2 * lboB, lboB, 128);
+                        sy_mma(d2, umma_desc(aHi + kb * 256, 128, kstr), dBI, id_catT, first);
+                        sy_mma(d2, umma_desc(aLo + kb * 256, 128, kstr), dBI, id_hiT, 1u);
+                    }
+                }
+                tc_commit(&empty[s]);
+                tc_commit(&tm_full[acc]);
+            }
+        }
+    } else {
+        // ------------------------------------------------ tile epilogue
+        const int ew = warp & 3;         // TMEM lane quadrant of this warp
+        const int row = ew * 32 + lane;  // row of the tile (use 1) / column (use 2)
+        const uint64_t pP = sy_policy_last();
+        int tt = 0;
+        for (int tile = blockIdx.x; tile < sa.ntiles; tile += gridDim.x, ++tt) {
+            const int acc = tt & 1;
+            const int b = tile / sa.ntri;
+            const short2 ij = sa.tri[tile % sa.ntri];
+            const int I = ij.x, J = ij.y;
+            mbar_wait(&tm_full[acc], (tt / 2) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            float g1[NR], g2[NR];
+            const uint32_t tq = tmem + acc * 4 * NR + ((uint32_t)(ew * 32) << 16);
+            tmem_ld_row<NR>(tq, g1);
+            if (I != J) tmem_ld_row<NR>(tq + 2 * NR, g2);
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tm_empty[acc]);
+
+            // partial products, unscaled exactly: 2^-(s_G + s_w)
+            float* part = sa.spart + (size_t)b * nRB * nRB * kSyT * NR;
+            const float fG = sy_pow2(-sa.sg[b]);
+            const int* wsJ = sa.WSin + ((size_t)b * nRB + J) * NR;
+            float4* pI = reinterpret_cast<float4*>(part + (((size_t)I * nRB + J) * kSyT + row) * NR);
+#pragma unroll
+            for (int q = 0; q < NR; q += 4)
+                sy_st_last(pI + q / 4,
+                           make_float4(g1[q] * fG * sy_pow2(-__ldg(wsJ + q)),
+                                       g1[q + 1] * fG * sy_pow2(-__ldg(wsJ + q + 1)),
+                                       g1[q + 2] * fG * sy_pow2(-__ldg(wsJ + q + 2)),
+                                       g1[q + 3] * fG * sy_pow2(-__ldg(wsJ + q + 3))),
+                           pP);
+            if (I != J) {
+                const int* wsI = sa.WSin + ((size_t)b * nRB + I) * NR;
+                float4* pJ =
+                    reinterpret_cast<float4*>(part + (((size_t)J * nRB + I) * kSyT + row) * NR);
+#pragma unroll
+                for (int q = 0; q < NR; q += 4)
+                    sy_st_last(pJ + q / 4,
+                               make_float4(g2[q] * fG * sy_pow2(-__ldg(wsI + q)),
+                                           g2[q + 1] * fG * sy_pow2(-__ldg(wsI + q + 1)),
+                                           g2[q + 2] * fG * sy_pow2(-__ldg(wsI + q + 2)),
+                                           g2[q + 3] * fG * sy_pow2(-__ldg(wsI + q + 3))),
+                               pP);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "n"(kSyTmemCols));
+}
+
+// Second pass of a step: block (b, K) sums its nRB partial products in slot
+// order (deterministic) and runs the fused update; step / Jacobi modes also
+// emit the fp16 B tile of the new w for the next launch.  256 threads: every
+// (row, half of the replicas) pair loads its 16 slots at once, then the first
+// 128 threads (one per row) run the update.
+template <int NR, int MODE>
+__global__ void __launch_bounds__(256) sym_finish_kernel(SymArgs sa) {
+    __shared__ double s_part[4][NR][3];
+    __shared__ unsigned s_max[4][NR];
+    __shared__ float s_gw[kSyT][NR + 1];
+    const TcArgs& a = sa.t;
+    constexpr bool kWritesW = MODE == EPI_STEP_BN || MODE == EPI_STEP_CN || MODE == EPI_JACOBI;
+    constexpr int H = NR / 2;  // replicas per half
+    const int K = blockIdx.x, b = blockIdx.y, nRB = a.nRB;
+    {
+        const int row = threadIdx.x & (kSyT - 1), half = threadIdx.x >> 7;
+        const float4* src = reinterpret_cast<const float4*>(
+            sa.spart + (((size_t)b * nRB + K) * nRB * kSyT + row) * NR + half * H);
+        constexpr size_t kSlot4 = (size_t)kSyT * NR / 4;
+        float g[H];
+#pragma unroll
+        for (int q = 0; q < H; ++q) g[q] = 0.f;
+        for (int s0 = 0; s0 < nRB; s0 += 8) {  // up to 8 slots x H/4 float4 in flight
+            float4 v[8][H / 4];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int q = 0; q < H / 4; ++q)
+                    if (s0 + u < nRB) v[u][q] = __ldcs(src + (s0 + u) * kSlot4 + q);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int q = 0; q < H / 4; ++q)
+                    if (s0 + u < nRB) {
+                        // slot 0 starts the sum (0 + x == x exactly)
+                        g[4 * q] = g[4 * q] + v[u][q].x;
+                        g[4 * q + 1] = g[4 * q + 1] + v[u][q].y;
+                        g[4 * q + 2] = g[4 * q + 2] + v[u][q].z;
+                        g[4 * q + 3] = g[4 * q + 3] + v[u][q].w;
+                    }
+        }
+#pragma unroll
+        for (int q = 0; q < H; ++q) s_gw[row][half * H + q] = g[q];
+    }
+    __syncthreads();
+    if (threadIdx.x >= kSyT) return;
+    const int row = threadIdx.x, lane = row & 31, ep = row >> 5;
+    float gw[NR];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) gw[q] = s_gw[row][q];
+    tc_row_update<NR, MODE>(a, b, K, row, lane, ep, gw, s_part);
+    if constexpr (kWritesW) {
+        const int i = K * kSyT + row;
+        float w[NR];
+#pragma unroll
+        for (int q = 0; q < NR; ++q) w[q] = i < a.N ? a.Wout[tc_wofs(a.ldJ, NR, b, i, q)] : 0.f;
+        sy_emit_block<NR>(w, row, lane, ep, s_max,
+                          sa.WBout + ((size_t)b * nRB + K) * (2 * NR * kSyT),
+                          sa.WSout + ((size_t)b * nRB + K) * NR, 2);
+    }
+}
+
+}  // namespace cimcs

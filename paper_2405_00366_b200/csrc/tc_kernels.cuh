@@ -151,6 +151,176 @@ struct TcArgs {
     StepScalars s;
 };
 
+// Per-row fused update after the contraction: thread `row` of the four
+// epilogue warps owns spin i = (rb0 + rb) * 128 + row of instance b and all NR
+// replicas; gw[q] = (G w)_iq.  Shared by the streaming kernel below and the
+// symmetric-tile kernel (sym_kernels.cuh).
+template <int NR, int MODE>
+__device__ __forceinline__ void tc_row_update(const TcArgs& a, int b, int rb, int row, int lane,
+                                              int ep, const float (&gw)[NR],
+                                              double (*s_part)[NR][3], int bar = 2) {
+    const StepScalars& sc = a.s;
+    const int N = a.N;
+    const int i = (a.rb0 + rb) * kTcRows + row;
+    bool fz[NR];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+        const int fg = a.fail_gstep[b * NR + q];
+        if (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN)
+            fz[q] = fg < a.alt->gstep_base + a.step;
+        else
+            fz[q] = fg != kFreeTraj;
+    }
+    const bool valid = i < N;
+    const size_t si = (size_t)b * a.ldN + i;
+    const size_t vi0 = si * NR;
+    if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
+        float lmin[NR];
+#pragma unroll
+        for (int q = 0; q < NR; ++q) lmin[q] = INFINITY;
+        if (valid) {
+            float wv[NR], Rv[NR], cv[NR], ev[NR];
+#pragma unroll
+            for (int q = 0; q < NR; ++q) wv[q] = __ldg(a.Win + tc_wofs(a.ldJ, NR, b, i, q));
+#pragma unroll
+            for (int q = 0; q < NR; q += 4) {
+                const float4 r4 = __ldg(reinterpret_cast<const float4*>(a.Rs + vi0 + q));
+                const float4 c4 = *reinterpret_cast<const float4*>(a.C + vi0 + q);
+                const float4 e4 = *reinterpret_cast<const float4*>(a.E + vi0 + q);
+                Rv[q] = r4.x; Rv[q + 1] = r4.y; Rv[q + 2] = r4.z; Rv[q + 3] = r4.w;
+                cv[q] = c4.x; cv[q + 1] = c4.y; cv[q + 2] = c4.z; cv[q + 3] = c4.w;
+                ev[q] = e4.x; ev[q + 1] = e4.y; ev[q + 2] = e4.z; ev[q + 3] = e4.w;
+            }
+            const float Dv = __ldg(a.D + si), hzv = __ldg(a.hz + si);
+            const float half_rt = (float)sc.half_rt, rt = (float)sc.rt, dt = (float)sc.dt;
+            const float Kj = (float)sc.Kj, nbeta = (float)sc.nbeta, tau = (float)sc.tau;
+            const double pd = a.pump ? a.pump[a.step] : a.p_scalar;
+            const float loss = sc.minus_j != 0.0 ? (float)((-1.0 + pd) - sc.minus_j)
+                                                 : (float)(-1.0 + pd);
+            const float thresh = (float)a.alt->thresh;
+            float cn[NR], en[NR];
+#pragma unroll
+            for (int q = 0; q < NR; ++q) {
+                const float c = cv[q], e = ev[q];
+                const float Jw = Dv * wv[q] - gw[q];
+                float h;
+                if constexpr (MODE == EPI_STEP_BN)
+                    h = half_rt * (Jw + hzv);
+                else
+                    h = Jw + half_rt * hzv;
+                if (a.Hdbg) a.Hdbg[vi0 + q] = h;
+                const float inj = (Kj * e) * (Rv[q] * h - thresh);
+                cn[q] = c + dt * ((loss - c * c) * c + inj);
+                en[q] = e + dt * ((nbeta * (c * c - tau)) * e);
+                if (fz[q]) {
+                    cn[q] = c;
+                    en[q] = e;
+                } else if (!isfinite(cn[q]) || !isfinite(en[q])) {
+                    atomicMin(&a.fail_gstep[b * NR + q], a.alt->gstep_base + a.step);
+                    atomicMin(&a.fail_idx[b * NR + q], i);
+                    cn[q] = c;
+                    en[q] = e;
+                } else {
+                    lmin[q] = en[q];
+                    float wn;
+                    if constexpr (MODE == EPI_STEP_BN)
+                        wn = Rv[q] * (cn[q] > 0.f ? 1.f : 0.f);
+                    else
+                        wn = (Rv[q] * 0.25f) * (cn[q] + rt);
+                    a.Wout[tc_wofs(a.ldJ, NR, b, i, q)] = wn;
+                    a.Wout[tc_wofs(a.ldJ, NR, b, i, NR + q)] = wn - trunc_tf32(wn);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < NR; q += 4) {
+                *reinterpret_cast<float4*>(a.C + vi0 + q) =
+                    make_float4(cn[q], cn[q + 1], cn[q + 2], cn[q + 3]);
+                *reinterpret_cast<float4*>(a.E + vi0 + q) =
+                    make_float4(en[q], en[q + 1], en[q + 2], en[q + 3]);
+            }
+        }
+        // per-replica min of e: warp reduce, one atomic per (warp, replica)
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+            float m = lmin[q];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1)
+                m = fminf(m, __shfl_xor_sync(0xffffffffu, m, off));
+            if (lane == q && m != INFINITY) atomicMin(&a.minE[b * NR + q], ord_key(m));
+        }
+    } else if constexpr (MODE == EPI_JACOBI) {
+        if (valid) {
+            const float Dv = __ldg(a.D + si), bv = __ldg(a.hz + si);
+            const float omd = (float)sc.one_minus_dtc, dtc = (float)sc.dt_c;
+#pragma unroll
+            for (int q = 0; q < NR; ++q) {
+                if (fz[q]) continue;
+                const float Rv = a.Rs[vi0 + q];
+                const bool on = a.sigma[vi0 + q] != 0;
+                float rn = Rv;
+                if (on) {
+                    if (Dv == 0.f) {
+                        atomicMin(a.err, i);
+                        continue;
+                    }
+                    const float off = gw[q] - Dv * Rv;
+                    rn = omd * Rv + dtc * ((bv - off) / Dv);
+                    a.Rs[vi0 + q] = rn;
+                }
+                const float wn = rn * (on ? 1.f : 0.f);
+                a.Wout[tc_wofs(a.ldJ, NR, b, i, q)] = wn;
+                a.Wout[tc_wofs(a.ldJ, NR, b, i, NR + q)] = wn - trunc_tf32(wn);
+            }
+        }
+    } else if constexpr (MODE == EPI_MATVEC) {
+        if (valid) {
+#pragma unroll
+            for (int q = 0; q < NR; ++q)
+                if (!fz[q]) a.Mv[vi0 + q] = (double)gw[q];
+        }
+    } else {  // EPI_SCORE
+        double pa[NR], pb[NR], pc[NR];
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+            pa[q] = pb[q] = pc[q] = 0.0;
+            if (valid && !fz[q]) {
+                const double wv = a.Win[tc_wofs(a.ldJ, NR, b, i, q)];
+                pa[q] = wv * (double)gw[q];
+                pb[q] = (double)a.hz[si] * wv;
+                if (a.xtrue) {
+                    const double xt = a.xitrue[si] ? a.xtrue[si] : 0.0;
+                    pc[q] = (wv - xt) * (wv - xt);
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                pa[q] += __shfl_xor_sync(0xffffffffu, pa[q], off);
+                pb[q] += __shfl_xor_sync(0xffffffffu, pb[q], off);
+                pc[q] += __shfl_xor_sync(0xffffffffu, pc[q], off);
+            }
+        }
+        if (lane < NR) {
+            s_part[ep][lane][0] = pa[lane];
+            s_part[ep][lane][1] = pb[lane];
+            s_part[ep][lane][2] = pc[lane];
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
+        if (ep == 0 && lane < NR) {
+            double A_ = 0, B_ = 0, C_ = 0;
+            for (int w = 0; w < 4; ++w) {
+                A_ += s_part[w][lane][0];
+                B_ += s_part[w][lane][1];
+                C_ += s_part[w][lane][2];
+            }
+            double* p = a.part + (((size_t)b * a.nRB + rb) * NR + lane) * 4;
+            p[0] = A_;
+            p[1] = B_;
+            p[2] = C_;
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
+    }
+}
+
 template <int NR, int MODE>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(TcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -285,12 +455,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(TcArgs a) {
         const int ew = warp & 3;                // TMEM lane quadrant of this warp
         const int row = ew * 32 + lane;         // spin row inside the tile
         const int ep = warp - 6;                // 0..3, stable order for reductions
-        const StepScalars& sc = a.s;
         int tt = 0;
         for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++tt) {
             const int acc = tt & 1;
             const int b = tile / a.nRB, rb = tile % a.nRB;
-            const int i = (a.rb0 + rb) * kTcRows + row;
             mbar_wait(&tm_full[acc], (tt / 2) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             float gw[NR];
@@ -299,163 +467,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(TcArgs a) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&tm_empty[acc]);
 
-            bool fz[NR];
-#pragma unroll
-            for (int q = 0; q < NR; ++q) {
-                const int fg = a.fail_gstep[b * NR + q];
-                if (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN)
-                    fz[q] = fg < a.alt->gstep_base + a.step;
-                else
-                    fz[q] = fg != kFreeTraj;
-            }
-            const bool valid = i < N;
-            const size_t si = (size_t)b * a.ldN + i;
-            const size_t vi0 = si * NR;
-            if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
-                float lmin[NR];
-#pragma unroll
-                for (int q = 0; q < NR; ++q) lmin[q] = INFINITY;
-                if (valid) {
-                    float wv[NR], Rv[NR], cv[NR], ev[NR];
-#pragma unroll
-                    for (int q = 0; q < NR; ++q) wv[q] = __ldg(a.Win + tc_wofs(a.ldJ, NR, b, i, q));
-#pragma unroll
-                    for (int q = 0; q < NR; q += 4) {
-                        const float4 r4 = __ldg(reinterpret_cast<const float4*>(a.Rs + vi0 + q));
-                        const float4 c4 = *reinterpret_cast<const float4*>(a.C + vi0 + q);
-                        const float4 e4 = *reinterpret_cast<const float4*>(a.E + vi0 + q);
-                        Rv[q] = r4.x; Rv[q + 1] = r4.y; Rv[q + 2] = r4.z; Rv[q + 3] = r4.w;
-                        cv[q] = c4.x; cv[q + 1] = c4.y; cv[q + 2] = c4.z; cv[q + 3] = c4.w;
-                        ev[q] = e4.x; ev[q + 1] = e4.y; ev[q + 2] = e4.z; ev[q + 3] = e4.w;
-                    }
-                    const float Dv = __ldg(a.D + si), hzv = __ldg(a.hz + si);
-                    const float half_rt = (float)sc.half_rt, rt = (float)sc.rt, dt = (float)sc.dt;
-                    const float Kj = (float)sc.Kj, nbeta = (float)sc.nbeta, tau = (float)sc.tau;
-                    const double pd = a.pump ? a.pump[a.step] : a.p_scalar;
-                    const float loss = sc.minus_j != 0.0 ? (float)((-1.0 + pd) - sc.minus_j)
-                                                         : (float)(-1.0 + pd);
-                    const float thresh = (float)a.alt->thresh;
-                    float cn[NR], en[NR];
-#pragma unroll
-                    for (int q = 0; q < NR; ++q) {
-                        const float c = cv[q], e = ev[q];
-                        const float Jw = Dv * wv[q] - gw[q];
-                        float h;
-                        if constexpr (MODE == EPI_STEP_BN)
-                            h = half_rt * (Jw + hzv);
-                        else
-                            h = Jw + half_rt * hzv;
-                        if (a.Hdbg) a.Hdbg[vi0 + q] = h;
-                        const float inj = (Kj * e) * (Rv[q] * h - thresh);
-                        cn[q] = c + dt * ((loss - c * c) * c + inj);
-                        en[q] = e + dt * ((nbeta * (c * c - tau)) * e);
-                        if (fz[q]) {
-                            cn[q] = c;
-                            en[q] = e;
-                        } else if (!isfinite(cn[q]) || !isfinite(en[q])) {
-                            atomicMin(&a.fail_gstep[b * NR + q], a.alt->gstep_base + a.step);
-                            atomicMin(&a.fail_idx[b * NR + q], i);
-                            cn[q] = c;
-                            en[q] = e;
-                        } else {
-                            lmin[q] = en[q];
-                            float wn;
-                            if constexpr (MODE == EPI_STEP_BN)
-                                wn = Rv[q] * (cn[q] > 0.f ? 1.f : 0.f);
-                            else
-                                wn = (Rv[q] * 0.25f) * (cn[q] + rt);
-                            a.Wout[tc_wofs(a.ldJ, NR, b, i, q)] = wn;
-                            a.Wout[tc_wofs(a.ldJ, NR, b, i, NR + q)] = wn - trunc_tf32(wn);
-                        }
-                    }
-#pragma unroll
-                    for (int q = 0; q < NR; q += 4) {
-                        *reinterpret_cast<float4*>(a.C + vi0 + q) =
-                            make_float4(cn[q], cn[q + 1], cn[q + 2], cn[q + 3]);
-                        *reinterpret_cast<float4*>(a.E + vi0 + q) =
-                            make_float4(en[q], en[q + 1], en[q + 2], en[q + 3]);
-                    }
-                }
-                // per-replica min of e: warp reduce, one atomic per (warp, replica)
-#pragma unroll
-                for (int q = 0; q < NR; ++q) {
-                    float m = lmin[q];
-#pragma unroll
-                    for (int off = 16; off > 0; off >>= 1)
-                        m = fminf(m, __shfl_xor_sync(0xffffffffu, m, off));
-                    if (lane == q && m != INFINITY) atomicMin(&a.minE[b * NR + q], ord_key(m));
-                }
-            } else if constexpr (MODE == EPI_JACOBI) {
-                if (valid) {
-                    const float Dv = __ldg(a.D + si), bv = __ldg(a.hz + si);
-                    const float omd = (float)sc.one_minus_dtc, dtc = (float)sc.dt_c;
-#pragma unroll
-                    for (int q = 0; q < NR; ++q) {
-                        if (fz[q]) continue;
-                        const float Rv = a.Rs[vi0 + q];
-                        const bool on = a.sigma[vi0 + q] != 0;
-                        float rn = Rv;
-                        if (on) {
-                            if (Dv == 0.f) {
-                                atomicMin(a.err, i);
-                                continue;
-                            }
-                            const float off = gw[q] - Dv * Rv;
-                            rn = omd * Rv + dtc * ((bv - off) / Dv);
-                            a.Rs[vi0 + q] = rn;
-                        }
-                        const float wn = rn * (on ? 1.f : 0.f);
-                        a.Wout[tc_wofs(a.ldJ, NR, b, i, q)] = wn;
-                        a.Wout[tc_wofs(a.ldJ, NR, b, i, NR + q)] = wn - trunc_tf32(wn);
-                    }
-                }
-            } else if constexpr (MODE == EPI_MATVEC) {
-                if (valid) {
-#pragma unroll
-                    for (int q = 0; q < NR; ++q)
-                        if (!fz[q]) a.Mv[vi0 + q] = (double)gw[q];
-                }
-            } else {  // EPI_SCORE
-                double pa[NR], pb[NR], pc[NR];
-#pragma unroll
-                for (int q = 0; q < NR; ++q) {
-                    pa[q] = pb[q] = pc[q] = 0.0;
-                    if (valid && !fz[q]) {
-                        const double wv = a.Win[tc_wofs(a.ldJ, NR, b, i, q)];
-                        pa[q] = wv * (double)gw[q];
-                        pb[q] = (double)a.hz[si] * wv;
-                        if (a.xtrue) {
-                            const double xt = a.xitrue[si] ? a.xtrue[si] : 0.0;
-                            pc[q] = (wv - xt) * (wv - xt);
-                        }
-                    }
-#pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) {
-                        pa[q] += __shfl_xor_sync(0xffffffffu, pa[q], off);
-                        pb[q] += __shfl_xor_sync(0xffffffffu, pb[q], off);
-                        pc[q] += __shfl_xor_sync(0xffffffffu, pc[q], off);
-                    }
-                }
-                if (lane < NR) {
-                    s_part[ep][lane][0] = pa[lane];
-                    s_part[ep][lane][1] = pb[lane];
-                    s_part[ep][lane][2] = pc[lane];
-                }
-                asm volatile("bar.sync 2, 128;" ::: "memory");
-                if (ep == 0 && lane < NR) {
-                    double A_ = 0, B_ = 0, C_ = 0;
-                    for (int w = 0; w < 4; ++w) {
-                        A_ += s_part[w][lane][0];
-                        B_ += s_part[w][lane][1];
-                        C_ += s_part[w][lane][2];
-                    }
-                    double* p = a.part + (((size_t)b * a.nRB + rb) * NR + lane) * 4;
-                    p[0] = A_;
-                    p[1] = B_;
-                    p[2] = C_;
-                }
-                asm volatile("bar.sync 2, 128;" ::: "memory");
-            }
+            tc_row_update<NR, MODE>(a, b, rb, row, lane, ep, gw, s_part);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -1,0 +1,124 @@
+"""Symmetric-tile fp32 path (sym_kernels.cuh): the upper-triangle gram tiles
+stored once as scaled fp16 hi/lo planes, each tile feeding G w and G^T w.
+
+Stated fp32 tolerances (the same as the streaming 3xTF32 path): gram within
+1e-6 of max |G|; local field within 2e-5 of the field scale vs the fp64
+oracle; refit within 1e-4; solve supports identical on >= 90 % of the
+trajectories with mean |dRMSE|/RMSE <= 5e-2.  The cross-CTA reduction runs
+in a fixed order, so two runs are bitwise identical.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx(P, insts, **opts):
+    ctx = P.Context(0, "f32")
+    for k, v in opts.items():
+        ctx.set_option(k, v)
+    ctx.set_problems(insts)
+    ctx.build_coupling()
+    return ctx
+
+
+@pytest.mark.parametrize("N", [513, 640, 1000])
+def test_sym_gram(gpu, O, N):
+    insts = [O.gen_instance(N, 0.5, 0.1, 0.01, 5), O.gen_instance(N, 0.7, 0.1, 0.01, 6)]
+    ctx = _ctx(gpu, insts)
+    for b, inst in enumerate(insts):
+        G, hz, D = ctx.get_coupling(b)
+        ref = O.Problem(inst, O.CANON).G
+        assert np.max(np.abs(G - ref)) <= 1e-6 * np.max(np.abs(ref))
+        assert np.array_equal(G, G.T)
+    ctx.close()
+
+
+@pytest.mark.parametrize("backend", ["mfz-bn", "mfz-cn"])
+@pytest.mark.parametrize("R", [3, 16])
+def test_sym_step_field_accuracy(gpu, O, backend, R):
+    insts = [O.gen_instance(700, 0.6, 0.2, 0.01, 3), O.gen_instance(700, 0.4, 0.1, 0.01, 4)]
+    probs = [O.Problem(i, O.CANON) for i in insts]
+    B, N = 2, 700
+    rng = np.random.default_rng(R)
+    Rs = rng.normal(size=(B, R, N))
+    Rs[0, 0, :50] *= 1e-4  # widely different magnitudes inside one replica
+    c = rng.normal(scale=0.5, size=(B, R, N))
+    e = np.abs(rng.normal(size=(B, R, N))) + 0.1
+    ctx = _ctx(gpu, insts)
+    out = ctx.mfz_step(R, backend, gpu.baseline_params(), 0.37, 0.83, Rs, c, e)
+    ctx.close()
+    ohp = O.baseline_params()
+    for b in range(B):
+        for r in range(R):
+            if backend == "mfz-bn":
+                h = probs[b].local_field_bn(Rs[b, r], (c[b, r] > 0).astype(np.int32), ohp.tau)
+            else:
+                h = probs[b].local_field_cn(Rs[b, r], c[b, r], ohp.tau)
+            err = np.max(np.abs(out["h"][b, r] - h)) / np.max(np.abs(h))
+            assert err < 2e-5, (b, r, err)
+
+
+def test_sym_refit_cg_and_score(gpu, O):
+    insts = [O.gen_instance(600, 0.6, 0.2, 0.01, 7)]
+    p = O.Problem(insts[0], O.CANON)
+    R = 16
+    rng = np.random.default_rng(2)
+    sigma = (rng.random((1, R, 600)) < 0.2).astype(np.int32)
+    Rp = rng.normal(size=(1, R, 600))
+    ctx = _ctx(gpu, insts)
+    out = ctx.refit(R, sigma, Rp, gpu.HyperParams())
+    outc = ctx.refit(R, sigma, Rp, gpu.HyperParams(), cdp="cg")
+    sc = ctx.score(R, Rp, sigma, 0.05)
+    ctx.close()
+    for r in range(R):
+        for res, m in ((out, O.CDP_JACOBI), (outc, O.CDP_CG)):
+            ref = p.cdp(sigma[0, r], Rp[0, r], m, O.HyperParams())
+            assert np.max(np.abs(res[0, r] - ref)) < 1e-4 * max(1.0, np.max(np.abs(ref)))
+        obj = p.objective_at(Rp[0, r], sigma[0, r], 0.05)
+        assert math.isclose(sc["objective"][0, r], obj, rel_tol=1e-5, abs_tol=1e-6)
+
+
+@pytest.mark.parametrize("backend", ["mfz-bn", "mfz-cn"])
+def test_sym_solve_matches_fp64_and_is_deterministic(gpu, O, backend):
+    insts = [O.gen_instance(600, 0.5, 0.1, 0.01, s) for s in range(1, 4)]
+    R = 4
+    hp = O.baseline_params(velo=7)
+    be = O.MFZ_BN if backend == "mfz-bn" else O.MFZ_CN
+    seeds = np.array([[O.mix_seed(i.seed, be + 3 * r) for r in range(R)] for i in insts],
+                     np.uint64)
+    runs = []
+    for _ in range(2):
+        ctx = _ctx(gpu, insts)
+        runs.append(ctx.solve(R, backend, gpu.baseline_params(velo=7), seeds))
+        ctx.close()
+    assert np.array_equal(runs[0]["R"], runs[1]["R"])
+    assert np.array_equal(runs[0]["sigma"], runs[1]["sigma"])
+    res = runs[0]
+    same, rel = 0, []
+    for b, inst in enumerate(insts):
+        for r in range(R):
+            ref = O.Problem(inst, O.CANON).alternating_minimize(be, hp, O.Rng(int(seeds[b, r])))
+            same += np.array_equal(res["sigma"][b, r], ref["sigma"])
+            g = O.rmse(res["R"][b, r], res["sigma"][b, r], inst.x_true, inst.xi_true)
+            rel.append(abs(g - ref["final_rmse"]) / ref["final_rmse"])
+    assert same >= 0.9 * len(insts) * R, same
+    assert np.mean(rel) <= 5e-2
+
+
+def test_sym_matches_streaming_kernel(gpu, O):
+    """symmetric=0 (tf32 streaming kernel) and the symmetric path agree to fp32 accuracy."""
+    insts = [O.gen_instance(800, 0.5, 0.1, 0.01, 9)]
+    R = 8
+    rng = np.random.default_rng(4)
+    Rs = rng.normal(size=(1, R, 800))
+    c = rng.normal(scale=0.5, size=(1, R, 800))
+    e = np.ones((1, R, 800))
+    outs = []
+    for sym in (1, 0):
+        ctx = _ctx(gpu, insts, symmetric=sym)
+        outs.append(ctx.mfz_step(R, "mfz-cn", gpu.baseline_params(), 0.4, 0.9, Rs, c, e)["h"])
+        ctx.close()
+    assert np.max(np.abs(outs[0] - outs[1])) <= 4e-5 * np.max(np.abs(outs[1]))
