@@ -138,7 +138,9 @@ def kernel_label(N, NR, dtype):
                 "register-resident, w over DSMEM; bound by the per-step FMA chain + DSMEM "
                 "round trip, so the HBM fraction is an HBM-equivalent figure)")
     if dtype == "f32":
-        return f"tc_step_kernel<{NR},BN> (fused Euler step, tcgen05 3xTF32)"
+        return (f"sym_step_kernel<{NR},BN> + sym_reduce_kernel + sym_finish_kernel (one fused "
+                "Euler step: upper-triangle gram tiles as fp16 hi/lo, each read once for G w "
+                "and G^T w on tcgen05; achieved counts the dense-gram algorithmic bytes)")
     return f"gemv_fused_kernel<double,{NR},BN> (fused Euler step, fp64 DFMA)"
 
 
@@ -354,6 +356,9 @@ def run_ours(args, ws, rank, local):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": ncu_traffic() if args.config == 1 and args.dtype == "f32" else None,
+                         "traffic_note": ("ncu dram read+write of the three kernels of one step "
+                                          "(profiles/ncu_step_summary.json)"
+                                          if args.config == 1 and args.dtype == "f32" else None),
                          "kernel": kernel_label(Nn, ctx_nr(R, args.dtype), args.dtype),
                          "bytes_per_launch": step_bytes, "peak_kind": peak_kind},
             "e2e": None if e2e_val is None else {

@@ -321,6 +321,10 @@ struct cimcs_ctx {
     short2* dTri = nullptr;
     int* dSg = nullptr;    // per-instance gram scale exponent
     float* dSpart = nullptr;  // partial products [B][nRB][nRB][128][NR]
+    float* dGw = nullptr;     // their slot sums [B][nRB * 128][NR]
+    int sym_groups = 0;       // instance groups pipelined across two streams (0: auto)
+    cudaStream_t sfin = nullptr;             // stream of the reduction / update kernels
+    cudaEvent_t evA[4] = {}, evF[4] = {};    // per group: tiles done / update done
     __half *WB0 = nullptr, *WB1 = nullptr;  // fp16 B tiles of W0 / W1 [B][nRB][2NR x 128]
     int *WS0 = nullptr, *WS1 = nullptr;     // their scale exponents [B][nRB][NR]
     size_t spart_elems = 0;
@@ -414,12 +418,12 @@ void free_state(cimcs_ctx* c) {
 void free_problems(cimcs_ctx* c) {
     free_state(c);
     void* ptrs[] = {c->dA, c->dy, c->dM, c->dG, c->dD, c->dhz, c->dx, c->dxi,
-                    c->dTri, c->dSg, c->dSpart};
+                    c->dTri, c->dSg, c->dSpart, c->dGw};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     c->dTri = nullptr;
     c->dSg = nullptr;
-    c->dSpart = nullptr;
+    c->dSpart = c->dGw = nullptr;
     c->spart_elems = 0;
     c->dA = c->dy = nullptr;
     c->dM = nullptr;
@@ -474,6 +478,13 @@ int ensure_state(cimcs_ctx* c, int NR) {
         (rc = dalloc(&c->rmse, nT * 8)) || (rc = dalloc(&c->ham, nT * 8)) ||
         (rc = dalloc(&c->tp, (size_t)nT * 5 * 8)) || (rc = dalloc(&c->fail_tmp, nT * 4)))
         return rc;
+    if (c->sym && !c->sfin) {
+        CK(cudaStreamCreateWithFlags(&c->sfin, cudaStreamNonBlocking));
+        for (int g = 0; g < 4; ++g) {
+            CK(cudaEventCreateWithFlags(&c->evA[g], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->evF[g], cudaEventDisableTiming));
+        }
+    }
     if (c->sym) {  // fp16 B tiles of W0/W1 and the partial products of the symmetric kernel
         const size_t nb = (size_t)c->B * c->nRB * 2 * NR * kSyT, ns = (size_t)c->B * c->nRB * NR;
         if ((rc = dalloc(&c->WB0, nb * 2)) || (rc = dalloc(&c->WB1, nb * 2)) ||
@@ -482,9 +493,12 @@ int ensure_state(cimcs_ctx* c, int NR) {
         const size_t ne = (size_t)c->B * c->nRB * c->nRB * kSyT * NR;
         if (c->spart_elems < ne) {
             if (c->dSpart) cudaFree(c->dSpart);
-            c->dSpart = nullptr;
+            if (c->dGw) cudaFree(c->dGw);
+            c->dSpart = c->dGw = nullptr;
             c->spart_elems = 0;
-            if ((rc = dalloc(&c->dSpart, ne * 4))) return rc;
+            if ((rc = dalloc(&c->dSpart, ne * 4)) ||
+                (rc = dalloc(&c->dGw, (size_t)c->B * c->nRB * kSyT * NR * 4)))
+                return rc;
             c->spart_elems = ne;
         }
     }
@@ -627,9 +641,12 @@ int launch_tc_t(cimcs_ctx* c, const GemvArgs& g) {
     return 0;
 }
 
-// symmetric-tile variant (sym_kernels.cuh): half the gram bytes per step
+// symmetric-tile variant (sym_kernels.cuh): half the gram bytes per step.
+// Instances [b0, b0 + nb): the tile kernel on stream sA, then (after evA) the
+// slot reduction and the fused update on stream sF.
 template <int NR, int MODE>
-int launch_sym_t(cimcs_ctx* c, const GemvArgs& g) {
+int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb, cudaStream_t sA,
+                 cudaStream_t sF, cudaEvent_t evA) {
     SymArgs sa{};
     sa.t = tc_args(c, g);
     sa.Gs = static_cast<const __half*>(c->dG);
@@ -641,7 +658,8 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g) {
     sa.spart = c->dSpart;
     sa.tri = c->dTri;
     sa.ntri = c->ntri;
-    sa.ntiles = c->B * c->ntri;
+    sa.ntiles = nb * c->ntri;
+    sa.b0 = b0;
     if (sa.ntiles == 0) return 0;
     auto kern = sym_step_kernel<NR, MODE>;
     constexpr size_t smem = sy_smem_bytes<NR>();
@@ -651,22 +669,37 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g) {
         attr = true;
     }
     const int grid = std::min(sa.ntiles, c->num_sms);
-    kern<<<grid, kSyThreads, smem, c->stream>>>(sa);
+    kern<<<grid, kSyThreads, smem, sA>>>(sa);
     CK(cudaGetLastError());
-    sym_finish_kernel<NR, MODE><<<dim3(c->nRB, c->B), 256, 0, c->stream>>>(sa);
+    if (sF != sA) {
+        CK(cudaEventRecord(evA, sA));
+        CK(cudaStreamWaitEvent(sF, evA, 0));
+    }
+    const size_t off = (size_t)b0 * c->nRB * kSyT * NR;
+    const int total = nb * c->nRB * kSyT * (NR / 4);
+    sym_reduce_kernel<NR><<<(total + 255) / 256, 256, 0, sF>>>(c->dSpart + off * c->nRB,
+                                                               c->dGw + off, c->nRB, total);
+    CK(cudaGetLastError());
+    sym_finish_kernel<NR, MODE><<<dim3(c->nRB, nb), 128, 0, sF>>>(sa, c->dGw);
     CK(cudaGetLastError());
     return 0;
 }
 
 template <int NR>
-int launch_sym_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
+int launch_sym_grp(cimcs_ctx* c, int mode, const GemvArgs& a, int b0, int nb, cudaStream_t sA,
+                   cudaStream_t sF, cudaEvent_t evA) {
     switch (mode) {
-        case EPI_STEP_BN: return launch_sym_t<NR, EPI_STEP_BN>(c, a);
-        case EPI_STEP_CN: return launch_sym_t<NR, EPI_STEP_CN>(c, a);
-        case EPI_JACOBI: return launch_sym_t<NR, EPI_JACOBI>(c, a);
-        case EPI_MATVEC: return launch_sym_t<NR, EPI_MATVEC>(c, a);
-        default: return launch_sym_t<NR, EPI_SCORE>(c, a);
+        case EPI_STEP_BN: return launch_sym_t<NR, EPI_STEP_BN>(c, a, b0, nb, sA, sF, evA);
+        case EPI_STEP_CN: return launch_sym_t<NR, EPI_STEP_CN>(c, a, b0, nb, sA, sF, evA);
+        case EPI_JACOBI: return launch_sym_t<NR, EPI_JACOBI>(c, a, b0, nb, sA, sF, evA);
+        case EPI_MATVEC: return launch_sym_t<NR, EPI_MATVEC>(c, a, b0, nb, sA, sF, evA);
+        default: return launch_sym_t<NR, EPI_SCORE>(c, a, b0, nb, sA, sF, evA);
     }
+}
+
+template <int NR>
+int launch_sym_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
+    return launch_sym_grp<NR>(c, mode, a, 0, c->B, c->stream, c->stream, nullptr);
 }
 
 template <int NR>
@@ -1009,6 +1042,36 @@ int launch_cluster(cimcs_ctx* c, int mode, const GemvArgs& a, int n_iters) {
                                  : launch_cluster_T<float>(c, mode, a, n_iters);
 }
 
+// n_iters launches of `mode` with W ping-pong (Euler steps or Jacobi sweeps) on
+// the symmetric path.  Option "sym_groups" > 1 splits the instances into
+// groups: the tile kernel of group g+1 runs on the context stream while the
+// reduction / update of group g runs on c->sfin, and group g's next tile
+// kernel waits only for its own update.  Measured on config 1 it does not pay
+// (the step is bound by the total HBM traffic of the three kernels, which
+// overlapping cannot reduce), so the default is one group.
+int enqueue_sym_loop(cimcs_ctx* c, int mode, GemvArgs a, int n_iters, bool steps) {
+    int G = c->sym_groups ? c->sym_groups : 1;
+    G = std::max(1, std::min(G, std::min(4, c->B)));
+    for (int k = 0; k < n_iters; ++k) {
+        if (steps) a.step = k;
+        a.Win = (k & 1) ? c->W1 : c->W0;
+        a.Wout = (k & 1) ? c->W0 : c->W1;
+        for (int g = 0; g < G; ++g) {
+            const int b0 = (int)((long long)c->B * g / G), b1 = (int)((long long)c->B * (g + 1) / G);
+            if (G > 1 && k > 0) CK(cudaStreamWaitEvent(c->stream, c->evF[g], 0));
+            cudaStream_t sF = G > 1 ? c->sfin : c->stream;
+            const int rc = c->NR == 8
+                               ? launch_sym_grp<8>(c, mode, a, b0, b1 - b0, c->stream, sF, c->evA[g])
+                               : launch_sym_grp<16>(c, mode, a, b0, b1 - b0, c->stream, sF, c->evA[g]);
+            if (rc) return rc;
+            if (G > 1) CK(cudaEventRecord(c->evF[g], c->sfin));
+        }
+    }
+    if (G > 1)
+        for (int g = 0; g < G; ++g) CK(cudaStreamWaitEvent(c->stream, c->evF[g], 0));
+    return 0;
+}
+
 int enqueue_steps(cimcs_ctx* c, int bn, const StepScalars& s, int n_steps) {
     GemvArgs a = base_args(c, s);
     a.pump = c->pump;
@@ -1019,6 +1082,7 @@ int enqueue_steps(cimcs_ctx* c, int bn, const StepScalars& s, int n_steps) {
         a.Wout = (n_steps & 1) ? c->W1 : c->W0;
         return launch_cluster(c, bn ? EPI_STEP_BN : EPI_STEP_CN, a, n_steps);
     }
+    if (c->sym) return enqueue_sym_loop(c, bn ? EPI_STEP_BN : EPI_STEP_CN, a, n_steps, true);
     for (int k = 0; k < n_steps; ++k) {
         a.step = k;
         a.Win = (k & 1) ? c->W1 : c->W0;
@@ -1040,6 +1104,10 @@ int enqueue_refit(cimcs_ctx* c, const StepScalars& s, int iters, bool do_support
         a.Win = c->W0;
         a.Wout = (iters & 1) ? c->W1 : c->W0;
         return launch_cluster(c, EPI_JACOBI, a, iters);
+    }
+    if (c->sym) {
+        if (int rc = enqueue_sym_loop(c, EPI_JACOBI, a, iters, false)) return rc;
+        return 0;
     }
     for (int it = 0; it < iters; ++it) {
         a.Win = (it & 1) ? c->W1 : c->W0;
@@ -1557,6 +1625,11 @@ void cimcs_destroy(cimcs_ctx* c) {
     drop_graphs(c);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->side) cudaStreamDestroy(c->side);
+    if (c->sfin) cudaStreamDestroy(c->sfin);
+    for (int g = 0; g < 4; ++g) {
+        if (c->evA[g]) cudaEventDestroy(c->evA[g]);
+        if (c->evF[g]) cudaEventDestroy(c->evF[g]);
+    }
     cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -1566,6 +1639,7 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
     const std::string k(key);
     if (k == "host_threads") c->host_threads = (int)std::max<int64_t>(1, v);
     else if (k == "use_graphs") c->use_graphs = v != 0;
+    else if (k == "sym_groups") c->sym_groups = (int)std::min<int64_t>(4, std::max<int64_t>(0, v));
     else if (k == "symmetric") {
         if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set symmetric before set_problems");
         c->want_sym = v != 0;

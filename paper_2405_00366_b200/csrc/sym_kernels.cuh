@@ -16,10 +16,10 @@
 // accumulated in fp32 in TMEM, and unscaled exactly.
 //
 // A row block K receives nRB partial products (one per tile touching it),
-// written to [B][nRB][slot][128][NR].  A second, evenly spread kernel
-// (sym_finish_kernel, one CTA per block) sums the slots in a FIXED order and
-// runs the fused Euler / Jacobi / score / matvec update (tc_row_update, shared
-// with the streaming kernel): deterministic, and no CTA waits for another.
+// written to [B][nRB][slot][128][NR].  Two evenly spread kernels finish the
+// step: sym_reduce_kernel sums the slots in a FIXED order (deterministic) and
+// sym_finish_kernel runs the fused Euler / Jacobi / score / matvec update
+// (tc_row_update, shared with the streaming kernel); no CTA waits for another.
 // (A fused variant with owner-CTA finisher warps and an L2-resident ring of
 // partials was measured slower: each finish is a chain of dependent L2 round
 // trips, and 7 of them per CTA behind the tile stream left a long tail.)
@@ -153,7 +153,8 @@ struct SymArgs {
     int* WSout;
     float* spart;          // [B][nRB][nRB][128][NR]
     const short2* tri;     // [ntri] -> (I, J)
-    int ntri, ntiles;      // tiles per instance, B * ntri
+    int ntri, ntiles;      // tiles per instance, tiles of this launch (nb * ntri)
+    int b0;                // first instance of this launch (instance groups)
 };
 
 template <int NR>
@@ -255,10 +256,11 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
             int tt = 0;
             for (int tile = blockIdx.x; tile < sa.ntiles; tile += gridDim.x, ++tt) {
                 const int s = tt % kSyStages;
-                const int b = tile / sa.ntri;
+                const int b = sa.b0 + tile / sa.ntri;
                 const short2 ij = sa.tri[tile % sa.ntri];
                 if (tt >= kSyStages) mbar_wait(&empty[s], ((tt / kSyStages) - 1) & 1);
-                const __half* src = sa.Gs + (size_t)tile * 2 * kSyPlaneHalfs;
+                const __half* src =
+                    sa.Gs + ((size_t)sa.b0 * sa.ntri + tile) * 2 * kSyPlaneHalfs;
                 const __half* wb = sa.WBin + (size_t)b * nRB * (2 * NR * kSyT);
                 unsigned char* st = smem + s * kStage;
                 const bool off = ij.x != ij.y;
@@ -315,7 +317,7 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
         int tt = 0;
         for (int tile = blockIdx.x; tile < sa.ntiles; tile += gridDim.x, ++tt) {
             const int acc = tt & 1;
-            const int b = tile / sa.ntri;
+            const int b = sa.b0 + tile / sa.ntri;
             const short2 ij = sa.tri[tile % sa.ntri];
             const int I = ij.x, J = ij.y;
             mbar_wait(&tm_full[acc], (tt / 2) & 1);
@@ -363,56 +365,57 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
                      "n"(kSyTmemCols));
 }
 
-// Second pass of a step: block (b, K) sums its nRB partial products in slot
-// order (deterministic) and runs the fused update; step / Jacobi modes also
-// emit the fp16 B tile of the new w for the next launch.  256 threads: every
-// (row, half of the replicas) pair loads its 16 slots at once, then the first
-// 128 threads (one per row) run the update.
+// Second pass of a step, part 1: sum the nRB partial products of every
+// (instance, row, 4 replicas) in slot order (deterministic) -> gw.  Light and
+// fully occupied: every thread has all its slot loads in flight at once.
+template <int NR>
+__global__ void __launch_bounds__(256) sym_reduce_kernel(const float* __restrict__ spart,
+                                                         float* __restrict__ gw, int nRB,
+                                                         int total) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;  // (b, K, row, q4)
+    if (t >= total) return;
+    constexpr int Q4 = NR / 4;
+    const int q4 = t % Q4, r = t / Q4;  // r = (b * nRB + K) * 128 + row
+    const int row = r % kSyT, bk = r / kSyT;
+    const float4* src =
+        reinterpret_cast<const float4*>(spart + ((size_t)bk * nRB * kSyT + row) * NR) + q4;
+    constexpr size_t kSlot4 = (size_t)kSyT * NR / 4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < nRB; s0 += 16) {
+        float4 v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (s0 + u < nRB) v[u] = __ldcs(src + (s0 + u) * kSlot4);
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (s0 + u < nRB) {
+                acc.x = acc.x + v[u].x;
+                acc.y = acc.y + v[u].y;
+                acc.z = acc.z + v[u].z;
+                acc.w = acc.w + v[u].w;
+            }
+    }
+    reinterpret_cast<float4*>(gw + (size_t)r * NR)[q4] = acc;
+}
+
+// Part 2: the fused update of block (b, K) from gw; step / Jacobi modes also
+// emit the fp16 B tile of the new w for the next launch.
 template <int NR, int MODE>
-__global__ void __launch_bounds__(256) sym_finish_kernel(SymArgs sa) {
+__global__ void __launch_bounds__(128) sym_finish_kernel(SymArgs sa, const float* __restrict__ gwb) {
     __shared__ double s_part[4][NR][3];
     __shared__ unsigned s_max[4][NR];
-    __shared__ float s_gw[kSyT][NR + 1];
     const TcArgs& a = sa.t;
     constexpr bool kWritesW = MODE == EPI_STEP_BN || MODE == EPI_STEP_CN || MODE == EPI_JACOBI;
-    constexpr int H = NR / 2;  // replicas per half
-    const int K = blockIdx.x, b = blockIdx.y, nRB = a.nRB;
-    {
-        const int row = threadIdx.x & (kSyT - 1), half = threadIdx.x >> 7;
-        const float4* src = reinterpret_cast<const float4*>(
-            sa.spart + (((size_t)b * nRB + K) * nRB * kSyT + row) * NR + half * H);
-        constexpr size_t kSlot4 = (size_t)kSyT * NR / 4;
-        float g[H];
-#pragma unroll
-        for (int q = 0; q < H; ++q) g[q] = 0.f;
-        for (int s0 = 0; s0 < nRB; s0 += 8) {  // up to 8 slots x H/4 float4 in flight
-            float4 v[8][H / 4];
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-#pragma unroll
-                for (int q = 0; q < H / 4; ++q)
-                    if (s0 + u < nRB) v[u][q] = __ldcs(src + (s0 + u) * kSlot4 + q);
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-#pragma unroll
-                for (int q = 0; q < H / 4; ++q)
-                    if (s0 + u < nRB) {
-                        // slot 0 starts the sum (0 + x == x exactly)
-                        g[4 * q] = g[4 * q] + v[u][q].x;
-                        g[4 * q + 1] = g[4 * q + 1] + v[u][q].y;
-                        g[4 * q + 2] = g[4 * q + 2] + v[u][q].z;
-                        g[4 * q + 3] = g[4 * q + 3] + v[u][q].w;
-                    }
-        }
-#pragma unroll
-        for (int q = 0; q < H; ++q) s_gw[row][half * H + q] = g[q];
-    }
-    __syncthreads();
-    if (threadIdx.x >= kSyT) return;
+    const int K = blockIdx.x, b = sa.b0 + blockIdx.y, nRB = a.nRB;
     const int row = threadIdx.x, lane = row & 31, ep = row >> 5;
+    const float4* g4 =
+        reinterpret_cast<const float4*>(gwb + (((size_t)b * nRB + K) * kSyT + row) * NR);
     float gw[NR];
 #pragma unroll
-    for (int q = 0; q < NR; ++q) gw[q] = s_gw[row][q];
+    for (int q = 0; q < NR; q += 4) {
+        const float4 v = __ldcs(g4 + q / 4);
+        gw[q] = v.x; gw[q + 1] = v.y; gw[q + 2] = v.z; gw[q + 3] = v.w;
+    }
     tc_row_update<NR, MODE>(a, b, K, row, lane, ep, gw, s_part);
     if constexpr (kWritesW) {
         const int i = K * kSyT + row;

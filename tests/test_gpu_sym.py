@@ -122,3 +122,19 @@ def test_sym_matches_streaming_kernel(gpu, O):
         outs.append(ctx.mfz_step(R, "mfz-cn", gpu.baseline_params(), 0.4, 0.9, Rs, c, e)["h"])
         ctx.close()
     assert np.max(np.abs(outs[0] - outs[1])) <= 4e-5 * np.max(np.abs(outs[1]))
+
+
+def test_sym_instance_groups_bitwise(gpu, O):
+    """sym_groups = 2 (two-stream pipelined groups) gives the same bits as one group."""
+    insts = [O.gen_instance(600, 0.5, 0.1, 0.01, s) for s in range(1, 5)]
+    R = 8
+    hp = gpu.baseline_params(velo=2, n_steps=300)
+    seeds = np.array([[O.mix_seed(i.seed, 1 + 3 * r) for r in range(R)] for i in insts],
+                     np.uint64)
+    outs = []
+    for g in (1, 2):
+        ctx = _ctx(gpu, insts, sym_groups=g)
+        outs.append(ctx.solve(R, "mfz-bn", hp, seeds))
+        ctx.close()
+    assert np.array_equal(outs[0]["R"], outs[1]["R"])
+    assert np.array_equal(outs[0]["sigma"], outs[1]["sigma"])
