@@ -52,8 +52,9 @@ def main(rep, name, note=""):
         e["units"] = {k: units.get(k) for k in KEYS if k in units}
         out.append(e)
     summary = {"report": rep, "note": note, "kernels": out}
-    if out:
-        summary["dram_bytes_per_launch"] = out[0].get("dram_bytes_per_launch")
+    if out:  # one step = every kernel captured (the symmetric path launches three)
+        vals = [k.get("dram_bytes_per_launch") for k in out]
+        summary["dram_bytes_per_launch"] = sum(v for v in vals if v) if all(vals) else vals[0]
     with open(f"profiles/{name}.json", "w") as f:
         json.dump(summary, f, indent=1)
     print(json.dumps(summary, indent=1)[:3000])
