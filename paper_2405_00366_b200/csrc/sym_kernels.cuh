@@ -416,12 +416,10 @@ __global__ void __launch_bounds__(128) sym_finish_kernel(SymArgs sa, const float
         const float4 v = __ldcs(g4 + q / 4);
         gw[q] = v.x; gw[q + 1] = v.y; gw[q + 2] = v.z; gw[q + 3] = v.w;
     }
-    tc_row_update<NR, MODE>(a, b, K, row, lane, ep, gw, s_part);
+    // the [W | W_lo] residue half is read only by the streaming kernel: skipped
+    float w[NR];
+    tc_row_update<NR, MODE, false>(a, b, K, row, lane, ep, gw, s_part, 2, w);
     if constexpr (kWritesW) {
-        const int i = K * kSyT + row;
-        float w[NR];
-#pragma unroll
-        for (int q = 0; q < NR; ++q) w[q] = i < a.N ? a.Wout[tc_wofs(a.ldJ, NR, b, i, q)] : 0.f;
         sy_emit_block<NR>(w, row, lane, ep, s_max,
                           sa.WBout + ((size_t)b * nRB + K) * (2 * NR * kSyT),
                           sa.WSout + ((size_t)b * nRB + K) * NR, 2);

@@ -154,14 +154,21 @@ struct TcArgs {
 // Per-row fused update after the contraction: thread `row` of the four
 // epilogue warps owns spin i = (rb0 + rb) * 128 + row of instance b and all NR
 // replicas; gw[q] = (G w)_iq.  Shared by the streaming kernel below and the
-// symmetric-tile kernel (sym_kernels.cuh).
-template <int NR, int MODE>
+// symmetric-tile kernel (sym_kernels.cuh).  kWLo: also store the tf32 residue
+// half of [W | W_lo] (only the streaming kernel reads it); wnv (optional)
+// receives the new contraction input of this row (0 where nothing was written).
+template <int NR, int MODE, bool kWLo = true>
 __device__ __forceinline__ void tc_row_update(const TcArgs& a, int b, int rb, int row, int lane,
                                               int ep, const float (&gw)[NR],
-                                              double (*s_part)[NR][3], int bar = 2) {
+                                              double (*s_part)[NR][3], int bar = 2,
+                                              float* wnv = nullptr) {
     const StepScalars& sc = a.s;
     const int N = a.N;
     const int i = (a.rb0 + rb) * kTcRows + row;
+    if (wnv) {
+#pragma unroll
+        for (int q = 0; q < NR; ++q) wnv[q] = 0.f;
+    }
     bool fz[NR];
 #pragma unroll
     for (int q = 0; q < NR; ++q) {
@@ -228,7 +235,8 @@ __device__ __forceinline__ void tc_row_update(const TcArgs& a, int b, int rb, in
                     else
                         wn = (Rv[q] * 0.25f) * (cn[q] + rt);
                     a.Wout[tc_wofs(a.ldJ, NR, b, i, q)] = wn;
-                    a.Wout[tc_wofs(a.ldJ, NR, b, i, NR + q)] = wn - trunc_tf32(wn);
+                    if (kWLo) a.Wout[tc_wofs(a.ldJ, NR, b, i, NR + q)] = wn - trunc_tf32(wn);
+                    if (wnv) wnv[q] = wn;
                 }
             }
 #pragma unroll
@@ -269,7 +277,8 @@ __device__ __forceinline__ void tc_row_update(const TcArgs& a, int b, int rb, in
                 }
                 const float wn = rn * (on ? 1.f : 0.f);
                 a.Wout[tc_wofs(a.ldJ, NR, b, i, q)] = wn;
-                a.Wout[tc_wofs(a.ldJ, NR, b, i, NR + q)] = wn - trunc_tf32(wn);
+                if (kWLo) a.Wout[tc_wofs(a.ldJ, NR, b, i, NR + q)] = wn - trunc_tf32(wn);
+                if (wnv) wnv[q] = wn;
             }
         }
     } else if constexpr (MODE == EPI_MATVEC) {
