@@ -43,6 +43,9 @@ WORKLOADS = {
        "instances x 8 replicas, 20 x 1000 steps",
     3: "BASELINE config 3: MRI-shaped synthetic, N=16384 (3-level Haar of a 128x128 ellipse "
        "phantom), M=6554 random DCT rows, 1 instance x 16 replicas, 20 x 1000 steps",
+    4: "BASELINE config 4 (single-GPU point of the strong-scaling run): gen_instance(N, 0.5, "
+       "0.05, 0.01, 7), N=100000 M=50000 K=5000, 1 instance x 4 replicas, 10 alternations x "
+       "500 steps",
 }
 METRIC = "MF-CIM spin-steps/s"
 UNIT = "spin-steps/s"
@@ -159,6 +162,8 @@ def make_instances(rank, config=1, ws=1):
         return W.config2(shard=sharding.instance_shard(costs, ws, rank))
     if config == 3:
         return W.config3()
+    if config == 4:
+        return W.config4(N=CFG.get("n4", 100_000))
     return W.config1(rank, CFG["B"])
 
 
@@ -178,6 +183,37 @@ def cpu_sample(insts, nthreads, alt_limit=1, n_steps=None):
                                        backend=O.MFZ_BN, mode=O.LITERAL)
     spin_steps = n * insts[0].N * n_steps * alt_limit
     return spin_steps / wall, wall, n
+
+
+def cpu_sample_steps(inst, nthreads, n_steps):
+    """Config 4 CPU sample: nthreads trajectories x n_steps Euler steps of run_mfz
+    with the reference's matrix-free A^T(A w) (no refit: its k x k gram alone is
+    O(M k^2)).  One oracle problem per thread (its LITERAL scratch is per problem,
+    A is shared read-only); only the steps are timed (ctypes releases the GIL)."""
+    import threading
+    from oracle import oracle as O
+    hp = O.baseline_params(velo=1, n_steps=n_steps)
+    oi = O.Instance(inst.A, inst.y, inst.x_true, inst.xi_true)
+    ready = threading.Barrier(nthreads + 1)
+    done = threading.Barrier(nthreads + 1)
+
+    def one(k):
+        p = O.Problem(oi, O.LITERAL)
+        R = p.hz.copy()
+        ready.wait()
+        p.run_mfz(R, hp, 0.8, O.MFZ_BN, O.Rng(O.mix_seed(inst.seed, 1 + 3 * k)))
+        done.wait()
+
+    th = [threading.Thread(target=one, args=(k,)) for k in range(nthreads)]
+    for t in th:
+        t.start()
+    ready.wait()
+    t0 = time.perf_counter()
+    done.wait()
+    wall = time.perf_counter() - t0
+    for t in th:
+        t.join()
+    return nthreads * inst.N * n_steps / wall, wall, nthreads
 
 
 def run_reference(args, ws, rank):
@@ -311,12 +347,17 @@ def run_ours(args, ws, rank, local):
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         nthreads = os.cpu_count() or 1
-        cs = 100 if args.config == 3 else hp.n_steps  # config 3: 100-step sample
-        v, wall_c, n = cpu_sample(insts, nthreads, n_steps=cs)
-        cpu = {"value": v, "unit": UNIT, "cores": nthreads, "kind": "port",
-               "sample": f"{n} trajectories (1/host thread) x 1 alternation x "
-                         f"{cs} Euler steps + refit, fp64 A^T(A w) "
-                         f"restatement, {wall_c:.1f}s wall"}
+        if args.config == 4:
+            cs = 2
+            v, wall_c, n = cpu_sample_steps(insts[0], min(nthreads, 8), cs)
+            sample = (f"{n} trajectories (1/host thread) x {cs} Euler steps of run_mfz, fp64 "
+                      f"A^T(A w) restatement, no refit, {wall_c:.1f}s wall")
+        else:
+            cs = 100 if args.config == 3 else hp.n_steps  # config 3: 100-step sample
+            v, wall_c, n = cpu_sample(insts, nthreads, n_steps=cs)
+            sample = (f"{n} trajectories (1/host thread) x 1 alternation x {cs} Euler steps "
+                      f"+ refit, fp64 A^T(A w) restatement, {wall_c:.1f}s wall")
+        cpu = {"value": v, "unit": UNIT, "cores": nthreads, "kind": "port", "sample": sample}
     ctx.close()
     fp64 = None
     if args.dtype == "f32" and not args.no_fp64 and args.config == 1:
@@ -344,7 +385,9 @@ def run_ours(args, ws, rank, local):
             "scaling": "strong" if args.config == 2 else "weak", "vs_baseline": None,
             "dtype": args.dtype,
             "data": "synthetic (seeded gen_instance, datagen.cpp:15-55)",
-            "config": {"workload": WORKLOADS[args.config],
+            "config": {"workload": (WORKLOADS[args.config] if args.config != 4 or args.n4 == 100_000
+                                    else WORKLOADS[4].replace("N=100000 M=50000 K=5000",
+                                                              f"N={Nn} (reduced)")),
                        "per_rank_instances": Bn, "replicas": R,
                        "step": "gram build + full alternating solve",
                        "l2": ("inputs larger than L2 (gram %.2f GB)" % (step_bytes / 1e9)
@@ -386,11 +429,13 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtype", default=None, choices=["f32", "f64"],
                     help="default: the config's (f32 for 1-3, f64 for 0)")
-    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3])
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
+    ap.add_argument("--n4", type=int, default=100_000, help="config 4 size (N)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fp64", action="store_true", help="skip the fp64 secondary line")
     args = ap.parse_args()
+    CFG["n4"] = args.n4
     ws, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, ws, rank)

@@ -9,6 +9,7 @@
 // runs the current one.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <cublas_v2.h>
 
 #include <algorithm>
 #include <atomic>
@@ -323,6 +324,8 @@ struct cimcs_ctx {
     float* dSpart = nullptr;  // partial products [B][nRB][nRB][128][NR]
     float* dGw = nullptr;     // their slot sums [B][nRB * 128][NR]
     int sym_groups = 0;       // instance groups pipelined across two streams (0: auto)
+    int gram_blas = 0;        // symmetric gram from cuBLAS DGEMM panels: 0 auto (N >= 8192), 1, -1
+    cublasHandle_t blas = nullptr;
     cudaStream_t sfin = nullptr;             // stream of the reduction / update kernels
     cudaEvent_t evA[4] = {}, evF[4] = {};    // per group: tiles done / update done
     __half *WB0 = nullptr, *WB1 = nullptr;  // fp16 B tiles of W0 / W1 [B][nRB][2NR x 128]
@@ -1535,13 +1538,15 @@ int cimcs_gen_instances(int32_t B, int32_t N, const double* alpha, const double*
                         double* const* y, double* const* x_true, int32_t* const* xi_true,
                         int32_t threads) {
     std::atomic<int> next{0}, bad{0};
+    if (threads <= 0) threads = (int)std::thread::hardware_concurrency();
+    // fewer instances than threads: the spare threads transform each instance's A
+    const int inner = std::max(1, threads / std::max(1, B));
     auto work = [&] {
         for (int b = next.fetch_add(1); b < B; b = next.fetch_add(1))
             if (gen_instance(N, alpha[b], a[b], nu[b], seeds[b], A[b], y[b], x_true[b],
-                             xi_true[b]))
+                             xi_true[b], inner))
                 bad = 1;
     };
-    if (threads <= 0) threads = (int)std::thread::hardware_concurrency();
     threads = std::max(1, std::min<int>(threads, B));
     std::vector<std::thread> pool;
     for (int t = 0; t < threads; ++t) pool.emplace_back(work);
@@ -1626,6 +1631,7 @@ void cimcs_destroy(cimcs_ctx* c) {
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->sfin) cudaStreamDestroy(c->sfin);
+    if (c->blas) cublasDestroy(c->blas);
     for (int g = 0; g < 4; ++g) {
         if (c->evA[g]) cudaEventDestroy(c->evA[g]);
         if (c->evF[g]) cudaEventDestroy(c->evF[g]);
@@ -1639,6 +1645,7 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
     const std::string k(key);
     if (k == "host_threads") c->host_threads = (int)std::max<int64_t>(1, v);
     else if (k == "use_graphs") c->use_graphs = v != 0;
+    else if (k == "gram_blas") c->gram_blas = v > 0 ? 1 : (v < 0 ? -1 : 0);
     else if (k == "sym_groups") c->sym_groups = (int)std::min<int64_t>(4, std::max<int64_t>(0, v));
     else if (k == "symmetric") {
         if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set symmetric before set_problems");
@@ -1781,8 +1788,40 @@ int cimcs_build_coupling(cimcs_ctx* c) {
                                                      c->ldN, c->dSg);
         CK(cudaGetLastError());
     }
+    // large instances on the symmetric path: G = A^T A by cuBLAS DGEMM over panels
+    // of 8 row blocks (upper triangle only), converted to the fp16 hi/lo tiles
+    const bool blas = c->sym && (c->gram_blas > 0 || (c->gram_blas == 0 && c->N >= 8192));
+    if (blas) {
+        if (!c->blas) {
+            if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS)
+                return fail(CIMCS_CUDA_ERROR, "cublasCreate failed");
+        }
+        cublasSetStream(c->blas, c->stream);
+        const int PB = 8, ldp = PB * kSyT;
+        double* P = nullptr;
+        if ((rc = dalloc(&P, (size_t)ldp * c->N * 8))) return rc;
+        std::unique_ptr<double, decltype(&cudaFree)> pguard(P, &cudaFree);
+        const double one = 1.0, zero = 0.0;
+        for (int b = 0; b < c->B; ++b) {
+            const int M = c->M[b];
+            const double* Ab = c->dA + (size_t)b * astride;
+            SymOut o{static_cast<__half*>(c->dG), c->dSg, c->nRB, c->ntri};
+            for (int I0 = 0; I0 < c->nRB; I0 += PB) {
+                const int nI = std::min(PB, c->nRB - I0), i0 = I0 * kSyT;
+                const int rows = std::min(nI * kSyT, c->N - i0), ncols = c->N - i0;
+                if (cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, rows, ncols, M, &one,
+                                Ab + (size_t)i0 * M, M, Ab + (size_t)i0 * M, M, &zero, P,
+                                ldp) != CUBLAS_STATUS_SUCCESS)
+                    return fail(CIMCS_CUDA_ERROR, "cublasDgemm failed");
+                sym_panel_kernel<<<4 * c->num_sms, 256, 0, c->stream>>>(P, ldp, I0, nI, ncols,
+                                                                       c->N, o, b);
+                CK(cudaGetLastError());
+            }
+        }
+        CK(cudaStreamSynchronize(c->stream));  // P is freed on return
+    }
     // one launch per run of equal M (instances of a phase grid differ in M)
-    for (int b = 0; b < c->B;) {
+    for (int b = 0; b < c->B && !blas;) {
         int e = b;
         while (e < c->B && c->M[e] == c->M[b]) ++e;
         const dim3 grid(nt, nti, e - b);

@@ -138,3 +138,23 @@ def test_sym_instance_groups_bitwise(gpu, O):
         ctx.close()
     assert np.array_equal(outs[0]["R"], outs[1]["R"])
     assert np.array_equal(outs[0]["sigma"], outs[1]["sigma"])
+
+
+def test_sym_gram_from_cublas_panels(gpu, O):
+    """gram_blas=1: the symmetric tiles built from cuBLAS DGEMM panels (the large-N
+    route, config 4) match the oracle gram and drive the same local field."""
+    insts = [O.gen_instance(1100, 0.5, 0.1, 0.01, 21), O.gen_instance(1100, 0.6, 0.1, 0.01, 22)]
+    ctx = _ctx(gpu, insts, gram_blas=1)
+    for b, inst in enumerate(insts):
+        G, hz, D = ctx.get_coupling(b)
+        ref = O.Problem(inst, O.CANON).G
+        assert np.max(np.abs(G - ref)) <= 1e-6 * np.max(np.abs(ref))
+    R = 8
+    rng = np.random.default_rng(9)
+    Rs = rng.normal(size=(2, R, 1100))
+    c = rng.normal(scale=0.5, size=(2, R, 1100))
+    out = ctx.mfz_step(R, "mfz-bn", gpu.baseline_params(), 0.4, 0.9, Rs, c, np.ones((2, R, 1100)))
+    ctx.close()
+    p = O.Problem(insts[1], O.CANON)
+    h = p.local_field_bn(Rs[1, 3], (c[1, 3] > 0).astype(np.int32), 1.0)
+    assert np.max(np.abs(out["h"][1, 3] - h)) < 2e-5 * np.max(np.abs(h))

@@ -97,3 +97,16 @@ def test_mix_seed_matches(O):
     from paper_2405_00366_b200 import cimcs as P
     for base, salt in ((0, 1), (1, 0), (123456789, 7), (2**64 - 1, 3)):
         assert P.mix_seed(base, salt) == O.mix_seed(base, salt)
+
+
+@pytest.mark.parametrize("threads", [2, 5])
+def test_parallel_matrix_generator_matches_oracle(O, threads):
+    """Large A (config 4 path): one thread draws the raw words in stream order,
+    the Box-Muller transform and the column-major scatter run on `threads`
+    workers; the result is the sequential stream bit for bit (ragged last chunk)."""
+    from paper_2405_00366_b200 import cimcs as P
+    args = (3001, 0.7, 0.1, 0.01, 11)  # M = 2101 rows: 32 chunks of 64 + a ragged one
+    inst = P.gen_instances(args[0], [args[1:]], threads=threads)[0]
+    ref = O.gen_instance(*args)
+    assert np.array_equal(inst.A, ref.A) and np.array_equal(inst.y, ref.y)
+    assert np.array_equal(inst.x_true, ref.x_true) and np.array_equal(inst.xi_true, ref.xi_true)
