@@ -398,6 +398,117 @@ int orc_mfz_step(int N, const double* c_in, const double* e_in, double p, const 
     return -1;
 }
 
+/* ============================================================ Positive-P */
+/* measured_amplitude solver_pp.cpp:22-29: mu + sqrt(g2/(4 j dt)) w */
+int orc_measured_amplitude(int N, const double* mu, const double* noise, const orc_hyper* h,
+                           double* mt) {
+    if (!(h->j > 0.0)) return 2;
+    const double scale = sqrt(h->g2 / (4.0 * h->j * h->dt));
+    for (int r = 0; r < N; ++r) mt[r] = mu[r] + scale * noise[r];
+    return 0;
+}
+
+/* local_field_pp solver_pp.cpp:31-38: w = (R*0.5)*(mt + rt); h = J w + rt*hz */
+void orc_local_field_pp(const orc_problem* p, const double* R, const double* mt, double tau,
+                        double* out) {
+    const int N = p->N;
+    const double rt = sqrt(tau);
+    double* w = (double*)malloc(sizeof(double) * (size_t)N);
+    for (int r = 0; r < N; ++r) w[r] = R[r] * 0.5 * (mt[r] + rt);
+    orc_coupling_apply(p, w, out);
+    for (int r = 0; r < N; ++r) out[r] = out[r] + rt * p->hz[r];
+    free(w);
+}
+
+/* pp_step solver_pp.cpp:45-98 (Euler-Maruyama, same association as the source) */
+int orc_pp_step(int N, const double* mu_in, const double* n_in, const double* m_in,
+                const double* e_in, double p, const orc_hyper* h, double eta, const double* R,
+                const double* hf, const double* noise, double* mu_o, double* n_o, double* m_o,
+                double* e_o) {
+    const double g2 = h->g2, j = h->j, dt = h->dt;
+    const double rt = sqrt(h->tau);
+    const double thresh = rt * eta * eta / 4.0;
+    const double sdt = sqrt(dt);
+    const double scale = sqrt(g2 / (4.0 * j * dt));
+    for (int r = 0; r < N; ++r) {
+        const double mu = mu_in[r], n = n_in[r], m = m_in[r], e = e_in[r];
+        const double mu2 = mu * mu;
+        const double mn2 = (m + n) * (m + n);
+        const double inj = h->K * j * e * (R[r] * hf[r] - thresh);
+        const double drift_mu = -(1.0 - p + j) * mu - mu * (mu2 + 2.0 * g2 * n + g2 * m) + inj;
+        const double diff_mu = sqrt(j * g2) * (m + n) * noise[r];
+        mu_o[r] = mu + dt * drift_mu + sdt * diff_mu;
+        n_o[r] = n + dt * (-2.0 * (1.0 + j) * n + 2.0 * p * m - 2.0 * mu2 * (2.0 * n + m) -
+                           j * mn2);
+        m_o[r] = m + dt * (-2.0 * (1.0 + j) * m + 2.0 * p * n - 2.0 * mu2 * (2.0 * m + n) + p -
+                           (mu2 + g2 * m) - j * mn2);
+        const double mt = mu + scale * noise[r];
+        e_o[r] = e + dt * (-h->beta * (mt * mt - h->tau) * e);
+        if (!isfinite(mu_o[r]) || !isfinite(n_o[r]) || !isfinite(m_o[r]) || !isfinite(e_o[r]))
+            return r;
+    }
+    return -1;
+}
+
+/* run_pp solver_pp.cpp:100-132 with init_pp :11-20 */
+int orc_run_pp(const orc_problem* p, const double* R, const orc_hyper* h, double eta,
+               orc_rng* rng, double* mu_out, double* n_out, double* m_out, double* e_out,
+               double* mt_out, int32_t* sigma_out, double* min_e, int* kind) {
+    if (orc_hyper_validate(h) || !(h->j > 0.0)) return -3;
+    const int N = p->N;
+    double* st = (double*)calloc((size_t)N * 8, sizeof(double));
+    double *mu = st, *n = st + N, *m = st + 2 * N, *e = st + 3 * N;
+    double *mu2 = st + 4 * N, *n2 = st + 5 * N, *m2 = st + 6 * N, *e2 = st + 7 * N;
+    double* mt = (double*)calloc((size_t)N, sizeof(double));
+    double* noise = (double*)malloc(sizeof(double) * (size_t)N);
+    double* hf = (double*)malloc(sizeof(double) * (size_t)N);
+    for (int r = 0; r < N; ++r) e[r] = 1.0;
+    double t = 0.0, me = 1.0;
+    const double T = (double)h->n_steps * h->dt;
+    int rc = -1;
+    if (kind) *kind = 0;
+    for (int step = 0; step < h->n_steps; ++step) {
+        const double pp = h->pump_kind == ORC_PUMP_LINEAR ? orc_pump_linear(t, h->pump_end, T)
+                                                          : orc_pump_sigmoid(t, h->p_thr, h->d);
+        for (int r = 0; r < N; ++r) noise[r] = orc_gauss(rng);
+        orc_measured_amplitude(N, mu, noise, h, mt);
+        orc_local_field_pp(p, R, mt, h->tau, hf);
+        rc = orc_pp_step(N, mu, n, m, e, pp, h, eta, R, hf, noise, mu2, n2, m2, e2);
+        if (rc != -1) break;
+        double* tmp;
+        tmp = mu; mu = mu2; mu2 = tmp;
+        tmp = n; n = n2; n2 = tmp;
+        tmp = m; m = m2; m2 = tmp;
+        tmp = e; e = e2; e2 = tmp;
+        t = t + h->dt;
+        double emin = e[0];
+        for (int r = 1; r < N; ++r)
+            if (e[r] < emin) emin = e[r];
+        me = emin < me ? emin : me;
+        for (int r = 0; r < N; ++r)
+            if (fabs(mu[r]) > h->mu_abort) {
+                rc = r;
+                if (kind) *kind = 1;
+                break;
+            }
+        if (rc != -1) break;
+    }
+    if (rc == -1) {
+        for (int r = 0; r < N; ++r) sigma_out[r] = mt[r] > 0.0 ? 1 : 0;
+        if (mu_out) memcpy(mu_out, mu, sizeof(double) * (size_t)N);
+        if (n_out) memcpy(n_out, n, sizeof(double) * (size_t)N);
+        if (m_out) memcpy(m_out, m, sizeof(double) * (size_t)N);
+        if (e_out) memcpy(e_out, e, sizeof(double) * (size_t)N);
+        if (mt_out) memcpy(mt_out, mt, sizeof(double) * (size_t)N);
+        if (min_e) *min_e = me;
+    }
+    free(st);
+    free(mt);
+    free(noise);
+    free(hf);
+    return rc;
+}
+
 /* run_mfz solver_mfz.cpp:90-124 with init_mfz :24-31 */
 int orc_run_mfz(const orc_problem* p, const double* R, const orc_hyper* h, double eta,
                 int backend, orc_rng* rng, double* c_out, double* e_out, int32_t* sigma_out,
@@ -734,8 +845,11 @@ static int alternating_impl(const orc_problem* p, int backend, const orc_hyper* 
         const double eta = orc_eta_schedule(i, h->eta_init, h->eta_end, h->velo);
         const double lambda = eta * eta / 2.0;
         double min_e;
-        const int frc = orc_run_mfz(p, R, h, eta, backend, rng, NULL, e, sig_new, &min_e, 0,
-                                    NULL, NULL, NULL, NULL, 0);
+        const int frc = backend == ORC_PP
+                            ? orc_run_pp(p, R, h, eta, rng, NULL, NULL, NULL, e, NULL, sig_new,
+                                         &min_e, NULL)
+                            : orc_run_mfz(p, R, h, eta, backend, rng, NULL, e, sig_new, &min_e, 0,
+                                          NULL, NULL, NULL, NULL, 0);
         if (frc >= 0) {
             *fail_alt = i;
             if (fail_index) *fail_index = frc;

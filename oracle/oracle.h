@@ -123,7 +123,23 @@ int orc_mfz_step(int N, const double* c, const double* e, double p, const orc_hy
                  double eta, const double* R, const double* hfield, double* c_out,
                  double* e_out);
 
-enum { ORC_MFZ_CN = 0, ORC_MFZ_BN = 1 }; /* == Backend::MfzCN / MfzBN, orchestrator.hpp:28 */
+enum { ORC_MFZ_CN = 0, ORC_MFZ_BN = 1, ORC_PP = 2 }; /* == Backend, orchestrator.hpp:28 */
+
+/* Positive-P SDE backend (solver_pp.cpp:9-132): measured_amplitude,
+ * local_field_pp, pp_step (mu, n, m, e from the pre-step state; returns -1 or
+ * the first spin with a non-finite value), run_pp (N deviates per step from
+ * rng; returns -1, the offending spin (non-finite: kind 0, |mu| > mu_abort:
+ * kind 1), -3 config_error). */
+int orc_measured_amplitude(int N, const double* mu, const double* noise, const orc_hyper* h,
+                           double* mt);
+void orc_local_field_pp(const orc_problem* p, const double* R, const double* mt, double tau,
+                        double* out);
+int orc_pp_step(int N, const double* mu, const double* n, const double* m, const double* e,
+                double p, const orc_hyper* h, double eta, const double* R, const double* hf,
+                const double* noise, double* mu_o, double* n_o, double* m_o, double* e_o);
+int orc_run_pp(const orc_problem* p, const double* R, const orc_hyper* h, double eta,
+               orc_rng* rng, double* mu_out, double* n_out, double* m_out, double* e_out,
+               double* mt_out, int32_t* sigma_out, double* min_e, int* kind);
 
 /* One CIM call (run_mfz).  c0 drawn from rng.  trace_* optional (NULL).
  * Returns -1 ok, >=0 offending spin index, -2 input_error, -3 config_error. */

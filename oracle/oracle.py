@@ -19,10 +19,10 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 LITERAL, CANON, EXPLICIT = 0, 1, 2
-MFZ_CN, MFZ_BN = 0, 1
+MFZ_CN, MFZ_BN, PP = 0, 1, 2
 CDP_JACOBI, CDP_CG = 0, 1
 PUMP_SIGMOID, PUMP_LINEAR = 0, 1
-BACKENDS = {"mfz-cn": MFZ_CN, "mfz-bn": MFZ_BN}
+BACKENDS = {"mfz-cn": MFZ_CN, "mfz-bn": MFZ_BN, "pp": PP}
 
 
 def build() -> str:
@@ -102,6 +102,10 @@ def lib():
         L.orc_mfz_step.argtypes = [i, vp, vp, d, vp, d, vp, vp, vp, vp]
         L.orc_run_mfz.argtypes = [vp, vp, vp, d, i, vp, vp, vp, vp, vp, i, vp, vp, vp, vp, i]
         L.orc_cdp_minimize.argtypes = [vp, vp, vp, i, vp, vp, vp]
+        L.orc_measured_amplitude.argtypes = [i, vp, vp, vp, vp]
+        L.orc_local_field_pp.argtypes = [vp, vp, vp, d, vp]
+        L.orc_pp_step.argtypes = [i, vp, vp, vp, vp, d, vp, d, vp, vp, vp, vp, vp, vp, vp]
+        L.orc_run_pp.argtypes = [vp, vp, vp, d, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         for f in ("orc_objective_at", "orc_hamiltonian_at"):
             getattr(L, f).restype = d
             getattr(L, f).argtypes = [vp, vp, vp, d]
@@ -377,6 +381,32 @@ class Problem:
             out["trace_e"] = te[:n].copy()
         return out
 
+    def local_field_pp(self, R, mt, tau):
+        """local_field_pp solver_pp.cpp:31-38."""
+        out = np.zeros(self.N)
+        lib().orc_local_field_pp(C.byref(self._p), _p(np.ascontiguousarray(R, np.float64)),
+                                 _p(np.ascontiguousarray(mt, np.float64)), tau, _p(out))
+        return out
+
+    def run_pp(self, R, hp: HyperParams, eta, rng: Rng):
+        """run_pp solver_pp.cpp:100-132.  Returns dict (raises DivergenceError)."""
+        R = np.ascontiguousarray(R, np.float64)
+        N = self.N
+        mu, n, m, e, mt = (np.zeros(N) for _ in range(5))
+        s = np.zeros(N, np.int32)
+        me = C.c_double()
+        kind = C.c_int(0)
+        h = hp.to_c()
+        rc = lib().orc_run_pp(C.byref(self._p), _p(R), C.byref(h), eta, rng.ptr, _p(mu), _p(n),
+                              _p(m), _p(e), _p(mt), _p(s), C.byref(me), C.byref(kind))
+        if rc == -3:
+            raise ConfigError("invalid hyper-parameters")
+        if rc >= 0:
+            if kind.value:
+                raise DivergenceError(f"run_pp: |mu| exceeded {hp.mu_abort:f} at spin {rc}", rc)
+            raise DivergenceError(f"pp_step: non-finite value at spin {rc}", rc)
+        return dict(mu=mu, n=n, m=m, e=e, mu_tilde=mt, sigma=s, min_e=me.value)
+
     def cdp(self, sigma, R_prev, method=CDP_JACOBI, hp: HyperParams | None = None):
         hp = hp or HyperParams()
         s = np.ascontiguousarray(sigma, np.int32)
@@ -424,7 +454,8 @@ class Problem:
              for r in hist[: nh.value]]
         res = dict(R=Rout, sigma=sout, history=H, failed=fa.value >= 0,
                    fail_alternation=fa.value, fail_index=fi.value,
-                   fail_reason=(f"mfz_step: non-finite amplitude at spin {fi.value}"
+                   fail_reason=((f"pp: divergence at spin {fi.value}" if backend == PP else
+                                 f"mfz_step: non-finite amplitude at spin {fi.value}")
                                 if fa.value >= 0 else ""))
         res["min_hamiltonian"] = min((r["hamiltonian"] for r in H), default=math.nan)
         res["final_rmse"] = H[-1]["rmse"] if H else math.nan
@@ -452,6 +483,32 @@ def mfz_step(c, e, p, hp: HyperParams, eta, R, h):
     if rc >= 0:
         raise DivergenceError(f"mfz_step: non-finite amplitude at spin {rc}", rc)
     return co, eo
+
+
+def measured_amplitude(mu, noise, hp: HyperParams):
+    """measured_amplitude solver_pp.cpp:22-29."""
+    mu = np.ascontiguousarray(mu, np.float64)
+    out = np.zeros_like(mu)
+    h = hp.to_c()
+    if lib().orc_measured_amplitude(len(mu), _p(mu), _p(np.ascontiguousarray(noise, np.float64)),
+                                    C.byref(h), _p(out)):
+        raise ConfigError("measured_amplitude: j must be positive")
+    return out
+
+
+def pp_step(mu, n, m, e, p, hp: HyperParams, eta, R, h, noise):
+    """pp_step solver_pp.cpp:45-98 -> (mu, n, m, e); raises DivergenceError."""
+    arrs = [np.ascontiguousarray(x, np.float64) for x in (mu, n, m, e, R, h, noise)]
+    N = len(arrs[0])
+    if any(len(x) != N for x in arrs):
+        raise InputError("pp_step: length mismatch")
+    outs = [np.zeros(N) for _ in range(4)]
+    hh = hp.to_c()
+    rc = lib().orc_pp_step(N, _p(arrs[0]), _p(arrs[1]), _p(arrs[2]), _p(arrs[3]), p, C.byref(hh),
+                           eta, _p(arrs[4]), _p(arrs[5]), _p(arrs[6]), *[_p(o) for o in outs])
+    if rc >= 0:
+        raise DivergenceError(f"pp_step: non-finite value at spin {rc}", rc)
+    return tuple(outs)
 
 
 def canon_dot(g, v, nseg=8, gran=8):
