@@ -29,7 +29,7 @@ extern "C" {
 enum { CIMCS_OK = 0, CIMCS_INPUT_ERROR = 1, CIMCS_CONFIG_ERROR = 2,
        CIMCS_DIVERGENCE = 3, CIMCS_CUDA_ERROR = 4 };
 enum { CIMCS_F32 = 0, CIMCS_F64 = 1 };
-/* == Backend {MfzCN, MfzBN, PositiveP}, orchestrator.hpp:28 (PositiveP: not on this path) */
+/* == Backend {MfzCN, MfzBN, PositiveP}, orchestrator.hpp:28 */
 enum { CIMCS_MFZ_CN = 0, CIMCS_MFZ_BN = 1, CIMCS_PP = 2 };
 /* == CdpMethod {Jacobi, ConjugateGradient}, cdp.hpp:60 */
 enum { CIMCS_CDP_JACOBI = 0, CIMCS_CDP_CG = 1 };
@@ -146,6 +146,17 @@ int cimcs_run_cim(cimcs_ctx* ctx, int32_t R, int32_t backend, const cimcs_hyper*
                   double eta, const double* Rsig, const double* c0, double* c_out,
                   double* e_out, int32_t* sigma_out, double* min_e, int32_t* fail_index);
 
+/* One Positive-P CIM call (run_pp, solver_pp.cpp:100-132; backend
+ * Backend::PositiveP) for all B x R trajectories.  seeds[b*R+r] seeds the
+ * trajectory's reference stream (N unit normals per step, drawn on the host
+ * bit-exactly and streamed to the device).  Outputs: final mu, e, the last
+ * measured amplitude mu~ and sigma = [mu~ > 0].  fp64 contexts or fp32 with
+ * tensor_cores = 0 (config_error otherwise).  Returns 3 on divergence
+ * (non-finite value or |mu| > mu_abort; fail_index = offending spin). */
+int cimcs_run_pp(cimcs_ctx* ctx, int32_t R, const cimcs_hyper* hp, double eta,
+                 const double* Rsig, const uint64_t* seeds, double* mu_out, double* e_out,
+                 double* mt_out, int32_t* sigma_out, double* min_e, int32_t* fail_index);
+
 /* Masked refit on each trajectory's support: cdp_minimize with damped
  * Jacobi (cdp.cpp:48-64, 132-139).  Entries with sigma = 0 are returned
  * bitwise untouched.  Singular active diagonal -> input_error. */
@@ -174,7 +185,8 @@ int cimcs_score(cimcs_ctx* ctx, int32_t R, const double* Rsig, const int32_t* si
  * supplies N normals per alternation for c0.  hist holds (velo+1)*B*R
  * records, trajectory-major; n_hist[b*R+r] = recorded alternations;
  * fail_alt = alternation that diverged or -1 (AlternatingResult::failed,
- * orchestrator.hpp:113-124).  cdp: CIMCS_CDP_JACOBI or CIMCS_CDP_CG. */
+ * orchestrator.hpp:113-124).  cdp: CIMCS_CDP_JACOBI or CIMCS_CDP_CG.
+ * backend CIMCS_PP runs run_pp per alternation (see cimcs_run_pp). */
 int cimcs_solve(cimcs_ctx* ctx, int32_t R, int32_t backend, const cimcs_hyper* hp,
                 int32_t cdp, const uint64_t* seeds, const double* R_init,
                 int32_t track_best, double* R_out, int32_t* sigma_out,

@@ -24,7 +24,7 @@ EXPORTS = (
     "cimcs_mix_seed", "cimcs_gemv_order", "cimcs_gen_dims", "cimcs_gen_instance",
     "cimcs_gen_instances", "cimcs_create", "cimcs_destroy", "cimcs_set_option",
     "cimcs_set_problems", "cimcs_build_coupling", "cimcs_get_coupling", "cimcs_mfz_step",
-    "cimcs_run_cim", "cimcs_refit", "cimcs_cdp_minimize", "cimcs_score", "cimcs_solve", "cimcs_get_timing",
+    "cimcs_run_cim", "cimcs_run_pp", "cimcs_refit", "cimcs_cdp_minimize", "cimcs_score", "cimcs_solve", "cimcs_get_timing",
     "cimcs_nccl_unique_id", "cimcs_create_sharded",
 )
 
@@ -90,6 +90,7 @@ def load() -> C.CDLL:
     L.cimcs_mfz_step.argtypes = [vp, i32, i32, vp, d, d, vp, vp, vp, vp, vp, vp, vp]
     L.cimcs_run_cim.argtypes = [vp, i32, i32, vp, d, vp, vp, vp, vp, vp, vp, vp]
     L.cimcs_refit.argtypes = [vp, i32, vp, vp, vp, vp]
+    L.cimcs_run_pp.argtypes = [vp, i32, vp, C.c_double, vp, vp, vp, vp, vp, vp, vp, vp]
     L.cimcs_cdp_minimize.argtypes = [vp, i32, vp, vp, i32, vp, vp, vp]
     L.cimcs_score.argtypes = [vp, i32, vp, vp, d, vp, vp, vp]
     L.cimcs_solve.argtypes = [vp, i32, i32, vp, i32, vp, vp, i32, vp, vp, vp, vp, vp, vp]

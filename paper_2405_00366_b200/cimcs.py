@@ -26,7 +26,7 @@ import numpy as np
 from . import _lib
 from ._lib import load
 
-BACKENDS = {"mfz-cn": _lib.MFZ_CN, "mfz-bn": _lib.MFZ_BN}
+BACKENDS = {"mfz-cn": _lib.MFZ_CN, "mfz-bn": _lib.MFZ_BN, "pp": _lib.PP}
 DTYPES = {"f32": _lib.F32, "fp32": _lib.F32, "float32": _lib.F32,
           "f64": _lib.F64, "fp64": _lib.F64, "float64": _lib.F64}
 
@@ -310,6 +310,23 @@ class Context:
             _check(rc)
         return dict(c=co, e=eo, sigma=so, min_e=me, fail_index=fi)
 
+    def run_pp(self, R: int, hp: HyperParams, eta: float, Rsig, seeds):
+        """run_pp (solver_pp.cpp:100-132) for every trajectory from its stream seed."""
+        B, N = self.B, self.N
+        Rs = _traj(Rsig, B, R, N)
+        sd = np.ascontiguousarray(seeds, np.uint64).reshape(B * R)
+        mu, e, mt = (np.zeros((B, R, N)) for _ in range(3))
+        so = np.zeros((B, R, N), np.int32)
+        me = np.zeros((B, R))
+        fi = np.zeros((B, R), np.int32)
+        h = hp.to_c()
+        rc = self._lib.cimcs_run_pp(self._ctx, R, C.byref(h), eta, Rs.ctypes.data, sd.ctypes.data,
+                                    mu.ctypes.data, e.ctypes.data, mt.ctypes.data, so.ctypes.data,
+                                    me.ctypes.data, fi.ctypes.data)
+        if rc not in (_lib.OK, _lib.DIVERGENCE):
+            _check(rc)
+        return dict(mu=mu, e=e, mu_tilde=mt, sigma=so, min_e=me, fail_index=fi)
+
     def refit(self, R: int, sigma, R_prev, hp: HyperParams | None = None,
               cdp: str = "jacobi", return_iterations: bool = False):
         """cdp_minimize (cdp.cpp:132-139) of every trajectory on its support:
@@ -363,7 +380,8 @@ class Context:
             ("i", np.int32), ("support", np.int32), ("eta", np.float64),
             ("hamiltonian", np.float64), ("rmse", np.float64), ("hamming", np.float64),
             ("min_e", np.float64), ("median_e", np.float64)])).reshape(B, R, nalt).copy()
-        return dict(R=Ro, sigma=So, history=H, n_hist=nh, fail_alt=fa, fail_index=fi)
+        return dict(R=Ro, sigma=So, history=H, n_hist=nh, fail_alt=fa, fail_index=fi,
+                    backend=backend)
 
     def timing(self) -> dict:
         t = _lib.Timing()
@@ -381,7 +399,9 @@ def _trial_dict(res, b, r, n_steps):
                  support=int(h["support"])) for h in H]
     failed = int(res["fail_alt"][b, r]) >= 0
     out = dict(R=res["R"][b, r].copy(), sigma=res["sigma"][b, r].copy(), failed=failed,
-               fail_reason=(f"mfz_step: non-finite amplitude at spin {int(res['fail_index'][b, r])}"
+               fail_reason=((f"pp: divergence at spin {int(res['fail_index'][b, r])}"
+                             if res.get("backend") == "pp" else
+                             f"mfz_step: non-finite amplitude at spin {int(res['fail_index'][b, r])}")
                             if failed else ""),
                fail_alternation=int(res["fail_alt"][b, r]), history=hist)
     out["min_hamiltonian"] = min((h["hamiltonian"] for h in hist), default=math.nan)

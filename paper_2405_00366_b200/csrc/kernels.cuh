@@ -58,18 +58,23 @@ __host__ __device__ constexpr size_t gemv_smem_bytes() {
 }
 
 // Mode of the fused epilogue that follows the G*v contraction.
-enum : int { EPI_STEP_BN = 1, EPI_STEP_CN = 0, EPI_JACOBI = 2, EPI_SCORE = 3, EPI_MATVEC = 4 };
+enum : int { EPI_STEP_BN = 1, EPI_STEP_CN = 0, EPI_JACOBI = 2, EPI_SCORE = 3, EPI_MATVEC = 4,
+             EPI_STEP_PP = 5 };
 
 // Per-call scalars (host-computed in fp64 exactly as the reference does).
 struct StepScalars {
     double dt, half_rt, rt, tau, nbeta, Kj, loss_off, minus_j;  // loss = (-1+p) [- j]
     double one_minus_dtc, dt_c;
+    // Positive-P (solver_pp.cpp:45-98), host-computed in fp64
+    double g2, j, pp_scale, pp_sdt, pp_sjg, pp_m2j, mu_abort;  // sqrt(g2/(4 j dt)), sqrt(dt),
+                                                                // sqrt(j g2), -2 (1 + j)
     int n_steps;
 };
 
 // Per-alternation values read by graph-captured kernels from device memory.
 struct AltParams {
     double thresh;     // ((eta*eta)/4.0)*rt
+    double thresh_pp;  // ((rt*eta)*eta)/4.0  (solver_pp.cpp:59)
     double lambda;     // (eta*eta)/2.0
     double eta;
     int alt;           // alternation index
@@ -87,6 +92,11 @@ struct GemvArgs {
     void* E;
     void* Hdbg;          // optional local-field dump [B][ldN][NR]
     double* Mv;          // EPI_MATVEC output G*v [B][ldN][NR] (CG refit)
+    void* Pn;            // Positive-P moments n, m and the measured amplitude [B][ldN][NR]
+    void* Pm;
+    void* MT;
+    const double* nz;    // this step's unit normals [B][ldN][NR] (host stream)
+    const double* nz_next;  // the next step's (contraction input of the next launch)
     const int8_t* sigma; // [B][ldN][NR]  (Jacobi / score)
     int* fail_gstep;     // [B*NR]
     int* fail_idx;       // [B*NR]
@@ -300,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<T>::kMinBlocks) gemv_fused_kerne
     if (threadIdx.x < NR) {
         const int g = a.fail_gstep ? a.fail_gstep[b * NR + threadIdx.x] : kFreeTraj;
         int frozen;
-        if (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN)
+        if (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN || MODE == EPI_STEP_PP)
             frozen = g < a.alt->gstep_base + a.step;  // failed at an earlier step
         else
             frozen = g != kFreeTraj;
@@ -456,6 +466,62 @@ __global__ void __launch_bounds__(kThreads, Cfg<T>::kMinBlocks) gemv_fused_kerne
             Wo[vi] = wn;
             local_min = en < local_min ? en : local_min;
         }
+    } else if constexpr (MODE == EPI_STEP_PP) {
+        // pp_step solver_pp.cpp:45-98 with h = (D∘w - G w) + rt*hz (local_field_pp :31-38);
+        // then the next contraction input w' = (R*0.5)*(mu~' + rt), mu~' = mu' + scale*w_{k+1}
+        T* __restrict__ Mu = static_cast<T*>(a.C);
+        T* __restrict__ Ep = static_cast<T*>(a.E);
+        T* __restrict__ Np = static_cast<T*>(a.Pn);
+        T* __restrict__ Mp = static_cast<T*>(a.Pm);
+        T* __restrict__ MTp = static_cast<T*>(a.MT);
+        const T* __restrict__ Wp = static_cast<const T*>(a.Win);
+        T* __restrict__ Wo = static_cast<T*>(a.Wout);
+        const double pd = a.pump ? a.pump[a.step] : a.p_scalar;
+        const T p = (T)pd, dt = (T)sc.dt, rt = (T)sc.rt, tau = (T)sc.tau, nbeta = (T)sc.nbeta;
+        const T g2 = (T)sc.g2, jj = (T)sc.j, Kj = (T)sc.Kj, m2j = (T)sc.pp_m2j;
+        const T scale = (T)sc.pp_scale, sdt = (T)sc.pp_sdt, sjg = (T)sc.pp_sjg;
+        const T thresh = (T)a.alt->thresh_pp, mu_abort = (T)sc.mu_abort;
+        const T q1 = -((T(1) - p) + jj);  // -(1.0 - p + j)
+#pragma unroll
+        for (int k = 0; k < OPT; ++k) {
+            if (!ok[k]) continue;
+            const size_t vi = ((size_t)b * ldN + iv[k]) * NR + q;
+            const size_t si = (size_t)b * ldN + iv[k];
+            const T w = Wp[vi], Dv = static_cast<const T*>(a.D)[si];
+            const T hzv = static_cast<const T*>(a.hz)[si], Rv = static_cast<const T*>(a.Rs)[vi];
+            const T h = (Dv * w - gwv[k]) + rt * hzv;
+            const T mu = Mu[vi], n = Np[vi], m = Mp[vi], e = Ep[vi];
+            const T nzk = (T)a.nz[vi];
+            const T mu2 = mu * mu;
+            const T mn2 = (m + n) * (m + n);
+            const T inj = (Kj * e) * (Rv * h - thresh);
+            const T drift = q1 * mu - mu * (mu2 + T(2) * g2 * n + g2 * m) + inj;
+            const T diff = sjg * (m + n) * nzk;
+            const T mun = mu + dt * drift + sdt * diff;
+            const T nn = n + dt * (m2j * n + T(2) * p * m - T(2) * mu2 * (T(2) * n + m) - jj * mn2);
+            const T mm = m + dt * (m2j * m + T(2) * p * n - T(2) * mu2 * (T(2) * m + n) + p -
+                                   (mu2 + g2 * m) - jj * mn2);
+            const T mt = mu + scale * nzk;
+            const T en = e + dt * ((nbeta * (mt * mt - tau)) * e);
+            const int traj = b * NR + q;
+            if (!finite_(mun) || !finite_(nn) || !finite_(mm) || !finite_(en)) {
+                atomicMin(&a.fail_gstep[traj], a.alt->gstep_base + a.step);
+                atomicMin(&a.fail_idx[traj], iv[k]);  // kind 0: non-finite (pp_step)
+                continue;
+            }
+            Mu[vi] = mun;
+            Np[vi] = nn;
+            Mp[vi] = mm;
+            Ep[vi] = en;
+            MTp[vi] = mt;  // the last step's measured amplitude gives sigma (run_pp :128)
+            local_min = en < local_min ? en : local_min;
+            if (fabs((double)mun) > (double)mu_abort) {  // run_pp :119-124, kind 1
+                atomicMin(&a.fail_gstep[traj], a.alt->gstep_base + a.step);
+                atomicMin(&a.fail_idx[traj], (1 << 30) + iv[k]);
+            }
+            const T mtn = mun + scale * (T)a.nz_next[vi];
+            Wo[vi] = (Rv * T(0.5)) * (mtn + rt);
+        }
     } else if constexpr (MODE == EPI_JACOBI) {
         // cdp.cpp:60-61: offdiag = G R - D∘R; R = (1-dt_c) R + dt_c (b - offdiag) / D
         T* __restrict__ Rp = static_cast<T*>(a.Rs);
@@ -514,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<T>::kMinBlocks) gemv_fused_kerne
         }
     }
 
-    if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
+    if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN || MODE == EPI_STEP_PP) {
         // per-replica min of e over this CTA, then one atomic per replica
         unsigned long long k = ord_key(local_min);
 #pragma unroll
@@ -736,6 +802,38 @@ __global__ void convert_kernel(const double* __restrict__ src, T* __restrict__ d
 // ------------------------------------------------------- state kernels
 // init_mfz (solver_mfz.cpp:24-31) + first contraction input.  c0 host
 // layout [b][r][i] (fp64); device [b][i][r].
+// init_pp (solver_pp.cpp:11-20): vacuum mu = n = m = 0, e = 1; first contraction
+// input w = (R*0.5)*(mu~ + rt) with mu~ = 0 + scale * w_0.
+template <typename T, int NR>
+__global__ void init_pp_kernel(int Rreal, int N, int ldN, int B, const T* __restrict__ Rs, T* C,
+                               T* E, T* Pn, T* Pm, T* MT, T* W, const int* fail_gstep,
+                               unsigned long long* minE, const double* __restrict__ nz0,
+                               double scale, double rt) {
+    const size_t total = (size_t)B * ldN * NR;
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < total;
+         k += (size_t)gridDim.x * blockDim.x) {
+        const int q = k % NR;
+        const size_t bi = k / NR;
+        const int i = bi % ldN;
+        const int b = bi / ldN;
+        const int traj = b * NR + q;
+        if (i == 0) minE[traj] = ord_key(T(1));
+        if (fail_gstep[traj] != kFreeTraj) continue;
+        C[k] = T(0);
+        Pn[k] = T(0);
+        Pm[k] = T(0);
+        E[k] = T(1);
+        if (i >= N || q >= Rreal) {
+            MT[k] = T(0);
+            W[k] = T(0);
+            continue;
+        }
+        const T mt = T(0) + (T)scale * (T)nz0[k];
+        MT[k] = mt;
+        W[k] = (Rs[k] * T(0.5)) * (mt + (T)rt);
+    }
+}
+
 template <typename T, int NR, int BN>
 __global__ void init_state_kernel(const double* __restrict__ c0, int Rreal, int N, int ldN,
                                   int B, const T* __restrict__ Rs, T* C, T* E, T* W,

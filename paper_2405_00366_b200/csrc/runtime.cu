@@ -370,6 +370,11 @@ struct cimcs_ctx {
     int pump_cap = 0;
     DevRecord* hist = nullptr;
     int hist_cap = 0;
+    // Positive-P state (allocated on first use): moments n, m, measured amplitude,
+    // unit normals in chunks of kPpChunk steps (device and pinned, double buffered)
+    void *Pn = nullptr, *Pm = nullptr, *MT = nullptr;
+    double *nzd[2] = {nullptr, nullptr}, *nzh[2] = {nullptr, nullptr};
+    size_t nz_elems = 0;
     // conjugate-gradient refit state (allocated on first use)
     double *cgX = nullptr, *cgR = nullptr, *cgP = nullptr, *cgGp = nullptr;
     int* cg_act = nullptr;
@@ -400,12 +405,21 @@ void free_state(cimcs_ctx* c) {
                     c->bestR, c->sig,    c->bestS,      c->fail_gstep, c->fail_idx, c->n_hist,
                     c->improved, c->minE, c->part,      c->best_obj, c->obj, c->rmse, c->ham,
                     c->tp, c->fail_tmp, c->cgX, c->cgR, c->cgP, c->cgGp, c->cg_act,
-                    c->cg_st, c->cg_live, c->WB0, c->WB1, c->WS0, c->WS1};
+                    c->cg_st, c->cg_live, c->WB0, c->WB1, c->WS0, c->WS1, c->Pn, c->Pm,
+                    c->MT, c->nzd[0], c->nzd[1]};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     c->cgX = c->cgR = c->cgP = c->cgGp = nullptr;
     c->WB0 = c->WB1 = nullptr;
     c->WS0 = c->WS1 = nullptr;
+    c->Pn = c->Pm = c->MT = nullptr;
+    c->nzd[0] = c->nzd[1] = nullptr;
+    for (double*& h : c->nzh)
+        if (h) {
+            cudaFreeHost(h);
+            h = nullptr;
+        }
+    c->nz_elems = 0;
     c->cg_act = c->cg_live = nullptr;
     c->cg_st = nullptr;
     c->Rs = c->C = c->E = c->W0 = c->W1 = c->Hdbg = c->bestR = nullptr;
@@ -519,6 +533,13 @@ StepScalars make_scalars(const cimcs_hyper* hp) {
     s.minus_j = hp->mfz_loss_minus_j ? hp->j : 0.0;
     s.one_minus_dtc = 1.0 - hp->dt_c;
     s.dt_c = hp->dt_c;
+    s.g2 = hp->g2;
+    s.j = hp->j;
+    s.pp_scale = std::sqrt(hp->g2 / (4.0 * hp->j * hp->dt));  // solver_pp.cpp:27
+    s.pp_sdt = std::sqrt(hp->dt);
+    s.pp_sjg = std::sqrt(hp->j * hp->g2);
+    s.pp_m2j = -2.0 * (1.0 + hp->j);
+    s.mu_abort = hp->mu_abort;
     s.n_steps = hp->n_steps;
     return s;
 }
@@ -527,6 +548,7 @@ AltParams make_alt(const cimcs_hyper* hp, double eta, int alt) {
     AltParams a{};
     const double rt = std::sqrt(hp->tau);
     a.thresh = eta * eta / 4.0 * rt;  // solver_mfz.cpp:69
+    a.thresh_pp = rt * eta * eta / 4.0;  // solver_pp.cpp:59
     a.lambda = eta * eta / 2.0;       // orchestrator.cpp:189
     a.eta = eta;
     a.alt = alt;
@@ -576,6 +598,7 @@ int launch_gemv_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
         case EPI_STEP_CN: return launch_gemv_t<T, NR, EPI_STEP_CN>(c, a);
         case EPI_JACOBI: return launch_gemv_t<T, NR, EPI_JACOBI>(c, a);
         case EPI_MATVEC: return launch_gemv_t<T, NR, EPI_MATVEC>(c, a);
+        case EPI_STEP_PP: return launch_gemv_t<T, NR, EPI_STEP_PP>(c, a);
         default: return launch_gemv_t<T, NR, EPI_SCORE>(c, a);
     }
 }
@@ -1476,6 +1499,140 @@ struct Events {
     }
 };
 
+// ------------------------------------------------------ Positive-P backend
+constexpr int kPpChunk = 64;  // steps of unit normals per host -> device chunk
+
+int ensure_pp(cimcs_ctx* c) {  // outside any capture
+    if (c->tc)
+        return fail(CIMCS_CONFIG_ERROR,
+                    "pp backend: use an fp64 context or tensor_cores=0 (the tcgen05 epilogues "
+                    "implement the MFZ update only)");
+    if (c->world > 1)
+        return fail(CIMCS_CONFIG_ERROR, "pp backend is not supported on row-sharded contexts");
+    const size_t n = c->state_elems();
+    if (!c->Pn) {
+        int rc;
+        if ((rc = dalloc(&c->Pn, n * c->elt())) || (rc = dalloc(&c->Pm, n * c->elt())) ||
+            (rc = dalloc(&c->MT, n * c->elt())))
+            return rc;
+    }
+    const size_t nz = (size_t)kPpChunk * n;
+    if (c->nz_elems < nz) {
+        for (int k = 0; k < 2; ++k) {
+            if (c->nzd[k]) cudaFree(c->nzd[k]);
+            if (c->nzh[k]) cudaFreeHost(c->nzh[k]);
+            c->nzd[k] = c->nzh[k] = nullptr;
+        }
+        for (int k = 0; k < 2; ++k) {
+            if (int rc = dalloc(&c->nzd[k], nz * 8)) return rc;
+            CK(cudaMallocHost(&c->nzh[k], nz * 8));
+            std::memset(c->nzh[k], 0, nz * 8);  // padded slots stay zero
+        }
+        c->nz_elems = nz;
+    }
+    return 0;
+}
+
+// kc steps of unit normals per trajectory (make_noise_draw, solver_pp.cpp:9: N
+// deviates per step from the trial stream), device layout [kc][B][ldN][NR]
+void gen_noise(cimcs_ctx* c, std::vector<HostRng>& rngs, int Rreal, int kc, double* out) {
+    const int nt = (int)rngs.size();
+    const size_t S = c->state_elems();
+    auto work = [&](int t0, int t1) {
+        for (int t = t0; t < t1; ++t) {
+            const int b = t / Rreal, r = t % Rreal;
+            for (int k = 0; k < kc; ++k) {
+                double* o = out + (size_t)k * S + ((size_t)b * c->ldN) * c->NR + r;
+                for (int i = 0; i < c->N; ++i) o[(size_t)i * c->NR] = rngs[t].gauss();
+            }
+        }
+    };
+    const int threads = std::max(1, std::min(c->host_threads, nt));
+    if (threads == 1) {
+        work(0, nt);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const int per = (nt + threads - 1) / threads;
+    for (int k = 0; k < threads; ++k) {
+        const int t0 = k * per, t1 = std::min(nt, t0 + per);
+        if (t0 < t1) pool.emplace_back(work, t0, t1);
+    }
+    for (auto& th : pool) th.join();
+}
+
+template <typename T>
+int pp_init_T(cimcs_ctx* c, int Rreal, const double* nz0, const StepScalars& s) {
+    const int g = grid_for(c->state_elems());
+    DISPATCH_NR(c->NR, {
+        init_pp_kernel<T, NR_><<<g, 256, 0, c->stream>>>(
+            Rreal, c->N, c->ldN, c->B, static_cast<const T*>(c->Rs), static_cast<T*>(c->C),
+            static_cast<T*>(c->E), static_cast<T*>(c->Pn), static_cast<T*>(c->Pm),
+            static_cast<T*>(c->MT), static_cast<T*>(c->W0), c->fail_gstep, c->minE, nz0,
+            s.pp_scale, s.rt);
+    });
+    CK(cudaGetLastError());
+    return 0;
+}
+
+// One Positive-P CIM call (run_pp, solver_pp.cpp:100-132) for all trajectories.
+// The unit normals are drawn on the host from each trajectory's reference
+// stream (bit-exact) and uploaded in chunks of kPpChunk steps while the GPU
+// integrates the previous chunk.  Host-driven (not captured).  Afterwards C
+// holds mu and MT the last measured amplitude (the sigma source, run_pp :126-129).
+int run_pp_cim(cimcs_ctx* c, int Rreal, const StepScalars& s, const cimcs_hyper* hp,
+               std::vector<HostRng>& rngs) {
+    const int n_steps = hp->n_steps, K = std::min(kPpChunk, n_steps);
+    const int nch = (n_steps + K - 1) / K;
+    const size_t S = c->state_elems();
+    Events cp(2);
+    auto stage = [&](int ch) -> int {
+        const int sl = ch & 1, kc = std::min(K, n_steps - ch * K);
+        gen_noise(c, rngs, Rreal, kc, c->nzh[sl]);
+        CK(cudaMemcpyAsync(c->nzd[sl], c->nzh[sl], (size_t)kc * S * 8, cudaMemcpyHostToDevice,
+                           c->stream));
+        CK(cudaEventRecord(cp.ev[sl], c->stream));
+        return 0;
+    };
+    int rc = stage(0);
+    if (!rc && nch > 1) rc = stage(1);
+    if (!rc)
+        rc = c->dtype == CIMCS_F64 ? pp_init_T<double>(c, Rreal, c->nzd[0], s)
+                                   : pp_init_T<float>(c, Rreal, c->nzd[0], s);
+    GemvArgs a = base_args(c, s);
+    a.pump = c->pump;
+    a.Hdbg = nullptr;
+    a.Pn = c->Pn;
+    a.Pm = c->Pm;
+    a.MT = c->MT;
+    for (int ch = 0; ch < nch && !rc; ++ch) {
+        const int k0 = ch * K, kc = std::min(K, n_steps - k0);
+        for (int k = k0; k < k0 + kc && !rc; ++k) {
+            a.step = k;
+            a.Win = (k & 1) ? c->W1 : c->W0;
+            a.Wout = (k & 1) ? c->W0 : c->W1;
+            a.nz = c->nzd[ch & 1] + (size_t)(k - k0) * S;
+            a.nz_next = k + 1 >= n_steps ? a.nz
+                        : k + 1 < k0 + kc ? a.nz + S
+                                          : c->nzd[(ch + 1) & 1];
+            rc = launch_gemv(c, EPI_STEP_PP, a);
+        }
+        if (!rc && ch + 2 < nch) {
+            CK(cudaEventSynchronize(cp.ev[ch & 1]));  // its pinned slot has been copied
+            rc = stage(ch + 2);
+        }
+    }
+    return rc;
+}
+
+// C = the measured amplitude (CimCallResult::amplitude of the PP backend), so the
+// support / refit path (support_kernel: sigma = C > 0) serves both backends
+int pp_amplitude_to_c(cimcs_ctx* c) {
+    CK(cudaMemcpyAsync(c->C, c->MT, c->state_elems() * c->elt(), cudaMemcpyDeviceToDevice,
+                       c->stream));
+    return 0;
+}
+
 }  // namespace
 
 // =================================================================== C ABI
@@ -1975,6 +2132,60 @@ int cimcs_mfz_step(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* 
     return div ? fail(CIMCS_DIVERGENCE, "mfz_step: non-finite amplitude") : 0;
 }
 
+int cimcs_run_pp(cimcs_ctx* c, int32_t R, const cimcs_hyper* hp, double eta, const double* Rsig,
+                 const uint64_t* seeds, double* mu_out, double* e_out, double* mt_out,
+                 int32_t* sigma_out, double* min_e, int32_t* fail_index) {
+    if (int rc = check_ready(c, R)) return rc;
+    if (int rc = validate(hp)) return rc;
+    if (!(hp->j > 0.0)) return fail(CIMCS_CONFIG_ERROR, "measured_amplitude: j must be positive");
+    if (!seeds) return fail(CIMCS_INPUT_ERROR, "null seeds");
+    CK(cudaSetDevice(c->device));
+    if (int rc = ensure_state(c, slots_for(c, R))) return rc;
+    if (int rc = ensure_pp(c)) return rc;
+    if (int rc = upload_pump(c, hp)) return rc;
+    if (int rc = reset_flags(c, R)) return rc;
+    if (int rc = set_alt(c, make_alt(hp, eta, 0))) return rc;
+    if (int rc = upload_traj(c, Rsig, c->Rs, R)) return rc;
+    std::vector<HostRng> rngs;
+    for (int t = 0; t < c->B * R; ++t) rngs.emplace_back(seeds[t]);
+    const StepScalars s = make_scalars(hp);
+    Events ev(2);
+    cudaEventRecord(ev.ev[0], c->stream);
+    int rc = run_pp_cim(c, R, s, hp, rngs);
+    cudaEventRecord(ev.ev[1], c->stream);
+    if (!rc && mu_out) rc = download_traj(c, c->C, mu_out, R);
+    if (!rc) rc = pp_amplitude_to_c(c);
+    if (!rc) rc = run_support(c);  // sigma = mu~ > 0
+    if (!rc && mt_out) rc = download_traj(c, c->C, mt_out, R);
+    if (!rc && e_out) rc = download_traj(c, c->E, e_out, R);
+    if (!rc && sigma_out) rc = download_sig(c, c->sig, sigma_out, R);
+    std::vector<int> fi(c->B * c->NR);
+    std::vector<unsigned long long> me(c->B * c->NR);
+    if (!rc) {
+        cudaMemcpyAsync(fi.data(), c->fail_idx, fi.size() * 4, cudaMemcpyDeviceToHost, c->stream);
+        cudaMemcpyAsync(me.data(), c->minE, me.size() * 8, cudaMemcpyDeviceToHost, c->stream);
+    }
+    cudaError_t se = cudaStreamSynchronize(c->stream);
+    if (rc) return rc;
+    if (se != cudaSuccess) return fail(CIMCS_CUDA_ERROR, cudaGetErrorString(se));
+    c->timing.cim_ms = ev.ms(0, 1);
+    c->timing.step_launches = hp->n_steps;
+    bool div = false;
+    int kind = 0;
+    for (int b = 0; b < c->B; ++b)
+        for (int r = 0; r < R; ++r) {
+            const int v = fi[b * c->NR + r];
+            const bool f = v != INT_MAX;
+            if (fail_index) fail_index[b * R + r] = f ? (v & ((1 << 30) - 1)) : -1;
+            if (min_e) min_e[b * R + r] = ord_val(me[b * c->NR + r]);
+            if (f && !div) kind = v >> 30;
+            div |= f;
+        }
+    return div ? fail(CIMCS_DIVERGENCE, kind ? "run_pp: |mu| exceeded mu_abort"
+                                             : "pp_step: non-finite value")
+               : 0;
+}
+
 int cimcs_run_cim(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp, double eta,
                   const double* Rsig, const double* c0, double* c_out, double* e_out,
                   int32_t* sigma_out, double* min_e, int32_t* fail_index) {
@@ -2120,8 +2331,11 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
                 int32_t* fail_index) {
     if (int rc = check_ready(c, R)) return rc;
     if (int rc = validate(hp)) return rc;
-    if (backend != CIMCS_MFZ_BN && backend != CIMCS_MFZ_CN)
-        return fail(CIMCS_CONFIG_ERROR, "backend must be mfz-bn or mfz-cn");
+    if (backend != CIMCS_MFZ_BN && backend != CIMCS_MFZ_CN && backend != CIMCS_PP)
+        return fail(CIMCS_CONFIG_ERROR, "backend must be mfz-bn, mfz-cn or pp");
+    const bool pp = backend == CIMCS_PP;
+    if (pp && !(hp->j > 0.0))
+        return fail(CIMCS_CONFIG_ERROR, "measured_amplitude: j must be positive");
     if (cdp != CIMCS_CDP_JACOBI && cdp != CIMCS_CDP_CG)
         return fail(CIMCS_CONFIG_ERROR, "cdp must be jacobi or cg");
     if (cdp == CIMCS_CDP_CG && c->world > 1)
@@ -2132,6 +2346,8 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
     if (int rc = ensure_state(c, NR)) return rc;
     if (cdp == CIMCS_CDP_CG)
         if (int rc = ensure_cg(c)) return rc;
+    if (pp)
+        if (int rc = ensure_pp(c)) return rc;
     if (int rc = upload_pump(c, hp)) return rc;
     const int nalt = hp->velo + 1;
     const int nT = c->B * NR;
@@ -2214,14 +2430,15 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
                                             (long long)(uintptr_t)dc0, bits(s.dt), bits(s.rt),
                                             bits(s.nbeta), bits(s.Kj), bits(s.minus_j),
                                             bits(s.dt_c), c->B, c->N, cdp, hp->cg_max_iters,
-                                            bits(hp->cg_tol)};
-        if (key != c->graph_key || !c->g_cim || !c->g_refit) {
+                                            bits(hp->cg_tol), backend};
+        if (key != c->graph_key || (!pp && !c->g_cim) || !c->g_refit) {
             drop_graphs(c);
             Graph gc, gr;
-            rc = capture(c, gc, [&] {
-                int r2 = run_init(c, R, bn, dc0, nullptr, s.rt);
-                return r2 ? r2 : enqueue_steps(c, bn, s, hp->n_steps);
-            });
+            if (!pp)  // the Positive-P CIM call is host-driven (chunked noise upload)
+                rc = capture(c, gc, [&] {
+                    int r2 = run_init(c, R, bn, dc0, nullptr, s.rt);
+                    return r2 ? r2 : enqueue_steps(c, bn, s, hp->n_steps);
+                });
             if (!rc)
                 rc = capture(c, gr, [&] {
                     if (cdp == CIMCS_CDP_CG) {
@@ -2238,15 +2455,19 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
         }
     }
     const int v_slot = cdp == CIMCS_CDP_CG ? 0 : hp->jacobi_iters & 1;
-    gen_c0(rngs, c->N, pinned, c->host_threads);
+    if (!pp) gen_c0(rngs, c->N, pinned, c->host_threads);
     for (int i = 0; i < nalt; ++i) {
         double* slot = pinned + (size_t)(i & 1) * nc0;
         CK(cudaMemcpyAsync(c->alt, &halts[i], sizeof(AltParams), cudaMemcpyHostToDevice,
                            c->stream));
-        CK(cudaMemcpyAsync(dc0, slot, nc0 * 8, cudaMemcpyHostToDevice, c->stream));
-        CK(cudaEventRecord(slot_done.ev[i & 1], c->stream));
+        if (!pp) {
+            CK(cudaMemcpyAsync(dc0, slot, nc0 * 8, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaEventRecord(slot_done.ev[i & 1], c->stream));
+        }
         CK(cudaEventRecord(ev.ev[4 * i + 0], c->stream));
-        if (c->use_graphs) {
+        if (pp) {
+            if ((rc = run_pp_cim(c, R, s, hp, rngs)) || (rc = pp_amplitude_to_c(c))) return rc;
+        } else if (c->use_graphs) {
             CK(cudaGraphLaunch(c->g_cim, c->stream));
         } else {
             rc = run_init(c, R, bn, dc0, nullptr, s.rt);
@@ -2265,7 +2486,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
         if ((rc = enqueue_score(c, s, v_slot, c->hist + (size_t)i * nT, track_best != 0)))
             return rc;
         CK(cudaEventRecord(ev.ev[4 * i + 3], c->stream));
-        if (i + 1 < nalt) {
+        if (i + 1 < nalt && !pp) {
             // draw the next alternation's c0 while the GPU works on this one
             CK(cudaEventSynchronize(slot_done.ev[(i + 1) & 1]));
             gen_c0(rngs, c->N, pinned + (size_t)((i + 1) & 1) * nc0, c->host_threads);
@@ -2361,7 +2582,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
             if (n_hist) n_hist[ht] = nh[dt];
             const bool failed = fg[dt] != kFreeTraj;
             if (fail_alt) fail_alt[ht] = failed ? fg[dt] / hp->n_steps : -1;
-            if (fail_index) fail_index[ht] = failed ? fi[dt] : -1;
+            if (fail_index) fail_index[ht] = failed ? (fi[dt] & ((1 << 30) - 1)) : -1;
             if (hist)
                 for (int i = 0; i < nalt; ++i) {
                     cimcs_record& o = hist[(size_t)ht * nalt + i];
