@@ -141,7 +141,7 @@ def kernel_label(N, NR, dtype):
                 "register-resident, w over DSMEM; bound by the per-step FMA chain + DSMEM "
                 "round trip, so the HBM fraction is an HBM-equivalent figure)")
     if dtype == "f32":
-        return (f"sym_step_kernel<{NR},BN> + sym_reduce_kernel + sym_finish_kernel (one fused "
+        return (f"sym_step_kernel<{NR},BN> + sym_update_kernel<{NR},BN> (one fused "
                 "Euler step: upper-triangle gram tiles as fp16 hi/lo, each read once for G w "
                 "and G^T w on tcgen05; achieved counts the dense-gram algorithmic bytes)")
     return f"gemv_fused_kernel<double,{NR},BN> (fused Euler step, fp64 DFMA)"
@@ -333,6 +333,7 @@ def run_ours(args, ws, rank, local):
             t1 = time.perf_counter()
             r2 = e2e_once()
             e2e_times.append(time.perf_counter() - t1)
+            print(f"e2e run {e2e_times[-1]:.3f}s", file=sys.stderr)
         ctx2.close()
         e2e_s = statistics.median(e2e_times)
         if dist is not None:

@@ -322,7 +322,6 @@ struct cimcs_ctx {
     short2* dTri = nullptr;
     int* dSg = nullptr;    // per-instance gram scale exponent
     float* dSpart = nullptr;  // partial products [B][nRB][nRB][128][NR]
-    float* dGw = nullptr;     // their slot sums [B][nRB * 128][NR]
     int sym_groups = 0;       // instance groups pipelined across two streams (0: auto)
     int gram_blas = 0;        // symmetric gram from cuBLAS DGEMM panels: 0 auto (N >= 8192), 1, -1
     cublasHandle_t blas = nullptr;
@@ -435,12 +434,12 @@ void free_state(cimcs_ctx* c) {
 void free_problems(cimcs_ctx* c) {
     free_state(c);
     void* ptrs[] = {c->dA, c->dy, c->dM, c->dG, c->dD, c->dhz, c->dx, c->dxi,
-                    c->dTri, c->dSg, c->dSpart, c->dGw};
+                    c->dTri, c->dSg, c->dSpart};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     c->dTri = nullptr;
     c->dSg = nullptr;
-    c->dSpart = c->dGw = nullptr;
+    c->dSpart = nullptr;
     c->spart_elems = 0;
     c->dA = c->dy = nullptr;
     c->dM = nullptr;
@@ -510,12 +509,9 @@ int ensure_state(cimcs_ctx* c, int NR) {
         const size_t ne = (size_t)c->B * c->nRB * c->nRB * kSyT * NR;
         if (c->spart_elems < ne) {
             if (c->dSpart) cudaFree(c->dSpart);
-            if (c->dGw) cudaFree(c->dGw);
-            c->dSpart = c->dGw = nullptr;
+            c->dSpart = nullptr;
             c->spart_elems = 0;
-            if ((rc = dalloc(&c->dSpart, ne * 4)) ||
-                (rc = dalloc(&c->dGw, (size_t)c->B * c->nRB * kSyT * NR * 4)))
-                return rc;
+            if ((rc = dalloc(&c->dSpart, ne * 4))) return rc;
             c->spart_elems = ne;
         }
     }
@@ -701,12 +697,7 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb, cudaStream_t s
         CK(cudaEventRecord(evA, sA));
         CK(cudaStreamWaitEvent(sF, evA, 0));
     }
-    const size_t off = (size_t)b0 * c->nRB * kSyT * NR;
-    const int total = nb * c->nRB * kSyT * (NR / 4);
-    sym_reduce_kernel<NR><<<(total + 255) / 256, 256, 0, sF>>>(c->dSpart + off * c->nRB,
-                                                               c->dGw + off, c->nRB, total);
-    CK(cudaGetLastError());
-    sym_finish_kernel<NR, MODE><<<dim3(c->nRB, nb), 128, 0, sF>>>(sa, c->dGw);
+    sym_update_kernel<NR, MODE><<<dim3(c->nRB, nb), kSyT * NR / 4, 0, sF>>>(sa);
     CK(cudaGetLastError());
     return 0;
 }

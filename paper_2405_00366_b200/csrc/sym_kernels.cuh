@@ -16,13 +16,13 @@
 // accumulated in fp32 in TMEM, and unscaled exactly.
 //
 // A row block K receives nRB partial products (one per tile touching it),
-// written to [B][nRB][slot][128][NR].  Two evenly spread kernels finish the
-// step: sym_reduce_kernel sums the slots in a FIXED order (deterministic) and
-// sym_finish_kernel runs the fused Euler / Jacobi / score / matvec update
-// (tc_row_update, shared with the streaming kernel); no CTA waits for another.
-// (A fused variant with owner-CTA finisher warps and an L2-resident ring of
-// partials was measured slower: each finish is a chain of dependent L2 round
-// trips, and 7 of them per CTA behind the tile stream left a long tail.)
+// written to [B][nRB][slot][128][NR].  A second, evenly spread kernel
+// (sym_update_kernel, one CTA per block, 4 replicas per thread) sums the slots
+// in a FIXED order (deterministic) and runs the fused Euler / Jacobi / score /
+// matvec update (the arithmetic of tc_row_update); no CTA waits for another.
+// (Fusing the finish into the tile kernel -- last-arriving CTA, or owner-CTA
+// finisher warps with an L2-resident ring of partials -- was measured slower:
+// each finish is a chain of dependent L2 round trips behind the tile stream.)
 //
 // The contraction input w is kept, next to the fp32 [W | W_lo] array the other
 // kernels use, as per-block fp16 B tiles [w_hi | w_lo] (2NR x 128, canonical
@@ -382,64 +382,214 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
                      "n"(kSyTmemCols));
 }
 
-// Second pass of a step, part 1: sum the nRB partial products of every
-// (instance, row, 4 replicas) in slot order (deterministic) -> gw.  Light and
-// fully occupied: every thread has all its slot loads in flight at once.
-template <int NR>
-__global__ void __launch_bounds__(256) sym_reduce_kernel(const float* __restrict__ spart,
-                                                         float* __restrict__ gw, int nRB,
-                                                         int total) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;  // (b, K, row, q4)
-    if (t >= total) return;
-    constexpr int Q4 = NR / 4;
-    const int q4 = t % Q4, r = t / Q4;  // r = (b * nRB + K) * 128 + row
-    const int row = r % kSyT, bk = r / kSyT;
-    const float4* src =
-        reinterpret_cast<const float4*>(spart + ((size_t)bk * nRB * kSyT + row) * NR) + q4;
-    constexpr size_t kSlot4 = (size_t)kSyT * NR / 4;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s0 = 0; s0 < nRB; s0 += 16) {
-        float4 v[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-            if (s0 + u < nRB) v[u] = __ldcs(src + (s0 + u) * kSlot4);
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-            if (s0 + u < nRB) {
-                acc.x = acc.x + v[u].x;
-                acc.y = acc.y + v[u].y;
-                acc.z = acc.z + v[u].z;
-                acc.w = acc.w + v[u].w;
-            }
-    }
-    reinterpret_cast<float4*>(gw + (size_t)r * NR)[q4] = acc;
-}
-
-// Part 2: the fused update of block (b, K) from gw; step / Jacobi modes also
-// emit the fp16 B tile of the new w for the next launch.
+// Second pass of a step in ONE kernel, 4 replicas per thread: block (b, K) is
+// handled by 128 x (NR / 4) threads; thread (row, g) sums its 4 replicas' nRB
+// partial products in slot order (deterministic), runs the fused update of
+// tc_row_update for replicas 4g..4g+3 and, in step / Jacobi modes, emits the
+// fp16 B tile of the new w.  4x the threads of a row-per-thread update: the
+// chains of dependent loads of different threads overlap.
 template <int NR, int MODE>
-__global__ void __launch_bounds__(128) sym_finish_kernel(SymArgs sa, const float* __restrict__ gwb) {
-    __shared__ double s_part[4][NR][3];
-    __shared__ unsigned s_max[4][NR];
+__global__ void __launch_bounds__(kSyT * NR / 4) sym_update_kernel(SymArgs sa) {
+    constexpr int QG = NR / 4;
+    __shared__ unsigned s_max[QG][4][4];    // [group][warp of the group][replica]
+    __shared__ double s_sc[QG][4][4][3];    // score partials
     const TcArgs& a = sa.t;
-    constexpr bool kWritesW = MODE == EPI_STEP_BN || MODE == EPI_STEP_CN || MODE == EPI_JACOBI;
-    const int K = blockIdx.x, b = sa.b0 + blockIdx.y, nRB = a.nRB;
-    const int row = threadIdx.x, lane = row & 31, ep = row >> 5;
-    const float4* g4 =
-        reinterpret_cast<const float4*>(gwb + (((size_t)b * nRB + K) * kSyT + row) * NR);
-    float gw[NR];
+    const StepScalars& sc = a.s;
+    const int K = blockIdx.x, b = sa.b0 + blockIdx.y, nRB = a.nRB, N = a.N;
+    const int t = threadIdx.x, row = t % kSyT, g = t / kSyT;
+    const int lane = t & 31, wg = row >> 5;  // warp inside the group
+    const int i = K * kSyT + row, q0 = 4 * g;
+    const bool valid = i < N;
+    const size_t si = (size_t)b * a.ldN + i, vi0 = si * NR + q0;
+    // ---- slot sums
+    float gw[4];
+    {
+        const float4* src = reinterpret_cast<const float4*>(
+                                sa.spart + (((size_t)b * nRB + K) * nRB * kSyT + row) * NR) +
+                            g;
+        constexpr size_t kSlot4 = (size_t)kSyT * NR / 4;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int s0 = 0; s0 < nRB; s0 += 16) {
+            float4 v[16];
 #pragma unroll
-    for (int q = 0; q < NR; q += 4) {
-        const float4 v = __ldcs(g4 + q / 4);
-        gw[q] = v.x; gw[q + 1] = v.y; gw[q + 2] = v.z; gw[q + 3] = v.w;
+            for (int u = 0; u < 16; ++u)
+                if (s0 + u < nRB) v[u] = __ldcs(src + (s0 + u) * kSlot4);
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                if (s0 + u < nRB) {
+                    acc.x = acc.x + v[u].x;
+                    acc.y = acc.y + v[u].y;
+                    acc.z = acc.z + v[u].z;
+                    acc.w = acc.w + v[u].w;
+                }
+        }
+        gw[0] = acc.x; gw[1] = acc.y; gw[2] = acc.z; gw[3] = acc.w;
     }
-    // the [W | W_lo] residue half is read only by the streaming kernel: skipped
-    float w[NR];
-    tc_row_update<NR, MODE, false>(a, b, K, row, lane, ep, gw, s_part, 2, w);
-    if constexpr (kWritesW) {
-        sy_emit_block<NR>(w, row, lane, ep, s_max,
-                          sa.WBout + ((size_t)b * nRB + K) * (2 * NR * kSyT),
-                          sa.WSout + ((size_t)b * nRB + K) * NR, 2);
+    bool fz[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int fg = a.fail_gstep[b * NR + q0 + u];
+        fz[u] = (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) ? fg < a.alt->gstep_base + a.step
+                                                             : fg != kFreeTraj;
+    }
+    float wn[4] = {0.f, 0.f, 0.f, 0.f};  // new contraction input (0: frozen / padding)
+    if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
+        float lmin[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+        if (valid) {
+            float wv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) wv[u] = __ldg(a.Win + tc_wofs(a.ldJ, NR, b, i, q0 + u));
+            const float4 r4 = __ldg(reinterpret_cast<const float4*>(a.Rs + vi0));
+            const float4 c4 = *reinterpret_cast<const float4*>(a.C + vi0);
+            const float4 e4 = *reinterpret_cast<const float4*>(a.E + vi0);
+            const float Rv[4] = {r4.x, r4.y, r4.z, r4.w}, cv[4] = {c4.x, c4.y, c4.z, c4.w};
+            const float ev[4] = {e4.x, e4.y, e4.z, e4.w};
+            const float Dv = __ldg(a.D + si), hzv = __ldg(a.hz + si);
+            const float half_rt = (float)sc.half_rt, rt = (float)sc.rt, dt = (float)sc.dt;
+            const float Kj = (float)sc.Kj, nbeta = (float)sc.nbeta, tau = (float)sc.tau;
+            const double pd = a.pump ? a.pump[a.step] : a.p_scalar;
+            const float loss = sc.minus_j != 0.0 ? (float)((-1.0 + pd) - sc.minus_j)
+                                                 : (float)(-1.0 + pd);
+            const float thresh = (float)a.alt->thresh;
+            float cn[4], en[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float c = cv[u], e = ev[u];
+                const float Jw = Dv * wv[u] - gw[u];
+                float h;
+                if constexpr (MODE == EPI_STEP_BN)
+                    h = half_rt * (Jw + hzv);
+                else
+                    h = Jw + half_rt * hzv;
+                if (a.Hdbg) a.Hdbg[vi0 + u] = h;
+                const float inj = (Kj * e) * (Rv[u] * h - thresh);
+                cn[u] = c + dt * ((loss - c * c) * c + inj);
+                en[u] = e + dt * ((nbeta * (c * c - tau)) * e);
+                if (fz[u]) {
+                    cn[u] = c;
+                    en[u] = e;
+                } else if (!isfinite(cn[u]) || !isfinite(en[u])) {
+                    atomicMin(&a.fail_gstep[b * NR + q0 + u], a.alt->gstep_base + a.step);
+                    atomicMin(&a.fail_idx[b * NR + q0 + u], i);
+                    cn[u] = c;
+                    en[u] = e;
+                } else {
+                    lmin[u] = en[u];
+                    float w;
+                    if constexpr (MODE == EPI_STEP_BN)
+                        w = Rv[u] * (cn[u] > 0.f ? 1.f : 0.f);
+                    else
+                        w = (Rv[u] * 0.25f) * (cn[u] + rt);
+                    a.Wout[tc_wofs(a.ldJ, NR, b, i, q0 + u)] = w;
+                    wn[u] = w;
+                }
+            }
+            *reinterpret_cast<float4*>(a.C + vi0) = make_float4(cn[0], cn[1], cn[2], cn[3]);
+            *reinterpret_cast<float4*>(a.E + vi0) = make_float4(en[0], en[1], en[2], en[3]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            float m = lmin[u];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1)
+                m = fminf(m, __shfl_xor_sync(0xffffffffu, m, off));
+            if (lane == u && m != INFINITY) atomicMin(&a.minE[b * NR + q0 + u], ord_key(m));
+        }
+    } else if constexpr (MODE == EPI_JACOBI) {
+        if (valid) {
+            const float Dv = __ldg(a.D + si), bv = __ldg(a.hz + si);
+            const float omd = (float)sc.one_minus_dtc, dtc = (float)sc.dt_c;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (fz[u]) continue;
+                const float Rv = a.Rs[vi0 + u];
+                const bool on = a.sigma[vi0 + u] != 0;
+                float rn = Rv;
+                if (on) {
+                    if (Dv == 0.f) {
+                        atomicMin(a.err, i);
+                        continue;
+                    }
+                    const float off = gw[u] - Dv * Rv;
+                    rn = omd * Rv + dtc * ((bv - off) / Dv);
+                    a.Rs[vi0 + u] = rn;
+                }
+                const float w = rn * (on ? 1.f : 0.f);
+                a.Wout[tc_wofs(a.ldJ, NR, b, i, q0 + u)] = w;
+                wn[u] = w;
+            }
+        }
+    } else if constexpr (MODE == EPI_MATVEC) {
+        if (valid) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (!fz[u]) a.Mv[vi0 + u] = (double)gw[u];
+        }
+    } else {  // EPI_SCORE: w.Gw, hz.w, |w - x|^2 partials of this 128-row block
+        double pa[4], pb[4], pc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            pa[u] = pb[u] = pc[u] = 0.0;
+            if (valid && !fz[u]) {
+                const double wv = a.Win[tc_wofs(a.ldJ, NR, b, i, q0 + u)];
+                pa[u] = wv * (double)gw[u];
+                pb[u] = (double)a.hz[si] * wv;
+                if (a.xtrue) {
+                    const double xt = a.xitrue[si] ? a.xtrue[si] : 0.0;
+                    pc[u] = (wv - xt) * (wv - xt);
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                pa[u] += __shfl_xor_sync(0xffffffffu, pa[u], off);
+                pb[u] += __shfl_xor_sync(0xffffffffu, pb[u], off);
+                pc[u] += __shfl_xor_sync(0xffffffffu, pc[u], off);
+            }
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                s_sc[g][wg][u][0] = pa[u];
+                s_sc[g][wg][u][1] = pb[u];
+                s_sc[g][wg][u][2] = pc[u];
+            }
+        }
+        __syncthreads();
+        if (row < 4) {  // thread (g, u = row) writes replica q0 + u
+            double A_ = 0, B_ = 0, C_ = 0;
+            for (int w = 0; w < 4; ++w) {
+                A_ += s_sc[g][w][row][0];
+                B_ += s_sc[g][w][row][1];
+                C_ += s_sc[g][w][row][2];
+            }
+            double* p = a.part + (((size_t)b * nRB + K) * NR + q0 + row) * 4;
+            p[0] = A_;
+            p[1] = B_;
+            p[2] = C_;
+        }
+    }
+    if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN || MODE == EPI_JACOBI) {
+        // fp16 B tile of the new w of block K: per-replica max over the 128 rows
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(wn[u])));
+            if (lane == 0) s_max[g][wg][u] = m;
+        }
+        __syncthreads();
+        unsigned char* B = reinterpret_cast<unsigned char*>(sa.WBout + ((size_t)b * nRB + K) *
+                                                                           (2 * NR * kSyT));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const unsigned m = max(max(s_max[g][0][u], s_max[g][1][u]),
+                                   max(s_max[g][2][u], s_max[g][3][u]));
+            const int e = sy_exp14(__uint_as_float(m));
+            const float ws = wn[u] * sy_pow2(e);
+            const __half hi = __float2half_rn(ws);
+            const __half lo = __float2half_rn(ws - __half2float(hi));
+            *reinterpret_cast<__half*>(B + sy_offk(q0 + u, row, 2 * NR)) = hi;
+            *reinterpret_cast<__half*>(B + sy_offk(NR + q0 + u, row, 2 * NR)) = lo;
+            if (row == 0) sa.WSout[((size_t)b * nRB + K) * NR + q0 + u] = e;
+        }
     }
 }
 
