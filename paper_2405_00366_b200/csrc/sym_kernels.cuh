@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
 // fp16 B tile of the new w.  4x the threads of a row-per-thread update: the
 // chains of dependent loads of different threads overlap.
 template <int NR, int MODE>
-__global__ void __launch_bounds__(kSyT * NR / 4) sym_update_kernel(SymArgs sa) {
+__global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_update_kernel(SymArgs sa) {
     constexpr int QG = NR / 4;
     __shared__ unsigned s_max[QG][4][4];    // [group][warp of the group][replica]
     __shared__ double s_sc[QG][4][4][3];    // score partials
@@ -409,13 +409,13 @@ __global__ void __launch_bounds__(kSyT * NR / 4) sym_update_kernel(SymArgs sa) {
                             g;
         constexpr size_t kSlot4 = (size_t)kSyT * NR / 4;
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int s0 = 0; s0 < nRB; s0 += 16) {
-            float4 v[16];
+        for (int s0 = 0; s0 < nRB; s0 += 8) {
+            float4 v[8];
 #pragma unroll
-            for (int u = 0; u < 16; ++u)
+            for (int u = 0; u < 8; ++u)
                 if (s0 + u < nRB) v[u] = __ldcs(src + (s0 + u) * kSlot4);
 #pragma unroll
-            for (int u = 0; u < 16; ++u)
+            for (int u = 0; u < 8; ++u)
                 if (s0 + u < nRB) {
                     acc.x = acc.x + v[u].x;
                     acc.y = acc.y + v[u].y;
