@@ -2552,8 +2552,9 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
     // kernels of this library per alternation: init + steps | support + sweeps |
     // score contraction, tp, finalize, median (+ best).  The small-N cluster loop
     // runs a whole CIM call / refit in one launch; CG counts its last iteration total.
-    const bool cl = cluster_ok(c);
-    tm.step_launches = (int64_t)nalt * (cl ? 1 : hp->n_steps);
+    const bool cl = cluster_ok(c) && !pp;
+    const int per = c->sym ? 2 : 1;  // symmetric path: tile kernel + update kernel
+    tm.step_launches = (int64_t)nalt * (cl ? 1 : per * hp->n_steps + (pp ? 1 : 0));
     if (cdp == CIMCS_CDP_CG) {
         std::vector<CgTraj> st(nT);
         cudaMemcpy(st.data(), c->cg_st, nT * sizeof(CgTraj), cudaMemcpyDeviceToHost);
@@ -2561,7 +2562,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
         for (const CgTraj& t : st) mx = std::max(mx, t.it);
         tm.refit_launches = (int64_t)nalt * (6 + 3 * (int64_t)mx);
     } else {
-        tm.refit_launches = (int64_t)nalt * (cl ? 1 : hp->jacobi_iters);
+        tm.refit_launches = (int64_t)nalt * (cl ? 1 : per * hp->jacobi_iters);
     }
     tm.other_launches = (int64_t)nalt * (2 + 4 + (track_best ? 1 : 0));
     tm.step_bytes = (double)c->B * c->N * (double)c->N * c->elt();  // dense G share
