@@ -575,10 +575,10 @@ template <typename T, int NR, int MODE>
 int launch_gemv_t(cimcs_ctx* c, const GemvArgs& a) {
     auto kern = gemv_fused_kernel<T, NR, MODE>;
     constexpr size_t smem = gemv_smem_bytes<T, NR>();
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;  // per device: the attribute is per context
+    if (!(attr >> c->device & 1ull)) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
+        attr |= 1ull << c->device;
     }
     if (c->nRB == 0) return 0;  // this rank holds no rows
     dim3 grid(c->nRB, c->B);
@@ -652,10 +652,10 @@ int launch_tc_t(cimcs_ctx* c, const GemvArgs& g) {
     if (a.ntiles == 0) return 0;
     auto kern = tc_step_kernel<NR, MODE>;
     constexpr size_t smem = tc_smem_bytes(NR);
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;  // per device: the attribute is per context
+    if (!(attr >> c->device & 1ull)) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
+        attr |= 1ull << c->device;
     }
     const int grid = std::min(a.ntiles, c->num_sms);
     kern<<<grid, kTcThreads, smem, c->stream>>>(a);
@@ -685,10 +685,10 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb, cudaStream_t s
     if (sa.ntiles == 0) return 0;
     auto kern = sym_step_kernel<NR, MODE>;
     constexpr size_t smem = sy_smem_bytes<NR>();
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;  // per device: the attribute is per context
+    if (!(attr >> c->device & 1ull)) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
+        attr |= 1ull << c->device;
     }
     const int grid = std::min(sa.ntiles, c->num_sms);
     kern<<<grid, kSyThreads, smem, sA>>>(sa);
@@ -1009,11 +1009,11 @@ template <typename T, int NR, int MODE>
 int launch_cluster_t(cimcs_ctx* c, GemvArgs a, int n_iters) {
     auto kern = cluster_loop_kernel<T, NR, MODE>;
     constexpr size_t smem = cluster_smem_bytes<T, NR>();
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;  // per device: the attribute is per context
+    if (!(attr >> c->device & 1ull)) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr = true;
+        attr |= 1ull << c->device;
     }
     a.tc_in = c->tc ? 1 : 0;
     const unsigned cs = (unsigned)((c->N + kClRows - 1) / kClRows);
