@@ -13,12 +13,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libcimcs_gpu.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("runtime.cu",)]
-DEPS = SOURCES + [
-    os.path.join(HERE, "csrc", "kernels.cuh"),
-    os.path.join(HERE, "csrc", "tc_kernels.cuh"),
-    os.path.join(HERE, "csrc", "host_rng.hpp"),
-    os.path.join(ROOT, "include", "cimcs_gpu.h"),
-]
+DEPS = SOURCES + sorted(
+    os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))
+    if f.endswith((".cuh", ".hpp"))) + [os.path.join(ROOT, "include", "cimcs_gpu.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -29,6 +29,7 @@
 #include "cg_kernels.cuh"
 #include "cluster_kernels.cuh"
 #include "sym_kernels.cuh"
+#include "fac_kernels.cuh"
 
 using namespace cimcs;
 
@@ -323,6 +324,15 @@ struct cimcs_ctx {
     int* dSg = nullptr;    // per-instance gram scale exponent
     float* dSpart = nullptr;  // partial products [B][nRB][nRB][128][NR]
     int sym_groups = 0;       // instance groups pipelined across two streams (0: auto)
+    // factored coupling A^T (A w) from fp16 hi/lo tiles of A (fac_kernels.cuh)
+    int fac_opt = -1;         // -1 auto, 0 off, 1 on (a symmetric-path variant)
+    int fac_requested = -1;
+    bool fac = false;
+    int nMB = 0, fac_w2 = 1, fac_skew = 10, ntask = 0;
+    int* dTask = nullptr;     // [ntask] task table (fa_task)
+    int* dCnt = nullptr;      // [2B] per-instance phase counters (self-resetting)
+    __half* UB = nullptr;     // fp16 B tiles of u = A w [B][nMB][2NR x 128]
+    int* US = nullptr;
     int gram_blas = 0;        // symmetric gram from cuBLAS DGEMM panels: 0 auto (N >= 8192), 1, -1
     cublasHandle_t blas = nullptr;
     cudaStream_t sfin = nullptr;             // stream of the reduction / update kernels
@@ -403,7 +413,7 @@ void free_state(cimcs_ctx* c) {
     void* ptrs[] = {c->Rs,  c->C,        c->E,          c->W0,  c->W1,       c->Hdbg,
                     c->bestR, c->sig,    c->bestS,      c->fail_gstep, c->fail_idx, c->n_hist,
                     c->improved, c->minE, c->part,      c->best_obj, c->obj, c->rmse, c->ham,
-                    c->tp, c->fail_tmp, c->cgX, c->cgR, c->cgP, c->cgGp, c->cg_act,
+                    c->tp, c->fail_tmp, c->UB, c->US, c->cgX, c->cgR, c->cgP, c->cgGp, c->cg_act,
                     c->cg_st, c->cg_live, c->WB0, c->WB1, c->WS0, c->WS1, c->Pn, c->Pm,
                     c->MT, c->nzd[0], c->nzd[1]};
     for (void* p : ptrs)
@@ -411,6 +421,8 @@ void free_state(cimcs_ctx* c) {
     c->cgX = c->cgR = c->cgP = c->cgGp = nullptr;
     c->WB0 = c->WB1 = nullptr;
     c->WS0 = c->WS1 = nullptr;
+    c->UB = nullptr;
+    c->US = nullptr;
     c->Pn = c->Pm = c->MT = nullptr;
     c->nzd[0] = c->nzd[1] = nullptr;
     for (double*& h : c->nzh)
@@ -434,9 +446,11 @@ void free_state(cimcs_ctx* c) {
 void free_problems(cimcs_ctx* c) {
     free_state(c);
     void* ptrs[] = {c->dA, c->dy, c->dM, c->dG, c->dD, c->dhz, c->dx, c->dxi,
-                    c->dTri, c->dSg, c->dSpart};
+                    c->dTri, c->dSg, c->dSpart, c->dTask, c->dCnt};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    c->dTask = nullptr;
+    c->dCnt = nullptr;
     c->dTri = nullptr;
     c->dSg = nullptr;
     c->dSpart = nullptr;
@@ -506,8 +520,11 @@ int ensure_state(cimcs_ctx* c, int NR) {
         if ((rc = dalloc(&c->WB0, nb * 2)) || (rc = dalloc(&c->WB1, nb * 2)) ||
             (rc = dalloc(&c->WS0, ns * 4)) || (rc = dalloc(&c->WS1, ns * 4)))
             return rc;
-        const size_t ne = (size_t)c->B * c->nRB * c->nRB * kSyT * NR;
-        if (c->spart_elems < ne) {
+        const size_t ne = c->fac ? 0 : (size_t)c->B * c->nRB * c->nRB * kSyT * NR;
+        if (c->fac && ((rc = dalloc(&c->UB, (size_t)c->B * c->nMB * 2 * NR * kSyT * 2)) ||
+                       (rc = dalloc(&c->US, (size_t)c->B * c->nMB * NR * 4))))
+            return rc;
+        if (ne && c->spart_elems < ne) {
             if (c->dSpart) cudaFree(c->dSpart);
             c->dSpart = nullptr;
             c->spart_elems = 0;
@@ -714,6 +731,56 @@ int launch_sym_grp(cimcs_ctx* c, int mode, const GemvArgs& a, int b0, int nb, cu
     }
 }
 
+// factored path: one cooperative launch per step / sweep (fac_kernels.cuh)
+template <int NR, int MODE>
+int launch_fac_t(cimcs_ctx* c, const GemvArgs& g) {
+    FacArgs f{};
+    f.t = tc_args(c, g);
+    f.As = static_cast<const __half*>(c->dG);
+    f.sa = c->dSg;
+    f.WBin = g.Win == c->W0 ? c->WB0 : c->WB1;
+    f.WSin = g.Win == c->W0 ? c->WS0 : c->WS1;
+    f.WBout = g.Wout == c->W0 ? c->WB0 : c->WB1;
+    f.WSout = g.Wout == c->W0 ? c->WS0 : c->WS1;
+    f.UB = c->UB;
+    f.US = c->US;
+    f.cnt = c->dCnt;
+    f.task = c->dTask;
+    f.ntask = c->ntask;
+    f.nMB = c->nMB;
+    f.W2 = c->fac_w2;
+    auto kern = fac_step_kernel<NR, MODE>;
+    constexpr size_t smem = fa_smem_bytes<NR>();
+    static unsigned long long attr = 0;
+    if (!(attr >> c->device & 1ull)) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr |= 1ull << c->device;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(std::min(f.ntask, c->num_sms));
+    cfg.blockDim = dim3(kFaThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;  // tasks wait on other CTAs' tasks
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kern, f));
+    return 0;
+}
+
+template <int NR>
+int launch_fac_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
+    switch (mode) {
+        case EPI_STEP_BN: return launch_fac_t<NR, EPI_STEP_BN>(c, a);
+        case EPI_STEP_CN: return launch_fac_t<NR, EPI_STEP_CN>(c, a);
+        case EPI_JACOBI: return launch_fac_t<NR, EPI_JACOBI>(c, a);
+        case EPI_MATVEC: return launch_fac_t<NR, EPI_MATVEC>(c, a);
+        default: return launch_fac_t<NR, EPI_SCORE>(c, a);
+    }
+}
+
 template <int NR>
 int launch_sym_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
     return launch_sym_grp<NR>(c, mode, a, 0, c->B, c->stream, c->stream, nullptr);
@@ -731,6 +798,7 @@ int launch_tc_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
 }
 
 int launch_gemv(cimcs_ctx* c, int mode, const GemvArgs& a) {
+    if (c->fac) return c->NR == 8 ? launch_fac_nr<8>(c, mode, a) : launch_fac_nr<16>(c, mode, a);
     if (c->sym) return c->NR == 8 ? launch_sym_nr<8>(c, mode, a) : launch_sym_nr<16>(c, mode, a);
     if (c->tc) return c->NR == 8 ? launch_tc_nr<8>(c, mode, a) : launch_tc_nr<16>(c, mode, a);
     return c->dtype == CIMCS_F64 ? launch_gemv_T<double>(c, mode, a)
@@ -1067,6 +1135,15 @@ int launch_cluster(cimcs_ctx* c, int mode, const GemvArgs& a, int n_iters) {
 // (the step is bound by the total HBM traffic of the three kernels, which
 // overlapping cannot reduce), so the default is one group.
 int enqueue_sym_loop(cimcs_ctx* c, int mode, GemvArgs a, int n_iters, bool steps) {
+    if (c->fac) {
+        for (int k = 0; k < n_iters; ++k) {
+            if (steps) a.step = k;
+            a.Win = (k & 1) ? c->W1 : c->W0;
+            a.Wout = (k & 1) ? c->W0 : c->W1;
+            if (int rc = launch_gemv(c, mode, a)) return rc;
+        }
+        return 0;
+    }
     int G = c->sym_groups ? c->sym_groups : 1;
     G = std::max(1, std::min(G, std::min(4, c->B)));
     for (int k = 0; k < n_iters; ++k) {
@@ -1795,7 +1872,12 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
     else if (k == "use_graphs") c->use_graphs = v != 0;
     else if (k == "gram_blas") c->gram_blas = v > 0 ? 1 : (v < 0 ? -1 : 0);
     else if (k == "sym_groups") c->sym_groups = (int)std::min<int64_t>(4, std::max<int64_t>(0, v));
-    else if (k == "symmetric") {
+    else if (k == "fac_skew") {
+        c->fac_skew = (int)std::max<int64_t>(0, v);  // applied by build_coupling
+    } else if (k == "factored") {
+        if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set factored before set_problems");
+        c->fac_opt = v > 0 ? 1 : (v < 0 ? -1 : 0);
+    } else if (k == "symmetric") {
         if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set symmetric before set_problems");
         c->want_sym = v != 0;
     } else if (k == "cluster_loop") {
@@ -1822,11 +1904,13 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
     // same shapes as the resident problem set: keep every device allocation
     const bool reuse = c->dA && c->B == B && c->N == N && c->has_truth == truth &&
                        std::equal(c->M.begin(), c->M.end(), M) && (int)c->M.size() == B &&
-                       c->want_tc == c->tc_requested && c->want_sym == c->sym_requested;
+                       c->want_tc == c->tc_requested && c->want_sym == c->sym_requested &&
+                       c->fac_opt == c->fac_requested;
     if (!reuse) free_problems(c);
     c->built = false;
     c->tc_requested = c->want_tc;
     c->sym_requested = c->want_sym;
+    c->fac_requested = c->fac_opt;
     c->B = B;
     c->N = N;
     c->ldN = (N + 31) / 32 * 32;
@@ -1853,6 +1937,14 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
     c->ntri = c->sym ? c->nRB * (c->nRB + 1) / 2 : 0;
     c->M.assign(M, M + B);
     c->Mmax = *std::max_element(c->M.begin(), c->M.end());
+    // factored variant: auto when A is read twice per step (phase 2 mostly misses
+    // L2: ncu, profiles/r01_fac_step.txt) and still moves fewer bytes than the
+    // gram triangle, i.e. M below about N/4, and the phase-1 tasks cover the SMs
+    c->nMB = (c->Mmax + kSyT - 1) / kSyT;
+    c->fac = c->sym && c->nMB < 0x8000 && B < 0x8000 &&
+             (c->fac_opt == 1 || (c->fac_opt == -1 && 2 * c->nMB * c->nRB <= c->ntri &&
+                                  B * c->nMB >= c->num_sms / 2));
+    c->fac_w2 = c->nRB >= 2 * c->nMB ? 2 : 1;
     c->has_truth = truth;
     const size_t astride = (size_t)c->Mmax * N;
     int rc;
@@ -1896,7 +1988,8 @@ int cimcs_build_coupling(cimcs_ctx* c) {
     CK(cudaSetDevice(c->device));
     const size_t es = c->elt();
     // gram bytes: symmetric fp16 hi/lo tiles, canonical tf32 panels, or CUDA-core panels
-    const size_t gbytes = c->sym ? (size_t)c->B * c->ntri * 2 * kSyPlaneBytes
+    const size_t gbytes = c->fac ? (size_t)c->B * c->nMB * c->nRB * 2 * kSyPlaneBytes
+                          : c->sym ? (size_t)c->B * c->ntri * 2 * kSyPlaneBytes
                           : c->tc ? (size_t)c->B * c->nRB * c->nch * kTcTileFloats * es
                                   : (size_t)c->B * c->nRB * c->ldJ * c->RB * es;
     const size_t nv = (size_t)c->B * c->ldN;
@@ -1912,9 +2005,28 @@ int cimcs_build_coupling(cimcs_ctx* c) {
             return rc;
         CK(cudaMemcpy(c->dTri, tab.data(), tab.size() * sizeof(short2), cudaMemcpyHostToDevice));
     }
+    if (c->fac) {
+        // task table: phase 1 of instance b + skew is interleaved with phase 2 of b
+        const int nP1 = c->nMB, nP2 = (c->nRB + c->fac_w2 - 1) / c->fac_w2;
+        const int k = std::min(c->fac_skew, c->B);
+        std::vector<int> tab;
+        auto p1 = [&](int b) { for (int i = 0; i < nP1; ++i) tab.push_back(fa_task(0, b, i)); };
+        for (int b = 0; b < k; ++b) p1(b);
+        for (int b = 0; b < c->B; ++b) {
+            for (int i = 0; i < nP2; ++i) tab.push_back(fa_task(1, b, i));
+            if (b + k < c->B) p1(b + k);
+        }
+        c->ntask = (int)tab.size();
+        if (c->dTask) cudaFree(c->dTask);
+        c->dTask = nullptr;
+        if ((rc = dalloc(&c->dTask, tab.size() * 4))) return rc;
+        CK(cudaMemcpy(c->dTask, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+        if (!c->dCnt && (rc = dalloc(&c->dCnt, (size_t)c->B * 2 * 4))) return rc;
+        CK(cudaMemset(c->dCnt, 0, (size_t)c->B * 2 * 4));
+    }
     Events ev(2);
     cudaEventRecord(ev.ev[0], c->stream);
-    CK(cudaMemsetAsync(c->dG, 0, gbytes, c->stream));
+    if (!c->fac) CK(cudaMemsetAsync(c->dG, 0, gbytes, c->stream));
     const int nt = (c->N + kG2T - 1) / kG2T;
     const int bi0 = c->row0 / kG2T;
     const int nti = c->world == 1 ? nt : (c->row1 - c->row0 + kG2T - 1) / kG2T;
@@ -1931,14 +2043,20 @@ int cimcs_build_coupling(cimcs_ctx* c) {
             c->dA, c->dy, c->dM, c->N, c->ldN, astride, c->Mmax, static_cast<float*>(c->dhz),
             static_cast<float*>(c->dD), c->B);
     CK(cudaGetLastError());
-    if (c->sym) {
+    if (c->fac) {
+        fac_scale_kernel<<<c->B, 1024, 0, c->stream>>>(c->dA, c->dM, c->N, astride, c->dSg);
+        fac_tiles_kernel<<<16 * c->num_sms, 256, 0, c->stream>>>(
+            c->dA, c->dM, c->N, astride, c->nMB, c->nRB, c->dSg, static_cast<__half*>(c->dG),
+            c->B);
+        CK(cudaGetLastError());
+    } else if (c->sym) {
         sym_scale_kernel<<<c->B, 256, 0, c->stream>>>(static_cast<const float*>(c->dD), c->N,
                                                      c->ldN, c->dSg);
         CK(cudaGetLastError());
     }
     // large instances on the symmetric path: G = A^T A by cuBLAS DGEMM over panels
     // of 8 row blocks (upper triangle only), converted to the fp16 hi/lo tiles
-    const bool blas = c->sym && (c->gram_blas > 0 || (c->gram_blas == 0 && c->N >= 8192));
+    const bool blas = c->sym && !c->fac && (c->gram_blas > 0 || (c->gram_blas == 0 && c->N >= 8192));
     if (blas) {
         if (!c->blas) {
             if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS)
@@ -1969,7 +2087,7 @@ int cimcs_build_coupling(cimcs_ctx* c) {
         CK(cudaStreamSynchronize(c->stream));  // P is freed on return
     }
     // one launch per run of equal M (instances of a phase grid differ in M)
-    for (int b = 0; b < c->B && !blas;) {
+    for (int b = 0; b < c->B && !blas && !c->fac;) {
         int e = b;
         while (e < c->B && c->M[e] == c->M[b]) ++e;
         const dim3 grid(nt, nti, e - b);
@@ -2027,7 +2145,21 @@ int cimcs_get_coupling(cimcs_ctx* c, int32_t b, double* G, double* hz, double* D
         return 0;
     };
     std::vector<double> h;
-    if (G && c->sym) {
+    if (G && c->fac) {  // not stored: G = A^T A in fp64 (cuBLAS) from the resident A
+        if (!c->blas && cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS)
+            return fail(CIMCS_CUDA_ERROR, "cublasCreate failed");
+        cublasSetStream(c->blas, c->stream);
+        double* P = nullptr;
+        if (int rc = dalloc(&P, (size_t)N * N * 8)) return rc;
+        std::unique_ptr<double, decltype(&cudaFree)> pguard(P, &cudaFree);
+        const double one = 1.0, zero = 0.0;
+        const double* Ab = c->dA + (size_t)b * c->Mmax * N;
+        if (cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, N, N, c->M[b], &one, Ab, c->M[b], Ab,
+                        c->M[b], &zero, P, N) != CUBLAS_STATUS_SUCCESS)
+            return fail(CIMCS_CUDA_ERROR, "cublasDgemm failed");
+        CK(cudaMemcpyAsync(G, P, (size_t)N * N * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));  // symmetric: column-major == row-major
+    } else if (G && c->sym) {
         const size_t nh = (size_t)c->ntri * 2 * kSyPlaneHalfs;
         std::vector<__half> t(nh);
         int sg = 0;
@@ -2553,7 +2685,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
     // score contraction, tp, finalize, median (+ best).  The small-N cluster loop
     // runs a whole CIM call / refit in one launch; CG counts its last iteration total.
     const bool cl = cluster_ok(c) && !pp;
-    const int per = c->sym ? 2 : 1;  // symmetric path: tile kernel + update kernel
+    const int per = c->sym && !c->fac ? 2 : 1;  // symmetric path: tile kernel + update kernel
     tm.step_launches = (int64_t)nalt * (cl ? 1 : per * hp->n_steps + (pp ? 1 : 0));
     if (cdp == CIMCS_CDP_CG) {
         std::vector<CgTraj> st(nT);
