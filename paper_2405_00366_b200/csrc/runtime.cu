@@ -12,6 +12,7 @@
 #include <cublas_v2.h>
 
 #include <algorithm>
+#include <queue>
 #include <atomic>
 #include <climits>
 #include <cmath>
@@ -320,9 +321,15 @@ struct cimcs_ctx {
     bool sym = false;      // active for the current problem set
     bool sym_requested = true;
     int ntri = 0;          // upper-triangle tiles per instance
-    short2* dTri = nullptr;
+    int nSB = 0;           // super-block items per row of the tile triangle (kSyS tiles)
+    struct SymSched {      // LPT placement of the items of nb instances on the CTAs
+        int nb = 0, nRB = 0, grid = 0;
+        int2* items = nullptr;
+        int* sched = nullptr;
+    };
+    std::vector<SymSched> ssched;
     int* dSg = nullptr;    // per-instance gram scale exponent
-    float* dSpart = nullptr;  // partial products [B][nRB][nRB][128][NR]
+    float* dSpart = nullptr;  // partial products [B][nRB][nSB][128][NR]
     int sym_groups = 0;       // instance groups pipelined across two streams (0: auto)
     // factored coupling A^T (A w) from fp16 hi/lo tiles of A (fac_kernels.cuh)
     int fac_opt = -1;         // -1 auto, 0 off, 1 on (a symmetric-path variant)
@@ -446,12 +453,16 @@ void free_state(cimcs_ctx* c) {
 void free_problems(cimcs_ctx* c) {
     free_state(c);
     void* ptrs[] = {c->dA, c->dy, c->dM, c->dG, c->dD, c->dhz, c->dx, c->dxi,
-                    c->dTri, c->dSg, c->dSpart, c->dTask, c->dCnt};
+                    c->dSg, c->dSpart, c->dTask, c->dCnt};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    for (auto& q : c->ssched) {
+        cudaFree(q.items);
+        cudaFree(q.sched);
+    }
+    c->ssched.clear();
     c->dTask = nullptr;
     c->dCnt = nullptr;
-    c->dTri = nullptr;
     c->dSg = nullptr;
     c->dSpart = nullptr;
     c->spart_elems = 0;
@@ -473,6 +484,59 @@ int dalloc(P** p, size_t bytes) {
     cudaMemset(*p, 0, std::max<size_t>(bytes, 16));
     return 0;
 }
+
+// Super-block items of nb instances placed on the persistent CTAs, largest
+// first onto the least-loaded CTA (LPT); built once per nb and cached.
+int sym_schedule(cimcs_ctx* c, int nb, const cimcs_ctx::SymSched** out) {
+    for (auto& q : c->ssched)
+        if (q.nb == nb && q.nRB == c->nRB) {
+            *out = &q;
+            return 0;
+        }
+    const int nRB = c->nRB, nSB = c->nSB;
+    std::vector<std::pair<int, int2>> items;  // (tiles, item)
+    for (int b = 0; b < nb; ++b)
+        for (int P = 0; P < nSB; ++P)
+            for (int Q = P; Q < nSB; ++Q) {
+                const int nI = std::min(kSyS, nRB - P * kSyS), nJ = std::min(kSyS, nRB - Q * kSyS);
+                const int t = P == Q ? nI * (nI + 1) / 2 : nI * nJ;
+                items.push_back({t, make_int2(b, P << 16 | Q)});
+            }
+    std::stable_sort(items.begin(), items.end(),
+                     [](const auto& x, const auto& y) { return x.first > y.first; });
+    const int grid = (int)std::min<size_t>(items.size(), (size_t)c->num_sms);
+    std::vector<std::vector<int2>> per(grid);
+    using L = std::pair<long long, int>;  // (load, cta)
+    std::priority_queue<L, std::vector<L>, std::greater<L>> pq;
+    for (int g = 0; g < grid; ++g) pq.push({0, g});
+    for (const auto& it : items) {
+        L l = pq.top();
+        pq.pop();
+        per[l.second].push_back(it.second);
+        pq.push({l.first + it.first, l.second});
+    }
+    std::vector<int2> flat;
+    std::vector<int> beg(grid + 1, 0);
+    for (int g = 0; g < grid; ++g) {
+        beg[g] = (int)flat.size();
+        flat.insert(flat.end(), per[g].begin(), per[g].end());
+    }
+    beg[grid] = (int)flat.size();
+    cimcs_ctx::SymSched q;
+    q.nb = nb;
+    q.nRB = nRB;
+    q.grid = grid;
+    int rc;
+    if ((rc = dalloc(&q.items, flat.size() * sizeof(int2))) ||
+        (rc = dalloc(&q.sched, beg.size() * sizeof(int))))
+        return rc;
+    CK(cudaMemcpy(q.items, flat.data(), flat.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(q.sched, beg.data(), beg.size() * sizeof(int), cudaMemcpyHostToDevice));
+    c->ssched.push_back(q);
+    *out = &c->ssched.back();
+    return 0;
+}
+
 
 int ensure_stage(cimcs_ctx* c, size_t elems) {
     if (c->stage_elems >= elems) return 0;
@@ -520,10 +584,19 @@ int ensure_state(cimcs_ctx* c, int NR) {
         if ((rc = dalloc(&c->WB0, nb * 2)) || (rc = dalloc(&c->WB1, nb * 2)) ||
             (rc = dalloc(&c->WS0, ns * 4)) || (rc = dalloc(&c->WS1, ns * 4)))
             return rc;
-        const size_t ne = c->fac ? 0 : (size_t)c->B * c->nRB * c->nRB * kSyT * NR;
+        const size_t ne = c->fac ? 0 : (size_t)c->B * c->nRB * c->nSB * kSyT * NR;
         if (c->fac && ((rc = dalloc(&c->UB, (size_t)c->B * c->nMB * 2 * NR * kSyT * 2)) ||
                        (rc = dalloc(&c->US, (size_t)c->B * c->nMB * NR * 4))))
             return rc;
+        // item schedules of every instance-group split (built outside graph capture)
+        if (!c->fac)
+            for (int G = 1; G <= std::min(4, c->B); ++G)
+                for (int g = 0; g < G; ++g) {
+                    const int b0 = (int)((long long)c->B * g / G);
+                    const int b1 = (int)((long long)c->B * (g + 1) / G);
+                    const cimcs_ctx::SymSched* ss;
+                    if (b1 > b0 && (rc = sym_schedule(c, b1 - b0, &ss))) return rc;
+                }
         if (ne && c->spart_elems < ne) {
             if (c->dSpart) cudaFree(c->dSpart);
             c->dSpart = nullptr;
@@ -695,11 +768,14 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb, cudaStream_t s
     sa.WBout = g.Wout == c->W0 ? c->WB0 : c->WB1;
     sa.WSout = g.Wout == c->W0 ? c->WS0 : c->WS1;
     sa.spart = c->dSpart;
-    sa.tri = c->dTri;
     sa.ntri = c->ntri;
-    sa.ntiles = nb * c->ntri;
+    sa.nSB = c->nSB;
     sa.b0 = b0;
-    if (sa.ntiles == 0) return 0;
+    if (nb == 0 || c->ntri == 0) return 0;
+    const cimcs_ctx::SymSched* ss = nullptr;
+    if (int rc = sym_schedule(c, nb, &ss)) return rc;
+    sa.items = ss->items;
+    sa.sched = ss->sched;
     auto kern = sym_step_kernel<NR, MODE>;
     constexpr size_t smem = sy_smem_bytes<NR>();
     static unsigned long long attr = 0;  // per device: the attribute is per context
@@ -707,8 +783,7 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb, cudaStream_t s
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr |= 1ull << c->device;
     }
-    const int grid = std::min(sa.ntiles, c->num_sms);
-    kern<<<grid, kSyThreads, smem, sA>>>(sa);
+    kern<<<ss->grid, kSyThreads, smem, sA>>>(sa);
     CK(cudaGetLastError());
     if (sF != sA) {
         CK(cudaEventRecord(evA, sA));
@@ -1935,6 +2010,7 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
     // reads the canonical panels; row-sharded contexts stream their own rows)
     c->sym = c->tc && c->want_sym && c->world == 1 && !c->sharded && N > kClMaxN;
     c->ntri = c->sym ? c->nRB * (c->nRB + 1) / 2 : 0;
+    c->nSB = (c->nRB + kSyS - 1) / kSyS;
     c->M.assign(M, M + B);
     c->Mmax = *std::max_element(c->M.begin(), c->M.end());
     // factored variant: auto when A is read twice per step (phase 2 mostly misses
@@ -1997,14 +2073,7 @@ int cimcs_build_coupling(cimcs_ctx* c) {
     if (!c->dG && (rc = dalloc(&c->dG, gbytes))) return rc;
     if (!c->dhz && (rc = dalloc(&c->dhz, nv * es))) return rc;
     if (!c->dD && (rc = dalloc(&c->dD, nv * es))) return rc;
-    if (c->sym && !c->dTri) {
-        std::vector<short2> tab(c->ntri);
-        for (int I = 0; I < c->nRB; ++I)
-            for (int J = I; J < c->nRB; ++J) tab[sy_tri(I, J, c->nRB)] = make_short2(I, J);
-        if ((rc = dalloc(&c->dTri, c->ntri * sizeof(short2))) || (rc = dalloc(&c->dSg, c->B * 4)))
-            return rc;
-        CK(cudaMemcpy(c->dTri, tab.data(), tab.size() * sizeof(short2), cudaMemcpyHostToDevice));
-    }
+    if (c->sym && !c->dSg && (rc = dalloc(&c->dSg, c->B * 4))) return rc;
     if (c->fac) {
         // task table: phase 1 of instance b + skew is interleaved with phase 2 of b
         const int nP1 = c->nMB, nP2 = (c->nRB + c->fac_w2 - 1) / c->fac_w2;

@@ -15,11 +15,19 @@
 // no value leaves fp16's normal range.  G w ~= G_hi [w_hi | w_lo] + G_lo w_hi,
 // accumulated in fp32 in TMEM, and unscaled exactly.
 //
-// A row block K receives nRB partial products (one per tile touching it),
-// written to [B][nRB][slot][128][NR].  A second, evenly spread kernel
-// (sym_update_kernel, one CTA per block, 4 replicas per thread) sums the slots
-// in a FIXED order (deterministic) and runs the fused Euler / Jacobi / score /
-// matvec update (the arithmetic of tc_row_update); no CTA waits for another.
+// Work is split into super-block ITEMS of up to kSyS x kSyS tiles (rows
+// [I0, I0 + kSyS) x columns [J0, J0 + kSyS) of the tile triangle).  The tile
+// epilogue sums the unscaled products of an item in registers, so an item
+// emits one partial per row block (use 1) and one per column block (use 2)
+// instead of one per tile and use: a row block K receives nSB = ceil(nRB /
+// kSyS) partials, written to [B][nRB][slot = nSB][128][NR] (4x fewer bytes at
+// N = 2000, small enough to stay in L2 until the update reads them).  Items
+// are placed on the persistent CTAs by a host LPT schedule (largest first onto
+// the least-loaded CTA), so every role of a CTA walks the same static list.
+// A second, evenly spread kernel (sym_update_kernel, one CTA per block, 4
+// replicas per thread) sums the slots in a FIXED order (deterministic) and runs
+// the fused Euler / Jacobi / score / matvec update (the arithmetic of
+// tc_row_update); no CTA waits for another.
 // (Fusing the finish into the tile kernel -- last-arriving CTA, or owner-CTA
 // finisher warps with an L2-resident ring of partials -- was measured slower:
 // each finish is a chain of dependent L2 round trips behind the tile stream.)
@@ -33,8 +41,8 @@
 // Persistent, warp-specialised CTA (one per SM, 6 warps):
 //   warp 0      producer: per tile bulk copies of G_hi, G_lo (32 KB each) and
 //               the two 8 KB B tiles
-//   warp 1      MMA issuer: 8 k-steps x (2 + 2) MMAs, double-buffered TMEM
-//   warps 2-5   tile epilogue: TMEM -> unscaled partial products
+//   warp 1      MMA issuer: 8 k-steps x (2 + 2) MMAs, kSyAcc TMEM accumulators
+//   warps 2-5   tile epilogue: TMEM -> unscaled products, summed per item
 #pragma once
 
 #include <cuda_fp16.h>
@@ -48,7 +56,10 @@ constexpr int kSyStages = 2;
 constexpr int kSyPlaneHalfs = kSyT * kSyT;             // 16384
 constexpr uint32_t kSyPlaneBytes = kSyPlaneHalfs * 2;  // 32 KB
 constexpr int kSyThreads = 6 * 32;
-constexpr int kSyTmemCols = 128;
+constexpr int kSyS = 4;                                // item edge in tiles
+constexpr int kSyAcc = 4;                              // TMEM accumulator buffers
+template <int NR>
+__host__ __device__ constexpr int sy_tmem_cols() { return kSyAcc * 4 * NR; }  // 256 (NR 16) / 128 (NR 8)
 
 // byte offset of element (mn, k) of an fp16 operand in the canonical no-swizzle
 // K-major layout (core matrix = 8 MN rows x 8 K = 16 bytes per row)
@@ -168,9 +179,10 @@ struct SymArgs {
     const int* WSin;       // [B][nRB][NR] their scale exponents
     __half* WBout;         // same for the output w (step / Jacobi modes)
     int* WSout;
-    float* spart;          // [B][nRB][nRB][128][NR]
-    const short2* tri;     // [ntri] -> (I, J)
-    int ntri, ntiles;      // tiles per instance, tiles of this launch (nb * ntri)
+    float* spart;          // [B][nRB][nSB][128][NR]
+    const int2* items;     // (b - b0, P << 16 | Q): super-block (P, Q), P <= Q
+    const int* sched;      // [grid + 1] item range of each CTA
+    int ntri, nSB;         // tiles per instance, super-blocks per row
     int b0;                // first instance of this launch (instance groups)
 };
 
@@ -183,6 +195,25 @@ __host__ __device__ constexpr size_t sy_stage_bytes() {
 template <int NR>
 __host__ __device__ constexpr size_t sy_smem_bytes() {
     return kSyStages * sy_stage_bytes<NR>() + 16 * 8 + 64;
+}
+
+// item k -> instance, first row / column block, extents
+struct SyItem {
+    int b, P, Q, I0, J0, nI, nJ;
+    bool diag;
+};
+__device__ __forceinline__ SyItem sy_item(const SymArgs& sa, int k, int nRB) {
+    const int2 it = sa.items[k];
+    SyItem r;
+    r.b = sa.b0 + it.x;
+    r.P = it.y >> 16;
+    r.Q = it.y & 0xffff;
+    r.I0 = r.P * kSyS;
+    r.J0 = r.Q * kSyS;
+    r.nI = min(kSyS, nRB - r.I0);
+    r.nJ = min(kSyS, nRB - r.J0);
+    r.diag = r.P == r.Q;
+    return r;
 }
 
 // fp16 B tile + scales of one 128-row block from the values w[q] of row k
@@ -231,25 +262,26 @@ __global__ void __launch_bounds__(128) sym_wconvert_kernel(const float* __restri
 template <int NR, int MODE>
 __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    const TcArgs& a = sa.t;
     constexpr uint32_t kBB = (uint32_t)sy_bbytes<NR>();
     constexpr uint32_t kStage = (uint32_t)sy_stage_bytes<NR>();
+    constexpr int kCols = sy_tmem_cols<NR>();
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSyStages * kStage);
     uint64_t* full = bars;                    // [2] G planes + B tiles landed
     uint64_t* empty = full + kSyStages;       // [2] MMAs of the stage retired
-    uint64_t* tm_full = empty + kSyStages;    // [2] accumulators complete
-    uint64_t* tm_empty = tm_full + 2;         // [2] accumulators drained
+    uint64_t* tm_full = empty + kSyStages;    // [kSyAcc] accumulators complete
+    uint64_t* tm_empty = tm_full + kSyAcc;    // [kSyAcc] accumulators drained
     __shared__ uint32_t s_tmem;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nRB = a.nRB;
+    const int nRB = sa.t.nRB;
+    const int it0 = sa.sched[blockIdx.x], it1 = sa.sched[blockIdx.x + 1];
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kSyStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kSyAcc; ++k) {
             mbar_init(&tm_full[k], 1);
             mbar_init(&tm_empty[k], 4);
         }
@@ -258,7 +290,7 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(&s_tmem)),
-                     "n"(kSyTmemCols));
+                     "n"(kCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -271,25 +303,28 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
         if (lane == 0) {
             const uint64_t pG = sy_policy_first(), pW = sy_policy_last();
             int tt = 0;
-            for (int tile = blockIdx.x; tile < sa.ntiles; tile += gridDim.x, ++tt) {
-                const int s = tt % kSyStages;
-                const int b = sa.b0 + tile / sa.ntri;
-                const short2 ij = sa.tri[tile % sa.ntri];
-                if (tt >= kSyStages) mbar_wait(&empty[s], ((tt / kSyStages) - 1) & 1);
-                const __half* src =
-                    sa.Gs + ((size_t)sa.b0 * sa.ntri + tile) * 2 * kSyPlaneHalfs;
-                const __half* wb = sa.WBin + (size_t)b * nRB * (2 * NR * kSyT);
-                unsigned char* st = smem + s * kStage;
-                const bool off = ij.x != ij.y;
-                mbar_arrive_expect_tx(&full[s], 2 * kSyPlaneBytes + (off ? 2 : 1) * kBB);
-                // the gram streams through L2 once per step; w tiles are re-read
-                sy_bulk_g2s(st, src, kSyPlaneBytes, &full[s], pG);
-                sy_bulk_g2s(st + kSyPlaneBytes, src + kSyPlaneHalfs, kSyPlaneBytes, &full[s], pG);
-                sy_bulk_g2s(st + 2 * kSyPlaneBytes, wb + (size_t)ij.y * (2 * NR * kSyT), kBB,
-                            &full[s], pW);
-                if (off)
-                    sy_bulk_g2s(st + 2 * kSyPlaneBytes + kBB, wb + (size_t)ij.x * (2 * NR * kSyT),
-                                kBB, &full[s], pW);
+            for (int k = it0; k < it1; ++k) {
+                const SyItem m = sy_item(sa, k, nRB);
+                const __half* wb = sa.WBin + (size_t)m.b * nRB * (2 * NR * kSyT);
+                const __half* gb = sa.Gs + (size_t)m.b * sa.ntri * 2 * kSyPlaneHalfs;
+                for (int ii = 0; ii < m.nI; ++ii)
+                    for (int jj = m.diag ? ii : 0; jj < m.nJ; ++jj, ++tt) {
+                        const int I = m.I0 + ii, J = m.J0 + jj, s = tt % kSyStages;
+                        if (tt >= kSyStages) mbar_wait(&empty[s], ((tt / kSyStages) - 1) & 1);
+                        const __half* src = gb + (size_t)sy_tri(I, J, nRB) * 2 * kSyPlaneHalfs;
+                        unsigned char* st = smem + s * kStage;
+                        const bool off = I != J;
+                        mbar_arrive_expect_tx(&full[s], 2 * kSyPlaneBytes + (off ? 2 : 1) * kBB);
+                        // the gram streams through L2 once per step; w tiles are re-read
+                        sy_bulk_g2s(st, src, kSyPlaneBytes, &full[s], pG);
+                        sy_bulk_g2s(st + kSyPlaneBytes, src + kSyPlaneHalfs, kSyPlaneBytes,
+                                    &full[s], pG);
+                        sy_bulk_g2s(st + 2 * kSyPlaneBytes, wb + (size_t)J * (2 * NR * kSyT), kBB,
+                                    &full[s], pW);
+                        if (off)
+                            sy_bulk_g2s(st + 2 * kSyPlaneBytes + kBB,
+                                        wb + (size_t)I * (2 * NR * kSyT), kBB, &full[s], pW);
+                    }
             }
         }
     } else if (warp == 1) {
@@ -300,78 +335,109 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
             constexpr uint32_t kstr = (kSyT / 8) * 128;   // K-group stride of the tile (2 KB)
             constexpr uint32_t lboB = (2 * NR / 8) * 128;  // K-group stride of a B tile
             int tt = 0;
-            for (int tile = blockIdx.x; tile < sa.ntiles; tile += gridDim.x, ++tt) {
-                const int s = tt % kSyStages, acc = tt & 1;
-                const short2 ij = sa.tri[tile % sa.ntri];
-                const bool off = ij.x != ij.y;
-                if (tt >= 2) mbar_wait(&tm_empty[acc], ((tt / 2) - 1) & 1);
-                mbar_wait(&full[s], (tt / kSyStages) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t aHi = smem_u32(smem + s * kStage), aLo = aHi + kSyPlaneBytes;
-                const uint32_t bJ = aHi + 2 * kSyPlaneBytes, bI = bJ + kBB;
-                const uint32_t d1 = tmem + acc * 4 * NR, d2 = d1 + 2 * NR;
+            for (int k = it0; k < it1; ++k) {
+                const SyItem m = sy_item(sa, k, nRB);
+                for (int ii = 0; ii < m.nI; ++ii)
+                    for (int jj = m.diag ? ii : 0; jj < m.nJ; ++jj, ++tt) {
+                        const int s = tt % kSyStages, acc = tt % kSyAcc;
+                        const bool off = m.I0 + ii != m.J0 + jj;
+                        if (tt >= kSyAcc) mbar_wait(&tm_empty[acc], ((tt / kSyAcc) - 1) & 1);
+                        mbar_wait(&full[s], (tt / kSyStages) & 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        const uint32_t aHi = smem_u32(smem + s * kStage), aLo = aHi + kSyPlaneBytes;
+                        const uint32_t bJ = aHi + 2 * kSyPlaneBytes, bI = bJ + kBB;
+                        const uint32_t d1 = tmem + acc * 4 * NR, d2 = d1 + 2 * NR;
 #pragma unroll
-                for (int kb = 0; kb < kSyT / 16; ++kb) {
-                    const uint32_t first = kb ? 1u : 0u;
-                    const uint64_t dBJ = umma_desc(bJ + kb * 2 * lboB, lboB, 128);
-                    sy_mma(d1, umma_desc(aHi + kb * 2 * kstr, kstr, 128), dBJ, id_cat, first);
-                    sy_mma(d1, umma_desc(aLo + kb * 2 * kstr, kstr, 128), dBJ, id_hi, 1u);
-                    if (off) {  // transposed view: K' = tile rows, 16 per k-step = 256 B
-                        const uint64_t dBI = umma_desc(bI + kb * 2 * lboB, lboB, 128);
-                        sy_mma(d2, umma_desc(aHi + kb * 256, 128, kstr), dBI, id_catT, first);
-                        sy_mma(d2, umma_desc(aLo + kb * 256, 128, kstr), dBI, id_hiT, 1u);
+                        for (int kb = 0; kb < kSyT / 16; ++kb) {
+                            const uint32_t first = kb ? 1u : 0u;
+                            const uint64_t dBJ = umma_desc(bJ + kb * 2 * lboB, lboB, 128);
+                            sy_mma(d1, umma_desc(aHi + kb * 2 * kstr, kstr, 128), dBJ, id_cat, first);
+                            sy_mma(d1, umma_desc(aLo + kb * 2 * kstr, kstr, 128), dBJ, id_hi, 1u);
+                            if (off) {  // transposed view: K' = tile rows, 16 per k-step = 256 B
+                                const uint64_t dBI = umma_desc(bI + kb * 2 * lboB, lboB, 128);
+                                sy_mma(d2, umma_desc(aHi + kb * 256, 128, kstr), dBI, id_catT, first);
+                                sy_mma(d2, umma_desc(aLo + kb * 256, 128, kstr), dBI, id_hiT, 1u);
+                            }
+                        }
+                        tc_commit(&empty[s]);
+                        tc_commit(&tm_full[acc]);
                     }
-                }
-                tc_commit(&empty[s]);
-                tc_commit(&tm_full[acc]);
             }
         }
     } else {
         // ------------------------------------------------ tile epilogue
+        // Thread `row` owns row `row` of every row block of the item (use 1)
+        // and column `row` of every column block (use 2); products are unscaled
+        // exactly (2^-(s_G + s_w)) and summed per item in tile order.
         const int ew = warp & 3;         // TMEM lane quadrant of this warp
-        const int row = ew * 32 + lane;  // row of the tile (use 1) / column (use 2)
+        const int row = ew * 32 + lane;
         const uint64_t pP = sy_policy_last();
-        int tt = 0;
-        for (int tile = blockIdx.x; tile < sa.ntiles; tile += gridDim.x, ++tt) {
-            const int acc = tt & 1;
-            const int b = sa.b0 + tile / sa.ntri;
-            const short2 ij = sa.tri[tile % sa.ntri];
-            const int I = ij.x, J = ij.y;
-            mbar_wait(&tm_full[acc], (tt / 2) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            float g1[NR], g2[NR];
-            const uint32_t tq = tmem + acc * 4 * NR + ((uint32_t)(ew * 32) << 16);
-            tmem_ld_row<NR>(tq, g1);
-            if (I != J) tmem_ld_row<NR>(tq + 2 * NR, g2);
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tm_empty[acc]);
-
-            // partial products, unscaled exactly: 2^-(s_G + s_w)
-            float* part = sa.spart + (size_t)b * nRB * nRB * kSyT * NR;
-            const float fG = sy_pow2(-sa.sg[b]);
-            const int* wsJ = sa.WSin + ((size_t)b * nRB + J) * NR;
-            float4* pI = reinterpret_cast<float4*>(part + (((size_t)I * nRB + J) * kSyT + row) * NR);
+        const int nSB = sa.nSB;
+        auto put = [&](int b, int K, int slot, const float (&v)[NR]) {
+            float4* p = reinterpret_cast<float4*>(
+                sa.spart + ((((size_t)b * nRB + K) * nSB + slot) * kSyT + row) * NR);
 #pragma unroll
             for (int q = 0; q < NR; q += 4)
-                sy_st_last(pI + q / 4,
-                           make_float4(g1[q] * fG * sy_pow2(-__ldg(wsJ + q)),
-                                       g1[q + 1] * fG * sy_pow2(-__ldg(wsJ + q + 1)),
-                                       g1[q + 2] * fG * sy_pow2(-__ldg(wsJ + q + 2)),
-                                       g1[q + 3] * fG * sy_pow2(-__ldg(wsJ + q + 3))),
-                           pP);
-            if (I != J) {
-                const int* wsI = sa.WSin + ((size_t)b * nRB + I) * NR;
-                float4* pJ =
-                    reinterpret_cast<float4*>(part + (((size_t)J * nRB + I) * kSyT + row) * NR);
+                sy_st_last(p + q / 4, make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]), pP);
+        };
+        int tt = 0;
+        for (int k = it0; k < it1; ++k) {
+            const SyItem m = sy_item(sa, k, nRB);
+            const float fG = sy_pow2(-sa.sg[m.b]);
+            const int* ws = sa.WSin + (size_t)m.b * nRB * NR;
+            float cacc[kSyS][NR];
 #pragma unroll
-                for (int q = 0; q < NR; q += 4)
-                    sy_st_last(pJ + q / 4,
-                               make_float4(g2[q] * fG * sy_pow2(-__ldg(wsI + q)),
-                                           g2[q + 1] * fG * sy_pow2(-__ldg(wsI + q + 1)),
-                                           g2[q + 2] * fG * sy_pow2(-__ldg(wsI + q + 2)),
-                                           g2[q + 3] * fG * sy_pow2(-__ldg(wsI + q + 3))),
-                               pP);
+            for (int jj = 0; jj < kSyS; ++jj)
+#pragma unroll
+                for (int q = 0; q < NR; ++q) cacc[jj][q] = 0.f;
+#pragma unroll
+            for (int ii = 0; ii < kSyS; ++ii) {
+                if (ii < m.nI) {
+                    float racc[NR];
+#pragma unroll
+                    for (int q = 0; q < NR; ++q) racc[q] = 0.f;
+#pragma unroll
+                    for (int jj = 0; jj < kSyS; ++jj) {
+                        if (jj < m.nJ && (!m.diag || jj >= ii)) {
+                            const int I = m.I0 + ii, J = m.J0 + jj;
+                            const bool off = I != J;
+                            const int acc = tt % kSyAcc;
+                            mbar_wait(&tm_full[acc], (tt / kSyAcc) & 1);
+                            ++tt;
+                            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                            float g1[NR], g2[NR];
+                            const uint32_t tq = tmem + acc * 4 * NR + ((uint32_t)(ew * 32) << 16);
+                            tmem_ld_row<NR>(tq, g1);
+                            if (off) tmem_ld_row<NR>(tq + 2 * NR, g2);
+                            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&tm_empty[acc]);
+#pragma unroll
+                            for (int q = 0; q < NR; ++q) {
+                                const float v = g1[q] * (fG * sy_pow2(-__ldg(ws + J * NR + q)));
+                                if (m.diag)
+                                    cacc[ii][q] += v;
+                                else
+                                    racc[q] += v;
+                            }
+                            if (off) {
+#pragma unroll
+                                for (int q = 0; q < NR; ++q)
+                                    cacc[jj][q] += g2[q] * (fG * sy_pow2(-__ldg(ws + I * NR + q)));
+                            }
+                        }
+                    }
+                    // row block I0 + ii is complete: all its tiles of this item are done
+                    if (m.diag)
+                        put(m.b, m.I0 + ii, m.P, cacc[ii]);
+                    else
+                        put(m.b, m.I0 + ii, m.Q, racc);
+                }
+            }
+            if (!m.diag) {
+#pragma unroll
+                for (int jj = 0; jj < kSyS; ++jj)
+                    if (jj < m.nJ) put(m.b, m.J0 + jj, m.P, cacc[jj]);
             }
         }
     }
@@ -379,11 +445,11 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
     __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                     "n"(kSyTmemCols));
+                     "n"(kCols));
 }
 
 // Second pass of a step in ONE kernel, 4 replicas per thread: block (b, K) is
-// handled by 128 x (NR / 4) threads; thread (row, g) sums its 4 replicas' nRB
+// handled by 128 x (NR / 4) threads; thread (row, g) sums its 4 replicas' nSB
 // partial products in slot order (deterministic), runs the fused update of
 // tc_row_update for replicas 4g..4g+3 and, in step / Jacobi modes, emits the
 // fp16 B tile of the new w.  4x the threads of a row-per-thread update: the
@@ -404,19 +470,20 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
     // ---- slot sums
     float gw[4];
     {
+        const int nSB = sa.nSB;
         const float4* src = reinterpret_cast<const float4*>(
-                                sa.spart + (((size_t)b * nRB + K) * nRB * kSyT + row) * NR) +
+                                sa.spart + (((size_t)b * nRB + K) * nSB * kSyT + row) * NR) +
                             g;
         constexpr size_t kSlot4 = (size_t)kSyT * NR / 4;
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int s0 = 0; s0 < nRB; s0 += 8) {
+        for (int s0 = 0; s0 < nSB; s0 += 8) {
             float4 v[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u)
-                if (s0 + u < nRB) v[u] = __ldcs(src + (s0 + u) * kSlot4);
+                if (s0 + u < nSB) v[u] = __ldcs(src + (s0 + u) * kSlot4);
 #pragma unroll
             for (int u = 0; u < 8; ++u)
-                if (s0 + u < nRB) {
+                if (s0 + u < nSB) {
                     acc.x = acc.x + v[u].x;
                     acc.y = acc.y + v[u].y;
                     acc.z = acc.z + v[u].z;
