@@ -408,6 +408,11 @@ struct cimcs_ctx {
 
 namespace {
 
+// contraction-input layout: the streaming and factored tcgen05 kernels read W
+// as the canonical [W | W_lo] operand (tc_wofs); the symmetric-tile path and
+// the CUDA-core paths use [b][i][r] (coalesced float4 rows in the update)
+inline int wcanon(const cimcs_ctx* c) { return c->tc && (!c->sym || c->fac) ? 1 : 0; }
+
 void drop_graphs(cimcs_ctx* c) {
     if (c->g_cim) cudaGraphExecDestroy(c->g_cim);
     if (c->g_refit) cudaGraphExecDestroy(c->g_refit);
@@ -892,8 +897,8 @@ int sym_sync_w(cimcs_ctx* c, const void* W) {
     const dim3 g(c->nRB, c->B);
     DISPATCH_NR_TC(c->NR, {
         sym_wconvert_kernel<NR_><<<g, 128, 0, c->stream>>>(
-            static_cast<const float*>(W), c->N, c->ldJ, c->nRB, w0 ? c->WB0 : c->WB1,
-            w0 ? c->WS0 : c->WS1);
+            static_cast<const float*>(W), c->N, c->ldJ, c->ldN, wcanon(c), c->nRB,
+            w0 ? c->WB0 : c->WB1, w0 ? c->WS0 : c->WS1);
     });
     CK(cudaGetLastError());
     return 0;
@@ -924,12 +929,12 @@ int run_init_T(cimcs_ctx* c, int Rreal, int bn, const double* dc0, const double*
             init_state_kernel<T, NR_, 1><<<g, 256, 0, c->stream>>>(
                 dc0, Rreal, c->N, c->ldN, c->B, static_cast<const T*>(c->Rs),
                 static_cast<T*>(c->C), static_cast<T*>(c->E), W, c->fail_gstep, c->minE, rt,
-                de0, c->tc ? 1 : 0, c->ldJ);
+                de0, wcanon(c), c->ldJ);
         else
             init_state_kernel<T, NR_, 0><<<g, 256, 0, c->stream>>>(
                 dc0, Rreal, c->N, c->ldN, c->B, static_cast<const T*>(c->Rs),
                 static_cast<T*>(c->C), static_cast<T*>(c->E), W, c->fail_gstep, c->minE, rt,
-                de0, c->tc ? 1 : 0, c->ldJ);
+                de0, wcanon(c), c->ldJ);
     });
     CK(cudaGetLastError());
     return sym_sync_w(c, c->W0);
@@ -946,7 +951,7 @@ int run_support_T(cimcs_ctx* c) {
     DISPATCH_NR(c->NR, {
         support_kernel<T, NR_><<<g, 256, 0, c->stream>>>(
             static_cast<const T*>(c->C), static_cast<const T*>(c->Rs), c->sig,
-            static_cast<T*>(c->W0), c->fail_gstep, c->N, c->ldN, c->B, c->tc ? 1 : 0, c->ldJ);
+            static_cast<T*>(c->W0), c->fail_gstep, c->N, c->ldN, c->B, wcanon(c), c->ldJ);
     });
     CK(cudaGetLastError());
     return sym_sync_w(c, c->W0);
@@ -1038,7 +1043,7 @@ int mask_T(cimcs_ctx* c, void* V) {
     DISPATCH_NR(c->NR, {
         mask_kernel<T, NR_><<<g, 256, 0, c->stream>>>(static_cast<const T*>(c->Rs), c->sig,
                                                       static_cast<T*>(V), c->state_elems(), c->N,
-                                                      c->ldN, c->ldJ, c->tc ? 1 : 0);
+                                                      c->ldN, c->ldJ, wcanon(c));
     });
     CK(cudaGetLastError());
     return sym_sync_w(c, V);
@@ -1158,7 +1163,7 @@ int launch_cluster_t(cimcs_ctx* c, GemvArgs a, int n_iters) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         attr |= 1ull << c->device;
     }
-    a.tc_in = c->tc ? 1 : 0;
+    a.tc_in = wcanon(c);
     const unsigned cs = (unsigned)((c->N + kClRows - 1) / kClRows);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(c->B * cs);
@@ -1318,7 +1323,7 @@ CgArgs cg_args(cimcs_ctx* c, const cimcs_hyper* hp) {
     a.fail_gstep = c->fail_gstep;
     a.W = c->W0;
     a.n_live = c->cg_live;
-    a.tc = c->tc ? 1 : 0;
+    a.tc = wcanon(c);
     a.ldJ = c->ldJ;
     a.N = c->N;
     a.ldN = c->ldN;

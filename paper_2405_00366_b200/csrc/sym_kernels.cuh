@@ -58,6 +58,7 @@ constexpr uint32_t kSyPlaneBytes = kSyPlaneHalfs * 2;  // 32 KB
 constexpr int kSyThreads = 6 * 32;
 constexpr int kSyS = 4;                                // item edge in tiles
 constexpr int kSyAcc = 4;                              // TMEM accumulator buffers
+constexpr int kSyBarBytes = 256;                       // mbarriers after the stages
 template <int NR>
 __host__ __device__ constexpr int sy_tmem_cols() { return kSyAcc * 4 * NR; }  // 256 (NR 16) / 128 (NR 8)
 
@@ -194,7 +195,7 @@ __host__ __device__ constexpr size_t sy_stage_bytes() {
 }
 template <int NR>
 __host__ __device__ constexpr size_t sy_smem_bytes() {
-    return kSyStages * sy_stage_bytes<NR>() + 16 * 8 + 64;
+    return kSyStages * sy_stage_bytes<NR>() + kSyBarBytes + (size_t)kSyS * NR * kSyT * 4;
 }
 
 // item k -> instance, first row / column block, extents
@@ -247,13 +248,16 @@ __device__ __forceinline__ void sy_emit_block(const float (&w)[NR], int k, int l
 // W other than the symmetric kernel (init, support, mask, CG).
 template <int NR>
 __global__ void __launch_bounds__(128) sym_wconvert_kernel(const float* __restrict__ W, int N,
-                                                           int ldJ, int nRB, __half* WB, int* WS) {
+                                                           int ldJ, int ldN, int canon, int nRB,
+                                                           __half* WB, int* WS) {
     __shared__ unsigned s_max[4][NR];
     const int X = blockIdx.x, b = blockIdx.y, k = threadIdx.x;
     const int j = X * kSyT + k;
     float w[NR];
 #pragma unroll
-    for (int q = 0; q < NR; ++q) w[q] = j < N ? W[tc_wofs(ldJ, NR, b, j, q)] : 0.f;
+    for (int q = 0; q < NR; ++q)
+        w[q] = j >= N ? 0.f
+                      : (canon ? W[tc_wofs(ldJ, NR, b, j, q)] : W[((size_t)b * ldN + j) * NR + q]);
     sy_emit_block<NR>(w, k, k & 31, k >> 5, s_max,
                       WB + ((size_t)b * nRB + X) * (2 * NR * kSyT),
                       WS + ((size_t)b * nRB + X) * NR, 1);
@@ -368,11 +372,14 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
         // ------------------------------------------------ tile epilogue
         // Thread `row` owns row `row` of every row block of the item (use 1)
         // and column `row` of every column block (use 2); products are unscaled
-        // exactly (2^-(s_G + s_w)) and summed per item in tile order.
+        // exactly (2^-(s_G + s_w)) and summed per item in tile order: the row
+        // block in registers, the column blocks in shared memory (own row only,
+        // [kSyS][NR][128]: conflict-free), so the loops need no unrolling.
         const int ew = warp & 3;         // TMEM lane quadrant of this warp
         const int row = ew * 32 + lane;
         const uint64_t pP = sy_policy_last();
         const int nSB = sa.nSB;
+        float* cs = reinterpret_cast<float*>(smem + kSyStages * kStage + kSyBarBytes) + row;
         auto put = [&](int b, int K, int slot, const float (&v)[NR]) {
             float4* p = reinterpret_cast<float4*>(
                 sa.spart + ((((size_t)b * nRB + K) * nSB + slot) * kSyT + row) * NR);
@@ -380,65 +387,60 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
             for (int q = 0; q < NR; q += 4)
                 sy_st_last(p + q / 4, make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]), pP);
         };
+        auto put_cs = [&](int b, int K, int slot, int jj) {
+            float v[NR];
+#pragma unroll
+            for (int q = 0; q < NR; ++q) v[q] = cs[(jj * NR + q) * kSyT];
+            put(b, K, slot, v);
+        };
         int tt = 0;
         for (int k = it0; k < it1; ++k) {
             const SyItem m = sy_item(sa, k, nRB);
             const float fG = sy_pow2(-sa.sg[m.b]);
             const int* ws = sa.WSin + (size_t)m.b * nRB * NR;
-            float cacc[kSyS][NR];
+            for (int jj = 0; jj < m.nJ; ++jj)
 #pragma unroll
-            for (int jj = 0; jj < kSyS; ++jj)
+                for (int q = 0; q < NR; ++q) cs[(jj * NR + q) * kSyT] = 0.f;
+            for (int ii = 0; ii < m.nI; ++ii) {
+                float racc[NR];
 #pragma unroll
-                for (int q = 0; q < NR; ++q) cacc[jj][q] = 0.f;
+                for (int q = 0; q < NR; ++q) racc[q] = 0.f;
+                for (int jj = m.diag ? ii : 0; jj < m.nJ; ++jj, ++tt) {
+                    const int I = m.I0 + ii, J = m.J0 + jj;
+                    const bool off = I != J;
+                    const int acc = tt % kSyAcc;
+                    mbar_wait(&tm_full[acc], (tt / kSyAcc) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    float g1[NR], g2[NR];
+                    const uint32_t tq = tmem + acc * 4 * NR + ((uint32_t)(ew * 32) << 16);
+                    tmem_ld_row<NR>(tq, g1);
+                    if (off) tmem_ld_row<NR>(tq + 2 * NR, g2);
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tm_empty[acc]);
+                    if (m.diag) {  // both uses land in the item's own blocks
 #pragma unroll
-            for (int ii = 0; ii < kSyS; ++ii) {
-                if (ii < m.nI) {
-                    float racc[NR];
+                        for (int q = 0; q < NR; ++q)
+                            cs[(ii * NR + q) * kSyT] += g1[q] * (fG * sy_pow2(-__ldg(ws + J * NR + q)));
+                    } else {
 #pragma unroll
-                    for (int q = 0; q < NR; ++q) racc[q] = 0.f;
-#pragma unroll
-                    for (int jj = 0; jj < kSyS; ++jj) {
-                        if (jj < m.nJ && (!m.diag || jj >= ii)) {
-                            const int I = m.I0 + ii, J = m.J0 + jj;
-                            const bool off = I != J;
-                            const int acc = tt % kSyAcc;
-                            mbar_wait(&tm_full[acc], (tt / kSyAcc) & 1);
-                            ++tt;
-                            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                            float g1[NR], g2[NR];
-                            const uint32_t tq = tmem + acc * 4 * NR + ((uint32_t)(ew * 32) << 16);
-                            tmem_ld_row<NR>(tq, g1);
-                            if (off) tmem_ld_row<NR>(tq + 2 * NR, g2);
-                            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive(&tm_empty[acc]);
-#pragma unroll
-                            for (int q = 0; q < NR; ++q) {
-                                const float v = g1[q] * (fG * sy_pow2(-__ldg(ws + J * NR + q)));
-                                if (m.diag)
-                                    cacc[ii][q] += v;
-                                else
-                                    racc[q] += v;
-                            }
-                            if (off) {
-#pragma unroll
-                                for (int q = 0; q < NR; ++q)
-                                    cacc[jj][q] += g2[q] * (fG * sy_pow2(-__ldg(ws + I * NR + q)));
-                            }
-                        }
+                        for (int q = 0; q < NR; ++q)
+                            racc[q] += g1[q] * (fG * sy_pow2(-__ldg(ws + J * NR + q)));
                     }
-                    // row block I0 + ii is complete: all its tiles of this item are done
-                    if (m.diag)
-                        put(m.b, m.I0 + ii, m.P, cacc[ii]);
-                    else
-                        put(m.b, m.I0 + ii, m.Q, racc);
-                }
-            }
-            if (!m.diag) {
+                    if (off) {
 #pragma unroll
-                for (int jj = 0; jj < kSyS; ++jj)
-                    if (jj < m.nJ) put(m.b, m.J0 + jj, m.P, cacc[jj]);
+                        for (int q = 0; q < NR; ++q)
+                            cs[(jj * NR + q) * kSyT] += g2[q] * (fG * sy_pow2(-__ldg(ws + I * NR + q)));
+                    }
+                }
+                // row block I0 + ii is complete: all its tiles of this item are done
+                if (m.diag)
+                    put_cs(m.b, m.I0 + ii, m.P, ii);
+                else
+                    put(m.b, m.I0 + ii, m.Q, racc);
             }
+            if (!m.diag)
+                for (int jj = 0; jj < m.nJ; ++jj) put_cs(m.b, m.J0 + jj, m.P, jj);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -449,21 +451,26 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
 }
 
 // Second pass of a step in ONE kernel, 4 replicas per thread: block (b, K) is
-// handled by 128 x (NR / 4) threads; thread (row, g) sums its 4 replicas' nSB
-// partial products in slot order (deterministic), runs the fused update of
-// tc_row_update for replicas 4g..4g+3 and, in step / Jacobi modes, emits the
-// fp16 B tile of the new w.  4x the threads of a row-per-thread update: the
-// chains of dependent loads of different threads overlap.
+// handled by 128 x (NR / 4) threads; thread (row, g), g = t % (NR / 4) fastest
+// so a warp reads whole 64-byte state rows (coalesced float4), sums its 4
+// replicas' nSB partial products in slot order (deterministic), runs the fused
+// update of tc_row_update for replicas 4g..4g+3 and, in step / Jacobi modes,
+// emits the fp16 B tile of the new w (staged in shared memory, stored with
+// 16-byte vectors).
 template <int NR, int MODE>
 __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_update_kernel(SymArgs sa) {
     constexpr int QG = NR / 4;
-    __shared__ unsigned s_max[QG][4][4];    // [group][warp of the group][replica]
-    __shared__ double s_sc[QG][4][4][3];    // score partials
+    constexpr int NW = kSyT * QG / 32;         // warps per CTA
+    __shared__ unsigned s_max[NW][NR];          // per warp, per replica max |w|
+    __shared__ int s_exp[NR];
+    __shared__ float s_min[NW][NR];             // per warp, per replica min e (step modes)
+    __shared__ double s_sc[NW][NR][3];          // score partials
+    __shared__ __align__(16) __half s_B[2 * NR * kSyT];
     const TcArgs& a = sa.t;
     const StepScalars& sc = a.s;
     const int K = blockIdx.x, b = sa.b0 + blockIdx.y, nRB = a.nRB, N = a.N;
-    const int t = threadIdx.x, row = t % kSyT, g = t / kSyT;
-    const int lane = t & 31, wg = row >> 5;  // warp inside the group
+    const int t = threadIdx.x, g = t % QG, row = t / QG;
+    const int lane = t & 31, wid = t >> 5;
     const int i = K * kSyT + row, q0 = 4 * g;
     const bool valid = i < N;
     const size_t si = (size_t)b * a.ldN + i, vi0 = si * NR + q0;
@@ -503,12 +510,11 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
     if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
         float lmin[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
         if (valid) {
-            float wv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) wv[u] = __ldg(a.Win + tc_wofs(a.ldJ, NR, b, i, q0 + u));
+            const float4 w4 = __ldg(reinterpret_cast<const float4*>(a.Win + vi0));
             const float4 r4 = __ldg(reinterpret_cast<const float4*>(a.Rs + vi0));
             const float4 c4 = *reinterpret_cast<const float4*>(a.C + vi0);
             const float4 e4 = *reinterpret_cast<const float4*>(a.E + vi0);
+            const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
             const float Rv[4] = {r4.x, r4.y, r4.z, r4.w}, cv[4] = {c4.x, c4.y, c4.z, c4.w};
             const float ev[4] = {e4.x, e4.y, e4.z, e4.w};
             const float Dv = __ldg(a.D + si), hzv = __ldg(a.hz + si);
@@ -518,7 +524,7 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
             const float loss = sc.minus_j != 0.0 ? (float)((-1.0 + pd) - sc.minus_j)
                                                  : (float)(-1.0 + pd);
             const float thresh = (float)a.alt->thresh;
-            float cn[4], en[4];
+            float cn[4], en[4], wo[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const float c = cv[u], e = ev[u];
@@ -532,6 +538,7 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
                 const float inj = (Kj * e) * (Rv[u] * h - thresh);
                 cn[u] = c + dt * ((loss - c * c) * c + inj);
                 en[u] = e + dt * ((nbeta * (c * c - tau)) * e);
+                wo[u] = wv[u];  // frozen / failing trajectories keep their output w
                 if (fz[u]) {
                     cn[u] = c;
                     en[u] = e;
@@ -547,44 +554,52 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
                         w = Rv[u] * (cn[u] > 0.f ? 1.f : 0.f);
                     else
                         w = (Rv[u] * 0.25f) * (cn[u] + rt);
-                    a.Wout[tc_wofs(a.ldJ, NR, b, i, q0 + u)] = w;
+                    wo[u] = w;
                     wn[u] = w;
                 }
             }
             *reinterpret_cast<float4*>(a.C + vi0) = make_float4(cn[0], cn[1], cn[2], cn[3]);
             *reinterpret_cast<float4*>(a.E + vi0) = make_float4(en[0], en[1], en[2], en[3]);
+            *reinterpret_cast<float4*>(a.Wout + vi0) = make_float4(wo[0], wo[1], wo[2], wo[3]);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 4; ++u) {  // min e: warp, then CTA (one atomic per replica)
             float m = lmin[u];
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1)
+            for (int off = 16; off >= QG; off >>= 1)
                 m = fminf(m, __shfl_xor_sync(0xffffffffu, m, off));
-            if (lane == u && m != INFINITY) atomicMin(&a.minE[b * NR + q0 + u], ord_key(m));
+            if (lane < QG) s_min[wid][q0 + u] = m;
         }
     } else if constexpr (MODE == EPI_JACOBI) {
         if (valid) {
             const float Dv = __ldg(a.D + si), bv = __ldg(a.hz + si);
             const float omd = (float)sc.one_minus_dtc, dtc = (float)sc.dt_c;
+            float4 r4 = *reinterpret_cast<const float4*>(a.Rs + vi0);
+            const float4 w4 = *reinterpret_cast<const float4*>(a.Win + vi0);
+            float* Rv = &r4.x;
+            float wo[4] = {w4.x, w4.y, w4.z, w4.w};
+            const char4 s4 = *reinterpret_cast<const char4*>(a.sigma + vi0);
+            const bool on4[4] = {s4.x != 0, s4.y != 0, s4.z != 0, s4.w != 0};
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 if (fz[u]) continue;
-                const float Rv = a.Rs[vi0 + u];
-                const bool on = a.sigma[vi0 + u] != 0;
-                float rn = Rv;
+                const bool on = on4[u];
+                float rn = Rv[u];
                 if (on) {
                     if (Dv == 0.f) {
                         atomicMin(a.err, i);
                         continue;
                     }
-                    const float off = gw[u] - Dv * Rv;
-                    rn = omd * Rv + dtc * ((bv - off) / Dv);
-                    a.Rs[vi0 + u] = rn;
+                    const float off = gw[u] - Dv * Rv[u];
+                    rn = omd * Rv[u] + dtc * ((bv - off) / Dv);
+                    Rv[u] = rn;
                 }
                 const float w = rn * (on ? 1.f : 0.f);
-                a.Wout[tc_wofs(a.ldJ, NR, b, i, q0 + u)] = w;
+                wo[u] = w;
                 wn[u] = w;
             }
+            *reinterpret_cast<float4*>(a.Rs + vi0) = r4;
+            *reinterpret_cast<float4*>(a.Wout + vi0) = make_float4(wo[0], wo[1], wo[2], wo[3]);
         }
     } else if constexpr (MODE == EPI_MATVEC) {
         if (valid) {
@@ -594,11 +609,14 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
         }
     } else {  // EPI_SCORE: w.Gw, hz.w, |w - x|^2 partials of this 128-row block
         double pa[4], pb[4], pc[4];
+        float4 w4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) w4 = *reinterpret_cast<const float4*>(a.Win + vi0);
+        const float wv4[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             pa[u] = pb[u] = pc[u] = 0.0;
             if (valid && !fz[u]) {
-                const double wv = a.Win[tc_wofs(a.ldJ, NR, b, i, q0 + u)];
+                const double wv = wv4[u];
                 pa[u] = wv * (double)gw[u];
                 pb[u] = (double)a.hz[si] * wv;
                 if (a.xtrue) {
@@ -607,29 +625,29 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
                 }
             }
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
+            for (int off = 16; off >= QG; off >>= 1) {
                 pa[u] += __shfl_xor_sync(0xffffffffu, pa[u], off);
                 pb[u] += __shfl_xor_sync(0xffffffffu, pb[u], off);
                 pc[u] += __shfl_xor_sync(0xffffffffu, pc[u], off);
             }
         }
-        if (lane == 0) {
+        if (lane < QG) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                s_sc[g][wg][u][0] = pa[u];
-                s_sc[g][wg][u][1] = pb[u];
-                s_sc[g][wg][u][2] = pc[u];
+                s_sc[wid][q0 + u][0] = pa[u];
+                s_sc[wid][q0 + u][1] = pb[u];
+                s_sc[wid][q0 + u][2] = pc[u];
             }
         }
         __syncthreads();
-        if (row < 4) {  // thread (g, u = row) writes replica q0 + u
+        if (t < NR) {  // thread t writes replica t: warps summed in a fixed order
             double A_ = 0, B_ = 0, C_ = 0;
-            for (int w = 0; w < 4; ++w) {
-                A_ += s_sc[g][w][row][0];
-                B_ += s_sc[g][w][row][1];
-                C_ += s_sc[g][w][row][2];
+            for (int w = 0; w < NW; ++w) {
+                A_ += s_sc[w][t][0];
+                B_ += s_sc[w][t][1];
+                C_ += s_sc[w][t][2];
             }
-            double* p = a.part + (((size_t)b * nRB + K) * NR + q0 + row) * 4;
+            double* p = a.part + (((size_t)b * nRB + K) * NR + t) * 4;
             p[0] = A_;
             p[1] = B_;
             p[2] = C_;
@@ -639,24 +657,38 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
         // fp16 B tile of the new w of block K: per-replica max over the 128 rows
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(wn[u])));
-            if (lane == 0) s_max[g][wg][u] = m;
+            unsigned m = __float_as_uint(fabsf(wn[u]));
+#pragma unroll
+            for (int off = 16; off >= QG; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+            if (lane < QG) s_max[wid][q0 + u] = m;
         }
         __syncthreads();
-        unsigned char* B = reinterpret_cast<unsigned char*>(sa.WBout + ((size_t)b * nRB + K) *
-                                                                           (2 * NR * kSyT));
+        if (t < NR) {
+            if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
+                float mn = INFINITY;
+                for (int w = 0; w < NW; ++w) mn = fminf(mn, s_min[w][t]);
+                if (mn != INFINITY) atomicMin(&a.minE[b * NR + t], ord_key(mn));
+            }
+            unsigned m = 0;
+            for (int w = 0; w < NW; ++w) m = max(m, s_max[w][t]);
+            const int e = sy_exp14(__uint_as_float(m));
+            s_exp[t] = e;
+            sa.WSout[((size_t)b * nRB + K) * NR + t] = e;
+        }
+        __syncthreads();
+        unsigned char* Bs = reinterpret_cast<unsigned char*>(s_B);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const unsigned m = max(max(s_max[g][0][u], s_max[g][1][u]),
-                                   max(s_max[g][2][u], s_max[g][3][u]));
-            const int e = sy_exp14(__uint_as_float(m));
-            const float ws = wn[u] * sy_pow2(e);
+            const float ws = wn[u] * sy_pow2(s_exp[q0 + u]);
             const __half hi = __float2half_rn(ws);
             const __half lo = __float2half_rn(ws - __half2float(hi));
-            *reinterpret_cast<__half*>(B + sy_offk(q0 + u, row, 2 * NR)) = hi;
-            *reinterpret_cast<__half*>(B + sy_offk(NR + q0 + u, row, 2 * NR)) = lo;
-            if (row == 0) sa.WSout[((size_t)b * nRB + K) * NR + q0 + u] = e;
+            *reinterpret_cast<__half*>(Bs + sy_offk(q0 + u, row, 2 * NR)) = hi;
+            *reinterpret_cast<__half*>(Bs + sy_offk(NR + q0 + u, row, 2 * NR)) = lo;
         }
+        __syncthreads();
+        uint4* dst = reinterpret_cast<uint4*>(sa.WBout + ((size_t)b * nRB + K) * (2 * NR * kSyT));
+        const uint4* srcB = reinterpret_cast<const uint4*>(s_B);
+        for (int o = t; o < 2 * NR * kSyT / 8; o += kSyT * QG) dst[o] = srcB[o];
     }
 }
 
