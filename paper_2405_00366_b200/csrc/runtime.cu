@@ -331,6 +331,7 @@ struct cimcs_ctx {
     int* dSg = nullptr;    // per-instance gram scale exponent
     float* dSpart = nullptr;  // partial products [B][nRB][nSB][128][NR]
     int sym_groups = 0;       // instance groups pipelined across two streams (0: auto)
+    bool use_pdl = true;      // programmatic dependent launch between the step kernels
     // factored coupling A^T (A w) from fp16 hi/lo tiles of A (fac_kernels.cuh)
     int fac_opt = -1;         // -1 auto, 0 off, 1 on (a symmetric-path variant)
     int fac_requested = -1;
@@ -788,14 +789,29 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb, cudaStream_t s
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr |= 1ull << c->device;
     }
-    kern<<<ss->grid, kSyThreads, smem, sA>>>(sa);
-    CK(cudaGetLastError());
+    // same stream: both kernels use programmatic dependent launch (the next
+    // kernel's prologue overlaps this one's tail; griddepcontrol.wait orders data)
+    const bool pdl = sF == sA && c->use_pdl;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ss->grid);
+    cfg.blockDim = dim3(kSyThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = sA;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, kern, sa));
     if (sF != sA) {
         CK(cudaEventRecord(evA, sA));
         CK(cudaStreamWaitEvent(sF, evA, 0));
     }
-    sym_update_kernel<NR, MODE><<<dim3(c->nRB, nb), kSyT * NR / 4, 0, sF>>>(sa);
-    CK(cudaGetLastError());
+    cfg.gridDim = dim3(c->nRB, nb);
+    cfg.blockDim = dim3(kSyT * NR / 4);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = sF;
+    CK(cudaLaunchKernelEx(&cfg, sym_update_kernel<NR, MODE>, sa));
     return 0;
 }
 
@@ -1951,6 +1967,10 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
     if (k == "host_threads") c->host_threads = (int)std::max<int64_t>(1, v);
     else if (k == "use_graphs") c->use_graphs = v != 0;
     else if (k == "gram_blas") c->gram_blas = v > 0 ? 1 : (v < 0 ? -1 : 0);
+    else if (k == "pdl") {
+        c->use_pdl = v != 0;
+        drop_graphs(c);
+    }
     else if (k == "sym_groups") c->sym_groups = (int)std::min<int64_t>(4, std::max<int64_t>(0, v));
     else if (k == "fac_skew") {
         c->fac_skew = (int)std::max<int64_t>(0, v);  // applied by build_coupling

@@ -157,6 +157,12 @@ __device__ __forceinline__ uint64_t sy_policy_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+// programmatic dependent launch (no-ops without the launch attribute)
+__device__ __forceinline__ void sy_pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void sy_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // bulk copy global -> shared with an L2 eviction-priority hint
 __device__ __forceinline__ void sy_bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                             uint64_t* bar, uint64_t pol) {
@@ -301,6 +307,11 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = s_tmem;
+    // programmatic dependent launch: the update kernel may be scheduled now (its
+    // CTAs wait for this grid in griddepcontrol.wait); this grid's own reads of
+    // w and writes of the partial products wait for the previous update kernel
+    sy_pdl_trigger();
+    sy_pdl_wait();
 
     if (warp == 0) {
         // ------------------------------------------------------ producer
@@ -474,6 +485,7 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
     const int i = K * kSyT + row, q0 = 4 * g;
     const bool valid = i < N;
     const size_t si = (size_t)b * a.ldN + i, vi0 = si * NR + q0;
+    sy_pdl_wait();  // the tile kernel's partial products
     // ---- slot sums
     float gw[4];
     {
@@ -690,6 +702,7 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
         const uint4* srcB = reinterpret_cast<const uint4*>(s_B);
         for (int o = t; o < 2 * NR * kSyT / 8; o += kSyT * QG) dst[o] = srcB[o];
     }
+    sy_pdl_trigger();  // late: the next tile kernel only overlaps the last CTAs
 }
 
 }  // namespace cimcs
