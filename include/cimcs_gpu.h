@@ -98,6 +98,31 @@ int cimcs_gen_instances(int32_t B, int32_t N, const double* alpha, const double*
                         double* const* y, double* const* x_true, int32_t* const* xi_true,
                         int32_t threads);
 
+/* ----------------------------------------- bundles and CSV (host, io.hpp) */
+/* format_double, io.hpp:13 / io.cpp:18-25: shortest text that round-trips. */
+int cimcs_format_double(double v, char* buf, int32_t cap);
+/* fnv1a64, io.hpp:16 / io.cpp:27-34 */
+uint64_t cimcs_fnv1a64(const char* bytes, uint64_t n);
+/* save_instance, io.hpp:20-28 / io.cpp:86-125.  A is M x N column-major;
+ * x_true / xi_true may be NULL (no truth.csv). */
+int cimcs_save_instance(const char* dir, int32_t N, int32_t M, const double* A, const double* y,
+                        const double* x_true, const int32_t* xi_true, double a, double alpha,
+                        double nu, uint64_t seed);
+/* load_instance, io.hpp:29 / io.cpp:127-167, in two calls: A == NULL reads
+ * meta.json (N, M, has_truth, a, alpha, nu, seed); then, with *N / *M as
+ * returned and caller-sized arrays, the CSVs (x_true / xi_true filled only
+ * when has_truth).  Row / column count mismatches are input errors. */
+int cimcs_load_instance(const char* dir, int32_t* N, int32_t* M, int32_t* has_truth, double* a,
+                        double* alpha, double* nu, uint64_t* seed, double* A, double* y,
+                        double* x_true, int32_t* xi_true);
+/* CsvWriter, io.hpp:31-48 / io.cpp:169-196: "# " comment lines, header,
+ * rows of exactly ncols cells (else input_error); written on close. */
+typedef struct cimcs_csv cimcs_csv;
+int cimcs_csv_open(const char* path, const char* const* comments, int32_t ncomments,
+                   const char* const* columns, int32_t ncols, cimcs_csv** out);
+int cimcs_csv_row(cimcs_csv* w, const char* const* cells, int32_t n);
+int cimcs_csv_close(cimcs_csv* w);
+
 /* ------------------------------------------------------------ context */
 /* One per host thread; owns device buffers, one CUDA stream and graphs. */
 int cimcs_create(int32_t device, int32_t dtype, cimcs_ctx** out);

@@ -25,7 +25,9 @@ EXPORTS = (
     "cimcs_gen_instances", "cimcs_create", "cimcs_destroy", "cimcs_set_option",
     "cimcs_set_problems", "cimcs_build_coupling", "cimcs_get_coupling", "cimcs_mfz_step",
     "cimcs_run_cim", "cimcs_run_pp", "cimcs_refit", "cimcs_cdp_minimize", "cimcs_score", "cimcs_solve", "cimcs_get_timing",
-    "cimcs_nccl_unique_id", "cimcs_create_sharded",
+    "cimcs_nccl_unique_id", "cimcs_create_sharded", "cimcs_format_double", "cimcs_fnv1a64",
+    "cimcs_save_instance", "cimcs_load_instance", "cimcs_csv_open", "cimcs_csv_row",
+    "cimcs_csv_close",
 )
 
 
@@ -97,6 +99,14 @@ def load() -> C.CDLL:
     L.cimcs_get_timing.argtypes = [vp, vp]
     L.cimcs_nccl_unique_id.argtypes = [vp, i32]
     L.cimcs_create_sharded.argtypes = [i32, i32, i32, i32, vp, vp]
+    L.cimcs_format_double.argtypes = [d, C.c_char_p, i32]
+    L.cimcs_fnv1a64.restype = u64
+    L.cimcs_fnv1a64.argtypes = [C.c_char_p, u64]
+    L.cimcs_save_instance.argtypes = [C.c_char_p, i32, i32, vp, vp, vp, vp, d, d, d, u64]
+    L.cimcs_load_instance.argtypes = [C.c_char_p, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.cimcs_csv_open.argtypes = [C.c_char_p, vp, i32, vp, i32, vp]
+    L.cimcs_csv_row.argtypes = [vp, vp, i32]
+    L.cimcs_csv_close.argtypes = [vp]
     _lib = L
     return L
 

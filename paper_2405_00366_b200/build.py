@@ -24,6 +24,24 @@ FLAGS = [
 LIBS = ["-lnccl", "-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
 
 
+def _torch_nccl_dir():
+    """torch's bundled libnccl.so.2 (newer than the system copy): linking and
+    rpath-ing it first means whichever of torch / this library loads first, the
+    process gets the one NCCL both can use."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations or []) if spec else []:
+        d = os.path.join(base, "nccl", "lib")
+        if os.path.exists(os.path.join(d, "libnccl.so.2")):
+            return d
+    return None
+
+
+_NCCL = _torch_nccl_dir()
+if _NCCL:
+    LIBS = ["-L" + _NCCL, "-Xlinker", "-rpath," + _NCCL, "-l:libnccl.so.2"] + LIBS[1:]
+
+
 def stale() -> bool:
     if not os.path.exists(LIB):
         return True

@@ -390,7 +390,7 @@ class Context:
 
 
 # ------------------------------------------------------------ public API
-def _trial_dict(res, b, r, n_steps):
+def trial_dict(res, b, r, n_steps):
     nh = int(res["n_hist"][b, r])
     H = res["history"][b, r, :nh]
     hist = [dict(i=int(h["i"]), eta=float(h["eta"]), hamiltonian=float(h["hamiltonian"]),
@@ -424,7 +424,7 @@ def solve(instance: Instance, backend: str = "mfz-bn", params: HyperParams | Non
         ctx.set_problems([instance])
         ctx.build_coupling()
         res = ctx.solve(1, backend, params, [seed], track_best=track_best, cdp=cdp)
-    return _trial_dict(res, 0, 0, params.n_steps)
+    return trial_dict(res, 0, 0, params.n_steps)
 
 
 def replica_seeds(instances: Sequence[Instance], R: int, backend: str) -> np.ndarray:

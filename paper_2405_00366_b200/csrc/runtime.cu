@@ -25,6 +25,7 @@
 
 #include "../../include/cimcs_gpu.h"
 #include "host_rng.hpp"
+#include "io.hpp"
 #include "kernels.cuh"
 #include "tc_kernels.cuh"
 #include "cg_kernels.cuh"
@@ -1845,6 +1846,97 @@ int cimcs_gen_dims(int32_t N, double alpha, double a, int32_t* M, int32_t* K) {
     if (M) *M = m;
     if (K) *K = k;
     return 0;
+}
+
+// ------------------------------------------------ bundles and CSV (io.hpp)
+int cimcs_format_double(double v, char* buf, int32_t cap) {
+    const std::string s = cimcs_io::fmt_double(v);
+    if (!buf || cap < (int32_t)s.size() + 1) return fail(CIMCS_INPUT_ERROR, "format_double: buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return 0;
+}
+
+uint64_t cimcs_fnv1a64(const char* bytes, uint64_t n) {
+    return cimcs_io::fnv1a(reinterpret_cast<const unsigned char*>(bytes), (size_t)n);
+}
+
+int cimcs_save_instance(const char* dir, int32_t N, int32_t M, const double* A, const double* y,
+                        const double* x_true, const int32_t* xi_true, double a, double alpha,
+                        double nu, uint64_t seed) {
+    if (!dir || N < 1 || M < 1 || !A || !y) return fail(CIMCS_INPUT_ERROR, "save_instance: bad arguments");
+    cimcs_io::Meta m;
+    m.N = N;
+    m.M = M;
+    m.a = a;
+    m.alpha = alpha;
+    m.nu = nu;
+    m.seed = seed;
+    std::string err;
+    if (!cimcs_io::save_bundle(dir, m, A, y, x_true, xi_true, &err)) return fail(CIMCS_INPUT_ERROR, err);
+    return 0;
+}
+
+int cimcs_load_instance(const char* dir, int32_t* N, int32_t* M, int32_t* has_truth, double* a,
+                        double* alpha, double* nu, uint64_t* seed, double* A, double* y,
+                        double* x_true, int32_t* xi_true) {
+    if (!dir || !N || !M) return fail(CIMCS_INPUT_ERROR, "load_instance: bad arguments");
+    cimcs_io::Meta m;
+    bool truth = false;
+    std::string err;
+    if (!cimcs_io::load_meta(dir, &m, &truth, &err)) return fail(CIMCS_INPUT_ERROR, err);
+    if (A) {  // phase 2: the caller sized the arrays from phase 1
+        if (*N != m.N || *M != m.M) return fail(CIMCS_INPUT_ERROR, "load_instance: size mismatch");
+        if (!y || !cimcs_io::load_arrays(dir, m, A, y, truth ? x_true : nullptr,
+                                         truth ? xi_true : nullptr, &err))
+            return fail(CIMCS_INPUT_ERROR, err.empty() ? "load_instance: bad arguments" : err);
+    }
+    *N = m.N;
+    *M = m.M;
+    if (has_truth) *has_truth = truth ? 1 : 0;
+    if (a) *a = m.a;
+    if (alpha) *alpha = m.alpha;
+    if (nu) *nu = m.nu;
+    if (seed) *seed = m.seed;
+    return 0;
+}
+
+struct cimcs_csv : cimcs_io::Csv {};
+
+int cimcs_csv_open(const char* path, const char* const* comments, int32_t ncomments,
+                   const char* const* columns, int32_t ncols, cimcs_csv** out) {
+    if (!path || !out || ncols < 0 || ncomments < 0) return fail(CIMCS_INPUT_ERROR, "csv_open: bad arguments");
+    auto* w = new cimcs_csv();
+    w->path = path;
+    w->ncols = (size_t)ncols;
+    for (int k = 0; k < ncomments; ++k) (w->buf += "# ") += std::string(comments[k]) + "\n";
+    for (int k = 0; k < ncols; ++k) {
+        if (k) w->buf += ',';
+        w->buf += columns[k];
+    }
+    w->buf += '\n';
+    *out = w;
+    return 0;
+}
+
+int cimcs_csv_row(cimcs_csv* w, const char* const* cells, int32_t n) {
+    if (!w || n < 0 || (size_t)n != w->ncols) return fail(CIMCS_INPUT_ERROR, "CsvWriter: cell count mismatch");
+    for (int k = 0; k < n; ++k) {
+        if (k) w->buf += ',';
+        w->buf += cells[k];
+    }
+    w->buf += '\n';
+    return 0;
+}
+
+int cimcs_csv_close(cimcs_csv* w) {
+    if (!w) return 0;
+    std::error_code ec;
+    const std::filesystem::path p(w->path);
+    std::filesystem::create_directories(p.parent_path().empty() ? "." : p.parent_path(), ec);
+    std::string err;
+    const bool ok = cimcs_io::put_file(p, w->buf, &err);
+    delete w;
+    return ok ? 0 : fail(CIMCS_INPUT_ERROR, err);
 }
 
 int cimcs_gen_instance(int32_t N, double alpha, double a, double nu, uint64_t seed, double* A,
