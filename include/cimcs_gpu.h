@@ -123,6 +123,10 @@ int cimcs_csv_open(const char* path, const char* const* comments, int32_t ncomme
 int cimcs_csv_row(cimcs_csv* w, const char* const* cells, int32_t n);
 int cimcs_csv_close(cimcs_csv* w);
 
+/* make_mask, mri.hpp:45 / mri.cpp:185-207: M distinct k-space positions of an
+ * H x W grid (reference Rng, partial Fisher-Yates), sorted into out[M]. */
+int cimcs_make_mask(int32_t H, int32_t W, int32_t M, uint64_t seed, int32_t* out);
+
 /* ------------------------------------------------------------ context */
 /* One per host thread; owns device buffers, one CUDA stream and graphs. */
 int cimcs_create(int32_t device, int32_t dtype, cimcs_ctx** out);
@@ -150,6 +154,18 @@ int cimcs_set_problems(cimcs_ctx* ctx, int32_t B, int32_t N, const int32_t* M,
  * resident.  Replaces coupling_from_observation (model.cpp:54-63) and the
  * per-step matrix-free A^T(A w) (orchestrator.cpp:86-88): J w = D∘w - G w. */
 int cimcs_build_coupling(cimcs_ctx* ctx);
+/* Matrix-free transform-chain problem: MriTransform(target_image, mask, gamma)
+ * + make_problem(t, &truth) (mri.hpp:46-99, mri.cpp:209-256, 393-411).
+ * target is H x W row-major (H, W powers of two, H*W <= 16384), mask the M
+ * sampled k-space indices (unique, in range), x_true the Haar coefficients of
+ * the target (nullable; xi = x != 0).  B = 1, fp32 contexts only.  Then
+ * cimcs_build_coupling computes hz = Re(A^H y) and diag(G); the quadratic form
+ * G = Re(A^H A) + gamma Psi (Dv'Dv + Dh'Dh) Psi' is applied matrix-free every
+ * step (mri_kernels.cuh).  Refits always use CG (orchestrator.cpp:128-133);
+ * damped Jacobi is a config_error (cdp.cpp:158-159).  get_coupling returns
+ * G by applying the chain to every basis vector. */
+int cimcs_set_mri_problem(cimcs_ctx* ctx, int32_t H, int32_t W, const double* target,
+                          int32_t M, const int32_t* mask, double gamma, const double* x_true);
 /* Copy instance b's coupling back (fp64 host buffers; N*N, N, N).  Test aid. */
 int cimcs_get_coupling(cimcs_ctx* ctx, int32_t b, double* G, double* hz, double* D);
 

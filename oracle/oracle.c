@@ -320,6 +320,27 @@ int orc_problem_init(orc_problem* p, int N, int M, const double* A, const double
     return 0;
 }
 
+/* make_problem(G_full, hz), orchestrator.cpp:100-115 (and, restated through the
+ * assembled matrix, the operator form make_problem(N, apply, diag, hz) :117-136):
+ * mode EXPLICIT with G given (row-major N x N, copied), no A. */
+int orc_problem_init_gram(orc_problem* p, int N, const double* G, const double* hz) {
+    memset(p, 0, sizeof(*p));
+    p->N = N;
+    p->M = 0;
+    p->mode = ORC_EXPLICIT;
+    p->nseg = 8;
+    p->gran = 8;
+    p->hz = (double*)malloc(sizeof(double) * (size_t)N);
+    p->D = (double*)malloc(sizeof(double) * (size_t)N);
+    p->work = (double*)malloc(sizeof(double) * (size_t)N);
+    p->G = (double*)malloc(sizeof(double) * (size_t)N * N);
+    if (!p->hz || !p->D || !p->work || !p->G) return 1;
+    memcpy(p->G, G, sizeof(double) * (size_t)N * N);
+    memcpy(p->hz, hz, sizeof(double) * (size_t)N);
+    for (int i = 0; i < N; ++i) p->D[i] = G[(size_t)i * N + i];
+    return 0;
+}
+
 void orc_problem_free(orc_problem* p) {
     free(p->G);
     free(p->hz);
@@ -633,6 +654,16 @@ int orc_cdp_minimize(const orc_problem* p, const int32_t* sigma, const double* R
             b[c] = p->hz[act[c]];
             D[c] = p->G[(size_t)act[c] * N + act[c]];
         }
+    } else if (!p->A) {
+        /* gram-given problem (orc_problem_init_gram): G_sub = G[act, act],
+         * b = hz[act] (cdp_minimize(G_full, hz, ...) orchestrator.cpp:110-113 /
+         * cdp_minimize_operator's restricted apply, cdp.cpp:161-167) */
+        Gs = (double*)malloc(sizeof(double) * (size_t)k * k);
+        for (int r = 0; r < k; ++r) {
+            for (int c = 0; c < k; ++c) Gs[(size_t)r * k + c] = p->G[(size_t)act[r] * N + act[c]];
+            b[r] = p->hz[act[r]];
+        }
+        for (int c = 0; c < k; ++c) D[c] = Gs[(size_t)c * k + c];
     } else {
         /* A_act^T A_act, A_act^T y (sequential) -- identical in LITERAL and
          * EXPLICIT since both build G sequentially without FMA. */

@@ -106,6 +106,7 @@ typedef struct {
     const int32_t* xi_true;
 } orc_problem;
 
+int orc_problem_init_gram(orc_problem* p, int N, const double* G, const double* hz);
 int orc_problem_init(orc_problem* p, int N, int M, const double* A, const double* y,
                      int mode, int nseg, int gran);
 void orc_problem_free(orc_problem* p);

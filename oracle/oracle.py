@@ -95,6 +95,7 @@ def lib():
         L.orc_eta_schedule.argtypes = [i, d, d, i]
         L.orc_trace_stride.argtypes = [i, i]
         L.orc_problem_init.argtypes = [vp, i, i, vp, vp, i, i, i]
+        L.orc_problem_init_gram.argtypes = [vp, i, vp, vp]
         L.orc_canon_dot.restype = d
         L.orc_canon_dot.argtypes = [vp, vp, i, i, i]
         L.orc_local_field_cn.argtypes = [vp, vp, vp, d, vp]
@@ -304,6 +305,27 @@ class Problem:
             lib().orc_problem_free(C.byref(self._p))
         except Exception:
             pass
+
+    @classmethod
+    def from_gram(cls, G, hz, x_true=None, xi_true=None):
+        """make_problem(G_full, hz) (orchestrator.cpp:100-115): an assembled
+        quadratic form (e.g. mri.assemble_operators) instead of an instance."""
+        self = cls.__new__(cls)
+        G = np.ascontiguousarray(G, np.float64)
+        self._G = G
+        self._hz = np.ascontiguousarray(hz, np.float64)
+        self.N, self.M = G.shape[0], 0
+        self.inst = None
+        self.A = self.y = None
+        self._x = None if x_true is None else np.ascontiguousarray(x_true, np.float64)
+        self._xi = None if xi_true is None else np.ascontiguousarray(xi_true, np.int32)
+        self.mode = EXPLICIT
+        self._p = _Problem()
+        if lib().orc_problem_init_gram(C.byref(self._p), self.N, _p(G), _p(self._hz)):
+            raise InputError("problem init failed")
+        self._p.x_true = _p(self._x)
+        self._p.xi_true = _p(self._xi)
+        return self
 
     @property
     def has_truth(self):

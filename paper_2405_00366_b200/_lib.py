@@ -27,7 +27,7 @@ EXPORTS = (
     "cimcs_run_cim", "cimcs_run_pp", "cimcs_refit", "cimcs_cdp_minimize", "cimcs_score", "cimcs_solve", "cimcs_get_timing",
     "cimcs_nccl_unique_id", "cimcs_create_sharded", "cimcs_format_double", "cimcs_fnv1a64",
     "cimcs_save_instance", "cimcs_load_instance", "cimcs_csv_open", "cimcs_csv_row",
-    "cimcs_csv_close",
+    "cimcs_csv_close", "cimcs_make_mask", "cimcs_set_mri_problem",
 )
 
 
@@ -107,6 +107,8 @@ def load() -> C.CDLL:
     L.cimcs_csv_open.argtypes = [C.c_char_p, vp, i32, vp, i32, vp]
     L.cimcs_csv_row.argtypes = [vp, vp, i32]
     L.cimcs_csv_close.argtypes = [vp]
+    L.cimcs_make_mask.argtypes = [i32, i32, i32, u64, vp]
+    L.cimcs_set_mri_problem.argtypes = [vp, i32, i32, vp, i32, vp, d, vp]
     _lib = L
     return L
 

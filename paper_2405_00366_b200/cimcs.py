@@ -269,15 +269,30 @@ class Context:
             P(xis) if truth else None))
         self.B, self.N = B, N
 
+    def set_mri_problem(self, target_image, mask, gamma: float, x_true=None):
+        """MriTransform(target_image, mask, gamma) + make_problem(t, &truth)
+        (mri.hpp:46-99, mri.cpp:393-411): the matrix-free transform-chain
+        problem (one instance, fp32 contexts)."""
+        img = np.ascontiguousarray(target_image, np.float64)
+        H, W = img.shape
+        m = np.ascontiguousarray(mask, np.int32)
+        x = None if x_true is None else np.ascontiguousarray(x_true, np.float64).reshape(-1)
+        if x is not None and x.size != H * W:
+            raise InputError("make_problem: truth length mismatch")
+        _check(self._lib.cimcs_set_mri_problem(self._ctx, H, W, img.ctypes.data, m.size,
+                                               m.ctypes.data, float(gamma),
+                                               None if x is None else x.ctypes.data))
+        self.B, self.N = 1, H * W
+
     def build_coupling(self):
         _check(self._lib.cimcs_build_coupling(self._ctx))
 
-    def get_coupling(self, b: int):
-        G = np.zeros((self.N, self.N))
+    def get_coupling(self, b: int, gram: bool = True):
+        G = np.zeros((self.N, self.N)) if gram else None
         hz = np.zeros(self.N)
         D = np.zeros(self.N)
-        _check(self._lib.cimcs_get_coupling(self._ctx, b, G.ctypes.data, hz.ctypes.data,
-                                            D.ctypes.data))
+        _check(self._lib.cimcs_get_coupling(self._ctx, b, None if G is None else G.ctypes.data,
+                                            hz.ctypes.data, D.ctypes.data))
         return G, hz, D
 
     def mfz_step(self, R: int, backend: str, hp: HyperParams, eta: float, p: float, Rsig, c, e):

@@ -31,6 +31,7 @@
 #include "cg_kernels.cuh"
 #include "cluster_kernels.cuh"
 #include "sym_kernels.cuh"
+#include "mri_kernels.cuh"
 #include "fac_kernels.cuh"
 
 using namespace cimcs;
@@ -343,6 +344,13 @@ struct cimcs_ctx {
     __half* UB = nullptr;     // fp16 B tiles of u = A w [B][nMB][2NR x 128]
     int* US = nullptr;
     int gram_blas = 0;        // symmetric gram from cuBLAS DGEMM panels: 0 auto (N >= 8192), 1, -1
+    // matrix-free MRI transform-chain problem (mri_kernels.cuh; mri.hpp:46-99)
+    bool mri = false;
+    int mH = 0, mW = 0, mL = 0;
+    float mgamma = 0.f;
+    unsigned char* dMaskBr = nullptr;  // [H*W] sampled, bit-reversed coordinates
+    float2* dTw = nullptr;             // [L/2] exp(-2 pi i k / L)
+    float* dTarget = nullptr;          // [H*W] target image (row-major)
     cublasHandle_t blas = nullptr;
     cudaStream_t sfin = nullptr;             // stream of the reduction / update kernels
     cudaEvent_t evA[4] = {}, evF[4] = {};    // per group: tiles done / update done
@@ -460,7 +468,7 @@ void free_state(cimcs_ctx* c) {
 void free_problems(cimcs_ctx* c) {
     free_state(c);
     void* ptrs[] = {c->dA, c->dy, c->dM, c->dG, c->dD, c->dhz, c->dx, c->dxi,
-                    c->dSg, c->dSpart, c->dTask, c->dCnt};
+                    c->dSg, c->dSpart, c->dTask, c->dCnt, c->dMaskBr, c->dTw, c->dTarget};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& q : c->ssched) {
@@ -472,6 +480,10 @@ void free_problems(cimcs_ctx* c) {
     c->dCnt = nullptr;
     c->dSg = nullptr;
     c->dSpart = nullptr;
+    c->dMaskBr = nullptr;
+    c->dTw = nullptr;
+    c->dTarget = nullptr;
+    c->mri = false;
     c->spart_elems = 0;
     c->dA = c->dy = nullptr;
     c->dM = nullptr;
@@ -584,6 +596,16 @@ int ensure_state(cimcs_ctx* c, int NR) {
         for (int g = 0; g < 4; ++g) {
             CK(cudaEventCreateWithFlags(&c->evA[g], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&c->evF[g], cudaEventDisableTiming));
+        }
+    }
+    if (c->mri) {  // G w of the transform chain, one slot: [N][NR]
+        const size_t ne = (size_t)c->nRB * kSyT * NR;
+        if (c->spart_elems < ne) {
+            if (c->dSpart) cudaFree(c->dSpart);
+            c->dSpart = nullptr;
+            c->spart_elems = 0;
+            if ((rc = dalloc(&c->dSpart, ne * 4))) return rc;
+            c->spart_elems = ne;
         }
     }
     if (c->sym) {  // fp16 B tiles of W0/W1 and the partial products of the symmetric kernel
@@ -894,7 +916,69 @@ int launch_tc_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
     }
 }
 
+// one mri_kernel launch of `grid` CTAs (basis vectors r0.. for DIAG / COLS)
+int mri_launch(cimcs_ctx* c, int mode, int grid, int r0, const float* in, float* out) {
+    MriArgs ma{};
+    ma.H = c->mH;
+    ma.W = c->mW;
+    ma.N = c->N;
+    ma.NR = 1;
+    ma.mask_br = c->dMaskBr;
+    ma.tw = c->dTw;
+    ma.L = c->mL;
+    ma.gamma = c->mgamma;
+    ma.scale = 1.f / (float)c->N;
+    ma.in = in;
+    ma.out = out;
+    ma.r0 = r0;
+    mri_kernel<<<grid, kMriThreads, mri_smem_bytes(c->N, c->mL), c->stream>>>(ma, mode);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+// transform-chain problems: G w by the matrix-free MRI kernel (one CTA per
+// replica slot) into the one-slot partial buffer, then the symmetric path's
+// update kernel for the fused epilogue of `mode`
+template <int NR, int MODE>
+int launch_mri_t(cimcs_ctx* c, const GemvArgs& g) {
+    MriArgs ma{};
+    ma.H = c->mH;
+    ma.W = c->mW;
+    ma.N = c->N;
+    ma.NR = NR;
+    ma.mask_br = c->dMaskBr;
+    ma.tw = c->dTw;
+    ma.L = c->mL;
+    ma.gamma = c->mgamma;
+    ma.scale = 1.f / (float)c->N;
+    ma.in = static_cast<const float*>(g.Win);
+    ma.out = c->dSpart;
+    const size_t smem = mri_smem_bytes(c->N, c->mL);
+    mri_kernel<<<NR, kMriThreads, smem, c->stream>>>(ma, MRI_APPLY);
+    CK(cudaGetLastError());
+    SymArgs sa{};
+    sa.t = tc_args(c, g);
+    sa.spart = c->dSpart;
+    sa.nSB = 1;
+    sa.b0 = 0;
+    sym_update_kernel<NR, MODE><<<dim3(c->nRB, 1), kSyT * NR / 4, 0, c->stream>>>(sa);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+template <int NR>
+int launch_mri_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
+    switch (mode) {
+        case EPI_STEP_BN: return launch_mri_t<NR, EPI_STEP_BN>(c, a);
+        case EPI_STEP_CN: return launch_mri_t<NR, EPI_STEP_CN>(c, a);
+        case EPI_MATVEC: return launch_mri_t<NR, EPI_MATVEC>(c, a);
+        case EPI_SCORE: return launch_mri_t<NR, EPI_SCORE>(c, a);
+        default: return fail(CIMCS_CONFIG_ERROR, "cdp_minimize_operator: damped Jacobi needs an assembled matrix");
+    }
+}
+
 int launch_gemv(cimcs_ctx* c, int mode, const GemvArgs& a) {
+    if (c->mri) return c->NR == 8 ? launch_mri_nr<8>(c, mode, a) : launch_mri_nr<16>(c, mode, a);
     if (c->fac) return c->NR == 8 ? launch_fac_nr<8>(c, mode, a) : launch_fac_nr<16>(c, mode, a);
     if (c->sym) return c->NR == 8 ? launch_sym_nr<8>(c, mode, a) : launch_sym_nr<16>(c, mode, a);
     if (c->tc) return c->NR == 8 ? launch_tc_nr<8>(c, mode, a) : launch_tc_nr<16>(c, mode, a);
@@ -924,7 +1008,7 @@ int sym_sync_w(cimcs_ctx* c, const void* W) {
 // replica slots: a power of two; the tensor-core path needs MMA N in {8, 16}
 int slots_for(const cimcs_ctx* c, int R) {
     const int p = pow2_slots(R);
-    return c->tc ? std::max(8, p) : p;
+    return c->tc || c->mri ? std::max(8, p) : p;
 }
 
 // Generic NR/T dispatch for the small state kernels.
@@ -1166,7 +1250,7 @@ int reconcile_cim(cimcs_ctx* c) {
 int cluster_max_nr(const cimcs_ctx* c) { return c->dtype == CIMCS_F64 ? 4 : 8; }
 
 bool cluster_ok(const cimcs_ctx* c) {
-    return c->use_cluster && c->world == 1 && !c->sharded && c->N <= kClMaxN &&
+    return c->use_cluster && !c->mri && c->world == 1 && !c->sharded && c->N <= kClMaxN &&
            c->NR <= cluster_max_nr(c);
 }
 
@@ -1668,6 +1752,8 @@ struct Events {
 constexpr int kPpChunk = 64;  // steps of unit normals per host -> device chunk
 
 int ensure_pp(cimcs_ctx* c) {  // outside any capture
+    if (c->mri)
+        return fail(CIMCS_CONFIG_ERROR, "pp backend: not on matrix-free MRI problems (fp32 MFZ only)");
     if (c->tc)
         return fail(CIMCS_CONFIG_ERROR,
                     "pp backend: use an fp64 context or tensor_cores=0 (the tcgen05 epilogues "
@@ -2176,9 +2262,124 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
     return 0;
 }
 
+int cimcs_make_mask(int32_t H, int32_t W, int32_t M, uint64_t seed, int32_t* out) {
+    const long long N = (long long)H * W;
+    if (H < 1 || W < 1) return fail(CIMCS_INPUT_ERROR, "make_mask: dims must be >= 1");
+    if (M < 1 || M > N) return fail(CIMCS_INPUT_ERROR, "make_mask: M out of range");
+    std::vector<int> pool((size_t)N);
+    for (long long k = 0; k < N; ++k) pool[k] = (int)k;
+    HostRng rng(seed);  // partial Fisher-Yates, mri.cpp:185-207
+    for (int i = 0; i < M; ++i) {
+        const long long pick = i + (long long)rng.uniform_below((uint64_t)(N - i));
+        std::swap(pool[i], pool[pick]);
+    }
+    std::sort(pool.begin(), pool.begin() + M);
+    std::copy(pool.begin(), pool.begin() + M, out);
+    return 0;
+}
+
+int cimcs_set_mri_problem(cimcs_ctx* c, int32_t H, int32_t W, const double* target,
+                          int32_t M, const int32_t* mask, double gamma, const double* x_true) {
+    if (!c) return fail(CIMCS_INPUT_ERROR, "null context");
+    auto pow2 = [](int v) { return v >= 1 && (v & (v - 1)) == 0; };
+    if (!pow2(H) || !pow2(W)) return fail(CIMCS_INPUT_ERROR, "MriTransform: dimensions must be powers of two");
+    if (H < 2 || W < 2 || H * W > kMriMaxPix)
+        return fail(CIMCS_INPUT_ERROR, "MriTransform: need 2 <= H, W and H * W <= 16384 (one CTA's shared memory)");
+    if (!(gamma >= 0.0)) return fail(CIMCS_INPUT_ERROR, "MriTransform: gamma must be >= 0");
+    if (!target || !mask || M < 1) return fail(CIMCS_INPUT_ERROR, "MriTransform: mask indices must be unique and in range");
+    std::vector<int> idx(mask, mask + M);
+    std::sort(idx.begin(), idx.end());
+    if (idx.front() < 0 || idx.back() >= H * W || std::adjacent_find(idx.begin(), idx.end()) != idx.end())
+        return fail(CIMCS_INPUT_ERROR, "MriTransform: mask indices must be unique and in range");
+    if (c->dtype != CIMCS_F32) return fail(CIMCS_CONFIG_ERROR, "matrix-free MRI problems run in fp32 contexts");
+    if (c->world > 1 || c->sharded) return fail(CIMCS_CONFIG_ERROR, "matrix-free MRI problems are single-GPU");
+    CK(cudaSetDevice(c->device));
+    free_problems(c);
+    const int N = H * W;
+    c->built = false;
+    c->mri = true;
+    c->mH = H;
+    c->mW = W;
+    c->mL = std::max(H, W);
+    c->mgamma = (float)gamma;
+    c->B = 1;
+    c->N = N;
+    c->ldN = c->ldJ = (N + 31) / 32 * 32;
+    c->tc = c->sym = c->fac = false;
+    c->RB = kSyT;
+    c->row0 = 0;
+    c->row1 = N;
+    c->rb0 = 0;
+    c->nRB = (N + kSyT - 1) / kSyT;
+    c->nSB = 1;
+    c->ntri = 0;
+    c->nch = 0;
+    c->M.assign(1, M);
+    c->Mmax = M;
+    c->has_truth = x_true != nullptr;
+    // mask in the bit-reversed coordinates of the DIF spectrum, twiddles, target
+    auto rev = [](int v, int n) {
+        int r = 0;
+        for (int b = 1; b < n; b <<= 1, v >>= 1) r = (r << 1) | (v & 1);
+        return r;
+    };
+    std::vector<unsigned char> full((size_t)N, 0), br((size_t)N, 0);
+    for (int k : idx) full[k] = 1;
+    for (int i = 0; i < H; ++i)
+        for (int j = 0; j < W; ++j) br[(size_t)i * W + j] = full[(size_t)rev(i, H) * W + rev(j, W)];
+    std::vector<float2> tw(c->mL / 2);
+    for (int k = 0; k < c->mL / 2; ++k) {
+        const double a = -2.0 * M_PI * k / c->mL;
+        tw[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    std::vector<float> tgt((size_t)N);
+    for (int k = 0; k < N; ++k) tgt[k] = (float)target[k];
+    int rc;
+    if ((rc = dalloc(&c->dMaskBr, (size_t)N)) || (rc = dalloc(&c->dTw, tw.size() * sizeof(float2))) ||
+        (rc = dalloc(&c->dTarget, (size_t)N * 4)))
+        return rc;
+    CK(cudaMemcpy(c->dMaskBr, br.data(), br.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->dTw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->dTarget, tgt.data(), tgt.size() * 4, cudaMemcpyHostToDevice));
+    static unsigned long long attr = 0;
+    if (!(attr >> c->device & 1ull)) {
+        CK(cudaFuncSetAttribute(mri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)mri_smem_bytes(kMriMaxPix, 128)));
+        attr |= 1ull << c->device;
+    }
+    if (c->has_truth) {  // make_problem(t, &truth): xi = (x != 0) (mri.cpp:398-405)
+        if ((rc = dalloc(&c->dx, (size_t)c->ldN * 8)) || (rc = dalloc(&c->dxi, (size_t)c->ldN)))
+            return rc;
+        std::vector<int8_t> xi8((size_t)c->ldN, 0);
+        for (int i = 0; i < N; ++i) xi8[i] = x_true[i] != 0.0 ? 1 : 0;
+        CK(cudaMemcpy(c->dx, x_true, (size_t)N * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->dxi, xi8.data(), xi8.size(), cudaMemcpyHostToDevice));
+    }
+    return 0;
+}
+
 int cimcs_build_coupling(cimcs_ctx* c) {
     if (!c || c->B < 1) return fail(CIMCS_INPUT_ERROR, "no problems set");
     CK(cudaSetDevice(c->device));
+    if (c->mri) {  // hz = Re(A^H y) and diag(G) of the transform chain (mri.cpp:236-254)
+        int rc;
+        const size_t nv = (size_t)c->ldN;
+        if (!c->dhz && (rc = dalloc(&c->dhz, nv * 4))) return rc;
+        if (!c->dD && (rc = dalloc(&c->dD, nv * 4))) return rc;
+        Events ev(2);
+        cudaEventRecord(ev.ev[0], c->stream);
+        CK(cudaMemsetAsync(c->dhz, 0, nv * 4, c->stream));
+        CK(cudaMemsetAsync(c->dD, 0, nv * 4, c->stream));
+        if ((rc = mri_launch(c, MRI_HZ, 1, 0, c->dTarget, static_cast<float*>(c->dhz))) ||
+            (rc = mri_launch(c, MRI_DIAG, c->N, 0, nullptr, static_cast<float*>(c->dD))))
+            return rc;
+        cudaEventRecord(ev.ev[1], c->stream);
+        CK(cudaStreamSynchronize(c->stream));
+        c->timing.gram_ms = ev.ms(0, 1);
+        c->timing.other_launches += 2;
+        c->built = true;
+        return 0;
+    }
     const size_t es = c->elt();
     // gram bytes: symmetric fp16 hi/lo tiles, canonical tf32 panels, or CUDA-core panels
     const size_t gbytes = c->fac ? (size_t)c->B * c->nMB * c->nRB * 2 * kSyPlaneBytes
@@ -2331,7 +2532,16 @@ int cimcs_get_coupling(cimcs_ctx* c, int32_t b, double* G, double* hz, double* D
         return 0;
     };
     std::vector<double> h;
-    if (G && c->fac) {  // not stored: G = A^T A in fp64 (cuBLAS) from the resident A
+    if (G && c->mri) {  // never stored: the columns G e_r of the transform chain
+        float* P = nullptr;
+        if (int rc = dalloc(&P, (size_t)N * N * 4)) return rc;
+        std::unique_ptr<float, decltype(&cudaFree)> pguard(P, &cudaFree);
+        if (int rc = mri_launch(c, MRI_COLS, N, 0, nullptr, P)) return rc;
+        CK(cudaStreamSynchronize(c->stream));  // c->stream does not sync with cudaMemcpy
+        std::vector<float> f((size_t)N * N);
+        CK(cudaMemcpy(f.data(), P, f.size() * 4, cudaMemcpyDeviceToHost));
+        for (size_t k = 0; k < f.size(); ++k) G[k] = f[k];
+    } else if (G && c->fac) {  // not stored: G = A^T A in fp64 (cuBLAS) from the resident A
         if (!c->blas && cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS)
             return fail(CIMCS_CUDA_ERROR, "cublasCreate failed");
         cublasSetStream(c->blas, c->stream);
@@ -2559,6 +2769,8 @@ int cimcs_cdp_minimize(cimcs_ctx* c, int32_t R, const int32_t* sigma, const doub
         return fail(CIMCS_CONFIG_ERROR, "cdp method must be jacobi or cg");
     if (method == CIMCS_CDP_CG && c->world > 1)
         return fail(CIMCS_CONFIG_ERROR, "cdp=cg is not supported on row-sharded contexts");
+    if (c->mri && method == CIMCS_CDP_JACOBI)  // cdp.cpp:158-159
+        return fail(CIMCS_CONFIG_ERROR, "cdp_minimize_operator: damped Jacobi needs an assembled matrix");
     CK(cudaSetDevice(c->device));
     if (int rc = ensure_state(c, slots_for(c, R))) return rc;
     if (method == CIMCS_CDP_CG)
@@ -2649,6 +2861,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
         return fail(CIMCS_CONFIG_ERROR, "cdp must be jacobi or cg");
     if (cdp == CIMCS_CDP_CG && c->world > 1)
         return fail(CIMCS_CONFIG_ERROR, "cdp=cg is not supported on row-sharded contexts");
+    if (c->mri) cdp = CIMCS_CDP_CG;  // transform-chain problems always use CG (orchestrator.cpp:128-133)
     if (!seeds) return fail(CIMCS_INPUT_ERROR, "null seeds");
     CK(cudaSetDevice(c->device));
     const int NR = slots_for(c, R);

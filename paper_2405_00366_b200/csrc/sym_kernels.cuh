@@ -667,6 +667,8 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
     }
     if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN || MODE == EPI_JACOBI) {
         // fp16 B tile of the new w of block K: per-replica max over the 128 rows
+        // (no tile when the contraction does not read them: transform chains)
+        const bool emit = sa.WBout != nullptr;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             unsigned m = __float_as_uint(fabsf(wn[u]));
@@ -685,7 +687,11 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
             for (int w = 0; w < NW; ++w) m = max(m, s_max[w][t]);
             const int e = sy_exp14(__uint_as_float(m));
             s_exp[t] = e;
-            sa.WSout[((size_t)b * nRB + K) * NR + t] = e;
+            if (emit) sa.WSout[((size_t)b * nRB + K) * NR + t] = e;
+        }
+        if (!emit) {
+            sy_pdl_trigger();
+            return;
         }
         __syncthreads();
         unsigned char* Bs = reinterpret_cast<unsigned char*>(s_B);
