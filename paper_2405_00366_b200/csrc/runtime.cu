@@ -931,7 +931,7 @@ int mri_launch(cimcs_ctx* c, int mode, int grid, int r0, const float* in, float*
     ma.in = in;
     ma.out = out;
     ma.r0 = r0;
-    mri_kernel<<<grid, kMriThreads, mri_smem_bytes(c->N, c->mL), c->stream>>>(ma, mode);
+    mri_kernel<<<grid, kMriThreads, mri_smem_bytes(c->mH, c->mW, c->mL), c->stream>>>(ma, mode);
     CK(cudaGetLastError());
     return 0;
 }
@@ -953,7 +953,7 @@ int launch_mri_t(cimcs_ctx* c, const GemvArgs& g) {
     ma.scale = 1.f / (float)c->N;
     ma.in = static_cast<const float*>(g.Win);
     ma.out = c->dSpart;
-    const size_t smem = mri_smem_bytes(c->N, c->mL);
+    const size_t smem = mri_smem_bytes(c->mH, c->mW, c->mL);
     mri_kernel<<<NR, kMriThreads, smem, c->stream>>>(ma, MRI_APPLY);
     CK(cudaGetLastError());
     SymArgs sa{};
@@ -2327,9 +2327,9 @@ int cimcs_set_mri_problem(cimcs_ctx* c, int32_t H, int32_t W, const double* targ
     for (int k : idx) full[k] = 1;
     for (int i = 0; i < H; ++i)
         for (int j = 0; j < W; ++j) br[(size_t)i * W + j] = full[(size_t)rev(i, H) * W + rev(j, W)];
-    std::vector<float2> tw(c->mL / 2);
-    for (int k = 0; k < c->mL / 2; ++k) {
-        const double a = -2.0 * M_PI * k / c->mL;
+    std::vector<float2> tw(64);  // exp(-2 pi i k / 128): every line length divides 128
+    for (int k = 0; k < 64; ++k) {
+        const double a = -2.0 * M_PI * k / 128.0;
         tw[k] = make_float2((float)std::cos(a), (float)std::sin(a));
     }
     std::vector<float> tgt((size_t)N);
@@ -2344,7 +2344,7 @@ int cimcs_set_mri_problem(cimcs_ctx* c, int32_t H, int32_t W, const double* targ
     static unsigned long long attr = 0;
     if (!(attr >> c->device & 1ull)) {
         CK(cudaFuncSetAttribute(mri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)mri_smem_bytes(kMriMaxPix, 128)));
+                                (int)mri_smem_bytes(128, 128, 128)));
         attr |= 1ull << c->device;
     }
     if (c->has_truth) {  // make_problem(t, &truth): xi = (x != 0) (mri.cpp:398-405)
