@@ -166,6 +166,13 @@ int cimcs_build_coupling(cimcs_ctx* ctx);
  * G by applying the chain to every basis vector. */
 int cimcs_set_mri_problem(cimcs_ctx* ctx, int32_t H, int32_t W, const double* target,
                           int32_t M, const int32_t* mask, double gamma, const double* x_true);
+/* lasso_init(t, lambda) (mri.cpp:372-377 -> lasso_normal_form :345-370): FISTA
+ * warm start on the built MRI problem with G = Re(A^H A), step `step` (1 in
+ * the reference), stop when |f - f_prev| <= tol max(1, |f_prev|) or after
+ * max_iters iterations.  x_out[N] (fp32 chain, fp64 objective), the iteration
+ * count and the final objective. */
+int cimcs_mri_lasso(cimcs_ctx* ctx, double lambda, int32_t max_iters, double tol, double step,
+                    double* x_out, int32_t* iterations, double* objective);
 /* Copy instance b's coupling back (fp64 host buffers; N*N, N, N).  Test aid. */
 int cimcs_get_coupling(cimcs_ctx* ctx, int32_t b, double* G, double* hz, double* D);
 

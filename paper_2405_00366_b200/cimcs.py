@@ -284,6 +284,16 @@ class Context:
                                                None if x is None else x.ctypes.data))
         self.B, self.N = 1, H * W
 
+    def mri_lasso(self, lambda_l1: float = 3e-4, max_iters: int = 5000, tol: float = 1e-8,
+                  step: float = 1.0):
+        """lasso_init(t, lambda) (mri.cpp:372-377): FISTA warm start of the
+        built MRI problem -> (x, iterations, objective)."""
+        x = np.zeros(self.N)
+        it, f = C.c_int32(), C.c_double()
+        _check(self._lib.cimcs_mri_lasso(self._ctx, float(lambda_l1), int(max_iters), float(tol),
+                                         float(step), x.ctypes.data, C.byref(it), C.byref(f)))
+        return x, it.value, f.value
+
     def build_coupling(self):
         _check(self._lib.cimcs_build_coupling(self._ctx))
 

@@ -312,6 +312,87 @@ __global__ void __launch_bounds__(kMriThreads, 1) mri_kernel(MriArgs a, int mode
     }
 }
 
+// ---------------------------------------------------------------- LASSO
+// lasso_normal_form (mri.cpp:345-370) as used by lasso_init(t, lambda)
+// (mri.cpp:372-377): FISTA on 1/2 x'Gx - hz.x + lambda |x|_1 with
+// G = Re(A^H A) (the chain without smoothness), step 1.  Each iteration is
+// one mri_kernel launch over the two slots [z | x] followed by this
+// one-CTA kernel: it first evaluates the objective of the x produced by the
+// previous update (its G x is the second slot) and stops on the reference's
+// test |f - f_prev| <= tol max(1, |f_prev|) (f_prev starts at 0) or after
+// max_iters updates; otherwise it applies the next update.  Reductions are
+// in fp64 in a fixed order.
+struct LassoState {
+    double t, f_prev, f;
+    int it, done;
+};
+
+constexpr int kLassoThreads = 1024;
+
+__global__ void __launch_bounds__(kLassoThreads) lasso_kernel(
+    const float* __restrict__ Gzx,  // [N][2]: G z, G x
+    float* __restrict__ zx,         // [N][2]: z, x (the next apply's input)
+    const float* __restrict__ hz, int N, double lambda, double step, double tol,
+    int max_iters, LassoState* st) {
+    __shared__ double red[3][kLassoThreads / 32];
+    __shared__ int s_stop;
+    if (st->done) return;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int it = st->it;
+    if (it >= 1) {
+        double a = 0.0, b = 0.0, c = 0.0;
+        for (int i = tid; i < N; i += kLassoThreads) {
+            const double x = zx[2 * i + 1];
+            a += x * (double)Gzx[2 * i + 1];
+            b += (double)hz[i] * x;
+            c += fabs(x);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+            c += __shfl_xor_sync(0xffffffffu, c, o);
+        }
+        if (lane == 0) {
+            red[0][wid] = a;
+            red[1][wid] = b;
+            red[2][wid] = c;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double A = 0.0, Bv = 0.0, Cv = 0.0;
+            for (int w = 0; w < kLassoThreads / 32; ++w) {
+                A += red[0][w];
+                Bv += red[1][w];
+                Cv += red[2][w];
+            }
+            const double f = 0.5 * A - Bv + lambda * Cv;
+            const double fp = st->f_prev;
+            int stop = fabs(f - fp) <= tol * fmax(1.0, fabs(fp)) || it >= max_iters;
+            st->f = f;
+            st->f_prev = f;
+            if (stop) st->done = 1;
+            s_stop = stop;
+        }
+        __syncthreads();
+        if (s_stop) return;
+    }
+    const double t = st->t, tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t)), mom = (t - 1.0) / tn;
+    const double thr = step * lambda;
+    for (int i = tid; i < N; i += kLassoThreads) {
+        const double z = zx[2 * i], x = zx[2 * i + 1];
+        const double g = (double)Gzx[2 * i] - (double)hz[i];
+        const double v = z - step * g, m = fabs(v) - thr;
+        const double xn = m > 0.0 ? (v > 0.0 ? m : -m) : 0.0;  // soft_threshold, mri.cpp:67-74
+        zx[2 * i] = (float)(xn + mom * (xn - x));
+        zx[2 * i + 1] = (float)xn;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        st->t = tn;
+        st->it = it + 1;
+    }
+}
+
 inline size_t mri_smem_bytes(int H, int W, int L) {
     return (size_t)H * (W + 1) * 8 + (size_t)H * W * 4 + 64 * 8;
 }

@@ -2262,6 +2262,57 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
     return 0;
 }
 
+int cimcs_mri_lasso(cimcs_ctx* c, double lambda, int32_t max_iters, double tol, double step,
+                    double* x_out, int32_t* iterations, double* objective) {
+    if (!c || !c->mri || !c->built) return fail(CIMCS_INPUT_ERROR, "mri_lasso: no built MRI problem");
+    if (lambda < 0.0) return fail(CIMCS_INPUT_ERROR, "lasso: lambda_l1 must be >= 0");
+    if (!(step > 0.0)) return fail(CIMCS_INPUT_ERROR, "lasso: step must be > 0");
+    if (max_iters < 0 || !x_out) return fail(CIMCS_INPUT_ERROR, "mri_lasso: bad arguments");
+    CK(cudaSetDevice(c->device));
+    const int N = c->N;
+    float *zx = nullptr, *gzx = nullptr;
+    LassoState* st = nullptr;
+    int rc;
+    if ((rc = dalloc(&zx, (size_t)N * 2 * 4)) || (rc = dalloc(&gzx, (size_t)N * 2 * 4)) ||
+        (rc = dalloc(&st, sizeof(LassoState))))
+        return rc;
+    std::unique_ptr<float, decltype(&cudaFree)> g1(zx, &cudaFree), g2(gzx, &cudaFree);
+    std::unique_ptr<LassoState, decltype(&cudaFree)> g3(st, &cudaFree);
+    LassoState s0{1.0, 0.0, 0.0, 0, max_iters == 0 ? 1 : 0};
+    CK(cudaMemsetAsync(zx, 0, (size_t)N * 2 * 4, c->stream));
+    CK(cudaMemcpyAsync(st, &s0, sizeof s0, cudaMemcpyHostToDevice, c->stream));
+    MriArgs ma{};
+    ma.H = c->mH;
+    ma.W = c->mW;
+    ma.N = N;
+    ma.NR = 2;
+    ma.mask_br = c->dMaskBr;
+    ma.tw = c->dTw;
+    ma.L = c->mL;
+    ma.gamma = 0.f;  // apply_fit: Re(A^H A), no smoothness (mri.cpp:299-301)
+    ma.scale = 1.f / (float)N;
+    ma.in = zx;
+    ma.out = gzx;
+    const size_t smem = mri_smem_bytes(c->mH, c->mW, c->mL);
+    LassoState hs = s0;
+    while (!hs.done) {
+        for (int k = 0; k < 64; ++k) {  // device-side stop: launches after it return at once
+            mri_kernel<<<2, kMriThreads, smem, c->stream>>>(ma, MRI_APPLY);
+            lasso_kernel<<<1, kLassoThreads, 0, c->stream>>>(gzx, zx, static_cast<const float*>(c->dhz),
+                                                             N, lambda, step, tol, max_iters, st);
+        }
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    std::vector<float> h((size_t)N * 2);
+    CK(cudaMemcpy(h.data(), zx, h.size() * 4, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < N; ++i) x_out[i] = h[2 * i + 1];
+    if (iterations) *iterations = hs.it;
+    if (objective) *objective = hs.f;
+    return 0;
+}
+
 int cimcs_make_mask(int32_t H, int32_t W, int32_t M, uint64_t seed, int32_t* out) {
     const long long N = (long long)H * W;
     if (H < 1 || W < 1) return fail(CIMCS_INPUT_ERROR, "make_mask: dims must be >= 1");

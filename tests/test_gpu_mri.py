@@ -139,3 +139,30 @@ def test_operator_problem_errors(gpu, Mr):
                 c.set_mri_problem(img, np.array(bad), 0.0)
         with pytest.raises(gpu.InputError):
             c.set_mri_problem(np.zeros((12, 16)), np.array([1, 2]), 0.0)
+
+
+def test_lasso_warm_start_matches_oracle(gpu, Mr):
+    """lasso_init(t, lambda) (mri.cpp:372-377) on the GPU chain: a fixed 300
+    FISTA iterations (tol 0) agree with the fp64 oracle to 1e-4 relative, and
+    the reference's default stopping rule reaches the oracle's objective (the
+    fp32 objective noise moves the stopping iteration, and the LASSO objective
+    is flat at its optimum, so x itself is held to 5e-2)."""
+    img, coeffs = Mr.sparsify_wavelet(Mr.phantom_image(32, 32), 0.1)
+    mask = Mr.make_mask(32, 32, 410, 3)
+    t = Mr.MriTransform(img, mask, 1e-4)
+    ref = Mr.lasso_normal_form(t.apply_fit, t.hz, 3e-4, max_iters=300, tol=0.0)
+    with _ctx(gpu, img, mask, 1e-4, coeffs) as ctx:
+        x, it, f = ctx.mri_lasso(3e-4, 300, 0.0)
+        assert it == 300
+        assert np.linalg.norm(x - ref) <= 1e-4 * np.linalg.norm(ref)
+        fo = 0.5 * ref @ t.apply_fit(ref) - t.hz @ ref + 3e-4 * np.abs(ref).sum()
+        assert abs(f - fo) <= 1e-5 * abs(fo)
+        x2, it2, f2 = ctx.mri_lasso()  # defaults: lambda 3e-4, 5000 iterations, tol 1e-8
+        ref2 = Mr.lasso_init(t, 3e-4)
+        f_ref2 = 0.5 * ref2 @ t.apply_fit(ref2) - t.hz @ ref2 + 3e-4 * np.abs(ref2).sum()
+        assert 1 <= it2 <= 5000
+        assert f2 <= f_ref2 + 1e-5 * abs(f_ref2)
+        assert np.linalg.norm(x2 - ref2) <= 5e-2 * np.linalg.norm(ref2)
+        # overwhelming shrinkage returns zero exactly (test_mri.cpp:250-260)
+        xz, _, _ = ctx.mri_lasso(10.0 * np.max(np.abs(t.hz)), 50, 1e-8)
+        assert np.max(np.abs(xz)) == 0.0
