@@ -21,7 +21,10 @@
 // epilogue on it.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 namespace cimcs {
 
@@ -86,7 +89,8 @@ __device__ __forceinline__ void fft_pass_t(float2* X, int nlines, int es, int ls
         wr2a = tw[lane];
         wr2b = tw[lane + 32];
     }
-    for (int l0 = warp * G; l0 < nlines; l0 += kMriWarps * G) {
+    const int nwarps = blockDim.x >> 5;
+    for (int l0 = warp * G; l0 < nlines; l0 += nwarps * G) {
         const int line = l0 + (n >= 32 ? 0 : lane >> LN);
         const bool on = line < nlines;
         float2* base = X + (size_t)(on ? line : 0) * ls;
@@ -167,46 +171,80 @@ __device__ __forceinline__ void fft_pass(float2* X, int nlines, int ln, int es, 
     }
 }
 
-// Haar level on the first 2^lcnt lines of length 2^ln: split (forward) or merge
-// (inverse), staged through registers (mri.cpp:29-48: s = 1/sqrt(2),
-// (a + b) s and (a - b) s).  cols: lines are columns (stride W) and the line
-// index runs fastest across threads, so a warp touches consecutive columns.
-template <bool SPLIT>
-__device__ __forceinline__ void haar_pass(float* X, int lcnt, int ln, int lW, bool cols) {
+// One whole Haar level on the leading 2^lh x 2^lw block as 2 x 2 butterflies
+// (row width 2^lW).  Forward = the reference's row split then column split
+// (mri.cpp:122-141): block (2a..2a+1, 2b..2b+1) -> (a, b), (a, w/2 + b),
+// (h/2 + a, b), (h/2 + a, w/2 + b), with the row sums rounded first exactly as
+// the two-pass order does; inverse = column merge then row merge
+// (mri.cpp:143-165).  Register-staged: all reads, barrier, all writes.
+template <bool FWD, int NT>
+__device__ __forceinline__ void haar_level(float* X, int lh, int lw, int lW) {
     const float s = 0.70710678118654752440f;
-    const int n = 1 << ln, np = 1 << (lcnt + ln - 1), hm = (n >> 1) - 1, cm = (1 << lcnt) - 1;
-    constexpr int kReg = kMriMaxPix / 2 / kMriThreads;  // pairs per thread (8)
-    float ra[kReg], rb[kReg];
-    auto at = [&](int line, int k) -> float* {
-        return cols ? X + ((size_t)k << lW) + line : X + ((size_t)line << lW) + k;
-    };
+    const int h2 = 1 << (lh - 1), w2 = 1 << (lw - 1), nb = h2 << (lw - 1);
+    constexpr int kReg = kMriMaxPix / 4 / NT;  // blocks per thread
+    float o[kReg][4];
 #pragma unroll
     for (int u = 0; u < kReg; ++u) {
-        const int t = threadIdx.x + u * kMriThreads;
-        if (t < np) {
-            const int line = cols ? t & cm : t >> (ln - 1), k = cols ? t >> lcnt : t & hm;
-            const float a = SPLIT ? *at(line, 2 * k) : *at(line, k);
-            const float b = SPLIT ? *at(line, 2 * k + 1) : *at(line, (n >> 1) + k);
-            ra[u] = (a + b) * s;
-            rb[u] = (a - b) * s;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < kReg; ++u) {
-        const int t = threadIdx.x + u * kMriThreads;
-        if (t < np) {
-            const int line = cols ? t & cm : t >> (ln - 1), k = cols ? t >> lcnt : t & hm;
-            if (SPLIT) {
-                *at(line, k) = ra[u];
-                *at(line, (n >> 1) + k) = rb[u];
+        const int t = threadIdx.x + u * NT;
+        if (t < nb) {
+            const int aa = t >> (lw - 1), bb = t & (w2 - 1);
+            if (FWD) {
+                const float* r0 = X + ((size_t)(2 * aa) << lW) + 2 * bb;
+                const float* r1 = r0 + ((size_t)1 << lW);
+                const float x00 = r0[0], x01 = r0[1], x10 = r1[0], x11 = r1[1];
+                const float p0 = (x00 + x01) * s, p1 = (x00 - x01) * s;  // row split, row 2a
+                const float q0 = (x10 + x11) * s, q1 = (x10 - x11) * s;  // row split, row 2a+1
+                o[u][0] = (p0 + q0) * s;  // (a, b)
+                o[u][1] = (p1 + q1) * s;  // (a, w/2 + b)
+                o[u][2] = (p0 - q0) * s;  // (h/2 + a, b)
+                o[u][3] = (p1 - q1) * s;  // (h/2 + a, w/2 + b)
             } else {
-                *at(line, 2 * k) = ra[u];
-                *at(line, 2 * k + 1) = rb[u];
+                const float* t0 = X + ((size_t)aa << lW);
+                const float* t1 = X + ((size_t)(h2 + aa) << lW);
+                const float LL = t0[bb], HL = t0[w2 + bb], LH = t1[bb], HH = t1[w2 + bb];
+                const float c00 = (LL + LH) * s, c10 = (LL - LH) * s;  // column merge
+                const float c01 = (HL + HH) * s, c11 = (HL - HH) * s;
+                o[u][0] = (c00 + c01) * s;  // (2a, 2b)
+                o[u][1] = (c00 - c01) * s;  // (2a, 2b + 1)
+                o[u][2] = (c10 + c11) * s;  // (2a + 1, 2b)
+                o[u][3] = (c10 - c11) * s;  // (2a + 1, 2b + 1)
             }
         }
     }
     __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kReg; ++u) {
+        const int t = threadIdx.x + u * NT;
+        if (t < nb) {
+            const int aa = t >> (lw - 1), bb = t & (w2 - 1);
+            if (FWD) {
+                float* t0 = X + ((size_t)aa << lW);
+                float* t1 = X + ((size_t)(h2 + aa) << lW);
+                t0[bb] = o[u][0];
+                t0[w2 + bb] = o[u][1];
+                t1[bb] = o[u][2];
+                t1[w2 + bb] = o[u][3];
+            } else {
+                float* r0 = X + ((size_t)(2 * aa) << lW) + 2 * bb;
+                float* r1 = r0 + ((size_t)1 << lW);
+                r0[0] = o[u][0];
+                r0[1] = o[u][1];
+                r1[0] = o[u][2];
+                r1[1] = o[u][3];
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// full multi-level transforms of an H x W image (H = 2^lH, W = 2^lW)
+template <int NT>
+__device__ __forceinline__ void haar_inverse(float* X, int lH, int lW) {
+    for (int l = min(lH, lW) - 1; l >= 0; --l) haar_level<false, NT>(X, lH - l, lW - l, lW);
+}
+template <int NT>
+__device__ __forceinline__ void haar_forward(float* X, int lH, int lW) {
+    for (int lh = lH, lw = lW; lh >= 1 && lw >= 1; --lh, --lw) haar_level<true, NT>(X, lh, lw, lW);
 }
 
 // second difference along an axis with reflective ends (mri.cpp:51-63):
@@ -248,15 +286,7 @@ __global__ void __launch_bounds__(kMriThreads, 1) mri_kernel(MriArgs a, int mode
         for (int i = threadIdx.x; i < N; i += blockDim.x) B[i] = a.in[i];
     }
     __syncthreads();
-    if (mode != MRI_HZ) {
-        // inverse Haar, deepest level first: columns then rows (mri.cpp:143-165)
-        const int nl = min(lH, lW);
-        for (int l = nl - 1; l >= 0; --l) {
-            const int lh = lH - l, lw = lW - l;
-            haar_pass<false>(B, lw, lh, lW, true);   // columns j < w, length h
-            haar_pass<false>(B, lh, lw, lW, false);  // rows i < h, length w
-        }
-    }
+    if (mode != MRI_HZ) haar_inverse<kMriThreads>(B, lH, lW);  // mri.cpp:143-165
     // ---- forward DFT (unitary scale folded into the mask step): DIF rows, DIF columns
     for (int p = threadIdx.x; p < N; p += blockDim.x)
         K[(size_t)(p >> lW) * KS + (p & wm)] = make_float2(B[p], 0.f);
@@ -296,11 +326,8 @@ __global__ void __launch_bounds__(kMriThreads, 1) mri_kernel(MriArgs a, int mode
         }
         __syncthreads();
     }
-    // ---- forward Haar: rows then columns per level (mri.cpp:122-141)
-    for (int lh = lH, lw = lW; lh >= 1 && lw >= 1; --lh, --lw) {
-        haar_pass<true>(B, lh, lw, lW, false);
-        haar_pass<true>(B, lw, lh, lW, true);
-    }
+    // ---- forward Haar (mri.cpp:122-141)
+    haar_forward<kMriThreads>(B, lH, lW);
     if (mode == MRI_APPLY) {
         for (int i = threadIdx.x; i < N; i += blockDim.x) a.out[(size_t)i * a.NR + q] = B[i];
     } else if (mode == MRI_DIAG) {
@@ -309,6 +336,143 @@ __global__ void __launch_bounds__(kMriThreads, 1) mri_kernel(MriArgs a, int mode
         for (int i = threadIdx.x; i < N; i += blockDim.x) a.out[(size_t)(a.r0 + q) * N + i] = B[i];
     } else {
         for (int i = threadIdx.x; i < N; i += blockDim.x) a.out[i] = B[i];
+    }
+}
+
+// ------------------------------------------------ cluster-distributed apply
+// The per-step G w of MRI_APPLY on a thread-block cluster of CS = 8 CTAs per
+// replica (H, W >= 16), so the 16 replicas of config 3 occupy 128 SMs instead
+// of 16.  CTA k owns image rows [r0, r0 + RH) (RH = H / 8, even) and k-space
+// columns [c0, c0 + CW) (CW = W / 8).  The Haar transform's first level is a
+// 2 x 2 butterfly whose row pairs never straddle two CTAs, and every deeper
+// level lives in the (H/2) x (W/2) low-pass quadrant:
+//   1. the quadrant's coefficients are inverse-transformed redundantly in
+//      every CTA (levels 2.., 1/4 of the work); the level-1 inverse is done
+//      only for the CTA's rows and a two-row halo (the smoothness stencil's
+//      reach), straight from the detail coefficients in global memory;
+//   2. DIF FFT of the own rows; the slab is scattered by column ownership
+//      into the peers' column slabs (DSMEM), cluster barrier;
+//   3. DIF FFT of the own columns, mask x 1/(HW), DIT inverse, gathered back
+//      by row ownership (DSMEM), cluster barrier;
+//   4. DIT inverse of the own rows, real part + gamma * fourth differences;
+//   5. level-1 forward Haar of the own rows: the detail quadrants are final
+//      and go straight to global memory, the low-pass rows are broadcast into
+//      every CTA's quadrant (DSMEM), cluster barrier, levels 2.. redundantly,
+//      each CTA stores its share of the quadrant.
+constexpr int kMriCThreads = 512;
+constexpr int kMriCluster = 8;
+
+inline int mri_cluster_size(int H, int W) { return std::min(kMriCluster, std::min(H, W)); }
+inline size_t mri_cluster_smem_bytes(int H, int W) {
+    const int RH = H / kMriCluster, CW = W / kMriCluster;
+    return (size_t)(H / 2) * (W / 2) * 4     // low-pass quadrant
+           + (size_t)(RH + 4) * W * 4        // inverse-Haar rows + halo
+           + (size_t)RH * W * 4              // result rows
+           + (size_t)RH * (W + 1) * 8        // own rows, complex
+           + (size_t)H * (CW + 1) * 8        // own columns, complex
+           + 64 * 8;
+}
+
+__global__ void __launch_bounds__(kMriCThreads, 1) mri_cluster_kernel(MriArgs a) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int H = a.H, W = a.W, NR = a.NR;
+    const int CS = kMriCluster, k = (int)cl.block_rank();
+    const int lH = __ffs(H) - 1, lW = __ffs(W) - 1;
+    const int RH = H >> 3, CW = W >> 3, lRH = lH - 3, lCW = lW - 3;
+    const int H2 = H >> 1, W2 = W >> 1, lW2 = lW - 1;
+    const int RS = W + 1, CSt = CW + 1;
+    const int r0 = k * RH, c0 = k * CW;
+    const int s0 = max(0, r0 - 2), s1 = min(H, r0 + RH + 2);      // rows of Bs
+    float* Q = reinterpret_cast<float*>(smem);                       // [H/2][W/2]
+    float* Bs = Q + (size_t)H2 * W2;                                 // [RH + 4][W]
+    float* Rr = Bs + (size_t)(RH + 4) * W;                           // [RH][W]
+    float2* Kr = reinterpret_cast<float2*>(Rr + (size_t)RH * W);     // [RH][W + 1]
+    float2* Kc = Kr + (size_t)RH * RS;                               // [H][CW + 1]
+    float2* tw = Kc + (size_t)H * CSt;                               // [64]
+    float* Bv = Bs - (size_t)s0 * W;  // virtual full image: rows [s0, s1) valid
+    const int q = blockIdx.x / CS;
+    const float* win = a.in;
+    const float s = 0.70710678118654752440f;
+    for (int t = threadIdx.x; t < 64; t += blockDim.x) tw[t] = a.tw[t];
+    // 1. low-pass quadrant (redundant), levels 2.. of the inverse
+    for (int t = threadIdx.x; t < H2 * W2; t += blockDim.x) {
+        const int i = t >> lW2, j = t & (W2 - 1);
+        Q[t] = win[((size_t)(i << lW) + j) * NR + q];
+    }
+    __syncthreads();
+    haar_inverse<kMriCThreads>(Q, lH - 1, lW - 1);
+    // level-1 inverse (column merge, then row merge) for rows [s0, s1)
+    for (int t = threadIdx.x; t < ((s1 - s0) >> 1) * W2; t += blockDim.x) {
+        const int aa = (s0 >> 1) + (t >> lW2), bb = t & (W2 - 1);
+        const float LL = Q[(aa << lW2) + bb];
+        const float HL = win[((size_t)(aa << lW) + W2 + bb) * NR + q];
+        const float LH = win[((size_t)((H2 + aa) << lW) + bb) * NR + q];
+        const float HH = win[((size_t)((H2 + aa) << lW) + W2 + bb) * NR + q];
+        const float c00 = (LL + LH) * s, c10 = (LL - LH) * s;
+        const float c01 = (HL + HH) * s, c11 = (HL - HH) * s;
+        float* o0 = Bv + ((size_t)(2 * aa) << lW) + 2 * bb;
+        float* o1 = o0 + W;
+        o0[0] = (c00 + c01) * s;
+        o0[1] = (c00 - c01) * s;
+        o1[0] = (c10 + c11) * s;
+        o1[1] = (c10 - c11) * s;
+    }
+    __syncthreads();
+    // 2. DIF rows, scatter to the column owners
+    for (int t = threadIdx.x; t < RH * W; t += blockDim.x)
+        Kr[(size_t)(t >> lW) * RS + (t & (W - 1))] = make_float2(Bv[((size_t)r0 << lW) + t], 0.f);
+    __syncthreads();
+    fft_pass<true>(Kr, RH, lW, 1, RS, tw);
+    for (int t = threadIdx.x; t < RH * W; t += blockDim.x) {
+        const int r = t >> lW, j = t & (W - 1), m = j >> lCW;
+        cl.map_shared_rank(Kc, m)[(size_t)(r0 + r) * CSt + (j & (CW - 1))] = Kr[(size_t)r * RS + j];
+    }
+    cl.sync();
+    // 3. DIF columns, mask, DIT columns, gather back to the row owners
+    fft_pass<true>(Kc, CW, lH, CSt, 1, tw);
+    for (int t = threadIdx.x; t < H * CW; t += blockDim.x) {
+        const int i = t >> lCW, jl = t & (CW - 1);
+        const float m = a.mask_br[((size_t)i << lW) + c0 + jl] ? a.scale : 0.f;
+        float2& z = Kc[(size_t)i * CSt + jl];
+        z = make_float2(z.x * m, z.y * m);
+    }
+    __syncthreads();
+    fft_pass<false>(Kc, CW, lH, CSt, 1, tw);
+    for (int t = threadIdx.x; t < H * CW; t += blockDim.x) {
+        const int i = t >> lCW, jl = t & (CW - 1), m = i >> lRH;
+        cl.map_shared_rank(Kr, m)[(size_t)(i & (RH - 1)) * RS + c0 + jl] = Kc[(size_t)i * CSt + jl];
+    }
+    cl.sync();
+    // 4. DIT rows; real part + smoothness
+    fft_pass<false>(Kr, RH, lW, 1, RS, tw);
+    const bool smooth = a.gamma > 0.f;
+    for (int t = threadIdx.x; t < RH * W; t += blockDim.x) {
+        const int i = r0 + (t >> lW), j = t & (W - 1);
+        float x = Kr[(size_t)(t >> lW) * RS + j].x;
+        if (smooth) x += a.gamma * (d4(Bv + j, i, H, W) + d4(Bv + ((size_t)i << lW), j, W, 1));
+        Rr[t] = x;
+    }
+    __syncthreads();
+    // 5. level-1 forward of the own rows (row split, then column split)
+    for (int t = threadIdx.x; t < (RH >> 1) * W2; t += blockDim.x) {
+        const int al = t >> lW2, bb = t & (W2 - 1), aa = (r0 >> 1) + al;
+        const float* p = Rr + ((size_t)(2 * al) << lW) + 2 * bb;
+        const float x00 = p[0], x01 = p[1], x10 = p[W], x11 = p[W + 1];
+        const float p0 = (x00 + x01) * s, p1 = (x00 - x01) * s;
+        const float q0 = (x10 + x11) * s, q1 = (x10 - x11) * s;
+        const float LL = (p0 + q0) * s;
+        a.out[((size_t)(aa << lW) + W2 + bb) * NR + q] = (p1 + q1) * s;          // HL
+        a.out[((size_t)((H2 + aa) << lW) + bb) * NR + q] = (p0 - q0) * s;        // LH
+        a.out[((size_t)((H2 + aa) << lW) + W2 + bb) * NR + q] = (p1 - q1) * s;   // HH
+        for (int m = 0; m < CS; ++m) cl.map_shared_rank(Q, m)[(aa << lW2) + bb] = LL;
+    }
+    cl.sync();
+    haar_forward<kMriCThreads>(Q, lH - 1, lW - 1);
+    for (int t = threadIdx.x; t < (RH >> 1) * W2; t += blockDim.x) {
+        const int idx = ((r0 >> 1) << lW2) + t, i = idx >> lW2, j = idx & (W2 - 1);
+        a.out[((size_t)(i << lW) + j) * NR + q] = Q[idx];
     }
 }
 

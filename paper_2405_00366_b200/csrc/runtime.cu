@@ -351,6 +351,7 @@ struct cimcs_ctx {
     unsigned char* dMaskBr = nullptr;  // [H*W] sampled, bit-reversed coordinates
     float2* dTw = nullptr;             // [L/2] exp(-2 pi i k / L)
     float* dTarget = nullptr;          // [H*W] target image (row-major)
+    bool mri_cluster = true;           // per-step apply on one cluster per replica
     cublasHandle_t blas = nullptr;
     cudaStream_t sfin = nullptr;             // stream of the reduction / update kernels
     cudaEvent_t evA[4] = {}, evF[4] = {};    // per group: tiles done / update done
@@ -953,8 +954,26 @@ int launch_mri_t(cimcs_ctx* c, const GemvArgs& g) {
     ma.scale = 1.f / (float)c->N;
     ma.in = static_cast<const float*>(g.Win);
     ma.out = c->dSpart;
-    const size_t smem = mri_smem_bytes(c->mH, c->mW, c->mL);
-    mri_kernel<<<NR, kMriThreads, smem, c->stream>>>(ma, MRI_APPLY);
+    if (c->mri_cluster && std::min(c->mH, c->mW) >= 2 * kMriCluster) {
+        // one thread-block cluster per replica (mri_cluster_kernel)
+        const int CS = mri_cluster_size(c->mH, c->mW);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(NR * CS);
+        cfg.blockDim = dim3(kMriCThreads);
+        cfg.dynamicSmemBytes = mri_cluster_smem_bytes(c->mH, c->mW);
+        cfg.stream = c->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CS;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, mri_cluster_kernel, ma));
+    } else {
+        const size_t smem = mri_smem_bytes(c->mH, c->mW, c->mL);
+        mri_kernel<<<NR, kMriThreads, smem, c->stream>>>(ma, MRI_APPLY);
+    }
     CK(cudaGetLastError());
     SymArgs sa{};
     sa.t = tc_args(c, g);
@@ -2145,7 +2164,10 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
     if (k == "host_threads") c->host_threads = (int)std::max<int64_t>(1, v);
     else if (k == "use_graphs") c->use_graphs = v != 0;
     else if (k == "gram_blas") c->gram_blas = v > 0 ? 1 : (v < 0 ? -1 : 0);
-    else if (k == "pdl") {
+    else if (k == "mri_cluster") {
+        c->mri_cluster = v != 0;
+        drop_graphs(c);
+    } else if (k == "pdl") {
         c->use_pdl = v != 0;
         drop_graphs(c);
     }
@@ -2396,6 +2418,8 @@ int cimcs_set_mri_problem(cimcs_ctx* c, int32_t H, int32_t W, const double* targ
     if (!(attr >> c->device & 1ull)) {
         CK(cudaFuncSetAttribute(mri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)mri_smem_bytes(128, 128, 128)));
+        CK(cudaFuncSetAttribute(mri_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)mri_cluster_smem_bytes(128, 128)));
         attr |= 1ull << c->device;
     }
     if (c->has_truth) {  // make_problem(t, &truth): xi = (x != 0) (mri.cpp:398-405)

@@ -12,6 +12,7 @@ size = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 R = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 img, coeffs, mask = PM.problem(size, 0.1, 0.4, 1)
 ctx = P.Context(0, "f32")
+ctx.set_option("mri_cluster", int(os.environ.get("MRI_CLUSTER", "1")))
 ctx.set_mri_problem(img, mask, 1e-4, coeffs)
 t0 = time.perf_counter()
 ctx.build_coupling()
