@@ -521,10 +521,11 @@ def run_mri(args, ws, rank, local):
                        "step": "hz/diag build + LASSO warm start (host-timed) + full alternating solve",
                        "l2": "operator applied from shared memory (no gram)"},
             "roofline": {"bound": "latency",
-                         "note": "per-step latency of one CTA per replica (FFT lines in warp "
-                                 "registers, Haar/smoothing in shared memory); no HBM stream",
+                         "note": "per-step latency of one 8-CTA cluster per replica (FFT lines "
+                                 "in warp registers, row/column slabs exchanged over DSMEM, "
+                                 "Haar level 1 distributed); no HBM stream",
                          "step_us": statistics.median(step_us),
-                         "kernel": "mri_kernel + sym_update_kernel<16,BN>"},
+                         "kernel": "mri_cluster_kernel + sym_update_kernel<16,BN>"},
             "replicas_ok": ok, "final_rmse_median": float(np.median(rm)),
             "gpu_launches": launches, "clocks": clocks.summary(),
         }
