@@ -450,3 +450,24 @@ def test_tc_cn_mode_and_track_best(gpu, O, cluster):
             ref = _oracle_solve(O, inst, O.MFZ_CN, hp, int(seeds[b, r]), track_best=True)
             same += np.array_equal(res["sigma"][b, r], ref["sigma"])
     assert same >= 0.9 * len(insts) * R
+
+
+def test_solve_config0_reference_literal_schedule_bitwise(gpu, O):
+    """SURVEY §8(d) "c0-ref" control: config 0's instance with the reference's OWN
+    schedule and defaults (HyperParams(), types.hpp:77-96: sigmoid pump p_thr 1,
+    d 0.4, dt 0.02, velo 51 -> 52 alternations x 1000 steps, Jacobi refit), no
+    builder extension: fp64 GPU solve bitwise equal to the oracle."""
+    inst = O.gen_instance(500, 0.6, 0.2, 0.01, 0)
+    hp = O.HyperParams()
+    seed = O.mix_seed(0, 1)
+    ref = _oracle_solve(O, inst, O.MFZ_BN, hp, seed)
+    ctx = _ctx(gpu, [inst])
+    res = ctx.solve(1, "mfz-bn", gpu.HyperParams(), [seed])
+    assert not ref["failed"] and res["fail_alt"][0, 0] == -1
+    assert res["n_hist"][0, 0] == len(ref["history"]) == 52
+    assert np.array_equal(res["sigma"][0, 0], ref["sigma"])
+    assert np.array_equal(res["R"][0, 0], ref["R"])
+    for h, g in zip(ref["history"], res["history"][0, 0]):
+        assert g["eta"] == h["eta"] and g["support"] == h["support"] and g["min_e"] == h["min_e"]
+        assert math.isclose(g["rmse"], h["rmse"], rel_tol=TOL_SCALAR)
+    ctx.close()
