@@ -261,8 +261,22 @@ def run_ours(args, ws, rank, local):
     nalt = hp.velo + 1
     Bn, Nn = len(insts), insts[0].N
     units = Bn * R * Nn * hp.n_steps * nalt  # spin-steps per rank per step
+    # config 4 on several GPUs (or --shard): ONE instance split by gram tiles
+    # across the ranks (tile-sharded contexts: replicated state, one NCCL
+    # all-reduce per step) -- strong scaling, every rank counts 1/ws of it
+    tile_sharded = args.config == 4 and (ws > 1 or args.shard)
 
-    ctx = P.Context(local, args.dtype)
+    def make_ctx():
+        if not tile_sharded:
+            return P.Context(local, args.dtype)
+        nid = [P.nccl_unique_id() if rank == 0 else None]
+        if dist is not None:
+            dist.broadcast_object_list(nid, src=0)
+        return P.Context(local, args.dtype, shard=(ws, rank, nid[0]))
+
+    if tile_sharded:
+        units = units / ws
+    ctx = make_ctx()
     ctx.set_problems(insts)
 
     def one_step():
@@ -319,12 +333,15 @@ def run_ours(args, ws, rank, local):
         step_bytes = Bn * (nrb * (nrb + 1) // 2) * 128 * 128 * 4
     step_s = statistics.median(step_ms_list) * 1e-3
     peak, peak_kind = measured_peaks()
+    if tile_sharded:  # per GPU: each rank streams its share of the gram tiles
+        step_bytes = step_bytes / ws
+        dense_bytes = dense_bytes / ws
     achieved = step_bytes / step_s / 1e9
 
     # e2e: public API with HOST buffers, H2D of the instances and D2H of results inside
     e2e_val, h2d, d2h = None, 0, 0
     if not args.no_e2e:
-        ctx2 = P.Context(local, args.dtype)
+        ctx2 = make_ctx()
 
         def e2e_once():
             ctx2.set_problems(insts)
@@ -390,17 +407,21 @@ def run_ours(args, ws, rank, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong" if args.config == 2 else "weak", "vs_baseline": None,
+            "scaling": "strong" if args.config == 2 or tile_sharded else "weak",
+            "vs_baseline": None,
             "dtype": args.dtype,
             "data": "synthetic (seeded gen_instance, datagen.cpp:15-55)",
             "config": {"workload": (WORKLOADS[args.config] if args.config != 4 or args.n4 == 100_000
                                     else WORKLOADS[4].replace("N=100000 M=50000 K=5000",
                                                               f"N={Nn} (reduced)")),
                        "per_rank_instances": Bn, "replicas": R,
+                       "parallelism": (f"tile-sharded gram x{ws} (replicated state, one NCCL "
+                                       "all-reduce per step)" if tile_sharded else
+                                       f"instance shards x{ws}"),
                        "step": "gram build + full alternating solve",
                        "l2": ("inputs larger than L2 (gram %.2f GB per step)" % (step_bytes / 1e9)
                               if step_bytes > 126e6 else "gram fits in L2 (no flush)")},
-            "instances_per_s": total_units / units * Bn / (ms_per_step * 1e-3),
+            "instances_per_s": (Bn if tile_sharded else total_units / units * Bn) / (ms_per_step * 1e-3),
             "breakdown_ms": {"gram": statistics.median(gram_ms), "cim": statistics.median(cim_ms),
                              "refit": statistics.median(refit_ms),
                              "score": statistics.median(score_ms)},
@@ -550,6 +571,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fp64", action="store_true", help="skip the fp64 secondary line")
+    ap.add_argument("--shard", action="store_true",
+                    help="config 4: use the tile-sharded context even on one GPU")
     ap.add_argument("--mri", action="store_true",
                     help="the reference's matrix-free MRI chain at config-3 size (run_mri)")
     args = ap.parse_args()

@@ -123,6 +123,10 @@ int cimcs_csv_open(const char* path, const char* const* comments, int32_t ncomme
 int cimcs_csv_row(cimcs_csv* w, const char* const* cells, int32_t n);
 int cimcs_csv_close(cimcs_csv* w);
 
+/* Tile sharding of the symmetric path (sharded contexts, option "tile_shard"):
+ * the super-rows [P0, P1) (4 row blocks of 128 each) whose upper-triangle gram
+ * tiles rank `rank` of `world` streams, contiguous and balanced by tile count. */
+int cimcs_tile_shard(int32_t nRB, int32_t world, int32_t rank, int32_t* P0, int32_t* P1);
 /* make_mask, mri.hpp:45 / mri.cpp:185-207: M distinct k-space positions of an
  * H x W grid (reference Rng, partial Fisher-Yates), sorted into out[M]. */
 int cimcs_make_mask(int32_t H, int32_t W, int32_t M, uint64_t seed, int32_t* out);

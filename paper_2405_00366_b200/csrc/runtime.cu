@@ -334,6 +334,16 @@ struct cimcs_ctx {
     float* dSpart = nullptr;  // partial products [B][nRB][nSB][128][NR]
     int sym_groups = 0;       // instance groups pipelined across two streams (0: auto)
     bool use_pdl = true;      // programmatic dependent launch between the step kernels
+    // tile sharding of the symmetric path (cimcs_create_sharded contexts, option
+    // "tile_shard", default on): every rank keeps the full state and streams only
+    // the gram tiles of its super-rows [sP0, sP1); the per-rank slot sums are
+    // all-reduced (NCCL) before the replicated update -- one collective per step
+    int sh_world = 1, sh_rank = 0;  // geometry given at creation
+    bool sh_rows = false;           // created sharded
+    int tshard_opt = 1;
+    bool tshard = false;            // active for the current problem set
+    int tworld = 1, trank = 0, sP0 = 0, sP1 = 0;
+    float* dH = nullptr;            // [B][nRB][128][NR] summed partial products
     // factored coupling A^T (A w) from fp16 hi/lo tiles of A (fac_kernels.cuh)
     int fac_opt = -1;         // -1 auto, 0 off, 1 on (a symmetric-path variant)
     int fac_requested = -1;
@@ -469,7 +479,8 @@ void free_state(cimcs_ctx* c) {
 void free_problems(cimcs_ctx* c) {
     free_state(c);
     void* ptrs[] = {c->dA, c->dy, c->dM, c->dG, c->dD, c->dhz, c->dx, c->dxi,
-                    c->dSg, c->dSpart, c->dTask, c->dCnt, c->dMaskBr, c->dTw, c->dTarget};
+                    c->dSg, c->dSpart, c->dTask, c->dCnt, c->dMaskBr, c->dTw, c->dTarget,
+                    c->dH};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& q : c->ssched) {
@@ -482,6 +493,7 @@ void free_problems(cimcs_ctx* c) {
     c->dSg = nullptr;
     c->dSpart = nullptr;
     c->dMaskBr = nullptr;
+    c->dH = nullptr;
     c->dTw = nullptr;
     c->dTarget = nullptr;
     c->mri = false;
@@ -505,6 +517,38 @@ int dalloc(P** p, size_t bytes) {
     return 0;
 }
 
+#define NK(x)                                                                           \
+    do {                                                                                \
+        ncclResult_t r_ = (x);                                                          \
+        if (r_ != ncclSuccess)                                                          \
+            return fail(CIMCS_CUDA_ERROR, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+// Super-rows [P0, P1) of rank `rank` of `world`: contiguous, balanced by the
+// number of upper-triangle tiles (super-row P holds the items (P, Q >= P)).
+void tile_shard(int nRB, int world, int rank, int* P0, int* P1) {
+    const int nSB = (nRB + kSyS - 1) / kSyS;
+    std::vector<long long> w(nSB, 0);
+    for (int P = 0; P < nSB; ++P)
+        for (int Q = P; Q < nSB; ++Q) {
+            const int nI = std::min(kSyS, nRB - P * kSyS), nJ = std::min(kSyS, nRB - Q * kSyS);
+            w[P] += P == Q ? nI * (nI + 1) / 2 : nI * nJ;
+        }
+    long long total = 0;
+    for (long long x : w) total += x;
+    std::vector<int> cut(world + 1, nSB);
+    cut[0] = 0;
+    long long acc = 0;
+    int P = 0;
+    for (int r = 1; r < world; ++r) {
+        const long long target = total * r / world;
+        while (P < nSB && acc + w[P] / 2 < target) acc += w[P++];
+        cut[r] = P;
+    }
+    *P0 = cut[rank];
+    *P1 = cut[rank + 1];
+}
+
 // Super-block items of nb instances placed on the persistent CTAs, largest
 // first onto the least-loaded CTA (LPT); built once per nb and cached.
 int sym_schedule(cimcs_ctx* c, int nb, const cimcs_ctx::SymSched** out) {
@@ -515,8 +559,9 @@ int sym_schedule(cimcs_ctx* c, int nb, const cimcs_ctx::SymSched** out) {
         }
     const int nRB = c->nRB, nSB = c->nSB;
     std::vector<std::pair<int, int2>> items;  // (tiles, item)
+    const int P0 = c->tshard ? c->sP0 : 0, P1 = c->tshard ? c->sP1 : nSB;
     for (int b = 0; b < nb; ++b)
-        for (int P = 0; P < nSB; ++P)
+        for (int P = P0; P < P1; ++P)
             for (int Q = P; Q < nSB; ++Q) {
                 const int nI = std::min(kSyS, nRB - P * kSyS), nJ = std::min(kSyS, nRB - Q * kSyS);
                 const int t = P == Q ? nI * (nI + 1) / 2 : nI * nJ;
@@ -524,7 +569,7 @@ int sym_schedule(cimcs_ctx* c, int nb, const cimcs_ctx::SymSched** out) {
             }
     std::stable_sort(items.begin(), items.end(),
                      [](const auto& x, const auto& y) { return x.first > y.first; });
-    const int grid = (int)std::min<size_t>(items.size(), (size_t)c->num_sms);
+    const int grid = (int)std::max<size_t>(1, std::min<size_t>(items.size(), (size_t)c->num_sms));
     std::vector<std::vector<int2>> per(grid);
     using L = std::pair<long long, int>;  // (load, cta)
     std::priority_queue<L, std::vector<L>, std::greater<L>> pq;
@@ -633,6 +678,12 @@ int ensure_state(cimcs_ctx* c, int NR) {
             c->spart_elems = 0;
             if ((rc = dalloc(&c->dSpart, ne * 4))) return rc;
             c->spart_elems = ne;
+        }
+        if (c->tshard) {  // slots of other ranks' items stay zero for good
+            CK(cudaMemset(c->dSpart, 0, ne * 4));
+            if (c->dH) cudaFree(c->dH);
+            c->dH = nullptr;
+            if ((rc = dalloc(&c->dH, (size_t)c->B * c->nRB * kSyT * NR * 4))) return rc;
         }
     }
     return 0;
@@ -815,7 +866,7 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb, cudaStream_t s
     }
     // same stream: both kernels use programmatic dependent launch (the next
     // kernel's prologue overlaps this one's tail; griddepcontrol.wait orders data)
-    const bool pdl = sF == sA && c->use_pdl;
+    const bool pdl = sF == sA && c->use_pdl && !c->tshard;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
@@ -830,6 +881,18 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb, cudaStream_t s
     if (sF != sA) {
         CK(cudaEventRecord(evA, sA));
         CK(cudaStreamWaitEvent(sF, evA, 0));
+    }
+    if (c->tshard) {  // own items' slot sums, then the cross-rank sum (one collective)
+        sym_slotsum_kernel<NR><<<dim3(c->nRB, nb), kSyT * NR / 4, 0, sF>>>(c->dSpart, c->dH, c->nRB,
+                                                                         c->nSB, b0);
+        CK(cudaGetLastError());
+        if (c->tworld > 1) {
+            const size_t per = (size_t)c->nRB * kSyT * NR;
+            NK(ncclAllReduce(c->dH + (size_t)b0 * per, c->dH + (size_t)b0 * per, (size_t)nb * per,
+                             ncclFloat32, ncclSum, c->comm, sF));
+        }
+        sa.spart = c->dH;
+        sa.nSB = 1;
     }
     cfg.gridDim = dim3(c->nRB, nb);
     cfg.blockDim = dim3(kSyT * NR / 4);
@@ -1208,12 +1271,6 @@ GemvArgs base_args(cimcs_ctx* c, const StepScalars& s) {
 int nRB_of(const cimcs_ctx* c) { return c->nRB; }
 
 // ------------------------------------------------ row-sharding collectives
-#define NK(x)                                                                           \
-    do {                                                                                \
-        ncclResult_t r_ = (x);                                                          \
-        if (r_ != ncclSuccess)                                                          \
-            return fail(CIMCS_CUDA_ERROR, std::string(#x) + ": " + ncclGetErrorString(r_)); \
-    } while (0)
 
 ncclDataType_t nccl_t(const cimcs_ctx* c) {
     return c->dtype == CIMCS_F64 ? ncclFloat64 : ncclFloat32;
@@ -2115,9 +2172,9 @@ int cimcs_create_sharded(int32_t device, int32_t dtype, int32_t world, int32_t r
         return fail(CIMCS_CONFIG_ERROR, "bad world/rank/id");
     if (int rc = cimcs_create(device, dtype, out)) return rc;
     cimcs_ctx* c = *out;
-    c->world = world;
-    c->rank = rank;
-    c->sharded = true;
+    c->world = c->sh_world = world;
+    c->rank = c->sh_rank = rank;
+    c->sharded = c->sh_rows = true;
     if (world > 1) {
         ncclUniqueId id;
         std::memcpy(&id, nccl_id, sizeof(id));
@@ -2164,7 +2221,10 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
     if (k == "host_threads") c->host_threads = (int)std::max<int64_t>(1, v);
     else if (k == "use_graphs") c->use_graphs = v != 0;
     else if (k == "gram_blas") c->gram_blas = v > 0 ? 1 : (v < 0 ? -1 : 0);
-    else if (k == "mri_cluster") {
+    else if (k == "tile_shard") {
+        if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set tile_shard before set_problems");
+        c->tshard_opt = v != 0 ? 1 : 0;
+    } else if (k == "mri_cluster") {
         c->mri_cluster = v != 0;
         drop_graphs(c);
     } else if (k == "pdl") {
@@ -2205,7 +2265,7 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
     const bool reuse = c->dA && c->B == B && c->N == N && c->has_truth == truth &&
                        std::equal(c->M.begin(), c->M.end(), M) && (int)c->M.size() == B &&
                        c->want_tc == c->tc_requested && c->want_sym == c->sym_requested &&
-                       c->fac_opt == c->fac_requested;
+                       c->fac_opt == c->fac_requested && !c->sh_rows;
     if (!reuse) free_problems(c);
     c->built = false;
     c->tc_requested = c->want_tc;
@@ -2221,6 +2281,19 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
     c->row1 = N;
     c->rb0 = 0;
     c->nRB = (N + c->RB - 1) / c->RB;
+    // sharded contexts on the symmetric path split gram TILES (replicated
+    // state, one all-reduce per step); otherwise gram ROWS (all-gather of w)
+    c->world = c->sh_rows ? c->sh_world : 1;
+    c->rank = c->sh_rows ? c->sh_rank : 0;
+    c->sharded = c->sh_rows;
+    c->tshard = c->sh_rows && c->tshard_opt && c->tc && c->want_sym && N > kClMaxN;
+    c->tworld = c->tshard ? c->world : 1;
+    c->trank = c->tshard ? c->rank : 0;
+    if (c->tshard) {
+        c->world = 1;
+        c->rank = 0;
+        c->sharded = false;
+    }
     if (c->sharded) {
         // row sharding: equal slices of whole 128-row tiles (sharding.row_shard)
         const int per = (N + c->world * 128 - 1) / (c->world * 128) * 128;
@@ -2236,13 +2309,14 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
     c->sym = c->tc && c->want_sym && c->world == 1 && !c->sharded && N > kClMaxN;
     c->ntri = c->sym ? c->nRB * (c->nRB + 1) / 2 : 0;
     c->nSB = (c->nRB + kSyS - 1) / kSyS;
+    if (c->tshard) tile_shard(c->nRB, c->tworld, c->trank, &c->sP0, &c->sP1);
     c->M.assign(M, M + B);
     c->Mmax = *std::max_element(c->M.begin(), c->M.end());
     // factored variant: auto when A is read twice per step (phase 2 mostly misses
     // L2: ncu, profiles/r01_fac_step.txt) and still moves fewer bytes than the
     // gram triangle, i.e. M below about N/4, and the phase-1 tasks cover the SMs
     c->nMB = (c->Mmax + kSyT - 1) / kSyT;
-    c->fac = c->sym && c->nMB < 0x8000 && B < 0x8000 &&
+    c->fac = c->sym && !c->tshard && c->nMB < 0x8000 && B < 0x8000 &&
              (c->fac_opt == 1 || (c->fac_opt == -1 && 2 * c->nMB * c->nRB <= c->ntri &&
                                   B * c->nMB >= c->num_sms / 2));
     c->fac_w2 = c->nRB >= 2 * c->nMB ? 2 : 1;
@@ -2332,6 +2406,16 @@ int cimcs_mri_lasso(cimcs_ctx* c, double lambda, int32_t max_iters, double tol, 
     for (int i = 0; i < N; ++i) x_out[i] = h[2 * i + 1];
     if (iterations) *iterations = hs.it;
     if (objective) *objective = hs.f;
+    return 0;
+}
+
+int cimcs_tile_shard(int32_t nRB, int32_t world, int32_t rank, int32_t* P0, int32_t* P1) {
+    if (nRB < 1 || world < 1 || rank < 0 || rank >= world || !P0 || !P1)
+        return fail(CIMCS_INPUT_ERROR, "tile_shard: bad arguments");
+    int a = 0, b = 0;
+    tile_shard(nRB, world, rank, &a, &b);
+    *P0 = a;
+    *P1 = b;
     return 0;
 }
 
@@ -2534,8 +2618,11 @@ int cimcs_build_coupling(cimcs_ctx* c) {
             const int M = c->M[b];
             const double* Ab = c->dA + (size_t)b * astride;
             SymOut o{static_cast<__half*>(c->dG), c->dSg, c->nRB, c->ntri};
-            for (int I0 = 0; I0 < c->nRB; I0 += PB) {
-                const int nI = std::min(PB, c->nRB - I0), i0 = I0 * kSyT;
+            // tile-sharded: only the row blocks of this rank's super-rows
+            const int Ib = c->tshard ? c->sP0 * kSyS : 0;
+            const int Ie = c->tshard ? std::min(c->nRB, c->sP1 * kSyS) : c->nRB;
+            for (int I0 = Ib; I0 < Ie; I0 += PB) {
+                const int nI = std::min(PB, Ie - I0), i0 = I0 * kSyT;
                 const int rows = std::min(nI * kSyT, c->N - i0), ncols = c->N - i0;
                 if (cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, rows, ncols, M, &one,
                                 Ab + (size_t)i0 * M, M, Ab + (size_t)i0 * M, M, &zero, P,
@@ -2590,7 +2677,8 @@ int cimcs_build_coupling(cimcs_ctx* c) {
 
 int cimcs_get_coupling(cimcs_ctx* c, int32_t b, double* G, double* hz, double* D) {
     if (!c || !c->built || b < 0 || b >= c->B) return fail(CIMCS_INPUT_ERROR, "bad instance");
-    if (c->world > 1) return fail(CIMCS_CONFIG_ERROR, "get_coupling: not on a row-sharded context");
+    if (c->world > 1 || c->tworld > 1)
+        return fail(CIMCS_CONFIG_ERROR, "get_coupling: not on a sharded context");
     const int N = c->N, ld = c->ldN, RB = c->RB, ldJ = c->ldJ;
     const size_t gstride = (size_t)c->nRB * ldJ * RB;
     auto fetch = [&](const void* d, size_t off, size_t n, std::vector<double>& h) -> int {

@@ -461,6 +461,29 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
                      "n"(kCols));
 }
 
+// Tile-sharded contexts (one rank per GPU, replicated state): the slot sums
+// of the rank's own items, in the update kernel's slot order, into a one-slot
+// buffer [B][nRB][128][NR] that NCCL all-reduces before the update.
+template <int NR>
+__global__ void __launch_bounds__(kSyT * NR / 4) sym_slotsum_kernel(const float* __restrict__ spart,
+                                                                     float* __restrict__ H, int nRB,
+                                                                     int nSB, int b0) {
+    constexpr int QG = NR / 4;
+    const int K = blockIdx.x, b = b0 + blockIdx.y, t = threadIdx.x, g = t % QG, row = t / QG;
+    const float4* src = reinterpret_cast<const float4*>(
+                            spart + (((size_t)b * nRB + K) * nSB * kSyT + row) * NR) + g;
+    constexpr size_t kSlot4 = (size_t)kSyT * NR / 4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < nSB; ++s) {
+        const float4 v = __ldcs(src + s * kSlot4);
+        acc.x = acc.x + v.x;
+        acc.y = acc.y + v.y;
+        acc.z = acc.z + v.z;
+        acc.w = acc.w + v.w;
+    }
+    reinterpret_cast<float4*>(H + (((size_t)b * nRB + K) * kSyT + row) * NR)[g] = acc;
+}
+
 // Second pass of a step in ONE kernel, 4 replicas per thread: block (b, K) is
 // handled by 128 x (NR / 4) threads; thread (row, g), g = t % (NR / 4) fastest
 // so a warp reads whole 64-byte state rows (coalesced float4), sums its 4

@@ -5,10 +5,16 @@ Two partitionings:
 * instance sharding (configs 1/2): independent instances are split into
   contiguous blocks balanced by gram-build + step cost; all replicas of an
   instance stay on one GPU (they share its gram).  No data-path collective.
-* row sharding (config 4): one instance too large for a GPU; rank k owns the
-  gram rows [r0, r1) (whole row blocks of the contraction tile) and the state
-  of those spins; after every Euler step (and every Jacobi sweep) the
-  contraction input w is all-gathered so each rank holds the full vector.
+* tile sharding (config 4 on the fp32 symmetric path, the default for sharded
+  contexts): every rank keeps the full state and streams only the upper-
+  triangle gram tiles of its super-rows (tile_shard); the per-rank partial
+  products G w are all-reduced once per step / sweep and every rank runs the
+  same update -- one collective, no all-gather, no reconciliation;
+* row sharding (fp64 / CUDA-core contexts): one instance too large for a GPU;
+  rank k owns the gram rows [r0, r1) (whole row blocks of the contraction
+  tile) and the state of those spins; after every Euler step (and every Jacobi
+  sweep) the contraction input w is all-gathered so each rank holds the full
+  vector.
 
 These helpers are pure host logic (tests/test_dist.py drives them with
 world_size 2 over gloo); the CUDA path consumes the plans.
@@ -56,3 +62,15 @@ def row_shard(N: int, world: int, rank: int, quantum: int = ROW_QUANTUM) -> tupl
 def padded_rows(N: int, world: int, quantum: int = ROW_QUANTUM) -> int:
     """Global padded length so every rank's slice has the same size (all-gather)."""
     return -(-N // (world * quantum)) * quantum * world
+
+
+def tile_shard(nRB: int, world: int, rank: int) -> tuple[int, int]:
+    """Super-rows [P0, P1) of the symmetric gram (4 row blocks of 128 each)
+    streamed by `rank`: the C runtime's own partition (cimcs_tile_shard),
+    contiguous and balanced by upper-triangle tile count."""
+    import ctypes as C
+    from ._lib import load
+    from .cimcs import _check
+    a, b = C.c_int32(), C.c_int32()
+    _check(load().cimcs_tile_shard(nRB, world, rank, C.byref(a), C.byref(b)))
+    return a.value, b.value

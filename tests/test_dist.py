@@ -6,7 +6,13 @@
   ranks and the contraction input all-gathered after every Euler step is
   bit-identical to the unsharded integration (config 4's exchange protocol),
   the per-rank step restating solver_mfz.cpp:47-88 with the oracle's
-  canonical contraction.
+  canonical contraction;
+* tile sharding (config 4 on the symmetric path): the runtime's own super-row
+  partition (cimcs_tile_shard) covers every upper-triangle tile exactly once,
+  and the per-rank products of the owned tiles (G w and G^T w of each tile),
+  all-reduced, give G w on every rank -- an MFZ trajectory integrated that
+  way on two ranks matches the unsharded integration and is identical on
+  both ranks (the replicated-state invariant).
 """
 import os
 import socket
@@ -100,6 +106,62 @@ def _row_worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
+def _tile_worker(rank, world, port, q):
+    from oracle import oracle as O
+    _init(rank, world, port)
+    T = 16  # tile edge of this host restatement (the GPU uses 128)
+    N = 150
+    nRB = -(-N // T)
+    inst = O.gen_instance(N, 0.6, 0.2, 0.01, 11)
+    p = O.Problem(inst, O.EXPLICIT)
+    G = np.zeros((nRB * T, nRB * T))
+    G[:N, :N] = p.G
+    P0, P1 = sharding.tile_shard(nRB, world, rank)
+    S = 4
+    mine = [(I, J) for P in range(P0, P1) for I in range(P * S, min(nRB, P * S + S))
+            for J in range(I, nRB)]
+    hp = O.baseline_params(velo=1, n_steps=60)
+    rng = O.Rng(O.mix_seed(11, 1))
+    c = np.array([rng.gauss() for _ in range(N)]) * 0.01
+    e = np.ones(N)
+    R = p.hz.copy()
+    traj = []
+    for k in range(hp.n_steps):
+        w = np.zeros(nRB * T)
+        w[:N] = R * (c > 0)
+        part = np.zeros(nRB * T)
+        for I, J in mine:  # each stored tile feeds both uses (sym_kernels.cuh)
+            g = G[I * T:(I + 1) * T, J * T:(J + 1) * T]
+            part[I * T:(I + 1) * T] += g @ w[J * T:(J + 1) * T]
+            if I != J:
+                part[J * T:(J + 1) * T] += g.T @ w[I * T:(I + 1) * T]
+        t = torch.from_numpy(part)
+        dist.all_reduce(t)  # one collective per step; every rank gets the same sum
+        Gw = t.numpy()[:N]
+        h = 0.5 * ((p.gram_diag * w[:N] - Gw) + p.hz)  # BN field, tau = 1
+        p_k = O.pump_table(hp)[k]
+        c, e = O.mfz_step(c, e, p_k, hp, 0.5, R, h)
+        traj.append(c.copy())
+    n_tiles = torch.tensor([len(mine)])
+    dist.all_reduce(n_tiles)
+    q.put((rank, np.array(traj), int(n_tiles), nRB))
+    dist.destroy_process_group()
+
+
+def _spawn_all(fn):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=fn, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in ps:
+        p_.start()
+    outs = [q.get(timeout=600) for _ in ps]
+    for p_ in ps:
+        p_.join(timeout=600)
+        assert p_.exitcode == 0
+    return sorted(outs, key=lambda o: o[0])
+
+
 def _spawn(fn):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -144,3 +206,40 @@ def test_instance_sharding_gloo(O):
 def test_row_sharded_step_gloo(O):
     c, ref = _spawn(_row_worker)
     assert np.array_equal(c, ref)
+
+
+def test_tile_shard_plan():
+    """Contiguous super-rows, every rank non-empty, balanced by tile count."""
+    for nRB, world in ((782, 8), (782, 2), (16, 2), (130, 4)):
+        spans = [sharding.tile_shard(nRB, world, r) for r in range(world)]
+        nSB = -(-nRB // 4)
+        assert spans[0][0] == 0 and spans[-1][1] == nSB
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+        tiles = []
+        for P0, P1 in spans:
+            tiles.append(sum(min(4, nRB - 4 * P) * (nRB - 4 * P) - (min(4, nRB - 4 * P) *
+                             (min(4, nRB - 4 * P) - 1)) // 2 for P in range(P0, P1)))
+        assert sum(tiles) == nRB * (nRB + 1) // 2
+        if nRB >= 130:
+            assert max(tiles) <= 1.35 * sum(tiles) / world, tiles
+
+
+def test_tile_sharded_step_gloo(O):
+    outs = _spawn_all(_tile_worker)
+    (_, t0, n_tiles, nRB), (_, t1, _, _) = outs
+    assert n_tiles == nRB * (nRB + 1) // 2  # every tile streamed by exactly one rank
+    assert np.array_equal(t0, t1)            # replicated state stays identical
+    # the unsharded integration with the dense product
+    N = 150
+    inst = O.gen_instance(N, 0.6, 0.2, 0.01, 11)
+    p = O.Problem(inst, O.EXPLICIT)
+    hp = O.baseline_params(velo=1, n_steps=60)
+    rng = O.Rng(O.mix_seed(11, 1))
+    c = np.array([rng.gauss() for _ in range(N)]) * 0.01
+    e = np.ones(N)
+    R = p.hz.copy()
+    for k in range(hp.n_steps):
+        w = R * (c > 0)
+        h = 0.5 * ((p.gram_diag * w - p.G @ w) + p.hz)
+        c, e = O.mfz_step(c, e, O.pump_table(hp)[k], hp, 0.5, R, h)
+        assert np.allclose(t0[k], c, rtol=1e-9, atol=1e-12)
