@@ -68,8 +68,8 @@ __device__ __forceinline__ float2 shfl2(float2 v, int m) {
 // DIT (inverse, conj twiddles): bit-reversed in, natural out,
 // (a, b) -> (a + b w*, a - b w*).  w = exp(-2 pi i pos / (2 span)).
 template <bool DIF, int LN>
-__device__ __forceinline__ void fft_pass_t(float2* X, int nlines, int es, int ls,
-                                           const float2* tw) {
+__device__ __noinline__ void fft_pass_t(float2* X, int nlines, int es, int ls,
+                                        const float2* tw) {  // one copy per call site kind: i-cache
     constexpr int n = 1 << LN;
     constexpr int E = n >= 32 ? n / 32 : 1;          // elements per lane
     constexpr int G = n >= 32 ? 1 : 32 / n;          // lines per warp

@@ -509,6 +509,19 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
     const bool valid = i < N;
     const size_t si = (size_t)b * a.ldN + i, vi0 = si * NR + q0;
     sy_pdl_wait();  // the tile kernel's partial products
+    // state of the step modes first: its loads are in flight with the slot loads
+    float4 st_w = make_float4(0.f, 0.f, 0.f, 0.f), st_r = st_w, st_c = st_w, st_e = st_w;
+    float st_D = 0.f, st_hz = 0.f;
+    if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
+        if (valid) {
+            st_w = __ldg(reinterpret_cast<const float4*>(a.Win + vi0));
+            st_r = __ldg(reinterpret_cast<const float4*>(a.Rs + vi0));
+            st_c = *reinterpret_cast<const float4*>(a.C + vi0);
+            st_e = *reinterpret_cast<const float4*>(a.E + vi0);
+            st_D = __ldg(a.D + si);
+            st_hz = __ldg(a.hz + si);
+        }
+    }
     // ---- slot sums
     float gw[4];
     {
@@ -535,9 +548,11 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
         gw[0] = acc.x; gw[1] = acc.y; gw[2] = acc.z; gw[3] = acc.w;
     }
     bool fz[4];
+    const int4 fg4 = *reinterpret_cast<const int4*>(a.fail_gstep + b * NR + q0);
+    const int fga[4] = {fg4.x, fg4.y, fg4.z, fg4.w};
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-        const int fg = a.fail_gstep[b * NR + q0 + u];
+        const int fg = fga[u];
         fz[u] = (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) ? fg < a.alt->gstep_base + a.step
                                                              : fg != kFreeTraj;
     }
@@ -545,14 +560,11 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
     if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
         float lmin[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
         if (valid) {
-            const float4 w4 = __ldg(reinterpret_cast<const float4*>(a.Win + vi0));
-            const float4 r4 = __ldg(reinterpret_cast<const float4*>(a.Rs + vi0));
-            const float4 c4 = *reinterpret_cast<const float4*>(a.C + vi0);
-            const float4 e4 = *reinterpret_cast<const float4*>(a.E + vi0);
+            const float4 w4 = st_w, r4 = st_r, c4 = st_c, e4 = st_e;
             const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
             const float Rv[4] = {r4.x, r4.y, r4.z, r4.w}, cv[4] = {c4.x, c4.y, c4.z, c4.w};
             const float ev[4] = {e4.x, e4.y, e4.z, e4.w};
-            const float Dv = __ldg(a.D + si), hzv = __ldg(a.hz + si);
+            const float Dv = st_D, hzv = st_hz;
             const float half_rt = (float)sc.half_rt, rt = (float)sc.rt, dt = (float)sc.dt;
             const float Kj = (float)sc.Kj, nbeta = (float)sc.nbeta, tau = (float)sc.tau;
             const double pd = a.pump ? a.pump[a.step] : a.p_scalar;
