@@ -1043,6 +1043,7 @@ int launch_mri_t(cimcs_ctx* c, const GemvArgs& g) {
     sa.spart = c->dSpart;
     sa.nSB = 1;
     sa.b0 = 0;
+    sa.keep_w = 1;  // the next apply reads the fp32 w
     sym_update_kernel<NR, MODE><<<dim3(c->nRB, 1), kSyT * NR / 4, 0, c->stream>>>(sa);
     CK(cudaGetLastError());
     return 0;

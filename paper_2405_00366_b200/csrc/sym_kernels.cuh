@@ -191,6 +191,7 @@ struct SymArgs {
     const int* sched;      // [grid + 1] item range of each CTA
     int ntri, nSB;         // tiles per instance, super-blocks per row
     int b0;                // first instance of this launch (instance groups)
+    int keep_w;            // step modes: also store the fp32 w (a consumer reads it)
 };
 
 template <int NR>
@@ -510,11 +511,12 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
     const size_t si = (size_t)b * a.ldN + i, vi0 = si * NR + q0;
     sy_pdl_wait();  // the tile kernel's partial products
     // state of the step modes first: its loads are in flight with the slot loads
-    float4 st_w = make_float4(0.f, 0.f, 0.f, 0.f), st_r = st_w, st_c = st_w, st_e = st_w;
+    float4 st_r = make_float4(0.f, 0.f, 0.f, 0.f), st_c = st_r, st_e = st_r;
     float st_D = 0.f, st_hz = 0.f;
     if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
         if (valid) {
-            st_w = __ldg(reinterpret_cast<const float4*>(a.Win + vi0));
+            // the input w is never loaded: in step modes it is a function of the
+            // stored c and R (init_state_kernel and every update write them so)
             st_r = __ldg(reinterpret_cast<const float4*>(a.Rs + vi0));
             st_c = *reinterpret_cast<const float4*>(a.C + vi0);
             st_e = *reinterpret_cast<const float4*>(a.E + vi0);
@@ -560,12 +562,16 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
     if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
         float lmin[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
         if (valid) {
-            const float4 w4 = st_w, r4 = st_r, c4 = st_c, e4 = st_e;
-            const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+            const float4 r4 = st_r, c4 = st_c, e4 = st_e;
             const float Rv[4] = {r4.x, r4.y, r4.z, r4.w}, cv[4] = {c4.x, c4.y, c4.z, c4.w};
             const float ev[4] = {e4.x, e4.y, e4.z, e4.w};
             const float Dv = st_D, hzv = st_hz;
             const float half_rt = (float)sc.half_rt, rt = (float)sc.rt, dt = (float)sc.dt;
+            float wv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                wv[u] = MODE == EPI_STEP_BN ? Rv[u] * (cv[u] > 0.f ? 1.f : 0.f)
+                                            : (Rv[u] * 0.25f) * (cv[u] + rt);
             const float Kj = (float)sc.Kj, nbeta = (float)sc.nbeta, tau = (float)sc.tau;
             const double pd = a.pump ? a.pump[a.step] : a.p_scalar;
             const float loss = sc.minus_j != 0.0 ? (float)((-1.0 + pd) - sc.minus_j)
@@ -607,7 +613,8 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
             }
             *reinterpret_cast<float4*>(a.C + vi0) = make_float4(cn[0], cn[1], cn[2], cn[3]);
             *reinterpret_cast<float4*>(a.E + vi0) = make_float4(en[0], en[1], en[2], en[3]);
-            *reinterpret_cast<float4*>(a.Wout + vi0) = make_float4(wo[0], wo[1], wo[2], wo[3]);
+            if (sa.keep_w)
+                *reinterpret_cast<float4*>(a.Wout + vi0) = make_float4(wo[0], wo[1], wo[2], wo[3]);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {  // min e: warp, then CTA (one atomic per replica)
