@@ -160,7 +160,7 @@ int cimcs_set_problems(cimcs_ctx* ctx, int32_t B, int32_t N, const int32_t* M,
 int cimcs_build_coupling(cimcs_ctx* ctx);
 /* Matrix-free transform-chain problem: MriTransform(target_image, mask, gamma)
  * + make_problem(t, &truth) (mri.hpp:46-99, mri.cpp:209-256, 393-411).
- * target is H x W row-major (H, W powers of two, H*W <= 16384), mask the M
+ * target is H x W row-major (H, W powers of two in [2, 128]), mask the M
  * sampled k-space indices (unique, in range), x_true the Haar coefficients of
  * the target (nullable; xi = x != 0).  B = 1, fp32 contexts only.  Then
  * cimcs_build_coupling computes hz = Re(A^H y) and diag(G); the quadratic form

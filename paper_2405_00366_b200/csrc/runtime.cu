@@ -2441,8 +2441,9 @@ int cimcs_set_mri_problem(cimcs_ctx* c, int32_t H, int32_t W, const double* targ
     if (!c) return fail(CIMCS_INPUT_ERROR, "null context");
     auto pow2 = [](int v) { return v >= 1 && (v & (v - 1)) == 0; };
     if (!pow2(H) || !pow2(W)) return fail(CIMCS_INPUT_ERROR, "MriTransform: dimensions must be powers of two");
-    if (H < 2 || W < 2 || H * W > kMriMaxPix)
-        return fail(CIMCS_INPUT_ERROR, "MriTransform: need 2 <= H, W and H * W <= 16384 (one CTA's shared memory)");
+    if (H < 2 || W < 2 || H > kMriMaxLine || W > kMriMaxLine)
+        return fail(CIMCS_INPUT_ERROR,
+                    "MriTransform: need 2 <= H, W <= 128 (an FFT line lives in one warp's registers)");
     if (!(gamma >= 0.0)) return fail(CIMCS_INPUT_ERROR, "MriTransform: gamma must be >= 0");
     if (!target || !mask || M < 1) return fail(CIMCS_INPUT_ERROR, "MriTransform: mask indices must be unique and in range");
     std::vector<int> idx(mask, mask + M);

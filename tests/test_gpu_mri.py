@@ -139,6 +139,8 @@ def test_operator_problem_errors(gpu, Mr):
                 c.set_mri_problem(img, np.array(bad), 0.0)
         with pytest.raises(gpu.InputError):
             c.set_mri_problem(np.zeros((12, 16)), np.array([1, 2]), 0.0)
+        with pytest.raises(gpu.InputError):  # FFT lines longer than 128
+            c.set_mri_problem(np.zeros((16, 256)), np.array([1, 2]), 0.0)
 
 
 def test_lasso_warm_start_matches_oracle(gpu, Mr):
