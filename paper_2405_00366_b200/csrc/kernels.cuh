@@ -233,8 +233,12 @@ struct Ops {
             const float4 v = *reinterpret_cast<const float4*>(gp);
             g[0] = v.x; g[1] = v.y; g[2] = v.z; g[3] = v.w;
         } else {
-            const double2 v = *reinterpret_cast<const double2*>(gp);
-            g[0] = v.x; g[1] = v.y;
+#pragma unroll
+            for (int r = 0; r < RPL; r += 2) {
+                const double2 v = *reinterpret_cast<const double2*>(gp + r);
+                g[r] = v.x;
+                g[r + 1] = v.y;
+            }
         }
         if constexpr (sizeof(T) == 4 && NR % 4 == 0) {
 #pragma unroll
