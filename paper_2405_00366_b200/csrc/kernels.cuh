@@ -38,7 +38,7 @@ template <> struct Cfg<float> {
 };
 template <> struct Cfg<double> {
     static constexpr int RPL = 2;
-    static constexpr int kStages = 3;
+    static constexpr int kStages = 4;
     static constexpr int kMinBlocks = 1;
 };
 
