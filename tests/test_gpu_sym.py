@@ -182,3 +182,29 @@ def test_tile_sharded_context_world1_bitwise(gpu, O, cdp):
     assert np.array_equal(a["sigma"], b["sigma"])
     assert np.array_equal(a["R"], b["R"])
     assert np.array_equal(a["history"]["hamiltonian"], b["history"]["hamiltonian"])
+
+
+def test_sym_phase_grid_mixed_M_matches_fp64(gpu, O):
+    """A config-2-style mini phase grid on the symmetric path: instances of one
+    context differ in M (alpha 0.3..0.9) and K, the gram tiles are built per run
+    of equal M, items of all instances share one LPT schedule; supports agree
+    with the fp64 oracle on >= 90 % of trajectories (fp32 stated tolerance)."""
+    cells = [(0.3, 0.05), (0.5, 0.1), (0.7, 0.2), (0.9, 0.3), (0.4, 0.15)]
+    insts = [O.gen_instance(700, al, a, 0.01, 100 + k) for k, (al, a) in enumerate(cells)]
+    R = 8
+    hp = O.baseline_params(velo=5, n_steps=400)
+    seeds = np.array([[O.mix_seed(i.seed, 1 + 3 * r) for r in range(R)] for i in insts],
+                     np.uint64)
+    ctx = _ctx(gpu, insts)
+    res = ctx.solve(R, "mfz-bn", gpu.baseline_params(velo=5, n_steps=400), seeds)
+    ctx.close()
+    same, rel = 0, []
+    for b, inst in enumerate(insts):
+        for r in range(R):
+            ref = O.Problem(inst, O.CANON).alternating_minimize(O.MFZ_BN, hp,
+                                                                O.Rng(int(seeds[b, r])))
+            same += np.array_equal(res["sigma"][b, r], ref["sigma"])
+            g = O.rmse(res["R"][b, r], res["sigma"][b, r], inst.x_true, inst.xi_true)
+            rel.append(abs(g - ref["final_rmse"]) / max(ref["final_rmse"], 1e-12))
+    assert same >= 0.9 * len(insts) * R, same
+    assert np.mean(rel) <= 5e-2, np.mean(rel)
