@@ -86,6 +86,12 @@ __device__ __forceinline__ void cl_st_async16(uint32_t raddr, uint64_t lo, uint6
         "l"(lo), "l"(hi), "r"(rbar)
         : "memory");
 }
+__device__ __forceinline__ void cl_st_async8(uint32_t raddr, uint64_t v, uint32_t rbar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+        "l"(v), "r"(rbar)
+        : "memory");
+}
 __device__ __forceinline__ void cl_st_async4(uint32_t raddr, uint32_t v, uint32_t rbar) {
     asm volatile(
         "st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(raddr),

@@ -395,7 +395,18 @@ __global__ void __launch_bounds__(kMriCThreads, 1) mri_cluster_kernel(MriArgs a)
     const int q = blockIdx.x / CS;
     const float* win = a.in;
     const float s = 0.70710678118654752440f;
+    // arrival barriers of the three exchanges (st.async ... complete_tx): a CTA
+    // proceeds as soon as ITS inputs have landed, no cluster-wide barrier
+    __shared__ __align__(8) uint64_t mb[3];  // column slab, row slab, low-pass quadrant
+    if (threadIdx.x == 0) {
+        for (int e = 0; e < 3; ++e) mbar_init(&mb[e], 1);
+        mbar_fence_init();
+        mbar_arrive_expect_tx(&mb[0], (uint32_t)(H * CW * 8));
+        mbar_arrive_expect_tx(&mb[1], (uint32_t)(RH * W * 8));
+        mbar_arrive_expect_tx(&mb[2], (uint32_t)(H2 * W2 * 4));
+    }
     for (int t = threadIdx.x; t < 64; t += blockDim.x) tw[t] = a.tw[t];
+    cl.sync();  // every CTA's barriers are armed before any peer stores into it
     // 1. low-pass quadrant (redundant), levels 2.. of the inverse
     for (int t = threadIdx.x; t < H2 * W2; t += blockDim.x) {
         const int i = t >> lW2, j = t & (W2 - 1);
@@ -427,9 +438,11 @@ __global__ void __launch_bounds__(kMriCThreads, 1) mri_cluster_kernel(MriArgs a)
     fft_pass<true>(Kr, RH, lW, 1, RS, tw);
     for (int t = threadIdx.x; t < RH * W; t += blockDim.x) {
         const int r = t >> lW, j = t & (W - 1), m = j >> lCW;
-        cl.map_shared_rank(Kc, m)[(size_t)(r0 + r) * CSt + (j & (CW - 1))] = Kr[(size_t)r * RS + j];
+        const float2 v = Kr[(size_t)r * RS + j];
+        cl_st_async8(cl_mapa(smem_u32(Kc + (size_t)(r0 + r) * CSt + (j & (CW - 1))), m),
+                     *reinterpret_cast<const uint64_t*>(&v), cl_mapa(smem_u32(&mb[0]), m));
     }
-    cl.sync();
+    cl_wait(&mb[0], 0);
     // 3. DIF columns, mask, DIT columns, gather back to the row owners
     fft_pass<true>(Kc, CW, lH, CSt, 1, tw);
     for (int t = threadIdx.x; t < H * CW; t += blockDim.x) {
@@ -442,9 +455,11 @@ __global__ void __launch_bounds__(kMriCThreads, 1) mri_cluster_kernel(MriArgs a)
     fft_pass<false>(Kc, CW, lH, CSt, 1, tw);
     for (int t = threadIdx.x; t < H * CW; t += blockDim.x) {
         const int i = t >> lCW, jl = t & (CW - 1), m = i >> lRH;
-        cl.map_shared_rank(Kr, m)[(size_t)(i & (RH - 1)) * RS + c0 + jl] = Kc[(size_t)i * CSt + jl];
+        const float2 v = Kc[(size_t)i * CSt + jl];
+        cl_st_async8(cl_mapa(smem_u32(Kr + (size_t)(i & (RH - 1)) * RS + c0 + jl), m),
+                     *reinterpret_cast<const uint64_t*>(&v), cl_mapa(smem_u32(&mb[1]), m));
     }
-    cl.sync();
+    cl_wait(&mb[1], 0);
     // 4. DIT rows; real part + smoothness
     fft_pass<false>(Kr, RH, lW, 1, RS, tw);
     const bool smooth = a.gamma > 0.f;
@@ -466,9 +481,11 @@ __global__ void __launch_bounds__(kMriCThreads, 1) mri_cluster_kernel(MriArgs a)
         a.out[((size_t)(aa << lW) + W2 + bb) * NR + q] = (p1 + q1) * s;          // HL
         a.out[((size_t)((H2 + aa) << lW) + bb) * NR + q] = (p0 - q0) * s;        // LH
         a.out[((size_t)((H2 + aa) << lW) + W2 + bb) * NR + q] = (p1 - q1) * s;   // HH
-        for (int m = 0; m < CS; ++m) cl.map_shared_rank(Q, m)[(aa << lW2) + bb] = LL;
+        const uint32_t dst = smem_u32(Q + (aa << lW2) + bb), bar = smem_u32(&mb[2]);
+        for (int m = 0; m < CS; ++m)
+            cl_st_async4(cl_mapa(dst, m), __float_as_uint(LL), cl_mapa(bar, m));
     }
-    cl.sync();
+    cl_wait(&mb[2], 0);
     haar_forward<kMriCThreads>(Q, lH - 1, lW - 1);
     for (int t = threadIdx.x; t < (RH >> 1) * W2; t += blockDim.x) {
         const int idx = ((r0 >> 1) << lW2) + t, i = idx >> lW2, j = idx & (W2 - 1);
