@@ -57,10 +57,10 @@ constexpr int kSyPlaneHalfs = kSyT * kSyT;             // 16384
 constexpr uint32_t kSyPlaneBytes = kSyPlaneHalfs * 2;  // 32 KB
 constexpr int kSyThreads = 6 * 32;
 constexpr int kSyS = 4;                                // item edge in tiles
-constexpr int kSyAcc = 4;                              // TMEM accumulator buffers
+constexpr int kSyAcc = 2;                              // TMEM accumulator buffers
 constexpr int kSyBarBytes = 256;                       // mbarriers after the stages
 template <int NR>
-__host__ __device__ constexpr int sy_tmem_cols() { return kSyAcc * 4 * NR; }  // 256 (NR 16) / 128 (NR 8)
+__host__ __device__ constexpr int sy_tmem_cols() { return kSyAcc * 4 * NR; }  // 128 (NR 16) / 64 (NR 8)
 
 // byte offset of element (mn, k) of an fp16 operand in the canonical no-swizzle
 // K-major layout (core matrix = 8 MN rows x 8 K = 16 bytes per row)
