@@ -164,8 +164,50 @@ def make_instances(rank, config=1, ws=1):
     if config == 3:
         return W.config3()
     if config == 4:
+        if ws > 1:
+            return shared_config4(rank, ws)
         return W.config4(N=CFG.get("n4", 100_000))
     return W.config1(rank, CFG["B"])
+
+
+def shared_config4(rank, ws):
+    """Config 4 under torchrun: the one instance (A alone is 40 GB at full size) is
+    generated once, by rank 0, into /dev/shm and memory-mapped by every rank (one
+    copy in the page cache instead of ws generators and ws copies); falls back to
+    per-rank generation when /dev/shm cannot hold it."""
+    import torch.distributed as dist
+    from paper_2405_00366_b200 import workloads as W
+    from paper_2405_00366_b200.cimcs import Instance
+    N = CFG.get("n4", 100_000)
+    d = f"/dev/shm/cimcs_c4_{N}_{os.environ.get('MASTER_PORT', '0')}"
+    ok = [False]
+    if rank == 0:
+        insts, R, hp, dt = W.config4(N=N)
+        try:
+            os.makedirs(d, exist_ok=True)
+            i = insts[0]
+            for name, arr in (("A", i.A), ("y", i.y), ("x", i.x_true), ("xi", i.xi_true)):
+                np.save(os.path.join(d, name + ".npy"), np.asfortranarray(arr))
+            ok = [True]
+        except OSError as e:
+            print(f"config 4: /dev/shm sharing failed ({e}); ranks generate their own copy",
+                  file=sys.stderr)
+    dist.broadcast_object_list(ok, src=0)
+    if rank == 0:
+        out = insts, R, hp, dt
+    elif ok[0]:
+        _, R, hp, dt = W.config4(N=8)  # schedule and replica count only
+        ld = lambda n: np.load(os.path.join(d, n + ".npy"), mmap_mode="r")  # noqa: E731
+        inst = Instance(ld("A"), np.array(ld("y")), np.array(ld("x")), np.array(ld("xi")),
+                        0.05, 0.5, 0.01, 7)
+        out = [inst], R, hp, dt
+    else:
+        out = W.config4(N=N)
+    dist.barrier()
+    if rank == 0 and ok[0]:
+        import shutil
+        shutil.rmtree(d, ignore_errors=True)  # mapped pages stay valid until unmapped
+    return out
 
 
 def cpu_sample(insts, nthreads, alt_limit=1, n_steps=None):
