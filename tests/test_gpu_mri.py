@@ -94,23 +94,26 @@ def test_full_sampling_recovers_sparse_image(gpu, Mr):
         assert H[-1]["hamming"] == 0.0 and H[-1]["rmse"] < 1e-5
 
 
-def test_solve_matches_fp64_oracle(gpu, O, Mr):
+@pytest.mark.parametrize("backend", ["mfz-bn", "mfz-cn"])
+def test_solve_matches_fp64_oracle(gpu, O, Mr, backend):
     """32 x 32, 40 % k-space, gamma 1e-4, BASELINE schedule shortened to 5 x 300
-    steps, 8 replicas: the GPU fp32 solve against the oracle's fp64 solve of
-    the assembled form (Problem.from_gram, CG as cdp_minimize_operator)."""
+    steps, 8 replicas (cluster-distributed apply): the GPU fp32 solve against the
+    oracle's fp64 solve of the assembled form (Problem.from_gram, CG as
+    cdp_minimize_operator), binarised and continuous feedback."""
     img, coeffs = Mr.sparsify_wavelet(Mr.phantom_image(32, 32), 0.1)
     mask = Mr.make_mask(32, 32, 410, 3)
     J, hz, _ = Mr.assemble_operators(img, mask, 1e-4)
     xi = (coeffs != 0).astype(np.int32)
     R = 8
-    seeds = np.array([[O.mix_seed(1, 1 + 3 * r) for r in range(R)]], np.uint64)
+    be = O.MFZ_BN if backend == "mfz-bn" else O.MFZ_CN
+    seeds = np.array([[O.mix_seed(1, be + 3 * r) for r in range(R)]], np.uint64)
     ohp = O.baseline_params(velo=4, n_steps=300)
     p = O.Problem.from_gram(J, hz, coeffs, xi)
     with _ctx(gpu, img, mask, 1e-4, coeffs) as ctx:
-        res = ctx.solve(R, "mfz-bn", gpu.baseline_params(velo=4, n_steps=300), seeds)
+        res = ctx.solve(R, backend, gpu.baseline_params(velo=4, n_steps=300), seeds)
     same, drm = 0, []
     for r in range(R):
-        ref = p.alternating_minimize(O.MFZ_BN, ohp, O.Rng(int(seeds[0, r])), cdp=O.CDP_CG)
+        ref = p.alternating_minimize(be, ohp, O.Rng(int(seeds[0, r])), cdp=O.CDP_CG)
         assert not ref["failed"] and res["fail_alt"][0, r] == -1
         same += np.array_equal(res["sigma"][0, r], ref["sigma"])
         g = res["history"][0, r][res["n_hist"][0, r] - 1]["rmse"]
