@@ -296,12 +296,21 @@ def run_ours(args, ws, rank, local):
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl")
-    insts, R, hp, wdtype = make_instances(rank, args.config, ws)
+    device_gen = args.device_gen and args.config == 4
+    if device_gen:  # counter-based instance drawn on the GPU (a deviation)
+        from paper_2405_00366_b200.workloads import config4 as _c4
+        _, R, hp, wdtype = _c4(N=8)
+        Nd = CFG.get("n4", 100_000)
+        gen_params = [(0.5, 0.05, 0.01, 7)]
+        Md, _ = P.gen_dims(Nd, 0.5, 0.05)
+        insts = [P.Instance(np.zeros((Md, 0)), np.zeros(0), seed=7)]  # shape/seed stand-in
+    else:
+        insts, R, hp, wdtype = make_instances(rank, args.config, ws)
     if args.dtype is None:
         args.dtype = wdtype
     seeds = P.replica_seeds(insts, R, "mfz-bn")
     nalt = hp.velo + 1
-    Bn, Nn = len(insts), insts[0].N
+    Bn, Nn = len(insts), (Nd if device_gen else insts[0].N)
     units = Bn * R * Nn * hp.n_steps * nalt  # spin-steps per rank per step
     # config 4 on several GPUs (or --shard): ONE instance split by gram tiles
     # across the ranks (tile-sharded contexts: replicated state, one NCCL
@@ -319,7 +328,17 @@ def run_ours(args, ws, rank, local):
     if tile_sharded:
         units = units / ws
     ctx = make_ctx()
-    ctx.set_problems(insts)
+
+    def load_problems(cx):
+        if device_gen:
+            cx.set_generated_problems(Nd, gen_params)
+        else:
+            cx.set_problems(insts)
+
+    t_gen = time.perf_counter()
+    load_problems(ctx)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t_gen
 
     def one_step():
         ctx.build_coupling()
@@ -386,7 +405,7 @@ def run_ours(args, ws, rank, local):
         ctx2 = make_ctx()
 
         def e2e_once():
-            ctx2.set_problems(insts)
+            load_problems(ctx2)
             ctx2.build_coupling()
             out = ctx2.solve(R, "mfz-bn", hp, seeds)
             torch.cuda.synchronize()
@@ -407,12 +426,13 @@ def run_ours(args, ws, rank, local):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
         e2e_val = total_units / e2e_s
-        h2d = sum(i.A.nbytes + i.y.nbytes + i.x_true.nbytes + i.xi_true.nbytes for i in insts)
+        h2d = 0 if device_gen else sum(i.A.nbytes + i.y.nbytes + i.x_true.nbytes +
+                                       i.xi_true.nbytes for i in insts)
         h2d += Bn * R * Nn * 8 * nalt  # host-drawn c0 streams
         d2h = r2["R"].nbytes + r2["sigma"].nbytes + r2["history"].nbytes
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
+    if rank == 0 and ws == 1 and not args.no_cpu and not device_gen:
         nthreads = os.cpu_count() or 1
         if args.config == 4:
             cs = 2
@@ -452,7 +472,9 @@ def run_ours(args, ws, rank, local):
             "scaling": "strong" if args.config == 2 or tile_sharded else "weak",
             "vs_baseline": None,
             "dtype": args.dtype,
-            "data": "synthetic (seeded gen_instance, datagen.cpp:15-55)",
+            "data": ("synthetic, generated on the GPU from counter-based Philox streams "
+                     "(documented deviation: not the reference's mt19937_64 instance)"
+                     if device_gen else "synthetic (seeded gen_instance, datagen.cpp:15-55)"),
             "config": {"workload": (WORKLOADS[args.config] if args.config != 4 or args.n4 == 100_000
                                     else WORKLOADS[4].replace("N=100000 M=50000 K=5000",
                                                               f"N={Nn} (reduced)")),
@@ -464,6 +486,7 @@ def run_ours(args, ws, rank, local):
                        "l2": ("inputs larger than L2 (gram %.2f GB per step)" % (step_bytes / 1e9)
                               if step_bytes > 126e6 else "gram fits in L2 (no flush)")},
             "instances_per_s": (Bn if tile_sharded else total_units / units * Bn) / (ms_per_step * 1e-3),
+            "problem_load_s": gen_s,
             "breakdown_ms": {"gram": statistics.median(gram_ms), "cim": statistics.median(cim_ms),
                              "refit": statistics.median(refit_ms),
                              "score": statistics.median(score_ms)},
@@ -613,6 +636,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fp64", action="store_true", help="skip the fp64 secondary line")
+    ap.add_argument("--device-gen", action="store_true",
+                    help="config 4: generate the instance on the GPU (counter-based deviation)")
     ap.add_argument("--shard", action="store_true",
                     help="config 4: use the tile-sharded context even on one GPU")
     ap.add_argument("--mri", action="store_true",

@@ -157,6 +157,17 @@ int cimcs_set_problems(cimcs_ctx* ctx, int32_t B, int32_t N, const int32_t* M,
 /* K1: G = A^T A (gram, full diagonal), hz = A^T y, D = diag(G), device
  * resident.  Replaces coupling_from_observation (model.cpp:54-63) and the
  * per-step matrix-free A^T(A w) (orchestrator.cpp:86-88): J w = D∘w - G w. */
+/* a DOCUMENTED DEVIATION for config-4-scale runs: B
+ * instances with gen_instance's recipe and shapes (datagen.cpp:15-55) drawn on
+ * the GPU from counter-based Philox4x32-10 streams instead of the reference's
+ * sequential mt19937_64 stream, so they are NOT the reference's instances
+ * (never used for parity).  Replaces cimcs_set_problems (A, y, x, xi resident). */
+int cimcs_set_generated_problems(cimcs_ctx* ctx, int32_t B, int32_t N, const double* alpha,
+                                 const double* a, const double* nu, const uint64_t* seeds);
+/* The resident instance b back on the host (A column-major M x N; x/xi when
+ * ground truth is set); e.g. to hand a generated instance to save_instance. */
+int cimcs_get_instance(cimcs_ctx* ctx, int32_t b, double* A, double* y, double* x_true,
+                       int32_t* xi_true);
 int cimcs_build_coupling(cimcs_ctx* ctx);
 /* Matrix-free transform-chain problem: MriTransform(target_image, mask, gamma)
  * + make_problem(t, &truth) (mri.hpp:46-99, mri.cpp:209-256, 393-411).

@@ -28,7 +28,8 @@ EXPORTS = (
     "cimcs_nccl_unique_id", "cimcs_create_sharded", "cimcs_format_double", "cimcs_fnv1a64",
     "cimcs_save_instance", "cimcs_load_instance", "cimcs_csv_open", "cimcs_csv_row",
     "cimcs_csv_close", "cimcs_make_mask", "cimcs_set_mri_problem",
-    "cimcs_mri_lasso", "cimcs_tile_shard",
+    "cimcs_mri_lasso", "cimcs_tile_shard", "cimcs_set_generated_problems",
+    "cimcs_get_instance",
 )
 
 
@@ -110,6 +111,8 @@ def load() -> C.CDLL:
     L.cimcs_csv_close.argtypes = [vp]
     L.cimcs_make_mask.argtypes = [i32, i32, i32, u64, vp]
     L.cimcs_tile_shard.argtypes = [i32, i32, i32, vp, vp]
+    L.cimcs_set_generated_problems.argtypes = [vp, i32, i32, vp, vp, vp, vp]
+    L.cimcs_get_instance.argtypes = [vp, i32, vp, vp, vp, vp]
     L.cimcs_set_mri_problem.argtypes = [vp, i32, i32, vp, i32, vp, d, vp]
     L.cimcs_mri_lasso.argtypes = [vp, d, i32, d, d, vp, vp, vp]
     _lib = L

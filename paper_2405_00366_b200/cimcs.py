@@ -294,6 +294,35 @@ class Context:
                                          float(step), x.ctypes.data, C.byref(it), C.byref(f)))
         return x, it.value, f.value
 
+    def set_generated_problems(self, N: int, params: Sequence[tuple]):
+        """Instances generated ON THE GPU from counter-based Philox streams
+        (gen_instance's recipe, NOT the reference's mt19937_64 stream: a documented
+        deviation for config-4-scale runs); params = [(alpha, a, nu, seed), ...]."""
+        B = len(params)
+        al = np.array([p[0] for p in params], np.float64)
+        aa = np.array([p[1] for p in params], np.float64)
+        nu = np.array([p[2] for p in params], np.float64)
+        sd = np.array([p[3] for p in params], np.uint64)
+        _check(self._lib.cimcs_set_generated_problems(self._ctx, B, N, al.ctypes.data,
+                                                      aa.ctypes.data, nu.ctypes.data,
+                                                      sd.ctypes.data))
+        self.B, self.N = B, N
+        self._gen_params = [tuple(p) for p in params]
+
+    def get_instance(self, b: int) -> Instance:
+        """The resident instance b (e.g. a generated one) back on the host."""
+        al, a, nu, seed = self._gen_params[b] if hasattr(self, "_gen_params") else (0, 0, 0, 0)
+        M, _ = gen_dims(self.N, al, a) if al else (None, None)
+        if M is None:
+            raise InputError("get_instance: only for generated problem sets")
+        A = np.zeros((M, self.N), order="F")
+        y = np.zeros(M)
+        x = np.zeros(self.N)
+        xi = np.zeros(self.N, np.int32)
+        _check(self._lib.cimcs_get_instance(self._ctx, b, A.ctypes.data, y.ctypes.data,
+                                            x.ctypes.data, xi.ctypes.data))
+        return Instance(A, y, x, xi, a, al, nu, int(seed))
+
     def build_coupling(self):
         _check(self._lib.cimcs_build_coupling(self._ctx))
 

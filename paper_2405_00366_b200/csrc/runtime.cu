@@ -2253,15 +2253,10 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
     return 0;
 }
 
-int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
-                       const double* const* A, const double* const* y,
-                       const double* const* x_true, const int32_t* const* xi_true) {
-    if (!c) return fail(CIMCS_INPUT_ERROR, "null context");
-    if (B < 1 || N < 1) return fail(CIMCS_INPUT_ERROR, "need B >= 1 and N >= 1");
-    for (int b = 0; b < B; ++b)
-        if (M[b] < 1 || !A[b] || !y[b]) return fail(CIMCS_INPUT_ERROR, "empty A");
+// Problem-set layout decisions and device allocations shared by set_problems
+// (host instances) and set_generated_problems (instances generated on the GPU).
+int prepare_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M, bool truth) {
     CK(cudaSetDevice(c->device));
-    const bool truth = x_true != nullptr && xi_true != nullptr;
     // same shapes as the resident problem set: keep every device allocation
     const bool reuse = c->dA && c->B == B && c->N == N && c->has_truth == truth &&
                        std::equal(c->M.begin(), c->M.end(), M) && (int)c->M.size() == B &&
@@ -2328,6 +2323,150 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
                    (rc = dalloc(&c->dy, (size_t)B * c->Mmax * 8)) ||
                    (rc = dalloc(&c->dM, (size_t)B * 4))))
         return rc;
+    if (truth && !c->dx) {
+        if ((rc = dalloc(&c->dx, (size_t)B * c->ldN * 8)) ||
+            (rc = dalloc(&c->dxi, (size_t)B * c->ldN)))
+            return rc;
+    }
+    return 0;
+}
+
+// ---------------------------------------- counter-based device generator
+// SURVEY 8f row 4, the documented deviation: config-4-scale instances (A alone
+// is 5e9 normals) drawn on the GPU from Philox4x32-10 streams instead of the
+// reference's single sequential mt19937_64 stream (datagen.cpp:15-55), whose
+// bit-exact reproduction needs that stream's order and glibc's log/cos.  Same
+// recipe and shapes: A_kr = N(0,1)/sqrt(M) (draw index k N + r, stream 0),
+// x_r = N(0,1) (stream 1), support = the K positions with the smallest
+// Philox keys (stream 2, a uniform K-subset), y = A (xi . x) + nu N(0,1)
+// (stream 3) summed over the support in ascending order as gen_instance does.
+// Different numbers from the reference's instances -- never used for parity.
+__host__ __device__ inline void philox4x32_10(uint32_t (&c)[4], uint32_t k0, uint32_t k1) {
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
+        const uint32_t h0 = (uint32_t)(p0 >> 32), l0 = (uint32_t)p0;
+        const uint32_t h1 = (uint32_t)(p1 >> 32), l1 = (uint32_t)p1;
+        const uint32_t n0 = h1 ^ c[1] ^ k0, n2 = h0 ^ c[3] ^ k1;
+        c[0] = n0;
+        c[1] = l1;
+        c[2] = n2;
+        c[3] = l0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+__host__ __device__ inline void philox_u64x2(uint64_t seed, uint32_t stream, uint64_t idx,
+                                             uint64_t* a, uint64_t* b) {
+    uint32_t c[4] = {(uint32_t)idx, (uint32_t)(idx >> 32), stream, 0x5eedu};
+    philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    *a = (uint64_t)c[0] | ((uint64_t)c[1] << 32);
+    *b = (uint64_t)c[2] | ((uint64_t)c[3] << 32);
+}
+__device__ inline double philox_normal(uint64_t seed, uint32_t stream, uint64_t idx) {
+    uint64_t a, b;
+    philox_u64x2(seed, stream, idx, &a, &b);
+    const double u1 = ((double)(a >> 11) + 1.0) * 0x1.0p-53, u2 = (double)(b >> 11) * 0x1.0p-53;
+    return sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);  // rng.hpp's Box-Muller form
+}
+__global__ void devgen_a_kernel(double* A, int M, int N, uint64_t seed, double col_std) {
+    const size_t total = (size_t)M * N;
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+         t += (size_t)gridDim.x * blockDim.x) {
+        const size_t r = t / M, k = t % M;  // column-major storage, row-major draw index
+        A[t] = col_std * philox_normal(seed, 0, (uint64_t)k * N + r);
+    }
+}
+__global__ void devgen_x_kernel(double* x, int N, uint64_t seed) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x)
+        x[r] = philox_normal(seed, 1, r);
+}
+__global__ void devgen_y_kernel(const double* __restrict__ A, int M, const int* __restrict__ supp,
+                                int K, const double* __restrict__ x, double nu, uint64_t seed,
+                                double* y) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < M; k += gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int s = 0; s < K; ++s) acc = acc + A[(size_t)supp[s] * M + k] * x[supp[s]];
+        y[k] = acc + nu * philox_normal(seed, 3, k);
+    }
+}
+
+int cimcs_set_generated_problems(cimcs_ctx* c, int32_t B, int32_t N, const double* alpha,
+                                 const double* a, const double* nu, const uint64_t* seeds) {
+    if (!c) return fail(CIMCS_INPUT_ERROR, "null context");
+    if (B < 1 || N < 1 || !alpha || !a || !nu || !seeds)
+        return fail(CIMCS_INPUT_ERROR, "set_generated_problems: bad arguments");
+    std::vector<int32_t> M(B), K(B);
+    for (int b = 0; b < B; ++b)
+        if (gen_dims(N, alpha[b], a[b], &M[b], &K[b]) || nu[b] < 0.0)
+            return fail(CIMCS_INPUT_ERROR, "gen_instance: bad arguments");
+    if (int rc = prepare_problems(c, B, N, M.data(), true)) return rc;
+    const size_t astride = (size_t)c->Mmax * N;
+    int* dsupp = nullptr;
+    if (int rc = dalloc(&dsupp, (size_t)N * 4)) return rc;
+    std::unique_ptr<int, decltype(&cudaFree)> g(dsupp, &cudaFree);
+    CK(cudaMemsetAsync(c->dx, 0, (size_t)B * c->ldN * 8, c->stream));
+    CK(cudaMemsetAsync(c->dxi, 0, (size_t)B * c->ldN, c->stream));
+    CK(cudaMemcpyAsync(c->dM, M.data(), (size_t)B * 4, cudaMemcpyHostToDevice, c->stream));
+    for (int b = 0; b < B; ++b) {
+        // support: the K smallest stream-2 keys (host, O(N log N))
+        std::vector<std::pair<uint64_t, int>> key(N);
+        for (int r = 0; r < N; ++r) {
+            uint64_t k0, k1;
+            philox_u64x2(seeds[b], 2, (uint64_t)r, &k0, &k1);
+            key[r] = {k0, r};
+        }
+        std::partial_sort(key.begin(), key.begin() + K[b], key.end());
+        std::vector<int> supp(K[b]);
+        for (int s = 0; s < K[b]; ++s) supp[s] = key[s].second;
+        std::sort(supp.begin(), supp.end());
+        std::vector<int8_t> xi8((size_t)c->ldN, 0);
+        for (int r : supp) xi8[r] = 1;
+        double* Ab = c->dA + (size_t)b * astride;
+        double* xb = c->dx + (size_t)b * c->ldN;
+        devgen_a_kernel<<<8 * c->num_sms, 256, 0, c->stream>>>(Ab, M[b], N, seeds[b],
+                                                              1.0 / std::sqrt((double)M[b]));
+        devgen_x_kernel<<<(N + 255) / 256, 256, 0, c->stream>>>(xb, N, seeds[b]);
+        CK(cudaMemcpyAsync(c->dxi + (size_t)b * c->ldN, xi8.data(), xi8.size(),
+                           cudaMemcpyHostToDevice, c->stream));
+        if (K[b] > 0)
+            CK(cudaMemcpyAsync(dsupp, supp.data(), (size_t)K[b] * 4, cudaMemcpyHostToDevice,
+                               c->stream));
+        devgen_y_kernel<<<(M[b] + 255) / 256, 256, 0, c->stream>>>(
+            Ab, M[b], dsupp, K[b], xb, nu[b], seeds[b], c->dy + (size_t)b * c->Mmax);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(c->stream));  // xi8 / supp are reused next instance
+    }
+    return 0;
+}
+
+// the resident instance b back on the host (A column-major M x N; truth when set)
+int cimcs_get_instance(cimcs_ctx* c, int32_t b, double* A, double* y, double* x_true,
+                       int32_t* xi_true) {
+    if (!c || b < 0 || b >= c->B || c->mri || !c->dA) return fail(CIMCS_INPUT_ERROR, "bad instance");
+    const int N = c->N, M = c->M[b];
+    const size_t astride = (size_t)c->Mmax * N;
+    if (A) CK(cudaMemcpy(A, c->dA + (size_t)b * astride, (size_t)M * N * 8, cudaMemcpyDeviceToHost));
+    if (y) CK(cudaMemcpy(y, c->dy + (size_t)b * c->Mmax, (size_t)M * 8, cudaMemcpyDeviceToHost));
+    if (c->has_truth && x_true)
+        CK(cudaMemcpy(x_true, c->dx + (size_t)b * c->ldN, (size_t)N * 8, cudaMemcpyDeviceToHost));
+    if (c->has_truth && xi_true) {
+        std::vector<int8_t> t((size_t)N);
+        CK(cudaMemcpy(t.data(), c->dxi + (size_t)b * c->ldN, (size_t)N, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < N; ++i) xi_true[i] = t[i];
+    }
+    return 0;
+}
+
+int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
+                       const double* const* A, const double* const* y,
+                       const double* const* x_true, const int32_t* const* xi_true) {
+    if (!c) return fail(CIMCS_INPUT_ERROR, "null context");
+    if (B < 1 || N < 1) return fail(CIMCS_INPUT_ERROR, "need B >= 1 and N >= 1");
+    for (int b = 0; b < B; ++b)
+        if (M[b] < 1 || !A[b] || !y[b]) return fail(CIMCS_INPUT_ERROR, "empty A");
+    const bool truth = x_true != nullptr && xi_true != nullptr;
+    if (int rc = prepare_problems(c, B, N, M, truth)) return rc;
+    const size_t astride = (size_t)c->Mmax * N;
     // A and y go through a pinned double buffer filled by host threads
     // (pageable cudaMemcpy runs at a fraction of the link rate)
     if (int rc2 = staged_upload(c, B, [&](int b) { return (size_t)M[b] * N * 8; },
@@ -2340,9 +2479,6 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
         return rc2;
     CK(cudaMemcpyAsync(c->dM, M, (size_t)B * 4, cudaMemcpyHostToDevice, c->stream));
     if (c->has_truth) {
-        if (!reuse && ((rc = dalloc(&c->dx, (size_t)B * c->ldN * 8)) ||
-                       (rc = dalloc(&c->dxi, (size_t)B * c->ldN))))
-            return rc;
         std::vector<int8_t> xi8((size_t)B * c->ldN, 0);
         for (int b = 0; b < B; ++b) {
             CK(cudaMemcpyAsync(c->dx + (size_t)b * c->ldN, x_true[b], (size_t)N * 8,
