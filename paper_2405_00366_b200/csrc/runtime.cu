@@ -746,10 +746,10 @@ template <typename T, int NR, int MODE>
 int launch_gemv_t(cimcs_ctx* c, const GemvArgs& a) {
     auto kern = gemv_fused_kernel<T, NR, MODE>;
     constexpr size_t smem = gemv_smem_bytes<T, NR>();
-    static unsigned long long attr = 0;  // per device: the attribute is per context
-    if (!(attr >> c->device & 1ull)) {
+    static std::atomic<unsigned long long> attr{0};  // per device: the attribute is per context
+    if (!(attr.load() >> c->device & 1ull)) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr |= 1ull << c->device;
+        attr.fetch_or(1ull << c->device);
     }
     if (c->nRB == 0) return 0;  // this rank holds no rows
     dim3 grid(c->nRB, c->B);
@@ -823,10 +823,10 @@ int launch_tc_t(cimcs_ctx* c, const GemvArgs& g) {
     if (a.ntiles == 0) return 0;
     auto kern = tc_step_kernel<NR, MODE>;
     constexpr size_t smem = tc_smem_bytes(NR);
-    static unsigned long long attr = 0;  // per device: the attribute is per context
-    if (!(attr >> c->device & 1ull)) {
+    static std::atomic<unsigned long long> attr{0};  // per device: the attribute is per context
+    if (!(attr.load() >> c->device & 1ull)) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr |= 1ull << c->device;
+        attr.fetch_or(1ull << c->device);
     }
     const int grid = std::min(a.ntiles, c->num_sms);
     kern<<<grid, kTcThreads, smem, c->stream>>>(a);
@@ -859,10 +859,10 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb, cudaStream_t s
     sa.sched = ss->sched;
     auto kern = sym_step_kernel<NR, MODE>;
     constexpr size_t smem = sy_smem_bytes<NR>();
-    static unsigned long long attr = 0;  // per device: the attribute is per context
-    if (!(attr >> c->device & 1ull)) {
+    static std::atomic<unsigned long long> attr{0};  // per device: the attribute is per context
+    if (!(attr.load() >> c->device & 1ull)) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr |= 1ull << c->device;
+        attr.fetch_or(1ull << c->device);
     }
     // same stream: both kernels use programmatic dependent launch (the next
     // kernel's prologue overlaps this one's tail; griddepcontrol.wait orders data)
@@ -934,10 +934,10 @@ int launch_fac_t(cimcs_ctx* c, const GemvArgs& g) {
     f.W2 = c->fac_w2;
     auto kern = fac_step_kernel<NR, MODE>;
     constexpr size_t smem = fa_smem_bytes<NR>();
-    static unsigned long long attr = 0;
-    if (!(attr >> c->device & 1ull)) {
+    static std::atomic<unsigned long long> attr{0};
+    if (!(attr.load() >> c->device & 1ull)) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr |= 1ull << c->device;
+        attr.fetch_or(1ull << c->device);
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(std::min(f.ntask, c->num_sms));
@@ -1335,11 +1335,11 @@ template <typename T, int NR, int MODE>
 int launch_cluster_t(cimcs_ctx* c, GemvArgs a, int n_iters) {
     auto kern = cluster_loop_kernel<T, NR, MODE>;
     constexpr size_t smem = cluster_smem_bytes<T, NR>();
-    static unsigned long long attr = 0;  // per device: the attribute is per context
-    if (!(attr >> c->device & 1ull)) {
+    static std::atomic<unsigned long long> attr{0};  // per device: the attribute is per context
+    if (!(attr.load() >> c->device & 1ull)) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr |= 1ull << c->device;
+        attr.fetch_or(1ull << c->device);
     }
     a.tc_in = wcanon(c);
     const unsigned cs = (unsigned)((c->N + kClRows - 1) / kClRows);
@@ -2636,13 +2636,13 @@ int cimcs_set_mri_problem(cimcs_ctx* c, int32_t H, int32_t W, const double* targ
     CK(cudaMemcpy(c->dMaskBr, br.data(), br.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->dTw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->dTarget, tgt.data(), tgt.size() * 4, cudaMemcpyHostToDevice));
-    static unsigned long long attr = 0;
-    if (!(attr >> c->device & 1ull)) {
+    static std::atomic<unsigned long long> attr{0};
+    if (!(attr.load() >> c->device & 1ull)) {
         CK(cudaFuncSetAttribute(mri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)mri_smem_bytes(128, 128, 128)));
         CK(cudaFuncSetAttribute(mri_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)mri_cluster_smem_bytes(128, 128)));
-        attr |= 1ull << c->device;
+        attr.fetch_or(1ull << c->device);
     }
     if (c->has_truth) {  // make_problem(t, &truth): xi = (x != 0) (mri.cpp:398-405)
         if ((rc = dalloc(&c->dx, (size_t)c->ldN * 8)) || (rc = dalloc(&c->dxi, (size_t)c->ldN)))
