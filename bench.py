@@ -431,6 +431,28 @@ def run_ours(args, ws, rank, local):
         h2d += Bn * R * Nn * 8 * nalt  # host-drawn c0 streams
         d2h = r2["R"].nbytes + r2["sigma"].nbytes + r2["history"].nbytes
 
+    # the dominant kernel alone: a short eager run with CUDA events around every
+    # step-mode launch of the tile kernel on its stream (outside the timed region;
+    # the step-level roofline above is the in-region figure)
+    dom = None
+    if args.dtype == "f32" and not (Nn <= 512) and not tile_sharded:
+        ctx.set_option("use_graphs", 0)
+        ctx.set_option("kernel_timing", 1)
+        ctx.solve(R, "mfz-bn", P.baseline_params(velo=1, n_steps=100), seeds)
+        tk = ctx.timing()
+        ctx.set_option("kernel_timing", 0)
+        ctx.set_option("use_graphs", 1)
+        if tk["tile_kernel_launches"] > 0:
+            t_tile = tk["tile_kernel_ms"] / tk["tile_kernel_launches"] * 1e-3
+            dom = {"kernel": f"sym_step_kernel<{ctx_nr(R, args.dtype)},BN>",
+                   "avg_us": t_tile * 1e6, "launches": int(tk["tile_kernel_launches"]),
+                   "bytes_per_launch": step_bytes, "achieved": step_bytes / t_tile / 1e9,
+                   "peak": peak, "unit": "GB/s", "frac": step_bytes / t_tile / 1e9 / peak,
+                   "share_of_step": t_tile / step_s,
+                   "how": ("eager run of 2 x 100 steps after the timed region, CUDA events on "
+                           "the launch stream around each launch (serialised: the kernel "
+                           "timed alone, burst peak)")}
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu and not device_gen:
         nthreads = os.cpu_count() or 1
@@ -498,6 +520,7 @@ def run_ours(args, ws, rank, local):
                                           if args.config == 1 and args.dtype == "f32" else None),
                          "kernel": kernel_label(Nn, ctx_nr(R, args.dtype), args.dtype),
                          "bytes_per_launch": step_bytes, "peak_kind": peak_kind,
+                         "dominant_kernel": dom,
                          "dense_equivalent": {"bytes_per_launch": dense_bytes,
                                               "achieved": dense_bytes / step_s / 1e9}},
             "e2e": None if e2e_val is None else {

@@ -69,6 +69,8 @@ typedef struct cimcs_timing {
     int64_t step_launches, refit_launches, other_launches;
     double step_bytes;    /* algorithmic bytes of one step launch (G share, dense) */
     double step_flops;    /* algorithmic flops of one step launch (2 N^2 R B) */
+    double tile_kernel_ms;        /* option "kernel_timing" (eager launches only): summed  */
+    int64_t tile_kernel_launches; /*   CUDA-event time of the step-mode tile-kernel launches */
 } cimcs_timing;
 
 typedef struct cimcs_ctx cimcs_ctx;

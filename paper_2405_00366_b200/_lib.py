@@ -59,6 +59,7 @@ class Timing(C.Structure):
         ("refit_ms", C.c_double), ("score_ms", C.c_double), ("h2d_ms", C.c_double),
         ("d2h_ms", C.c_double), ("step_launches", C.c_int64), ("refit_launches", C.c_int64),
         ("other_launches", C.c_int64), ("step_bytes", C.c_double), ("step_flops", C.c_double),
+        ("tile_kernel_ms", C.c_double), ("tile_kernel_launches", C.c_int64),
     ]
 
 

@@ -334,6 +334,8 @@ struct cimcs_ctx {
     float* dSpart = nullptr;  // partial products [B][nRB][nSB][128][NR]
     int sym_groups = 0;       // instance groups pipelined across two streams (0: auto)
     bool use_pdl = true;      // programmatic dependent launch between the step kernels
+    bool kernel_timing = false;  // eager mode: CUDA events around each step-mode tile kernel
+    cudaEvent_t kt_ev[2] = {nullptr, nullptr};
     // tile sharding of the symmetric path (cimcs_create_sharded contexts, option
     // "tile_shard", default on): every rank keeps the full state and streams only
     // the gram tiles of its super-rows [sP0, sP1); the per-rank slot sums are
@@ -877,7 +879,26 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb, cudaStream_t s
     cfg.stream = sA;
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    const bool timed = c->kernel_timing && (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) &&
+                       cudaStreamIsCapturing(sA, &cap) == cudaSuccess &&
+                       cap == cudaStreamCaptureStatusNone;
+    if (timed) {
+        if (!c->kt_ev[0]) {
+            CK(cudaEventCreate(&c->kt_ev[0]));
+            CK(cudaEventCreate(&c->kt_ev[1]));
+        }
+        CK(cudaEventRecord(c->kt_ev[0], sA));
+    }
     CK(cudaLaunchKernelEx(&cfg, kern, sa));
+    if (timed) {  // the kernel alone, on its own stream (serialises the step: a measurement mode)
+        CK(cudaEventRecord(c->kt_ev[1], sA));
+        CK(cudaEventSynchronize(c->kt_ev[1]));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->kt_ev[0], c->kt_ev[1]));
+        c->timing.tile_kernel_ms += ms;
+        c->timing.tile_kernel_launches += 1;
+    }
     if (sF != sA) {
         CK(cudaEventRecord(evA, sA));
         CK(cudaStreamWaitEvent(sF, evA, 0));
@@ -2222,7 +2243,12 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
     if (k == "host_threads") c->host_threads = (int)std::max<int64_t>(1, v);
     else if (k == "use_graphs") c->use_graphs = v != 0;
     else if (k == "gram_blas") c->gram_blas = v > 0 ? 1 : (v < 0 ? -1 : 0);
-    else if (k == "tile_shard") {
+    else if (k == "kernel_timing") {
+        c->kernel_timing = v != 0;
+        c->timing.tile_kernel_ms = 0.0;
+        c->timing.tile_kernel_launches = 0;
+        drop_graphs(c);
+    } else if (k == "tile_shard") {
         if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set tile_shard before set_problems");
         c->tshard_opt = v != 0 ? 1 : 0;
     } else if (k == "mri_cluster") {
