@@ -288,8 +288,10 @@ def run_reference(args, ws, rank):
 
 
 def run_ours(args, ws, rank, local):
-    import torch
     import paper_2405_00366_b200 as P
+    from paper_2405_00366_b200 import _lib
+    _lib.load()  # before torch: the system cuBLAS 12.9 (fp32-emulated gram GEMMs) wins
+    import torch
 
     torch.cuda.set_device(local)
     dist = None

@@ -8,6 +8,7 @@
 // thread pool from each trajectory's std::mt19937_64 stream while the GPU
 // runs the current one.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 #include <cublas_v2.h>
 
@@ -356,6 +357,10 @@ struct cimcs_ctx {
     __half* UB = nullptr;     // fp16 B tiles of u = A w [B][nMB][2NR x 128]
     int* US = nullptr;
     int gram_blas = 0;        // symmetric gram from cuBLAS DGEMM panels: 0 auto (N >= 8192), 1, -1
+    int gram_emu = -1;        // ... as fp32-emulated (BF16x9) GEMMs on the tensor cores:
+                              // -1 auto (N >= 32768: 14.0 -> 5.0 s at config 4; slower
+                              // than DGEMM at config 3's N = 16384), 1 on, 0 off
+    bool timing_gram_emu = false;  // the last build used them
     // matrix-free MRI transform-chain problem (mri_kernels.cuh; mri.hpp:46-99)
     bool mri = false;
     int mH = 0, mW = 0, mL = 0;
@@ -999,6 +1004,12 @@ int launch_tc_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
         case EPI_MATVEC: return launch_tc_t<NR, EPI_MATVEC>(c, a);
         default: return launch_tc_t<NR, EPI_SCORE>(c, a);
     }
+}
+
+__global__ void f64_to_f32_kernel(const double* __restrict__ a, float* __restrict__ o, size_t n) {
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
+         t += (size_t)gridDim.x * blockDim.x)
+        o[t] = (float)a[t];
 }
 
 // one mri_kernel launch of `grid` CTAs (basis vectors r0.. for DIAG / COLS)
@@ -2243,6 +2254,7 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
     if (k == "host_threads") c->host_threads = (int)std::max<int64_t>(1, v);
     else if (k == "use_graphs") c->use_graphs = v != 0;
     else if (k == "gram_blas") c->gram_blas = v > 0 ? 1 : (v < 0 ? -1 : 0);
+    else if (k == "gram_emu") c->gram_emu = v > 0 ? 1 : (v < 0 ? -1 : 0);
     else if (k == "kernel_timing") {
         c->kernel_timing = v != 0;
         c->timing.tile_kernel_ms = 0.0;
@@ -2774,13 +2786,34 @@ int cimcs_build_coupling(cimcs_ctx* c) {
         }
         cublasSetStream(c->blas, c->stream);
         const int PB = 8, ldp = PB * kSyT;
-        double* P = nullptr;
-        if ((rc = dalloc(&P, (size_t)ldp * c->N * 8))) return rc;
-        std::unique_ptr<double, decltype(&cudaFree)> pguard(P, &cudaFree);
+        // the tiles hold ~22 bits (fp16 hi/lo): an fp32-accurate GEMM suffices, run as
+        // cuBLAS's BF16x9 fp32 emulation on the tensor cores (option "gram_emu", default
+        // on) instead of fp64 DGEMM on the CUDA cores
+        // (cuBLAS >= 12.9: when an older libcublas.so.12 was loaded first -- e.g. by
+        // torch -- the emulation entry point is absent and the fp64 DGEMM runs)
+        using SetEmu = cublasStatus_t (*)(cublasHandle_t, cublasEmulationStrategy_t);
+        static SetEmu set_emu =
+            reinterpret_cast<SetEmu>(dlsym(RTLD_DEFAULT, "cublasSetEmulationStrategy"));
+        bool emu = (c->gram_emu > 0 || (c->gram_emu < 0 && c->N >= 32768)) && set_emu != nullptr;
+        void* Pv = nullptr;  // sized for fp64 panels: the DGEMM route may take over mid-build
+        if ((rc = dalloc(reinterpret_cast<char**>(&Pv), (size_t)ldp * c->N * 8))) return rc;
+        std::unique_ptr<void, decltype(&cudaFree)> pguard(Pv, &cudaFree);
+        float* A32 = nullptr;
+        if (emu && (rc = dalloc(&A32, (size_t)c->Mmax * c->N * 4))) return rc;
+        c->timing_gram_emu = emu;
+        std::unique_ptr<float, decltype(&cudaFree)> aguard(A32, &cudaFree);
+        if (emu && set_emu(c->blas, CUBLAS_EMULATION_STRATEGY_EAGER) != CUBLAS_STATUS_SUCCESS)
+            emu = false;
         const double one = 1.0, zero = 0.0;
+        const float onef = 1.f, zerof = 0.f;
         for (int b = 0; b < c->B; ++b) {
             const int M = c->M[b];
             const double* Ab = c->dA + (size_t)b * astride;
+            if (emu && A32) {
+                const size_t n = (size_t)M * c->N;
+                f64_to_f32_kernel<<<8 * c->num_sms, 256, 0, c->stream>>>(Ab, A32, n);
+                CK(cudaGetLastError());
+            }
             SymOut o{static_cast<__half*>(c->dG), c->dSg, c->nRB, c->ntri};
             // tile-sharded: only the row blocks of this rank's super-rows
             const int Ib = c->tshard ? c->sP0 * kSyS : 0;
@@ -2788,12 +2821,23 @@ int cimcs_build_coupling(cimcs_ctx* c) {
             for (int I0 = Ib; I0 < Ie; I0 += PB) {
                 const int nI = std::min(PB, Ie - I0), i0 = I0 * kSyT;
                 const int rows = std::min(nI * kSyT, c->N - i0), ncols = c->N - i0;
-                if (cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, rows, ncols, M, &one,
-                                Ab + (size_t)i0 * M, M, Ab + (size_t)i0 * M, M, &zero, P,
-                                ldp) != CUBLAS_STATUS_SUCCESS)
-                    return fail(CIMCS_CUDA_ERROR, "cublasDgemm failed");
-                sym_panel_kernel<<<4 * c->num_sms, 256, 0, c->stream>>>(P, ldp, I0, nI, ncols,
-                                                                       c->N, o, b);
+                if (emu && cublasGemmEx(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, rows, ncols, M, &onef,
+                                        A32 + (size_t)i0 * M, CUDA_R_32F, M, A32 + (size_t)i0 * M,
+                                        CUDA_R_32F, M, &zerof, Pv, CUDA_R_32F, ldp,
+                                        CUBLAS_COMPUTE_32F_EMULATED_16BFX9,
+                                        CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
+                    emu = false;  // not supported by the loaded cuBLAS: fp64 DGEMM from here
+                if (emu) {
+                    sym_panel_kernel<float><<<4 * c->num_sms, 256, 0, c->stream>>>(
+                        static_cast<const float*>(Pv), ldp, I0, nI, ncols, c->N, o, b);
+                } else {
+                    if (cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, rows, ncols, M, &one,
+                                    Ab + (size_t)i0 * M, M, Ab + (size_t)i0 * M, M, &zero,
+                                    static_cast<double*>(Pv), ldp) != CUBLAS_STATUS_SUCCESS)
+                        return fail(CIMCS_CUDA_ERROR, "cublasDgemm failed");
+                    sym_panel_kernel<double><<<4 * c->num_sms, 256, 0, c->stream>>>(
+                        static_cast<const double*>(Pv), ldp, I0, nI, ncols, c->N, o, b);
+                }
                 CK(cudaGetLastError());
             }
         }

@@ -105,7 +105,8 @@ __device__ __forceinline__ float sy_pow2(int e) { return __int_as_float((127 + e
 // Gram panel from a library GEMM (large N, fp32 contexts): P[il][jc] (column-major,
 // ld = ldp) = G[i0 + il][i0 + jc] for the rows of nI row blocks starting at block I0;
 // the upper-triangle tiles are written as SymOut does.
-__global__ void sym_panel_kernel(const double* __restrict__ P, int ldp, int I0, int nI, int ncols,
+template <typename PT>
+__global__ void sym_panel_kernel(const PT* __restrict__ P, int ldp, int I0, int nI, int ncols,
                                  int N, SymOut o, int b) {
     const int i0 = I0 * kSyT;
     const size_t total = (size_t)nI * kSyT * ncols;
@@ -115,7 +116,7 @@ __global__ void sym_panel_kernel(const double* __restrict__ P, int ldp, int I0, 
         const int jc = (int)(t / (nI * kSyT));
         const int i = i0 + il, j = i0 + jc;
         if (i >= N || j >= N || j / kSyT < i / kSyT) continue;
-        o.store(b, i, j, P[(size_t)jc * ldp + il]);
+        o.store(b, i, j, (double)P[(size_t)jc * ldp + il]);
     }
 }
 

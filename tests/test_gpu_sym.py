@@ -140,11 +140,13 @@ def test_sym_instance_groups_bitwise(gpu, O):
     assert np.array_equal(outs[0]["sigma"], outs[1]["sigma"])
 
 
-def test_sym_gram_from_cublas_panels(gpu, O):
-    """gram_blas=1: the symmetric tiles built from cuBLAS DGEMM panels (the large-N
-    route, config 4) match the oracle gram and drive the same local field."""
+@pytest.mark.parametrize("emu", [1, 0])
+def test_sym_gram_from_cublas_panels(gpu, O, emu):
+    """gram_blas=1: the symmetric tiles built from cuBLAS panels (the large-N route,
+    configs 3/4) -- fp32-emulated BF16x9 tensor-core GEMMs (default) or fp64 DGEMM --
+    match the oracle gram and drive the same local field."""
     insts = [O.gen_instance(1100, 0.5, 0.1, 0.01, 21), O.gen_instance(1100, 0.6, 0.1, 0.01, 22)]
-    ctx = _ctx(gpu, insts, gram_blas=1)
+    ctx = _ctx(gpu, insts, gram_blas=1, gram_emu=emu)
     for b, inst in enumerate(insts):
         G, hz, D = ctx.get_coupling(b)
         ref = O.Problem(inst, O.CANON).G
