@@ -407,6 +407,10 @@ __global__ void __launch_bounds__(kMriCThreads, 1) mri_cluster_kernel(MriArgs a)
     }
     for (int t = threadIdx.x; t < 64; t += blockDim.x) tw[t] = a.tw[t];
     cl.sync();  // every CTA's barriers are armed before any peer stores into it
+    // programmatic dependent launch: the update kernel may be scheduled now; this
+    // grid's reads of w wait for the previous step's update kernel
+    sy_pdl_trigger();
+    sy_pdl_wait();
     // 1. low-pass quadrant (redundant), levels 2.. of the inverse
     for (int t = threadIdx.x; t < H2 * W2; t += blockDim.x) {
         const int i = t >> lW2, j = t & (W2 - 1);

@@ -1057,13 +1057,15 @@ int launch_mri_t(cimcs_ctx* c, const GemvArgs& g) {
         cfg.blockDim = dim3(kMriCThreads);
         cfg.dynamicSmemBytes = mri_cluster_smem_bytes(c->mH, c->mW);
         cfg.stream = c->stream;
-        cudaLaunchAttribute at[1];
+        cudaLaunchAttribute at[2];
         at[0].id = cudaLaunchAttributeClusterDimension;
         at[0].val.clusterDim.x = CS;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = c->use_pdl ? 2 : 1;
         CK(cudaLaunchKernelEx(&cfg, mri_cluster_kernel, ma));
     } else {
         const size_t smem = mri_smem_bytes(c->mH, c->mW, c->mL);
@@ -1076,7 +1078,18 @@ int launch_mri_t(cimcs_ctx* c, const GemvArgs& g) {
     sa.nSB = 1;
     sa.b0 = 0;
     sa.keep_w = 1;  // the next apply reads the fp32 w
-    sym_update_kernel<NR, MODE><<<dim3(c->nRB, 1), kSyT * NR / 4, 0, c->stream>>>(sa);
+    {
+        cudaLaunchConfig_t ucfg{};
+        ucfg.gridDim = dim3(c->nRB, 1);
+        ucfg.blockDim = dim3(kSyT * NR / 4);
+        ucfg.stream = c->stream;
+        cudaLaunchAttribute ua[1];
+        ua[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        ua[0].val.programmaticStreamSerializationAllowed = 1;
+        ucfg.attrs = ua;
+        ucfg.numAttrs = c->use_pdl ? 1 : 0;
+        CK(cudaLaunchKernelEx(&ucfg, sym_update_kernel<NR, MODE>, sa));
+    }
     CK(cudaGetLastError());
     return 0;
 }
