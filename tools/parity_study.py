@@ -12,9 +12,10 @@ import numpy as np
 import paper_2405_00366_b200 as P
 from paper_2405_00366_b200 import workloads as W
 
-insts, R, hp, _ = W.config1()
-seeds = P.replica_seeds(insts, R, "mfz-bn")
 variant = sys.argv[1] if len(sys.argv) > 1 else "sym"  # sym | stream | cudacore
+cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 1     # BASELINE config 1 or 2
+insts, R, hp, _ = W.config1() if cfg == 1 else W.config2()
+seeds = P.replica_seeds(insts, R, "mfz-bn")
 out = {}
 for dt in ("f64", "f32"):
     with P.Context(0, dt) as ctx:
@@ -46,7 +47,7 @@ def quality(r):
     return {"rmse_mean": float(rm.mean()), "rmse_median": float(np.median(rm)),
             "exact_support_fraction": float((ham == 0).mean()),
             "hamming_mean": float(ham.mean())}
-line = {"workload": "BASELINE config 1 (64 x 16, N=2000, 20 x 1000 steps)", "fp32_variant": variant,
+line = {"workload": (f"BASELINE config {cfg} ({B} x {R}, N=2000, 20 x 1000 steps)"), "fp32_variant": variant,
         "quality_vs_truth": {"f64": quality(a), "f32": quality(b)},
         "trajectories": int(B * R), "failed": int(fail.sum()),
         "support_identical_trajectories": float(same.mean()),
