@@ -311,34 +311,52 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
     const uint32_t tmem = s_tmem;
     // programmatic dependent launch: the update kernel may be scheduled now (its
     // CTAs wait for this grid in griddepcontrol.wait); this grid's own reads of
-    // w and writes of the partial products wait for the previous update kernel
+    // w and writes of the partial products wait for the previous update kernel.
+    // In the step modes the producer thread waits later: every CIM call starts
+    // with a plain (non-PDL) launch issued after the gram was built, and nothing
+    // writes the gram tiles during the call, so the planes of the first stages
+    // are copied while the previous update kernel finishes.
+    constexpr bool kEarly = MODE == EPI_STEP_BN || MODE == EPI_STEP_CN;
     sy_pdl_trigger();
-    sy_pdl_wait();
+    if (!kEarly || threadIdx.x != 0) sy_pdl_wait();
 
     if (warp == 0) {
         // ------------------------------------------------------ producer
         if (lane == 0) {
             const uint64_t pG = sy_policy_first(), pW = sy_policy_last();
+            // stage s of tile tt: expect its bytes, copy the two gram planes
+            auto g_part = [&](int s, int b, int I, int J) {
+                const __half* src = sa.Gs + (size_t)b * sa.ntri * 2 * kSyPlaneHalfs +
+                                    (size_t)sy_tri(I, J, nRB) * 2 * kSyPlaneHalfs;
+                unsigned char* st = smem + s * kStage;
+                mbar_arrive_expect_tx(&full[s], 2 * kSyPlaneBytes + (I != J ? 2 : 1) * kBB);
+                // the gram streams through L2 once per step; w tiles are re-read
+                sy_bulk_g2s(st, src, kSyPlaneBytes, &full[s], pG);
+                sy_bulk_g2s(st + kSyPlaneBytes, src + kSyPlaneHalfs, kSyPlaneBytes, &full[s], pG);
+            };
             int tt = 0;
+            for (int k = it0; k < it1 && tt < kSyStages; ++k) {
+                const SyItem m = sy_item(sa, k, nRB);
+                for (int ii = 0; ii < m.nI && tt < kSyStages; ++ii)
+                    for (int jj = m.diag ? ii : 0; jj < m.nJ && tt < kSyStages; ++jj, ++tt)
+                        g_part(tt, m.b, m.I0 + ii, m.J0 + jj);
+            }
+            if (kEarly) sy_pdl_wait();
+            tt = 0;
             for (int k = it0; k < it1; ++k) {
                 const SyItem m = sy_item(sa, k, nRB);
                 const __half* wb = sa.WBin + (size_t)m.b * nRB * (2 * NR * kSyT);
-                const __half* gb = sa.Gs + (size_t)m.b * sa.ntri * 2 * kSyPlaneHalfs;
                 for (int ii = 0; ii < m.nI; ++ii)
                     for (int jj = m.diag ? ii : 0; jj < m.nJ; ++jj, ++tt) {
                         const int I = m.I0 + ii, J = m.J0 + jj, s = tt % kSyStages;
-                        if (tt >= kSyStages) mbar_wait(&empty[s], ((tt / kSyStages) - 1) & 1);
-                        const __half* src = gb + (size_t)sy_tri(I, J, nRB) * 2 * kSyPlaneHalfs;
+                        if (tt >= kSyStages) {
+                            mbar_wait(&empty[s], ((tt / kSyStages) - 1) & 1);
+                            g_part(s, m.b, I, J);
+                        }
                         unsigned char* st = smem + s * kStage;
-                        const bool off = I != J;
-                        mbar_arrive_expect_tx(&full[s], 2 * kSyPlaneBytes + (off ? 2 : 1) * kBB);
-                        // the gram streams through L2 once per step; w tiles are re-read
-                        sy_bulk_g2s(st, src, kSyPlaneBytes, &full[s], pG);
-                        sy_bulk_g2s(st + kSyPlaneBytes, src + kSyPlaneHalfs, kSyPlaneBytes,
-                                    &full[s], pG);
                         sy_bulk_g2s(st + 2 * kSyPlaneBytes, wb + (size_t)J * (2 * NR * kSyT), kBB,
                                     &full[s], pW);
-                        if (off)
+                        if (I != J)
                             sy_bulk_g2s(st + 2 * kSyPlaneBytes + kBB,
                                         wb + (size_t)I * (2 * NR * kSyT), kBB, &full[s], pW);
                     }
