@@ -35,6 +35,9 @@ KEYS = [
 ]
 
 
+STEP = ("sym_step_kernel", "sym_update_kernel", "mri_cluster_kernel")
+
+
 def main(rep, name, note=""):
     rows, units = raw(rep)
     out = []
@@ -52,8 +55,11 @@ def main(rep, name, note=""):
         e["units"] = {k: units.get(k) for k in KEYS if k in units}
         out.append(e)
     summary = {"report": rep, "note": note, "kernels": out}
-    if out:  # one step = every kernel captured (the symmetric path launches three)
-        vals = [k.get("dram_bytes_per_launch") for k in out]
+    if out:  # one step = the step kernels captured (setup kernels such as the gram
+        # scale / w conversion launched once per call are listed but not counted)
+        step = [k for k in out if any(s in (k.get("Kernel Name") or "") for s in STEP)] or out
+        vals = [k.get("dram_bytes_per_launch") for k in step]
+        summary["step_kernels"] = [k.get("Kernel Name") for k in step]
         summary["dram_bytes_per_launch"] = sum(v for v in vals if v) if all(vals) else vals[0]
     with open(f"profiles/{name}.json", "w") as f:
         json.dump(summary, f, indent=1)
