@@ -520,7 +520,13 @@ int dalloc(P** p, size_t bytes) {
     cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(bytes, 16));
     if (e != cudaSuccess)
         return fail(CIMCS_CUDA_ERROR, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-    cudaMemset(*p, 0, std::max<size_t>(bytes, 16));
+    // the zero fill runs on the legacy stream, which does not order against the
+    // context's non-blocking stream: finish it before any upload can land (a
+    // second context's 39 GB fill used to overwrite freshly uploaded instances)
+    e = cudaMemset(*p, 0, std::max<size_t>(bytes, 16));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess)
+        return fail(CIMCS_CUDA_ERROR, std::string("cudaMemset: ") + cudaGetErrorString(e));
     return 0;
 }
 
@@ -687,7 +693,7 @@ int ensure_state(cimcs_ctx* c, int NR) {
             c->spart_elems = ne;
         }
         if (c->tshard) {  // slots of other ranks' items stay zero for good
-            CK(cudaMemset(c->dSpart, 0, ne * 4));
+            CK(cudaMemsetAsync(c->dSpart, 0, ne * 4, c->stream));
             if (c->dH) cudaFree(c->dH);
             c->dH = nullptr;
             if ((rc = dalloc(&c->dH, (size_t)c->B * c->nRB * kSyT * NR * 4))) return rc;
@@ -2494,6 +2500,7 @@ int cimcs_set_generated_problems(cimcs_ctx* c, int32_t B, int32_t N, const doubl
 int cimcs_get_instance(cimcs_ctx* c, int32_t b, double* A, double* y, double* x_true,
                        int32_t* xi_true) {
     if (!c || b < 0 || b >= c->B || c->mri || !c->dA) return fail(CIMCS_INPUT_ERROR, "bad instance");
+    CK(cudaStreamSynchronize(c->stream));  // cudaMemcpy does not order against c->stream
     const int N = c->N, M = c->M[b];
     const size_t astride = (size_t)c->Mmax * N;
     if (A) CK(cudaMemcpy(A, c->dA + (size_t)b * astride, (size_t)M * N * 8, cudaMemcpyDeviceToHost));
@@ -2757,7 +2764,7 @@ int cimcs_build_coupling(cimcs_ctx* c) {
         if ((rc = dalloc(&c->dTask, tab.size() * 4))) return rc;
         CK(cudaMemcpy(c->dTask, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
         if (!c->dCnt && (rc = dalloc(&c->dCnt, (size_t)c->B * 2 * 4))) return rc;
-        CK(cudaMemset(c->dCnt, 0, (size_t)c->B * 2 * 4));
+        CK(cudaMemsetAsync(c->dCnt, 0, (size_t)c->B * 2 * 4, c->stream));
     }
     Events ev(2);
     cudaEventRecord(ev.ev[0], c->stream);

@@ -210,3 +210,30 @@ def test_sym_phase_grid_mixed_M_matches_fp64(gpu, O):
             rel.append(abs(g - ref["final_rmse"]) / max(ref["final_rmse"], 1e-12))
     assert same >= 0.9 * len(insts) * R, same
     assert np.mean(rel) <= 5e-2, np.mean(rel)
+
+
+def test_two_live_contexts_load_identically(gpu):
+    """Regression (r01h): a second live context's zero fill of its instance
+    buffer ran on the legacy stream and could land after the uploads on the
+    context's non-blocking stream (bench e2e at config 2: 1212 of 1344
+    instances read back with diag(G) = 0).  Every context must see its own
+    upload: mixed-M instances, diag and hz bitwise equal across contexts."""
+    insts = [gpu.gen_instance(2000, alpha, 0.1, 0.01, s)
+             for s, alpha in enumerate((0.3, 0.9, 0.6, 0.9) * 16, start=1)]
+    ctxs = []
+    try:
+        for _ in range(3):
+            c = gpu.Context(0, "f32")
+            c.set_problems(insts)
+            c.build_coupling()
+            ctxs.append(c)
+        for b in (0, 1, 37, 63):
+            ref = insts[b].A
+            d_host = (np.asarray(ref) ** 2).sum(axis=0)
+            outs = [c.get_coupling(b, gram=False) for c in ctxs]
+            for _, hz, D in outs:
+                assert np.max(np.abs(D - d_host)) <= 1e-5 * np.max(d_host)
+                assert np.array_equal(hz, outs[0][1]) and np.array_equal(D, outs[0][2])
+    finally:
+        for c in ctxs:
+            c.close()
