@@ -2001,6 +2001,10 @@ int run_pp_cim(cimcs_ctx* c, int Rreal, const StepScalars& s, const cimcs_hyper*
             rc = stage(ch + 2);
         }
     }
+    // the next call refills both pinned slots at once: the copies still queued
+    // behind this call's kernels must have read them first
+    CK(cudaEventSynchronize(cp.ev[0]));
+    CK(cudaEventSynchronize(cp.ev[1]));
     return rc;
 }
 
