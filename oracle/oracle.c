@@ -530,6 +530,13 @@ int orc_run_pp(const orc_problem* p, const double* R, const orc_hyper* h, double
     return rc;
 }
 
+/* Precision-sensitivity knob (tools/precision_study.py only; 0 everywhere
+ * else): bit 1 rounds the local field to fp32 every step, bit 2 the state c, e
+ * after every step, bit 4 the refit R after every alternation.  It measures
+ * which fp32 quantity moves the fp64 answer; the reference has no such knob. */
+static int g_perturb = 0;
+void orc_set_perturb(int mode) { g_perturb = mode; }
+
 /* run_mfz solver_mfz.cpp:90-124 with init_mfz :24-31 */
 int orc_run_mfz(const orc_problem* p, const double* R, const orc_hyper* h, double eta,
                 int backend, orc_rng* rng, double* c_out, double* e_out, int32_t* sigma_out,
@@ -571,8 +578,15 @@ int orc_run_mfz(const orc_problem* p, const double* R, const orc_hyper* h, doubl
         } else {
             orc_local_field_cn(p, R, c, h->tau, hf);
         }
+        if (g_perturb & 1)
+            for (int r = 0; r < N; ++r) hf[r] = (double)(float)hf[r];
         rc = orc_mfz_step(N, c, e, pp, h, eta, R, hf, c2, e2);
         if (rc != -1) break;
+        if (g_perturb & 2)
+            for (int r = 0; r < N; ++r) {
+                c2[r] = (double)(float)c2[r];
+                e2[r] = (double)(float)e2[r];
+            }
         double* tmp = c;
         c = c2;
         c2 = tmp;
@@ -898,6 +912,8 @@ static int alternating_impl(const orc_problem* p, int backend, const orc_hyper* 
             break;
         }
         memcpy(R, Rn, sizeof(double) * (size_t)N);
+        if (g_perturb & 4)
+            for (int r = 0; r < N; ++r) R[r] = (double)(float)R[r];
         orc_record* rec = &hist[nh];
         rec->i = i;
         rec->eta = eta;

@@ -144,6 +144,7 @@ int orc_run_pp(const orc_problem* p, const double* R, const orc_hyper* h, double
 
 /* One CIM call (run_mfz).  c0 drawn from rng.  trace_* optional (NULL).
  * Returns -1 ok, >=0 offending spin index, -2 input_error, -3 config_error. */
+void orc_set_perturb(int mode); /* sensitivity study knob, see oracle.c */
 int orc_run_mfz(const orc_problem* p, const double* R, const orc_hyper* h, double eta,
                 int backend, orc_rng* rng, double* c_out, double* e_out,
                 int32_t* sigma_out, double* min_e, int trace_mode, int* trace_count,

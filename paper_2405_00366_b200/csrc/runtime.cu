@@ -335,6 +335,7 @@ struct cimcs_ctx {
     float* dSpart = nullptr;  // partial products [B][nRB][nSB][128][NR]
     int sym_groups = 0;       // instance groups pipelined across two streams (0: auto)
     bool use_pdl = true;      // programmatic dependent launch between the step kernels
+    int gram_l2 = 0;          // gram tiles copied with evict_last (L2 time-blocking experiment)
     bool kernel_timing = false;  // eager mode: CUDA events around each step-mode tile kernel
     cudaEvent_t kt_ev[2] = {nullptr, nullptr};
     // tile sharding of the symmetric path (cimcs_create_sharded contexts, option
@@ -865,6 +866,7 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb, cudaStream_t s
     sa.ntri = c->ntri;
     sa.nSB = c->nSB;
     sa.b0 = b0;
+    sa.gram_keep = c->gram_l2;
     if (nb == 0 || c->ntri == 0) return 0;
     const cimcs_ctx::SymSched* ss = nullptr;
     if (int rc = sym_schedule(c, nb, &ss)) return rc;
@@ -2288,6 +2290,9 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
         c->tshard_opt = v != 0 ? 1 : 0;
     } else if (k == "mri_cluster") {
         c->mri_cluster = v != 0;
+        drop_graphs(c);
+    } else if (k == "gram_l2") {
+        c->gram_l2 = v != 0;
         drop_graphs(c);
     } else if (k == "pdl") {
         c->use_pdl = v != 0;

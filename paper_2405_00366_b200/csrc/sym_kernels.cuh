@@ -193,6 +193,7 @@ struct SymArgs {
     int ntri, nSB;         // tiles per instance, super-blocks per row
     int b0;                // first instance of this launch (instance groups)
     int keep_w;            // step modes: also store the fp32 w (a consumer reads it)
+    int gram_keep;         // 1: gram tiles copied with evict_last (L2-resident groups)
 };
 
 template <int NR>
@@ -323,7 +324,8 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
     if (warp == 0) {
         // ------------------------------------------------------ producer
         if (lane == 0) {
-            const uint64_t pG = sy_policy_first(), pW = sy_policy_last();
+            const uint64_t pG = sa.gram_keep ? sy_policy_last() : sy_policy_first();
+            const uint64_t pW = sy_policy_last();
             // stage s of tile tt: expect its bytes, copy the two gram planes
             auto g_part = [&](int s, int b, int I, int J) {
                 const __half* src = sa.Gs + (size_t)b * sa.ntri * 2 * kSyPlaneHalfs +
