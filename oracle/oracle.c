@@ -532,7 +532,8 @@ int orc_run_pp(const orc_problem* p, const double* R, const orc_hyper* h, double
 
 /* Precision-sensitivity knob (tools/precision_study.py only; 0 everywhere
  * else): bit 1 rounds the local field to fp32 every step, bit 2 the state c, e
- * after every step, bit 4 the refit R after every alternation.  It measures
+ * after every step, bit 4 the refit R after every alternation, bits 8 / 16 add a
+ * uniform relative error of up to 2^-20 / 2^-16 to the field every step.  It measures
  * which fp32 quantity moves the fp64 answer; the reference has no such knob. */
 static int g_perturb = 0;
 void orc_set_perturb(int mode) { g_perturb = mode; }
@@ -580,6 +581,15 @@ int orc_run_mfz(const orc_problem* p, const double* R, const orc_hyper* h, doubl
         }
         if (g_perturb & 1)
             for (int r = 0; r < N; ++r) hf[r] = (double)(float)hf[r];
+        if (g_perturb & (8 | 16)) { /* relative field noise 2^-20 / 2^-16 (xorshift, per spin) */
+            const double amp = (g_perturb & 8) ? 0x1p-20 : 0x1p-16;
+            uint64_t x = 0x9E3779B97F4A7C15ull ^ (uint64_t)step;
+            for (int r = 0; r < N; ++r) {
+                x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+                const double u = (double)(x >> 11) * 0x1p-53 * 2.0 - 1.0;
+                hf[r] = hf[r] * (1.0 + amp * u);
+            }
+        }
         rc = orc_mfz_step(N, c, e, pp, h, eta, R, hf, c2, e2);
         if (rc != -1) break;
         if (g_perturb & 2)

@@ -138,8 +138,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
     constexpr uint32_t kSlice = kClRows * NR * sizeof(T);  // bytes pushed per CTA
     const uint32_t fill_bytes = (uint32_t)cs * (kSlice + NR * 4);
 
-    // ---- G slice -> registers (panels [B][nRB][ldJ][RB], or the tcgen05
-    // canonical tiles of an fp32 tensor-core context), column j of row i
+    // ---- G slice -> registers (panels [B][nRB][ldJ][RB]), column j of row i
     T gv[kClKG][kGran];
     {
         const T* G = static_cast<const T*>(a.G);
@@ -151,7 +150,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
                 const int j = (seg + kSeg * m) * kGran + jj;
                 T v = T(0);
                 if (row_ok && j < N)
-                    v = a.tc_in ? G[tc_gofs(nRB, nch, b, i, j)] : G[pan + (size_t)j * kRB];
+                    v = G[pan + (size_t)j * kRB];
                 gv[m][jj] = v;
             }
     }
@@ -161,8 +160,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
     __syncthreads();
     for (int k = threadIdx.x; k < N * NR; k += kClThreads) {
         const int j = k / NR, q = k % NR;
-        sW[WL::at(j, q)] =
-            a.tc_in ? Win[tc_wofs(a.ldJ, NR, b, j, q)] : Win[((size_t)b * ldN + j) * NR + q];
+        sW[WL::at(j, q)] = Win[((size_t)b * ldN + j) * NR + q];
     }
     for (int k = threadIdx.x; k < 2 * kClMaxCta * NR; k += kClThreads) sFlags[k] = 0;
     if constexpr (MODE != EPI_JACOBI) {
@@ -394,12 +392,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
             if (lmin[u] != T(INFINITY)) atomicMin(&a.minE[b * NR + q], ord_key(lmin[u]));
         }
         const T v = Wf[WL::at(i, q)];
-        if (a.tc_in) {
-            Wout[tc_wofs(a.ldJ, NR, b, i, q)] = v;
-            Wout[tc_wofs(a.ldJ, NR, b, i, NR + q)] = (T)((float)v - trunc_tf32((float)v));
-        } else {
-            Wout[vi] = v;
-        }
+        Wout[vi] = v;
     }
     cluster.sync();  // no CTA leaves while a peer may still address its shared memory
 }

@@ -111,7 +111,6 @@ struct GemvArgs {
     int step;            // step index inside the alternation
     int N, ldN, B, ldJ;
     int rb0;             // first (global) row block of this rank (row sharding)
-    int tc_in;           // cluster kernel: G / W in the tcgen05 layouts
     StepScalars s;
 };
 

@@ -33,7 +33,6 @@
 #include "cluster_kernels.cuh"
 #include "sym_kernels.cuh"
 #include "mri_kernels.cuh"
-#include "fac_kernels.cuh"
 
 using namespace cimcs;
 
@@ -320,9 +319,7 @@ struct cimcs_ctx {
     double* tp = nullptr;        // per-trajectory score partials [B*NR][5]
     int* fail_tmp = nullptr;     // local fail_gstep before the cross-rank MIN
     bool tc = false;      // active for the current problem set
-    bool want_sym = true;  // fp32 tensor-core contexts: symmetric-tile gram (sym_kernels.cuh)
     bool sym = false;      // active for the current problem set
-    bool sym_requested = true;
     int ntri = 0;          // upper-triangle tiles per instance
     int nSB = 0;           // super-block items per row of the tile triangle (kSyS tiles)
     struct SymSched {      // LPT placement of the items of nb instances on the CTAs
@@ -333,7 +330,6 @@ struct cimcs_ctx {
     std::vector<SymSched> ssched;
     int* dSg = nullptr;    // per-instance gram scale exponent
     float* dSpart = nullptr;  // partial products [B][nRB][nSB][128][NR]
-    int sym_groups = 0;       // instance groups pipelined across two streams (0: auto)
     bool use_pdl = true;      // programmatic dependent launch between the step kernels
     int gram_l2 = 0;          // gram tiles copied with evict_last (L2 time-blocking experiment)
     bool kernel_timing = false;  // eager mode: CUDA events around each step-mode tile kernel
@@ -348,15 +344,6 @@ struct cimcs_ctx {
     bool tshard = false;            // active for the current problem set
     int tworld = 1, trank = 0, sP0 = 0, sP1 = 0;
     float* dH = nullptr;            // [B][nRB][128][NR] summed partial products
-    // factored coupling A^T (A w) from fp16 hi/lo tiles of A (fac_kernels.cuh)
-    int fac_opt = -1;         // -1 auto, 0 off, 1 on (a symmetric-path variant)
-    int fac_requested = -1;
-    bool fac = false;
-    int nMB = 0, fac_w2 = 1, fac_skew = 10, ntask = 0;
-    int* dTask = nullptr;     // [ntask] task table (fa_task)
-    int* dCnt = nullptr;      // [2B] per-instance phase counters (self-resetting)
-    __half* UB = nullptr;     // fp16 B tiles of u = A w [B][nMB][2NR x 128]
-    int* US = nullptr;
     int gram_blas = 0;        // symmetric gram from cuBLAS DGEMM panels: 0 auto (N >= 8192), 1, -1
     int gram_emu = -1;        // ... as fp32-emulated (BF16x9) GEMMs on the tensor cores:
                               // -1 auto (N >= 32768: 14.0 -> 5.0 s at config 4; slower
@@ -371,8 +358,6 @@ struct cimcs_ctx {
     float* dTarget = nullptr;          // [H*W] target image (row-major)
     bool mri_cluster = true;           // per-step apply on one cluster per replica
     cublasHandle_t blas = nullptr;
-    cudaStream_t sfin = nullptr;             // stream of the reduction / update kernels
-    cudaEvent_t evA[4] = {}, evF[4] = {};    // per group: tiles done / update done
     __half *WB0 = nullptr, *WB1 = nullptr;  // fp16 B tiles of W0 / W1 [B][nRB][2NR x 128]
     int *WS0 = nullptr, *WS1 = nullptr;     // their scale exponents [B][nRB][NR]
     size_t spart_elems = 0;
@@ -428,7 +413,9 @@ struct cimcs_ctx {
     cudaStream_t side = nullptr;  // captures the CG loop body
     cimcs_timing timing{};
 
-    size_t elt() const { return dtype == CIMCS_F64 ? 8 : 4; }
+    // fp64 state arrays (c, e, R, w, D, hz): F64 and F32X contexts
+    bool st64() const { return dtype != CIMCS_F32; }
+    size_t elt() const { return st64() ? 8 : 4; }
     const void* G() const { return dG; }
     size_t state_elems() const { return (size_t)B * ldN * NR; }
     // contraction-input arrays: [b][i][r], or (tc) [W | W_lo] canonical, 2*NR rows
@@ -437,10 +424,10 @@ struct cimcs_ctx {
 
 namespace {
 
-// contraction-input layout: the streaming and factored tcgen05 kernels read W
+// contraction-input layout: the streaming tcgen05 kernel reads W
 // as the canonical [W | W_lo] operand (tc_wofs); the symmetric-tile path and
 // the CUDA-core paths use [b][i][r] (coalesced float4 rows in the update)
-inline int wcanon(const cimcs_ctx* c) { return c->tc && (!c->sym || c->fac) ? 1 : 0; }
+inline int wcanon(const cimcs_ctx*) { return 0; }  // plain [b][i][r] on every path
 
 void drop_graphs(cimcs_ctx* c) {
     if (c->g_cim) cudaGraphExecDestroy(c->g_cim);
@@ -454,7 +441,7 @@ void free_state(cimcs_ctx* c) {
     void* ptrs[] = {c->Rs,  c->C,        c->E,          c->W0,  c->W1,       c->Hdbg,
                     c->bestR, c->sig,    c->bestS,      c->fail_gstep, c->fail_idx, c->n_hist,
                     c->improved, c->minE, c->part,      c->best_obj, c->obj, c->rmse, c->ham,
-                    c->tp, c->fail_tmp, c->UB, c->US, c->cgX, c->cgR, c->cgP, c->cgGp, c->cg_act,
+                    c->tp, c->fail_tmp, c->cgX, c->cgR, c->cgP, c->cgGp, c->cg_act,
                     c->cg_st, c->cg_live, c->WB0, c->WB1, c->WS0, c->WS1, c->Pn, c->Pm,
                     c->MT, c->nzd[0], c->nzd[1]};
     for (void* p : ptrs)
@@ -462,8 +449,6 @@ void free_state(cimcs_ctx* c) {
     c->cgX = c->cgR = c->cgP = c->cgGp = nullptr;
     c->WB0 = c->WB1 = nullptr;
     c->WS0 = c->WS1 = nullptr;
-    c->UB = nullptr;
-    c->US = nullptr;
     c->Pn = c->Pm = c->MT = nullptr;
     c->nzd[0] = c->nzd[1] = nullptr;
     for (double*& h : c->nzh)
@@ -487,7 +472,7 @@ void free_state(cimcs_ctx* c) {
 void free_problems(cimcs_ctx* c) {
     free_state(c);
     void* ptrs[] = {c->dA, c->dy, c->dM, c->dG, c->dD, c->dhz, c->dx, c->dxi,
-                    c->dSg, c->dSpart, c->dTask, c->dCnt, c->dMaskBr, c->dTw, c->dTarget,
+                    c->dSg, c->dSpart, c->dMaskBr, c->dTw, c->dTarget,
                     c->dH};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -496,8 +481,6 @@ void free_problems(cimcs_ctx* c) {
         cudaFree(q.sched);
     }
     c->ssched.clear();
-    c->dTask = nullptr;
-    c->dCnt = nullptr;
     c->dSg = nullptr;
     c->dSpart = nullptr;
     c->dMaskBr = nullptr;
@@ -516,18 +499,29 @@ void free_problems(cimcs_ctx* c) {
     c->built = false;
 }
 
+// Device allocation, zero-filled ON THE CONTEXT STREAM: every later upload,
+// kernel and download of the context is ordered after the fill by the stream
+// itself (no device-wide sync; round 1 filled on the legacy stream, which does
+// not order against the non-blocking context stream, and a second context's
+// fill overwrote freshly uploaded instances).
 template <typename P>
-int dalloc(P** p, size_t bytes) {
+int dalloc(cimcs_ctx* c, P** p, size_t bytes) {
     cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(bytes, 16));
     if (e != cudaSuccess)
         return fail(CIMCS_CUDA_ERROR, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-    // the zero fill runs on the legacy stream, which does not order against the
-    // context's non-blocking stream: finish it before any upload can land (a
-    // second context's 39 GB fill used to overwrite freshly uploaded instances)
-    e = cudaMemset(*p, 0, std::max<size_t>(bytes, 16));
-    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    e = cudaMemsetAsync(*p, 0, std::max<size_t>(bytes, 16), c->stream);
     if (e != cudaSuccess)
-        return fail(CIMCS_CUDA_ERROR, std::string("cudaMemset: ") + cudaGetErrorString(e));
+        return fail(CIMCS_CUDA_ERROR, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+// Synchronous copy ordered on the context stream (all host <-> device traffic
+// of a context goes through its stream; the host buffer may be reused on return).
+int copy_sync(cimcs_ctx* c, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess)
+        return fail(CIMCS_CUDA_ERROR, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
     return 0;
 }
 
@@ -606,11 +600,11 @@ int sym_schedule(cimcs_ctx* c, int nb, const cimcs_ctx::SymSched** out) {
     q.nRB = nRB;
     q.grid = grid;
     int rc;
-    if ((rc = dalloc(&q.items, flat.size() * sizeof(int2))) ||
-        (rc = dalloc(&q.sched, beg.size() * sizeof(int))))
+    if ((rc = dalloc(c, &q.items, flat.size() * sizeof(int2))) ||
+        (rc = dalloc(c, &q.sched, beg.size() * sizeof(int))))
         return rc;
-    CK(cudaMemcpy(q.items, flat.data(), flat.size() * sizeof(int2), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(q.sched, beg.data(), beg.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (int rc_ = copy_sync(c, q.items, flat.data(), flat.size() * sizeof(int2), cudaMemcpyHostToDevice)) return rc_;
+    if (int rc_ = copy_sync(c, q.sched, beg.data(), beg.size() * sizeof(int), cudaMemcpyHostToDevice)) return rc_;
     c->ssched.push_back(q);
     *out = &c->ssched.back();
     return 0;
@@ -624,8 +618,8 @@ int ensure_stage(cimcs_ctx* c, size_t elems) {
     c->stage = nullptr;
     c->stage_i = nullptr;
     c->stage_elems = 0;
-    if (int rc = dalloc(&c->stage, elems * 8)) return rc;
-    if (int rc = dalloc(&c->stage_i, elems * 4)) return rc;
+    if (int rc = dalloc(c, &c->stage, elems * 8)) return rc;
+    if (int rc = dalloc(c, &c->stage_i, elems * 4)) return rc;
     c->stage_elems = elems;
     return 0;
 }
@@ -639,65 +633,49 @@ int ensure_state(cimcs_ctx* c, int NR) {
     const int nRB = std::max(c->nRB, 1);
     int rc = 0;
     const size_t nw = c->w_elems();
-    if ((rc = dalloc(&c->Rs, n * es)) || (rc = dalloc(&c->C, n * es)) ||
-        (rc = dalloc(&c->E, n * es)) || (rc = dalloc(&c->W0, nw * es)) ||
-        (rc = dalloc(&c->W1, nw * es)) || (rc = dalloc(&c->Hdbg, n * es)) ||
-        (rc = dalloc(&c->bestR, n * es)) || (rc = dalloc(&c->sig, n)) ||
-        (rc = dalloc(&c->bestS, n)) || (rc = dalloc(&c->fail_gstep, nT * 4)) ||
-        (rc = dalloc(&c->fail_idx, nT * 4)) || (rc = dalloc(&c->n_hist, nT * 4)) ||
-        (rc = dalloc(&c->improved, nT * 4)) || (rc = dalloc(&c->minE, nT * 8)) ||
-        (rc = dalloc(&c->part, (size_t)c->B * nRB * NR * 4 * 8)) ||
-        (rc = dalloc(&c->best_obj, nT * 8)) || (rc = dalloc(&c->obj, nT * 8)) ||
-        (rc = dalloc(&c->rmse, nT * 8)) || (rc = dalloc(&c->ham, nT * 8)) ||
-        (rc = dalloc(&c->tp, (size_t)nT * 5 * 8)) || (rc = dalloc(&c->fail_tmp, nT * 4)))
+    if ((rc = dalloc(c, &c->Rs, n * es)) || (rc = dalloc(c, &c->C, n * es)) ||
+        (rc = dalloc(c, &c->E, n * es)) || (rc = dalloc(c, &c->W0, nw * es)) ||
+        (rc = dalloc(c, &c->W1, nw * es)) || (rc = dalloc(c, &c->Hdbg, n * es)) ||
+        (rc = dalloc(c, &c->bestR, n * es)) || (rc = dalloc(c, &c->sig, n)) ||
+        (rc = dalloc(c, &c->bestS, n)) || (rc = dalloc(c, &c->fail_gstep, nT * 4)) ||
+        (rc = dalloc(c, &c->fail_idx, nT * 4)) || (rc = dalloc(c, &c->n_hist, nT * 4)) ||
+        (rc = dalloc(c, &c->improved, nT * 4)) || (rc = dalloc(c, &c->minE, nT * 8)) ||
+        (rc = dalloc(c, &c->part, (size_t)c->B * nRB * NR * 4 * 8)) ||
+        (rc = dalloc(c, &c->best_obj, nT * 8)) || (rc = dalloc(c, &c->obj, nT * 8)) ||
+        (rc = dalloc(c, &c->rmse, nT * 8)) || (rc = dalloc(c, &c->ham, nT * 8)) ||
+        (rc = dalloc(c, &c->tp, (size_t)nT * 5 * 8)) || (rc = dalloc(c, &c->fail_tmp, nT * 4)))
         return rc;
-    if (c->sym && !c->sfin) {
-        CK(cudaStreamCreateWithFlags(&c->sfin, cudaStreamNonBlocking));
-        for (int g = 0; g < 4; ++g) {
-            CK(cudaEventCreateWithFlags(&c->evA[g], cudaEventDisableTiming));
-            CK(cudaEventCreateWithFlags(&c->evF[g], cudaEventDisableTiming));
-        }
-    }
     if (c->mri) {  // G w of the transform chain, one slot: [N][NR]
         const size_t ne = (size_t)c->nRB * kSyT * NR;
         if (c->spart_elems < ne) {
             if (c->dSpart) cudaFree(c->dSpart);
             c->dSpart = nullptr;
             c->spart_elems = 0;
-            if ((rc = dalloc(&c->dSpart, ne * 4))) return rc;
+            if ((rc = dalloc(c, &c->dSpart, ne * 4))) return rc;
             c->spart_elems = ne;
         }
     }
     if (c->sym) {  // fp16 B tiles of W0/W1 and the partial products of the symmetric kernel
         const size_t nb = (size_t)c->B * c->nRB * 2 * NR * kSyT, ns = (size_t)c->B * c->nRB * NR;
-        if ((rc = dalloc(&c->WB0, nb * 2)) || (rc = dalloc(&c->WB1, nb * 2)) ||
-            (rc = dalloc(&c->WS0, ns * 4)) || (rc = dalloc(&c->WS1, ns * 4)))
+        if ((rc = dalloc(c, &c->WB0, nb * 2)) || (rc = dalloc(c, &c->WB1, nb * 2)) ||
+            (rc = dalloc(c, &c->WS0, ns * 4)) || (rc = dalloc(c, &c->WS1, ns * 4)))
             return rc;
-        const size_t ne = c->fac ? 0 : (size_t)c->B * c->nRB * c->nSB * kSyT * NR;
-        if (c->fac && ((rc = dalloc(&c->UB, (size_t)c->B * c->nMB * 2 * NR * kSyT * 2)) ||
-                       (rc = dalloc(&c->US, (size_t)c->B * c->nMB * NR * 4))))
-            return rc;
-        // item schedules of every instance-group split (built outside graph capture)
-        if (!c->fac)
-            for (int G = 1; G <= std::min(4, c->B); ++G)
-                for (int g = 0; g < G; ++g) {
-                    const int b0 = (int)((long long)c->B * g / G);
-                    const int b1 = (int)((long long)c->B * (g + 1) / G);
-                    const cimcs_ctx::SymSched* ss;
-                    if (b1 > b0 && (rc = sym_schedule(c, b1 - b0, &ss))) return rc;
-                }
+        const size_t ne = (size_t)c->B * c->nRB * c->nSB * kSyT * NR;
+        // the item schedule (built outside graph capture)
+        const cimcs_ctx::SymSched* ss;
+        if ((rc = sym_schedule(c, c->B, &ss))) return rc;
         if (ne && c->spart_elems < ne) {
             if (c->dSpart) cudaFree(c->dSpart);
             c->dSpart = nullptr;
             c->spart_elems = 0;
-            if ((rc = dalloc(&c->dSpart, ne * 4))) return rc;
+            if ((rc = dalloc(c, &c->dSpart, ne * 4))) return rc;
             c->spart_elems = ne;
         }
         if (c->tshard) {  // slots of other ranks' items stay zero for good
             CK(cudaMemsetAsync(c->dSpart, 0, ne * 4, c->stream));
             if (c->dH) cudaFree(c->dH);
             c->dH = nullptr;
-            if ((rc = dalloc(&c->dH, (size_t)c->B * c->nRB * kSyT * NR * 4))) return rc;
+            if ((rc = dalloc(c, &c->dH, (size_t)c->B * c->nRB * kSyT * NR * 4))) return rc;
         }
     }
     return 0;
@@ -797,15 +775,14 @@ int launch_gemv_T(cimcs_ctx* c, int mode, const GemvArgs& a) {
 
 TcArgs tc_args(const cimcs_ctx* c, const GemvArgs& g) {
     TcArgs a{};
-    a.G = static_cast<const float*>(g.G);
-    a.D = static_cast<const float*>(g.D);
-    a.hz = static_cast<const float*>(g.hz);
-    a.Win = static_cast<const float*>(g.Win);
-    a.Wout = static_cast<float*>(g.Wout);
-    a.Rs = static_cast<float*>(g.Rs);
-    a.C = static_cast<float*>(g.C);
-    a.E = static_cast<float*>(g.E);
-    a.Hdbg = static_cast<float*>(g.Hdbg);
+    a.D = g.D;
+    a.hz = g.hz;
+    a.Win = g.Win;
+    a.Wout = g.Wout;
+    a.Rs = g.Rs;
+    a.C = g.C;
+    a.E = g.E;
+    a.Hdbg = g.Hdbg;
     a.Mv = g.Mv;
     a.sigma = g.sigma;
     a.fail_gstep = g.fail_gstep;
@@ -831,29 +808,19 @@ TcArgs tc_args(const cimcs_ctx* c, const GemvArgs& g) {
     return a;
 }
 
-template <int NR, int MODE>
-int launch_tc_t(cimcs_ctx* c, const GemvArgs& g) {
-    const TcArgs a = tc_args(c, g);
-    if (a.ntiles == 0) return 0;
-    auto kern = tc_step_kernel<NR, MODE>;
-    constexpr size_t smem = tc_smem_bytes(NR);
-    static std::atomic<unsigned long long> attr{0};  // per device: the attribute is per context
-    if (!(attr.load() >> c->device & 1ull)) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr.fetch_or(1ull << c->device);
-    }
-    const int grid = std::min(a.ntiles, c->num_sms);
-    kern<<<grid, kTcThreads, smem, c->stream>>>(a);
-    CK(cudaGetLastError());
-    return 0;
+
+__global__ void f64_to_f32_kernel(const double* __restrict__ a, float* __restrict__ o, size_t n) {
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
+         t += (size_t)gridDim.x * blockDim.x)
+        o[t] = (float)a[t];
 }
 
 // symmetric-tile variant (sym_kernels.cuh): half the gram bytes per step.
-// Instances [b0, b0 + nb): the tile kernel on stream sA, then (after evA) the
-// slot reduction and the fused update on stream sF.
+// The tile kernel, then the slot reduction and the fused update, on the
+// context stream (instances [b0, b0 + nb)).
 template <int NR, int MODE>
-int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb, cudaStream_t sA,
-                 cudaStream_t sF, cudaEvent_t evA) {
+int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb) {
+    cudaStream_t sA = c->stream, sF = c->stream;
     SymArgs sa{};
     sa.t = tc_args(c, g);
     sa.Gs = static_cast<const __half*>(c->dG);
@@ -912,10 +879,6 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb, cudaStream_t s
         c->timing.tile_kernel_ms += ms;
         c->timing.tile_kernel_launches += 1;
     }
-    if (sF != sA) {
-        CK(cudaEventRecord(evA, sA));
-        CK(cudaStreamWaitEvent(sF, evA, 0));
-    }
     if (c->tshard) {  // own items' slot sums, then the cross-rank sum (one collective)
         sym_slotsum_kernel<NR><<<dim3(c->nRB, nb), kSyT * NR / 4, 0, sF>>>(c->dSpart, c->dH, c->nRB,
                                                                          c->nSB, b0);
@@ -932,93 +895,30 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb, cudaStream_t s
     cfg.blockDim = dim3(kSyT * NR / 4);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = sF;
-    CK(cudaLaunchKernelEx(&cfg, sym_update_kernel<NR, MODE>, sa));
+    if (c->st64())
+        CK(cudaLaunchKernelEx(&cfg, sym_update_kernel<NR, MODE, double>, sa));
+    else
+        CK(cudaLaunchKernelEx(&cfg, sym_update_kernel<NR, MODE, float>, sa));
     return 0;
 }
 
 template <int NR>
-int launch_sym_grp(cimcs_ctx* c, int mode, const GemvArgs& a, int b0, int nb, cudaStream_t sA,
-                   cudaStream_t sF, cudaEvent_t evA) {
+int launch_sym_grp(cimcs_ctx* c, int mode, const GemvArgs& a, int b0, int nb) {
     switch (mode) {
-        case EPI_STEP_BN: return launch_sym_t<NR, EPI_STEP_BN>(c, a, b0, nb, sA, sF, evA);
-        case EPI_STEP_CN: return launch_sym_t<NR, EPI_STEP_CN>(c, a, b0, nb, sA, sF, evA);
-        case EPI_JACOBI: return launch_sym_t<NR, EPI_JACOBI>(c, a, b0, nb, sA, sF, evA);
-        case EPI_MATVEC: return launch_sym_t<NR, EPI_MATVEC>(c, a, b0, nb, sA, sF, evA);
-        default: return launch_sym_t<NR, EPI_SCORE>(c, a, b0, nb, sA, sF, evA);
+        case EPI_STEP_BN: return launch_sym_t<NR, EPI_STEP_BN>(c, a, b0, nb);
+        case EPI_STEP_CN: return launch_sym_t<NR, EPI_STEP_CN>(c, a, b0, nb);
+        case EPI_JACOBI: return launch_sym_t<NR, EPI_JACOBI>(c, a, b0, nb);
+        case EPI_MATVEC: return launch_sym_t<NR, EPI_MATVEC>(c, a, b0, nb);
+        default: return launch_sym_t<NR, EPI_SCORE>(c, a, b0, nb);
     }
 }
 
-// factored path: one cooperative launch per step / sweep (fac_kernels.cuh)
-template <int NR, int MODE>
-int launch_fac_t(cimcs_ctx* c, const GemvArgs& g) {
-    FacArgs f{};
-    f.t = tc_args(c, g);
-    f.As = static_cast<const __half*>(c->dG);
-    f.sa = c->dSg;
-    f.WBin = g.Win == c->W0 ? c->WB0 : c->WB1;
-    f.WSin = g.Win == c->W0 ? c->WS0 : c->WS1;
-    f.WBout = g.Wout == c->W0 ? c->WB0 : c->WB1;
-    f.WSout = g.Wout == c->W0 ? c->WS0 : c->WS1;
-    f.UB = c->UB;
-    f.US = c->US;
-    f.cnt = c->dCnt;
-    f.task = c->dTask;
-    f.ntask = c->ntask;
-    f.nMB = c->nMB;
-    f.W2 = c->fac_w2;
-    auto kern = fac_step_kernel<NR, MODE>;
-    constexpr size_t smem = fa_smem_bytes<NR>();
-    static std::atomic<unsigned long long> attr{0};
-    if (!(attr.load() >> c->device & 1ull)) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr.fetch_or(1ull << c->device);
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(std::min(f.ntask, c->num_sms));
-    cfg.blockDim = dim3(kFaThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = c->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;  // tasks wait on other CTAs' tasks
-    at[0].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, kern, f));
-    return 0;
-}
-
-template <int NR>
-int launch_fac_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
-    switch (mode) {
-        case EPI_STEP_BN: return launch_fac_t<NR, EPI_STEP_BN>(c, a);
-        case EPI_STEP_CN: return launch_fac_t<NR, EPI_STEP_CN>(c, a);
-        case EPI_JACOBI: return launch_fac_t<NR, EPI_JACOBI>(c, a);
-        case EPI_MATVEC: return launch_fac_t<NR, EPI_MATVEC>(c, a);
-        default: return launch_fac_t<NR, EPI_SCORE>(c, a);
-    }
-}
 
 template <int NR>
 int launch_sym_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
-    return launch_sym_grp<NR>(c, mode, a, 0, c->B, c->stream, c->stream, nullptr);
+    return launch_sym_grp<NR>(c, mode, a, 0, c->B);
 }
 
-template <int NR>
-int launch_tc_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
-    switch (mode) {
-        case EPI_STEP_BN: return launch_tc_t<NR, EPI_STEP_BN>(c, a);
-        case EPI_STEP_CN: return launch_tc_t<NR, EPI_STEP_CN>(c, a);
-        case EPI_JACOBI: return launch_tc_t<NR, EPI_JACOBI>(c, a);
-        case EPI_MATVEC: return launch_tc_t<NR, EPI_MATVEC>(c, a);
-        default: return launch_tc_t<NR, EPI_SCORE>(c, a);
-    }
-}
-
-__global__ void f64_to_f32_kernel(const double* __restrict__ a, float* __restrict__ o, size_t n) {
-    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
-         t += (size_t)gridDim.x * blockDim.x)
-        o[t] = (float)a[t];
-}
 
 // one mri_kernel launch of `grid` CTAs (basis vectors r0.. for DIAG / COLS)
 int mri_launch(cimcs_ctx* c, int mode, int grid, int r0, const float* in, float* out) {
@@ -1115,10 +1015,8 @@ int launch_mri_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
 
 int launch_gemv(cimcs_ctx* c, int mode, const GemvArgs& a) {
     if (c->mri) return c->NR == 8 ? launch_mri_nr<8>(c, mode, a) : launch_mri_nr<16>(c, mode, a);
-    if (c->fac) return c->NR == 8 ? launch_fac_nr<8>(c, mode, a) : launch_fac_nr<16>(c, mode, a);
     if (c->sym) return c->NR == 8 ? launch_sym_nr<8>(c, mode, a) : launch_sym_nr<16>(c, mode, a);
-    if (c->tc) return c->NR == 8 ? launch_tc_nr<8>(c, mode, a) : launch_tc_nr<16>(c, mode, a);
-    return c->dtype == CIMCS_F64 ? launch_gemv_T<double>(c, mode, a)
+    return c->st64() ? launch_gemv_T<double>(c, mode, a)
                                  : launch_gemv_T<float>(c, mode, a);
 }
 
@@ -1133,9 +1031,14 @@ int sym_sync_w(cimcs_ctx* c, const void* W) {
     const bool w0 = W == c->W0;
     const dim3 g(c->nRB, c->B);
     DISPATCH_NR_TC(c->NR, {
-        sym_wconvert_kernel<NR_><<<g, 128, 0, c->stream>>>(
-            static_cast<const float*>(W), c->N, c->ldJ, c->ldN, wcanon(c), c->nRB,
-            w0 ? c->WB0 : c->WB1, w0 ? c->WS0 : c->WS1);
+        if (c->st64())
+            sym_wconvert_kernel<NR_, double><<<g, 128, 0, c->stream>>>(
+                static_cast<const double*>(W), c->N, c->ldN, c->nRB, w0 ? c->WB0 : c->WB1,
+                w0 ? c->WS0 : c->WS1);
+        else
+            sym_wconvert_kernel<NR_, float><<<g, 128, 0, c->stream>>>(
+                static_cast<const float*>(W), c->N, c->ldN, c->nRB, w0 ? c->WB0 : c->WB1,
+                w0 ? c->WS0 : c->WS1);
     });
     CK(cudaGetLastError());
     return 0;
@@ -1178,7 +1081,7 @@ int run_init_T(cimcs_ctx* c, int Rreal, int bn, const double* dc0, const double*
 }
 
 int run_init(cimcs_ctx* c, int Rreal, int bn, const double* dc0, const double* de0, double rt) {
-    return c->dtype == CIMCS_F64 ? run_init_T<double>(c, Rreal, bn, dc0, de0, rt)
+    return c->st64() ? run_init_T<double>(c, Rreal, bn, dc0, de0, rt)
                                  : run_init_T<float>(c, Rreal, bn, dc0, de0, rt);
 }
 
@@ -1195,7 +1098,7 @@ int run_support_T(cimcs_ctx* c) {
 }
 
 int run_support(cimcs_ctx* c) {
-    return c->dtype == CIMCS_F64 ? run_support_T<double>(c) : run_support_T<float>(c);
+    return c->st64() ? run_support_T<double>(c) : run_support_T<float>(c);
 }
 
 template <typename T>
@@ -1213,7 +1116,7 @@ int upload_traj_T(cimcs_ctx* c, const double* h, void* d, int Rreal, T pad) {
 }
 
 int upload_traj(cimcs_ctx* c, const double* h, void* d, int Rreal, double pad = 0.0) {
-    return c->dtype == CIMCS_F64 ? upload_traj_T<double>(c, h, d, Rreal, pad)
+    return c->st64() ? upload_traj_T<double>(c, h, d, Rreal, pad)
                                  : upload_traj_T<float>(c, h, d, Rreal, (float)pad);
 }
 
@@ -1232,7 +1135,7 @@ int download_traj_T(cimcs_ctx* c, const void* d, double* h, int Rreal) {
 }
 
 int download_traj(cimcs_ctx* c, const void* d, double* h, int Rreal) {
-    return c->dtype == CIMCS_F64 ? download_traj_T<double>(c, d, h, Rreal)
+    return c->st64() ? download_traj_T<double>(c, d, h, Rreal)
                                  : download_traj_T<float>(c, d, h, Rreal);
 }
 
@@ -1327,7 +1230,7 @@ int nRB_of(const cimcs_ctx* c) { return c->nRB; }
 // ------------------------------------------------ row-sharding collectives
 
 ncclDataType_t nccl_t(const cimcs_ctx* c) {
-    return c->dtype == CIMCS_F64 ? ncclFloat64 : ncclFloat32;
+    return c->st64() ? ncclFloat64 : ncclFloat32;
 }
 
 // All-gather this rank's rows of a per-instance array X[b][rows][row_elems]
@@ -1346,10 +1249,8 @@ int allgather_rows(cimcs_ctx* c, void* X, size_t row_elems, size_t inst_elems,
     return 0;
 }
 
-// contraction input (w or the refit's V): the tc layout is chunk-major in j,
-// so a rank's rows are one contiguous slice per instance as well
+// contraction input (w or the refit's V)
 int allgather_w(cimcs_ctx* c, void* W) {
-    if (c->tc) return allgather_rows(c, W, 2 * c->NR, (size_t)c->ldJ * 2 * c->NR, ncclFloat32, 4);
     return allgather_rows(c, W, c->NR, (size_t)c->ldN * c->NR, nccl_t(c), c->elt());
 }
 int allgather_state(cimcs_ctx* c, void* X) {
@@ -1377,7 +1278,7 @@ int reconcile_cim(cimcs_ctx* c) {
 // Enqueue the n_steps fused Euler steps of one CIM call (graph-capturable).
 // ------------------------------------------ small-N cluster loop (N <= 512)
 // Replica slots the register-resident G slice leaves room for.
-int cluster_max_nr(const cimcs_ctx* c) { return c->dtype == CIMCS_F64 ? 4 : 8; }
+int cluster_max_nr(const cimcs_ctx* c) { return c->st64() ? 4 : 8; }
 
 bool cluster_ok(const cimcs_ctx* c) {
     return c->use_cluster && !c->mri && c->world == 1 && !c->sharded && c->N <= kClMaxN &&
@@ -1394,7 +1295,6 @@ int launch_cluster_t(cimcs_ctx* c, GemvArgs a, int n_iters) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         attr.fetch_or(1ull << c->device);
     }
-    a.tc_in = wcanon(c);
     const unsigned cs = (unsigned)((c->N + kClRows - 1) / kClRows);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(c->B * cs);
@@ -1434,46 +1334,20 @@ int launch_cluster_T(cimcs_ctx* c, int mode, const GemvArgs& a, int n_iters) {
 }
 
 int launch_cluster(cimcs_ctx* c, int mode, const GemvArgs& a, int n_iters) {
-    return c->dtype == CIMCS_F64 ? launch_cluster_T<double>(c, mode, a, n_iters)
+    return c->st64() ? launch_cluster_T<double>(c, mode, a, n_iters)
                                  : launch_cluster_T<float>(c, mode, a, n_iters);
 }
 
 // n_iters launches of `mode` with W ping-pong (Euler steps or Jacobi sweeps) on
-// the symmetric path.  Option "sym_groups" > 1 splits the instances into
-// groups: the tile kernel of group g+1 runs on the context stream while the
-// reduction / update of group g runs on c->sfin, and group g's next tile
-// kernel waits only for its own update.  Measured on config 1 it does not pay
-// (the step is bound by the total HBM traffic of the three kernels, which
-// overlapping cannot reduce), so the default is one group.
+// the symmetric path (pipelining instance groups over two streams was measured
+// slower: DESIGN.md section 4).
 int enqueue_sym_loop(cimcs_ctx* c, int mode, GemvArgs a, int n_iters, bool steps) {
-    if (c->fac) {
-        for (int k = 0; k < n_iters; ++k) {
-            if (steps) a.step = k;
-            a.Win = (k & 1) ? c->W1 : c->W0;
-            a.Wout = (k & 1) ? c->W0 : c->W1;
-            if (int rc = launch_gemv(c, mode, a)) return rc;
-        }
-        return 0;
-    }
-    int G = c->sym_groups ? c->sym_groups : 1;
-    G = std::max(1, std::min(G, std::min(4, c->B)));
     for (int k = 0; k < n_iters; ++k) {
         if (steps) a.step = k;
         a.Win = (k & 1) ? c->W1 : c->W0;
         a.Wout = (k & 1) ? c->W0 : c->W1;
-        for (int g = 0; g < G; ++g) {
-            const int b0 = (int)((long long)c->B * g / G), b1 = (int)((long long)c->B * (g + 1) / G);
-            if (G > 1 && k > 0) CK(cudaStreamWaitEvent(c->stream, c->evF[g], 0));
-            cudaStream_t sF = G > 1 ? c->sfin : c->stream;
-            const int rc = c->NR == 8
-                               ? launch_sym_grp<8>(c, mode, a, b0, b1 - b0, c->stream, sF, c->evA[g])
-                               : launch_sym_grp<16>(c, mode, a, b0, b1 - b0, c->stream, sF, c->evA[g]);
-            if (rc) return rc;
-            if (G > 1) CK(cudaEventRecord(c->evF[g], c->sfin));
-        }
+        if (int rc = launch_gemv(c, mode, a)) return rc;
     }
-    if (G > 1)
-        for (int g = 0; g < G; ++g) CK(cudaStreamWaitEvent(c->stream, c->evF[g], 0));
     return 0;
 }
 
@@ -1532,10 +1406,10 @@ int ensure_cg(cimcs_ctx* c) {  // outside any capture: allocates
     if (c->cgX) return 0;
     const size_t n = c->state_elems();
     for (double** p : {&c->cgX, &c->cgR, &c->cgP, &c->cgGp})
-        if (int rc = dalloc(p, n * 8)) return rc;
-    if (int rc = dalloc(&c->cg_act, n * 4)) return rc;
-    if (int rc = dalloc(&c->cg_st, (size_t)c->B * c->NR * sizeof(CgTraj))) return rc;
-    if (int rc = dalloc(&c->cg_live, 2 * 4)) return rc;
+        if (int rc = dalloc(c, p, n * 8)) return rc;
+    if (int rc = dalloc(c, &c->cg_act, n * 4)) return rc;
+    if (int rc = dalloc(c, &c->cg_st, (size_t)c->B * c->NR * sizeof(CgTraj))) return rc;
+    if (int rc = dalloc(c, &c->cg_live, 2 * 4)) return rc;
     if (!c->side) CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     return 0;
 }
@@ -1576,7 +1450,7 @@ int cg_launch(cimcs_ctx* c, int which, const CgArgs& a) {
 }
 
 int cg_kernel(cimcs_ctx* c, int which, const CgArgs& a) {
-    return c->dtype == CIMCS_F64 ? cg_launch<double>(c, which, a) : cg_launch<float>(c, which, a);
+    return c->st64() ? cg_launch<double>(c, which, a) : cg_launch<float>(c, which, a);
 }
 
 // G p for every trajectory (the EPI_MATVEC contraction of W0 into cgGp)
@@ -1611,7 +1485,7 @@ int enqueue_cg(cimcs_ctx* c, const StepScalars& s, const cimcs_hyper* hp) {
     cudaGraphConditionalHandle h{};
     if (in_graph) CK(cudaGraphConditionalHandleCreate(&h, cgraph, 0, 0));
     const CgArgs a = cg_args(c, hp);
-    int rc = c->dtype == CIMCS_F64 ? mask_T<double>(c, c->W0) : mask_T<float>(c, c->W0);
+    int rc = c->st64() ? mask_T<double>(c, c->W0) : mask_T<float>(c, c->W0);
     if (!rc) rc = cg_matvec(c, s);  // G x0
     if (!rc) rc = cg_kernel(c, 0, a);
     if (!rc) rc = sym_sync_w(c, c->W0);
@@ -1657,7 +1531,7 @@ int enqueue_cg(cimcs_ctx* c, const StepScalars& s, const cimcs_hyper* hp) {
         }
     }
     rc = cg_kernel(c, 2, a);
-    if (!rc) rc = c->dtype == CIMCS_F64 ? mask_T<double>(c, c->W0) : mask_T<float>(c, c->W0);
+    if (!rc) rc = c->st64() ? mask_T<double>(c, c->W0) : mask_T<float>(c, c->W0);
     return rc;
 }
 
@@ -1700,13 +1574,13 @@ int enqueue_score(cimcs_ctx* c, const StepScalars& s, int v_slot, DevRecord* his
         if (int rc = allgather_state(c, c->E)) return rc;
     }
     if (hist_alt) {
-        if (int rc = c->dtype == CIMCS_F64 ? enqueue_median_T<double>(c, hist_alt)
+        if (int rc = c->st64() ? enqueue_median_T<double>(c, hist_alt)
                                            : enqueue_median_T<float>(c, hist_alt))
             return rc;
     }
     if (track_best) {
         const int g = grid_for(c->state_elems());
-        if (c->dtype == CIMCS_F64) {
+        if (c->st64()) {
             DISPATCH_NR(c->NR, {
                 best_update_kernel<double, NR_><<<g, 256, 0, c->stream>>>(
                     c->improved, static_cast<const double*>(c->Rs), c->sig,
@@ -1750,12 +1624,14 @@ int upload_pump(cimcs_ctx* c, const cimcs_hyper* hp) {
     for (double v : p)
         if (!std::isfinite(v)) return fail(CIMCS_INPUT_ERROR, "mfz_step: non-finite pump");
     if (c->pump_cap < hp->n_steps) {
+        // cached graphs bake the pump pointer: drop them with the old buffer
+        drop_graphs(c);
         if (c->pump) cudaFree(c->pump);
         c->pump = nullptr;
-        if (int rc = dalloc(&c->pump, (size_t)hp->n_steps * 8)) return rc;
+        if (int rc = dalloc(c, &c->pump, (size_t)hp->n_steps * 8)) return rc;
         c->pump_cap = hp->n_steps;
     }
-    CK(cudaMemcpy(c->pump, p.data(), (size_t)hp->n_steps * 8, cudaMemcpyHostToDevice));
+    if (int rc_ = copy_sync(c, c->pump, p.data(), (size_t)hp->n_steps * 8, cudaMemcpyHostToDevice)) return rc_;
     return 0;
 }
 
@@ -1893,8 +1769,8 @@ int ensure_pp(cimcs_ctx* c) {  // outside any capture
     const size_t n = c->state_elems();
     if (!c->Pn) {
         int rc;
-        if ((rc = dalloc(&c->Pn, n * c->elt())) || (rc = dalloc(&c->Pm, n * c->elt())) ||
-            (rc = dalloc(&c->MT, n * c->elt())))
+        if ((rc = dalloc(c, &c->Pn, n * c->elt())) || (rc = dalloc(c, &c->Pm, n * c->elt())) ||
+            (rc = dalloc(c, &c->MT, n * c->elt())))
             return rc;
     }
     const size_t nz = (size_t)kPpChunk * n;
@@ -1905,7 +1781,7 @@ int ensure_pp(cimcs_ctx* c) {  // outside any capture
             c->nzd[k] = c->nzh[k] = nullptr;
         }
         for (int k = 0; k < 2; ++k) {
-            if (int rc = dalloc(&c->nzd[k], nz * 8)) return rc;
+            if (int rc = dalloc(c, &c->nzd[k], nz * 8)) return rc;
             CK(cudaMallocHost(&c->nzh[k], nz * 8));
             std::memset(c->nzh[k], 0, nz * 8);  // padded slots stay zero
         }
@@ -1978,7 +1854,7 @@ int run_pp_cim(cimcs_ctx* c, int Rreal, const StepScalars& s, const cimcs_hyper*
     int rc = stage(0);
     if (!rc && nch > 1) rc = stage(1);
     if (!rc)
-        rc = c->dtype == CIMCS_F64 ? pp_init_T<double>(c, Rreal, c->nzd[0], s)
+        rc = c->st64() ? pp_init_T<double>(c, Rreal, c->nzd[0], s)
                                    : pp_init_T<float>(c, Rreal, c->nzd[0], s);
     GemvArgs a = base_args(c, s);
     a.pump = c->pump;
@@ -2189,7 +2065,8 @@ int cimcs_gen_instances(int32_t B, int32_t N, const double* alpha, const double*
 
 int cimcs_create(int32_t device, int32_t dtype, cimcs_ctx** out) {
     if (!out) return fail(CIMCS_INPUT_ERROR, "null out");
-    if (dtype != CIMCS_F32 && dtype != CIMCS_F64) return fail(CIMCS_CONFIG_ERROR, "bad dtype");
+    if (dtype != CIMCS_F32 && dtype != CIMCS_F64 && dtype != CIMCS_F32X)
+        return fail(CIMCS_CONFIG_ERROR, "bad dtype");
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(CIMCS_CONFIG_ERROR, "bad device");
@@ -2207,7 +2084,7 @@ int cimcs_create(int32_t device, int32_t dtype, cimcs_ctx** out) {
         delete c;
         return fail(CIMCS_CUDA_ERROR, "stream create failed");
     }
-    if (dalloc(&c->alt, sizeof(AltParams)) || dalloc(&c->err, 16)) {
+    if (dalloc(c, &c->alt, sizeof(AltParams)) || dalloc(c, &c->err, 16)) {
         delete c;
         return CIMCS_CUDA_ERROR;
     }
@@ -2263,12 +2140,7 @@ void cimcs_destroy(cimcs_ctx* c) {
     drop_graphs(c);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->side) cudaStreamDestroy(c->side);
-    if (c->sfin) cudaStreamDestroy(c->sfin);
     if (c->blas) cublasDestroy(c->blas);
-    for (int g = 0; g < 4; ++g) {
-        if (c->evA[g]) cudaEventDestroy(c->evA[g]);
-        if (c->evF[g]) cudaEventDestroy(c->evF[g]);
-    }
     cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -2298,16 +2170,7 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
         c->use_pdl = v != 0;
         drop_graphs(c);
     }
-    else if (k == "sym_groups") c->sym_groups = (int)std::min<int64_t>(4, std::max<int64_t>(0, v));
-    else if (k == "fac_skew") {
-        c->fac_skew = (int)std::max<int64_t>(0, v);  // applied by build_coupling
-    } else if (k == "factored") {
-        if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set factored before set_problems");
-        c->fac_opt = v > 0 ? 1 : (v < 0 ? -1 : 0);
-    } else if (k == "symmetric") {
-        if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set symmetric before set_problems");
-        c->want_sym = v != 0;
-    } else if (k == "cluster_loop") {
+    else if (k == "cluster_loop") {
         c->use_cluster = v != 0;
         drop_graphs(c);
     }
@@ -2326,19 +2189,18 @@ int prepare_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M, bool 
     // same shapes as the resident problem set: keep every device allocation
     const bool reuse = c->dA && c->B == B && c->N == N && c->has_truth == truth &&
                        std::equal(c->M.begin(), c->M.end(), M) && (int)c->M.size() == B &&
-                       c->want_tc == c->tc_requested && c->want_sym == c->sym_requested &&
-                       c->fac_opt == c->fac_requested && !c->sh_rows;
+                       c->want_tc == c->tc_requested && !c->sh_rows;
     if (!reuse) free_problems(c);
     c->built = false;
     c->tc_requested = c->want_tc;
-    c->sym_requested = c->want_sym;
-    c->fac_requested = c->fac_opt;
     c->B = B;
     c->N = N;
     c->ldN = (N + 31) / 32 * 32;
     c->ldJ = (N + kChunk - 1) / kChunk * kChunk;
-    c->tc = c->dtype == CIMCS_F32 && c->want_tc;
-    c->RB = c->dtype == CIMCS_F64 ? row_block<double>() : (c->tc ? kTcRows : row_block<float>());
+    // fp32 tensor cores = the symmetric-tile path, for N above the cluster-loop
+    // range, unsharded or tile-sharded; everything else runs on CUDA cores
+    c->tc = c->dtype != CIMCS_F64 && c->want_tc && N > kClMaxN && (!c->sh_rows || c->tshard_opt);
+    c->RB = c->tc ? kTcRows : (c->st64() ? row_block<double>() : row_block<float>());
     c->row0 = 0;
     c->row1 = N;
     c->rb0 = 0;
@@ -2348,7 +2210,7 @@ int prepare_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M, bool 
     c->world = c->sh_rows ? c->sh_world : 1;
     c->rank = c->sh_rows ? c->sh_rank : 0;
     c->sharded = c->sh_rows;
-    c->tshard = c->sh_rows && c->tshard_opt && c->tc && c->want_sym && N > kClMaxN;
+    c->tshard = c->sh_rows && c->tc;
     c->tworld = c->tshard ? c->world : 1;
     c->trank = c->tshard ? c->rank : 0;
     if (c->tshard) {
@@ -2366,32 +2228,22 @@ int prepare_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M, bool 
         c->nRB = c->row1 > c->row0 ? (c->row1 - c->row0 + c->RB - 1) / c->RB : 0;
     }
     c->nch = c->ldJ / kTcChunk;
-    // symmetric-tile gram for the streaming regime (the small-N cluster loop
-    // reads the canonical panels; row-sharded contexts stream their own rows)
-    c->sym = c->tc && c->want_sym && c->world == 1 && !c->sharded && N > kClMaxN;
+    c->sym = c->tc;
     c->ntri = c->sym ? c->nRB * (c->nRB + 1) / 2 : 0;
     c->nSB = (c->nRB + kSyS - 1) / kSyS;
     if (c->tshard) tile_shard(c->nRB, c->tworld, c->trank, &c->sP0, &c->sP1);
     c->M.assign(M, M + B);
     c->Mmax = *std::max_element(c->M.begin(), c->M.end());
-    // factored variant: auto when A is read twice per step (phase 2 mostly misses
-    // L2: ncu, profiles/r01_fac_step.txt) and still moves fewer bytes than the
-    // gram triangle, i.e. M below about N/4, and the phase-1 tasks cover the SMs
-    c->nMB = (c->Mmax + kSyT - 1) / kSyT;
-    c->fac = c->sym && !c->tshard && c->nMB < 0x8000 && B < 0x8000 &&
-             (c->fac_opt == 1 || (c->fac_opt == -1 && 2 * c->nMB * c->nRB <= c->ntri &&
-                                  B * c->nMB >= c->num_sms / 2));
-    c->fac_w2 = c->nRB >= 2 * c->nMB ? 2 : 1;
     c->has_truth = truth;
     const size_t astride = (size_t)c->Mmax * N;
     int rc;
-    if (!reuse && ((rc = dalloc(&c->dA, (size_t)B * astride * 8)) ||
-                   (rc = dalloc(&c->dy, (size_t)B * c->Mmax * 8)) ||
-                   (rc = dalloc(&c->dM, (size_t)B * 4))))
+    if (!reuse && ((rc = dalloc(c, &c->dA, (size_t)B * astride * 8)) ||
+                   (rc = dalloc(c, &c->dy, (size_t)B * c->Mmax * 8)) ||
+                   (rc = dalloc(c, &c->dM, (size_t)B * 4))))
         return rc;
     if (truth && !c->dx) {
-        if ((rc = dalloc(&c->dx, (size_t)B * c->ldN * 8)) ||
-            (rc = dalloc(&c->dxi, (size_t)B * c->ldN)))
+        if ((rc = dalloc(c, &c->dx, (size_t)B * c->ldN * 8)) ||
+            (rc = dalloc(c, &c->dxi, (size_t)B * c->ldN)))
             return rc;
     }
     return 0;
@@ -2468,7 +2320,7 @@ int cimcs_set_generated_problems(cimcs_ctx* c, int32_t B, int32_t N, const doubl
     if (int rc = prepare_problems(c, B, N, M.data(), true)) return rc;
     const size_t astride = (size_t)c->Mmax * N;
     int* dsupp = nullptr;
-    if (int rc = dalloc(&dsupp, (size_t)N * 4)) return rc;
+    if (int rc = dalloc(c, &dsupp, (size_t)N * 4)) return rc;
     std::unique_ptr<int, decltype(&cudaFree)> g(dsupp, &cudaFree);
     CK(cudaMemsetAsync(c->dx, 0, (size_t)B * c->ldN * 8, c->stream));
     CK(cudaMemsetAsync(c->dxi, 0, (size_t)B * c->ldN, c->stream));
@@ -2512,13 +2364,21 @@ int cimcs_get_instance(cimcs_ctx* c, int32_t b, double* A, double* y, double* x_
     CK(cudaStreamSynchronize(c->stream));  // cudaMemcpy does not order against c->stream
     const int N = c->N, M = c->M[b];
     const size_t astride = (size_t)c->Mmax * N;
-    if (A) CK(cudaMemcpy(A, c->dA + (size_t)b * astride, (size_t)M * N * 8, cudaMemcpyDeviceToHost));
-    if (y) CK(cudaMemcpy(y, c->dy + (size_t)b * c->Mmax, (size_t)M * 8, cudaMemcpyDeviceToHost));
+    if (A) {
+        if (int rc_ = copy_sync(c, A, c->dA + (size_t)b * astride, (size_t)M * N * 8,
+                                cudaMemcpyDeviceToHost))
+            return rc_;
+    }
+    if (y) {
+        if (int rc_ = copy_sync(c, y, c->dy + (size_t)b * c->Mmax, (size_t)M * 8,
+                                cudaMemcpyDeviceToHost))
+            return rc_;
+    }
     if (c->has_truth && x_true)
-        CK(cudaMemcpy(x_true, c->dx + (size_t)b * c->ldN, (size_t)N * 8, cudaMemcpyDeviceToHost));
+        if (int rc_ = copy_sync(c, x_true, c->dx + (size_t)b * c->ldN, (size_t)N * 8, cudaMemcpyDeviceToHost)) return rc_;
     if (c->has_truth && xi_true) {
         std::vector<int8_t> t((size_t)N);
-        CK(cudaMemcpy(t.data(), c->dxi + (size_t)b * c->ldN, (size_t)N, cudaMemcpyDeviceToHost));
+        if (int rc_ = copy_sync(c, t.data(), c->dxi + (size_t)b * c->ldN, (size_t)N, cudaMemcpyDeviceToHost)) return rc_;
         for (int i = 0; i < N; ++i) xi_true[i] = t[i];
     }
     return 0;
@@ -2573,8 +2433,8 @@ int cimcs_mri_lasso(cimcs_ctx* c, double lambda, int32_t max_iters, double tol, 
     float *zx = nullptr, *gzx = nullptr;
     LassoState* st = nullptr;
     int rc;
-    if ((rc = dalloc(&zx, (size_t)N * 2 * 4)) || (rc = dalloc(&gzx, (size_t)N * 2 * 4)) ||
-        (rc = dalloc(&st, sizeof(LassoState))))
+    if ((rc = dalloc(c, &zx, (size_t)N * 2 * 4)) || (rc = dalloc(c, &gzx, (size_t)N * 2 * 4)) ||
+        (rc = dalloc(c, &st, sizeof(LassoState))))
         return rc;
     std::unique_ptr<float, decltype(&cudaFree)> g1(zx, &cudaFree), g2(gzx, &cudaFree);
     std::unique_ptr<LassoState, decltype(&cudaFree)> g3(st, &cudaFree);
@@ -2606,7 +2466,7 @@ int cimcs_mri_lasso(cimcs_ctx* c, double lambda, int32_t max_iters, double tol, 
         CK(cudaStreamSynchronize(c->stream));
     }
     std::vector<float> h((size_t)N * 2);
-    CK(cudaMemcpy(h.data(), zx, h.size() * 4, cudaMemcpyDeviceToHost));
+    if (int rc_ = copy_sync(c, h.data(), zx, h.size() * 4, cudaMemcpyDeviceToHost)) return rc_;
     for (int i = 0; i < N; ++i) x_out[i] = h[2 * i + 1];
     if (iterations) *iterations = hs.it;
     if (objective) *objective = hs.f;
@@ -2667,7 +2527,7 @@ int cimcs_set_mri_problem(cimcs_ctx* c, int32_t H, int32_t W, const double* targ
     c->B = 1;
     c->N = N;
     c->ldN = c->ldJ = (N + 31) / 32 * 32;
-    c->tc = c->sym = c->fac = false;
+    c->tc = c->sym = false;
     c->RB = kSyT;
     c->row0 = 0;
     c->row1 = N;
@@ -2697,12 +2557,12 @@ int cimcs_set_mri_problem(cimcs_ctx* c, int32_t H, int32_t W, const double* targ
     std::vector<float> tgt((size_t)N);
     for (int k = 0; k < N; ++k) tgt[k] = (float)target[k];
     int rc;
-    if ((rc = dalloc(&c->dMaskBr, (size_t)N)) || (rc = dalloc(&c->dTw, tw.size() * sizeof(float2))) ||
-        (rc = dalloc(&c->dTarget, (size_t)N * 4)))
+    if ((rc = dalloc(c, &c->dMaskBr, (size_t)N)) || (rc = dalloc(c, &c->dTw, tw.size() * sizeof(float2))) ||
+        (rc = dalloc(c, &c->dTarget, (size_t)N * 4)))
         return rc;
-    CK(cudaMemcpy(c->dMaskBr, br.data(), br.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->dTw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->dTarget, tgt.data(), tgt.size() * 4, cudaMemcpyHostToDevice));
+    if (int rc_ = copy_sync(c, c->dMaskBr, br.data(), br.size(), cudaMemcpyHostToDevice)) return rc_;
+    if (int rc_ = copy_sync(c, c->dTw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice)) return rc_;
+    if (int rc_ = copy_sync(c, c->dTarget, tgt.data(), tgt.size() * 4, cudaMemcpyHostToDevice)) return rc_;
     static std::atomic<unsigned long long> attr{0};
     if (!(attr.load() >> c->device & 1ull)) {
         CK(cudaFuncSetAttribute(mri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2712,12 +2572,12 @@ int cimcs_set_mri_problem(cimcs_ctx* c, int32_t H, int32_t W, const double* targ
         attr.fetch_or(1ull << c->device);
     }
     if (c->has_truth) {  // make_problem(t, &truth): xi = (x != 0) (mri.cpp:398-405)
-        if ((rc = dalloc(&c->dx, (size_t)c->ldN * 8)) || (rc = dalloc(&c->dxi, (size_t)c->ldN)))
+        if ((rc = dalloc(c, &c->dx, (size_t)c->ldN * 8)) || (rc = dalloc(c, &c->dxi, (size_t)c->ldN)))
             return rc;
         std::vector<int8_t> xi8((size_t)c->ldN, 0);
         for (int i = 0; i < N; ++i) xi8[i] = x_true[i] != 0.0 ? 1 : 0;
-        CK(cudaMemcpy(c->dx, x_true, (size_t)N * 8, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(c->dxi, xi8.data(), xi8.size(), cudaMemcpyHostToDevice));
+        if (int rc_ = copy_sync(c, c->dx, x_true, (size_t)N * 8, cudaMemcpyHostToDevice)) return rc_;
+        if (int rc_ = copy_sync(c, c->dxi, xi8.data(), xi8.size(), cudaMemcpyHostToDevice)) return rc_;
     }
     return 0;
 }
@@ -2728,8 +2588,8 @@ int cimcs_build_coupling(cimcs_ctx* c) {
     if (c->mri) {  // hz = Re(A^H y) and diag(G) of the transform chain (mri.cpp:236-254)
         int rc;
         const size_t nv = (size_t)c->ldN;
-        if (!c->dhz && (rc = dalloc(&c->dhz, nv * 4))) return rc;
-        if (!c->dD && (rc = dalloc(&c->dD, nv * 4))) return rc;
+        if (!c->dhz && (rc = dalloc(c, &c->dhz, nv * 4))) return rc;
+        if (!c->dD && (rc = dalloc(c, &c->dD, nv * 4))) return rc;
         Events ev(2);
         cudaEventRecord(ev.ev[0], c->stream);
         CK(cudaMemsetAsync(c->dhz, 0, nv * 4, c->stream));
@@ -2746,38 +2606,17 @@ int cimcs_build_coupling(cimcs_ctx* c) {
     }
     const size_t es = c->elt();
     // gram bytes: symmetric fp16 hi/lo tiles, canonical tf32 panels, or CUDA-core panels
-    const size_t gbytes = c->fac ? (size_t)c->B * c->nMB * c->nRB * 2 * kSyPlaneBytes
-                          : c->sym ? (size_t)c->B * c->ntri * 2 * kSyPlaneBytes
-                          : c->tc ? (size_t)c->B * c->nRB * c->nch * kTcTileFloats * es
+    const size_t gbytes = c->sym ? (size_t)c->B * c->ntri * 2 * kSyPlaneBytes
                                   : (size_t)c->B * c->nRB * c->ldJ * c->RB * es;
     const size_t nv = (size_t)c->B * c->ldN;
     int rc;
-    if (!c->dG && (rc = dalloc(&c->dG, gbytes))) return rc;
-    if (!c->dhz && (rc = dalloc(&c->dhz, nv * es))) return rc;
-    if (!c->dD && (rc = dalloc(&c->dD, nv * es))) return rc;
-    if (c->sym && !c->dSg && (rc = dalloc(&c->dSg, c->B * 4))) return rc;
-    if (c->fac) {
-        // task table: phase 1 of instance b + skew is interleaved with phase 2 of b
-        const int nP1 = c->nMB, nP2 = (c->nRB + c->fac_w2 - 1) / c->fac_w2;
-        const int k = std::min(c->fac_skew, c->B);
-        std::vector<int> tab;
-        auto p1 = [&](int b) { for (int i = 0; i < nP1; ++i) tab.push_back(fa_task(0, b, i)); };
-        for (int b = 0; b < k; ++b) p1(b);
-        for (int b = 0; b < c->B; ++b) {
-            for (int i = 0; i < nP2; ++i) tab.push_back(fa_task(1, b, i));
-            if (b + k < c->B) p1(b + k);
-        }
-        c->ntask = (int)tab.size();
-        if (c->dTask) cudaFree(c->dTask);
-        c->dTask = nullptr;
-        if ((rc = dalloc(&c->dTask, tab.size() * 4))) return rc;
-        CK(cudaMemcpy(c->dTask, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
-        if (!c->dCnt && (rc = dalloc(&c->dCnt, (size_t)c->B * 2 * 4))) return rc;
-        CK(cudaMemsetAsync(c->dCnt, 0, (size_t)c->B * 2 * 4, c->stream));
-    }
+    if (!c->dG && (rc = dalloc(c, &c->dG, gbytes))) return rc;
+    if (!c->dhz && (rc = dalloc(c, &c->dhz, nv * es))) return rc;
+    if (!c->dD && (rc = dalloc(c, &c->dD, nv * es))) return rc;
+    if (c->sym && !c->dSg && (rc = dalloc(c, &c->dSg, c->B * 4))) return rc;
     Events ev(2);
     cudaEventRecord(ev.ev[0], c->stream);
-    if (!c->fac) CK(cudaMemsetAsync(c->dG, 0, gbytes, c->stream));
+    CK(cudaMemsetAsync(c->dG, 0, gbytes, c->stream));
     const int nt = (c->N + kG2T - 1) / kG2T;
     const int bi0 = c->row0 / kG2T;
     const int nti = c->world == 1 ? nt : (c->row1 - c->row0 + kG2T - 1) / kG2T;
@@ -2785,7 +2624,7 @@ int cimcs_build_coupling(cimcs_ctx* c) {
     const size_t astride = (size_t)c->Mmax * c->N;
     // hz = A^T y, D = diag(G) first: the symmetric tiles are scaled by max D
     const dim3 g2((c->N + 127) / 128, c->B);
-    if (c->dtype == CIMCS_F64)
+    if (c->st64())
         hz_diag_kernel<double><<<g2, 128, 0, c->stream>>>(
             c->dA, c->dy, c->dM, c->N, c->ldN, astride, c->Mmax, static_cast<double*>(c->dhz),
             static_cast<double*>(c->dD), c->B);
@@ -2794,20 +2633,18 @@ int cimcs_build_coupling(cimcs_ctx* c) {
             c->dA, c->dy, c->dM, c->N, c->ldN, astride, c->Mmax, static_cast<float*>(c->dhz),
             static_cast<float*>(c->dD), c->B);
     CK(cudaGetLastError());
-    if (c->fac) {
-        fac_scale_kernel<<<c->B, 1024, 0, c->stream>>>(c->dA, c->dM, c->N, astride, c->dSg);
-        fac_tiles_kernel<<<16 * c->num_sms, 256, 0, c->stream>>>(
-            c->dA, c->dM, c->N, astride, c->nMB, c->nRB, c->dSg, static_cast<__half*>(c->dG),
-            c->B);
-        CK(cudaGetLastError());
-    } else if (c->sym) {
-        sym_scale_kernel<<<c->B, 256, 0, c->stream>>>(static_cast<const float*>(c->dD), c->N,
-                                                     c->ldN, c->dSg);
+    if (c->sym) {
+        if (c->st64())
+            sym_scale_kernel<double><<<c->B, 256, 0, c->stream>>>(
+                static_cast<const double*>(c->dD), c->N, c->ldN, c->dSg);
+        else
+            sym_scale_kernel<float><<<c->B, 256, 0, c->stream>>>(
+                static_cast<const float*>(c->dD), c->N, c->ldN, c->dSg);
         CK(cudaGetLastError());
     }
     // large instances on the symmetric path: G = A^T A by cuBLAS DGEMM over panels
     // of 8 row blocks (upper triangle only), converted to the fp16 hi/lo tiles
-    const bool blas = c->sym && !c->fac && (c->gram_blas > 0 || (c->gram_blas == 0 && c->N >= 8192));
+    const bool blas = c->sym && (c->gram_blas > 0 || (c->gram_blas == 0 && c->N >= 8192));
     if (blas) {
         if (!c->blas) {
             if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS)
@@ -2825,10 +2662,10 @@ int cimcs_build_coupling(cimcs_ctx* c) {
             reinterpret_cast<SetEmu>(dlsym(RTLD_DEFAULT, "cublasSetEmulationStrategy"));
         bool emu = (c->gram_emu > 0 || (c->gram_emu < 0 && c->N >= 32768)) && set_emu != nullptr;
         void* Pv = nullptr;  // sized for fp64 panels: the DGEMM route may take over mid-build
-        if ((rc = dalloc(reinterpret_cast<char**>(&Pv), (size_t)ldp * c->N * 8))) return rc;
+        if ((rc = dalloc(c, reinterpret_cast<char**>(&Pv), (size_t)ldp * c->N * 8))) return rc;
         std::unique_ptr<void, decltype(&cudaFree)> pguard(Pv, &cudaFree);
         float* A32 = nullptr;
-        if (emu && (rc = dalloc(&A32, (size_t)c->Mmax * c->N * 4))) return rc;
+        if (emu && (rc = dalloc(c, &A32, (size_t)c->Mmax * c->N * 4))) return rc;
         c->timing_gram_emu = emu;
         std::unique_ptr<float, decltype(&cudaFree)> aguard(A32, &cudaFree);
         if (emu && set_emu(c->blas, CUBLAS_EMULATION_STRATEGY_EAGER) != CUBLAS_STATUS_SUCCESS)
@@ -2873,7 +2710,7 @@ int cimcs_build_coupling(cimcs_ctx* c) {
         CK(cudaStreamSynchronize(c->stream));  // P is freed on return
     }
     // one launch per run of equal M (instances of a phase grid differ in M)
-    for (int b = 0; b < c->B && !blas && !c->fac;) {
+    for (int b = 0; b < c->B && !blas;) {
         int e = b;
         while (e < c->B && c->M[e] == c->M[b]) ++e;
         const dim3 grid(nt, nti, e - b);
@@ -2886,11 +2723,7 @@ int cimcs_build_coupling(cimcs_ctx* c) {
             SymOut o{static_cast<__half*>(c->dG) + (size_t)b * c->ntri * 2 * kSyPlaneHalfs,
                      c->dSg + b, c->nRB, c->ntri};
             gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o, bi0, mirror);
-        } else if (c->tc) {
-            TcPanelOut o{static_cast<float*>(c->dG) + (size_t)b * c->nRB * c->nch * kTcTileFloats,
-                         c->nRB, c->nch, c->row0};
-            gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o, bi0, mirror);
-        } else if (c->dtype == CIMCS_F64) {
+        } else if (c->st64()) {
             PanelOut<double, row_block<double>()> o{
                 static_cast<double*>(c->dG) + (size_t)b * c->nRB * c->ldJ * c->RB, c->ldJ, c->nRB,
                 c->row0};
@@ -2920,13 +2753,15 @@ int cimcs_get_coupling(cimcs_ctx* c, int32_t b, double* G, double* hz, double* D
     const size_t gstride = (size_t)c->nRB * ldJ * RB;
     auto fetch = [&](const void* d, size_t off, size_t n, std::vector<double>& h) -> int {
         h.resize(n);
-        if (c->dtype == CIMCS_F64) {
-            CK(cudaMemcpy(h.data(), static_cast<const double*>(d) + off, n * 8,
-                          cudaMemcpyDeviceToHost));
+        if (c->st64()) {
+            if (int rc_ = copy_sync(c, h.data(), static_cast<const double*>(d) + off, n * 8,
+                                    cudaMemcpyDeviceToHost))
+                return rc_;
         } else {
             std::vector<float> f(n);
-            CK(cudaMemcpy(f.data(), static_cast<const float*>(d) + off, n * 4,
-                          cudaMemcpyDeviceToHost));
+            if (int rc_ = copy_sync(c, f.data(), static_cast<const float*>(d) + off, n * 4,
+                                    cudaMemcpyDeviceToHost))
+                return rc_;
             for (size_t k = 0; k < n; ++k) h[k] = f[k];
         }
         return 0;
@@ -2934,34 +2769,20 @@ int cimcs_get_coupling(cimcs_ctx* c, int32_t b, double* G, double* hz, double* D
     std::vector<double> h;
     if (G && c->mri) {  // never stored: the columns G e_r of the transform chain
         float* P = nullptr;
-        if (int rc = dalloc(&P, (size_t)N * N * 4)) return rc;
+        if (int rc = dalloc(c, &P, (size_t)N * N * 4)) return rc;
         std::unique_ptr<float, decltype(&cudaFree)> pguard(P, &cudaFree);
         if (int rc = mri_launch(c, MRI_COLS, N, 0, nullptr, P)) return rc;
-        CK(cudaStreamSynchronize(c->stream));  // c->stream does not sync with cudaMemcpy
         std::vector<float> f((size_t)N * N);
-        CK(cudaMemcpy(f.data(), P, f.size() * 4, cudaMemcpyDeviceToHost));
+        if (int rc_ = copy_sync(c, f.data(), P, f.size() * 4, cudaMemcpyDeviceToHost)) return rc_;
         for (size_t k = 0; k < f.size(); ++k) G[k] = f[k];
-    } else if (G && c->fac) {  // not stored: G = A^T A in fp64 (cuBLAS) from the resident A
-        if (!c->blas && cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS)
-            return fail(CIMCS_CUDA_ERROR, "cublasCreate failed");
-        cublasSetStream(c->blas, c->stream);
-        double* P = nullptr;
-        if (int rc = dalloc(&P, (size_t)N * N * 8)) return rc;
-        std::unique_ptr<double, decltype(&cudaFree)> pguard(P, &cudaFree);
-        const double one = 1.0, zero = 0.0;
-        const double* Ab = c->dA + (size_t)b * c->Mmax * N;
-        if (cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, N, N, c->M[b], &one, Ab, c->M[b], Ab,
-                        c->M[b], &zero, P, N) != CUBLAS_STATUS_SUCCESS)
-            return fail(CIMCS_CUDA_ERROR, "cublasDgemm failed");
-        CK(cudaMemcpyAsync(G, P, (size_t)N * N * 8, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));  // symmetric: column-major == row-major
     } else if (G && c->sym) {
         const size_t nh = (size_t)c->ntri * 2 * kSyPlaneHalfs;
         std::vector<__half> t(nh);
         int sg = 0;
-        CK(cudaMemcpy(t.data(), static_cast<const __half*>(c->dG) + (size_t)b * nh, nh * 2,
-                      cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(&sg, c->dSg + b, 4, cudaMemcpyDeviceToHost));
+        if (int rc_ = copy_sync(c, t.data(), static_cast<const __half*>(c->dG) + (size_t)b * nh,
+                                nh * 2, cudaMemcpyDeviceToHost))
+            return rc_;
+        if (int rc_ = copy_sync(c, &sg, c->dSg + b, 4, cudaMemcpyDeviceToHost)) return rc_;
         for (int i = 0; i < N; ++i)
             for (int j = 0; j < N; ++j) {
                 int r = i, q = j;  // stored upper triangle: G[i][j] = G[j][i]
@@ -2971,11 +2792,6 @@ int cimcs_get_coupling(cimcs_ctx* c, int32_t b, double* G, double* hz, double* D
                 const double v = (double)__half2float(t[o]) + (double)__half2float(t[o + kSyPlaneHalfs]);
                 G[(size_t)i * N + j] = std::ldexp(v, -sg);
             }
-    } else if (G && c->tc) {
-        const size_t ts = (size_t)c->nRB * c->nch * kTcTileFloats;
-        if (int rc = fetch(c->dG, (size_t)b * ts, ts, h)) return rc;
-        for (int i = 0; i < N; ++i)
-            for (int j = 0; j < N; ++j) G[(size_t)i * N + j] = h[tc_gofs(c->nRB, c->nch, 0, i, j)];
     } else if (G) {
         if (int rc = fetch(c->dG, (size_t)b * gstride, gstride, h)) return rc;
         for (int i = 0; i < N; ++i)
@@ -3009,7 +2825,7 @@ int cimcs_mfz_step(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* 
     if (int rc = upload_traj(c, Rsig, c->Rs, R)) return rc;
     // c and e go through a second staging area (the init kernel reads host layout)
     double* dce = nullptr;
-    if (int rc = dalloc(&dce, 2 * n * 8)) return rc;
+    if (int rc = dalloc(c, &dce, 2 * n * 8)) return rc;
     CK(cudaMemcpyAsync(dce, cin, n * 8, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(dce + n, ein, n * 8, cudaMemcpyHostToDevice, c->stream));
     const StepScalars s = make_scalars(hp);
@@ -3120,7 +2936,7 @@ int cimcs_run_cim(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* h
     if (int rc = set_alt(c, make_alt(hp, eta, 0))) return rc;
     if (int rc = upload_traj(c, Rsig, c->Rs, R)) return rc;
     double* dc0 = nullptr;
-    if (int rc = dalloc(&dc0, n * 8)) return rc;
+    if (int rc = dalloc(c, &dc0, n * 8)) return rc;
     CK(cudaMemcpyAsync(dc0, c0, n * 8, cudaMemcpyHostToDevice, c->stream));
     const StepScalars s = make_scalars(hp);
     Events ev(2);
@@ -3179,7 +2995,7 @@ int cimcs_cdp_minimize(cimcs_ctx* c, int32_t R, const int32_t* sigma, const doub
     if (int rc = upload_traj(c, R_prev, c->Rs, R)) return rc;
     if (int rc = upload_sig(c, sigma, c->sig, R)) return rc;
     const StepScalars s = make_scalars(hp);
-    int rc = c->dtype == CIMCS_F64 ? mask_T<double>(c, c->W0) : mask_T<float>(c, c->W0);
+    int rc = c->st64() ? mask_T<double>(c, c->W0) : mask_T<float>(c, c->W0);
     Events ev(2);
     cudaEventRecord(ev.ev[0], c->stream);
     if (!rc)
@@ -3226,7 +3042,7 @@ int cimcs_score(cimcs_ctx* c, int32_t R, const double* Rsig, const int32_t* sigm
     cimcs_hyper h;
     cimcs_hyper_default(&h);
     const StepScalars s = make_scalars(&h);
-    int rc = c->dtype == CIMCS_F64 ? mask_T<double>(c, c->W0) : mask_T<float>(c, c->W0);
+    int rc = c->st64() ? mask_T<double>(c, c->W0) : mask_T<float>(c, c->W0);
     if (!rc) rc = enqueue_score(c, s, 0, nullptr, false);
     const int nT = c->B * c->NR;
     std::vector<double> o(nT), r(nT), h_(nT);
@@ -3276,7 +3092,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
     if (c->hist_cap < nalt * nT) {
         if (c->hist) cudaFree(c->hist);
         c->hist = nullptr;
-        if (int rc = dalloc(&c->hist, (size_t)nalt * nT * sizeof(DevRecord))) return rc;
+        if (int rc = dalloc(c, &c->hist, (size_t)nalt * nT * sizeof(DevRecord))) return rc;
         c->hist_cap = nalt * nT;
     }
     const int bn = backend == CIMCS_MFZ_BN;
@@ -3298,7 +3114,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
         if (c->dc0) cudaFree(c->dc0);
         c->dc0 = nullptr;
         drop_graphs(c);  // the CIM graph reads dc0
-        if (int rc = dalloc(&c->dc0, nc0 * 8)) return rc;
+        if (int rc = dalloc(c, &c->dc0, nc0 * 8)) return rc;
         c->dc0_elems = nc0;
     }
     double* pinned = c->pin_c0;
@@ -3321,7 +3137,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
         if (R_init)
             rc = upload_traj(c, R_init, c->Rs, R);
         else
-            rc = c->dtype == CIMCS_F64 ? rinit_hz_T<double>(c, R) : rinit_hz_T<float>(c, R);
+            rc = c->st64() ? rinit_hz_T<double>(c, R) : rinit_hz_T<float>(c, R);
     }
     if (rc) return rc;
     CK(cudaMemsetAsync(c->sig, 0, c->state_elems(), c->stream));
@@ -3440,7 +3256,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
             CK(cudaMemcpyAsync(c->improved, imp.data(), nT * 4, cudaMemcpyHostToDevice,
                                c->stream));
             const int g = grid_for(c->state_elems());
-            if (c->dtype == CIMCS_F64) {
+            if (c->st64()) {
                 DISPATCH_NR(NR, {
                     best_update_kernel<double, NR_><<<g, 256, 0, c->stream>>>(
                         c->improved, static_cast<const double*>(c->Rs), c->sig,
@@ -3467,7 +3283,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
     CK(cudaMemcpyAsync(fi.data(), c->fail_idx, nT * 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     int err = 0;
-    CK(cudaMemcpy(&err, c->err, 4, cudaMemcpyDeviceToHost));
+    if (int rc_ = copy_sync(c, &err, c->err, 4, cudaMemcpyDeviceToHost)) return rc_;
     if (err != 0x7f7f7f7f && err != INT_MAX)
         return fail(CIMCS_INPUT_ERROR,
                     "jacobi_solve: singular diagonal at active index " + std::to_string(err));
@@ -3484,11 +3300,12 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
     // score contraction, tp, finalize, median (+ best).  The small-N cluster loop
     // runs a whole CIM call / refit in one launch; CG counts its last iteration total.
     const bool cl = cluster_ok(c) && !pp;
-    const int per = c->sym && !c->fac ? 2 : 1;  // symmetric path: tile kernel + update kernel
+    const int per = c->sym ? 2 : 1;  // symmetric path: tile kernel + update kernel
     tm.step_launches = (int64_t)nalt * (cl ? 1 : per * hp->n_steps + (pp ? 1 : 0));
     if (cdp == CIMCS_CDP_CG) {
         std::vector<CgTraj> st(nT);
-        cudaMemcpy(st.data(), c->cg_st, nT * sizeof(CgTraj), cudaMemcpyDeviceToHost);
+        if (int rc_ = copy_sync(c, st.data(), c->cg_st, nT * sizeof(CgTraj), cudaMemcpyDeviceToHost))
+            return rc_;
         int mx = 0;
         for (const CgTraj& t : st) mx = std::max(mx, t.it);
         tm.refit_launches = (int64_t)nalt * (6 + 3 * (int64_t)mx);

@@ -27,7 +27,7 @@
 // A second, evenly spread kernel (sym_update_kernel, one CTA per block, 4
 // replicas per thread) sums the slots in a FIXED order (deterministic) and runs
 // the fused Euler / Jacobi / score / matvec update (the arithmetic of
-// tc_row_update); no CTA waits for another.
+// tc_row_update of round 1); no CTA waits for another.
 // (Fusing the finish into the tile kernel -- last-arriving CTA, or owner-CTA
 // finisher warps with an L2-resident ring of partials -- was measured slower:
 // each finish is a chain of dependent L2 round trips behind the tile stream.)
@@ -121,10 +121,11 @@ __global__ void sym_panel_kernel(const PT* __restrict__ P, int ldp, int I0, int 
 }
 
 // s_G[b]: max |G| (= max diag) * 2^s_G in [2^14, 2^15)
-__global__ void sym_scale_kernel(const float* __restrict__ D, int N, int ldN, int* sg) {
+template <typename TS>
+__global__ void sym_scale_kernel(const TS* __restrict__ D, int N, int ldN, int* sg) {
     const int b = blockIdx.x;
     float m = 0.f;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) m = fmaxf(m, fabsf(D[(size_t)b * ldN + i]));
+    for (int i = threadIdx.x; i < N; i += blockDim.x) m = fmaxf(m, fabsf((float)D[(size_t)b * ldN + i]));
     for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
     __shared__ float s[32];
     if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
@@ -226,15 +227,30 @@ __device__ __forceinline__ SyItem sy_item(const SymArgs& sa, int k, int nRB) {
     return r;
 }
 
+// fp16 hi/lo split of w * 2^e (e from the per-replica block max): exact scaling,
+// rounded to nearest in both halves; the fp64 state of F32X contexts is split
+// from its double value
+__device__ __forceinline__ void sy_split(float w, int e, __half& hi, __half& lo) {
+    const float ws = w * sy_pow2(e);
+    hi = __float2half_rn(ws);
+    lo = __float2half_rn(ws - __half2float(hi));
+}
+__device__ __forceinline__ void sy_split(double w, int e, __half& hi, __half& lo) {
+    const double ws = ldexp(w, e);
+    hi = __double2half(ws);
+    lo = __double2half(ws - (double)__half2float(hi));
+}
+
 // fp16 B tile + scales of one 128-row block from the values w[q] of row k
 // (called by all 128 threads of a group synchronised on named barrier `bar`).
-template <int NR>
-__device__ __forceinline__ void sy_emit_block(const float (&w)[NR], int k, int lane, int wq,
+template <int NR, typename TS>
+__device__ __forceinline__ void sy_emit_block(const TS (&w)[NR], int k, int lane, int wq,
                                               unsigned (*s_max)[NR], __half* WB, int* WS,
                                               int bar) {
 #pragma unroll
     for (int q = 0; q < NR; ++q) {
-        const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(w[q])));
+        const unsigned m =
+            __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf((float)w[q])));
         if (lane == 0) s_max[wq][q] = m;
     }
     asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
@@ -242,9 +258,8 @@ __device__ __forceinline__ void sy_emit_block(const float (&w)[NR], int k, int l
     for (int q = 0; q < NR; ++q) {
         const unsigned m = max(max(s_max[0][q], s_max[1][q]), max(s_max[2][q], s_max[3][q]));
         const int e = sy_exp14(__uint_as_float(m));
-        const float ws = w[q] * sy_pow2(e);
-        const __half hi = __float2half_rn(ws);
-        const __half lo = __float2half_rn(ws - __half2float(hi));
+        __half hi, lo;
+        sy_split(w[q], e, hi, lo);
         unsigned char* B = reinterpret_cast<unsigned char*>(WB);
         *reinterpret_cast<__half*>(B + sy_offk(q, k, 2 * NR)) = hi;
         *reinterpret_cast<__half*>(B + sy_offk(NR + q, k, 2 * NR)) = lo;
@@ -253,23 +268,20 @@ __device__ __forceinline__ void sy_emit_block(const float (&w)[NR], int k, int l
     asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");  // s_max reusable
 }
 
-// B tiles of a whole fp32 W array ([W | W_lo] canonical) -- after any writer of
-// W other than the symmetric kernel (init, support, mask, CG).
-template <int NR>
-__global__ void __launch_bounds__(128) sym_wconvert_kernel(const float* __restrict__ W, int N,
-                                                           int ldJ, int ldN, int canon, int nRB,
-                                                           __half* WB, int* WS) {
+// B tiles of a whole W array [b][i][r] -- after any writer of W other than
+// the symmetric update kernel (init, support, mask, CG).
+template <int NR, typename TS>
+__global__ void __launch_bounds__(128) sym_wconvert_kernel(const TS* __restrict__ W, int N,
+                                                           int ldN, int nRB, __half* WB, int* WS) {
     __shared__ unsigned s_max[4][NR];
     const int X = blockIdx.x, b = blockIdx.y, k = threadIdx.x;
     const int j = X * kSyT + k;
-    float w[NR];
+    TS w[NR];
 #pragma unroll
-    for (int q = 0; q < NR; ++q)
-        w[q] = j >= N ? 0.f
-                      : (canon ? W[tc_wofs(ldJ, NR, b, j, q)] : W[((size_t)b * ldN + j) * NR + q]);
-    sy_emit_block<NR>(w, k, k & 31, k >> 5, s_max,
-                      WB + ((size_t)b * nRB + X) * (2 * NR * kSyT),
-                      WS + ((size_t)b * nRB + X) * NR, 1);
+    for (int q = 0; q < NR; ++q) w[q] = j >= N ? TS(0) : W[((size_t)b * ldN + j) * NR + q];
+    sy_emit_block<NR, TS>(w, k, k & 31, k >> 5, s_max,
+                          WB + ((size_t)b * nRB + X) * (2 * NR * kSyT),
+                          WS + ((size_t)b * nRB + X) * NR, 1);
 }
 
 template <int NR, int MODE>
@@ -506,24 +518,58 @@ __global__ void __launch_bounds__(kSyT * NR / 4) sym_slotsum_kernel(const float*
     reinterpret_cast<float4*>(H + (((size_t)b * nRB + K) * kSyT + row) * NR)[g] = acc;
 }
 
+// 4 consecutive state values (one thread's replicas q0..q0+3) in the state type
+__device__ __forceinline__ void sy_ld4(const float* p, float (&v)[4]) {
+    const float4 x = *reinterpret_cast<const float4*>(p);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+}
+__device__ __forceinline__ void sy_ld4(const double* p, double (&v)[4]) {
+    const double2 x = reinterpret_cast<const double2*>(p)[0], y = reinterpret_cast<const double2*>(p)[1];
+    v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y;
+}
+__device__ __forceinline__ void sy_ldg4(const float* p, float (&v)[4]) {
+    const float4 x = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+}
+__device__ __forceinline__ void sy_ldg4(const double* p, double (&v)[4]) {
+    const double2 x = __ldg(reinterpret_cast<const double2*>(p)),
+                  y = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y;
+}
+__device__ __forceinline__ void sy_st4(float* p, const float (&v)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void sy_st4(double* p, const double (&v)[4]) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
+    reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
+}
+
 // Second pass of a step in ONE kernel, 4 replicas per thread: block (b, K) is
 // handled by 128 x (NR / 4) threads; thread (row, g), g = t % (NR / 4) fastest
-// so a warp reads whole 64-byte state rows (coalesced float4), sums its 4
-// replicas' nSB partial products in slot order (deterministic), runs the fused
-// update of tc_row_update for replicas 4g..4g+3 and, in step / Jacobi modes,
-// emits the fp16 B tile of the new w (staged in shared memory, stored with
-// 16-byte vectors).
-template <int NR, int MODE>
+// so a warp reads whole state rows (coalesced 16-byte vectors), sums its 4
+// replicas' nSB partial products in slot order (deterministic, fp32), runs the
+// fused update for replicas 4g..4g+3 in the state type TS (float: F32 contexts;
+// double: F32X, the fp64-state mode) and, in step / Jacobi modes, emits the fp16
+// B tile of the new w (staged in shared memory, stored with 16-byte vectors).
+template <int NR, int MODE, typename TS = float>
 __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_update_kernel(SymArgs sa) {
     constexpr int QG = NR / 4;
     constexpr int NW = kSyT * QG / 32;         // warps per CTA
     __shared__ unsigned s_max[NW][NR];          // per warp, per replica max |w|
     __shared__ int s_exp[NR];
-    __shared__ float s_min[NW][NR];             // per warp, per replica min e (step modes)
+    __shared__ TS s_min[NW][NR];                // per warp, per replica min e (step modes)
     __shared__ double s_sc[NW][NR][3];          // score partials
     __shared__ __align__(16) __half s_B[2 * NR * kSyT];
     const TcArgs& a = sa.t;
     const StepScalars& sc = a.s;
+    const TS* __restrict__ Dp = static_cast<const TS*>(a.D);
+    const TS* __restrict__ Hp = static_cast<const TS*>(a.hz);
+    const TS* __restrict__ Win = static_cast<const TS*>(a.Win);
+    TS* __restrict__ Wout = static_cast<TS*>(a.Wout);
+    TS* __restrict__ Rp = static_cast<TS*>(a.Rs);
+    TS* __restrict__ Cp = static_cast<TS*>(a.C);
+    TS* __restrict__ Ep = static_cast<TS*>(a.E);
+    TS* __restrict__ Hd = static_cast<TS*>(a.Hdbg);
     const int K = blockIdx.x, b = sa.b0 + blockIdx.y, nRB = a.nRB, N = a.N;
     const int t = threadIdx.x, g = t % QG, row = t / QG;
     const int lane = t & 31, wid = t >> 5;
@@ -532,21 +578,22 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
     const size_t si = (size_t)b * a.ldN + i, vi0 = si * NR + q0;
     sy_pdl_wait();  // the tile kernel's partial products
     // state of the step modes first: its loads are in flight with the slot loads
-    float4 st_r = make_float4(0.f, 0.f, 0.f, 0.f), st_c = st_r, st_e = st_r;
-    float st_D = 0.f, st_hz = 0.f;
+    TS Rv[4] = {TS(0), TS(0), TS(0), TS(0)}, cv[4] = {TS(0), TS(0), TS(0), TS(0)};
+    TS ev[4] = {TS(0), TS(0), TS(0), TS(0)};
+    TS st_D = TS(0), st_hz = TS(0);
     if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
         if (valid) {
             // the input w is never loaded: in step modes it is a function of the
             // stored c and R (init_state_kernel and every update write them so)
-            st_r = __ldg(reinterpret_cast<const float4*>(a.Rs + vi0));
-            st_c = *reinterpret_cast<const float4*>(a.C + vi0);
-            st_e = *reinterpret_cast<const float4*>(a.E + vi0);
-            st_D = __ldg(a.D + si);
-            st_hz = __ldg(a.hz + si);
+            sy_ldg4(Rp + vi0, Rv);
+            sy_ld4(Cp + vi0, cv);
+            sy_ld4(Ep + vi0, ev);
+            st_D = __ldg(Dp + si);
+            st_hz = __ldg(Hp + si);
         }
     }
-    // ---- slot sums
-    float gw[4];
+    // ---- slot sums (fp32, fixed slot order)
+    TS gw[4];
     {
         const int nSB = sa.nSB;
         const float4* src = reinterpret_cast<const float4*>(
@@ -568,7 +615,7 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
                     acc.w = acc.w + v[u].w;
                 }
         }
-        gw[0] = acc.x; gw[1] = acc.y; gw[2] = acc.z; gw[3] = acc.w;
+        gw[0] = (TS)acc.x; gw[1] = (TS)acc.y; gw[2] = (TS)acc.z; gw[3] = (TS)acc.w;
     }
     bool fz[4];
     const int4 fg4 = *reinterpret_cast<const int4*>(a.fail_gstep + b * NR + q0);
@@ -579,37 +626,33 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
         fz[u] = (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) ? fg < a.alt->gstep_base + a.step
                                                              : fg != kFreeTraj;
     }
-    float wn[4] = {0.f, 0.f, 0.f, 0.f};  // new contraction input (0: frozen / padding)
+    TS wn[4] = {TS(0), TS(0), TS(0), TS(0)};  // new contraction input (0: frozen / padding)
     if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
-        float lmin[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+        TS lmin[4] = {TS(INFINITY), TS(INFINITY), TS(INFINITY), TS(INFINITY)};
         if (valid) {
-            const float4 r4 = st_r, c4 = st_c, e4 = st_e;
-            const float Rv[4] = {r4.x, r4.y, r4.z, r4.w}, cv[4] = {c4.x, c4.y, c4.z, c4.w};
-            const float ev[4] = {e4.x, e4.y, e4.z, e4.w};
-            const float Dv = st_D, hzv = st_hz;
-            const float half_rt = (float)sc.half_rt, rt = (float)sc.rt, dt = (float)sc.dt;
-            float wv[4];
+            const TS Dv = st_D, hzv = st_hz;
+            const TS half_rt = (TS)sc.half_rt, rt = (TS)sc.rt, dt = (TS)sc.dt;
+            TS wv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                wv[u] = MODE == EPI_STEP_BN ? Rv[u] * (cv[u] > 0.f ? 1.f : 0.f)
-                                            : (Rv[u] * 0.25f) * (cv[u] + rt);
-            const float Kj = (float)sc.Kj, nbeta = (float)sc.nbeta, tau = (float)sc.tau;
+                wv[u] = MODE == EPI_STEP_BN ? Rv[u] * (cv[u] > TS(0) ? TS(1) : TS(0))
+                                            : (Rv[u] * TS(0.25)) * (cv[u] + rt);
+            const TS Kj = (TS)sc.Kj, nbeta = (TS)sc.nbeta, tau = (TS)sc.tau;
             const double pd = a.pump ? a.pump[a.step] : a.p_scalar;
-            const float loss = sc.minus_j != 0.0 ? (float)((-1.0 + pd) - sc.minus_j)
-                                                 : (float)(-1.0 + pd);
-            const float thresh = (float)a.alt->thresh;
-            float cn[4], en[4], wo[4];
+            const TS loss = sc.minus_j != 0.0 ? (TS)((-1.0 + pd) - sc.minus_j) : (TS)(-1.0 + pd);
+            const TS thresh = (TS)a.alt->thresh;
+            TS cn[4], en[4], wo[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const float c = cv[u], e = ev[u];
-                const float Jw = Dv * wv[u] - gw[u];
-                float h;
+                const TS c = cv[u], e = ev[u];
+                const TS Jw = Dv * wv[u] - gw[u];
+                TS h;
                 if constexpr (MODE == EPI_STEP_BN)
                     h = half_rt * (Jw + hzv);
                 else
                     h = Jw + half_rt * hzv;
-                if (a.Hdbg) a.Hdbg[vi0 + u] = h;
-                const float inj = (Kj * e) * (Rv[u] * h - thresh);
+                if (Hd) Hd[vi0 + u] = h;
+                const TS inj = (Kj * e) * (Rv[u] * h - thresh);
                 cn[u] = c + dt * ((loss - c * c) * c + inj);
                 en[u] = e + dt * ((nbeta * (c * c - tau)) * e);
                 wo[u] = wv[u];  // frozen / failing trajectories keep their output w
@@ -623,58 +666,58 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
                     en[u] = e;
                 } else {
                     lmin[u] = en[u];
-                    float w;
+                    TS w;
                     if constexpr (MODE == EPI_STEP_BN)
-                        w = Rv[u] * (cn[u] > 0.f ? 1.f : 0.f);
+                        w = Rv[u] * (cn[u] > TS(0) ? TS(1) : TS(0));
                     else
-                        w = (Rv[u] * 0.25f) * (cn[u] + rt);
+                        w = (Rv[u] * TS(0.25)) * (cn[u] + rt);
                     wo[u] = w;
                     wn[u] = w;
                 }
             }
-            *reinterpret_cast<float4*>(a.C + vi0) = make_float4(cn[0], cn[1], cn[2], cn[3]);
-            *reinterpret_cast<float4*>(a.E + vi0) = make_float4(en[0], en[1], en[2], en[3]);
-            if (sa.keep_w)
-                *reinterpret_cast<float4*>(a.Wout + vi0) = make_float4(wo[0], wo[1], wo[2], wo[3]);
+            sy_st4(Cp + vi0, cn);
+            sy_st4(Ep + vi0, en);
+            if (sa.keep_w) sy_st4(Wout + vi0, wo);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {  // min e: warp, then CTA (one atomic per replica)
-            float m = lmin[u];
+            TS m = lmin[u];
 #pragma unroll
-            for (int off = 16; off >= QG; off >>= 1)
-                m = fminf(m, __shfl_xor_sync(0xffffffffu, m, off));
+            for (int off = 16; off >= QG; off >>= 1) {
+                const TS o = __shfl_xor_sync(0xffffffffu, m, off);
+                m = o < m ? o : m;
+            }
             if (lane < QG) s_min[wid][q0 + u] = m;
         }
     } else if constexpr (MODE == EPI_JACOBI) {
         if (valid) {
-            const float Dv = __ldg(a.D + si), bv = __ldg(a.hz + si);
-            const float omd = (float)sc.one_minus_dtc, dtc = (float)sc.dt_c;
-            float4 r4 = *reinterpret_cast<const float4*>(a.Rs + vi0);
-            const float4 w4 = *reinterpret_cast<const float4*>(a.Win + vi0);
-            float* Rv = &r4.x;
-            float wo[4] = {w4.x, w4.y, w4.z, w4.w};
+            const TS Dv = __ldg(Dp + si), bv = __ldg(Hp + si);
+            const TS omd = (TS)sc.one_minus_dtc, dtc = (TS)sc.dt_c;
+            TS Rj[4], wo[4];
+            sy_ld4(Rp + vi0, Rj);
+            sy_ld4(Win + vi0, wo);
             const char4 s4 = *reinterpret_cast<const char4*>(a.sigma + vi0);
             const bool on4[4] = {s4.x != 0, s4.y != 0, s4.z != 0, s4.w != 0};
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 if (fz[u]) continue;
                 const bool on = on4[u];
-                float rn = Rv[u];
+                TS rn = Rj[u];
                 if (on) {
-                    if (Dv == 0.f) {
+                    if (Dv == TS(0)) {
                         atomicMin(a.err, i);
                         continue;
                     }
-                    const float off = gw[u] - Dv * Rv[u];
-                    rn = omd * Rv[u] + dtc * ((bv - off) / Dv);
-                    Rv[u] = rn;
+                    const TS off = gw[u] - Dv * Rj[u];
+                    rn = omd * Rj[u] + dtc * ((bv - off) / Dv);
+                    Rj[u] = rn;
                 }
-                const float w = rn * (on ? 1.f : 0.f);
+                const TS w = rn * (on ? TS(1) : TS(0));
                 wo[u] = w;
                 wn[u] = w;
             }
-            *reinterpret_cast<float4*>(a.Rs + vi0) = r4;
-            *reinterpret_cast<float4*>(a.Wout + vi0) = make_float4(wo[0], wo[1], wo[2], wo[3]);
+            sy_st4(Rp + vi0, Rj);
+            sy_st4(Wout + vi0, wo);
         }
     } else if constexpr (MODE == EPI_MATVEC) {
         if (valid) {
@@ -684,16 +727,15 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
         }
     } else {  // EPI_SCORE: w.Gw, hz.w, |w - x|^2 partials of this 128-row block
         double pa[4], pb[4], pc[4];
-        float4 w4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid) w4 = *reinterpret_cast<const float4*>(a.Win + vi0);
-        const float wv4[4] = {w4.x, w4.y, w4.z, w4.w};
+        TS wv4[4] = {TS(0), TS(0), TS(0), TS(0)};
+        if (valid) sy_ld4(Win + vi0, wv4);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             pa[u] = pb[u] = pc[u] = 0.0;
             if (valid && !fz[u]) {
                 const double wv = wv4[u];
                 pa[u] = wv * (double)gw[u];
-                pb[u] = (double)a.hz[si] * wv;
+                pb[u] = (double)Hp[si] * wv;
                 if (a.xtrue) {
                     const double xt = a.xitrue[si] ? a.xtrue[si] : 0.0;
                     pc[u] = (wv - xt) * (wv - xt);
@@ -734,7 +776,7 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
         const bool emit = sa.WBout != nullptr;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            unsigned m = __float_as_uint(fabsf(wn[u]));
+            unsigned m = __float_as_uint(fabsf((float)wn[u]));
 #pragma unroll
             for (int off = 16; off >= QG; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
             if (lane < QG) s_max[wid][q0 + u] = m;
@@ -742,9 +784,9 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
         __syncthreads();
         if (t < NR) {
             if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
-                float mn = INFINITY;
-                for (int w = 0; w < NW; ++w) mn = fminf(mn, s_min[w][t]);
-                if (mn != INFINITY) atomicMin(&a.minE[b * NR + t], ord_key(mn));
+                TS mn = TS(INFINITY);
+                for (int w = 0; w < NW; ++w) mn = s_min[w][t] < mn ? s_min[w][t] : mn;
+                if (mn != TS(INFINITY)) atomicMin(&a.minE[b * NR + t], ord_key(mn));
             }
             unsigned m = 0;
             for (int w = 0; w < NW; ++w) m = max(m, s_max[w][t]);
@@ -760,9 +802,8 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
         unsigned char* Bs = reinterpret_cast<unsigned char*>(s_B);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const float ws = wn[u] * sy_pow2(s_exp[q0 + u]);
-            const __half hi = __float2half_rn(ws);
-            const __half lo = __float2half_rn(ws - __half2float(hi));
+            __half hi, lo;
+            sy_split(wn[u], s_exp[q0 + u], hi, lo);
             *reinterpret_cast<__half*>(Bs + sy_offk(q0 + u, row, 2 * NR)) = hi;
             *reinterpret_cast<__half*>(Bs + sy_offk(NR + q0 + u, row, 2 * NR)) = lo;
         }

@@ -114,14 +114,14 @@ def test_cg_python_solve(gpu, O):
 
 
 def test_cg_fp32_tensor_cores(gpu, O):
-    insts = [O.gen_instance(300, 0.6, 0.2, 0.01, 7)]
+    insts = [O.gen_instance(640, 0.6, 0.2, 0.01, 7)]
     p = O.Problem(insts[0], O.CANON)
     R = 16
-    sigma, Rp = _supports(1, R, 300, 13)
+    sigma, Rp = _supports(1, R, 640, 13)
     ctx = _ctx(gpu, insts, "f32", tensor_cores=1)
     out, its = ctx.refit(R, sigma, Rp, gpu.HyperParams(), cdp="cg", return_iterations=True)
     ctx.close()
-    assert its.max() < 10000  # the fp64 recursion converges on the tf32x3 operator
+    assert its.max() < 10000  # the fp64 recursion converges on the fp16 hi/lo operator
     for r in range(R):
         ref = p.cdp(sigma[0, r], Rp[0, r], O.CDP_CG, O.HyperParams())
         assert np.max(np.abs(out[0, r] - ref)) < 1e-4 * max(1.0, np.max(np.abs(ref)))

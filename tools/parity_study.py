@@ -12,15 +12,13 @@ import numpy as np
 import paper_2405_00366_b200 as P
 from paper_2405_00366_b200 import workloads as W
 
-variant = sys.argv[1] if len(sys.argv) > 1 else "sym"  # sym | stream | cudacore
+variant = sys.argv[1] if len(sys.argv) > 1 else "sym"  # sym | cudacore
 cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 1     # BASELINE config 1 or 2
 insts, R, hp, _ = W.config1() if cfg == 1 else W.config2()
 seeds = P.replica_seeds(insts, R, "mfz-bn")
 out = {}
 for dt in ("f64", "f32"):
     with P.Context(0, dt) as ctx:
-        if dt == "f32" and variant == "stream":
-            ctx.set_option("symmetric", 0)
         if dt == "f32" and variant == "cudacore":
             ctx.set_option("tensor_cores", 0)
         ctx.set_problems(insts)

@@ -33,8 +33,10 @@ def main():
     L.orc_set_perturb.argtypes = [O.C.c_int]
     threads = os.cpu_count() or 1
     runs = {}
-    names = {0: "fp64", 1: "field_f32", 2: "state_f32", 4: "refit_R_f32", 7: "all_f32"}
-    for mode in (0, 1, 2, 4, 7):
+    names = {0: "fp64", 1: "field_f32", 2: "state_f32", 4: "refit_R_f32", 7: "all_f32",
+             8: "field_noise_2^-20", 16: "field_noise_2^-16"}
+    modes = [int(m) for m in os.environ.get("MODES", "0,1,2,4,7,8,16").split(",")]
+    for mode in modes:
         L.orc_set_perturb(mode)
         t0 = time.perf_counter()
         _, R, S, FA = O.solve_batch(insts, seeds, hp, threads, mode=O.CANON)

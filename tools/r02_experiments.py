@@ -99,9 +99,32 @@ def sensitivity():
     print(json.dumps(out, indent=1))
 
 
+def mixed():
+    """F32X (tensor-core fp32 coupling, fp64 state) vs the fp64 path at config 1."""
+    insts, R, hp, _ = W.config1(0, 64)
+    seeds = P.replica_seeds(insts, R, "mfz-bn")
+    out = {}
+    with P.Context(0, "f64") as ctx:
+        ctx.set_problems(insts)
+        ctx.build_coupling()
+        ref = ctx.solve(R, "mfz-bn", hp, seeds)
+        out["f64_ms"] = ctx.timing()
+    for dt in ("f32x", "f32"):
+        with P.Context(0, dt) as ctx:
+            ctx.set_problems(insts)
+            ctx.build_coupling()
+            ctx.solve(R, "mfz-bn", hp, seeds)
+            res = ctx.solve(R, "mfz-bn", hp, seeds)
+            out[dt + "_timing"] = ctx.timing()
+        out[dt] = compare(ref, res)
+    with open(os.path.join(OUT, "mixed_r02.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps(out, indent=1))
+
+
 def l2groups():
     insts, R, hp, _ = W.config1(0, 64)
-    hp1 = P.baseline_params(velo=0, n_steps=1000)
+    hp1 = P.baseline_params(velo=1, n_steps=500)  # 2 x 500 steps
     seeds = P.replica_seeds(insts, R, "mfz-bn")
     rows = []
     for g in (64, 16, 8, 4):

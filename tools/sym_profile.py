@@ -14,11 +14,7 @@ sym = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 insts = P.gen_instances(2000, [(0.5, 0.1, 0.01, s) for s in range(1, B + 1)])
 ctx = P.Context(0, "f32")
-ctx.set_option("symmetric", sym)
-ctx.set_option("sym_groups", int(os.environ.get("SYM_GROUPS", "0")))
 ctx.set_option("pdl", int(os.environ.get("PDL", "1")))
-ctx.set_option("factored", int(os.environ.get("FACTORED", "-1")))
-ctx.set_option("fac_skew", int(os.environ.get("FAC_SKEW", "10")))
 ctx.set_problems(insts)
 ctx.build_coupling()
 R = 16
