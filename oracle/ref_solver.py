@@ -18,20 +18,31 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "_ref", "libref_solver.so")
-_L = None
+# the same sources built for speed (AVX2/FMA, reassociated reductions like
+# Eigen's SIMD kernels): bench.py's timed CPU arm only, never a parity pin
+SO_SIMD = os.path.join(HERE, "_ref", "libref_solver_simd.so")
+_L = {}
+_FAST = False
 
 
-def available() -> bool:
-    if not os.path.exists(SO) and os.path.isdir("/root/reference/proj"):
+def available(fast: bool = False) -> bool:
+    so = SO_SIMD if fast else SO
+    if not os.path.exists(so) and os.path.isdir("/root/reference/proj"):
         subprocess.call(["make", "-s", "-C", HERE, "-f", "Makefile.ref"])
-    return os.path.exists(SO)
+    return os.path.exists(so)
+
+
+def use_fast(flag: bool = True):
+    """Route the calls below to the SIMD timing build (bench.py)."""
+    global _FAST
+    _FAST = flag
 
 
 def lib():
-    global _L
-    if _L is None:
+    so = SO_SIMD if _FAST else SO
+    if so not in _L:
         from . import oracle as O
-        L = C.CDLL(SO)
+        L = C.CDLL(so)
         vp, i, d, u64 = C.c_void_p, C.c_int, C.c_double, C.c_uint64
         hp = C.POINTER(O._Hyper)
         L.ref_last_error.restype = C.c_char_p
@@ -40,8 +51,8 @@ def lib():
         L.ref_run_cim.argtypes = [i, i, vp, vp, i, hp, d, u64, vp, vp, vp, vp, vp]
         L.ref_cdp_minimize.argtypes = [i, i, vp, vp, vp, vp, i, hp, vp]
         L.ref_score.argtypes = [i, i, vp, vp, vp, vp, vp, vp, d, vp, vp, vp]
-        _L = L
-    return _L
+        _L[so] = L
+    return _L[so]
 
 
 def _arrs(inst):

@@ -90,9 +90,11 @@ def test_pp_fp32_cuda_cores(gpu, O):
 
 
 def test_pp_rejected_on_tensor_core_context(gpu, O):
-    insts = [O.gen_instance(64, 0.6, 0.2, 0.01, 1)]
+    """Positive-P runs on the CUDA-core contexts only: an fp32 context on the
+    tcgen05 symmetric path (N > 512) rejects it with ConfigError."""
+    insts = [O.gen_instance(640, 0.6, 0.2, 0.01, 1)]
     ctx = _ctx(gpu, insts, "f32")
     with pytest.raises(gpu.ConfigError):
-        ctx.run_pp(1, gpu.HyperParams(n_steps=10), 0.5, np.zeros((1, 1, 64)),
+        ctx.run_pp(1, gpu.HyperParams(n_steps=10), 0.5, np.zeros((1, 1, 640)),
                    np.array([1], np.uint64))
     ctx.close()
