@@ -92,6 +92,12 @@ uint64_t cimcs_mix_seed(uint64_t base, uint64_t salt);
 /* The fixed summation order of every G*v contraction (fp64 path is bitwise
  * reproducible against the oracle's ORC_CANON mode with these values). */
 int cimcs_gemv_order(int dtype, int32_t* nseg, int32_t* gran);
+/* The canonical fp64 contraction order of a context's resident problems, as
+ * the oracle's ORC_CANON (nseg, gran): (ceil(N/512), 512) on the DMMA symmetric
+ * path (unsharded fp64, N > 512), (8, 8) on the grid / cluster kernels.  Replaces
+ * nothing in the reference (its Eigen GEMV order is unpinnable); it is the
+ * reproducibility contract of the fp64 path. */
+int cimcs_canon_order(const cimcs_ctx* ctx, int32_t* nseg, int32_t* gran);
 
 /* Host instance generator: gen_instance, datagen.cpp:15-55 (same seeded
  * stream and draw order; std::mt19937_64 + Box-Muller as rng.hpp:21-64).

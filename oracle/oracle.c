@@ -217,9 +217,12 @@ void orc_pump_table(const orc_hyper* h, double* p) {
 /* Canonical segmented order: segment s = {j : (j / gran) % nseg == s}; each
  * segment is an fma chain over ascending j starting from +0.0; the segment
  * partials are then added left to right.  fma() is correctly rounded in both
- * the hardware and the libm path, so the dispatch below changes speed only. */
+ * the hardware and the libm path, so the dispatch below changes speed only.
+ * The GPU uses (nseg, gran) = (8, 8) on its grid / cluster kernels and
+ * (ceil(N / 512), 512) -- contiguous 512-column segments -- on the fp64 DMMA
+ * symmetric-tile path (cimcs_canon_order; sym64_kernels.cuh derives it). */
 #define CANON_BODY                                                                  \
-    double P[64];                                                               \
+    double P[256];                                                              \
     for (int s = 0; s < nseg; ++s) P[s] = 0.0;                                  \
     int s = 0;                                                                  \
     for (int j0 = 0; j0 < N; j0 += gran) {                                      \
@@ -284,7 +287,7 @@ int orc_problem_init(orc_problem* p, int N, int M, const double* A, const double
     p->mode = mode;
     p->nseg = nseg > 0 ? nseg : 8;
     p->gran = gran > 0 ? gran : 8;
-    if (p->nseg > 64) return 1;
+    if (p->nseg > 256) return 1;
     p->hz = (double*)malloc(sizeof(double) * (size_t)N);
     p->D = (double*)malloc(sizeof(double) * (size_t)N);
     p->work = (double*)malloc(sizeof(double) * (size_t)(M > N ? M : N));

@@ -21,7 +21,7 @@ PUMP_SIGMOID, PUMP_LINEAR = 0, 1
 # every symbol include/cimcs_gpu.h declares
 EXPORTS = (
     "cimcs_abi_version", "cimcs_last_error", "cimcs_hyper_default", "cimcs_hyper_validate",
-    "cimcs_mix_seed", "cimcs_gemv_order", "cimcs_gen_dims", "cimcs_gen_instance",
+    "cimcs_mix_seed", "cimcs_gemv_order", "cimcs_canon_order", "cimcs_gen_dims", "cimcs_gen_instance",
     "cimcs_gen_instances", "cimcs_create", "cimcs_destroy", "cimcs_set_option",
     "cimcs_set_problems", "cimcs_build_coupling", "cimcs_get_coupling", "cimcs_mfz_step",
     "cimcs_run_cim", "cimcs_run_pp", "cimcs_refit", "cimcs_cdp_minimize", "cimcs_score", "cimcs_solve", "cimcs_get_timing",
@@ -81,6 +81,7 @@ def load() -> C.CDLL:
     L.cimcs_mix_seed.restype = u64
     L.cimcs_mix_seed.argtypes = [u64, u64]
     L.cimcs_gemv_order.argtypes = [C.c_int, vp, vp]
+    L.cimcs_canon_order.argtypes = [vp, vp, vp]
     L.cimcs_gen_dims.argtypes = [i32, d, d, vp, vp]
     L.cimcs_gen_instance.argtypes = [i32, d, d, d, u64, vp, vp, vp, vp]
     L.cimcs_gen_instances.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, i32]

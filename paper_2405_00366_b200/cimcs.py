@@ -324,6 +324,13 @@ class Context:
                                             x.ctypes.data, xi.ctypes.data))
         return Instance(A, y, x, xi, a, al, nu, int(seed))
 
+    def canon_order(self):
+        """(nseg, gran) of the fp64 contraction order of the resident problems
+        (the oracle's ORC_CANON parameters, cimcs_canon_order)."""
+        ns, gr = C.c_int32(), C.c_int32()
+        _check(self._lib.cimcs_canon_order(self._ctx, C.byref(ns), C.byref(gr)))
+        return ns.value, gr.value
+
     def build_coupling(self):
         _check(self._lib.cimcs_build_coupling(self._ctx))
 

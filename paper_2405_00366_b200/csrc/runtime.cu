@@ -32,6 +32,7 @@
 #include "cg_kernels.cuh"
 #include "cluster_kernels.cuh"
 #include "sym_kernels.cuh"
+#include "sym64_kernels.cuh"
 #include "mri_kernels.cuh"
 
 using namespace cimcs;
@@ -320,10 +321,16 @@ struct cimcs_ctx {
     int* fail_tmp = nullptr;     // local fail_gstep before the cross-rank MIN
     bool tc = false;      // active for the current problem set
     bool sym = false;      // active for the current problem set
+    // fp64 symmetric-tile path on the DMMA tensor cores (sym64_kernels.cuh):
+    // unsharded fp64 contexts with N > kClMaxN (option "sym64", default on)
+    bool want_sym64 = true;
+    bool sym64 = false;
+    double *WT0 = nullptr, *WT1 = nullptr;  // fp64 w tiles of W0 / W1 [B][nRB][64][NR]
+    double* dPart6 = nullptr;               // partials [B][nRB][nSB][64][NR]
     int ntri = 0;          // upper-triangle tiles per instance
     int nSB = 0;           // super-block items per row of the tile triangle (kSyS tiles)
     struct SymSched {      // LPT placement of the items of nb instances on the CTAs
-        int nb = 0, nRB = 0, grid = 0;
+        int nb = 0, nRB = 0, S = 0, grid = 0;
         int2* items = nullptr;
         int* sched = nullptr;
     };
@@ -442,13 +449,14 @@ void free_state(cimcs_ctx* c) {
                     c->bestR, c->sig,    c->bestS,      c->fail_gstep, c->fail_idx, c->n_hist,
                     c->improved, c->minE, c->part,      c->best_obj, c->obj, c->rmse, c->ham,
                     c->tp, c->fail_tmp, c->cgX, c->cgR, c->cgP, c->cgGp, c->cg_act,
-                    c->cg_st, c->cg_live, c->WB0, c->WB1, c->WS0, c->WS1, c->Pn, c->Pm,
-                    c->MT, c->nzd[0], c->nzd[1]};
+                    c->cg_st, c->cg_live, c->WB0, c->WB1, c->WS0, c->WS1, c->WT0, c->WT1, c->Pn, c->Pm,
+                    c->MT, c->nzd[0], c->nzd[1], c->dPart6};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     c->cgX = c->cgR = c->cgP = c->cgGp = nullptr;
     c->WB0 = c->WB1 = nullptr;
     c->WS0 = c->WS1 = nullptr;
+    c->WT0 = c->WT1 = c->dPart6 = nullptr;
     c->Pn = c->Pm = c->MT = nullptr;
     c->nzd[0] = c->nzd[1] = nullptr;
     for (double*& h : c->nzh)
@@ -560,8 +568,9 @@ void tile_shard(int nRB, int world, int rank, int* P0, int* P1) {
 // Super-block items of nb instances placed on the persistent CTAs, largest
 // first onto the least-loaded CTA (LPT); built once per nb and cached.
 int sym_schedule(cimcs_ctx* c, int nb, const cimcs_ctx::SymSched** out) {
+    const int kS = c->sym64 ? kS6 : kSyS;  // item edge in tiles
     for (auto& q : c->ssched)
-        if (q.nb == nb && q.nRB == c->nRB) {
+        if (q.nb == nb && q.nRB == c->nRB && q.S == kS) {
             *out = &q;
             return 0;
         }
@@ -571,7 +580,7 @@ int sym_schedule(cimcs_ctx* c, int nb, const cimcs_ctx::SymSched** out) {
     for (int b = 0; b < nb; ++b)
         for (int P = P0; P < P1; ++P)
             for (int Q = P; Q < nSB; ++Q) {
-                const int nI = std::min(kSyS, nRB - P * kSyS), nJ = std::min(kSyS, nRB - Q * kSyS);
+                const int nI = std::min(kS, nRB - P * kS), nJ = std::min(kS, nRB - Q * kS);
                 const int t = P == Q ? nI * (nI + 1) / 2 : nI * nJ;
                 items.push_back({t, make_int2(b, P << 16 | Q)});
             }
@@ -598,6 +607,7 @@ int sym_schedule(cimcs_ctx* c, int nb, const cimcs_ctx::SymSched** out) {
     cimcs_ctx::SymSched q;
     q.nb = nb;
     q.nRB = nRB;
+    q.S = kS;
     q.grid = grid;
     int rc;
     if ((rc = dalloc(c, &q.items, flat.size() * sizeof(int2))) ||
@@ -654,6 +664,14 @@ int ensure_state(cimcs_ctx* c, int NR) {
             if ((rc = dalloc(c, &c->dSpart, ne * 4))) return rc;
             c->spart_elems = ne;
         }
+    }
+    if (c->sym64) {  // fp64 w tiles of W0/W1, the slot partials and the item schedule
+        const size_t nw = (size_t)c->B * c->nRB * kT6 * NR;
+        if ((rc = dalloc(c, &c->WT0, nw * 8)) || (rc = dalloc(c, &c->WT1, nw * 8)) ||
+            (rc = dalloc(c, &c->dPart6, nw * c->nSB * 8)))
+            return rc;
+        const cimcs_ctx::SymSched* ss;
+        if ((rc = sym_schedule(c, c->B, &ss))) return rc;
     }
     if (c->sym) {  // fp16 B tiles of W0/W1 and the partial products of the symmetric kernel
         const size_t nb = (size_t)c->B * c->nRB * 2 * NR * kSyT, ns = (size_t)c->B * c->nRB * NR;
@@ -920,6 +938,77 @@ int launch_sym_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
 }
 
 
+// fp64 symmetric-tile path (sym64_kernels.cuh): the DMMA tile kernel, then the
+// fused fp64 update, both on the context stream with PDL between them.
+template <int NR, int MODE>
+int launch_sym64_t(cimcs_ctx* c, const GemvArgs& g) {
+    Sym64Args sa{};
+    sa.t = tc_args(c, g);
+    sa.Gt = static_cast<const double*>(c->dG);
+    sa.WTin = g.Win == c->W0 ? c->WT0 : c->WT1;
+    sa.WTout = g.Wout == c->W0 ? c->WT0 : (g.Wout == c->W1 ? c->WT1 : nullptr);
+    sa.part = c->dPart6;
+    sa.ntri = c->ntri;
+    sa.nSB = c->nSB;
+    const cimcs_ctx::SymSched* ss = nullptr;
+    if (int rc = sym_schedule(c, c->B, &ss)) return rc;
+    sa.items = ss->items;
+    sa.sched = ss->sched;
+    auto kern = sym64_step_kernel<NR, MODE>;
+    constexpr size_t smem = s6_smem_bytes<NR>();
+    static std::atomic<unsigned long long> attr{0};
+    if (!(attr.load() >> c->device & 1ull)) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr.fetch_or(1ull << c->device);
+    }
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ss->grid);
+    cfg.blockDim = dim3(kT6Threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cfg.attrs = at;
+    cfg.numAttrs = c->use_pdl ? 1 : 0;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    const bool timed = c->kernel_timing && (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) &&
+                       cudaStreamIsCapturing(c->stream, &cap) == cudaSuccess &&
+                       cap == cudaStreamCaptureStatusNone;
+    if (timed) {
+        if (!c->kt_ev[0]) {
+            CK(cudaEventCreate(&c->kt_ev[0]));
+            CK(cudaEventCreate(&c->kt_ev[1]));
+        }
+        CK(cudaEventRecord(c->kt_ev[0], c->stream));
+    }
+    CK(cudaLaunchKernelEx(&cfg, kern, sa));
+    if (timed) {
+        CK(cudaEventRecord(c->kt_ev[1], c->stream));
+        CK(cudaEventSynchronize(c->kt_ev[1]));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->kt_ev[0], c->kt_ev[1]));
+        c->timing.tile_kernel_ms += ms;
+        c->timing.tile_kernel_launches += 1;
+    }
+    cfg.gridDim = dim3(c->nRB, c->B);
+    cfg.blockDim = dim3(kT6 * NR / 4);
+    cfg.dynamicSmemBytes = 0;
+    CK(cudaLaunchKernelEx(&cfg, sym64_update_kernel<NR, MODE>, sa));
+    return 0;
+}
+
+template <int NR>
+int launch_sym64_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
+    switch (mode) {
+        case EPI_STEP_BN: return launch_sym64_t<NR, EPI_STEP_BN>(c, a);
+        case EPI_STEP_CN: return launch_sym64_t<NR, EPI_STEP_CN>(c, a);
+        case EPI_JACOBI: return launch_sym64_t<NR, EPI_JACOBI>(c, a);
+        case EPI_MATVEC: return launch_sym64_t<NR, EPI_MATVEC>(c, a);
+        default: return launch_sym64_t<NR, EPI_SCORE>(c, a);
+    }
+}
+
 // one mri_kernel launch of `grid` CTAs (basis vectors r0.. for DIAG / COLS)
 int mri_launch(cimcs_ctx* c, int mode, int grid, int r0, const float* in, float* out) {
     MriArgs ma{};
@@ -1015,6 +1104,7 @@ int launch_mri_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
 
 int launch_gemv(cimcs_ctx* c, int mode, const GemvArgs& a) {
     if (c->mri) return c->NR == 8 ? launch_mri_nr<8>(c, mode, a) : launch_mri_nr<16>(c, mode, a);
+    if (c->sym64) return c->NR == 8 ? launch_sym64_nr<8>(c, mode, a) : launch_sym64_nr<16>(c, mode, a);
     if (c->sym) return c->NR == 8 ? launch_sym_nr<8>(c, mode, a) : launch_sym_nr<16>(c, mode, a);
     return c->st64() ? launch_gemv_T<double>(c, mode, a)
                                  : launch_gemv_T<float>(c, mode, a);
@@ -1027,9 +1117,17 @@ int launch_gemv(cimcs_ctx* c, int mode, const GemvArgs& a) {
 // symmetric path: refresh the fp16 B tiles of W (W0 or W1) after a writer
 // other than the symmetric kernel itself
 int sym_sync_w(cimcs_ctx* c, const void* W) {
-    if (!c->sym) return 0;
     const bool w0 = W == c->W0;
     const dim3 g(c->nRB, c->B);
+    if (c->sym64) {
+        DISPATCH_NR_TC(c->NR, {
+            sym64_wconvert_kernel<NR_><<<g, 256, 0, c->stream>>>(
+                static_cast<const double*>(W), c->N, c->ldN, c->nRB, w0 ? c->WT0 : c->WT1);
+        });
+        CK(cudaGetLastError());
+        return 0;
+    }
+    if (!c->sym) return 0;
     DISPATCH_NR_TC(c->NR, {
         if (c->st64())
             sym_wconvert_kernel<NR_, double><<<g, 128, 0, c->stream>>>(
@@ -1047,7 +1145,7 @@ int sym_sync_w(cimcs_ctx* c, const void* W) {
 // replica slots: a power of two; the tensor-core path needs MMA N in {8, 16}
 int slots_for(const cimcs_ctx* c, int R) {
     const int p = pow2_slots(R);
-    return c->tc || c->mri ? std::max(8, p) : p;
+    return c->tc || c->mri || c->sym64 ? std::max(8, p) : p;
 }
 
 // Generic NR/T dispatch for the small state kernels.
@@ -1361,7 +1459,8 @@ int enqueue_steps(cimcs_ctx* c, int bn, const StepScalars& s, int n_steps) {
         a.Wout = (n_steps & 1) ? c->W1 : c->W0;
         return launch_cluster(c, bn ? EPI_STEP_BN : EPI_STEP_CN, a, n_steps);
     }
-    if (c->sym) return enqueue_sym_loop(c, bn ? EPI_STEP_BN : EPI_STEP_CN, a, n_steps, true);
+    if (c->sym || c->sym64)
+        return enqueue_sym_loop(c, bn ? EPI_STEP_BN : EPI_STEP_CN, a, n_steps, true);
     for (int k = 0; k < n_steps; ++k) {
         a.step = k;
         a.Win = (k & 1) ? c->W1 : c->W0;
@@ -1384,7 +1483,7 @@ int enqueue_refit(cimcs_ctx* c, const StepScalars& s, int iters, bool do_support
         a.Wout = (iters & 1) ? c->W1 : c->W0;
         return launch_cluster(c, EPI_JACOBI, a, iters);
     }
-    if (c->sym) {
+    if (c->sym || c->sym64) {
         if (int rc = enqueue_sym_loop(c, EPI_JACOBI, a, iters, false)) return rc;
         return 0;
     }
@@ -1936,6 +2035,17 @@ int cimcs_gemv_order(int dtype, int32_t* nseg, int32_t* gran) {
     return 0;
 }
 
+// The fp64 contraction order of the resident problem set (ORC_CANON's
+// (nseg, gran)): the DMMA symmetric path sums 512-column segments, the grid and
+// cluster kernels 8 interleaved segments of 8-column granules.
+int cimcs_canon_order(const cimcs_ctx* c, int32_t* nseg, int32_t* gran) {
+    if (!c || c->B < 1) return fail(CIMCS_INPUT_ERROR, "no problems set");
+    const bool s64 = c->sym64;
+    if (nseg) *nseg = s64 ? c->nSB : kSeg;
+    if (gran) *gran = s64 ? kT6Seg : kGran;
+    return 0;
+}
+
 int cimcs_gen_dims(int32_t N, double alpha, double a, int32_t* M, int32_t* K) {
     int m = 0, k = 0;
     if (gen_dims(N, alpha, a, &m, &k)) return fail(CIMCS_INPUT_ERROR, "gen_instance: bad dims");
@@ -2177,6 +2287,9 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
     else if (k == "tensor_cores") {
         if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set tensor_cores before set_problems");
         c->want_tc = v != 0;
+    } else if (k == "sym64") {
+        if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set sym64 before set_problems");
+        c->want_sym64 = v != 0;
     }
     else return fail(CIMCS_CONFIG_ERROR, "unknown option " + k);
     return 0;
@@ -2229,8 +2342,11 @@ int prepare_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M, bool 
     }
     c->nch = c->ldJ / kTcChunk;
     c->sym = c->tc;
-    c->ntri = c->sym ? c->nRB * (c->nRB + 1) / 2 : 0;
-    c->nSB = (c->nRB + kSyS - 1) / kSyS;
+    // fp64: DMMA symmetric tiles for unsharded contexts above the cluster range
+    // (64-row blocks = row_block<double>(), 512 x 512 items)
+    c->sym64 = c->dtype == CIMCS_F64 && c->want_sym64 && !c->sh_rows && N > kClMaxN;
+    c->ntri = c->sym || c->sym64 ? c->nRB * (c->nRB + 1) / 2 : 0;
+    c->nSB = (c->nRB + (c->sym64 ? kS6 : kSyS) - 1) / (c->sym64 ? kS6 : kSyS);
     if (c->tshard) tile_shard(c->nRB, c->tworld, c->trank, &c->sP0, &c->sP1);
     c->M.assign(M, M + B);
     c->Mmax = *std::max_element(c->M.begin(), c->M.end());
@@ -2527,7 +2643,7 @@ int cimcs_set_mri_problem(cimcs_ctx* c, int32_t H, int32_t W, const double* targ
     c->B = 1;
     c->N = N;
     c->ldN = c->ldJ = (N + 31) / 32 * 32;
-    c->tc = c->sym = false;
+    c->tc = c->sym = c->sym64 = false;
     c->RB = kSyT;
     c->row0 = 0;
     c->row1 = N;
@@ -2605,9 +2721,10 @@ int cimcs_build_coupling(cimcs_ctx* c) {
         return 0;
     }
     const size_t es = c->elt();
-    // gram bytes: symmetric fp16 hi/lo tiles, canonical tf32 panels, or CUDA-core panels
-    const size_t gbytes = c->sym ? (size_t)c->B * c->ntri * 2 * kSyPlaneBytes
-                                  : (size_t)c->B * c->nRB * c->ldJ * c->RB * es;
+    // gram bytes: symmetric fp16 hi/lo tiles, symmetric fp64 tiles, or CUDA-core panels
+    const size_t gbytes = c->sym     ? (size_t)c->B * c->ntri * 2 * kSyPlaneBytes
+                          : c->sym64 ? (size_t)c->B * c->ntri * kT6TileBytes
+                                     : (size_t)c->B * c->nRB * c->ldJ * c->RB * es;
     const size_t nv = (size_t)c->B * c->ldN;
     int rc;
     if (!c->dG && (rc = dalloc(c, &c->dG, gbytes))) return rc;
@@ -2723,6 +2840,10 @@ int cimcs_build_coupling(cimcs_ctx* c) {
             SymOut o{static_cast<__half*>(c->dG) + (size_t)b * c->ntri * 2 * kSyPlaneHalfs,
                      c->dSg + b, c->nRB, c->ntri};
             gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o, bi0, mirror);
+        } else if (c->sym64) {
+            Sym64Out o{static_cast<double*>(c->dG) + (size_t)b * c->ntri * (kT6 * kT6), c->nRB,
+                       c->ntri};
+            gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o, bi0, mirror);
         } else if (c->st64()) {
             PanelOut<double, row_block<double>()> o{
                 static_cast<double*>(c->dG) + (size_t)b * c->nRB * c->ldJ * c->RB, c->ldJ, c->nRB,
@@ -2775,6 +2896,19 @@ int cimcs_get_coupling(cimcs_ctx* c, int32_t b, double* G, double* hz, double* D
         std::vector<float> f((size_t)N * N);
         if (int rc_ = copy_sync(c, f.data(), P, f.size() * 4, cudaMemcpyDeviceToHost)) return rc_;
         for (size_t k = 0; k < f.size(); ++k) G[k] = f[k];
+    } else if (G && c->sym64) {
+        const size_t nt = (size_t)c->ntri * kT6 * kT6;
+        std::vector<double> t(nt);
+        if (int rc_ = copy_sync(c, t.data(), static_cast<const double*>(c->dG) + (size_t)b * nt,
+                                nt * 8, cudaMemcpyDeviceToHost))
+            return rc_;
+        for (int i = 0; i < N; ++i)
+            for (int j = 0; j < N; ++j) {
+                int r = i, q = j;  // stored upper triangle: G[i][j] = G[j][i]
+                if (r / kT6 > q / kT6) std::swap(r, q);
+                G[(size_t)i * N + j] = t[(size_t)sy_tri(r / kT6, q / kT6, c->nRB) * kT6 * kT6 +
+                                         s6_gofs(r % kT6, q % kT6)];
+            }
     } else if (G && c->sym) {
         const size_t nh = (size_t)c->ntri * 2 * kSyPlaneHalfs;
         std::vector<__half> t(nh);
@@ -3300,7 +3434,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
     // score contraction, tp, finalize, median (+ best).  The small-N cluster loop
     // runs a whole CIM call / refit in one launch; CG counts its last iteration total.
     const bool cl = cluster_ok(c) && !pp;
-    const int per = c->sym ? 2 : 1;  // symmetric path: tile kernel + update kernel
+    const int per = c->sym || c->sym64 ? 2 : 1;  // symmetric paths: tile kernel + update kernel
     tm.step_launches = (int64_t)nalt * (cl ? 1 : per * hp->n_steps + (pp ? 1 : 0));
     if (cdp == CIMCS_CDP_CG) {
         std::vector<CgTraj> st(nT);

@@ -121,13 +121,15 @@ def test_cluster_divergence_matches_grid(gpu, O):
 
 
 def test_grid_path_beyond_cluster_limit(gpu, O):
-    """N = 513 is outside the cluster loop: the grid kernels still match the oracle."""
+    """N = 513 is outside the cluster loop: the fp64 DMMA symmetric path (in its
+    own canonical order, cimcs_canon_order) still matches the oracle."""
     inst = O.gen_instance(513, 0.5, 0.2, 0.01, 4)
     hp = O.baseline_params(velo=2, n_steps=200)
     seed = O.mix_seed(4, 1)
     ctx = _ctx(gpu, [inst])
+    order = ctx.canon_order()
     res = ctx.solve(1, "mfz-bn", gpu.baseline_params(velo=2, n_steps=200), [seed])
     ctx.close()
-    ref = O.Problem(inst, O.CANON).alternating_minimize(O.MFZ_BN, hp, O.Rng(seed))
+    ref = O.Problem(inst, O.CANON, *order).alternating_minimize(O.MFZ_BN, hp, O.Rng(seed))
     assert np.array_equal(res["R"][0, 0], ref["R"])
     assert np.array_equal(res["sigma"][0, 0], ref["sigma"])

@@ -1,0 +1,161 @@
+"""fp64 DMMA symmetric-tile path (sym64_kernels.cuh) against the oracle, BITWISE.
+
+Unsharded fp64 contexts with N > 512 store the gram as upper-triangle 64 x 64
+fp64 tiles and contract on the FP64 tensor cores (mma.sync m8n8k4, which the
+B200 evaluates as a sequential fma chain, tools/peaks_probe.cu).  Their order
+is the oracle's ORC_CANON with (nseg, gran) = (ceil(N/512), 512), reported by
+cimcs_canon_order; every quantity below is compared bit for bit with the oracle
+in that order, except reduced scalars (objective, rmse: 1e-12 relative).
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx(P, insts, dtype="f64", **opts):
+    ctx = P.Context(0, dtype)
+    for k, v in opts.items():
+        ctx.set_option(k, v)
+    ctx.set_problems(insts)
+    ctx.build_coupling()
+    return ctx
+
+
+def _probs(O, insts, order):
+    return [O.Problem(i, O.CANON, *order) for i in insts]
+
+
+@pytest.mark.parametrize("N", [600, 1100, 2000])
+def test_order_and_gram_tiles(gpu, O, N):
+    insts = [O.gen_instance(N, 0.5, 0.1, 0.01, 5)]
+    ctx = _ctx(gpu, insts)
+    order = ctx.canon_order()
+    assert order == (-(-N // 512), 512)
+    G, hz, D = ctx.get_coupling(0)
+    p = _probs(O, insts, order)[0]
+    assert np.array_equal(G, p.G) and np.array_equal(hz, p.hz) and np.array_equal(D, p.gram_diag)
+    ctx.close()
+    ctx = _ctx(gpu, insts, sym64=0)  # the CUDA-core grid kernel keeps the (8, 8) order
+    assert ctx.canon_order() == (8, 8)
+    ctx.close()
+
+
+@pytest.mark.parametrize("backend", ["mfz-bn", "mfz-cn"])
+@pytest.mark.parametrize("N,R", [(600, 3), (1100, 16), (2000, 8)])
+def test_single_step_bitwise(gpu, O, backend, N, R):
+    insts = [O.gen_instance(N, 0.6, 0.2, 0.01, 3), O.gen_instance(N, 0.4, 0.1, 0.01, 4)]
+    ctx = _ctx(gpu, insts)
+    probs = _probs(O, insts, ctx.canon_order())
+    B = len(insts)
+    rng = np.random.default_rng(R)
+    Rs = rng.normal(size=(B, R, N))
+    c = rng.normal(scale=0.5, size=(B, R, N))
+    e = np.abs(rng.normal(size=(B, R, N))) + 0.1
+    hp, ghp = O.baseline_params(), gpu.baseline_params()
+    out = ctx.mfz_step(R, backend, ghp, 0.37, 0.83, Rs, c, e)
+    for b in range(B):
+        for r in range(R):
+            if backend == "mfz-bn":
+                h = probs[b].local_field_bn(Rs[b, r], (c[b, r] > 0).astype(np.int32), hp.tau)
+            else:
+                h = probs[b].local_field_cn(Rs[b, r], c[b, r], hp.tau)
+            co, eo = O.mfz_step(c[b, r], e[b, r], 0.83, hp, 0.37, Rs[b, r], h)
+            assert np.array_equal(out["h"][b, r], h)
+            assert np.array_equal(out["c"][b, r], co)
+            assert np.array_equal(out["e"][b, r], eo)
+    ctx.close()
+
+
+@pytest.mark.parametrize("backend", ["mfz-bn", "mfz-cn"])
+def test_run_cim_bitwise(gpu, O, backend):
+    """A whole CIM call (300 steps) from identical c0 / R."""
+    insts = [O.gen_instance(700, 0.5, 0.1, 0.01, s) for s in (1, 2)]
+    R, N = 5, 700
+    ctx = _ctx(gpu, insts)
+    probs = _probs(O, insts, ctx.canon_order())
+    hp = O.baseline_params(n_steps=300)
+    seeds = [[O.mix_seed(inst.seed, 1 + 3 * r) for r in range(R)] for inst in insts]
+    c0 = np.zeros((2, R, N))
+    for b in range(2):
+        for r in range(R):
+            g = O.Rng(seeds[b][r])
+            c0[b, r] = [0.01 * g.gauss() for _ in range(N)]
+    Rs = np.stack([np.stack([p.hz] * R) for p in probs])
+    out = ctx.run_cim(R, backend, gpu.baseline_params(n_steps=300), 0.6, Rs, c0)
+    be = O.BACKENDS[backend]
+    for b in range(2):
+        for r in range(R):
+            ref = probs[b].run_mfz(Rs[b, r], hp, 0.6, be, O.Rng(seeds[b][r]))
+            assert np.array_equal(out["c"][b, r], ref["c"])
+            assert np.array_equal(out["e"][b, r], ref["e"])
+            assert np.array_equal(out["sigma"][b, r], ref["sigma"])
+            assert out["min_e"][b, r] == ref["min_e"]
+    ctx.close()
+
+
+@pytest.mark.parametrize("cdp", ["jacobi", "cg"])
+def test_refit_bitwise(gpu, O, cdp):
+    insts = [O.gen_instance(900, 0.5, 0.1, 0.01, 8)]
+    R = 8
+    ctx = _ctx(gpu, insts)
+    p = _probs(O, insts, ctx.canon_order())[0]
+    rng = np.random.default_rng(2)
+    sigma = (rng.random((1, R, 900)) < 0.25).astype(np.int32)
+    Rp = rng.normal(size=(1, R, 900))
+    out = ctx.refit(R, sigma, Rp, gpu.HyperParams(), cdp=cdp)
+    sc = ctx.score(R, Rp, sigma, 0.05)
+    ctx.close()
+    m = O.CDP_JACOBI if cdp == "jacobi" else O.CDP_CG
+    for r in range(R):
+        ref = p.cdp(sigma[0, r], Rp[0, r], m, O.HyperParams())
+        assert np.array_equal(out[0, r], ref)
+        obj = p.objective_at(Rp[0, r], sigma[0, r], 0.05)
+        assert math.isclose(sc["objective"][0, r], obj, rel_tol=1e-12, abs_tol=1e-14)
+
+
+@pytest.mark.parametrize("backend,track_best", [("mfz-bn", False), ("mfz-cn", True)])
+def test_solve_bitwise(gpu, O, backend, track_best):
+    """Whole alternating solves: 2 instances x 3 replicas (NR padded to 8), N=600."""
+    insts = [O.gen_instance(600, 0.5, 0.1, 0.01, s) for s in (11, 12)]
+    R = 3
+    be = O.BACKENDS[backend]
+    seeds = np.array([[O.mix_seed(i.seed, be + 3 * r) for r in range(R)] for i in insts],
+                     np.uint64)
+    ctx = _ctx(gpu, insts)
+    order = ctx.canon_order()
+    res = ctx.solve(R, backend, gpu.baseline_params(velo=3, n_steps=300), seeds,
+                    track_best=track_best)
+    ctx.close()
+    hp = O.baseline_params(velo=3, n_steps=300)
+    for b, inst in enumerate(insts):
+        p = O.Problem(inst, O.CANON, *order)
+        for r in range(R):
+            ref = p.alternating_minimize(be, hp, O.Rng(int(seeds[b, r])), track_best=track_best)
+            assert np.array_equal(res["R"][b, r], ref["R"])
+            assert np.array_equal(res["sigma"][b, r], ref["sigma"])
+            for h, g in zip(ref["history"], res["history"][b, r]):
+                assert g["support"] == h["support"] and g["min_e"] == h["min_e"]
+                assert g["median_e"] == h["median_e"]
+                assert math.isclose(g["hamiltonian"], h["hamiltonian"], rel_tol=1e-12,
+                                    abs_tol=1e-14)
+
+
+def test_solve_config1_shape_bitwise(gpu, O):
+    """BASELINE config-1 shape (N=2000, M=1000), 16 replicas, 2 x 200 steps:
+    two replicas checked bitwise against the oracle."""
+    insts = [O.gen_instance(2000, 0.5, 0.1, 0.01, 1)]
+    R = 16
+    seeds = np.array([[O.mix_seed(1, 1 + 3 * r) for r in range(R)]], np.uint64)
+    ctx = _ctx(gpu, insts)
+    order = ctx.canon_order()
+    res = ctx.solve(R, "mfz-bn", gpu.baseline_params(velo=1, n_steps=200), seeds)
+    ctx.close()
+    p = O.Problem(insts[0], O.CANON, *order)
+    for r in (0, 15):
+        ref = p.alternating_minimize(O.MFZ_BN, O.baseline_params(velo=1, n_steps=200),
+                                     O.Rng(int(seeds[0, r])))
+        assert np.array_equal(res["R"][0, r], ref["R"])
+        assert np.array_equal(res["sigma"][0, r], ref["sigma"])

@@ -122,6 +122,34 @@ def mixed():
     print(json.dumps(out, indent=1))
 
 
+def f64perf():
+    """fp64 config 1: DMMA symmetric path vs the CUDA-core grid kernel (sym64=0)."""
+    insts, R, hp, _ = W.config1(0, 64)
+    seeds = P.replica_seeds(insts, R, "mfz-bn")
+    out = {}
+    res = {}
+    for s64 in (1, 0):
+        with P.Context(0, "f64") as ctx:
+            ctx.set_option("sym64", s64)
+            ctx.set_problems(insts)
+            ctx.build_coupling()
+            ctx.solve(R, "mfz-bn", hp, seeds)
+            res[s64] = ctx.solve(R, "mfz-bn", hp, seeds)
+            t = ctx.timing()
+            out[f"sym64={s64}"] = {k: t[k] for k in ("total_ms", "gram_ms", "cim_ms", "refit_ms")}
+            out[f"sym64={s64}"]["us_per_step"] = t["cim_ms"] / 20000 * 1e3
+            if s64:
+                ctx.set_option("use_graphs", 0)
+                ctx.set_option("kernel_timing", 1)
+                ctx.solve(R, "mfz-bn", P.baseline_params(velo=1, n_steps=100), seeds)
+                tk = ctx.timing()
+                out["sym64_tile_kernel_us"] = tk["tile_kernel_ms"] / tk["tile_kernel_launches"] * 1e3
+    out["vs_cudacore"] = compare(res[0], res[1])
+    with open(os.path.join(OUT, "f64perf_r02.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps(out, indent=1))
+
+
 def l2groups():
     insts, R, hp, _ = W.config1(0, 64)
     hp1 = P.baseline_params(velo=1, n_steps=500)  # 2 x 500 steps
