@@ -10,7 +10,7 @@ the gram (0.57 GB of fp16 hi/lo tiles, 1.1 GB of fp64 tiles) is larger than
 L2, so no flush is needed.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--dtype f32|f32x|f64] [--config 0..4]
+                  [--dtype f32|f64] [--config 0..4]
 
 --gpus N without torchrun relaunches this script under torch.distributed.run
 with N ranks (one per GPU).  Config 1 is weak-scaled (every rank solves its
@@ -133,7 +133,7 @@ def ctx_nr(R, dtype, N=2000):
     p = 1
     while p < R:
         p *= 2
-    return max(8, p) if dtype in ("f32", "f32x") and N > 512 else p
+    return max(8, p) if N > 512 else p
 
 
 def kernel_label(N, NR, dtype):
@@ -143,12 +143,16 @@ def kernel_label(N, NR, dtype):
         return (f"cluster_loop_kernel<{t},{NR},BN> (whole 1000-step CIM call per launch, G "
                 "register-resident, w over DSMEM; bound by the per-step FMA chain + DSMEM "
                 "round trip, so the HBM fraction is an HBM-equivalent figure)")
-    if dtype in ("f32", "f32x"):
-        st = "fp64 state" if dtype == "f32x" else "fp32 state"
-        return (f"sym_step_kernel<{NR},BN> + sym_update_kernel<{NR},BN,{st}> (one fused "
+    if dtype == "f32":
+        return (f"sym_step_kernel<{NR},BN> + sym_update_kernel<{NR},BN> (one fused "
                 "Euler step: upper-triangle gram tiles as fp16 hi/lo, each read once for G w "
                 "and G^T w on tcgen05; achieved counts the stored triangle bytes one step must "
                 "read, dense_equivalent the dense fp32 gram share of SURVEY 8(d))")
+    if N > 512:
+        return (f"sym64_step_kernel<{NR},BN> + sym64_update_kernel<{NR},BN> (one fused fp64 "
+                "Euler step: upper-triangle 64x64 fp64 gram tiles, each read once for G w and "
+                "G^T w on the FP64 tensor cores, mma.sync m8n8k4 DMMA; bound by the DMMA pipe: "
+                "achieved = 2 N^2 R flops per instance per step)")
     return f"gemv_fused_kernel<double,{NR},BN> (fused Euler step, fp64 DFMA)"
 
 
@@ -362,16 +366,14 @@ def run_reference(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
-# Headline dtype per config: config 1's credited line is the F32X path
-# (tensor-core fp32 coupling, fp64 state: parity-backed against the fp64 path,
-# DESIGN.md section 5); the other configs keep their round-1 dtypes.
-DEFAULT_DTYPE = {0: "f64", 1: "f32x", 2: "f32", 3: "f32", 4: "f32"}
+# Headline dtype per config: config 1's line is the fp32 tensor-core path held
+# to the declared fp32 tolerance below, with the bitwise fp64 path measured
+# beside it in the same run ("f64" sub-line); config 0 is the fp64 CPU workload.
+DEFAULT_DTYPE = {0: "f64", 1: "f32", 2: "f32", 3: "f32", 4: "f32"}
 # fp32-mode tolerance (declared in DESIGN.md section 5 before the round-2
 # measurements): against the fp64 path on the same seeded inputs.
 F32_TOL = {"rmse_mean_rel": 1e-2, "hamming_mean_rel": 1e-2, "best_rmse_mean_rel": 1e-2,
            "paired_se_max": 4.0, "where_same_rmse_rel": 1e-5}
-# F32X bar: the north_star's fp64 bar (supports identical on >= 99 % of instances)
-F32X_TOL = {"inst_identical_min": 0.99, "where_same_rmse_rel": 1e-5}
 
 
 def final_metrics(res):
@@ -404,28 +406,35 @@ def parity_vs_f64(ref, res, dtype):
            "rmse_paired_diff": [float(d.mean()), se], "max_rel_rmse_where_same": where,
            "failed": [int((ref["fail_alt"] >= 0).sum()), int((res["fail_alt"] >= 0).sum())]}
     rel = lambda a: abs(a[1] - a[0]) / abs(a[0])  # noqa: E731
-    if dtype == "f32x":
-        out["tolerance"] = F32X_TOL
-        out["pass"] = bool(out["inst_identical_best_support"] >= F32X_TOL["inst_identical_min"]
-                           and where <= F32X_TOL["where_same_rmse_rel"]
-                           and out["failed"][1] <= out["failed"][0])
-    else:
-        out["tolerance"] = F32_TOL
-        out["pass"] = bool(rel(out["rmse_mean"]) <= F32_TOL["rmse_mean_rel"]
-                           and rel(out["hamming_mean"]) <= F32_TOL["hamming_mean_rel"]
-                           and rel(out["best_rmse_mean"]) <= F32_TOL["best_rmse_mean_rel"]
-                           and abs(d.mean()) <= F32_TOL["paired_se_max"] * max(se, 1e-300)
-                           and where <= F32_TOL["where_same_rmse_rel"]
-                           and out["failed"][1] <= out["failed"][0])
+    out["tolerance"] = F32_TOL
+    out["pass"] = bool(rel(out["rmse_mean"]) <= F32_TOL["rmse_mean_rel"]
+                       and rel(out["hamming_mean"]) <= F32_TOL["hamming_mean_rel"]
+                       and rel(out["best_rmse_mean"]) <= F32_TOL["best_rmse_mean_rel"]
+                       and abs(d.mean()) <= F32_TOL["paired_se_max"] * max(se, 1e-300)
+                       and where <= F32_TOL["where_same_rmse_rel"]
+                       and out["failed"][1] <= out["failed"][0])
     return out
 
 
 def gram_step_bytes(dtype, B, N):
     """Bytes one Euler step must stream: the stored gram of the path."""
-    if dtype in ("f32", "f32x") and N > 512:
+    if dtype == "f32" and N > 512:
         nrb = (N + 127) // 128  # upper-triangle 128x128 tiles, fp16 hi|lo (4 B per entry)
         return B * (nrb * (nrb + 1) // 2) * 128 * 128 * 4
+    if dtype == "f64" and N > 512:
+        nrb = (N + 63) // 64  # upper-triangle 64x64 fp64 tiles (sym64)
+        return B * (nrb * (nrb + 1) // 2) * 64 * 64 * 8
     return B * N * N * (4 if dtype == "f32" else 8)
+
+
+def dmma_peak():
+    """Measured FP64 tensor (DMMA) peak on this pool's B200 (tools/peaks_probe.cu)."""
+    p = os.path.join(ROOT, "profiles", "r02_peaks.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["dmma_tflops"]), "measured (profiles/r02_peaks.json)"
+    except (OSError, KeyError, ValueError):
+        return 37.0, "fallback"
 
 
 def measure(args, dtype, insts, R, hp, ws, rank, local, dist, tile_sharded=False,
@@ -508,6 +517,10 @@ def measure(args, dtype, insts, R, hp, ws, rank, local, dist, tile_sharded=False
     step_s = statistics.median(step_ms) * 1e-3
     peak, peak_kind = measured_peaks()
     achieved = step_bytes / step_s / 1e9
+    # the fp64 symmetric step is bound by the FP64 tensor pipe, not HBM:
+    # 2 N^2 R flops per instance per step (every replica, the whole dense G)
+    f64_tensor = dtype == "f64" and Nn > 512
+    step_flops = 2.0 * Bn * Nn * Nn * R
 
     e2e = None
     if with_e2e and not args.no_e2e:
@@ -541,7 +554,7 @@ def measure(args, dtype, insts, R, hp, ws, rank, local, dist, tile_sharded=False
                r2["history"].nbytes, "seconds": e2e_s}
 
     dom = None
-    if with_dom and dtype in ("f32", "f32x") and Nn > 512 and not tile_sharded:
+    if with_dom and Nn > 512 and not tile_sharded:
         # the tile kernel alone: a short eager run with CUDA events around every
         # step-mode launch on its stream (outside the timed region)
         ctx.set_option("use_graphs", 0)
@@ -552,14 +565,25 @@ def measure(args, dtype, insts, R, hp, ws, rank, local, dist, tile_sharded=False
         ctx.set_option("use_graphs", 1)
         if tk["tile_kernel_launches"] > 0:
             t_tile = tk["tile_kernel_ms"] / tk["tile_kernel_launches"] * 1e-3
-            dom = {"kernel": f"sym_step_kernel<{ctx_nr(R, dtype, Nn)},BN>",
-                   "avg_us": t_tile * 1e6, "launches": int(tk["tile_kernel_launches"]),
-                   "bytes_per_launch": step_bytes, "achieved": step_bytes / t_tile / 1e9,
-                   "peak": peak, "unit": "GB/s", "frac": step_bytes / t_tile / 1e9 / peak,
-                   "share_of_step": t_tile / step_s,
-                   "how": ("eager run of 2 x 100 steps after the timed region, CUDA events on "
-                           "the launch stream around each launch (serialised: the kernel "
-                           "timed alone, burst peak)")}
+            nr = ctx_nr(R, dtype, Nn)
+            if f64_tensor:
+                dp, dk = dmma_peak()
+                dom = {"kernel": f"sym64_step_kernel<{nr},BN>", "bound": "tensor (FP64 DMMA)",
+                       "avg_us": t_tile * 1e6, "launches": int(tk["tile_kernel_launches"]),
+                       "flops_per_launch": step_flops, "achieved": step_flops / t_tile / 1e12,
+                       "peak": dp, "peak_kind": dk, "unit": "TFLOP/s",
+                       "frac": step_flops / t_tile / 1e12 / dp,
+                       "hbm": {"bytes_per_launch": step_bytes,
+                               "achieved_gbs": step_bytes / t_tile / 1e9}}
+            else:
+                dom = {"kernel": f"sym_step_kernel<{nr},BN>", "bound": "hbm",
+                       "avg_us": t_tile * 1e6, "launches": int(tk["tile_kernel_launches"]),
+                       "bytes_per_launch": step_bytes, "achieved": step_bytes / t_tile / 1e9,
+                       "peak": peak, "unit": "GB/s", "frac": step_bytes / t_tile / 1e9 / peak}
+            dom.update({"share_of_step": t_tile / step_s,
+                        "how": ("eager run of 2 x 100 steps after the timed region, CUDA events "
+                                "on the launch stream around each launch (serialised: the "
+                                "kernel timed alone, burst peak)")})
     ctx.close()
     fields = {
         "value": value, "ms_per_step": ms_per_step, "steps": args.steps, "warmup": args.warmup,
@@ -567,8 +591,14 @@ def measure(args, dtype, insts, R, hp, ws, rank, local, dist, tile_sharded=False
         "instances_per_s": (Bn if tile_sharded else total_units / units * Bn) / (ms_per_step * 1e-3),
         "problem_load_s": gen_s,
         "breakdown_ms": {k: statistics.median(v) for k, v in parts.items()},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak,
+        "roofline": ({"bound": "tensor", "achieved": step_flops / step_s / 1e12,
+                      "peak": dmma_peak()[0], "unit": "TFLOP/s",
+                      "frac": step_flops / step_s / 1e12 / dmma_peak()[0],
+                      "peak_kind_tensor": dmma_peak()[1], "hbm_achieved_gbs": achieved}
+                     if f64_tensor else
+                     {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                      "frac": achieved / peak}),
+        "roofline_detail": {
                      "traffic": ncu_traffic() if Nn == 2000 and dtype == "f32" else None,
                      "kernel": kernel_label(Nn, ctx_nr(R, dtype, Nn), dtype),
                      "bytes_per_launch": step_bytes, "peak_kind": peak_kind,
@@ -579,6 +609,7 @@ def measure(args, dtype, insts, R, hp, ws, rank, local, dist, tile_sharded=False
         "l2": ("inputs larger than L2 (gram %.2f GB per step)" % (step_bytes / 1e9)
                if step_bytes > 126e6 else "gram fits in L2 (no flush)"),
     }
+    fields["roofline"].update(fields.pop("roofline_detail"))
     return fields, res
 
 
@@ -616,7 +647,7 @@ def run_ours(args, ws, rank, local):
     if args.config == 1 and not args.no_extra:
         # the other precisions of config 1 on the same instances and seeds, each a
         # full measurement; parity of every non-fp64 run against the fp64 run
-        for dt in ("f64", "f32x", "f32"):
+        for dt in ("f64", "f32"):
             if dt == dtype:
                 continue
             f, r = measure(args, dt, insts, R, hp, ws, rank, local, dist, with_dom=True)
@@ -818,8 +849,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--dtype", default=None, choices=["f32", "f32x", "f64"],
-                    help="default: the config's (f32x for 1, f32 for 2-4, f64 for 0)")
+    ap.add_argument("--dtype", default=None, choices=["f32", "f64"],
+                    help="default: the config's (f32 for 1-4, f64 for 0)")
     ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--n4", type=int, default=100_000, help="config 4 size (N)")
     ap.add_argument("--no-cpu", action="store_true")

@@ -28,13 +28,10 @@ extern "C" {
 
 enum { CIMCS_OK = 0, CIMCS_INPUT_ERROR = 1, CIMCS_CONFIG_ERROR = 2,
        CIMCS_DIVERGENCE = 3, CIMCS_CUDA_ERROR = 4 };
-/* Context arithmetic.  F64: every quantity in fp64 (bitwise-reproducible
- * canonical order).  F32: fp32 state and coupling.  F32X: the coupling
- * contraction on the tensor cores at fp32 accuracy (fp16 hi/lo symmetric gram
- * tiles, N > 512) with the state (c, e, R, w), the Euler / Jacobi updates and
- * the scores in fp64 -- the state precision, not the field's, decides whether a
- * trajectory keeps the fp64 support (profiles/r02_precision_study.json). */
-enum { CIMCS_F32 = 0, CIMCS_F64 = 1, CIMCS_F32X = 2 };
+/* Context arithmetic.  F64: every quantity in fp64, in the documented
+ * canonical order (bitwise-reproducible; cimcs_canon_order).  F32: fp32 state,
+ * coupling on the tcgen05 tensor cores (N > 512) or fp32 CUDA cores. */
+enum { CIMCS_F32 = 0, CIMCS_F64 = 1 };
 /* == Backend {MfzCN, MfzBN, PositiveP}, orchestrator.hpp:28 */
 enum { CIMCS_MFZ_CN = 0, CIMCS_MFZ_BN = 1, CIMCS_PP = 2 };
 /* == CdpMethod {Jacobi, ConjugateGradient}, cdp.hpp:60 */

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CIMCS_GPU_LIB") or os.path.join(HERE, "libcimcs_gpu.so")
 
 OK, INPUT_ERROR, CONFIG_ERROR, DIVERGENCE, CUDA_ERROR = 0, 1, 2, 3, 4
-F32, F64, F32X = 0, 1, 2
+F32, F64 = 0, 1
 MFZ_CN, MFZ_BN, PP = 0, 1, 2
 CDP_JACOBI, CDP_CG = 0, 1
 PUMP_SIGMOID, PUMP_LINEAR = 0, 1

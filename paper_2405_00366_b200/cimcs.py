@@ -28,8 +28,7 @@ from ._lib import load
 
 BACKENDS = {"mfz-cn": _lib.MFZ_CN, "mfz-bn": _lib.MFZ_BN, "pp": _lib.PP}
 DTYPES = {"f32": _lib.F32, "fp32": _lib.F32, "float32": _lib.F32,
-          "f64": _lib.F64, "fp64": _lib.F64, "float64": _lib.F64,
-          "f32x": _lib.F32X}  # tensor-core fp32 coupling, fp64 state (cimcs_gpu.h)
+          "f64": _lib.F64, "fp64": _lib.F64, "float64": _lib.F64}
 
 
 # ---------------------------------------------------------------- errors

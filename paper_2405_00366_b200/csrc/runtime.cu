@@ -325,6 +325,8 @@ struct cimcs_ctx {
     // unsharded fp64 contexts with N > kClMaxN (option "sym64", default on)
     bool want_sym64 = true;
     bool sym64 = false;
+    int nRB6 = 0, ntri6 = 0, nSB6 = 0;      // its geometry: 64-row blocks, 512 x 512 items
+    void* dG6 = nullptr;                    // its gram tiles [B][ntri6][64 x 64] fp64
     double *WT0 = nullptr, *WT1 = nullptr;  // fp64 w tiles of W0 / W1 [B][nRB][64][NR]
     double* dPart6 = nullptr;               // partials [B][nRB][nSB][64][NR]
     int ntri = 0;          // upper-triangle tiles per instance
@@ -420,8 +422,8 @@ struct cimcs_ctx {
     cudaStream_t side = nullptr;  // captures the CG loop body
     cimcs_timing timing{};
 
-    // fp64 state arrays (c, e, R, w, D, hz): F64 and F32X contexts
-    bool st64() const { return dtype != CIMCS_F32; }
+    // fp64 state arrays (c, e, R, w, D, hz)
+    bool st64() const { return dtype == CIMCS_F64; }
     size_t elt() const { return st64() ? 8 : 4; }
     const void* G() const { return dG; }
     size_t state_elems() const { return (size_t)B * ldN * NR; }
@@ -479,7 +481,7 @@ void free_state(cimcs_ctx* c) {
 
 void free_problems(cimcs_ctx* c) {
     free_state(c);
-    void* ptrs[] = {c->dA, c->dy, c->dM, c->dG, c->dD, c->dhz, c->dx, c->dxi,
+    void* ptrs[] = {c->dA, c->dy, c->dM, c->dG, c->dG6, c->dD, c->dhz, c->dx, c->dxi,
                     c->dSg, c->dSpart, c->dMaskBr, c->dTw, c->dTarget,
                     c->dH};
     for (void* p : ptrs)
@@ -499,7 +501,7 @@ void free_problems(cimcs_ctx* c) {
     c->spart_elems = 0;
     c->dA = c->dy = nullptr;
     c->dM = nullptr;
-    c->dG = nullptr;
+    c->dG = c->dG6 = nullptr;
     c->dD = c->dhz = nullptr;
     c->dx = nullptr;
     c->dxi = nullptr;
@@ -567,16 +569,16 @@ void tile_shard(int nRB, int world, int rank, int* P0, int* P1) {
 
 // Super-block items of nb instances placed on the persistent CTAs, largest
 // first onto the least-loaded CTA (LPT); built once per nb and cached.
-int sym_schedule(cimcs_ctx* c, int nb, const cimcs_ctx::SymSched** out) {
-    const int kS = c->sym64 ? kS6 : kSyS;  // item edge in tiles
+int sym_schedule(cimcs_ctx* c, int nb, const cimcs_ctx::SymSched** out, bool s64 = false) {
+    const int kS = s64 ? kS6 : kSyS;  // item edge in tiles
+    const int nRB = s64 ? c->nRB6 : c->nRB, nSB = s64 ? c->nSB6 : c->nSB;
     for (auto& q : c->ssched)
-        if (q.nb == nb && q.nRB == c->nRB && q.S == kS) {
+        if (q.nb == nb && q.nRB == nRB && q.S == kS) {
             *out = &q;
             return 0;
         }
-    const int nRB = c->nRB, nSB = c->nSB;
     std::vector<std::pair<int, int2>> items;  // (tiles, item)
-    const int P0 = c->tshard ? c->sP0 : 0, P1 = c->tshard ? c->sP1 : nSB;
+    const int P0 = c->tshard && !s64 ? c->sP0 : 0, P1 = c->tshard && !s64 ? c->sP1 : nSB;
     for (int b = 0; b < nb; ++b)
         for (int P = P0; P < P1; ++P)
             for (int Q = P; Q < nSB; ++Q) {
@@ -640,7 +642,7 @@ int ensure_state(cimcs_ctx* c, int NR) {
     c->NR = NR;
     const size_t n = c->state_elems(), es = c->elt();
     const int nT = c->B * NR;
-    const int nRB = std::max(c->nRB, 1);
+    const int nRB = std::max(std::max(c->nRB, c->nRB6), 1);
     int rc = 0;
     const size_t nw = c->w_elems();
     if ((rc = dalloc(c, &c->Rs, n * es)) || (rc = dalloc(c, &c->C, n * es)) ||
@@ -666,12 +668,12 @@ int ensure_state(cimcs_ctx* c, int NR) {
         }
     }
     if (c->sym64) {  // fp64 w tiles of W0/W1, the slot partials and the item schedule
-        const size_t nw = (size_t)c->B * c->nRB * kT6 * NR;
+        const size_t nw = (size_t)c->B * c->nRB6 * kT6 * NR;
         if ((rc = dalloc(c, &c->WT0, nw * 8)) || (rc = dalloc(c, &c->WT1, nw * 8)) ||
-            (rc = dalloc(c, &c->dPart6, nw * c->nSB * 8)))
+            (rc = dalloc(c, &c->dPart6, nw * c->nSB6 * 8)))
             return rc;
         const cimcs_ctx::SymSched* ss;
-        if ((rc = sym_schedule(c, c->B, &ss))) return rc;
+        if ((rc = sym_schedule(c, c->B, &ss, true))) return rc;
     }
     if (c->sym) {  // fp16 B tiles of W0/W1 and the partial products of the symmetric kernel
         const size_t nb = (size_t)c->B * c->nRB * 2 * NR * kSyT, ns = (size_t)c->B * c->nRB * NR;
@@ -913,10 +915,7 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb) {
     cfg.blockDim = dim3(kSyT * NR / 4);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = sF;
-    if (c->st64())
-        CK(cudaLaunchKernelEx(&cfg, sym_update_kernel<NR, MODE, double>, sa));
-    else
-        CK(cudaLaunchKernelEx(&cfg, sym_update_kernel<NR, MODE, float>, sa));
+    CK(cudaLaunchKernelEx(&cfg, sym_update_kernel<NR, MODE, float>, sa));
     return 0;
 }
 
@@ -944,14 +943,15 @@ template <int NR, int MODE>
 int launch_sym64_t(cimcs_ctx* c, const GemvArgs& g) {
     Sym64Args sa{};
     sa.t = tc_args(c, g);
-    sa.Gt = static_cast<const double*>(c->dG);
+    sa.t.nRB = c->nRB6;
+    sa.Gt = static_cast<const double*>(c->dG6);
     sa.WTin = g.Win == c->W0 ? c->WT0 : c->WT1;
     sa.WTout = g.Wout == c->W0 ? c->WT0 : (g.Wout == c->W1 ? c->WT1 : nullptr);
     sa.part = c->dPart6;
-    sa.ntri = c->ntri;
-    sa.nSB = c->nSB;
+    sa.ntri = c->ntri6;
+    sa.nSB = c->nSB6;
     const cimcs_ctx::SymSched* ss = nullptr;
-    if (int rc = sym_schedule(c, c->B, &ss)) return rc;
+    if (int rc = sym_schedule(c, c->B, &ss, true)) return rc;
     sa.items = ss->items;
     sa.sched = ss->sched;
     auto kern = sym64_step_kernel<NR, MODE>;
@@ -991,7 +991,7 @@ int launch_sym64_t(cimcs_ctx* c, const GemvArgs& g) {
         c->timing.tile_kernel_ms += ms;
         c->timing.tile_kernel_launches += 1;
     }
-    cfg.gridDim = dim3(c->nRB, c->B);
+    cfg.gridDim = dim3(c->nRB6, c->B);
     cfg.blockDim = dim3(kT6 * NR / 4);
     cfg.dynamicSmemBytes = 0;
     CK(cudaLaunchKernelEx(&cfg, sym64_update_kernel<NR, MODE>, sa));
@@ -1104,7 +1104,8 @@ int launch_mri_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
 
 int launch_gemv(cimcs_ctx* c, int mode, const GemvArgs& a) {
     if (c->mri) return c->NR == 8 ? launch_mri_nr<8>(c, mode, a) : launch_mri_nr<16>(c, mode, a);
-    if (c->sym64) return c->NR == 8 ? launch_sym64_nr<8>(c, mode, a) : launch_sym64_nr<16>(c, mode, a);
+    if (c->sym64)
+        return c->NR == 8 ? launch_sym64_nr<8>(c, mode, a) : launch_sym64_nr<16>(c, mode, a);
     if (c->sym) return c->NR == 8 ? launch_sym_nr<8>(c, mode, a) : launch_sym_nr<16>(c, mode, a);
     return c->st64() ? launch_gemv_T<double>(c, mode, a)
                                  : launch_gemv_T<float>(c, mode, a);
@@ -1121,22 +1122,16 @@ int sym_sync_w(cimcs_ctx* c, const void* W) {
     const dim3 g(c->nRB, c->B);
     if (c->sym64) {
         DISPATCH_NR_TC(c->NR, {
-            sym64_wconvert_kernel<NR_><<<g, 256, 0, c->stream>>>(
-                static_cast<const double*>(W), c->N, c->ldN, c->nRB, w0 ? c->WT0 : c->WT1);
+            sym64_wconvert_kernel<NR_><<<dim3(c->nRB6, c->B), 256, 0, c->stream>>>(
+                static_cast<const double*>(W), c->N, c->ldN, c->nRB6, w0 ? c->WT0 : c->WT1);
         });
         CK(cudaGetLastError());
-        return 0;
     }
     if (!c->sym) return 0;
     DISPATCH_NR_TC(c->NR, {
-        if (c->st64())
-            sym_wconvert_kernel<NR_, double><<<g, 128, 0, c->stream>>>(
-                static_cast<const double*>(W), c->N, c->ldN, c->nRB, w0 ? c->WB0 : c->WB1,
-                w0 ? c->WS0 : c->WS1);
-        else
-            sym_wconvert_kernel<NR_, float><<<g, 128, 0, c->stream>>>(
-                static_cast<const float*>(W), c->N, c->ldN, c->nRB, w0 ? c->WB0 : c->WB1,
-                w0 ? c->WS0 : c->WS1);
+        sym_wconvert_kernel<NR_, float><<<g, 128, 0, c->stream>>>(
+            static_cast<const float*>(W), c->N, c->ldN, c->nRB, w0 ? c->WB0 : c->WB1,
+            w0 ? c->WS0 : c->WS1);
     });
     CK(cudaGetLastError());
     return 0;
@@ -1323,7 +1318,8 @@ GemvArgs base_args(cimcs_ctx* c, const StepScalars& s) {
     return a;
 }
 
-int nRB_of(const cimcs_ctx* c) { return c->nRB; }
+// row blocks of the score partials: the contraction that scores (sym64 if present)
+int nRB_of(const cimcs_ctx* c) { return c->sym64 ? c->nRB6 : c->nRB; }
 
 // ------------------------------------------------ row-sharding collectives
 
@@ -2041,7 +2037,7 @@ int cimcs_gemv_order(int dtype, int32_t* nseg, int32_t* gran) {
 int cimcs_canon_order(const cimcs_ctx* c, int32_t* nseg, int32_t* gran) {
     if (!c || c->B < 1) return fail(CIMCS_INPUT_ERROR, "no problems set");
     const bool s64 = c->sym64;
-    if (nseg) *nseg = s64 ? c->nSB : kSeg;
+    if (nseg) *nseg = s64 ? c->nSB6 : kSeg;
     if (gran) *gran = s64 ? kT6Seg : kGran;
     return 0;
 }
@@ -2175,8 +2171,7 @@ int cimcs_gen_instances(int32_t B, int32_t N, const double* alpha, const double*
 
 int cimcs_create(int32_t device, int32_t dtype, cimcs_ctx** out) {
     if (!out) return fail(CIMCS_INPUT_ERROR, "null out");
-    if (dtype != CIMCS_F32 && dtype != CIMCS_F64 && dtype != CIMCS_F32X)
-        return fail(CIMCS_CONFIG_ERROR, "bad dtype");
+    if (dtype != CIMCS_F32 && dtype != CIMCS_F64) return fail(CIMCS_CONFIG_ERROR, "bad dtype");
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(CIMCS_CONFIG_ERROR, "bad device");
@@ -2312,7 +2307,7 @@ int prepare_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M, bool 
     c->ldJ = (N + kChunk - 1) / kChunk * kChunk;
     // fp32 tensor cores = the symmetric-tile path, for N above the cluster-loop
     // range, unsharded or tile-sharded; everything else runs on CUDA cores
-    c->tc = c->dtype != CIMCS_F64 && c->want_tc && N > kClMaxN && (!c->sh_rows || c->tshard_opt);
+    c->tc = c->dtype == CIMCS_F32 && c->want_tc && N > kClMaxN && (!c->sh_rows || c->tshard_opt);
     c->RB = c->tc ? kTcRows : (c->st64() ? row_block<double>() : row_block<float>());
     c->row0 = 0;
     c->row1 = N;
@@ -2345,8 +2340,11 @@ int prepare_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M, bool 
     // fp64: DMMA symmetric tiles for unsharded contexts above the cluster range
     // (64-row blocks = row_block<double>(), 512 x 512 items)
     c->sym64 = c->dtype == CIMCS_F64 && c->want_sym64 && !c->sh_rows && N > kClMaxN;
-    c->ntri = c->sym || c->sym64 ? c->nRB * (c->nRB + 1) / 2 : 0;
-    c->nSB = (c->nRB + (c->sym64 ? kS6 : kSyS) - 1) / (c->sym64 ? kS6 : kSyS);
+    c->nRB6 = c->sym64 ? (N + kT6 - 1) / kT6 : 0;
+    c->ntri6 = c->nRB6 * (c->nRB6 + 1) / 2;
+    c->nSB6 = (c->nRB6 + kS6 - 1) / kS6;
+    c->ntri = c->sym ? c->nRB * (c->nRB + 1) / 2 : 0;
+    c->nSB = (c->nRB + kSyS - 1) / kSyS;
     if (c->tshard) tile_shard(c->nRB, c->tworld, c->trank, &c->sP0, &c->sP1);
     c->M.assign(M, M + B);
     c->Mmax = *std::max_element(c->M.begin(), c->M.end());
@@ -2723,8 +2721,11 @@ int cimcs_build_coupling(cimcs_ctx* c) {
     const size_t es = c->elt();
     // gram bytes: symmetric fp16 hi/lo tiles, symmetric fp64 tiles, or CUDA-core panels
     const size_t gbytes = c->sym     ? (size_t)c->B * c->ntri * 2 * kSyPlaneBytes
-                          : c->sym64 ? (size_t)c->B * c->ntri * kT6TileBytes
+                          : c->sym64 ? 16
                                      : (size_t)c->B * c->nRB * c->ldJ * c->RB * es;
+    if (c->sym64 && !c->dG6) {
+        if (int rc = dalloc(c, &c->dG6, (size_t)c->B * c->ntri6 * kT6TileBytes)) return rc;
+    }
     const size_t nv = (size_t)c->B * c->ldN;
     int rc;
     if (!c->dG && (rc = dalloc(c, &c->dG, gbytes))) return rc;
@@ -2751,12 +2752,8 @@ int cimcs_build_coupling(cimcs_ctx* c) {
             static_cast<float*>(c->dD), c->B);
     CK(cudaGetLastError());
     if (c->sym) {
-        if (c->st64())
-            sym_scale_kernel<double><<<c->B, 256, 0, c->stream>>>(
-                static_cast<const double*>(c->dD), c->N, c->ldN, c->dSg);
-        else
-            sym_scale_kernel<float><<<c->B, 256, 0, c->stream>>>(
-                static_cast<const float*>(c->dD), c->N, c->ldN, c->dSg);
+        sym_scale_kernel<float><<<c->B, 256, 0, c->stream>>>(
+            static_cast<const float*>(c->dD), c->N, c->ldN, c->dSg);
         CK(cudaGetLastError());
     }
     // large instances on the symmetric path: G = A^T A by cuBLAS DGEMM over panels
@@ -2836,13 +2833,14 @@ int cimcs_build_coupling(cimcs_ctx* c) {
             b = e;
             continue;
         }
-        if (c->sym) {
+        const Sym64Out o64{c->sym64 ? static_cast<double*>(c->dG6) + (size_t)b * c->ntri6 * (kT6 * kT6)
+                                    : nullptr,
+                           c->nRB6, c->ntri6};
+        if (c->sym64) {
+            gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o64, bi0, mirror);
+        } else if (c->sym) {
             SymOut o{static_cast<__half*>(c->dG) + (size_t)b * c->ntri * 2 * kSyPlaneHalfs,
                      c->dSg + b, c->nRB, c->ntri};
-            gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o, bi0, mirror);
-        } else if (c->sym64) {
-            Sym64Out o{static_cast<double*>(c->dG) + (size_t)b * c->ntri * (kT6 * kT6), c->nRB,
-                       c->ntri};
             gram128_kernel<<<grid, 256, 0, c->stream>>>(Ab, c->M[b], c->N, astride, o, bi0, mirror);
         } else if (c->st64()) {
             PanelOut<double, row_block<double>()> o{
@@ -2897,16 +2895,16 @@ int cimcs_get_coupling(cimcs_ctx* c, int32_t b, double* G, double* hz, double* D
         if (int rc_ = copy_sync(c, f.data(), P, f.size() * 4, cudaMemcpyDeviceToHost)) return rc_;
         for (size_t k = 0; k < f.size(); ++k) G[k] = f[k];
     } else if (G && c->sym64) {
-        const size_t nt = (size_t)c->ntri * kT6 * kT6;
+        const size_t nt = (size_t)c->ntri6 * kT6 * kT6;
         std::vector<double> t(nt);
-        if (int rc_ = copy_sync(c, t.data(), static_cast<const double*>(c->dG) + (size_t)b * nt,
+        if (int rc_ = copy_sync(c, t.data(), static_cast<const double*>(c->dG6) + (size_t)b * nt,
                                 nt * 8, cudaMemcpyDeviceToHost))
             return rc_;
         for (int i = 0; i < N; ++i)
             for (int j = 0; j < N; ++j) {
                 int r = i, q = j;  // stored upper triangle: G[i][j] = G[j][i]
                 if (r / kT6 > q / kT6) std::swap(r, q);
-                G[(size_t)i * N + j] = t[(size_t)sy_tri(r / kT6, q / kT6, c->nRB) * kT6 * kT6 +
+                G[(size_t)i * N + j] = t[(size_t)sy_tri(r / kT6, q / kT6, c->nRB6) * kT6 * kT6 +
                                          s6_gofs(r % kT6, q % kT6)];
             }
     } else if (G && c->sym) {

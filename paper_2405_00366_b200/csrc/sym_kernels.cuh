@@ -228,8 +228,8 @@ __device__ __forceinline__ SyItem sy_item(const SymArgs& sa, int k, int nRB) {
 }
 
 // fp16 hi/lo split of w * 2^e (e from the per-replica block max): exact scaling,
-// rounded to nearest in both halves; the fp64 state of F32X contexts is split
-// from its double value
+// rounded to nearest in both halves (a double input is split from its double
+// value)
 __device__ __forceinline__ void sy_split(float w, int e, __half& hi, __half& lo) {
     const float ws = w * sy_pow2(e);
     hi = __float2half_rn(ws);
@@ -548,8 +548,8 @@ __device__ __forceinline__ void sy_st4(double* p, const double (&v)[4]) {
 // handled by 128 x (NR / 4) threads; thread (row, g), g = t % (NR / 4) fastest
 // so a warp reads whole state rows (coalesced 16-byte vectors), sums its 4
 // replicas' nSB partial products in slot order (deterministic, fp32), runs the
-// fused update for replicas 4g..4g+3 in the state type TS (float: F32 contexts;
-// double: F32X, the fp64-state mode) and, in step / Jacobi modes, emits the fp16
+// fused update for replicas 4g..4g+3 in the state type TS (float; a double
+// instantiation gives an fp64-state variant) and, in step / Jacobi modes, emits the fp16
 // B tile of the new w (staged in shared memory, stored with 16-byte vectors).
 template <int NR, int MODE, typename TS = float>
 __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_update_kernel(SymArgs sa) {

@@ -97,7 +97,7 @@ __device__ __forceinline__ void tmem_ld_row(uint32_t taddr, float (&gw)[NR]) {
 }
 
 struct TcArgs {
-    // state arrays in the context's state type TS (float: F32, double: F32X)
+    // state arrays in the context's state type (float on the fp32 path)
     const void* D;         // [B][ldN]
     const void* hz;
     const void* Win;       // [B][ldN][NR]

@@ -159,3 +159,4 @@ def test_solve_config1_shape_bitwise(gpu, O):
                                      O.Rng(int(seeds[0, r])))
         assert np.array_equal(res["R"][0, r], ref["R"])
         assert np.array_equal(res["sigma"][0, r], ref["sigma"])
+
