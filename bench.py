@@ -616,7 +616,7 @@ def measure(args, dtype, insts, R, hp, ws, rank, local, dist, tile_sharded=False
 def run_ours(args, ws, rank, local):
     import paper_2405_00366_b200 as P
     from paper_2405_00366_b200 import _lib
-    _lib.load()  # before torch: the system cuBLAS 12.9 (fp32-emulated gram GEMMs) wins
+    _lib.load()  # before torch (the product library binds torch's NCCL)
     import torch
 
     torch.cuda.set_device(local)

@@ -21,7 +21,7 @@ FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
     "-fmad=false", "-Xcompiler", "-fPIC,-O3", "-shared", "-cudart", "static",
 ]
-LIBS = ["-lnccl", "-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+LIBS = ["-lnccl", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
 
 
 def _torch_nccl_dir():

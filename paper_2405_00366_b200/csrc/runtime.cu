@@ -8,9 +8,7 @@
 // thread pool from each trajectory's std::mt19937_64 stream while the GPU
 // runs the current one.
 #include <cuda_runtime.h>
-#include <dlfcn.h>
 #include <nccl.h>
-#include <cublas_v2.h>
 
 #include <algorithm>
 #include <queue>
@@ -33,6 +31,7 @@
 #include "cluster_kernels.cuh"
 #include "sym_kernels.cuh"
 #include "sym64_kernels.cuh"
+#include "gram_tc_kernels.cuh"
 #include "mri_kernels.cuh"
 
 using namespace cimcs;
@@ -353,11 +352,7 @@ struct cimcs_ctx {
     bool tshard = false;            // active for the current problem set
     int tworld = 1, trank = 0, sP0 = 0, sP1 = 0;
     float* dH = nullptr;            // [B][nRB][128][NR] summed partial products
-    int gram_blas = 0;        // symmetric gram from cuBLAS DGEMM panels: 0 auto (N >= 8192), 1, -1
-    int gram_emu = -1;        // ... as fp32-emulated (BF16x9) GEMMs on the tensor cores:
-                              // -1 auto (N >= 32768: 14.0 -> 5.0 s at config 4; slower
-                              // than DGEMM at config 3's N = 16384), 1 on, 0 off
-    bool timing_gram_emu = false;  // the last build used them
+    int gram_tc = 0;          // large-N fp32 gram on tcgen05 (gram_tc_kernels.cuh): 0 auto (N >= 8192), 1, -1
     // matrix-free MRI transform-chain problem (mri_kernels.cuh; mri.hpp:46-99)
     bool mri = false;
     int mH = 0, mW = 0, mL = 0;
@@ -366,7 +361,6 @@ struct cimcs_ctx {
     float2* dTw = nullptr;             // [L/2] exp(-2 pi i k / L)
     float* dTarget = nullptr;          // [H*W] target image (row-major)
     bool mri_cluster = true;           // per-step apply on one cluster per replica
-    cublasHandle_t blas = nullptr;
     __half *WB0 = nullptr, *WB1 = nullptr;  // fp16 B tiles of W0 / W1 [B][nRB][2NR x 128]
     int *WS0 = nullptr, *WS1 = nullptr;     // their scale exponents [B][nRB][NR]
     size_t spart_elems = 0;
@@ -829,11 +823,7 @@ TcArgs tc_args(const cimcs_ctx* c, const GemvArgs& g) {
 }
 
 
-__global__ void f64_to_f32_kernel(const double* __restrict__ a, float* __restrict__ o, size_t n) {
-    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
-         t += (size_t)gridDim.x * blockDim.x)
-        o[t] = (float)a[t];
-}
+
 
 // symmetric-tile variant (sym_kernels.cuh): half the gram bytes per step.
 // The tile kernel, then the slot reduction and the fused update, on the
@@ -2245,7 +2235,6 @@ void cimcs_destroy(cimcs_ctx* c) {
     drop_graphs(c);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->side) cudaStreamDestroy(c->side);
-    if (c->blas) cublasDestroy(c->blas);
     cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -2255,8 +2244,7 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
     const std::string k(key);
     if (k == "host_threads") c->host_threads = (int)std::max<int64_t>(1, v);
     else if (k == "use_graphs") c->use_graphs = v != 0;
-    else if (k == "gram_blas") c->gram_blas = v > 0 ? 1 : (v < 0 ? -1 : 0);
-    else if (k == "gram_emu") c->gram_emu = v > 0 ? 1 : (v < 0 ? -1 : 0);
+    else if (k == "gram_tc") c->gram_tc = v > 0 ? 1 : (v < 0 ? -1 : 0);
     else if (k == "kernel_timing") {
         c->kernel_timing = v != 0;
         c->timing.tile_kernel_ms = 0.0;
@@ -2756,70 +2744,53 @@ int cimcs_build_coupling(cimcs_ctx* c) {
             static_cast<const float*>(c->dD), c->N, c->ldN, c->dSg);
         CK(cudaGetLastError());
     }
-    // large instances on the symmetric path: G = A^T A by cuBLAS DGEMM over panels
-    // of 8 row blocks (upper triangle only), converted to the fp16 hi/lo tiles
-    const bool blas = c->sym && (c->gram_blas > 0 || (c->gram_blas == 0 && c->N >= 8192));
+    // large instances on the symmetric path (N >= 8192: configs 3 and 4): G = A^T A
+    // on the tcgen05 tensor cores from fp16 hi/lo splits of A, written straight into
+    // the fp16 hi/lo tiles (gram_tc_kernels.cuh); option "gram_tc": 0 auto, 1 on, -1 off
+    const bool blas = c->sym && (c->gram_tc > 0 || (c->gram_tc == 0 && c->N >= 8192));
     if (blas) {
-        if (!c->blas) {
-            if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS)
-                return fail(CIMCS_CUDA_ERROR, "cublasCreate failed");
+        const int Np = c->nRB * kSyT;
+        const int nchx = (c->Mmax + kGtK - 1) / kGtK;
+        __half* Pv = nullptr;
+        unsigned long long* amax = nullptr;
+        if ((rc = dalloc(c, &Pv, (size_t)nchx * 2 * Np * kGtK * 2)) ||
+            (rc = dalloc(c, &amax, (size_t)c->B * 8)))
+            return rc;
+        std::unique_ptr<__half, decltype(&cudaFree)> pguard(Pv, &cudaFree);
+        std::unique_ptr<unsigned long long, decltype(&cudaFree)> aguard(amax, &cudaFree);
+        static std::atomic<unsigned long long> attr{0};
+        if (!(attr.load() >> c->device & 1ull)) {
+            CK(cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kGtSmem));
+            attr.fetch_or(1ull << c->device);
         }
-        cublasSetStream(c->blas, c->stream);
-        const int PB = 8, ldp = PB * kSyT;
-        // the tiles hold ~22 bits (fp16 hi/lo): an fp32-accurate GEMM suffices, run as
-        // cuBLAS's BF16x9 fp32 emulation on the tensor cores (option "gram_emu", default
-        // on) instead of fp64 DGEMM on the CUDA cores
-        // (cuBLAS >= 12.9: when an older libcublas.so.12 was loaded first -- e.g. by
-        // torch -- the emulation entry point is absent and the fp64 DGEMM runs)
-        using SetEmu = cublasStatus_t (*)(cublasHandle_t, cublasEmulationStrategy_t);
-        static SetEmu set_emu =
-            reinterpret_cast<SetEmu>(dlsym(RTLD_DEFAULT, "cublasSetEmulationStrategy"));
-        bool emu = (c->gram_emu > 0 || (c->gram_emu < 0 && c->N >= 32768)) && set_emu != nullptr;
-        void* Pv = nullptr;  // sized for fp64 panels: the DGEMM route may take over mid-build
-        if ((rc = dalloc(c, reinterpret_cast<char**>(&Pv), (size_t)ldp * c->N * 8))) return rc;
-        std::unique_ptr<void, decltype(&cudaFree)> pguard(Pv, &cudaFree);
-        float* A32 = nullptr;
-        if (emu && (rc = dalloc(c, &A32, (size_t)c->Mmax * c->N * 4))) return rc;
-        c->timing_gram_emu = emu;
-        std::unique_ptr<float, decltype(&cudaFree)> aguard(A32, &cudaFree);
-        if (emu && set_emu(c->blas, CUBLAS_EMULATION_STRATEGY_EAGER) != CUBLAS_STATUS_SUCCESS)
-            emu = false;
-        const double one = 1.0, zero = 0.0;
-        const float onef = 1.f, zerof = 0.f;
-        for (int b = 0; b < c->B; ++b) {
-            const int M = c->M[b];
+        // tile-sharded: only the row blocks of this rank's super-rows
+        const int Ib = c->tshard ? c->sP0 * kSyS : 0;
+        const int Ie = c->tshard ? std::min(c->nRB, c->sP1 * kSyS) : c->nRB;
+        long long ntile = 0;
+        for (int I = Ib; I < Ie; ++I) ntile += c->nRB - I;
+        for (int b = 0; b < c->B && ntile > 0; ++b) {
+            const int M = c->M[b], nch = (M + kGtK - 1) / kGtK;
             const double* Ab = c->dA + (size_t)b * astride;
-            if (emu && A32) {
-                const size_t n = (size_t)M * c->N;
-                f64_to_f32_kernel<<<8 * c->num_sms, 256, 0, c->stream>>>(Ab, A32, n);
-                CK(cudaGetLastError());
-            }
-            SymOut o{static_cast<__half*>(c->dG), c->dSg, c->nRB, c->ntri};
-            // tile-sharded: only the row blocks of this rank's super-rows
-            const int Ib = c->tshard ? c->sP0 * kSyS : 0;
-            const int Ie = c->tshard ? std::min(c->nRB, c->sP1 * kSyS) : c->nRB;
-            for (int I0 = Ib; I0 < Ie; I0 += PB) {
-                const int nI = std::min(PB, Ie - I0), i0 = I0 * kSyT;
-                const int rows = std::min(nI * kSyT, c->N - i0), ncols = c->N - i0;
-                if (emu && cublasGemmEx(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, rows, ncols, M, &onef,
-                                        A32 + (size_t)i0 * M, CUDA_R_32F, M, A32 + (size_t)i0 * M,
-                                        CUDA_R_32F, M, &zerof, Pv, CUDA_R_32F, ldp,
-                                        CUBLAS_COMPUTE_32F_EMULATED_16BFX9,
-                                        CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
-                    emu = false;  // not supported by the loaded cuBLAS: fp64 DGEMM from here
-                if (emu) {
-                    sym_panel_kernel<float><<<4 * c->num_sms, 256, 0, c->stream>>>(
-                        static_cast<const float*>(Pv), ldp, I0, nI, ncols, c->N, o, b);
-                } else {
-                    if (cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, rows, ncols, M, &one,
-                                    Ab + (size_t)i0 * M, M, Ab + (size_t)i0 * M, M, &zero,
-                                    static_cast<double*>(Pv), ldp) != CUBLAS_STATUS_SUCCESS)
-                        return fail(CIMCS_CUDA_ERROR, "cublasDgemm failed");
-                    sym_panel_kernel<double><<<4 * c->num_sms, 256, 0, c->stream>>>(
-                        static_cast<const double*>(Pv), ldp, I0, nI, ncols, c->N, o, b);
-                }
-                CK(cudaGetLastError());
-            }
+            gt_absmax_kernel<<<8 * c->num_sms, 256, 0, c->stream>>>(Ab, (size_t)M * c->N, amax + b);
+            gt_split_kernel<<<8 * c->num_sms, 256, 0, c->stream>>>(Ab, M, c->N, Np, nch, amax + b, Pv);
+            CK(cudaGetLastError());
+            GtArgs ga{};
+            ga.P = Pv;
+            ga.amax = amax + b;
+            ga.out = SymOut{static_cast<__half*>(c->dG), c->dSg, c->nRB, c->ntri};
+            ga.b = b;
+            ga.N = c->N;
+            ga.Np = Np;
+            ga.nch = nch;
+            ga.I0 = Ib;
+            ga.I1 = Ie;
+            ga.nRB = c->nRB;
+            ga.ntile = ntile;
+            const int grid = (int)std::min<long long>(ntile, c->num_sms);
+            gram_tc_kernel<<<grid, kGtThreads, kGtSmem, c->stream>>>(ga);
+            CK(cudaGetLastError());
+            c->timing.other_launches += 3;
         }
         CK(cudaStreamSynchronize(c->stream));  // P is freed on return
     }

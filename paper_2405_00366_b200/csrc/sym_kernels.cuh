@@ -102,24 +102,6 @@ __host__ __device__ inline int sy_exp14(float m) {
 // exact 2^e as a float, |e| <= 126
 __device__ __forceinline__ float sy_pow2(int e) { return __int_as_float((127 + e) << 23); }
 
-// Gram panel from a library GEMM (large N, fp32 contexts): P[il][jc] (column-major,
-// ld = ldp) = G[i0 + il][i0 + jc] for the rows of nI row blocks starting at block I0;
-// the upper-triangle tiles are written as SymOut does.
-template <typename PT>
-__global__ void sym_panel_kernel(const PT* __restrict__ P, int ldp, int I0, int nI, int ncols,
-                                 int N, SymOut o, int b) {
-    const int i0 = I0 * kSyT;
-    const size_t total = (size_t)nI * kSyT * ncols;
-    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
-         t += (size_t)gridDim.x * blockDim.x) {
-        const int il = (int)(t % (nI * kSyT));
-        const int jc = (int)(t / (nI * kSyT));
-        const int i = i0 + il, j = i0 + jc;
-        if (i >= N || j >= N || j / kSyT < i / kSyT) continue;
-        o.store(b, i, j, (double)P[(size_t)jc * ldp + il]);
-    }
-}
-
 // s_G[b]: max |G| (= max diag) * 2^s_G in [2^14, 2^15)
 template <typename TS>
 __global__ void sym_scale_kernel(const TS* __restrict__ D, int N, int ldN, int* sg) {

@@ -8,9 +8,8 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
-# Load the CUDA library before any test module imports torch: its libcublas.so.12
-# (12.8) would otherwise shadow the system cuBLAS 12.9 that provides the fp32
-# emulation used by the large-N gram build (the library then falls back to DGEMM).
+# Load the CUDA library early (it pins torch's NCCL for the sharded contexts);
+# the test modules that import torch come later.
 try:
     from paper_2405_00366_b200 import _lib as _early
     _early.load()
