@@ -98,3 +98,25 @@ def test_pp_rejected_on_tensor_core_context(gpu, O):
         ctx.run_pp(1, gpu.HyperParams(n_steps=10), 0.5, np.zeros((1, 1, 640)),
                    np.array([1], np.uint64))
     ctx.close()
+
+
+def test_pp_on_fp64_large_n_needs_cuda_core_kernel(gpu, O):
+    """fp64 contexts with N > 512 run the DMMA symmetric path, whose epilogue is
+    the MFZ update only: Positive-P is a ConfigError there, and with sym64=0 (the
+    CUDA-core grid kernel) it runs and matches the oracle bitwise."""
+    insts = [O.gen_instance(600, 0.6, 0.2, 0.01, 2)]
+    R = 2
+    seeds = np.array([[O.mix_seed(2, 2 + 3 * r) for r in range(R)]], np.uint64)
+    p = O.Problem(insts[0], O.CANON)
+    Rs = np.stack([np.stack([p.hz] * R)])
+    ctx = _ctx(gpu, insts)
+    with pytest.raises(gpu.ConfigError):
+        ctx.run_pp(R, gpu.HyperParams(n_steps=10), 0.5, Rs, seeds)
+    ctx.close()
+    ctx = _ctx(gpu, insts, sym64=0)
+    out = ctx.run_pp(R, gpu.HyperParams(n_steps=70), 0.5, Rs, seeds)
+    ctx.close()
+    for r in range(R):
+        ref = p.run_pp(Rs[0, r], O.HyperParams(n_steps=70), 0.5, O.Rng(int(seeds[0, r])))
+        assert np.array_equal(out["mu_tilde"][0, r], ref["mu_tilde"])
+        assert np.array_equal(out["sigma"][0, r], ref["sigma"])

@@ -160,3 +160,18 @@ def test_solve_config1_shape_bitwise(gpu, O):
         assert np.array_equal(res["R"][0, r], ref["R"])
         assert np.array_equal(res["sigma"][0, r], ref["sigma"])
 
+
+
+def test_divergence_on_sym64_path(gpu, O):
+    """A blown-up trajectory on the DMMA path fails at the same alternation and
+    spin as the oracle (solver_mfz.cpp:75-85, orchestrator.cpp:222-227)."""
+    inst = O.gen_instance(600, 0.6, 0.2, 0.01, 5)
+    seed = O.mix_seed(5, 1)
+    ctx = _ctx(gpu, [inst])
+    order = ctx.canon_order()
+    res = ctx.solve(1, "mfz-bn", gpu.HyperParams(velo=2, dt=5.0, n_steps=50), [seed])
+    ctx.close()
+    ref = O.Problem(inst, O.CANON, *order).alternating_minimize(
+        O.MFZ_BN, O.HyperParams(velo=2, dt=5.0, n_steps=50), O.Rng(seed))
+    assert ref["failed"] and res["fail_alt"][0, 0] == ref["fail_alternation"]
+    assert res["fail_index"][0, 0] == ref["fail_index"]
