@@ -187,7 +187,7 @@ int launch_sym_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
 
 // fp64 symmetric-tile path (sym64_kernels.cuh): the DMMA tile kernel, then the
 // fused fp64 update, both on the context stream with PDL between them.
-template <int NR, int MODE>
+template <int NR, int MODE, int NC>
 int launch_sym64_t(cimcs_ctx* c, const GemvArgs& g) {
     Sym64Args sa{};
     sa.t = tc_args(c, g);
@@ -202,7 +202,7 @@ int launch_sym64_t(cimcs_ctx* c, const GemvArgs& g) {
     if (int rc = sym_schedule(c, c->B, &ss, true)) return rc;
     sa.items = ss->items;
     sa.sched = ss->sched;
-    auto kern = sym64_step_kernel<NR, MODE>;
+    auto kern = sym64_step_kernel<NR, MODE, NC>;
     constexpr size_t smem = s6_smem_bytes<NR>();
     static std::atomic<unsigned long long> attr{0};
     if (!(attr.load() >> c->device & 1ull)) {
@@ -214,7 +214,7 @@ int launch_sym64_t(cimcs_ctx* c, const GemvArgs& g) {
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ss->grid);
-    cfg.blockDim = dim3(kT6Threads);
+    cfg.blockDim = dim3((NC + 1) * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c->stream;
     cfg.attrs = at;
@@ -246,15 +246,22 @@ int launch_sym64_t(cimcs_ctx* c, const GemvArgs& g) {
     return 0;
 }
 
+template <int NR, int NC>
+int launch_sym64_nc(cimcs_ctx* c, int mode, const GemvArgs& a) {
+    switch (mode) {
+        case EPI_STEP_BN: return launch_sym64_t<NR, EPI_STEP_BN, NC>(c, a);
+        case EPI_STEP_CN: return launch_sym64_t<NR, EPI_STEP_CN, NC>(c, a);
+        case EPI_JACOBI: return launch_sym64_t<NR, EPI_JACOBI, NC>(c, a);
+        case EPI_MATVEC: return launch_sym64_t<NR, EPI_MATVEC, NC>(c, a);
+        default: return launch_sym64_t<NR, EPI_SCORE, NC>(c, a);
+    }
+}
+
+// 8 DMMA warps (4 per use): 16 warps measured slower (297 vs 291 us at config 1,
+// bitwise-equal results)
 template <int NR>
 int launch_sym64_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
-    switch (mode) {
-        case EPI_STEP_BN: return launch_sym64_t<NR, EPI_STEP_BN>(c, a);
-        case EPI_STEP_CN: return launch_sym64_t<NR, EPI_STEP_CN>(c, a);
-        case EPI_JACOBI: return launch_sym64_t<NR, EPI_JACOBI>(c, a);
-        case EPI_MATVEC: return launch_sym64_t<NR, EPI_MATVEC>(c, a);
-        default: return launch_sym64_t<NR, EPI_SCORE>(c, a);
-    }
+    return launch_sym64_nc<NR, 8>(c, mode, a);
 }
 
 // one mri_kernel launch of `grid` CTAs (basis vectors r0.. for DIAG / COLS)

@@ -45,8 +45,6 @@ namespace cimcs {
 constexpr int kT6 = 64;                         // tile edge
 constexpr int kS6 = 8;                          // item edge in tiles (512 = one segment)
 constexpr int kT6Stages = 3;
-constexpr int kT6Compute = 8;                   // DMMA warps (4 per use)
-constexpr int kT6Threads = (kT6Compute + 1) * 32;
 constexpr uint32_t kT6TileBytes = kT6 * kT6 * 8;  // 32 KB
 constexpr int kT6Seg = kT6 * kS6;               // canonical segment (512)
 
@@ -96,84 +94,101 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                  : "d"(a), "d"(b));
 }
 
+// Warp tiling of one use: WPU warps per use split the 64 x NR output block into
+// RW rows x (NT x 8) replicas each (MT = RW / 8 row fragments).  WPU = 4: 16 rows
+// x NR; WPU = 8 (NR 16): 16 rows x 8 replicas (more warps to hide the DMMA
+// issue latency, same chains per SM sub-partition).
+template <int NR, int WPU>
+struct S6Map {
+    static constexpr int NSPLIT = (NR / 8 >= 2 && WPU == 8) ? 2 : 1;  // warps across replicas
+    static constexpr int NT = NR / 8 / NSPLIT;
+    static constexpr int RW = 64 * NSPLIT / WPU;
+    static constexpr int MT = RW / 8;
+    __device__ static int m0(int u) { return (u / NSPLIT) * RW; }
+    __device__ static int n0(int u) { return (u % NSPLIT) * NT * 8; }
+};
+
 // One use of one tile for one warp: acc (MT x NT fragments, 2 doubles each)
-// += A(16 rows of the warp) * B(w tile).  use 1: A[m][k] = tile[m][k];
-// use 2: A[m][k] = tile[k][m].  k runs 0..63 ascending (4 per DMMA).
-template <int NR, bool kT>
+// += A(rows m0.. of the warp) * B(w tile, replicas n0..).  use 1: A[m][k] =
+// tile[m][k]; use 2: A[m][k] = tile[k][m].  k runs 0..63 ascending (4 per DMMA).
+template <int NR, int MT, int NT, bool kT>
 __device__ __forceinline__ void s6_tile_mma(const double* __restrict__ tile,
-                                            const double* __restrict__ wt, int m0, int lane,
-                                            double (&acc)[2][NR / 8][2]) {
-    constexpr int NT = NR / 8;
+                                            const double* __restrict__ wt, int m0, int n0,
+                                            int lane, double (&acc)[MT][NT][2]) {
     const int g = lane >> 2, t = lane & 3;
-    double a[2], b[NT], an[2], bn[NT];
-    auto load = [&](int k0, double (&aa)[2], double (&bb)[NT]) {
+    double a[MT], b[NT], an[MT], bn[NT];
+    auto load = [&](int k0, double (&aa)[MT], double (&bb)[NT]) {
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
+        for (int mt = 0; mt < MT; ++mt) {
             const int m = m0 + 8 * mt + g, k = k0 + t;
             aa[mt] = kT ? tile[s6_gofs(k, m)] : tile[s6_gofs(m, k)];
         }
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) bb[nt] = wt[s6_wofs<NR>(k0 + t, 8 * nt + g)];
+        for (int nt = 0; nt < NT; ++nt) bb[nt] = wt[s6_wofs<NR>(k0 + t, n0 + 8 * nt + g)];
     };
     load(0, a, b);
 #pragma unroll
     for (int k0 = 0; k0 < kT6; k0 += 4) {
         if (k0 + 4 < kT6) load(k0 + 4, an, bn);
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
         if (k0 + 4 < kT6) {
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt) a[mt] = an[mt];
+            for (int mt = 0; mt < MT; ++mt) a[mt] = an[mt];
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) b[nt] = bn[nt];
         }
     }
 }
 
-// accumulator fragments <-> a [64][NR] block (row-major, padded stride NR + 1
-// doubles would break 16-B alignment; a plain [64][NR] with the C-fragment
+// accumulator fragments <-> a [64][NR] block (row-major; the C-fragment
 // pattern g*NR + 2t hits 8 distinct 16-B columns per quarter-warp)
-template <int NR>
-__device__ __forceinline__ void s6_acc_ld(const double* blk, int m0, int lane,
-                                          double (&acc)[2][NR / 8][2]) {
+template <int NR, int MT, int NT>
+__device__ __forceinline__ void s6_acc_ld(const double* blk, int m0, int n0, int lane,
+                                          double (&acc)[MT][NT][2]) {
     const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NR / 8; ++nt) {
-            const double2 v =
-                *reinterpret_cast<const double2*>(blk + (m0 + 8 * mt + g) * NR + 8 * nt + 2 * t);
+        for (int nt = 0; nt < NT; ++nt) {
+            const double2 v = *reinterpret_cast<const double2*>(
+                blk + (m0 + 8 * mt + g) * NR + n0 + 8 * nt + 2 * t);
             acc[mt][nt][0] = v.x;
             acc[mt][nt][1] = v.y;
         }
 }
-template <int NR>
-__device__ __forceinline__ void s6_acc_st(double* blk, int m0, int lane,
-                                          const double (&acc)[2][NR / 8][2]) {
+template <int NR, int MT, int NT>
+__device__ __forceinline__ void s6_acc_st(double* blk, int m0, int n0, int lane,
+                                          const double (&acc)[MT][NT][2]) {
     const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NR / 8; ++nt)
-            *reinterpret_cast<double2*>(blk + (m0 + 8 * mt + g) * NR + 8 * nt + 2 * t) =
+        for (int nt = 0; nt < NT; ++nt)
+            *reinterpret_cast<double2*>(blk + (m0 + 8 * mt + g) * NR + n0 + 8 * nt + 2 * t) =
                 make_double2(acc[mt][nt][0], acc[mt][nt][1]);
 }
-template <int NR>
-__device__ __forceinline__ void s6_acc_zero(double (&acc)[2][NR / 8][2]) {
+template <int MT, int NT>
+__device__ __forceinline__ void s6_acc_zero(double (&acc)[MT][NT][2]) {
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NR / 8; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+        for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
 }
 
+template <int NC>
 __device__ __forceinline__ void s6_bar(int id) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kT6Compute * 32) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NC * 32) : "memory");
 }
 
-template <int NR, int MODE>
-__global__ void __launch_bounds__(kT6Threads, 1) sym64_step_kernel(Sym64Args sa) {
+// NC = DMMA warps (NC / 2 per use); one more warp produces.
+template <int NR, int MODE, int NC>
+__global__ void __launch_bounds__((NC + 1) * 32, 1) sym64_step_kernel(Sym64Args sa) {
+    constexpr int kT6Compute = NC;
+    using Map = S6Map<NR, NC / 2>;
+    constexpr int MT = Map::MT, NT = Map::NT;
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr size_t kStage = s6_stage_bytes<NR>();
     constexpr size_t kWB = s6_wbytes<NR>();
@@ -252,9 +267,10 @@ __global__ void __launch_bounds__(kT6Threads, 1) sym64_step_kernel(Sym64Args sa)
         return;
     }
     // ---------------------------------------------------------- DMMA warps
-    const bool use2 = warp >= 4;
-    const int m0 = (warp & 3) * 16;  // this warp's 16 rows (use 1) / columns (use 2)
-    double racc[2][NR / 8][2];
+    const bool use2 = warp >= NC / 2;
+    const int u = warp % (NC / 2);
+    const int m0 = Map::m0(u), n0 = Map::n0(u);  // rows (use 1) / columns (use 2), replicas
+    double racc[MT][NT][2];
     int tt = 0;
     for (int k = it0; k < it1; ++k) {
         int b, P, Q, nI, nJ;
@@ -265,11 +281,12 @@ __global__ void __launch_bounds__(kT6Threads, 1) sym64_step_kernel(Sym64Args sa)
         // groups touch the same rows of a diagonal item's blocks)
         if (use2) {
             for (int kb = 0; kb < nblk; ++kb)
-                for (int e = lane; e < 16 * NR; e += 32) accs[kb * kBlk + m0 * NR + e] = 0.0;
+                for (int e = lane; e < Map::RW * NT * 8; e += 32)
+                    accs[kb * kBlk + (m0 + e / (NT * 8)) * NR + n0 + e % (NT * 8)] = 0.0;
         }
-        s6_bar(1);
+        s6_bar<NC>(1);
         for (int ii = 0; ii < nI; ++ii) {
-            if (!use2) s6_acc_zero<NR>(racc);
+            if (!use2) s6_acc_zero<MT, NT>(racc);
             for (int jj = diag ? ii : 0; jj < nJ; ++jj, ++tt) {
                 const int I = P * kS6 + ii, J = Q * kS6 + jj, s = tt % kT6Stages;
                 mbar_wait(&full[s], (tt / kT6Stages) & 1);
@@ -278,27 +295,27 @@ __global__ void __launch_bounds__(kT6Threads, 1) sym64_step_kernel(Sym64Args sa)
                 const double* wI = wJ + kT6 * NR;
                 if (!use2) {
                     if (diag) {  // use 1 into block ii's shared accumulator
-                        double acc[2][NR / 8][2];
-                        s6_acc_ld<NR>(accs + ii * kBlk, m0, lane, acc);
-                        s6_tile_mma<NR, false>(tile, wJ, m0, lane, acc);
-                        s6_acc_st<NR>(accs + ii * kBlk, m0, lane, acc);
+                        double acc[MT][NT][2];
+                        s6_acc_ld<NR, MT, NT>(accs + ii * kBlk, m0, n0, lane, acc);
+                        s6_tile_mma<NR, MT, NT, false>(tile, wJ, m0, n0, lane, acc);
+                        s6_acc_st<NR, MT, NT>(accs + ii * kBlk, m0, n0, lane, acc);
                     } else {
-                        s6_tile_mma<NR, false>(tile, wJ, m0, lane, racc);
+                        s6_tile_mma<NR, MT, NT, false>(tile, wJ, m0, n0, lane, racc);
                     }
                 } else if (I != J) {  // use 2 into column block jj
-                    double acc[2][NR / 8][2];
-                    s6_acc_ld<NR>(accs + jj * kBlk, m0, lane, acc);
-                    s6_tile_mma<NR, true>(tile, wI, m0, lane, acc);
-                    s6_acc_st<NR>(accs + jj * kBlk, m0, lane, acc);
+                    double acc[MT][NT][2];
+                    s6_acc_ld<NR, MT, NT>(accs + jj * kBlk, m0, n0, lane, acc);
+                    s6_tile_mma<NR, MT, NT, true>(tile, wI, m0, n0, lane, acc);
+                    s6_acc_st<NR, MT, NT>(accs + jj * kBlk, m0, n0, lane, acc);
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
             }
             if (diag) {
-                s6_bar(1);  // use-2 of rows <= ii lands before use 1 of row ii + 1
+                s6_bar<NC>(1);  // use-2 of rows <= ii lands before use 1 of row ii + 1
             } else if (!use2) {  // row block I complete for this item: slot Q
                 double* p = sa.part + ((((size_t)b * nRB + P * kS6 + ii) * nSB + Q) * kT6) * NR;
-                s6_acc_st<NR>(p, m0, lane, racc);
+                s6_acc_st<NR, MT, NT>(p, m0, n0, lane, racc);
             }
         }
         // item done: shared accumulators -> partials (slot P)
@@ -306,12 +323,14 @@ __global__ void __launch_bounds__(kT6Threads, 1) sym64_step_kernel(Sym64Args sa)
             const int J0 = (diag ? P : Q) * kS6;
             for (int kb = 0; kb < nblk; ++kb) {
                 double* p = sa.part + ((((size_t)b * nRB + J0 + kb) * nSB + P) * kT6) * NR;
-                const double2* src = reinterpret_cast<const double2*>(accs + kb * kBlk + m0 * NR);
-                double2* dst = reinterpret_cast<double2*>(p + m0 * NR);
-                for (int e = lane; e < 16 * NR / 2; e += 32) dst[e] = src[e];
+                for (int e = lane; e < Map::RW * NT * 4; e += 32) {  // 2 doubles per element
+                    const int r = m0 + e / (NT * 4), cc = n0 + 2 * (e % (NT * 4));
+                    *reinterpret_cast<double2*>(p + r * NR + cc) =
+                        *reinterpret_cast<const double2*>(accs + kb * kBlk + r * NR + cc);
+                }
             }
         }
-        s6_bar(1);  // accumulators free for the next item
+        s6_bar<NC>(1);  // accumulators free for the next item
     }
 }
 

@@ -25,3 +25,24 @@ def test_reference_arm_json_line():
     assert cb["value"] == line["value"]
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert line["config"]["workload"].startswith("BASELINE config 1")
+
+
+def test_gpus_flag_relaunches_under_torchrun(monkeypatch):
+    """bench.py --gpus N outside torchrun relaunches itself with N ranks on this
+    node (127.0.0.1 rendezvous); under torchrun (WORLD_SIZE set) it does not."""
+    import importlib
+    sys.path.insert(0, ROOT)
+    bench = importlib.import_module("bench")
+    calls = []
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: calls.append(cmd) or 0)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "2"])
+    try:
+        bench.main()
+    except SystemExit as e:
+        assert e.code == 0
+    assert len(calls) == 1
+    cmd = calls[0]
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "2"]

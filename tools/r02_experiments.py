@@ -150,6 +150,31 @@ def f64perf():
     print(json.dumps(out, indent=1))
 
 
+def sym64warps():
+    """DMMA tile kernel with 8 vs 16 DMMA warps: per-step time, bitwise-equal results."""
+    insts, R, hp, _ = W.config1(0, 64)
+    hp = P.baseline_params(velo=3, n_steps=1000)
+    seeds = P.replica_seeds(insts, R, "mfz-bn")
+    out, res = {}, {}
+    for nw in (8, 16):
+        with P.Context(0, "f64") as ctx:
+            ctx.set_option("sym64_warps", nw)
+            ctx.set_problems(insts)
+            ctx.build_coupling()
+            ctx.solve(R, "mfz-bn", hp, seeds)
+            res[nw] = ctx.solve(R, "mfz-bn", hp, seeds)
+            t = ctx.timing()
+            out[nw] = {"us_per_step": t["cim_ms"] / 4000 * 1e3, "refit_ms": t["refit_ms"]}
+            ctx.set_option("use_graphs", 0)
+            ctx.set_option("kernel_timing", 1)
+            ctx.solve(R, "mfz-bn", P.baseline_params(velo=1, n_steps=100), seeds)
+            tk = ctx.timing()
+            out[nw]["tile_us"] = tk["tile_kernel_ms"] / tk["tile_kernel_launches"] * 1e3
+    out["bitwise_equal"] = bool(np.array_equal(res[8]["R"], res[16]["R"]) and
+                                np.array_equal(res[8]["sigma"], res[16]["sigma"]))
+    print(json.dumps(out, indent=1))
+
+
 def l2groups():
     insts, R, hp, _ = W.config1(0, 64)
     hp1 = P.baseline_params(velo=1, n_steps=500)  # 2 x 500 steps
