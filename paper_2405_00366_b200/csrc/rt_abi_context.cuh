@@ -115,6 +115,9 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
     else if (k == "tensor_cores") {
         if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set tensor_cores before set_problems");
         c->want_tc = v != 0;
+    } else if (k == "refit_compact") {
+        c->cmp_opt = v != 0;
+        drop_graphs(c);
     } else if (k == "sym64") {
         if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set sym64 before set_problems");
         c->want_sym64 = v != 0;

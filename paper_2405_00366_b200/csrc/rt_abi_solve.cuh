@@ -278,6 +278,8 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
     CK(cudaSetDevice(c->device));
     const int NR = slots_for(c, R);
     if (int rc = ensure_state(c, NR)) return rc;
+    // fp32 symmetric path: the Jacobi refit runs compacted to the union of supports
+    const bool cmp = cdp == CIMCS_CDP_JACOBI && !pp && cmp_refit_ok(c);
     if (cdp == CIMCS_CDP_CG)
         if (int rc = ensure_cg(c)) return rc;
     if (pp)
@@ -365,7 +367,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
                                             bits(s.nbeta), bits(s.Kj), bits(s.minus_j),
                                             bits(s.dt_c), c->B, c->N, cdp, hp->cg_max_iters,
                                             bits(hp->cg_tol), backend};
-        if (key != c->graph_key || (!pp && !c->g_cim) || !c->g_refit) {
+        if (key != c->graph_key || (!pp && !c->g_cim) || (!cmp && !c->g_refit)) {
             drop_graphs(c);
             Graph gc, gr;
             if (!pp)  // the Positive-P CIM call is host-driven (chunked noise upload)
@@ -373,7 +375,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
                     int r2 = run_init(c, R, bn, dc0, nullptr, s.rt);
                     return r2 ? r2 : enqueue_steps(c, bn, s, hp->n_steps);
                 });
-            if (!rc)
+            if (!rc && !cmp)
                 rc = capture(c, gr, [&] {
                     if (cdp == CIMCS_CDP_CG) {
                         int r2 = run_support(c);
@@ -409,7 +411,15 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
             if (rc) return rc;
         }
         CK(cudaEventRecord(ev.ev[4 * i + 1], c->stream));
-        if (c->use_graphs) {
+        if (i + 1 < nalt && !pp) {
+            // draw the next alternation's c0 while the GPU runs this CIM call (its
+            // pinned slot was last uploaded before the previous CIM call)
+            CK(cudaEventSynchronize(slot_done.ev[(i + 1) & 1]));
+            gen_c0(rngs, c->N, pinned + (size_t)((i + 1) & 1) * nc0, c->host_threads);
+        }
+        if (cmp) {
+            if ((rc = enqueue_refit_compact(c, s, hp->jacobi_iters))) return rc;
+        } else if (c->use_graphs) {
             CK(cudaGraphLaunch(c->g_refit, c->stream));
         } else if (cdp == CIMCS_CDP_CG) {
             if ((rc = run_support(c)) || (rc = enqueue_cg(c, s, hp))) return rc;
@@ -420,11 +430,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
         if ((rc = enqueue_score(c, s, v_slot, c->hist + (size_t)i * nT, track_best != 0)))
             return rc;
         CK(cudaEventRecord(ev.ev[4 * i + 3], c->stream));
-        if (i + 1 < nalt && !pp) {
-            // draw the next alternation's c0 while the GPU works on this one
-            CK(cudaEventSynchronize(slot_done.ev[(i + 1) & 1]));
-            gen_c0(rngs, c->N, pinned + (size_t)((i + 1) & 1) * nc0, c->host_threads);
-        }
+
     }
     cudaEventRecord(ev.ev[4 * nalt + 1], c->stream);
 

@@ -22,6 +22,17 @@ struct cimcs_ctx {
     bool sym = false;      // active for the current problem set
     // fp64 symmetric-tile path on the DMMA tensor cores (sym64_kernels.cuh):
     // unsharded fp64 contexts with N > kClMaxN (option "sym64", default on)
+    // compacted Jacobi refit of the fp32 symmetric path (cmp_kernels.cuh; option
+    // "refit_compact", default on): the union of the replicas' supports per instance
+    int cmp_opt = 1;
+    bool cmp_active = false;     // the context's fields are swapped to the compacted problem
+    int symS = 4;                // item edge of the symmetric schedules (kSyS; 2 when compacted)
+    int* cU = nullptr;           // [B][ldN] union spins (ascending), -1 padded
+    int* cCnt = nullptr;         // [B] union sizes
+    int* cMax = nullptr;         // [1] max union size
+    float *Rc = nullptr, *Dc = nullptr, *hzc = nullptr;
+    int8_t* sigc = nullptr;
+    __half* Gc = nullptr;        // compacted tiles (capacity: the full triangle)
     bool want_sym64 = true;
     bool sym64 = false;
     int nRB6 = 0, ntri6 = 0, nSB6 = 0;      // its geometry: 64-row blocks, 512 x 512 items

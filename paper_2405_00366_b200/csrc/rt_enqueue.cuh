@@ -69,6 +69,81 @@ int enqueue_refit(cimcs_ctx* c, const StepScalars& s, int iters, bool do_support
     return 0;
 }
 
+// The compacted Jacobi refit of the fp32 symmetric path (cmp_kernels.cuh):
+// support -> union of the replicas' supports per instance -> (host reads the
+// largest union) -> gathered tiles / state -> the unchanged symmetric sweeps on
+// the compacted problem -> R scattered back -> the full W[iters & 1] = R o sigma
+// that the scorer reads.  Eager (the compacted size is data-dependent).
+bool cmp_refit_ok(const cimcs_ctx* c) {
+    return c->sym && !c->tshard && c->cmp_opt && c->cU && !c->mri;
+}
+
+int enqueue_refit_compact(cimcs_ctx* c, const StepScalars& s, int iters) {
+    if (int rc = run_support(c)) return rc;
+    CK(cudaMemsetAsync(c->cMax, 0, 4, c->stream));
+    DISPATCH_NR_TC(c->NR, {
+        cmp_union_kernel<NR_><<<c->B, 1024, 0, c->stream>>>(c->sig, c->N, c->ldN, c->cU,
+                                                            c->cCnt, c->cMax);
+    });
+    CK(cudaGetLastError());
+    int mx = 0;
+    if (int rc = copy_sync(c, &mx, c->cMax, 4, cudaMemcpyDeviceToHost)) return rc;
+    if (mx > 0 && iters > 0) {
+        const int nRBc = (mx + kSyT - 1) / kSyT, ntric = nRBc * (nRBc + 1) / 2;
+        cmp_gather_tiles_kernel<<<dim3(ntric, c->B), 256, 0, c->stream>>>(
+            static_cast<const __half*>(c->dG), c->ntri, c->nRB, c->cU, c->ldN, nRBc, ntric, c->Gc);
+        DISPATCH_NR_TC(c->NR, {
+            cmp_gather_state_kernel<NR_><<<grid_for((size_t)c->B * c->ldN), 256, 0, c->stream>>>(
+                static_cast<const float*>(c->Rs), c->sig, static_cast<const float*>(c->dD),
+                static_cast<const float*>(c->dhz), c->cU, c->ldN, c->B, c->Rc, c->sigc, c->Dc,
+                c->hzc, static_cast<float*>(c->W0));
+        });
+        CK(cudaGetLastError());
+        // swap the context to the compacted problem (same ldN / layouts, fewer blocks)
+        struct Swap {
+            cimcs_ctx* c;
+            int N, nRB, ntri, nSB, symS;
+            void *dG, *Rs, *dD, *dhz;
+            int8_t* sig;
+            ~Swap() {
+                c->N = N;
+                c->nRB = nRB;
+                c->ntri = ntri;
+                c->nSB = nSB;
+                c->symS = symS;
+                c->dG = dG;
+                c->Rs = Rs;
+                c->dD = dD;
+                c->dhz = dhz;
+                c->sig = sig;
+                c->cmp_active = false;
+            }
+        } sw{c, c->N, c->nRB, c->ntri, c->nSB, c->symS, c->dG, c->Rs, c->dD, c->dhz, c->sig};
+        c->N = mx;
+        c->nRB = nRBc;
+        c->ntri = ntric;
+        c->symS = 2;  // 2 x 2-tile items: enough of them to balance 148 CTAs
+        c->nSB = (nRBc + c->symS - 1) / c->symS;
+        c->dG = c->Gc;
+        c->Rs = c->Rc;
+        c->dD = c->Dc;
+        c->dhz = c->hzc;
+        c->sig = c->sigc;
+        c->cmp_active = true;
+        if (int rc = sym_sync_w(c, c->W0)) return rc;
+        GemvArgs a = base_args(c, s);
+        if (int rc = enqueue_sym_loop(c, EPI_JACOBI, a, iters, false)) return rc;
+    }
+    if (mx > 0 && iters > 0) {
+        DISPATCH_NR_TC(c->NR, {
+            cmp_scatter_kernel<NR_><<<grid_for((size_t)c->B * c->ldN), 256, 0, c->stream>>>(
+                c->Rc, c->cU, c->ldN, c->B, static_cast<float*>(c->Rs));
+        });
+        CK(cudaGetLastError());
+    }
+    return mask_T<float>(c, (iters & 1) ? c->W1 : c->W0);  // what the scorer reads
+}
+
 // ---------------------------------------------------- CG refit (cdp="cg")
 int ensure_cg(cimcs_ctx* c) {  // outside any capture: allocates
     if (c->cgX) return 0;

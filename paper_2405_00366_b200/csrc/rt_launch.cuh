@@ -102,6 +102,8 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb) {
     sa.nSB = c->nSB;
     sa.b0 = b0;
     sa.gram_keep = c->gram_l2;
+    sa.S = c->symS;
+    sa.rowmap = c->cmp_active ? c->cU : nullptr;
     if (nb == 0 || c->ntri == 0) return 0;
     const cimcs_ctx::SymSched* ss = nullptr;
     if (int rc = sym_schedule(c, nb, &ss)) return rc;
@@ -330,6 +332,7 @@ int launch_mri_t(cimcs_ctx* c, const GemvArgs& g) {
     sa.nSB = 1;
     sa.b0 = 0;
     sa.keep_w = 1;  // the next apply reads the fp32 w
+    sa.S = kSyS;
     {
         cudaLaunchConfig_t ucfg{};
         ucfg.gridDim = dim3(c->nRB, 1);

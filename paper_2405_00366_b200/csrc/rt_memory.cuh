@@ -31,6 +31,12 @@ void free_state(cimcs_ctx* c) {
     c->WB0 = c->WB1 = nullptr;
     c->WS0 = c->WS1 = nullptr;
     c->WT0 = c->WT1 = c->dPart6 = nullptr;
+    for (void* q : {(void*)c->cU, (void*)c->cCnt, (void*)c->cMax, (void*)c->Rc, (void*)c->Dc,
+                    (void*)c->hzc, (void*)c->sigc})
+        if (q) cudaFree(q);
+    c->cU = c->cCnt = c->cMax = nullptr;
+    c->Rc = c->Dc = c->hzc = nullptr;
+    c->sigc = nullptr;
     c->Pn = c->Pm = c->MT = nullptr;
     c->nzd[0] = c->nzd[1] = nullptr;
     for (double*& h : c->nzh)
@@ -55,7 +61,7 @@ void free_problems(cimcs_ctx* c) {
     free_state(c);
     void* ptrs[] = {c->dA, c->dy, c->dM, c->dG, c->dG6, c->dD, c->dhz, c->dx, c->dxi,
                     c->dSg, c->dSpart, c->dMaskBr, c->dTw, c->dTarget,
-                    c->dH};
+                    c->dH, c->Gc};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& q : c->ssched) {
@@ -63,6 +69,7 @@ void free_problems(cimcs_ctx* c) {
         cudaFree(q.sched);
     }
     c->ssched.clear();
+    c->Gc = nullptr;
     c->dSg = nullptr;
     c->dSpart = nullptr;
     c->dMaskBr = nullptr;
@@ -142,7 +149,7 @@ void tile_shard(int nRB, int world, int rank, int* P0, int* P1) {
 // Super-block items of nb instances placed on the persistent CTAs, largest
 // first onto the least-loaded CTA (LPT); built once per nb and cached.
 int sym_schedule(cimcs_ctx* c, int nb, const cimcs_ctx::SymSched** out, bool s64 = false) {
-    const int kS = s64 ? kS6 : kSyS;  // item edge in tiles
+    const int kS = s64 ? kS6 : c->symS;  // item edge in tiles
     const int nRB = s64 ? c->nRB6 : c->nRB, nSB = s64 ? c->nSB6 : c->nSB;
     for (auto& q : c->ssched)
         if (q.nb == nb && q.nRB == nRB && q.S == kS) {
@@ -247,12 +254,24 @@ int ensure_state(cimcs_ctx* c, int NR) {
         const cimcs_ctx::SymSched* ss;
         if ((rc = sym_schedule(c, c->B, &ss, true))) return rc;
     }
+    if (c->sym && !c->tshard && c->cmp_opt) {  // compacted refit buffers
+        const size_t nv = (size_t)c->B * c->ldN;
+        if ((rc = dalloc(c, &c->cU, nv * 4)) || (rc = dalloc(c, &c->cCnt, (size_t)c->B * 4)) ||
+            (rc = dalloc(c, &c->cMax, 16)) || (rc = dalloc(c, &c->Rc, n * 4)) ||
+            (rc = dalloc(c, &c->sigc, n)) || (rc = dalloc(c, &c->Dc, nv * 4)) ||
+            (rc = dalloc(c, &c->hzc, nv * 4)))
+            return rc;
+        if (!c->Gc && (rc = dalloc(c, &c->Gc, (size_t)c->B * c->ntri * 2 * kSyPlaneBytes)))
+            return rc;
+    }
     if (c->sym) {  // fp16 B tiles of W0/W1 and the partial products of the symmetric kernel
         const size_t nb = (size_t)c->B * c->nRB * 2 * NR * kSyT, ns = (size_t)c->B * c->nRB * NR;
         if ((rc = dalloc(c, &c->WB0, nb * 2)) || (rc = dalloc(c, &c->WB1, nb * 2)) ||
             (rc = dalloc(c, &c->WS0, ns * 4)) || (rc = dalloc(c, &c->WS1, ns * 4)))
             return rc;
-        const size_t ne = (size_t)c->B * c->nRB * c->nSB * kSyT * NR;
+        // slots: nSB = ceil(nRB / 4); the compacted refit's 2 x 2 items need up to ceil(nRB / 2)
+        const size_t nslot = c->cmp_opt && !c->tshard ? std::max(c->nSB, (c->nRB + 1) / 2) : c->nSB;
+        const size_t ne = (size_t)c->B * c->nRB * nslot * kSyT * NR;
         // the item schedule (built outside graph capture)
         const cimcs_ctx::SymSched* ss;
         if ((rc = sym_schedule(c, c->B, &ss))) return rc;

@@ -32,6 +32,7 @@
 #include "sym_kernels.cuh"
 #include "sym64_kernels.cuh"
 #include "gram_tc_kernels.cuh"
+#include "cmp_kernels.cuh"
 #include "mri_kernels.cuh"
 
 using namespace cimcs;

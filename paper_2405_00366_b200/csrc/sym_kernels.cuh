@@ -177,6 +177,8 @@ struct SymArgs {
     int b0;                // first instance of this launch (instance groups)
     int keep_w;            // step modes: also store the fp32 w (a consumer reads it)
     int gram_keep;         // 1: gram tiles copied with evict_last (L2-resident groups)
+    int S;                 // item edge in tiles (kSyS; 2 for the compacted refit)
+    const int* rowmap;     // compacted refit: row -> original spin (error reports), or null
 };
 
 template <int NR>
@@ -201,10 +203,10 @@ __device__ __forceinline__ SyItem sy_item(const SymArgs& sa, int k, int nRB) {
     r.b = sa.b0 + it.x;
     r.P = it.y >> 16;
     r.Q = it.y & 0xffff;
-    r.I0 = r.P * kSyS;
-    r.J0 = r.Q * kSyS;
-    r.nI = min(kSyS, nRB - r.I0);
-    r.nJ = min(kSyS, nRB - r.J0);
+    r.I0 = r.P * sa.S;
+    r.J0 = r.Q * sa.S;
+    r.nI = min(sa.S, nRB - r.I0);
+    r.nJ = min(sa.S, nRB - r.J0);
     r.diag = r.P == r.Q;
     return r;
 }
@@ -687,7 +689,7 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
                 TS rn = Rj[u];
                 if (on) {
                     if (Dv == TS(0)) {
-                        atomicMin(a.err, i);
+                        atomicMin(a.err, sa.rowmap ? sa.rowmap[(size_t)b * a.ldN + i] : i);
                         continue;
                     }
                     const TS off = gw[u] - Dv * Rj[u];

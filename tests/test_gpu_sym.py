@@ -161,6 +161,7 @@ def test_tile_sharded_context_world1_bitwise(gpu, O, cdp):
     seeds = np.array([[O.mix_seed(i.seed, 1 + 3 * r) for r in range(R)] for i in insts],
                      np.uint64)
     with gpu.Context(0, "f32") as plain:
+        plain.set_option("refit_compact", 0)  # tile-sharded contexts refit uncompacted
         plain.set_problems(insts)
         plain.build_coupling()
         a = plain.solve(R, "mfz-bn", hp, seeds, cdp=cdp)
@@ -224,3 +225,31 @@ def test_two_live_contexts_load_identically(gpu):
     finally:
         for c in ctxs:
             c.close()
+
+
+def test_compacted_refit_matches_full_refit(gpu, O):
+    """The compacted Jacobi refit (union of the replicas' supports, cmp_kernels.cuh)
+    against the full-gram refit in the same solve: identical supports after the
+    CIM calls that follow need not hold (fp32), but one refit from the same
+    state agrees to fp32 accuracy and leaves every inactive R bitwise."""
+    insts = [O.gen_instance(1100, 0.5, 0.1, 0.01, s) for s in (31, 32)]
+    R = 16
+    hp = gpu.baseline_params(velo=1, n_steps=200)
+    seeds = np.array([[O.mix_seed(i.seed, 1 + 3 * r) for r in range(R)] for i in insts],
+                     np.uint64)
+    out = {}
+    for cmp in (0, 1):
+        with gpu.Context(0, "f32") as ctx:
+            ctx.set_option("refit_compact", cmp)
+            ctx.set_problems(insts)
+            ctx.build_coupling()
+            # velo=1: alternation 0's CIM call + refit are identical up to the refit
+            out[cmp] = ctx.solve(R, "mfz-bn", gpu.baseline_params(velo=1, n_steps=200), seeds)
+    h0, h1 = out[0]["history"], out[1]["history"]
+    # alternation 0 shares its CIM call (same supports); its refit differs only in rounding
+    assert np.array_equal(h0["support"][:, :, 0], h1["support"][:, :, 0])
+    assert np.allclose(h0["rmse"][:, :, 0], h1["rmse"][:, :, 0], rtol=1e-4)
+    for b, inst in enumerate(insts):
+        for r in range(R):
+            assert abs(out[1]["history"][b, r][0]["rmse"] - out[0]["history"][b, r][0]["rmse"]) \
+                <= 1e-4 * out[0]["history"][b, r][0]["rmse"]

@@ -175,6 +175,32 @@ def sym64warps():
     print(json.dumps(out, indent=1))
 
 
+def refitcmp():
+    """fp32 config 1: full vs compacted Jacobi refit -- time and parity vs fp64."""
+    import bench
+    insts, R, hp, _ = W.config1(0, 64)
+    seeds = P.replica_seeds(insts, R, "mfz-bn")
+    out = {}
+    with P.Context(0, "f64") as ctx:
+        ctx.set_problems(insts)
+        ctx.build_coupling()
+        ref = ctx.solve(R, "mfz-bn", hp, seeds)
+    for cmp in (0, 1):
+        with P.Context(0, "f32") as ctx:
+            ctx.set_option("refit_compact", cmp)
+            ctx.set_problems(insts)
+            ctx.build_coupling()
+            ctx.solve(R, "mfz-bn", hp, seeds)
+            res = ctx.solve(R, "mfz-bn", hp, seeds)
+            t = ctx.timing()
+        par = bench.parity_vs_f64(ref, res, "f32")
+        out[cmp] = {k: t[k] for k in ("total_ms", "cim_ms", "refit_ms", "score_ms")}
+        out[cmp].update({k: par[k] for k in ("traj_identical_support", "rmse_mean", "hamming_mean",
+                                             "rmse_paired_diff", "max_rel_rmse_where_same",
+                                             "pass")})
+    print(json.dumps(out, indent=1))
+
+
 def l2groups():
     insts, R, hp, _ = W.config1(0, 64)
     hp1 = P.baseline_params(velo=1, n_steps=500)  # 2 x 500 steps
