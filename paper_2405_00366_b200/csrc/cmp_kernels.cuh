@@ -14,6 +14,7 @@
 #pragma once
 
 #include "sym_kernels.cuh"
+#include "sym64_kernels.cuh"
 
 namespace cimcs {
 
@@ -144,6 +145,119 @@ __global__ void cmp_gather_state_kernel(const float* __restrict__ Rs, const int8
 template <int NR>
 __global__ void cmp_scatter_kernel(const float* __restrict__ Rc, const int* __restrict__ cU,
                                    int ldN, int B, float* Rs) {
+    const size_t total = (size_t)B * ldN;
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+         t += (size_t)gridDim.x * blockDim.x) {
+        const int i = cU[t];
+        if (i < 0) continue;
+        const size_t si = (size_t)(t / ldN) * ldN + i;
+#pragma unroll
+        for (int q = 0; q < NR; ++q) Rs[si * NR + q] = Rc[t * NR + q];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// The fp64 (DMMA) path's compacted refit keeps the oracle order BITWISE: the
+// canonical order sums 512-column segments left to right, each an ascending
+// fma chain, and fma(g, +-0, acc) == acc exactly (acc is never -0: chains
+// start at +0), so dropping the zero w of non-union spins changes nothing as
+// long as no compacted 64-column block mixes two original segments.  Each
+// original segment s is therefore compacted on its own, padded to a multiple of
+// 64 (the batch maximum), and segments no instance uses are dropped (their
+// partial is an exact +0).  The DMMA kernels then run on the variable-width
+// segments (Sym64Args::seg).
+namespace cmp64 {
+constexpr int kSeg = 512;     // the canonical segment (oracle CANON gran)
+constexpr int kMaxSeg = 256;  // oracle P[256]: N <= 131072
+}
+
+// per (instance, original segment): union spins in it
+__global__ void cmp64_segcount_kernel(const int* __restrict__ cU, const int* __restrict__ cnt,
+                                      int ldN, int nseg, int B, int* segc) {
+    const size_t total = (size_t)B * ldN;
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+         t += (size_t)gridDim.x * blockDim.x) {
+        const int b = (int)(t / ldN), k = (int)(t % ldN);
+        if (k < cnt[b]) atomicAdd(&segc[b * nseg + cU[t] / cmp64::kSeg], 1);
+    }
+}
+
+// compacted index -> original spin: segment s of instance b starts at segoff[s]
+// (-1: dropped) and holds its union spins in ascending order
+__global__ void cmp64_map_kernel(const int* __restrict__ cU, const int* __restrict__ cnt,
+                                 const int* __restrict__ segpfx, const int* __restrict__ segoff,
+                                 int ldN, int nseg, int B, int* cU6) {
+    const size_t total = (size_t)B * ldN;
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+         t += (size_t)gridDim.x * blockDim.x) {
+        const int b = (int)(t / ldN), k = (int)(t % ldN);
+        if (k >= cnt[b]) continue;
+        const int i = cU[t], s = i / cmp64::kSeg;
+        const int rank = k - segpfx[b * nseg + s];  // position inside the segment
+        cU6[(size_t)b * ldN + segoff[s] + rank] = i;
+    }
+}
+
+// compacted fp64 tiles (64 x 64, XOR-swizzled as sym64), element (r, c) = G[u_r][u_c]
+__global__ void __launch_bounds__(256) cmp64_gather_tiles_kernel(
+    const double* __restrict__ Gt, int ntri, int nRB, const int* __restrict__ cU6, int ldN,
+    int nRBc, int ntric, double* Gc) {
+    const int b = blockIdx.y;
+    int t = blockIdx.x, I = 0;
+    while (t >= nRBc - I) {
+        t -= nRBc - I;
+        ++I;
+    }
+    const int J = I + t;
+    const int* ub = cU6 + (size_t)b * ldN;
+    const double* Gb = Gt + (size_t)b * ntri * (kT6 * kT6);
+    double* out = Gc + ((size_t)b * ntric + sy_tri(I, J, nRBc)) * (kT6 * kT6);
+    for (int e = threadIdx.x; e < kT6 * kT6; e += blockDim.x) {
+        const int r = e / kT6, cc = e % kT6;
+        const int i = ub[I * kT6 + r], j = ub[J * kT6 + cc];
+        double v = 0.0;
+        if (i >= 0 && j >= 0) {
+            int p = i, q = j;
+            if (p / kT6 > q / kT6) {
+                p = j;
+                q = i;
+            }
+            v = Gb[(size_t)sy_tri(p / kT6, q / kT6, nRB) * (kT6 * kT6) + s6_gofs(p % kT6, q % kT6)];
+        }
+        out[s6_gofs(r, cc)] = v;
+    }
+}
+
+template <int NR>
+__global__ void cmp64_gather_state_kernel(const double* __restrict__ Rs,
+                                          const int8_t* __restrict__ sig,
+                                          const double* __restrict__ D,
+                                          const double* __restrict__ hz, const int* __restrict__ cU,
+                                          int ldN, int B, double* Rc, int8_t* sigc, double* Dc,
+                                          double* hzc, double* Wc) {
+    const size_t total = (size_t)B * ldN;
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+         t += (size_t)gridDim.x * blockDim.x) {
+        const int b = (int)(t / ldN);
+        const int i = cU[t];
+        const bool on = i >= 0;
+        const size_t si = (size_t)b * ldN + (on ? i : 0);
+        Dc[t] = on ? D[si] : 0.0;
+        hzc[t] = on ? hz[si] : 0.0;
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+            const double r = on ? Rs[si * NR + q] : 0.0;
+            const int8_t s = on ? sig[si * NR + q] : 0;
+            Rc[t * NR + q] = r;
+            sigc[t * NR + q] = s;
+            Wc[t * NR + q] = r * (s ? 1.0 : 0.0);
+        }
+    }
+}
+
+template <int NR>
+__global__ void cmp64_scatter_kernel(const double* __restrict__ Rc, const int* __restrict__ cU,
+                                     int ldN, int B, double* Rs) {
     const size_t total = (size_t)B * ldN;
     for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
          t += (size_t)gridDim.x * blockDim.x) {

@@ -195,8 +195,9 @@ int cimcs_cdp_minimize(cimcs_ctx* c, int32_t R, const int32_t* sigma, const doub
     Events ev(2);
     cudaEventRecord(ev.ev[0], c->stream);
     if (!rc)
-        rc = method == CIMCS_CDP_JACOBI ? enqueue_refit(c, s, hp->jacobi_iters, false)
-                                        : enqueue_cg(c, s, hp);
+        rc = method == CIMCS_CDP_CG  ? enqueue_cg(c, s, hp)
+             : cmp64_refit_ok(c)    ? enqueue_refit_compact64(c, s, hp->jacobi_iters, false)
+                                    : enqueue_refit(c, s, hp->jacobi_iters, false);
     cudaEventRecord(ev.ev[1], c->stream);
     if (!rc) rc = download_traj(c, c->Rs, R_out, R);
     int err = INT_MAX;
@@ -280,6 +281,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
     if (int rc = ensure_state(c, NR)) return rc;
     // fp32 symmetric path: the Jacobi refit runs compacted to the union of supports
     const bool cmp = cdp == CIMCS_CDP_JACOBI && !pp && cmp_refit_ok(c);
+    const bool cmp64 = cdp == CIMCS_CDP_JACOBI && !pp && cmp64_refit_ok(c);
     if (cdp == CIMCS_CDP_CG)
         if (int rc = ensure_cg(c)) return rc;
     if (pp)
@@ -367,7 +369,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
                                             bits(s.nbeta), bits(s.Kj), bits(s.minus_j),
                                             bits(s.dt_c), c->B, c->N, cdp, hp->cg_max_iters,
                                             bits(hp->cg_tol), backend};
-        if (key != c->graph_key || (!pp && !c->g_cim) || (!cmp && !c->g_refit)) {
+        if (key != c->graph_key || (!pp && !c->g_cim) || (!cmp && !cmp64 && !c->g_refit)) {
             drop_graphs(c);
             Graph gc, gr;
             if (!pp)  // the Positive-P CIM call is host-driven (chunked noise upload)
@@ -375,7 +377,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
                     int r2 = run_init(c, R, bn, dc0, nullptr, s.rt);
                     return r2 ? r2 : enqueue_steps(c, bn, s, hp->n_steps);
                 });
-            if (!rc && !cmp)
+            if (!rc && !cmp && !cmp64)
                 rc = capture(c, gr, [&] {
                     if (cdp == CIMCS_CDP_CG) {
                         int r2 = run_support(c);
@@ -419,6 +421,8 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
         }
         if (cmp) {
             if ((rc = enqueue_refit_compact(c, s, hp->jacobi_iters))) return rc;
+        } else if (cmp64) {
+            if ((rc = enqueue_refit_compact64(c, s, hp->jacobi_iters, true))) return rc;
         } else if (c->use_graphs) {
             CK(cudaGraphLaunch(c->g_refit, c->stream));
         } else if (cdp == CIMCS_CDP_CG) {

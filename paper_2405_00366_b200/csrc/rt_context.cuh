@@ -33,6 +33,15 @@ struct cimcs_ctx {
     float *Rc = nullptr, *Dc = nullptr, *hzc = nullptr;
     int8_t* sigc = nullptr;
     __half* Gc = nullptr;        // compacted tiles (capacity: the full triangle)
+    // the fp64 path's segment-preserving compacted refit (cmp_kernels.cuh, cmp64):
+    // 512-column segments compacted one by one so the canonical fma order is kept
+    int* cU6 = nullptr;          // [B][ldN] compacted index -> spin (-1: pad)
+    int* cSegc = nullptr;        // [B][nseg] union spins per original segment
+    int* cPfx = nullptr;         // [B][nseg] their exclusive prefix per instance
+    int* cSegOff = nullptr;      // [nseg] compacted offset of segment s (-1: dropped)
+    int2* cSeg = nullptr;        // [nseg] compacted segments: (first block, blocks)
+    double *Rc6 = nullptr, *Dc6 = nullptr, *hzc6 = nullptr;
+    void* Gc6 = nullptr;         // compacted fp64 tiles (capacity: the full triangle)
     bool want_sym64 = true;
     bool sym64 = false;
     int nRB6 = 0, ntri6 = 0, nSB6 = 0;      // its geometry: 64-row blocks, 512 x 512 items
@@ -47,6 +56,8 @@ struct cimcs_ctx {
         int* sched = nullptr;
     };
     std::vector<SymSched> ssched;
+    SymSched cmp_sched;    // the compacted fp64 refit's schedule (rebuilt per alternation)
+    int cmp_items_cap = 0;
     int* dSg = nullptr;    // per-instance gram scale exponent
     float* dSpart = nullptr;  // partial products [B][nRB][nSB][128][NR]
     bool use_pdl = true;      // programmatic dependent launch between the step kernels

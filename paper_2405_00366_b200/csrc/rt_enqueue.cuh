@@ -144,6 +144,128 @@ int enqueue_refit_compact(cimcs_ctx* c, const StepScalars& s, int iters) {
     return mask_T<float>(c, (iters & 1) ? c->W1 : c->W0);  // what the scorer reads
 }
 
+// fp64 path: the segment-preserving compacted refit (cmp_kernels.cuh, cmp64) --
+// bitwise the full refit's result
+bool cmp64_refit_ok(const cimcs_ctx* c) {
+    return c->sym64 && c->cmp_opt && c->cU6 && (c->N + cmp64::kSeg - 1) / cmp64::kSeg <= cmp64::kMaxSeg &&
+           c->nSB6 == (c->N + cmp64::kSeg - 1) / cmp64::kSeg;
+}
+
+int enqueue_refit_compact64(cimcs_ctx* c, const StepScalars& s, int iters, bool do_support) {
+    if (do_support)
+        if (int rc = run_support(c)) return rc;
+    const int nseg = c->nSB6, B = c->B;
+    CK(cudaMemsetAsync(c->cMax, 0, 4, c->stream));
+    CK(cudaMemsetAsync(c->cSegc, 0, (size_t)B * nseg * 4, c->stream));
+    DISPATCH_NR_TC(c->NR, {
+        cmp_union_kernel<NR_><<<B, 1024, 0, c->stream>>>(c->sig, c->N, c->ldN, c->cU, c->cCnt,
+                                                         c->cMax);
+    });
+    cmp64_segcount_kernel<<<grid_for((size_t)B * c->ldN), 256, 0, c->stream>>>(
+        c->cU, c->cCnt, c->ldN, nseg, B, c->cSegc);
+    CK(cudaGetLastError());
+    std::vector<int> segc((size_t)B * nseg), pfx((size_t)B * nseg), off(nseg, -1);
+    if (int rc = copy_sync(c, segc.data(), c->cSegc, segc.size() * 4, cudaMemcpyDeviceToHost))
+        return rc;
+    // compacted segment widths: the batch maximum, rounded up to 64-row blocks
+    std::vector<int2> seg;
+    int Nc = 0;
+    for (int sg = 0; sg < nseg; ++sg) {
+        int w = 0;
+        for (int b = 0; b < B; ++b) w = std::max(w, segc[(size_t)b * nseg + sg]);
+        w = (w + kT6 - 1) / kT6 * kT6;
+        if (!w) continue;  // no instance uses it: its partial is an exact +0
+        off[sg] = Nc;
+        seg.push_back(make_int2(Nc / kT6, w / kT6));
+        Nc += w;
+    }
+    for (int b = 0; b < B; ++b)
+        for (int sg = 0, a = 0; sg < nseg; ++sg) {
+            pfx[(size_t)b * nseg + sg] = a;
+            a += segc[(size_t)b * nseg + sg];
+        }
+    if (Nc > 0 && iters > 0) {
+        const int nsc = (int)seg.size(), nRBc = Nc / kT6, ntric = nRBc * (nRBc + 1) / 2;
+        // the LPT schedule of the variable-width segment items
+        std::vector<std::pair<int, int2>> items;
+        for (int b = 0; b < B; ++b)
+            for (int P = 0; P < nsc; ++P)
+                for (int Q = P; Q < nsc; ++Q) {
+                    const int nI = seg[P].y, nJ = seg[Q].y;
+                    items.push_back({P == Q ? nI * (nI + 1) / 2 : nI * nJ, make_int2(b, P << 16 | Q)});
+                }
+        if ((int)items.size() > c->cmp_items_cap) return fail(CIMCS_CUDA_ERROR, "cmp64 schedule capacity");
+        std::vector<int2> flat;
+        std::vector<int> beg;
+        c->cmp_sched.grid = lpt_place(items, c->num_sms, flat, beg);
+        c->cmp_sched.nb = B;
+        c->cmp_sched.nRB = nRBc;
+        c->cmp_sched.S = kS6;
+        int rc;
+        if ((rc = copy_sync(c, c->cmp_sched.items, flat.data(), flat.size() * sizeof(int2),
+                            cudaMemcpyHostToDevice)) ||
+            (rc = copy_sync(c, c->cmp_sched.sched, beg.data(), beg.size() * 4,
+                            cudaMemcpyHostToDevice)) ||
+            (rc = copy_sync(c, c->cSeg, seg.data(), seg.size() * sizeof(int2),
+                            cudaMemcpyHostToDevice)) ||
+            (rc = copy_sync(c, c->cSegOff, off.data(), off.size() * 4, cudaMemcpyHostToDevice)) ||
+            (rc = copy_sync(c, c->cPfx, pfx.data(), pfx.size() * 4, cudaMemcpyHostToDevice)))
+            return rc;
+        CK(cudaMemsetAsync(c->cU6, 0xff, (size_t)B * c->ldN * 4, c->stream));  // -1: pad
+        cmp64_map_kernel<<<grid_for((size_t)B * c->ldN), 256, 0, c->stream>>>(
+            c->cU, c->cCnt, c->cPfx, c->cSegOff, c->ldN, nseg, B, c->cU6);
+        cmp64_gather_tiles_kernel<<<dim3(ntric, B), 256, 0, c->stream>>>(
+            static_cast<const double*>(c->dG6), c->ntri6, c->nRB6, c->cU6, c->ldN, nRBc, ntric,
+            static_cast<double*>(c->Gc6));
+        DISPATCH_NR_TC(c->NR, {
+            cmp64_gather_state_kernel<NR_><<<grid_for((size_t)B * c->ldN), 256, 0, c->stream>>>(
+                static_cast<const double*>(c->Rs), c->sig, static_cast<const double*>(c->dD),
+                static_cast<const double*>(c->dhz), c->cU6, c->ldN, B, c->Rc6, c->sigc, c->Dc6,
+                c->hzc6, static_cast<double*>(c->W0));
+        });
+        CK(cudaGetLastError());
+        struct Swap {  // the context runs the compacted problem until this goes out of scope
+            cimcs_ctx* c;
+            int N, nRB6, ntri6, nSB6;
+            void *dG6, *Rs, *dD, *dhz;
+            int8_t* sig;
+            ~Swap() {
+                c->N = N;
+                c->nRB6 = nRB6;
+                c->ntri6 = ntri6;
+                c->nSB6 = nSB6;
+                c->dG6 = dG6;
+                c->Rs = Rs;
+                c->dD = dD;
+                c->dhz = dhz;
+                c->sig = sig;
+                c->cmp_active = false;
+            }
+        } sw{c, c->N, c->nRB6, c->ntri6, c->nSB6, c->dG6, c->Rs, c->dD, c->dhz, c->sig};
+        c->N = Nc;
+        c->nRB6 = nRBc;
+        c->ntri6 = ntric;
+        c->nSB6 = nsc;
+        c->dG6 = c->Gc6;
+        c->Rs = c->Rc6;
+        c->dD = c->Dc6;
+        c->dhz = c->hzc6;
+        c->sig = c->sigc;
+        c->cmp_active = true;
+        if ((rc = sym_sync_w(c, c->W0))) return rc;
+        GemvArgs a = base_args(c, s);
+        if ((rc = enqueue_sym_loop(c, EPI_JACOBI, a, iters, false))) return rc;
+    }
+    if (Nc > 0 && iters > 0) {
+        DISPATCH_NR_TC(c->NR, {
+            cmp64_scatter_kernel<NR_><<<grid_for((size_t)B * c->ldN), 256, 0, c->stream>>>(
+                c->Rc6, c->cU6, c->ldN, B, static_cast<double*>(c->Rs));
+        });
+        CK(cudaGetLastError());
+    }
+    return mask_T<double>(c, (iters & 1) ? c->W1 : c->W0);
+}
+
 // ---------------------------------------------------- CG refit (cdp="cg")
 int ensure_cg(cimcs_ctx* c) {  // outside any capture: allocates
     if (c->cgX) return 0;

@@ -200,6 +200,8 @@ int launch_sym64_t(cimcs_ctx* c, const GemvArgs& g) {
     sa.part = c->dPart6;
     sa.ntri = c->ntri6;
     sa.nSB = c->nSB6;
+    sa.seg = c->cmp_active ? c->cSeg : nullptr;  // compacted refit: variable segments
+    sa.rowmap = c->cmp_active ? c->cU6 : nullptr;
     const cimcs_ctx::SymSched* ss = nullptr;
     if (int rc = sym_schedule(c, c->B, &ss, true)) return rc;
     sa.items = ss->items;

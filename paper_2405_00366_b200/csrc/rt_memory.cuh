@@ -32,8 +32,16 @@ void free_state(cimcs_ctx* c) {
     c->WS0 = c->WS1 = nullptr;
     c->WT0 = c->WT1 = c->dPart6 = nullptr;
     for (void* q : {(void*)c->cU, (void*)c->cCnt, (void*)c->cMax, (void*)c->Rc, (void*)c->Dc,
-                    (void*)c->hzc, (void*)c->sigc})
+                    (void*)c->hzc, (void*)c->sigc, (void*)c->cU6, (void*)c->cSegc,
+                    (void*)c->cPfx, (void*)c->cSegOff, (void*)c->cSeg, (void*)c->Rc6,
+                    (void*)c->Dc6, (void*)c->hzc6, (void*)c->cmp_sched.items,
+                    (void*)c->cmp_sched.sched})
         if (q) cudaFree(q);
+    c->cU6 = c->cSegc = c->cPfx = c->cSegOff = nullptr;
+    c->cSeg = nullptr;
+    c->Rc6 = c->Dc6 = c->hzc6 = nullptr;
+    c->cmp_sched = cimcs_ctx::SymSched{};
+    c->cmp_items_cap = 0;
     c->cU = c->cCnt = c->cMax = nullptr;
     c->Rc = c->Dc = c->hzc = nullptr;
     c->sigc = nullptr;
@@ -61,7 +69,7 @@ void free_problems(cimcs_ctx* c) {
     free_state(c);
     void* ptrs[] = {c->dA, c->dy, c->dM, c->dG, c->dG6, c->dD, c->dhz, c->dx, c->dxi,
                     c->dSg, c->dSpart, c->dMaskBr, c->dTw, c->dTarget,
-                    c->dH, c->Gc};
+                    c->dH, c->Gc, c->Gc6};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& q : c->ssched) {
@@ -70,6 +78,7 @@ void free_problems(cimcs_ctx* c) {
     }
     c->ssched.clear();
     c->Gc = nullptr;
+    c->Gc6 = nullptr;
     c->dSg = nullptr;
     c->dSpart = nullptr;
     c->dMaskBr = nullptr;
@@ -148,7 +157,37 @@ void tile_shard(int nRB, int world, int rank, int* P0, int* P1) {
 
 // Super-block items of nb instances placed on the persistent CTAs, largest
 // first onto the least-loaded CTA (LPT); built once per nb and cached.
+// LPT placement of weighted items on min(items, SMs) CTAs: flat item list + CTA ranges
+int lpt_place(std::vector<std::pair<int, int2>>& items, int nsm, std::vector<int2>& flat,
+              std::vector<int>& beg) {
+    std::stable_sort(items.begin(), items.end(),
+                     [](const auto& x, const auto& y) { return x.first > y.first; });
+    const int grid = (int)std::max<size_t>(1, std::min<size_t>(items.size(), (size_t)nsm));
+    std::vector<std::vector<int2>> per(grid);
+    using L = std::pair<long long, int>;  // (load, cta)
+    std::priority_queue<L, std::vector<L>, std::greater<L>> pq;
+    for (int g = 0; g < grid; ++g) pq.push({0, g});
+    for (const auto& it : items) {
+        L l = pq.top();
+        pq.pop();
+        per[l.second].push_back(it.second);
+        pq.push({l.first + it.first, l.second});
+    }
+    flat.clear();
+    beg.assign(grid + 1, 0);
+    for (int g = 0; g < grid; ++g) {
+        beg[g] = (int)flat.size();
+        flat.insert(flat.end(), per[g].begin(), per[g].end());
+    }
+    beg[grid] = (int)flat.size();
+    return grid;
+}
+
 int sym_schedule(cimcs_ctx* c, int nb, const cimcs_ctx::SymSched** out, bool s64 = false) {
+    if (s64 && c->cmp_active) {  // built per alternation by enqueue_refit_compact64
+        *out = &c->cmp_sched;
+        return 0;
+    }
     const int kS = s64 ? kS6 : c->symS;  // item edge in tiles
     const int nRB = s64 ? c->nRB6 : c->nRB, nSB = s64 ? c->nSB6 : c->nSB;
     for (auto& q : c->ssched)
@@ -165,26 +204,9 @@ int sym_schedule(cimcs_ctx* c, int nb, const cimcs_ctx::SymSched** out, bool s64
                 const int t = P == Q ? nI * (nI + 1) / 2 : nI * nJ;
                 items.push_back({t, make_int2(b, P << 16 | Q)});
             }
-    std::stable_sort(items.begin(), items.end(),
-                     [](const auto& x, const auto& y) { return x.first > y.first; });
-    const int grid = (int)std::max<size_t>(1, std::min<size_t>(items.size(), (size_t)c->num_sms));
-    std::vector<std::vector<int2>> per(grid);
-    using L = std::pair<long long, int>;  // (load, cta)
-    std::priority_queue<L, std::vector<L>, std::greater<L>> pq;
-    for (int g = 0; g < grid; ++g) pq.push({0, g});
-    for (const auto& it : items) {
-        L l = pq.top();
-        pq.pop();
-        per[l.second].push_back(it.second);
-        pq.push({l.first + it.first, l.second});
-    }
     std::vector<int2> flat;
-    std::vector<int> beg(grid + 1, 0);
-    for (int g = 0; g < grid; ++g) {
-        beg[g] = (int)flat.size();
-        flat.insert(flat.end(), per[g].begin(), per[g].end());
-    }
-    beg[grid] = (int)flat.size();
+    std::vector<int> beg;
+    const int grid = lpt_place(items, c->num_sms, flat, beg);
     cimcs_ctx::SymSched q;
     q.nb = nb;
     q.nRB = nRB;
@@ -253,6 +275,23 @@ int ensure_state(cimcs_ctx* c, int NR) {
             return rc;
         const cimcs_ctx::SymSched* ss;
         if ((rc = sym_schedule(c, c->B, &ss, true))) return rc;
+    }
+    if (c->sym64 && c->cmp_opt) {  // the fp64 compacted refit's buffers
+        const size_t nv = (size_t)c->B * c->ldN, ns = (size_t)c->B * cmp64::kMaxSeg;
+        const int cap = c->B * c->nSB6 * (c->nSB6 + 1) / 2;
+        if ((rc = dalloc(c, &c->cU, nv * 4)) || (rc = dalloc(c, &c->cCnt, (size_t)c->B * 4)) ||
+            (rc = dalloc(c, &c->cMax, 16)) || (rc = dalloc(c, &c->cU6, nv * 4)) ||
+            (rc = dalloc(c, &c->cSegc, ns * 4)) || (rc = dalloc(c, &c->cPfx, ns * 4)) ||
+            (rc = dalloc(c, &c->cSegOff, cmp64::kMaxSeg * 4)) ||
+            (rc = dalloc(c, &c->cSeg, cmp64::kMaxSeg * sizeof(int2))) ||
+            (rc = dalloc(c, &c->Rc6, n * 8)) || (rc = dalloc(c, &c->sigc, n)) ||
+            (rc = dalloc(c, &c->Dc6, nv * 8)) || (rc = dalloc(c, &c->hzc6, nv * 8)) ||
+            (rc = dalloc(c, &c->cmp_sched.items, (size_t)cap * sizeof(int2))) ||
+            (rc = dalloc(c, &c->cmp_sched.sched, (size_t)(c->num_sms + 1) * 4)))
+            return rc;
+        c->cmp_items_cap = cap;
+        if (!c->Gc6 && (rc = dalloc(c, &c->Gc6, (size_t)c->B * c->ntri6 * kT6 * kT6 * 8)))
+            return rc;
     }
     if (c->sym && !c->tshard && c->cmp_opt) {  // compacted refit buffers
         const size_t nv = (size_t)c->B * c->ldN;

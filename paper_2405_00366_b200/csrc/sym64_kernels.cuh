@@ -76,6 +76,8 @@ struct Sym64Args {
     const int* sched;      // [grid + 1]
     int ntri, nSB;
     int keep_w;            // step modes: also store the plain [b][i][r] w
+    const int2* seg;       // compacted refit: per segment (first block, blocks), or null
+    const int* rowmap;     // compacted refit: row -> original spin (error reports), or null
 };
 
 template <int NR>
@@ -219,9 +221,13 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) sym64_step_kernel(Sym64Args 
         b = it.x;
         P = it.y >> 16;
         Q = it.y & 0xffff;
-        nI = min(kS6, nRB - P * kS6);
-        nJ = min(kS6, nRB - Q * kS6);
+        nI = sa.seg ? sa.seg[P].y : min(kS6, nRB - P * kS6);
+        nJ = sa.seg ? sa.seg[Q].y : min(kS6, nRB - Q * kS6);
     };
+    // first 64-row block of segment P (fixed 8-block segments, or the compacted
+    // refit's variable ones: each compacted segment is one original 512-column
+    // segment, so the canonical order is unchanged)
+    auto blk0 = [&](int P) { return sa.seg ? sa.seg[P].x : P * kS6; };
 
     if (warp == kT6Compute) {
         // ------------------------------------------------------ producer
@@ -240,7 +246,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) sym64_step_kernel(Sym64Args 
                 item(k, b, P, Q, nI, nJ);
                 for (int ii = 0; ii < nI && tt < kT6Stages; ++ii)
                     for (int jj = P == Q ? ii : 0; jj < nJ && tt < kT6Stages; ++jj, ++tt)
-                        g_part(tt, b, P * kS6 + ii, Q * kS6 + jj);
+                        g_part(tt, b, blk0(P) + ii, blk0(Q) + jj);
             }
             if (kEarly) sy_pdl_wait();
             tt = 0;
@@ -250,7 +256,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) sym64_step_kernel(Sym64Args 
                 const double* Wb = sa.WTin + (size_t)b * nRB * (kT6 * NR);
                 for (int ii = 0; ii < nI; ++ii)
                     for (int jj = P == Q ? ii : 0; jj < nJ; ++jj, ++tt) {
-                        const int I = P * kS6 + ii, J = Q * kS6 + jj, s = tt % kT6Stages;
+                        const int I = blk0(P) + ii, J = blk0(Q) + jj, s = tt % kT6Stages;
                         if (tt >= kT6Stages) {
                             mbar_wait(&empty[s], ((tt / kT6Stages) - 1) & 1);
                             g_part(s, b, I, J);
@@ -288,7 +294,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) sym64_step_kernel(Sym64Args 
         for (int ii = 0; ii < nI; ++ii) {
             if (!use2) s6_acc_zero<MT, NT>(racc);
             for (int jj = diag ? ii : 0; jj < nJ; ++jj, ++tt) {
-                const int I = P * kS6 + ii, J = Q * kS6 + jj, s = tt % kT6Stages;
+                const int I = blk0(P) + ii, J = blk0(Q) + jj, s = tt % kT6Stages;
                 mbar_wait(&full[s], (tt / kT6Stages) & 1);
                 const double* tile = reinterpret_cast<const double*>(smem + s * kStage);
                 const double* wJ = reinterpret_cast<const double*>(smem + s * kStage + kT6TileBytes);
@@ -314,13 +320,13 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) sym64_step_kernel(Sym64Args 
             if (diag) {
                 s6_bar<NC>(1);  // use-2 of rows <= ii lands before use 1 of row ii + 1
             } else if (!use2) {  // row block I complete for this item: slot Q
-                double* p = sa.part + ((((size_t)b * nRB + P * kS6 + ii) * nSB + Q) * kT6) * NR;
+                double* p = sa.part + ((((size_t)b * nRB + blk0(P) + ii) * nSB + Q) * kT6) * NR;
                 s6_acc_st<NR, MT, NT>(p, m0, n0, lane, racc);
             }
         }
         // item done: shared accumulators -> partials (slot P)
         if (use2) {
-            const int J0 = (diag ? P : Q) * kS6;
+            const int J0 = blk0(diag ? P : Q);
             for (int kb = 0; kb < nblk; ++kb) {
                 double* p = sa.part + ((((size_t)b * nRB + J0 + kb) * nSB + P) * kT6) * NR;
                 for (int e = lane; e < Map::RW * NT * 4; e += 32) {  // 2 doubles per element
@@ -490,7 +496,7 @@ __global__ void __launch_bounds__(kT6 * NR / 4) sym64_update_kernel(Sym64Args sa
                 double rn = Rj[u];
                 if (on) {
                     if (Dv == 0.0) {
-                        atomicMin(a.err, i);
+                        atomicMin(a.err, sa.rowmap ? sa.rowmap[(size_t)b * a.ldN + i] : i);
                         continue;
                     }
                     const double off = gw[u] - Dv * Rj[u];

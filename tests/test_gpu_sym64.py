@@ -116,6 +116,53 @@ def test_refit_bitwise(gpu, O, cdp):
         assert math.isclose(sc["objective"][0, r], obj, rel_tol=1e-12, abs_tol=1e-14)
 
 
+@pytest.mark.parametrize("cmp", [0, 1])
+def test_compacted_refit_bitwise(gpu, O, cmp):
+    """The segment-preserving compacted Jacobi refit (cmp_kernels.cuh, cmp64) is
+    bitwise the oracle's: N=1700 (4 segments of 512, the last ragged), supports
+    chosen so that segment 1 is empty in every instance (dropped), the union
+    widths differ per instance and per segment, and one instance has a single
+    active spin."""
+    N, R = 1700, 8
+    insts = [O.gen_instance(N, 0.5, 0.1, 0.01, s) for s in (41, 42, 43)]
+    ctx = _ctx(gpu, insts, refit_compact=cmp)
+    order = ctx.canon_order()
+    assert order == (4, 512)
+    rng = np.random.default_rng(7)
+    sigma = np.zeros((3, R, N), np.int32)
+    sigma[0, :, :512] = rng.random((R, 512)) < 0.3
+    sigma[0, :, 1024:1536] = rng.random((R, 512)) < 0.05
+    sigma[1, :, 1024:] = rng.random((R, N - 1024)) < 0.4
+    sigma[2, 3, 1600] = 1
+    Rp = rng.normal(size=(3, R, N))
+    out = ctx.refit(R, sigma, Rp, gpu.HyperParams())
+    ctx.close()
+    for b, inst in enumerate(insts):
+        p = O.Problem(inst, O.CANON, *order)
+        for r in range(R):
+            ref = p.cdp(sigma[b, r], Rp[b, r], O.CDP_JACOBI, O.HyperParams())
+            assert np.array_equal(out[b, r], ref), (b, r)
+
+
+def test_compacted_refit_solve_matches_full(gpu, O):
+    """Whole solves with the compacted refit on and off: bitwise equal."""
+    insts = [O.gen_instance(1300, 0.5, 0.1, 0.01, s) for s in (51, 52)]
+    R = 8
+    seeds = np.array([[O.mix_seed(i.seed, 1 + 3 * r) for r in range(R)] for i in insts],
+                     np.uint64)
+    res = {}
+    for cmp in (0, 1):
+        ctx = _ctx(gpu, insts, refit_compact=cmp)
+        res[cmp] = ctx.solve(R, "mfz-bn", gpu.baseline_params(velo=3, n_steps=200), seeds)
+        ctx.close()
+    assert np.array_equal(res[0]["R"], res[1]["R"])
+    assert np.array_equal(res[0]["sigma"], res[1]["sigma"])
+    for b in range(2):
+        for r in range(R):
+            for h0, h1 in zip(res[0]["history"][b, r], res[1]["history"][b, r]):
+                assert h0 == h1
+
+
 @pytest.mark.parametrize("backend,track_best", [("mfz-bn", False), ("mfz-cn", True)])
 def test_solve_bitwise(gpu, O, backend, track_best):
     """Whole alternating solves: 2 instances x 3 replicas (NR padded to 8), N=600."""
