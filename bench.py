@@ -724,6 +724,138 @@ def run_ours(args, ws, rank, local):
         dist.destroy_process_group()
 
 
+def run_chain3(args, ws, rank, local):
+    """Config 3 through the matrix-free DCT o Haar^-1 chain (csrc/dct_kernels.cuh):
+    the same instance as the dense config-3 path (same phantom, frequencies,
+    observations), G never stored.  A step is hz/diag build + the full
+    alternating solve (20 x 1000 steps, damped Jacobi refits on the chain).
+    Replicas-only under torchrun (each rank its own seed)."""
+    import torch
+    import paper_2405_00366_b200 as P
+    from paper_2405_00366_b200 import _lib, workloads
+    _lib.load()
+
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    n, L, freqs, y, w = workloads.config3_chain(seed=3 + rank)
+    R, hp = 16, P.baseline_params()
+    N, nalt = n * n, hp.velo + 1
+    units = R * N * hp.n_steps * nalt
+    seeds = np.array([[P.mix_seed(3 + rank, 1 + 3 * r) for r in range(R)]], np.uint64)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    ctx = P.Context(local, "f32")
+    ctx.set_dct_problem(n, L, freqs, y, w)
+
+    def one_step():
+        ctx.build_coupling()
+        return ctx.solve(R, "mfz-bn", hp, seeds), ctx.timing()
+
+    for _ in range(args.warmup):
+        one_step()
+    dev_ms, step_us, launches = [], [], 0
+    parts = {"gram": [], "cim": [], "refit": [], "score": []}
+    barrier()
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            res, tm = one_step()
+            dev_ms.append(tm["gram_ms"] + tm["total_ms"])
+            for k in parts:
+                parts[k].append(tm[k + "_ms"])
+            step_us.append(1e3 * tm["cim_ms"] / (nalt * hp.n_steps))
+            launches += int(tm["step_launches"] + tm["refit_launches"] + tm["other_launches"]) + 2
+        barrier()
+    total = sum(dev_ms)
+    if dist is not None:
+        t = torch.tensor([total], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total = float(t.item())
+    ms = total / args.steps
+    value = units * ws / (ms * 1e-3)
+    # the chain kernel alone (eager, CUDA events around each step launch)
+    ctx.set_option("use_graphs", 0)
+    ctx.set_option("kernel_timing", 1)
+    ctx.solve(R, "mfz-bn", P.baseline_params(velo=1, n_steps=100), seeds)
+    tk = ctx.timing()
+    ctx.set_option("kernel_timing", 0)
+    ctx.set_option("use_graphs", 1)
+    ctx.close()
+    e2e = None
+    if not args.no_e2e:
+        def e2e_once():
+            with P.Context(local, "f32") as c2:
+                c2.set_dct_problem(n, L, freqs, y, w)
+                c2.build_coupling()
+                out = c2.solve(R, "mfz-bn", hp, seeds)
+            torch.cuda.synchronize()
+            return out
+        e2e_once()
+        barrier()
+        times = []
+        for _ in range(max(1, min(args.steps, 3))):
+            t1 = time.perf_counter()
+            r2 = e2e_once()
+            times.append(time.perf_counter() - t1)
+        e2e_s = statistics.median(times)
+        if dist is not None:
+            t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        h2d = freqs.nbytes + y.nbytes + w.nbytes + 2 * N * 4 + N + R * N * 8 * nalt
+        e2e = {"value": units * ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": r2["R"].nbytes + r2["sigma"].nbytes + r2["history"].nbytes,
+               "seconds": e2e_s}
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        insts, _, _, _ = workloads.config3()  # the dense instance the reference would run
+        nthreads = os.cpu_count() or 1
+        cs = 5
+        v, wall_c, k = cpu_sample_steps(insts[0], min(nthreads, 8), cs)
+        cpu = {"value": v, "unit": UNIT, "cores": k, "kind": "port",
+               "sample": (f"{k} trajectories (1/host thread) x {cs} Euler steps of run_mfz on "
+                          f"the dense config-3 instance, fp64 A^T(A w) restatement, no refit, "
+                          f"{wall_c:.1f}s wall")}
+    if rank == 0:
+        st = statistics.median(step_us)
+        t_k = tk["tile_kernel_ms"] / max(1, tk["tile_kernel_launches"]) * 1e-3
+        fl = 4 * 2.0 * n ** 3 * 3 * R  # 4 slab products x 3 TF32 passes per vector
+        rm = [res["history"][0, r][res["n_hist"][0, r] - 1]["rmse"] for r in range(R)]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (workloads.config3_chain: the config-3 phantom, frequencies, noise)",
+            "config": {"workload": WORKLOADS[3] + " -- matrix-free DCT o Haar^-1 chain, G never "
+                                   "stored",
+                       "step": "hz/diag build + full alternating solve (20 x 1000, Jacobi refit)",
+                       "l2": "no gram: DCT matrix + 16 images, L2/SMEM resident (no flush)"},
+            "breakdown_ms": {k: statistics.median(v) for k, v in parts.items()},
+            "roofline": {"bound": "latency",
+                         "note": ("one 8-CTA cluster per replica: 4 slab products 16x128x128 on "
+                                  "mma.sync TF32 (3xTF32), 2 DSMEM all-gathers, Haar in the slab;"
+                                  " no HBM stream"),
+                         "step_us": st, "chain_kernel_us": t_k * 1e6,
+                         "chain_tflops": fl / t_k / 1e12 if t_k > 0 else None,
+                         "kernel": "dct_cluster_kernel + sym_update_kernel<16,BN>",
+                         "dense_path_step_us": 120.0},
+            "e2e": e2e, "final_rmse_median": float(np.median(rm)),
+            "gpu_launches": launches, "clocks": clocks.summary(),
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def run_mri(args, ws, rank, local):
     """--mri: the reference's own transform-chain MRI problem (mri.cpp, cmd_mri
     tools/main.cpp:506-560) at config-3 size, matrix-free on the GPU
@@ -853,6 +985,8 @@ def main():
                     help="default: the config's (f32 for 1-4, f64 for 0)")
     ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--n4", type=int, default=100_000, help="config 4 size (N)")
+    ap.add_argument("--dense", action="store_true",
+                    help="config 3: the dense gram path instead of the matrix-free chain")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true",
@@ -873,6 +1007,8 @@ def main():
               file=sys.stderr)
     if args.mri and args.impl == "ours":
         run_mri(args, ws, rank, local)
+    elif args.config == 3 and args.impl == "ours" and not args.dense:
+        run_chain3(args, ws, rank, local)
     elif args.impl == "reference":
         run_reference(args, ws, rank)
     else:

@@ -192,6 +192,18 @@ int cimcs_build_coupling(cimcs_ctx* ctx);
  * G by applying the chain to every basis vector. */
 int cimcs_set_mri_problem(cimcs_ctx* ctx, int32_t H, int32_t W, const double* target,
                           int32_t M, const int32_t* mask, double gamma, const double* x_true);
+/* BASELINE config 3 as a matrix-free chain (dct_kernels.cuh): the dense
+ * config-3 instance has A = S C2 Psi_L^-1 (row m = the L-level orthonormal
+ * Mallat Haar transform -- the reference's average / difference split,
+ * mri.cpp:30-48 / 122-165, stopped after L levels -- of the orthonormal 2-D
+ * DCT-II basis image of frequency freqs[m] = u * n + v) and observations y[M].
+ * The context keeps only the DCT matrix, the frequency mask and y on the
+ * frequency grid; every G w is Psi C^T (mask o (C Psi^-1 w C^T)) C, hz = A^T y
+ * and D = diag(G) come from the same chain.  n must be 128, 1 <= levels <= 3,
+ * fp32 single-GPU contexts.  Unlike the DFT chain, damped Jacobi refits are
+ * allowed (this is the dense problem's G).  x_true (N) optional. */
+int cimcs_set_dct_problem(cimcs_ctx* ctx, int32_t n, int32_t levels, int32_t M,
+                          const int32_t* freqs, const double* y, const double* x_true);
 /* lasso_init(t, lambda) (mri.cpp:372-377 -> lasso_normal_form :345-370): FISTA
  * warm start on the built MRI problem with G = Re(A^H A), step `step` (1 in
  * the reference), stop when |f - f_prev| <= tol max(1, |f_prev|) or after

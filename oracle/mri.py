@@ -58,33 +58,39 @@ def _merge(v, n):
     v[..., 1:n:2] = (a - b) * _S
 
 
-def haar2_forward(img):
-    """mri.cpp:122-141: per level, rows (first w of the first h) then columns."""
+def haar2_forward(img, levels=None):
+    """mri.cpp:122-141: per level, rows (first w of the first h) then columns.
+    `levels` stops after that many levels (BASELINE config 3's 3-level
+    transform; the reference always runs to full depth)."""
     X = np.array(img, np.float64)
-    H, W = X.shape
+    H, W = X.shape[-2], X.shape[-1]
     if not (_pow2(H) and _pow2(W)):
         raise InputError("haar2_forward: dimensions must be powers of two")
     h, w = H, W
-    while h >= 2 and w >= 2:
-        blk = X[:h, :w]
+    done = 0
+    while h >= 2 and w >= 2 and (levels is None or done < levels):
+        done += 1
+        blk = X[..., :h, :w]
         _split(blk, w)
-        blkT = blk.T.copy()
+        blkT = np.swapaxes(blk, -1, -2).copy()
         _split(blkT, h)
-        X[:h, :w] = blkT.T
+        X[..., :h, :w] = np.swapaxes(blkT, -1, -2)
         h //= 2
         w //= 2
     return X
 
 
-def haar2_inverse(C):
-    """mri.cpp:143-165: deepest level first, columns then rows."""
+def haar2_inverse(C, levels=None):
+    """mri.cpp:143-165: deepest level first, columns then rows (`levels` as in
+    haar2_forward)."""
     X = np.array(C, np.float64)
     H, W = X.shape
     if not (_pow2(H) and _pow2(W)):
         raise InputError("haar2_inverse: dimensions must be powers of two")
+    nlev = levels
     levels = []
     h, w = H, W
-    while h >= 2 and w >= 2:
+    while h >= 2 and w >= 2 and (nlev is None or len(levels) < nlev):
         levels.append((h, w))
         h //= 2
         w //= 2

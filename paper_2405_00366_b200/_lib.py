@@ -27,7 +27,7 @@ EXPORTS = (
     "cimcs_run_cim", "cimcs_run_pp", "cimcs_refit", "cimcs_cdp_minimize", "cimcs_score", "cimcs_solve", "cimcs_get_timing",
     "cimcs_nccl_unique_id", "cimcs_create_sharded", "cimcs_format_double", "cimcs_fnv1a64",
     "cimcs_save_instance", "cimcs_load_instance", "cimcs_csv_open", "cimcs_csv_row",
-    "cimcs_csv_close", "cimcs_make_mask", "cimcs_set_mri_problem",
+    "cimcs_csv_close", "cimcs_make_mask", "cimcs_set_mri_problem", "cimcs_set_dct_problem",
     "cimcs_mri_lasso", "cimcs_tile_shard", "cimcs_set_generated_problems",
     "cimcs_get_instance",
 )
@@ -117,6 +117,7 @@ def load() -> C.CDLL:
     L.cimcs_get_instance.argtypes = [vp, i32, vp, vp, vp, vp]
     L.cimcs_set_mri_problem.argtypes = [vp, i32, i32, vp, i32, vp, d, vp]
     L.cimcs_mri_lasso.argtypes = [vp, d, i32, d, d, vp, vp, vp]
+    L.cimcs_set_dct_problem.argtypes = [vp, i32, i32, i32, vp, vp, vp]
     _lib = L
     return L
 

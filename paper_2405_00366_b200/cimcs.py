@@ -284,6 +284,22 @@ class Context:
                                                None if x is None else x.ctypes.data))
         self.B, self.N = 1, H * W
 
+    def set_dct_problem(self, n: int, levels: int, freqs, y, x_true=None):
+        """BASELINE config 3 as the matrix-free DCT o Haar^-1 chain (one instance,
+        fp32 contexts): the dense instance's A = S C2 Psi_levels^-1 with rows in
+        the order of `freqs` (u * n + v) and observations `y`."""
+        f = np.ascontiguousarray(freqs, np.int32).reshape(-1)
+        yy = np.ascontiguousarray(y, np.float64).reshape(-1)
+        if yy.size != f.size:
+            raise InputError("dct problem: one observation per frequency")
+        x = None if x_true is None else np.ascontiguousarray(x_true, np.float64).reshape(-1)
+        if x is not None and x.size != n * n:
+            raise InputError("dct problem: truth length mismatch")
+        _check(self._lib.cimcs_set_dct_problem(self._ctx, int(n), int(levels), f.size,
+                                               f.ctypes.data, yy.ctypes.data,
+                                               None if x is None else x.ctypes.data))
+        self.B, self.N = 1, n * n
+
     def mri_lasso(self, lambda_l1: float = 3e-4, max_iters: int = 5000, tol: float = 1e-8,
                   step: float = 1.0):
         """lasso_init(t, lambda) (mri.cpp:372-377): FISTA warm start of the

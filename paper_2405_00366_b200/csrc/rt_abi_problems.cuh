@@ -254,6 +254,7 @@ int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
 int cimcs_mri_lasso(cimcs_ctx* c, double lambda, int32_t max_iters, double tol, double step,
                     double* x_out, int32_t* iterations, double* objective) {
     if (!c || !c->mri || !c->built) return fail(CIMCS_INPUT_ERROR, "mri_lasso: no built MRI problem");
+    if (c->mri_kind != 0) return fail(CIMCS_CONFIG_ERROR, "mri_lasso: DFT transform-chain problems only");
     if (lambda < 0.0) return fail(CIMCS_INPUT_ERROR, "lasso: lambda_l1 must be >= 0");
     if (!(step > 0.0)) return fail(CIMCS_INPUT_ERROR, "lasso: step must be > 0");
     if (max_iters < 0 || !x_out) return fail(CIMCS_INPUT_ERROR, "mri_lasso: bad arguments");
@@ -411,6 +412,82 @@ int cimcs_set_mri_problem(cimcs_ctx* c, int32_t H, int32_t W, const double* targ
     return 0;
 }
 
+int cimcs_set_dct_problem(cimcs_ctx* c, int32_t n, int32_t levels, int32_t M,
+                          const int32_t* freqs, const double* y, const double* x_true) {
+    if (!c) return fail(CIMCS_INPUT_ERROR, "null context");
+    if (n != kDctN) return fail(CIMCS_INPUT_ERROR, "dct problem: the image edge must be 128");
+    if (levels < 1 || levels > kDctMaxLevels)
+        return fail(CIMCS_INPUT_ERROR, "dct problem: Haar levels must be in [1, 3]");
+    const int N = n * n;
+    if (M < 1 || M > N || !freqs || !y)
+        return fail(CIMCS_INPUT_ERROR, "dct problem: need 1 <= M <= N frequencies and observations");
+    std::vector<int> idx(freqs, freqs + M);
+    std::sort(idx.begin(), idx.end());
+    if (idx.front() < 0 || idx.back() >= N || std::adjacent_find(idx.begin(), idx.end()) != idx.end())
+        return fail(CIMCS_INPUT_ERROR, "dct problem: frequencies must be unique and in range");
+    if (c->dtype != CIMCS_F32) return fail(CIMCS_CONFIG_ERROR, "matrix-free chain problems run in fp32 contexts");
+    if (c->world > 1 || c->sharded) return fail(CIMCS_CONFIG_ERROR, "matrix-free chain problems are single-GPU");
+    CK(cudaSetDevice(c->device));
+    free_problems(c);
+    c->built = false;
+    c->mri = true;
+    c->mri_kind = 1;
+    c->dct_L = levels;
+    c->mH = c->mW = c->mL = n;
+    c->mgamma = 0.f;
+    c->B = 1;
+    c->N = N;
+    c->ldN = c->ldJ = N;
+    c->tc = c->sym = c->sym64 = false;
+    c->RB = kSyT;
+    c->row0 = 0;
+    c->row1 = N;
+    c->rb0 = 0;
+    c->nRB = (N + kSyT - 1) / kSyT;
+    c->nSB = 1;
+    c->ntri = 0;
+    c->nch = 0;
+    c->M.assign(1, M);
+    c->Mmax = M;
+    c->has_truth = x_true != nullptr;
+    // orthonormal DCT-II rows, stored in the kernel's swizzled shared-memory layout
+    std::vector<float> C((size_t)N), Y((size_t)N, 0.f);
+    for (int u = 0; u < n; ++u)
+        for (int x = 0; x < n; ++x)
+            C[(size_t)dofs(u, x)] = (float)(std::cos(M_PI * (2 * x + 1) * u / (2.0 * n)) *
+                                           std::sqrt((u ? 2.0 : 1.0) / n));
+    std::vector<unsigned char> mask((size_t)N, 0);
+    for (int m = 0; m < M; ++m) {
+        mask[freqs[m]] = 1;
+        Y[freqs[m]] = (float)y[m];
+    }
+    int rc;
+    if ((rc = dalloc(c, &c->dDctC, (size_t)N * 4)) || (rc = dalloc(c, &c->dDctMask, (size_t)N)) ||
+        (rc = dalloc(c, &c->dDctY, (size_t)N * 4)))
+        return rc;
+    if ((rc = copy_sync(c, c->dDctC, C.data(), C.size() * 4, cudaMemcpyHostToDevice)) ||
+        (rc = copy_sync(c, c->dDctMask, mask.data(), mask.size(), cudaMemcpyHostToDevice)) ||
+        (rc = copy_sync(c, c->dDctY, Y.data(), Y.size() * 4, cudaMemcpyHostToDevice)))
+        return rc;
+    static std::atomic<unsigned long long> attr{0};
+    if (!(attr.load() >> c->device & 1ull)) {
+        for (auto k : {dct_cluster_kernel<1>, dct_cluster_kernel<2>, dct_cluster_kernel<3>})
+            CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)dct_smem_bytes()));
+        attr.fetch_or(1ull << c->device);
+    }
+    if (c->has_truth) {
+        if ((rc = dalloc(c, &c->dx, (size_t)c->ldN * 8)) || (rc = dalloc(c, &c->dxi, (size_t)c->ldN)))
+            return rc;
+        std::vector<int8_t> xi8((size_t)c->ldN, 0);
+        for (int i = 0; i < N; ++i) xi8[i] = x_true[i] != 0.0 ? 1 : 0;
+        if ((rc = copy_sync(c, c->dx, x_true, (size_t)N * 8, cudaMemcpyHostToDevice)) ||
+            (rc = copy_sync(c, c->dxi, xi8.data(), xi8.size(), cudaMemcpyHostToDevice)))
+            return rc;
+    }
+    return 0;
+}
+
 int cimcs_build_coupling(cimcs_ctx* c) {
     if (!c || c->B < 1) return fail(CIMCS_INPUT_ERROR, "no problems set");
     CK(cudaSetDevice(c->device));
@@ -423,9 +500,14 @@ int cimcs_build_coupling(cimcs_ctx* c) {
         cudaEventRecord(ev.ev[0], c->stream);
         CK(cudaMemsetAsync(c->dhz, 0, nv * 4, c->stream));
         CK(cudaMemsetAsync(c->dD, 0, nv * 4, c->stream));
-        if ((rc = mri_launch(c, MRI_HZ, 1, 0, c->dTarget, static_cast<float*>(c->dhz))) ||
-            (rc = mri_launch(c, MRI_DIAG, c->N, 0, nullptr, static_cast<float*>(c->dD))))
+        if (c->mri_kind == 1) {  // hz = A^T y = Psi C^T Y C, D = diag of the chain
+            if ((rc = dct_launch(c, DCT_HZ, 1, 0, c->dDctY, static_cast<float*>(c->dhz), 1)) ||
+                (rc = dct_launch(c, DCT_DIAG, c->N, 0, nullptr, static_cast<float*>(c->dD), 1)))
+                return rc;
+        } else if ((rc = mri_launch(c, MRI_HZ, 1, 0, c->dTarget, static_cast<float*>(c->dhz))) ||
+                   (rc = mri_launch(c, MRI_DIAG, c->N, 0, nullptr, static_cast<float*>(c->dD)))) {
             return rc;
+        }
         cudaEventRecord(ev.ev[1], c->stream);
         CK(cudaStreamSynchronize(c->stream));
         c->timing.gram_ms = ev.ms(0, 1);
@@ -588,7 +670,9 @@ int cimcs_get_coupling(cimcs_ctx* c, int32_t b, double* G, double* hz, double* D
         float* P = nullptr;
         if (int rc = dalloc(c, &P, (size_t)N * N * 4)) return rc;
         std::unique_ptr<float, decltype(&cudaFree)> pguard(P, &cudaFree);
-        if (int rc = mri_launch(c, MRI_COLS, N, 0, nullptr, P)) return rc;
+        if (int rc = c->mri_kind == 1 ? dct_launch(c, DCT_COLS, N, 0, nullptr, P, 1)
+                                      : mri_launch(c, MRI_COLS, N, 0, nullptr, P))
+            return rc;
         std::vector<float> f((size_t)N * N);
         if (int rc_ = copy_sync(c, f.data(), P, f.size() * 4, cudaMemcpyDeviceToHost)) return rc_;
         for (size_t k = 0; k < f.size(); ++k) G[k] = f[k];

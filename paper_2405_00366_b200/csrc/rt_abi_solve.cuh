@@ -181,7 +181,7 @@ int cimcs_cdp_minimize(cimcs_ctx* c, int32_t R, const int32_t* sigma, const doub
         return fail(CIMCS_CONFIG_ERROR, "cdp method must be jacobi or cg");
     if (method == CIMCS_CDP_CG && c->world > 1)
         return fail(CIMCS_CONFIG_ERROR, "cdp=cg is not supported on row-sharded contexts");
-    if (c->mri && method == CIMCS_CDP_JACOBI)  // cdp.cpp:158-159
+    if (c->mri && c->mri_kind == 0 && method == CIMCS_CDP_JACOBI)  // cdp.cpp:158-159
         return fail(CIMCS_CONFIG_ERROR, "cdp_minimize_operator: damped Jacobi needs an assembled matrix");
     CK(cudaSetDevice(c->device));
     if (int rc = ensure_state(c, slots_for(c, R))) return rc;
@@ -274,7 +274,9 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
         return fail(CIMCS_CONFIG_ERROR, "cdp must be jacobi or cg");
     if (cdp == CIMCS_CDP_CG && c->world > 1)
         return fail(CIMCS_CONFIG_ERROR, "cdp=cg is not supported on row-sharded contexts");
-    if (c->mri) cdp = CIMCS_CDP_CG;  // transform-chain problems always use CG (orchestrator.cpp:128-133)
+    // the reference's DFT transform-chain problems always use CG (orchestrator.cpp:128-133);
+    // the DCT chain stands in for config 3's dense matrix and keeps the requested refit
+    if (c->mri && c->mri_kind == 0) cdp = CIMCS_CDP_CG;
     if (!seeds) return fail(CIMCS_INPUT_ERROR, "null seeds");
     CK(cudaSetDevice(c->device));
     const int NR = slots_for(c, R);

@@ -83,6 +83,14 @@ struct cimcs_ctx {
     float2* dTw = nullptr;             // [L/2] exp(-2 pi i k / L)
     float* dTarget = nullptr;          // [H*W] target image (row-major)
     bool mri_cluster = true;           // per-step apply on one cluster per replica
+    // chain kind: 0 the reference's DFT chain, 1 config 3's DCT o Haar^-1 chain
+    // (dct_kernels.cuh; A = S C2 Psi_L^-1, damped Jacobi allowed: its G is the
+    // dense config-3 problem's)
+    int mri_kind = 0;
+    int dct_L = 0;                     // Haar levels
+    float* dDctC = nullptr;            // [128][128] DCT-II matrix
+    unsigned char* dDctMask = nullptr; // [128 * 128] sampled frequencies
+    float* dDctY = nullptr;            // [128 * 128] observations on the frequency grid
     __half *WB0 = nullptr, *WB1 = nullptr;  // fp16 B tiles of W0 / W1 [B][nRB][2NR x 128]
     int *WS0 = nullptr, *WS1 = nullptr;     // their scale exponents [B][nRB][NR]
     size_t spart_elems = 0;

@@ -288,6 +288,39 @@ int mri_launch(cimcs_ctx* c, int mode, int grid, int r0, const float* in, float*
     return 0;
 }
 
+// one dct_cluster_kernel launch: `count` vectors (replica slots for APPLY,
+// basis vectors r0.. for DIAG / COLS, 1 for HZ), a cluster of 8 CTAs each
+int dct_launch(cimcs_ctx* c, int mode, int count, int r0, const float* in, float* out, int NR) {
+    DctArgs da{};
+    da.NR = NR;
+    da.C = c->dDctC;
+    da.mask = c->dDctMask;
+    da.in = in;
+    da.out = out;
+    da.r0 = r0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(count * kDctCS);
+    cfg.blockDim = dim3(kDctThreads);
+    cfg.dynamicSmemBytes = dct_smem_bytes();
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kDctCS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = mode == DCT_APPLY && c->use_pdl ? 2 : 1;
+    switch (c->dct_L) {
+        case 1: CK(cudaLaunchKernelEx(&cfg, dct_cluster_kernel<1>, da, mode)); break;
+        case 2: CK(cudaLaunchKernelEx(&cfg, dct_cluster_kernel<2>, da, mode)); break;
+        default: CK(cudaLaunchKernelEx(&cfg, dct_cluster_kernel<3>, da, mode)); break;
+    }
+    CK(cudaGetLastError());
+    return 0;
+}
+
 // transform-chain problems: G w by the matrix-free MRI kernel (one CTA per
 // replica slot) into the one-slot partial buffer, then the symmetric path's
 // update kernel for the fused epilogue of `mode`
@@ -305,7 +338,20 @@ int launch_mri_t(cimcs_ctx* c, const GemvArgs& g) {
     ma.scale = 1.f / (float)c->N;
     ma.in = static_cast<const float*>(g.Win);
     ma.out = c->dSpart;
-    if (c->mri_cluster && std::min(c->mH, c->mW) >= 2 * kMriCluster) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    const bool timed = c->kernel_timing && (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) &&
+                       cudaStreamIsCapturing(c->stream, &cap) == cudaSuccess &&
+                       cap == cudaStreamCaptureStatusNone;
+    if (timed) {  // eager mode: CUDA events around the chain kernel
+        if (!c->kt_ev[0]) {
+            CK(cudaEventCreate(&c->kt_ev[0]));
+            CK(cudaEventCreate(&c->kt_ev[1]));
+        }
+        CK(cudaEventRecord(c->kt_ev[0], c->stream));
+    }
+    if (c->mri_kind == 1) {
+        if (int rc = dct_launch(c, DCT_APPLY, NR, 0, ma.in, ma.out, NR)) return rc;
+    } else if (c->mri_cluster && std::min(c->mH, c->mW) >= 2 * kMriCluster) {
         // one thread-block cluster per replica (mri_cluster_kernel)
         const int CS = mri_cluster_size(c->mH, c->mW);
         cudaLaunchConfig_t cfg{};
@@ -328,6 +374,14 @@ int launch_mri_t(cimcs_ctx* c, const GemvArgs& g) {
         mri_kernel<<<NR, kMriThreads, smem, c->stream>>>(ma, MRI_APPLY);
     }
     CK(cudaGetLastError());
+    if (timed) {
+        CK(cudaEventRecord(c->kt_ev[1], c->stream));
+        CK(cudaEventSynchronize(c->kt_ev[1]));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->kt_ev[0], c->kt_ev[1]));
+        c->timing.tile_kernel_ms += ms;
+        c->timing.tile_kernel_launches += 1;
+    }
     SymArgs sa{};
     sa.t = tc_args(c, g);
     sa.spart = c->dSpart;
@@ -358,6 +412,9 @@ int launch_mri_nr(cimcs_ctx* c, int mode, const GemvArgs& a) {
         case EPI_STEP_CN: return launch_mri_t<NR, EPI_STEP_CN>(c, a);
         case EPI_MATVEC: return launch_mri_t<NR, EPI_MATVEC>(c, a);
         case EPI_SCORE: return launch_mri_t<NR, EPI_SCORE>(c, a);
+        case EPI_JACOBI:
+            if (c->mri_kind == 1) return launch_mri_t<NR, EPI_JACOBI>(c, a);
+            [[fallthrough]];
         default: return fail(CIMCS_CONFIG_ERROR, "cdp_minimize_operator: damped Jacobi needs an assembled matrix");
     }
 }

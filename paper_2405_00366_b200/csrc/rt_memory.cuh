@@ -69,7 +69,7 @@ void free_problems(cimcs_ctx* c) {
     free_state(c);
     void* ptrs[] = {c->dA, c->dy, c->dM, c->dG, c->dG6, c->dD, c->dhz, c->dx, c->dxi,
                     c->dSg, c->dSpart, c->dMaskBr, c->dTw, c->dTarget,
-                    c->dH, c->Gc, c->Gc6};
+                    c->dH, c->Gc, c->Gc6, c->dDctC, c->dDctMask, c->dDctY};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& q : c->ssched) {
@@ -86,6 +86,10 @@ void free_problems(cimcs_ctx* c) {
     c->dTw = nullptr;
     c->dTarget = nullptr;
     c->mri = false;
+    c->mri_kind = 0;
+    c->dDctC = nullptr;
+    c->dDctMask = nullptr;
+    c->dDctY = nullptr;
     c->spart_elems = 0;
     c->dA = c->dy = nullptr;
     c->dM = nullptr;

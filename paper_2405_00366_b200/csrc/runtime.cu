@@ -34,6 +34,7 @@
 #include "gram_tc_kernels.cuh"
 #include "cmp_kernels.cuh"
 #include "mri_kernels.cuh"
+#include "dct_kernels.cuh"
 
 using namespace cimcs;
 

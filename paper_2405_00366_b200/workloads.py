@@ -120,6 +120,43 @@ def config3(seed: int = 3, n: int = 128, levels: int = 3, alpha: float = 0.4,
     return [inst], 16, baseline_params(), "f32"
 
 
+def config3_chain(seed: int = 3, n: int = 128, levels: int = 3, alpha: float = 0.4,
+                  noise: float = 0.005):
+    """Config 3 without its dense matrix: (n, levels, freqs, y, w) for
+    Context.set_dct_problem.  Same draws as config3 (same phantom, frequencies
+    and noise); y = S C2 w_image + noise evaluated by fast transforms."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    img = ellipse_phantom(n, 10, rng)
+    w = haar2(img, levels).reshape(-1)
+    N = n * n
+    M = int(math.floor(alpha * N + 0.5))
+    freqs = rng.choice(N, size=M, replace=False)
+    C = _dct_matrix(n)
+    spec = (C @ ihaar2(w.reshape(n, n), levels) @ C.T).reshape(-1)
+    y = spec[freqs] + noise * rng.standard_normal(M)
+    return n, levels, freqs.astype(np.int32), y, w.copy()
+
+
+def ihaar2(X: np.ndarray, levels: int) -> np.ndarray:
+    """Inverse of haar2 (column merge then row merge per level, coarsest first)."""
+    X = np.array(X, dtype=np.float64, copy=True)
+    s = 1.0 / math.sqrt(2.0)
+    n0, m0 = X.shape[-2], X.shape[-1]
+    for lev in range(levels - 1, -1, -1):
+        h, w = n0 >> lev, m0 >> lev
+        blk = X[..., :h, :w].copy()
+        a, d = blk[..., : h // 2, :], blk[..., h // 2:, :]
+        out = np.empty_like(blk)
+        out[..., 0::2, :] = (a + d) * s
+        out[..., 1::2, :] = (a - d) * s
+        a, d = out[..., :, : w // 2], out[..., :, w // 2:]
+        out2 = np.empty_like(out)
+        out2[..., :, 0::2] = (a + d) * s
+        out2[..., :, 1::2] = (a - d) * s
+        X[..., :h, :w] = out2
+    return X
+
+
 def config4(N: int = 100_000, seed: int = 7):
     """Strong-scaling workload: gen_instance(N, 0.5, 0.05, 0.01, 7), 4 replicas,
     10 alternations x 500 steps.  (Host generation of the 5e9-draw reference
