@@ -216,6 +216,7 @@ int cimcs_get_instance(cimcs_ctx* c, int32_t b, double* A, double* y, double* x_
 int cimcs_set_problems(cimcs_ctx* c, int32_t B, int32_t N, const int32_t* M,
                        const double* const* A, const double* const* y,
                        const double* const* x_true, const int32_t* const* xi_true) {
+    NvtxRange nvtx_range_("cimcs_set_problems");
     if (!c) return fail(CIMCS_INPUT_ERROR, "null context");
     if (B < 1 || N < 1) return fail(CIMCS_INPUT_ERROR, "need B >= 1 and N >= 1");
     for (int b = 0; b < B; ++b)
@@ -489,6 +490,7 @@ int cimcs_set_dct_problem(cimcs_ctx* c, int32_t n, int32_t levels, int32_t M,
 }
 
 int cimcs_build_coupling(cimcs_ctx* c) {
+    NvtxRange nvtx_range_("cimcs_build_coupling");
     if (!c || c->B < 1) return fail(CIMCS_INPUT_ERROR, "no problems set");
     CK(cudaSetDevice(c->device));
     if (c->mri) {  // hz = Re(A^H y) and diag(G) of the transform chain (mri.cpp:236-254)

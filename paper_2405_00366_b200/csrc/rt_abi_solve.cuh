@@ -8,6 +8,8 @@ extern "C" {
 int cimcs_mfz_step(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp, double eta,
                    double p, const double* Rsig, const double* cin, const double* ein,
                    double* c_out, double* e_out, double* h_out, int32_t* fail_index) {
+    NvtxRange nvtx_range_("cimcs_mfz_step");
+    NvtxRange nv_solve("cimcs_solve");
     if (int rc = check_ready(c, R)) return rc;
     if (int rc = validate(hp)) return rc;
     if (!std::isfinite(p)) return fail(CIMCS_INPUT_ERROR, "mfz_step: non-finite pump");
@@ -120,6 +122,7 @@ int cimcs_run_pp(cimcs_ctx* c, int32_t R, const cimcs_hyper* hp, double eta, con
 int cimcs_run_cim(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp, double eta,
                   const double* Rsig, const double* c0, double* c_out, double* e_out,
                   int32_t* sigma_out, double* min_e, int32_t* fail_index) {
+    NvtxRange nvtx_range_("cimcs_run_cim");
     if (int rc = check_ready(c, R)) return rc;
     if (int rc = validate(hp)) return rc;
     if (backend != CIMCS_MFZ_BN && backend != CIMCS_MFZ_CN)
@@ -175,6 +178,7 @@ int cimcs_run_cim(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* h
 int cimcs_cdp_minimize(cimcs_ctx* c, int32_t R, const int32_t* sigma, const double* R_prev,
                        int32_t method, const cimcs_hyper* hp, double* R_out,
                        int32_t* iterations) {
+    NvtxRange nvtx_range_("cimcs_cdp_minimize");
     if (int rc = check_ready(c, R)) return rc;
     if (!hp) return fail(CIMCS_CONFIG_ERROR, "null hyper-parameters");
     if (method != CIMCS_CDP_JACOBI && method != CIMCS_CDP_CG)
@@ -404,6 +408,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
             CK(cudaMemcpyAsync(dc0, slot, nc0 * 8, cudaMemcpyHostToDevice, c->stream));
             CK(cudaEventRecord(slot_done.ev[i & 1], c->stream));
         }
+        NvtxRange nv_alt("alternation");
         CK(cudaEventRecord(ev.ev[4 * i + 0], c->stream));
         if (pp) {
             if ((rc = run_pp_cim(c, R, s, hp, rngs)) || (rc = pp_amplitude_to_c(c))) return rc;

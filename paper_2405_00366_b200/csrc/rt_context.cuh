@@ -2,6 +2,15 @@
 // order): struct cimcs_ctx: the device context (problems, state, paths, graphs).
 #pragma once
 
+// NVTX ranges around the host-side phases of the ABI calls (header-only NVTX v3:
+// no-ops unless a tool such as Nsight Systems injects itself)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // ======================================================================= ctx
 struct cimcs_ctx {
     int device = 0, dtype = CIMCS_F32;

@@ -9,6 +9,7 @@
 // runs the current one.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <queue>
