@@ -102,7 +102,7 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
         c->mri_cluster = v != 0;
         drop_graphs(c);
     } else if (k == "gram_l2") {
-        c->gram_l2 = v != 0;
+        c->gram_l2 = v < 0 ? 0 : (int)v;
         drop_graphs(c);
     } else if (k == "pdl") {
         c->use_pdl = v != 0;

@@ -70,7 +70,8 @@ struct cimcs_ctx {
     int* dSg = nullptr;    // per-instance gram scale exponent
     float* dSpart = nullptr;  // partial products [B][nRB][nSB][128][NR]
     bool use_pdl = true;      // programmatic dependent launch between the step kernels
-    int gram_l2 = 0;          // gram tiles copied with evict_last (L2 time-blocking experiment)
+    int gram_l2 = 0;          // per instance, the first gram_l2 tiles of the triangle are copied
+                              // with evict_last (an L2-resident subset), the rest evict_first
     bool kernel_timing = false;  // eager mode: CUDA events around each step-mode tile kernel
     cudaEvent_t kt_ev[2] = {nullptr, nullptr};
     // tile sharding of the symmetric path (cimcs_create_sharded contexts, option

@@ -176,7 +176,7 @@ struct SymArgs {
     int ntri, nSB;         // tiles per instance, super-blocks per row
     int b0;                // first instance of this launch (instance groups)
     int keep_w;            // step modes: also store the fp32 w (a consumer reads it)
-    int gram_keep;         // 1: gram tiles copied with evict_last (L2-resident groups)
+    int gram_keep;         // tiles t < gram_keep of each triangle copied with evict_last
     int S;                 // item edge in tiles (kSyS; 2 for the compacted refit)
     const int* rowmap;     // compacted refit: row -> original spin (error reports), or null
 };
@@ -320,12 +320,13 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
     if (warp == 0) {
         // ------------------------------------------------------ producer
         if (lane == 0) {
-            const uint64_t pG = sa.gram_keep ? sy_policy_last() : sy_policy_first();
-            const uint64_t pW = sy_policy_last();
+            const uint64_t pGf = sy_policy_first(), pW = sy_policy_last();
             // stage s of tile tt: expect its bytes, copy the two gram planes
             auto g_part = [&](int s, int b, int I, int J) {
+                const int tri = sy_tri(I, J, nRB);
                 const __half* src = sa.Gs + (size_t)b * sa.ntri * 2 * kSyPlaneHalfs +
-                                    (size_t)sy_tri(I, J, nRB) * 2 * kSyPlaneHalfs;
+                                    (size_t)tri * 2 * kSyPlaneHalfs;
+                const uint64_t pG = tri < sa.gram_keep ? pW : pGf;
                 unsigned char* st = smem + s * kStage;
                 mbar_arrive_expect_tx(&full[s], 2 * kSyPlaneBytes + (I != J ? 2 : 1) * kBB);
                 // the gram streams through L2 once per step; w tiles are re-read

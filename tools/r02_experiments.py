@@ -223,6 +223,30 @@ def l2groups():
         json.dump(rows, f, indent=1)
 
 
+def l2subset():
+    """A fixed L2-resident SUBSET of the gram: the first `keep` tiles of every
+    instance's triangle copied with evict_last, the rest evict_first."""
+    insts, R, hp, _ = W.config1(0, 64)
+    hp1 = P.baseline_params(velo=1, n_steps=500)
+    seeds = P.replica_seeds(insts, R, "mfz-bn")
+    rows = []
+    with P.Context(0, "f32") as ctx:
+        ctx.set_problems(insts)
+        ctx.build_coupling()
+        for keep in (0, 4, 8, 12, 16, 24, 32, 0):
+            ctx.set_option("gram_l2", keep)
+            ctx.solve(R, "mfz-bn", hp1, seeds)
+            ts = []
+            for _ in range(2):
+                ctx.solve(R, "mfz-bn", hp1, seeds)
+                ts.append(ctx.timing()["cim_ms"] / 1000 * 1e3)
+            rows.append({"keep_tiles_per_instance": keep, "kept_MB": keep * 64 * 65536 / 1e6,
+                         "us_per_step": min(ts)})
+            print(rows[-1], flush=True)
+    with open(os.path.join(OUT, "l2subset_r02.json"), "w") as f:
+        json.dump(rows, f, indent=1)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["sensitivity", "l2groups"]
     for w in which:
