@@ -25,6 +25,7 @@ EXPORTS = (
     "cimcs_gen_instances", "cimcs_create", "cimcs_destroy", "cimcs_set_option",
     "cimcs_set_problems", "cimcs_build_coupling", "cimcs_get_coupling", "cimcs_mfz_step",
     "cimcs_run_cim", "cimcs_run_pp", "cimcs_refit", "cimcs_cdp_minimize", "cimcs_score", "cimcs_solve", "cimcs_get_timing",
+    "cimcs_get_timeline",
     "cimcs_nccl_unique_id", "cimcs_create_sharded", "cimcs_format_double", "cimcs_fnv1a64",
     "cimcs_save_instance", "cimcs_load_instance", "cimcs_csv_open", "cimcs_csv_row",
     "cimcs_csv_close", "cimcs_make_mask", "cimcs_set_mri_problem", "cimcs_set_dct_problem",
@@ -101,6 +102,7 @@ def load() -> C.CDLL:
     L.cimcs_score.argtypes = [vp, i32, vp, vp, d, vp, vp, vp]
     L.cimcs_solve.argtypes = [vp, i32, i32, vp, i32, vp, vp, i32, vp, vp, vp, vp, vp, vp]
     L.cimcs_get_timing.argtypes = [vp, vp]
+    L.cimcs_get_timeline.argtypes = [vp, vp, C.c_int64, vp]
     L.cimcs_nccl_unique_id.argtypes = [vp, i32]
     L.cimcs_create_sharded.argtypes = [i32, i32, i32, i32, vp, vp]
     L.cimcs_format_double.argtypes = [d, C.c_char_p, i32]

@@ -51,7 +51,8 @@ def stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
-        cmd = [NVCC, *FLAGS, "-o", LIB, *SOURCES, *LIBS]
+        cmd = [NVCC, *FLAGS, *os.environ.get("CIMCS_NVCC_EXTRA", "").split(), "-o", LIB, *SOURCES,
+               *LIBS]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)

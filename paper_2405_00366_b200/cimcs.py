@@ -460,6 +460,14 @@ class Context:
         return dict(R=Ro, sigma=So, history=H, n_hist=nh, fail_alt=fa, fail_index=fi,
                     backend=backend)
 
+    def timeline(self) -> np.ndarray:
+        """%globaltimer stamps [CTA][4] of the last tile / update launch pair (option
+        "timeline" = 1; rows 0..255 tile CTAs, rows 256.. update CTAs b * nRB + K)."""
+        out = np.zeros((256 + 8192, 4), np.uint64)
+        n = C.c_int64(0)
+        _check(self._lib.cimcs_get_timeline(self._ctx, out.ctypes.data, out.size, C.byref(n)))
+        return out
+
     def timing(self) -> dict:
         t = _lib.Timing()
         _check(self._lib.cimcs_get_timing(self._ctx, C.byref(t)))

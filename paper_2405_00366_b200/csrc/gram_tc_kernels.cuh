@@ -5,10 +5,10 @@
 //
 // The tiles keep ~22 bits, so the GEMM must be fp32-accurate.  A (fp64, scaled
 // by an exact 2^s_A per instance) is split once into fp16 hi/lo planes,
-// x ~= hi + lo (~22 bits), stored PRE-TILED in the UMMA canonical no-swizzle
-// K-major layout over all N columns per 32-row k-chunk:
-//     plane(c, p)[ (k/8) * (Np/8) * 128 B + (j/8) * 128 B + (j%8) * 16 B + (k%8) * 2 B ]
-// so the 128-column slice of one k-group is ONE contiguous 2 KB bulk copy.
+// x ~= hi + lo (~22 bits), stored PRE-TILED per 32-row k-chunk, plane and 128-column
+// block in the UMMA canonical no-swizzle K-major layout (M/N = 128, K = 32):
+//     plane(c, p)[ (j/128) * 8 KB + (k/8) * 2 KB + ((j%128)/8) * 128 B + (j%8) * 16 B + (k%8) * 2 B ]
+// so one operand plane of a stage is ONE contiguous 8 KB bulk copy (4 per stage).
 // Per k-step (K = 16) the MMA warp issues
 //     D += A_hi_I^T A_hi_J + A_hi_I^T A_lo_J + A_lo_I^T A_hi_J     (kind::f16, M = N = 128)
 // (the lo*lo term is below fp32 resolution).
@@ -20,10 +20,20 @@
 // resolution), double-buffered in TMEM; eight epilogue warps drain each chunk
 // into fp32 registers with a two-level sum (16 chunks, then a running total),
 // so the fp32 rounding of the long K sum stays at ~sqrt(K / 512) ulp.
-// Persistent CTAs walk the upper-triangle tiles row-major (concurrent CTAs share
-// the A_I operand in L2); warp 0 produces (bulk copies into a 4-stage ring),
-// warp 1 issues the MMAs, warps 2-9 drain TMEM and finally store the fp16 hi/lo
-// SymOut values (G * 2^s_G).
+// Measured on the kernel (tools/gram_pipeline.py, tools/gram_time.py): a k-chunk costs
+// 0.55 us per CTA, 0.35 us of it the six MMAs themselves -- each reads 8 KB of operands
+// from shared memory while the ring's bulk copies write 32 KB per chunk into it, so the
+// chunk moves 80 KB through a 128 B/clk port: the kernel is bound by shared-memory
+// bandwidth, not by loads (a 7-stage ring with the second-level sums moved to TMEM gave
+// 0.56 us) nor by the tensor pipe (6 x 64 clk).
+// Persistent CTAs walk the upper-triangle tiles super-block by super-block (kGtSB x
+// kGtSB tiles, about one per wave of 148 CTAs), so the CTAs of a wave share 2 x kGtSB
+// operand blocks in L2 instead of streaming one A_J block each from HBM; warp 0
+// produces (bulk copies into a 4-stage ring), warp 1 issues the MMAs, warps 2-9
+// drain TMEM and finally store the fp16 hi/lo SymOut values (G * 2^s_G).  Producer
+// and MMA warps run convergently on warp-uniform operands with one elected lane
+// issuing (see sym_step_kernel: issuing from inside `if (lane == 0)` costs an
+// ELECT / R2UR / BRA.U.ANY loop per instruction).
 #pragma once
 
 #include "sym_kernels.cuh"
@@ -40,10 +50,14 @@ constexpr uint32_t kGtStage = 4 * kGtPlane;       // A_I hi, lo; A_J hi, lo
 // + the second-level sums of the epilogue threads ([64][256] fp32, conflict-free)
 constexpr size_t kGtS2 = (size_t)64 * kGtEpi * 32 * 4;
 constexpr size_t kGtSmem = (size_t)kGtStages * kGtStage + kGtS2 + 256;
+constexpr int kGtTmemCols = 256;                  // 2 x 128 accumulator columns
+
+constexpr int kGtSB = 12;                         // super-block edge in tiles (L2 reuse)
 
 // byte offset of (column j, k within the chunk) in one plane of a k-chunk
-__host__ __device__ inline size_t gt_off(int j, int k, int Np) {
-    return (size_t)(k / 8) * (Np / 8) * 128 + (size_t)(j / 8) * 128 + (j % 8) * 16 + (k % 8) * 2;
+__host__ __device__ inline size_t gt_off(int j, int k, int /*Np*/) {
+    return (size_t)(j / kSyT) * kGtPlane + (size_t)(k / 8) * ((kSyT / 8) * 128) +
+           (size_t)((j % kSyT) / 8) * 128 + (j % 8) * 16 + (k % 8) * 2;
 }
 
 // per-instance exact scale: max|A| * 2^s in [2^14, 2^15)
@@ -101,16 +115,43 @@ struct GtArgs {
     int I0, I1;                      // row blocks built by this rank [I0, I1)
     int nRB;                         // column blocks (ceil(N / 128))
     long long ntile;                 // tiles (I, J), I0 <= I < I1, I <= J < nRB
+    unsigned* round;                 // zeroed per launch: producers that finished issuing a round
+    unsigned long long* tlog;        // option "timeline": CTA 0's per-chunk stamps (sym_kernels.cuh rows)
 };
 
-// tile t -> (I, J): row-major over the upper triangle rows [I0, I1)
+// tile t -> (I, J): super-blocks of kGtSB x kGtSB tiles, row-major over the super-
+// block triangle of the rows [I0, I1); inside a super-block row-major (I <= J)
 __device__ __forceinline__ void gt_tile(const GtArgs& a, long long t, int& I, int& J) {
-    I = a.I0;
-    while (t >= a.nRB - I) {
-        t -= a.nRB - I;
-        ++I;
+    for (int R0 = a.I0; R0 < a.I1; R0 += kGtSB) {
+        const int nI = min(kGtSB, a.I1 - R0);
+        // this super-row: the diagonal block (columns R0 .. R0 + nI), then full blocks
+        const long long diag = (long long)nI * (nI + 1) / 2;
+        const long long rest = (long long)nI * (a.nRB - R0 - nI);
+        if (t >= diag + rest) {
+            t -= diag + rest;
+            continue;
+        }
+        if (t < diag) {  // row i has nI - i tiles
+            int i = 0;
+            while (t >= nI - i) {
+                t -= nI - i;
+                ++i;
+            }
+            I = R0 + i;
+            J = I + (int)t;
+            return;
+        }
+        t -= diag;
+        const long long per = (long long)nI * kGtSB;  // tiles of a full super-block
+        const int sb = (int)(t / per);
+        t -= sb * per;
+        const int C0 = R0 + nI + sb * kGtSB;
+        const int nJ = min(kGtSB, a.nRB - C0);
+        I = R0 + (int)(t / nJ);
+        J = C0 + (int)(t % nJ);
+        return;
     }
-    J = I + (int)t;
+    I = J = a.I1 - 1;  // not reached for t < ntile
 }
 
 __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GtArgs a) {
@@ -136,7 +177,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GtArgs a) {
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(&s_tmem)),
-                     "n"(256));
+                     "n"(kGtTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -144,53 +185,82 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GtArgs a) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = s_tmem;
     const size_t plane = (size_t)a.Np * kGtK * 2;  // bytes per plane
-    const size_t kgs = (size_t)(a.Np / 8) * 128;   // bytes per k-group row of a plane
     const unsigned char* Pb = reinterpret_cast<const unsigned char*>(a.P);
     constexpr uint32_t kBlk = (kSyT / 8) * 128;    // 2 KB: one k-group of one 128-column block
 
-    if (warp == 0) {
-        if (lane == 0) {  // ---------------------------------------------- producer
-            const uint64_t pol = sy_policy_last();
-            long long it = 0;
-            for (long long t = blockIdx.x; t < a.ntile; t += gridDim.x) {
-                int I, J;
-                gt_tile(a, t, I, J);
-                for (int c = 0; c < a.nch; ++c, ++it) {
-                    const int s = (int)(it % kGtStages);
-                    if (it >= kGtStages) mbar_wait(&empty[s], (uint32_t)(((it / kGtStages) - 1) & 1));
-                    unsigned char* st = smem + s * kGtStage;
-                    mbar_arrive_expect_tx(&full[s], kGtStage);
-                    for (int p = 0; p < 2; ++p)
-                        for (int kg = 0; kg < kGtK / 8; ++kg) {
-                            const unsigned char* src = Pb + ((size_t)c * 2 + p) * plane + kg * kgs;
-                            sy_bulk_g2s(st + p * kGtPlane + kg * kBlk, src + (size_t)I * kBlk, kBlk,
-                                        &full[s], pol);
-                            sy_bulk_g2s(st + (2 + p) * kGtPlane + kg * kBlk, src + (size_t)J * kBlk,
-                                        kBlk, &full[s], pol);
-                        }
-                }
+    if (warp == 0) {  // -------------------------------------------------- producer
+        const uint64_t pol = sy_policy_last();
+        const uint32_t smem0 = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
+        const uint32_t full0 = __shfl_sync(0xffffffffu, smem_u32(full), 0);
+        long long it = 0;
+        unsigned rnd = 0;
+        for (long long t = blockIdx.x; t < a.ntile; t += gridDim.x, ++rnd) {
+            // Round gate (a locality hint, never needed for correctness): start round r
+            // only when every CTA's producer has issued all of round r - 1, so the CTAs
+            // of a wave walk the k-chunks of ONE super-block together and its 2 x kGtSB
+            // operand blocks are read from HBM once and from L2 by everyone else.  Without
+            // it the CTAs drift apart by whole tiles and each streams its own operands
+            // from HBM (measured: 32 KB per chunk-step at the HBM rate).  The wait is
+            // bounded (~0.5 ms); on expiry the CTA simply goes on.
+            if (rnd && lane == 0) {
+                const unsigned want = rnd * gridDim.x;
+                const long long t0 = clock64();
+                unsigned v;
+                do {
+                    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.round) : "memory");
+                } while (v < want && clock64() - t0 < (1ll << 20));
             }
+            __syncwarp();
+            int I, J;
+            gt_tile(a, t, I, J);
+            I = __shfl_sync(0xffffffffu, I, 0);
+            J = __shfl_sync(0xffffffffu, J, 0);
+            const unsigned char* srcI = Pb + (size_t)I * kGtPlane;
+            const unsigned char* srcJ = Pb + (size_t)J * kGtPlane;
+            for (int c = 0; c < a.nch; ++c, ++it) {
+                const int s = (int)(it % kGtStages);
+                if (it >= kGtStages) mbar_wait(&empty[s], (uint32_t)(((it / kGtStages) - 1) & 1));
+                if (a.tlog && blockIdx.x == 0 && it < 128 && lane == 0)
+                    a.tlog[(kTlTile + it) * 4 + 3] = sy_gtime();
+                if (sy_elect_one()) {
+                    const uint32_t st = smem0 + s * kGtStage, fb = full0 + s * 8;
+                    sy_expect_tx_u(fb, kGtStage);
+#pragma unroll
+                    for (int p = 0; p < 2; ++p) {
+                        const size_t o = ((size_t)c * 2 + p) * plane;
+                        sy_bulk_u(st + p * kGtPlane, srcI + o, kGtPlane, fb, pol);
+                        sy_bulk_u(st + (2 + p) * kGtPlane, srcJ + o, kGtPlane, fb, pol);
+                    }
+                }
+                __syncwarp();
+            }
+            if (lane == 0) atomicAdd(a.round, 1u);
         }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---------------------------------------------- MMA issuer
-            constexpr uint32_t idesc = sy_idesc(kSyT, 0);  // F32 += F16 x F16, M = N = 128
-            long long it = 0;
-            for (long long t = blockIdx.x; t < a.ntile; t += gridDim.x) {
-                for (int c = 0; c < a.nch; ++c, ++it) {
-                    const int s = (int)(it % kGtStages), buf = (int)(it & 1);
-                    if (it >= 2) mbar_wait(&tm_empty[buf], (uint32_t)(((it >> 1) - 1) & 1));
-                    mbar_wait(&full[s], (uint32_t)((it / kGtStages) & 1));
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t aHi = smem_u32(smem + s * kGtStage), aLo = aHi + kGtPlane;
-                    const uint32_t bHi = aHi + 2 * kGtPlane, bLo = aHi + 3 * kGtPlane;
-                    const uint32_t d = tmem + buf * kSyT;
+    } else if (warp == 1) {  // ------------------------------------------ MMA issuer
+        constexpr uint32_t idesc = sy_idesc(kSyT, 0);  // F32 += F16 x F16, M = N = 128
+        const uint32_t smem0 = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
+        const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+        long long it = 0;
+        for (long long t = blockIdx.x; t < a.ntile; t += gridDim.x) {
+            for (int c = 0; c < a.nch; ++c, ++it) {
+                const int s = (int)(it % kGtStages), buf = (int)(it & 1);
+                const bool tl = a.tlog && blockIdx.x == 0 && it < 128 && lane == 0;
+                if (it >= 2) mbar_wait(&tm_empty[buf], (uint32_t)(((it >> 1) - 1) & 1));
+                if (tl) a.tlog[(kTlTile + it) * 4 + 0] = sy_gtime();
+                mbar_wait(&full[s], (uint32_t)((it / kGtStages) & 1));
+                if (tl) a.tlog[(kTlTile + it) * 4 + 1] = sy_gtime();
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t aHi = smem0 + s * kGtStage;
+                const uint32_t d = tmem_u + buf * kSyT;
+                // descriptors of k-step 0; planes and k-steps only move the start address
+                const uint64_t dAh0 = umma_desc(aHi, kBlk, 128);
+                if (sy_elect_one()) {
 #pragma unroll
                     for (int kb = 0; kb < kGtK / 16; ++kb) {
-                        const uint32_t o = kb * 2 * kBlk;
-                        const uint64_t dAh = umma_desc(aHi + o, kBlk, 128);
-                        const uint64_t dAl = umma_desc(aLo + o, kBlk, 128);
-                        const uint64_t dBh = umma_desc(bHi + o, kBlk, 128);
-                        const uint64_t dBl = umma_desc(bLo + o, kBlk, 128);
+                        const uint64_t dAh = dAh0 + (uint64_t)(kb * 2 * kBlk >> 4);
+                        const uint64_t dAl = dAh + (uint64_t)(kGtPlane >> 4);
+                        const uint64_t dBh = dAh + (uint64_t)(2 * kGtPlane >> 4);
+                        const uint64_t dBl = dAh + (uint64_t)(3 * kGtPlane >> 4);
                         sy_mma(d, dAh, dBh, idesc, kb ? 1u : 0u);  // a fresh accumulator per chunk
                         sy_mma(d, dAh, dBl, idesc, 1u);
                         sy_mma(d, dAl, dBh, idesc, 1u);
@@ -198,6 +268,8 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GtArgs a) {
                     tc_commit(&empty[s]);
                     tc_commit(&tm_full[buf]);
                 }
+                __syncwarp();
+                if (tl) a.tlog[(kTlTile + it) * 4 + 2] = sy_gtime();
             }
         }
     } else {  // ----------------------------------------------------- epilogue
@@ -219,6 +291,8 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GtArgs a) {
             for (int c = 0; c < a.nch; ++c, ++it) {
                 const int buf = (int)(it & 1);
                 mbar_wait(&tm_full[buf], (uint32_t)((it >> 1) & 1));
+                const bool tle = a.tlog && blockIdx.x == 0 && it < 128 && threadIdx.x == 64;
+                if (tle) a.tlog[(kTlTile + 128 + it) * 4 + 0] = sy_gtime();
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t ta = tmem + buf * kSyT + h * 64 + ((uint32_t)(q * 32) << 16);
 #pragma unroll
@@ -236,6 +310,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GtArgs a) {
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tm_empty[buf]);
+                if (tle) a.tlog[(kTlTile + 128 + it) * 4 + 1] = sy_gtime();
                 if ((c + 1) % kGtInner == 0) {
 #pragma unroll
                     for (int u = 0; u < 64; ++u) {
@@ -267,7 +342,8 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GtArgs a) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(256));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "n"(kGtTmemCols));
 }
 
 }  // namespace cimcs

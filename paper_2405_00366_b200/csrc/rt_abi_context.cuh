@@ -73,6 +73,7 @@ void cimcs_destroy(cimcs_ctx* c) {
     if (c->alt) cudaFree(c->alt);
     if (c->err) cudaFree(c->err);
     if (c->pump) cudaFree(c->pump);
+    if (c->dTl) cudaFree(c->dTl);
     if (c->hist) cudaFree(c->hist);
     if (c->pin) cudaFreeHost(c->pin);
     if (c->pin_c0) cudaFreeHost(c->pin_c0);
@@ -108,6 +109,20 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
         c->use_pdl = v != 0;
         drop_graphs(c);
     }
+    else if (k == "timeline") {  // measurement aid: stamps of the last tile / update launch pair
+        if (v != 0 && !c->dTl) {
+            if (int rc = dalloc(c, &c->dTl, (size_t)kTlCap * 4 * 8)) return rc;
+        } else if (v == 0 && c->dTl) {
+            cudaStreamSynchronize(c->stream);
+            cudaFree(c->dTl);
+            c->dTl = nullptr;
+        }
+        drop_graphs(c);
+    }
+    else if (k == "sched_ctas") {  // measurement aid: persistent CTAs of the item schedules
+        if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set sched_ctas before set_problems");
+        c->sched_ctas = (int)std::max<int64_t>(0, v);
+    }
     else if (k == "cluster_loop") {
         c->use_cluster = v != 0;
         drop_graphs(c);
@@ -124,6 +139,14 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
     }
     else return fail(CIMCS_CONFIG_ERROR, "unknown option " + k);
     return 0;
+}
+
+
+int cimcs_get_timeline(cimcs_ctx* c, uint64_t* out, int64_t cap, int64_t* n) {
+    if (!c || !out || !n) return fail(CIMCS_INPUT_ERROR, "null argument");
+    if (!c->dTl) return fail(CIMCS_CONFIG_ERROR, "set option timeline = 1 first");
+    *n = std::min<int64_t>(cap, (int64_t)kTlCap * 4);
+    return copy_sync(c, out, c->dTl, (size_t)*n * 8, cudaMemcpyDeviceToHost);
 }
 
 }  // extern "C"

@@ -564,9 +564,11 @@ int cimcs_build_coupling(cimcs_ctx* c) {
         const int nchx = (c->Mmax + kGtK - 1) / kGtK;
         __half* Pv = nullptr;
         unsigned long long* amax = nullptr;
+        unsigned* rounds = nullptr;  // per instance: the tile kernel's round gate (zeroed)
         if ((rc = dalloc(c, &Pv, (size_t)nchx * 2 * Np * kGtK * 2)) ||
-            (rc = dalloc(c, &amax, (size_t)c->B * 8)))
+            (rc = dalloc(c, &amax, (size_t)c->B * 8)) || (rc = dalloc(c, &rounds, (size_t)c->B * 4)))
             return rc;
+        std::unique_ptr<unsigned, decltype(&cudaFree)> rguard(rounds, &cudaFree);
         std::unique_ptr<__half, decltype(&cudaFree)> pguard(Pv, &cudaFree);
         std::unique_ptr<unsigned long long, decltype(&cudaFree)> aguard(amax, &cudaFree);
         static std::atomic<unsigned long long> attr{0};
@@ -598,7 +600,9 @@ int cimcs_build_coupling(cimcs_ctx* c) {
             ga.I1 = Ie;
             ga.nRB = c->nRB;
             ga.ntile = ntile;
-            const int grid = (int)std::min<long long>(ntile, c->num_sms);
+            ga.round = rounds + b;
+            ga.tlog = c->dTl;
+            const int grid = (int)std::min<long long>(ntile, c->sched_n());
             gram_tc_kernel<<<grid, kGtThreads, kGtSmem, c->stream>>>(ga);
             CK(cudaGetLastError());
             c->timing.other_launches += 3;

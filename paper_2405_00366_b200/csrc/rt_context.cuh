@@ -70,6 +70,7 @@ struct cimcs_ctx {
     int* dSg = nullptr;    // per-instance gram scale exponent
     float* dSpart = nullptr;  // partial products [B][nRB][nSB][128][NR]
     bool use_pdl = true;      // programmatic dependent launch between the step kernels
+    unsigned long long* dTl = nullptr;  // option "timeline": per-CTA %globaltimer stamps
     int gram_l2 = 0;          // per instance, the first gram_l2 tiles of the triangle are copied
                               // with evict_last (an L2-resident subset), the rest evict_first
     bool kernel_timing = false;  // eager mode: CUDA events around each step-mode tile kernel
@@ -106,6 +107,8 @@ struct cimcs_ctx {
     size_t spart_elems = 0;
     int nch = 0;
     int num_sms = 148;
+    int sched_ctas = 0;   // option: CTAs of the symmetric item schedules (0: one per SM)
+    int sched_n() const { return sched_ctas > 0 ? std::min(sched_ctas, num_sms) : num_sms; }
     // problems
     int B = 0, N = 0, ldN = 0, Mmax = 0;
     std::vector<int> M;

@@ -197,7 +197,7 @@ int enqueue_refit_compact64(cimcs_ctx* c, const StepScalars& s, int iters, bool 
         if ((int)items.size() > c->cmp_items_cap) return fail(CIMCS_CUDA_ERROR, "cmp64 schedule capacity");
         std::vector<int2> flat;
         std::vector<int> beg;
-        c->cmp_sched.grid = lpt_place(items, c->num_sms, flat, beg);
+        c->cmp_sched.grid = lpt_place(items, c->sched_n(), flat, beg);
         c->cmp_sched.nb = B;
         c->cmp_sched.nRB = nRBc;
         c->cmp_sched.S = kS6;

@@ -104,6 +104,7 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb) {
     sa.gram_keep = c->gram_l2;
     sa.S = c->symS;
     sa.rowmap = c->cmp_active ? c->cU : nullptr;
+    sa.tlog = c->dTl && (size_t)c->B * c->nRB <= (size_t)(kTlCap - kTlUpd) ? c->dTl : nullptr;
     if (nb == 0 || c->ntri == 0) return 0;
     const cimcs_ctx::SymSched* ss = nullptr;
     if (int rc = sym_schedule(c, nb, &ss)) return rc;

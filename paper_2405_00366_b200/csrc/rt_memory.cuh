@@ -210,7 +210,7 @@ int sym_schedule(cimcs_ctx* c, int nb, const cimcs_ctx::SymSched** out, bool s64
             }
     std::vector<int2> flat;
     std::vector<int> beg;
-    const int grid = lpt_place(items, c->num_sms, flat, beg);
+    const int grid = lpt_place(items, c->sched_n(), flat, beg);
     cimcs_ctx::SymSched q;
     q.nb = nb;
     q.nRB = nRB;

@@ -214,7 +214,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) sym64_step_kernel(Sym64Args 
     // inside a CIM call, so the first stages' gram copies may start earlier)
     constexpr bool kEarly = MODE == EPI_STEP_BN || MODE == EPI_STEP_CN;
     sy_pdl_trigger();
-    if (!kEarly || threadIdx.x != kT6Compute * 32) sy_pdl_wait();
+    if (!kEarly || warp != kT6Compute) sy_pdl_wait();
 
     auto item = [&](int k, int& b, int& P, int& Q, int& nI, int& nJ) {
         const int2 it = sa.items[k];
@@ -231,44 +231,68 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) sym64_step_kernel(Sym64Args 
 
     if (warp == kT6Compute) {
         // ------------------------------------------------------ producer
-        if (lane == 0) {
-            const uint64_t pG = sy_policy_first(), pW = sy_policy_last();
-            // stage s of tile tt: expect its bytes, copy the gram tile
-            auto g_part = [&](int s, int b, int I, int J) {
-                unsigned char* st = smem + s * kStage;
-                mbar_arrive_expect_tx(&full[s], kT6TileBytes + (I != J ? 2 : 1) * (uint32_t)kWB);
-                sy_bulk_g2s(st, sa.Gt + ((size_t)b * sa.ntri + sy_tri(I, J, nRB)) * (kT6 * kT6),
-                            kT6TileBytes, &full[s], pG);
-            };
-            int tt = 0;
-            for (int k = it0; k < it1 && tt < kT6Stages; ++k) {  // fill before the PDL wait
-                int b, P, Q, nI, nJ;
-                item(k, b, P, Q, nI, nJ);
-                for (int ii = 0; ii < nI && tt < kT6Stages; ++ii)
-                    for (int jj = P == Q ? ii : 0; jj < nJ && tt < kT6Stages; ++jj, ++tt)
-                        g_part(tt, b, blk0(P) + ii, blk0(Q) + jj);
+        // (convergent warp, warp-uniform operands, one elected lane issues: a bulk copy
+        // issued from inside `if (lane == 0)` is wrapped in an ELECT / R2UR / BRA.U.ANY
+        // loop by ptxas -- sym_kernels.cuh)
+        const uint64_t pG = sy_policy_first(), pW = sy_policy_last();
+        const uint32_t smem0 = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
+        const uint32_t full0 = __shfl_sync(0xffffffffu, smem_u32(full), 0);
+        const int k0 = __shfl_sync(0xffffffffu, it0, 0), k1 = __shfl_sync(0xffffffffu, it1, 0);
+        auto item_u = [&](int k, int& b, int& P, int& Q, int& nI, int& nJ) {
+            const int2 itv = sa.items[k];
+            b = __shfl_sync(0xffffffffu, itv.x, 0);
+            const int iy = __shfl_sync(0xffffffffu, itv.y, 0);
+            P = iy >> 16;
+            Q = iy & 0xffff;
+            nI = sa.seg ? __shfl_sync(0xffffffffu, sa.seg[P].y, 0) : min(kS6, nRB - P * kS6);
+            nJ = sa.seg ? __shfl_sync(0xffffffffu, sa.seg[Q].y, 0) : min(kS6, nRB - Q * kS6);
+        };
+        auto blk0_u = [&](int P) {
+            return sa.seg ? __shfl_sync(0xffffffffu, sa.seg[P].x, 0) : P * kS6;
+        };
+        // stage s of a tile: expect its bytes, copy the gram tile
+        auto g_part = [&](int s, int b, int I, int J) {
+            const double* src = sa.Gt + ((size_t)b * sa.ntri + sy_tri(I, J, nRB)) * (kT6 * kT6);
+            if (sy_elect_one()) {
+                const uint32_t fb = full0 + s * 8;
+                sy_expect_tx_u(fb, kT6TileBytes + (I != J ? 2 : 1) * (uint32_t)kWB);
+                sy_bulk_u(smem0 + s * (uint32_t)kStage, src, kT6TileBytes, fb, pG);
             }
-            if (kEarly) sy_pdl_wait();
-            tt = 0;
-            for (int k = it0; k < it1; ++k) {
-                int b, P, Q, nI, nJ;
-                item(k, b, P, Q, nI, nJ);
-                const double* Wb = sa.WTin + (size_t)b * nRB * (kT6 * NR);
-                for (int ii = 0; ii < nI; ++ii)
-                    for (int jj = P == Q ? ii : 0; jj < nJ; ++jj, ++tt) {
-                        const int I = blk0(P) + ii, J = blk0(Q) + jj, s = tt % kT6Stages;
-                        if (tt >= kT6Stages) {
-                            mbar_wait(&empty[s], ((tt / kT6Stages) - 1) & 1);
-                            g_part(s, b, I, J);
-                        }
-                        unsigned char* st = smem + s * kStage;
-                        sy_bulk_g2s(st + kT6TileBytes, Wb + (size_t)J * (kT6 * NR), kWB,
-                                    &full[s], pW);
-                        if (I != J)
-                            sy_bulk_g2s(st + kT6TileBytes + kWB, Wb + (size_t)I * (kT6 * NR),
-                                        kWB, &full[s], pW);
+            __syncwarp();
+        };
+        int tt = 0;
+        for (int k = k0; k < k1 && tt < kT6Stages; ++k) {  // fill before the PDL wait
+            int b, P, Q, nI, nJ;
+            item_u(k, b, P, Q, nI, nJ);
+            const int bP = blk0_u(P), bQ = blk0_u(Q);
+            for (int ii = 0; ii < nI && tt < kT6Stages; ++ii)
+                for (int jj = P == Q ? ii : 0; jj < nJ && tt < kT6Stages; ++jj, ++tt)
+                    g_part(tt, b, bP + ii, bQ + jj);
+        }
+        if (kEarly) sy_pdl_wait();
+        tt = 0;
+        for (int k = k0; k < k1; ++k) {
+            int b, P, Q, nI, nJ;
+            item_u(k, b, P, Q, nI, nJ);
+            const int bP = blk0_u(P), bQ = blk0_u(Q);
+            const double* Wb = sa.WTin + (size_t)b * nRB * (kT6 * NR);
+            for (int ii = 0; ii < nI; ++ii)
+                for (int jj = P == Q ? ii : 0; jj < nJ; ++jj, ++tt) {
+                    const int I = bP + ii, J = bQ + jj, s = tt % kT6Stages;
+                    if (tt >= kT6Stages) {
+                        mbar_wait(&empty[s], ((tt / kT6Stages) - 1) & 1);
+                        g_part(s, b, I, J);
                     }
-            }
+                    if (sy_elect_one()) {
+                        const uint32_t st = smem0 + s * (uint32_t)kStage + kT6TileBytes,
+                                       fb = full0 + s * 8;
+                        sy_bulk_u(st, Wb + (size_t)J * (kT6 * NR), (uint32_t)kWB, fb, pW);
+                        if (I != J)
+                            sy_bulk_u(st + (uint32_t)kWB, Wb + (size_t)I * (kT6 * NR), (uint32_t)kWB,
+                                      fb, pW);
+                    }
+                    __syncwarp();
+                }
         }
         return;
     }

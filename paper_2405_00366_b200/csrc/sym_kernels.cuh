@@ -51,6 +51,9 @@
 
 namespace cimcs {
 
+#ifndef SY_UPD_OCC
+#define SY_UPD_OCC 2  // update-kernel CTAs per SM the register cap allows (3 / 4 spill; measured)
+#endif
 constexpr int kSyT = 128;                              // tile edge
 constexpr int kSyStages = 2;
 constexpr int kSyPlaneHalfs = kSyT * kSyT;             // 16384
@@ -131,6 +134,14 @@ __device__ __forceinline__ void sy_mma(uint32_t d, uint64_t da, uint64_t db, uin
         "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
+// one lane of the (converged) warp
+__device__ __forceinline__ bool sy_elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ uint64_t sy_policy_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -156,6 +167,19 @@ __device__ __forceinline__ void sy_bulk_g2s(void* dst, const void* src, uint32_t
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
+// the same with shared addresses as 32-bit values (warp-uniform: uniform registers)
+__device__ __forceinline__ void sy_bulk_u(uint32_t dst, const void* src, uint32_t bytes,
+                                          uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+        "[%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void sy_expect_tx_u(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void sy_st_last(float4* p, float4 v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
                  "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
@@ -179,7 +203,20 @@ struct SymArgs {
     int gram_keep;         // tiles t < gram_keep of each triangle copied with evict_last
     int S;                 // item edge in tiles (kSyS; 2 for the compacted refit)
     const int* rowmap;     // compacted refit: row -> original spin (error reports), or null
+    // measurement aid (option "timeline"): %globaltimer stamps of the last launch pair,
+    // 4 per CTA: tile CTA x at [x] = (entry, past the PDL wait, last item stored, -),
+    // update CTA (K, b) at [kTlUpd + b * nRB + K] = (entry, past the PDL wait, exit, -)
+    unsigned long long* tlog;
 };
+// per-tile stamps of tile CTA 0 at [kTlTile + tt] = (MMA thread: accumulator free, tile
+// landed, MMAs issued; producer: refill of the tile's stage issued) and [kTlTile + 128 +
+// tt] = (epilogue warp 2: accumulator complete, accumulator read + released, -, -)
+constexpr int kTlUpd = 256, kTlTile = 4096, kTlCap = kTlUpd + 8192;
+__device__ __forceinline__ unsigned long long sy_gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 template <int NR>
 __host__ __device__ constexpr size_t sy_bbytes() { return (size_t)2 * NR * kSyT * 2; }
@@ -309,94 +346,143 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
     // programmatic dependent launch: the update kernel may be scheduled now (its
     // CTAs wait for this grid in griddepcontrol.wait); this grid's own reads of
     // w and writes of the partial products wait for the previous update kernel.
-    // In the step modes the producer thread waits later: every CIM call starts
+    // In the step modes the producer warp waits later: every CIM call starts
     // with a plain (non-PDL) launch issued after the gram was built, and nothing
     // writes the gram tiles during the call, so the planes of the first stages
     // are copied while the previous update kernel finishes.
     constexpr bool kEarly = MODE == EPI_STEP_BN || MODE == EPI_STEP_CN;
+    if (sa.tlog && threadIdx.x == 0) sa.tlog[blockIdx.x * 4 + 0] = sy_gtime();
     sy_pdl_trigger();
-    if (!kEarly || threadIdx.x != 0) sy_pdl_wait();
+    if (!kEarly || warp != 0) sy_pdl_wait();
 
     if (warp == 0) {
         // ------------------------------------------------------ producer
-        if (lane == 0) {
-            const uint64_t pGf = sy_policy_first(), pW = sy_policy_last();
-            // stage s of tile tt: expect its bytes, copy the two gram planes
-            auto g_part = [&](int s, int b, int I, int J) {
-                const int tri = sy_tri(I, J, nRB);
-                const __half* src = sa.Gs + (size_t)b * sa.ntri * 2 * kSyPlaneHalfs +
-                                    (size_t)tri * 2 * kSyPlaneHalfs;
-                const uint64_t pG = tri < sa.gram_keep ? pW : pGf;
-                unsigned char* st = smem + s * kStage;
-                mbar_arrive_expect_tx(&full[s], 2 * kSyPlaneBytes + (I != J ? 2 : 1) * kBB);
+        // (convergent warp, warp-uniform operands, one elected lane issues: see the
+        // MMA issuer below for why)
+        const uint64_t pGf = sy_policy_first(), pW = sy_policy_last();
+        const uint32_t smem0 = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
+        const uint32_t full0 = __shfl_sync(0xffffffffu, smem_u32(full), 0);
+        const int k0 = __shfl_sync(0xffffffffu, it0, 0), k1 = __shfl_sync(0xffffffffu, it1, 0);
+        auto item_u = [&](int k, int& b, int& I0, int& J0, int& nI, int& nJ, bool& diag) {
+            const int2 itv = sa.items[k];
+            b = sa.b0 + __shfl_sync(0xffffffffu, itv.x, 0);
+            const int iy = __shfl_sync(0xffffffffu, itv.y, 0);
+            const int P = iy >> 16, Q = iy & 0xffff;
+            I0 = P * sa.S;
+            J0 = Q * sa.S;
+            nI = min(sa.S, nRB - I0);
+            nJ = min(sa.S, nRB - J0);
+            diag = P == Q;
+        };
+        // stage s of a tile: expect its bytes, copy the two gram planes
+        auto g_part = [&](int s, int b, int I, int J) {
+            const int tri = sy_tri(I, J, nRB);
+            const __half* src = sa.Gs + ((size_t)b * sa.ntri + tri) * 2 * kSyPlaneHalfs;
+            const uint64_t pG = tri < sa.gram_keep ? pW : pGf;
+            if (sy_elect_one()) {
+                const uint32_t st = smem0 + s * kStage, fb = full0 + s * 8;
+                sy_expect_tx_u(fb, 2 * kSyPlaneBytes + (I != J ? 2 : 1) * kBB);
                 // the gram streams through L2 once per step; w tiles are re-read
-                sy_bulk_g2s(st, src, kSyPlaneBytes, &full[s], pG);
-                sy_bulk_g2s(st + kSyPlaneBytes, src + kSyPlaneHalfs, kSyPlaneBytes, &full[s], pG);
-            };
-            int tt = 0;
-            for (int k = it0; k < it1 && tt < kSyStages; ++k) {
-                const SyItem m = sy_item(sa, k, nRB);
-                for (int ii = 0; ii < m.nI && tt < kSyStages; ++ii)
-                    for (int jj = m.diag ? ii : 0; jj < m.nJ && tt < kSyStages; ++jj, ++tt)
-                        g_part(tt, m.b, m.I0 + ii, m.J0 + jj);
+                sy_bulk_u(st, src, kSyPlaneBytes, fb, pG);
+                sy_bulk_u(st + kSyPlaneBytes, src + kSyPlaneHalfs, kSyPlaneBytes, fb, pG);
             }
-            if (kEarly) sy_pdl_wait();
-            tt = 0;
-            for (int k = it0; k < it1; ++k) {
-                const SyItem m = sy_item(sa, k, nRB);
-                const __half* wb = sa.WBin + (size_t)m.b * nRB * (2 * NR * kSyT);
-                for (int ii = 0; ii < m.nI; ++ii)
-                    for (int jj = m.diag ? ii : 0; jj < m.nJ; ++jj, ++tt) {
-                        const int I = m.I0 + ii, J = m.J0 + jj, s = tt % kSyStages;
-                        if (tt >= kSyStages) {
-                            mbar_wait(&empty[s], ((tt / kSyStages) - 1) & 1);
-                            g_part(s, m.b, I, J);
-                        }
-                        unsigned char* st = smem + s * kStage;
-                        sy_bulk_g2s(st + 2 * kSyPlaneBytes, wb + (size_t)J * (2 * NR * kSyT), kBB,
-                                    &full[s], pW);
-                        if (I != J)
-                            sy_bulk_g2s(st + 2 * kSyPlaneBytes + kBB,
-                                        wb + (size_t)I * (2 * NR * kSyT), kBB, &full[s], pW);
+            __syncwarp();
+        };
+        int tt = 0;
+        for (int k = k0; k < k1 && tt < kSyStages; ++k) {
+            int b, I0, J0, nI, nJ;
+            bool diag;
+            item_u(k, b, I0, J0, nI, nJ, diag);
+            for (int ii = 0; ii < nI && tt < kSyStages; ++ii)
+                for (int jj = diag ? ii : 0; jj < nJ && tt < kSyStages; ++jj, ++tt)
+                    g_part(tt, b, I0 + ii, J0 + jj);
+        }
+        if (kEarly) sy_pdl_wait();
+        if (sa.tlog && lane == 0) sa.tlog[blockIdx.x * 4 + 1] = sy_gtime();
+        tt = 0;
+        for (int k = k0; k < k1; ++k) {
+            int b, I0, J0, nI, nJ;
+            bool diag;
+            item_u(k, b, I0, J0, nI, nJ, diag);
+            const __half* wb = sa.WBin + (size_t)b * nRB * (2 * NR * kSyT);
+            for (int ii = 0; ii < nI; ++ii)
+                for (int jj = diag ? ii : 0; jj < nJ; ++jj, ++tt) {
+                    const int I = I0 + ii, J = J0 + jj, s = tt % kSyStages;
+                    if (tt >= kSyStages) {
+                        mbar_wait(&empty[s], ((tt / kSyStages) - 1) & 1);
+                        g_part(s, b, I, J);
                     }
-            }
+                    if (sa.tlog && blockIdx.x == 0 && tt < 128 && lane == 0)
+                        sa.tlog[(kTlTile + tt) * 4 + 3] = sy_gtime();
+                    if (sy_elect_one()) {
+                        const uint32_t st = smem0 + s * kStage, fb = full0 + s * 8;
+                        sy_bulk_u(st + 2 * kSyPlaneBytes, wb + (size_t)J * (2 * NR * kSyT), kBB, fb, pW);
+                        if (I != J)
+                            sy_bulk_u(st + 2 * kSyPlaneBytes + kBB, wb + (size_t)I * (2 * NR * kSyT),
+                                      kBB, fb, pW);
+                    }
+                    __syncwarp();
+                }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t id_cat = sy_idesc(2 * NR, 0), id_hi = sy_idesc(NR, 0);
-            constexpr uint32_t id_catT = sy_idesc(2 * NR, 1), id_hiT = sy_idesc(NR, 1);
-            constexpr uint32_t kstr = (kSyT / 8) * 128;   // K-group stride of the tile (2 KB)
-            constexpr uint32_t lboB = (2 * NR / 8) * 128;  // K-group stride of a B tile
-            int tt = 0;
-            for (int k = it0; k < it1; ++k) {
-                const SyItem m = sy_item(sa, k, nRB);
-                for (int ii = 0; ii < m.nI; ++ii)
-                    for (int jj = m.diag ? ii : 0; jj < m.nJ; ++jj, ++tt) {
-                        const int s = tt % kSyStages, acc = tt % kSyAcc;
-                        const bool off = m.I0 + ii != m.J0 + jj;
-                        if (tt >= kSyAcc) mbar_wait(&tm_empty[acc], ((tt / kSyAcc) - 1) & 1);
-                        mbar_wait(&full[s], (tt / kSyStages) & 1);
-                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                        const uint32_t aHi = smem_u32(smem + s * kStage), aLo = aHi + kSyPlaneBytes;
-                        const uint32_t bJ = aHi + 2 * kSyPlaneBytes, bI = bJ + kBB;
-                        const uint32_t d1 = tmem + acc * 4 * NR, d2 = d1 + 2 * NR;
+        // The whole warp walks the tile list convergently and every operand is
+        // warp-uniform (loaded values go through __shfl_sync(.., 0) so the compiler
+        // keeps them in uniform registers); one elected lane issues.  Issuing from
+        // inside an `if (lane == 0)` branch instead made ptxas wrap EVERY tcgen05.mma
+        // in an ELECT / 5 x R2UR / BRA.U.ANY loop: 1.37 us of issue per tile, which
+        // bound the whole kernel (tools/tile_pipeline.py).
+        constexpr uint32_t id_cat = sy_idesc(2 * NR, 0), id_hi = sy_idesc(NR, 0);
+        constexpr uint32_t id_catT = sy_idesc(2 * NR, 1), id_hiT = sy_idesc(NR, 1);
+        constexpr uint32_t kstr = (kSyT / 8) * 128;   // K-group stride of the tile (2 KB)
+        constexpr uint32_t lboB = (2 * NR / 8) * 128;  // K-group stride of a B tile
+        const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+        const uint32_t smem0 = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
+        const int k0 = __shfl_sync(0xffffffffu, it0, 0), k1 = __shfl_sync(0xffffffffu, it1, 0);
+        int tt = 0;
+        for (int k = k0; k < k1; ++k) {
+            const int2 itv = sa.items[k];
+            const int iy = __shfl_sync(0xffffffffu, itv.y, 0);
+            const int P = iy >> 16, Q = iy & 0xffff;
+            const int nI = min(sa.S, nRB - P * sa.S), nJ = min(sa.S, nRB - Q * sa.S);
+            const bool diag = P == Q;
+            for (int ii = 0; ii < nI; ++ii)
+                for (int jj = diag ? ii : 0; jj < nJ; ++jj, ++tt) {
+                    const int s = tt % kSyStages, acc = tt % kSyAcc;
+                    const bool off = !(diag && ii == jj);
+                    const bool tlt = sa.tlog && blockIdx.x == 0 && tt < 128 && lane == 0;
+                    if (tt >= kSyAcc) mbar_wait(&tm_empty[acc], ((tt / kSyAcc) - 1) & 1);
+                    if (tlt) sa.tlog[(kTlTile + tt) * 4 + 0] = sy_gtime();
+                    mbar_wait(&full[s], (tt / kSyStages) & 1);
+                    if (tlt) sa.tlog[(kTlTile + tt) * 4 + 1] = sy_gtime();
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t aHi = smem0 + s * kStage, aLo = aHi + kSyPlaneBytes;
+                    const uint32_t bJ = aHi + 2 * kSyPlaneBytes, bI = bJ + kBB;
+                    const uint32_t d1 = tmem_u + acc * 4 * NR, d2 = d1 + 2 * NR;
+                    // descriptors of k-step 0; a k-step only moves the 14-bit start
+                    // address field (>> 4), which cannot carry out (smem < 256 KB)
+                    const uint64_t dA1h = umma_desc(aHi, kstr, 128), dA1l = umma_desc(aLo, kstr, 128);
+                    const uint64_t dA2h = umma_desc(aHi, 128, kstr), dA2l = umma_desc(aLo, 128, kstr);
+                    const uint64_t dBJ0 = umma_desc(bJ, lboB, 128), dBI0 = umma_desc(bI, lboB, 128);
+                    if (sy_elect_one()) {
 #pragma unroll
                         for (int kb = 0; kb < kSyT / 16; ++kb) {
                             const uint32_t first = kb ? 1u : 0u;
-                            const uint64_t dBJ = umma_desc(bJ + kb * 2 * lboB, lboB, 128);
-                            sy_mma(d1, umma_desc(aHi + kb * 2 * kstr, kstr, 128), dBJ, id_cat, first);
-                            sy_mma(d1, umma_desc(aLo + kb * 2 * kstr, kstr, 128), dBJ, id_hi, 1u);
+                            const uint64_t dBJ = dBJ0 + (uint64_t)(kb * 2 * lboB >> 4);
+                            sy_mma(d1, dA1h + (uint64_t)(kb * 2 * kstr >> 4), dBJ, id_cat, first);
+                            sy_mma(d1, dA1l + (uint64_t)(kb * 2 * kstr >> 4), dBJ, id_hi, 1u);
                             if (off) {  // transposed view: K' = tile rows, 16 per k-step = 256 B
-                                const uint64_t dBI = umma_desc(bI + kb * 2 * lboB, lboB, 128);
-                                sy_mma(d2, umma_desc(aHi + kb * 256, 128, kstr), dBI, id_catT, first);
-                                sy_mma(d2, umma_desc(aLo + kb * 256, 128, kstr), dBI, id_hiT, 1u);
+                                const uint64_t dBI = dBI0 + (uint64_t)(kb * 2 * lboB >> 4);
+                                sy_mma(d2, dA2h + (uint64_t)(kb * 256 >> 4), dBI, id_catT, first);
+                                sy_mma(d2, dA2l + (uint64_t)(kb * 256 >> 4), dBI, id_hiT, 1u);
                             }
                         }
                         tc_commit(&empty[s]);
                         tc_commit(&tm_full[acc]);
                     }
-            }
+                    __syncwarp();
+                    if (tlt) sa.tlog[(kTlTile + tt) * 4 + 2] = sy_gtime();
+                }
         }
     } else {
         // ------------------------------------------------ tile epilogue
@@ -440,6 +526,8 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
                     const bool off = I != J;
                     const int acc = tt % kSyAcc;
                     mbar_wait(&tm_full[acc], (tt / kSyAcc) & 1);
+                    const bool tle = sa.tlog && blockIdx.x == 0 && tt < 128 && row == 0;
+                    if (tle) sa.tlog[(kTlTile + 128 + tt) * 4 + 0] = sy_gtime();
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     float g1[NR], g2[NR];
                     const uint32_t tq = tmem + acc * 4 * NR + ((uint32_t)(ew * 32) << 16);
@@ -448,6 +536,7 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tm_empty[acc]);
+                    if (tle) sa.tlog[(kTlTile + 128 + tt) * 4 + 1] = sy_gtime();
                     if (m.diag) {  // both uses land in the item's own blocks
 #pragma unroll
                         for (int q = 0; q < NR; ++q)
@@ -472,6 +561,7 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
             if (!m.diag)
                 for (int jj = 0; jj < m.nJ; ++jj) put_cs(m.b, m.J0 + jj, m.P, jj);
         }
+        if (sa.tlog && row == 0) sa.tlog[blockIdx.x * 4 + 2] = sy_gtime();
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -537,7 +627,7 @@ __device__ __forceinline__ void sy_st4(double* p, const double (&v)[4]) {
 // instantiation gives an fp64-state variant) and, in step / Jacobi modes, emits the fp16
 // B tile of the new w (staged in shared memory, stored with 16-byte vectors).
 template <int NR, int MODE, typename TS = float>
-__global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_update_kernel(SymArgs sa) {
+__global__ void __launch_bounds__(kSyT * NR / 4, SY_UPD_OCC) sym_update_kernel(SymArgs sa) {
     constexpr int QG = NR / 4;
     constexpr int NW = kSyT * QG / 32;         // warps per CTA
     __shared__ unsigned s_max[NW][NR];          // per warp, per replica max |w|
@@ -561,7 +651,10 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
     const int i = K * kSyT + row, q0 = 4 * g;
     const bool valid = i < N;
     const size_t si = (size_t)b * a.ldN + i, vi0 = si * NR + q0;
+    unsigned long long* tl = sa.tlog && t == 0 ? sa.tlog + (kTlUpd + (size_t)b * nRB + K) * 4 : nullptr;
+    if (tl) tl[0] = sy_gtime();
     sy_pdl_wait();  // the tile kernel's partial products
+    if (tl) tl[1] = sy_gtime();
     // state of the step modes first: its loads are in flight with the slot loads
     TS Rv[4] = {TS(0), TS(0), TS(0), TS(0)}, cv[4] = {TS(0), TS(0), TS(0), TS(0)};
     TS ev[4] = {TS(0), TS(0), TS(0), TS(0)};
@@ -798,6 +891,7 @@ __global__ void __launch_bounds__(kSyT * NR / 4, 1024 / (kSyT * NR / 4)) sym_upd
         for (int o = t; o < 2 * NR * kSyT / 8; o += kSyT * QG) dst[o] = srcB[o];
     }
     sy_pdl_trigger();  // late: the next tile kernel only overlaps the last CTAs
+    if (tl) tl[2] = sy_gtime();
 }
 
 }  // namespace cimcs
