@@ -70,9 +70,13 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+READ_PEAK_PROBE_GBS = 7230.0  # profiles/r02_bulk_probe.json (chunk 65536, 148 CTAs, 128 KB in flight)
+
+
 def ncu_traffic():
-    """Per-launch DRAM traffic of the step kernel from the committed ncu capture."""
-    p = os.path.join(ROOT, "profiles", "ncu_step_summary.json")
+    """Per-launch DRAM traffic of the dominant (tile) kernel from the committed ncu
+    --set full capture of the current kernel (profiles/r02e_ncu_sym_step.json)."""
+    p = os.path.join(ROOT, "profiles", "r02e_ncu_sym_step.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
@@ -579,7 +583,13 @@ def measure(args, dtype, insts, R, hp, ws, rank, local, dist, tile_sharded=False
                 dom = {"kernel": f"sym_step_kernel<{nr},BN>", "bound": "hbm",
                        "avg_us": t_tile * 1e6, "launches": int(tk["tile_kernel_launches"]),
                        "bytes_per_launch": step_bytes, "achieved": step_bytes / t_tile / 1e9,
-                       "peak": peak, "unit": "GB/s", "frac": step_bytes / t_tile / 1e9 / peak}
+                       "peak": peak, "unit": "GB/s", "frac": step_bytes / t_tile / 1e9 / peak,
+                       # the driver's copy figure (read + write) understates what a pure
+                       # read stream reaches: tools/bulk_probe.cu measured 7.23 TB/s for
+                       # cp.async.bulk reads with 148 CTAs x 128 KB in flight
+                       "read_peak_probe": {"gbs": READ_PEAK_PROBE_GBS,
+                                           "frac": step_bytes / t_tile / 1e9 / READ_PEAK_PROBE_GBS,
+                                           "source": "profiles/r02_bulk_probe.json"}}
             dom.update({"share_of_step": t_tile / step_s,
                         "how": ("eager run of 2 x 100 steps after the timed region, CUDA events "
                                 "on the launch stream around each launch (serialised: the "

@@ -284,9 +284,9 @@ int cimcs_get_timing(const cimcs_ctx* ctx, cimcs_timing* out);
 /* Measurement aid with no reference counterpart (option "timeline" = 1 first): the
  * %globaltimer stamps (ns) of the LAST symmetric tile / update launch pair, 4 per CTA --
  * tile CTA x at out[4x..] = (entry, past the PDL wait, last item stored, 0), update
- * CTA (row block K, instance b) at out[4 (256 + b nRB + K)..] = (entry, past the PDL
- * wait, exit, 0); tile CTA 0's per-tile stamps at out[4 (4096 + t)..] and out[4 (4224 + t)..]
- * (csrc/sym_kernels.cuh).  *n = the number of values written (<= cap). */
+ * CTA x of instance b at out[4 (256 + b gridDim.x + x)..] = (entry, past the PDL wait /
+ * item flags, exit, 0); tile CTA 0's per-tile stamps at out[4 (8192 + t)..] and
+ * out[4 (8320 + t)..] (csrc/sym_kernels.cuh).  *n = the number of values written (<= cap). */
 int cimcs_get_timeline(cimcs_ctx* ctx, uint64_t* out, int64_t cap, int64_t* n);
 
 #ifdef __cplusplus

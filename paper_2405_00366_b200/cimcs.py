@@ -462,8 +462,9 @@ class Context:
 
     def timeline(self) -> np.ndarray:
         """%globaltimer stamps [CTA][4] of the last tile / update launch pair (option
-        "timeline" = 1; rows 0..255 tile CTAs, rows 256.. update CTAs b * nRB + K)."""
-        out = np.zeros((256 + 8192, 4), np.uint64)
+        "timeline" = 1; rows 0..255 tile CTAs, rows 256..8191 update CTAs b * gridDim.x + x,
+        rows 8192.. tile CTA 0's per-tile stamps)."""
+        out = np.zeros((8192 + 256, 4), np.uint64)
         n = C.c_int64(0)
         _check(self._lib.cimcs_get_timeline(self._ctx, out.ctypes.data, out.size, C.byref(n)))
         return out

@@ -176,6 +176,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// one lane of the (converged) warp
+__device__ __forceinline__ bool elect_one_sync() {
+    uint32_t pred;
+    asm volatile(
+        "{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
     asm volatile(
@@ -330,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<T>::kMinBlocks) gemv_fused_kerne
             const int nj = min(kChunk, N - j0);
             const int njw = min(kChunk, ldN - j0);  // W rows (zero padded to ldN)
             const uint32_t wbytes = (uint32_t)njw * NR * sizeof(T);
-            if (lane == 0) {
+            if (elect_one_sync()) {  // (not `lane == 0`: ptxas then loops per bulk copy)
                 mbar_arrive_expect_tx(&full[s], nj * row_bytes + wbytes);
                 bulk_g2s(stageG(s), Pb + (size_t)j0 * RB, nj * row_bytes, &full[s]);
                 bulk_g2s(stageW(s), Wb + (size_t)j0 * NR, wbytes, &full[s]);

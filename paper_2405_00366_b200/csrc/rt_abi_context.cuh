@@ -123,6 +123,10 @@ int cimcs_set_option(cimcs_ctx* c, const char* key, int64_t v) {
         if (c->B > 0) return fail(CIMCS_CONFIG_ERROR, "set sched_ctas before set_problems");
         c->sched_ctas = (int)std::max<int64_t>(0, v);
     }
+    else if (k == "overlap_update") {
+        c->overlap_upd = v != 0;
+        drop_graphs(c);
+    }
     else if (k == "cluster_loop") {
         c->use_cluster = v != 0;
         drop_graphs(c);

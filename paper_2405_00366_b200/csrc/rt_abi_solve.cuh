@@ -218,6 +218,7 @@ int cimcs_cdp_minimize(cimcs_ctx* c, int32_t R, const int32_t* sigma, const doub
             for (int q = 0; q < R; ++q)
                 iterations[b * R + q] =
                     method == CIMCS_CDP_CG ? st[b * c->NR + q].it : hp->jacobi_iters;
+    if (err == -2) return fail(CIMCS_CUDA_ERROR, "update kernel: item flags timed out");
     if (method == CIMCS_CDP_JACOBI && err != 0x7f7f7f7f && err != INT_MAX)
         return fail(CIMCS_INPUT_ERROR,
                     "jacobi_solve: singular diagonal at active index " + std::to_string(err));
@@ -497,6 +498,7 @@ int cimcs_solve(cimcs_ctx* c, int32_t R, int32_t backend, const cimcs_hyper* hp,
     CK(cudaStreamSynchronize(c->stream));
     int err = 0;
     if (int rc_ = copy_sync(c, &err, c->err, 4, cudaMemcpyDeviceToHost)) return rc_;
+    if (err == -2) return fail(CIMCS_CUDA_ERROR, "update kernel: item flags timed out");
     if (err != 0x7f7f7f7f && err != INT_MAX)
         return fail(CIMCS_INPUT_ERROR,
                     "jacobi_solve: singular diagonal at active index " + std::to_string(err));

@@ -70,6 +70,8 @@ struct cimcs_ctx {
     int* dSg = nullptr;    // per-instance gram scale exponent
     float* dSpart = nullptr;  // partial products [B][nRB][nSB][128][NR]
     bool use_pdl = true;      // programmatic dependent launch between the step kernels
+    bool overlap_upd = true;  // fp64 DMMA path: item flags, an instance's update runs under the tile kernel
+    unsigned* dDone = nullptr;  // [2][B] item / update-CTA counters of the flags
     unsigned long long* dTl = nullptr;  // option "timeline": per-CTA %globaltimer stamps
     int gram_l2 = 0;          // per instance, the first gram_l2 tiles of the triangle are copied
                               // with evict_last (an L2-resident subset), the rest evict_first

@@ -104,7 +104,7 @@ int launch_sym_t(cimcs_ctx* c, const GemvArgs& g, int b0, int nb) {
     sa.gram_keep = c->gram_l2;
     sa.S = c->symS;
     sa.rowmap = c->cmp_active ? c->cU : nullptr;
-    sa.tlog = c->dTl && (size_t)c->B * c->nRB <= (size_t)(kTlCap - kTlUpd) ? c->dTl : nullptr;
+    sa.tlog = c->dTl && (size_t)c->B * c->nRB <= (size_t)(kTlTile - kTlUpd) ? c->dTl : nullptr;
     if (nb == 0 || c->ntri == 0) return 0;
     const cimcs_ctx::SymSched* ss = nullptr;
     if (int rc = sym_schedule(c, nb, &ss)) return rc;
@@ -203,6 +203,12 @@ int launch_sym64_t(cimcs_ctx* c, const GemvArgs& g) {
     sa.nSB = c->nSB6;
     sa.seg = c->cmp_active ? c->cSeg : nullptr;  // compacted refit: variable segments
     sa.rowmap = c->cmp_active ? c->cU6 : nullptr;
+    sa.tlog = c->dTl && (size_t)2 * c->B * c->nRB6 <= (size_t)(kTlTile - kTlUpd) ? c->dTl : nullptr;
+    if (c->overlap_upd && c->dDone) {  // item flags (sym64_kernels.cuh)
+        sa.done = c->dDone;
+        sa.taken = c->dDone + c->B;
+        sa.ipi = (unsigned)(c->nSB6 * (c->nSB6 + 1) / 2);
+    }
     const cimcs_ctx::SymSched* ss = nullptr;
     if (int rc = sym_schedule(c, c->B, &ss, true)) return rc;
     sa.items = ss->items;
@@ -212,6 +218,15 @@ int launch_sym64_t(cimcs_ctx* c, const GemvArgs& g) {
     static std::atomic<unsigned long long> attr{0};
     if (!(attr.load() >> c->device & 1ull)) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        // Both kernels ask for the largest shared-memory carveout (228 KB), not the smallest
+        // that fits (an SM runs CTAs of one L1 / shared split at a time): with the defaults no
+        // update CTA became resident before its SM's tile CTA had exited (timeline, DESIGN 4).
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                (int)cudaSharedmemCarveoutMaxShared));
+        constexpr int kRowsU = (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) && NR == 16 ? kT6 / 2 : kT6;
+        CK(cudaFuncSetAttribute((sym64_update_kernel<NR, MODE, kRowsU>),
+                                cudaFuncAttributePreferredSharedMemoryCarveout,
+                                (int)cudaSharedmemCarveoutMaxShared));
         attr.fetch_or(1ull << c->device);
     }
     cudaLaunchAttribute at[1];
@@ -244,10 +259,12 @@ int launch_sym64_t(cimcs_ctx* c, const GemvArgs& g) {
         c->timing.tile_kernel_ms += ms;
         c->timing.tile_kernel_launches += 1;
     }
-    cfg.gridDim = dim3(c->nRB6, c->B);
-    cfg.blockDim = dim3(kT6 * NR / 4);
+    // step modes: 32-row CTAs (4 warps), the size that fits beside a resident tile CTA
+    constexpr int kRows = (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) && NR == 16 ? kT6 / 2 : kT6;
+    cfg.gridDim = dim3(c->nRB6 * (kT6 / kRows), c->B);
+    cfg.blockDim = dim3(kRows * NR / 4);
     cfg.dynamicSmemBytes = 0;
-    CK(cudaLaunchKernelEx(&cfg, sym64_update_kernel<NR, MODE>, sa));
+    CK(cudaLaunchKernelEx(&cfg, (sym64_update_kernel<NR, MODE, kRows>), sa));
     return 0;
 }
 

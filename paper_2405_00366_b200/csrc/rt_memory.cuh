@@ -31,6 +31,8 @@ void free_state(cimcs_ctx* c) {
     c->WB0 = c->WB1 = nullptr;
     c->WS0 = c->WS1 = nullptr;
     c->WT0 = c->WT1 = c->dPart6 = nullptr;
+    if (c->dDone) cudaFree(c->dDone);
+    c->dDone = nullptr;
     for (void* q : {(void*)c->cU, (void*)c->cCnt, (void*)c->cMax, (void*)c->Rc, (void*)c->Dc,
                     (void*)c->hzc, (void*)c->sigc, (void*)c->cU6, (void*)c->cSegc,
                     (void*)c->cPfx, (void*)c->cSegOff, (void*)c->cSeg, (void*)c->Rc6,
@@ -180,6 +182,10 @@ int lpt_place(std::vector<std::pair<int, int2>>& items, int nsm, std::vector<int
     flat.clear();
     beg.assign(grid + 1, 0);
     for (int g = 0; g < grid; ++g) {
+        // a CTA walks its items in instance order, so instance b's last item (and with the
+        // fp64 path's item flags its update) finishes about b / B into the launch
+        std::stable_sort(per[g].begin(), per[g].end(),
+                         [](const int2& x, const int2& y) { return x.x < y.x; });
         beg[g] = (int)flat.size();
         flat.insert(flat.end(), per[g].begin(), per[g].end());
     }
@@ -262,6 +268,7 @@ int ensure_state(cimcs_ctx* c, int NR) {
         (rc = dalloc(c, &c->rmse, nT * 8)) || (rc = dalloc(c, &c->ham, nT * 8)) ||
         (rc = dalloc(c, &c->tp, (size_t)nT * 5 * 8)) || (rc = dalloc(c, &c->fail_tmp, nT * 4)))
         return rc;
+    if (c->sym64 && (rc = dalloc(c, &c->dDone, (size_t)2 * c->B * 4))) return rc;
     if (c->mri) {  // G w of the transform chain, one slot: [N][NR]
         const size_t ne = (size_t)c->nRB * kSyT * NR;
         if (c->spart_elems < ne) {

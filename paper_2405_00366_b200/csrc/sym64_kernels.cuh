@@ -78,7 +78,47 @@ struct Sym64Args {
     int keep_w;            // step modes: also store the plain [b][i][r] w
     const int2* seg;       // compacted refit: per segment (first block, blocks), or null
     const int* rowmap;     // compacted refit: row -> original spin (error reports), or null
+    // Item flags (null: the update kernel waits for the whole tile grid).  The tile
+    // kernel is bound by the DMMA pipe and leaves HBM and the other pipes idle, so the
+    // update CTAs of instance b run under it as soon as b's `ipi` items are published:
+    // done[b] counts published items, taken[b] the update CTAs that saw it complete.
+    unsigned* done;
+    unsigned* taken;
+    unsigned ipi;
+    unsigned long long* tlog;  // option "timeline": per-CTA stamps (rows as in sym_kernels.cuh)
 };
+
+// The tile kernel's consumers of an item fence their partial-product stores and meet
+// on the item's last barrier; one thread publishes (s6_item_done).  An update CTA of
+// instance b waits for all `ipi` items of b (s6_wait_items); the last of the
+// instance's `nblk` update CTAs to pass zeroes both counters, and the next tile
+// kernel publishes nothing before that update grid has completed (its threads
+// trigger their dependents only after their own griddepcontrol.wait, so the next
+// update grid cannot even become resident earlier).  The wait is bounded: on expiry
+// the CTA reports through *err (-2) instead of hanging the GPU.
+__device__ __forceinline__ void s6_item_done(unsigned* done, int b) {
+    __threadfence();
+    atomicAdd(done + b, 1u);
+}
+__device__ __forceinline__ void s6_wait_items(unsigned* done, unsigned* taken, int b, unsigned ipi,
+                                              unsigned nblk, int* err) {
+    unsigned v;
+    const long long t0 = clock64();
+    for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done + b) : "memory");
+        if (v >= ipi) break;
+        __nanosleep(256);
+        if (clock64() - t0 > (1ll << 32)) {
+            if (err) atomicMin(err, -2);
+            break;
+        }
+    }
+    if (atomicAdd(taken + b, 1u) == nblk - 1) {
+        taken[b] = 0;
+        done[b] = 0;
+        __threadfence();
+    }
+}
 
 template <int NR>
 __host__ __device__ constexpr size_t s6_wbytes() { return (size_t)kT6 * NR * 8; }
@@ -213,8 +253,12 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) sym64_step_kernel(Sym64Args 
     // writes wait for the previous update kernel (the gram is never written
     // inside a CIM call, so the first stages' gram copies may start earlier)
     constexpr bool kEarly = MODE == EPI_STEP_BN || MODE == EPI_STEP_CN;
-    sy_pdl_trigger();
-    if (!kEarly || warp != kT6Compute) sy_pdl_wait();
+    if (sa.tlog && threadIdx.x == 0) sa.tlog[blockIdx.x * 4 + 0] = sy_gtime();
+    if (!sa.done) sy_pdl_trigger();
+    if (!kEarly || warp != kT6Compute) {
+        sy_pdl_wait();
+        if (sa.done) sy_pdl_trigger();  // item flags: only after the previous update grid
+    }
 
     auto item = [&](int k, int& b, int& P, int& Q, int& nI, int& nJ) {
         const int2 it = sa.items[k];
@@ -269,7 +313,10 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) sym64_step_kernel(Sym64Args 
                 for (int jj = P == Q ? ii : 0; jj < nJ && tt < kT6Stages; ++jj, ++tt)
                     g_part(tt, b, bP + ii, bQ + jj);
         }
-        if (kEarly) sy_pdl_wait();
+        if (kEarly) {
+            sy_pdl_wait();
+            if (sa.done) sy_pdl_trigger();
+        }
         tt = 0;
         for (int k = k0; k < k1; ++k) {
             int b, P, Q, nI, nJ;
@@ -360,8 +407,11 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) sym64_step_kernel(Sym64Args 
                 }
             }
         }
+        if (sa.done) __threadfence();  // this thread's partial products, before the barrier
         s6_bar<NC>(1);  // accumulators free for the next item
+        if (sa.done && threadIdx.x == 0) s6_item_done(sa.done, b);
     }
+    if (sa.tlog && threadIdx.x == 0) sa.tlog[blockIdx.x * 4 + 2] = sy_gtime();
 }
 
 // w tiles [nRB][64][NR] from a plain [b][i][r] W (after init / support / mask / CG)
@@ -381,10 +431,16 @@ __global__ void sym64_wconvert_kernel(const double* __restrict__ W, int N, int l
 // ((0 + P_0) + P_1 + ...), runs the fused fp64 update (the arithmetic of
 // gemv_fused_kernel<double>'s epilogue: bitwise the oracle's) and emits the w
 // tile of the new w.
-template <int NR, int MODE>
-__global__ void __launch_bounds__(kT6 * NR / 4) sym64_update_kernel(Sym64Args sa) {
+// ROWS = rows per CTA: 64 (a whole block), or 32 in the step modes -- a 4-warp CTA
+// of 80 registers is what fits beside a resident tile CTA (its 9 warps x 144 registers
+// leave 2560 registers on the SM sub-partition that holds three of them: one warp),
+// and the step modes reduce across rows only through an atomicMin.
+template <int NR, int MODE, int ROWS = kT6>
+__global__ void __maxnreg__(80) sym64_update_kernel(Sym64Args sa) {
     constexpr int QG = NR / 4;
-    constexpr int NW = kT6 * QG / 32;
+    constexpr int NW = (ROWS * QG + 31) / 32;
+    constexpr int SPLIT = kT6 / ROWS;  // CTAs per 64-row block
+    static_assert(ROWS == kT6 || MODE == EPI_STEP_BN || MODE == EPI_STEP_CN, "half blocks: step modes");
     __shared__ double s_min[NW][NR];
     __shared__ double s_sc[NW][NR][3];
     const TcArgs& a = sa.t;
@@ -397,13 +453,22 @@ __global__ void __launch_bounds__(kT6 * NR / 4) sym64_update_kernel(Sym64Args sa
     double* __restrict__ Cp = static_cast<double*>(a.C);
     double* __restrict__ Ep = static_cast<double*>(a.E);
     double* __restrict__ Hd = static_cast<double*>(a.Hdbg);
-    const int K = blockIdx.x, b = blockIdx.y, nRB = a.nRB, N = a.N;
-    const int t = threadIdx.x, g = t % QG, row = t / QG;
+    const int K = blockIdx.x / SPLIT, b = blockIdx.y, nRB = a.nRB, N = a.N;
+    const int t = threadIdx.x, g = t % QG, row = (blockIdx.x % SPLIT) * ROWS + t / QG;
     const int lane = t & 31, wid = t >> 5;
     const int i = K * kT6 + row, q0 = 4 * g;
     const bool valid = i < N;
     const size_t si = (size_t)b * a.ldN + i, vi0 = si * NR + q0;
-    sy_pdl_wait();
+    unsigned long long* tl =
+        sa.tlog && t == 0 ? sa.tlog + (kTlUpd + (size_t)b * gridDim.x + blockIdx.x) * 4 : nullptr;
+    if (tl) tl[0] = sy_gtime();
+    if (sa.done) {  // this instance's items only: the tile grid may still be running
+        if (t == 0) s6_wait_items(sa.done, sa.taken, b, sa.ipi, gridDim.x, a.err);
+        __syncthreads();
+    } else {
+        sy_pdl_wait();
+    }
+    if (tl) tl[1] = sy_gtime();
     double Rv[4] = {0, 0, 0, 0}, cv[4] = {0, 0, 0, 0}, ev[4] = {0, 0, 0, 0};
     double st_D = 0.0, st_hz = 0.0;
     if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
@@ -590,6 +655,7 @@ __global__ void __launch_bounds__(kT6 * NR / 4) sym64_update_kernel(Sym64Args sa
         sy_st4(wt + s6_wofs<NR>(row, q0), wn);
     }
     sy_pdl_trigger();
+    if (tl) tl[2] = sy_gtime();
 }
 
 }  // namespace cimcs

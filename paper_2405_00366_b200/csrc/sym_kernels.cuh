@@ -134,14 +134,7 @@ __device__ __forceinline__ void sy_mma(uint32_t d, uint64_t da, uint64_t db, uin
         "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
-// one lane of the (converged) warp
-__device__ __forceinline__ bool sy_elect_one() {
-    uint32_t pred;
-    asm volatile(
-        "{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(pred));
-    return pred != 0;
-}
+__device__ __forceinline__ bool sy_elect_one() { return elect_one_sync(); }
 __device__ __forceinline__ uint64_t sy_policy_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -211,7 +204,7 @@ struct SymArgs {
 // per-tile stamps of tile CTA 0 at [kTlTile + tt] = (MMA thread: accumulator free, tile
 // landed, MMAs issued; producer: refill of the tile's stage issued) and [kTlTile + 128 +
 // tt] = (epilogue warp 2: accumulator complete, accumulator read + released, -, -)
-constexpr int kTlUpd = 256, kTlTile = 4096, kTlCap = kTlUpd + 8192;
+constexpr int kTlUpd = 256, kTlTile = 8192, kTlCap = kTlTile + 256;
 __device__ __forceinline__ unsigned long long sy_gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

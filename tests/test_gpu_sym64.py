@@ -222,3 +222,35 @@ def test_divergence_on_sym64_path(gpu, O):
         O.MFZ_BN, O.HyperParams(velo=2, dt=5.0, n_steps=50), O.Rng(seed))
     assert ref["failed"] and res["fail_alt"][0, 0] == ref["fail_alternation"]
     assert res["fail_index"][0, 0] == ref["fail_index"]
+
+
+@pytest.mark.parametrize("backend", ["mfz-bn", "mfz-cn"])
+def test_item_flags_do_not_change_results(gpu, O, backend):
+    """Item flags (option overlap_update: an instance's update CTAs run under the
+    DMMA tile kernel as soon as its items are published) only change WHEN an update
+    CTA runs: 12 instances x 16 replicas (more items than one wave of update CTAs
+    can hold resident), N = 1100 (3 segments, 6 items per instance), whole solves --
+    R, sigma and the histories are bitwise equal with the flags off and on, and
+    equal to the oracle for one trajectory."""
+    insts = [O.gen_instance(1100, 0.5, 0.1, 0.01, s) for s in range(21, 33)]
+    R = 16
+    be = O.BACKENDS[backend]
+    seeds = np.array([[O.mix_seed(i.seed, be + 3 * r) for r in range(R)] for i in insts],
+                     np.uint64)
+    res = []
+    for ov in (0, 1):
+        ctx = _ctx(gpu, insts, overlap_update=ov)
+        order = ctx.canon_order()
+        res.append(ctx.solve(R, backend, gpu.baseline_params(velo=2, n_steps=150), seeds))
+        ctx.close()
+    assert np.array_equal(res[0]["R"], res[1]["R"])
+    assert np.array_equal(res[0]["sigma"], res[1]["sigma"])
+    assert np.array_equal(res[0]["fail_alt"], res[1]["fail_alt"])
+    for b in range(len(insts)):
+        for r in range(R):
+            for h0, h1 in zip(res[0]["history"][b, r], res[1]["history"][b, r]):
+                assert h0 == h1
+    ref = O.Problem(insts[5], O.CANON, *order).alternating_minimize(
+        be, O.baseline_params(velo=2, n_steps=150), O.Rng(int(seeds[5, 7])))
+    assert np.array_equal(res[1]["R"][5, 7], ref["R"])
+    assert np.array_equal(res[1]["sigma"][5, 7], ref["sigma"])

@@ -21,7 +21,7 @@ def main():
     seeds = P.replica_seeds(insts, R, "mfz-bn")
     out = {}
     for dt in dts:
-        for n in (148, 132, 111, 96, 74):
+        for n in [int(x) for x in os.environ.get("CTAS", "148,132,111,96,74").split(",")]:
             with P.Context(0, dt) as ctx:
                 ctx.set_option("sched_ctas", n)
                 ctx.set_option("kernel_timing", 0)

@@ -15,8 +15,8 @@ def main():
         ctx.build_coupling()
         ctx.build_coupling()
         tl = ctx.timeline().astype(np.int64)
-    a = tl[4096:4096 + 128]
-    e = tl[4096 + 128:4096 + 256]
+    a = tl[8192:8192 + 128]
+    e = tl[8192 + 128:8192 + 256]
     t0 = a[0, 0]
     a = (a - t0) / 1e3
     e = (e - t0) / 1e3

@@ -22,8 +22,8 @@ def main():
         for _ in range(2):
             ctx.run_cim(R, "mfz-bn", hp, 0.5, Rs, c0)
         tl = ctx.timeline().astype(np.int64)
-    a = tl[4096:4096 + 128]
-    e = tl[4096 + 128:4096 + 256]
+    a = tl[8192:8192 + 128]
+    e = tl[8192 + 128:8192 + 256]
     n = int((a[:, 1] > 0).sum())
     t0 = tl[0, 0]
     a = (a[:n] - t0) / 1e3

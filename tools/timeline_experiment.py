@@ -33,18 +33,20 @@ def main():
     c0 = rng.normal(scale=1e-2, size=(B, R, N))
     out = {}
     for dt in dts:
-        for _once in (0,):
+        for ov in ((0, 1) if dt == "f64" else (0,)):  # fp64: item flags off / on
             with P.Context(0, dt) as ctx:
                 ctx.set_option("timeline", 1)
+                if dt == "f64":
+                    ctx.set_option("overlap_update", ov)
                 ctx.set_problems(insts)
                 ctx.build_coupling()
                 for _ in range(2):
                     ctx.run_cim(R, "mfz-bn", hp, 0.5, Rs, c0)
                 tl = ctx.timeline().astype(np.int64)
-            np.savez_compressed(os.path.join(ROOT, "gpurun_out", f"timeline_{dt}.npz"), tl=tl)
+            np.savez_compressed(os.path.join(ROOT, "gpurun_out", f"timeline_{dt}_flags{ov}.npz"), tl=tl)
             tile = tl[:256]
             tile = tile[tile[:, 0] > 0]
-            upd = tl[256:4096]
+            upd = tl[256:8192]
             upd = upd[upd[:, 0] > 0]
             t0 = tile[:, 0].min()
             us = lambda a: (a - t0) / 1e3
@@ -57,8 +59,11 @@ def main():
                 "upd_run_us": q((upd[:, 2] - upd[:, 1]) / 1e3),
                 "upd_exit_after_last_tile_item_us": round(float(us(upd[:, 2]).max() - us(tile[:, 2]).max()), 2),
             }
-            out[dt] = rec
-            print(dt, json.dumps(rec), flush=True)
+            nrb = len(upd) // B
+            fin = us(upd[:, 1]).reshape(B, nrb).min(axis=1)
+            rec["instance_update_start_us_by_b"] = [round(float(v), 1) for v in fin[::4]]
+            out[f"{dt}_flags{ov}"] = rec
+            print(f"{dt}_flags{ov}", json.dumps(rec), flush=True)
     with open(os.path.join(ROOT, "gpurun_out", "timeline_summary.json"), "w") as f:
         json.dump(out, f, indent=1)
 
