@@ -253,3 +253,34 @@ def test_compacted_refit_matches_full_refit(gpu, O):
         for r in range(R):
             assert abs(out[1]["history"][b, r][0]["rmse"] - out[0]["history"][b, r][0]["rmse"]) \
                 <= 1e-4 * out[0]["history"][b, r][0]["rmse"]
+
+
+def test_timeline_stamps(gpu, O):
+    """Option `timeline` (measurement aid, cimcs_get_timeline): after a CIM call every
+    tile CTA and every update CTA of the last launch pair has stamped entry <= past its
+    PDL wait <= exit, the update CTAs exit after the tile CTAs' last items, and tile
+    CTA 0's per-tile stamps are ordered (accumulator free <= landed <= issued)."""
+    N, B, R = 1100, 3, 16
+    insts = [O.gen_instance(N, 0.5, 0.1, 0.01, s) for s in range(41, 41 + B)]
+    ctx = gpu.Context(0, "f32")
+    ctx.set_option("timeline", 1)
+    ctx.set_problems(insts)
+    ctx.build_coupling()
+    rng = np.random.default_rng(3)
+    Rs = np.abs(rng.normal(size=(B, R, N))) * 0.1
+    c0 = rng.normal(scale=1e-2, size=(B, R, N))
+    ctx.run_cim(R, "mfz-bn", gpu.baseline_params(velo=1, n_steps=20), 0.5, Rs, c0)
+    tl = ctx.timeline().astype(np.int64)
+    ctx.close()
+    nRB = -(-N // 128)
+    tile = tl[:256]
+    tile = tile[tile[:, 0] > 0]
+    upd = tl[256:256 + B * nRB]
+    assert len(tile) >= 1 and np.all(upd[:, 0] > 0)
+    assert np.all(tile[:, 0] <= tile[:, 1]) and np.all(tile[:, 1] <= tile[:, 2])
+    assert np.all(upd[:, 0] <= upd[:, 1]) and np.all(upd[:, 1] <= upd[:, 2])
+    assert upd[:, 1].min() >= tile[:, 2].max()  # fp32: the update waits for the whole tile grid
+    per = tl[8192:8192 + 128]
+    n = int((per[:, 1] > 0).sum())
+    assert n >= 1
+    assert np.all(per[:n, 0] <= per[:n, 1]) and np.all(per[:n, 1] <= per[:n, 2])
