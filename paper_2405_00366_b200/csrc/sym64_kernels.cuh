@@ -88,8 +88,9 @@ struct Sym64Args {
     unsigned long long* tlog;  // option "timeline": per-CTA stamps (rows as in sym_kernels.cuh)
 };
 
-// The tile kernel's consumers of an item fence their partial-product stores and meet
-// on the item's last barrier; one thread publishes (s6_item_done).  An update CTA of
+// The tile kernel's consumers of an item meet on the item's last barrier after their
+// partial-product stores; one thread then fences (gpu scope, cumulative) and publishes
+// (s6_item_done).  An update CTA of
 // instance b waits for all `ipi` items of b (s6_wait_items); the last of the
 // instance's `nblk` update CTAs to pass zeroes both counters, and the next tile
 // kernel publishes nothing before that update grid has completed (its threads
@@ -407,8 +408,9 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) sym64_step_kernel(Sym64Args 
                 }
             }
         }
-        if (sa.done) __threadfence();  // this thread's partial products, before the barrier
-        s6_bar<NC>(1);  // accumulators free for the next item
+        s6_bar<NC>(1);  // accumulators free for the next item; every warp's partials are stored
+        // (the barrier orders the other threads' stores before thread 0's cumulative
+        // gpu-scope fence in s6_item_done: the __syncthreads / __threadfence / atomic pattern)
         if (sa.done && threadIdx.x == 0) s6_item_done(sa.done, b);
     }
     if (sa.tlog && threadIdx.x == 0) sa.tlog[blockIdx.x * 4 + 2] = sy_gtime();
