@@ -14,11 +14,6 @@ namespace cimcs {
 
 constexpr int kTcRows = 128;           // M of the MMA, spins per tile
 constexpr int kTcChunk = kTcChunkJ;    // j per pipeline stage
-constexpr int kTcStages = 4;
-constexpr int kTcThreads = 10 * 32;
-constexpr int kTcTileFloats = kTcRows * kTcChunk;  // 8192
-constexpr int kTcLoCol = 64;           // first TMEM column of the G_lo buffers
-constexpr int kTcTmemCols = 256;
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
@@ -28,26 +23,6 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
     return d;                // SWIZZLE_NONE, base offset 0
 }
 
-// F32 accumulate, A/B = TF32, both K-major, N, M = 128
-__host__ __device__ constexpr uint32_t tc_idesc(int n) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) |
-           ((uint32_t)(kTcRows >> 4) << 24);
-}
-
-__device__ __forceinline__ void tc_mma_ss(uint32_t d, uint64_t da, uint64_t db, uint32_t idesc,
-                                          uint32_t acc) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-        "l"(da), "l"(db), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void tc_mma_ts(uint32_t d, uint32_t ta, uint64_t db, uint32_t idesc,
-                                          uint32_t acc) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
-        "r"(ta), "l"(db), "r"(idesc), "r"(acc));
-}
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
     asm volatile(
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -70,14 +45,6 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[16], int 
         : "=r"(r[off + 0]), "=r"(r[off + 1]), "=r"(r[off + 2]), "=r"(r[off + 3]),
           "=r"(r[off + 4]), "=r"(r[off + 5]), "=r"(r[off + 6]), "=r"(r[off + 7])
         : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
-        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
-        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
-        "r"(v[15]));
 }
 
 // accumulator row of this thread: gw[q] = D[q] + D[NR + q]  (hi*W + lo*W  +  hi*W_lo)
