@@ -184,6 +184,10 @@ int enqueue_refit_compact64(cimcs_ctx* c, const StepScalars& s, int iters, bool 
             pfx[(size_t)b * nseg + sg] = a;
             a += segc[(size_t)b * nseg + sg];
         }
+    // Dense unions: every segment's width rounds UP to 64 rows, so the compacted size can
+    // exceed the state's leading dimension ldN = round_up(N, 32) (N = 1100: 512 + 512 + 128
+    // = 1152 > 1120).  Nothing to gain then: the full refit, bitwise the same result.
+    if (Nc > c->ldN) return enqueue_refit(c, s, iters, false);
     if (Nc > 0 && iters > 0) {
         const int nsc = (int)seg.size(), nRBc = Nc / kT6, ntric = nRBc * (nRBc + 1) / 2;
         // the LPT schedule of the variable-width segment items

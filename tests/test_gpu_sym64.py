@@ -231,7 +231,9 @@ def test_item_flags_do_not_change_results(gpu, O, backend):
     CTA runs: 12 instances x 16 replicas (more items than one wave of update CTAs
     can hold resident), N = 1100 (3 segments, 6 items per instance), whole solves --
     R, sigma and the histories are bitwise equal with the flags off and on, and
-    equal to the oracle for one trajectory."""
+    equal to the oracle for one trajectory.  (Also the regression case of the compacted
+    refit's dense-union fallback: with 12 x 16 supports the per-segment widths round up
+    to 512 + 512 + 128 = 1152 rows > ldN = 1120, which used to overrun the state.)"""
     insts = [O.gen_instance(1100, 0.5, 0.1, 0.01, s) for s in range(21, 33)]
     R = 16
     be = O.BACKENDS[backend]
