@@ -38,10 +38,6 @@
 
 #include "sym_kernels.cuh"
 
-#ifndef GT_WAIT
-#define GT_WAIT mbar_wait
-#endif
-
 namespace cimcs {
 
 constexpr int kGtK = 32;                          // k per chunk / pipeline stage
@@ -223,7 +219,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GtArgs a) {
             const unsigned char* srcJ = Pb + (size_t)J * kGtPlane;
             for (int c = 0; c < a.nch; ++c, ++it) {
                 const int s = (int)(it % kGtStages);
-                if (it >= kGtStages) GT_WAIT(&empty[s], (uint32_t)(((it / kGtStages) - 1) & 1));
+                if (it >= kGtStages) mbar_wait(&empty[s], (uint32_t)(((it / kGtStages) - 1) & 1));
                 if (a.tlog && blockIdx.x == 0 && it < 128 && lane == 0)
                     a.tlog[(kTlTile + it) * 4 + 3] = sy_gtime();
                 if (sy_elect_one()) {
@@ -249,9 +245,9 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GtArgs a) {
             for (int c = 0; c < a.nch; ++c, ++it) {
                 const int s = (int)(it % kGtStages), buf = (int)(it & 1);
                 const bool tl = a.tlog && blockIdx.x == 0 && it < 128 && lane == 0;
-                if (it >= 2) GT_WAIT(&tm_empty[buf], (uint32_t)(((it >> 1) - 1) & 1));
+                if (it >= 2) mbar_wait(&tm_empty[buf], (uint32_t)(((it >> 1) - 1) & 1));
                 if (tl) a.tlog[(kTlTile + it) * 4 + 0] = sy_gtime();
-                GT_WAIT(&full[s], (uint32_t)((it / kGtStages) & 1));
+                mbar_wait(&full[s], (uint32_t)((it / kGtStages) & 1));
                 if (tl) a.tlog[(kTlTile + it) * 4 + 1] = sy_gtime();
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t aHi = smem0 + s * kGtStage;
@@ -294,7 +290,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GtArgs a) {
             }
             for (int c = 0; c < a.nch; ++c, ++it) {
                 const int buf = (int)(it & 1);
-                GT_WAIT(&tm_full[buf], (uint32_t)((it >> 1) & 1));
+                mbar_wait(&tm_full[buf], (uint32_t)((it >> 1) & 1));
                 const bool tle = a.tlog && blockIdx.x == 0 && it < 128 && threadIdx.x == 64;
                 if (tle) a.tlog[(kTlTile + 128 + it) * 4 + 0] = sy_gtime();
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
