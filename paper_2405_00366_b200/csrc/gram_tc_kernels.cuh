@@ -29,7 +29,7 @@
 // Persistent CTAs walk the upper-triangle tiles super-block by super-block (kGtSB x
 // kGtSB tiles, about one per wave of 148 CTAs), so the CTAs of a wave share 2 x kGtSB
 // operand blocks in L2 instead of streaming one A_J block each from HBM; warp 0
-// produces (bulk copies into a 4-stage ring), warp 1 issues the MMAs, warps 2-9
+// produces (bulk copies into a 4-stage ring), warps 1 and 10 issue the MMAs (alternate k-chunks), warps 2-9
 // drain TMEM and finally store the fp16 hi/lo SymOut values (G * 2^s_G).  Producer
 // and MMA warps run convergently on warp-uniform operands with one elected lane
 // issuing (see sym_step_kernel: issuing from inside `if (lane == 0)` costs an
@@ -43,7 +43,8 @@ namespace cimcs {
 constexpr int kGtK = 32;                          // k per chunk / pipeline stage
 constexpr int kGtStages = 4;
 constexpr int kGtEpi = 8;                         // epilogue warps (2 per TMEM lane quadrant)
-constexpr int kGtThreads = (2 + kGtEpi) * 32;
+constexpr int kGtMma2 = 2 + kGtEpi;                // second MMA issuer warp (odd chunks)
+constexpr int kGtThreads = (3 + kGtEpi) * 32;
 constexpr int kGtInner = 16;                      // chunks per first-level sum
 constexpr uint32_t kGtPlane = kSyT * kGtK * 2;    // 8 KB: one plane of one 128-column block
 constexpr uint32_t kGtStage = 4 * kGtPlane;       // A_I hi, lo; A_J hi, lo
@@ -236,7 +237,13 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GtArgs a) {
             }
             if (lane == 0) atomicAdd(a.round, 1u);
         }
-    } else if (warp == 1) {  // ------------------------------------------ MMA issuer
+    } else if (warp == 1 || warp == kGtMma2) {  // ------------------------ MMA issuers
+        // Two issuer warps take alternate k-chunks (each owns one TMEM accumulator): the
+        // ~0.2 us a warp spends between chunks (barrier waits, fences, descriptors) is
+        // hidden behind the other warp's six MMAs.  The chunks of the two warps touch
+        // different stages and accumulators, so their relative issue order is free; each
+        // warp commits its own MMAs.
+        const int par = warp == 1 ? 0 : 1;
         constexpr uint32_t idesc = sy_idesc(kSyT, 0);  // F32 += F16 x F16, M = N = 128
         const uint32_t smem0 = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
         const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
@@ -244,6 +251,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GtArgs a) {
         for (long long t = blockIdx.x; t < a.ntile; t += gridDim.x) {
             for (int c = 0; c < a.nch; ++c, ++it) {
                 const int s = (int)(it % kGtStages), buf = (int)(it & 1);
+                if (buf != par) continue;
                 const bool tl = a.tlog && blockIdx.x == 0 && it < 128 && lane == 0;
                 if (it >= 2) mbar_wait(&tm_empty[buf], (uint32_t)(((it >> 1) - 1) & 1));
                 if (tl) a.tlog[(kTlTile + it) * 4 + 0] = sy_gtime();
@@ -272,7 +280,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GtArgs a) {
                 if (tl) a.tlog[(kTlTile + it) * 4 + 2] = sy_gtime();
             }
         }
-    } else {  // ----------------------------------------------------- epilogue
+    } else if (warp < kGtMma2) {  // ------------------------------------ epilogue
         const int q = warp & 3;           // TMEM lane quadrant (warps 2..9)
         const int h = (warp - 2) >> 2;    // column half: 64 columns each
         const int row = q * 32 + lane;
