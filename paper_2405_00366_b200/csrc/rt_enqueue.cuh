@@ -196,7 +196,7 @@ int enqueue_refit_compact64(cimcs_ctx* c, const StepScalars& s, int iters, bool 
             for (int P = 0; P < nsc; ++P)
                 for (int Q = P; Q < nsc; ++Q) {
                     const int nI = seg[P].y, nJ = seg[Q].y;
-                    items.push_back({P == Q ? nI * (nI + 1) / 2 : nI * nJ, make_int2(b, P << 16 | Q)});
+                    items.push_back({sym_item_cost(P == Q, nI, nJ), make_int2(b, P << 16 | Q)});
                 }
         if ((int)items.size() > c->cmp_items_cap) return fail(CIMCS_CUDA_ERROR, "cmp64 schedule capacity");
         std::vector<int2> flat;

@@ -193,6 +193,12 @@ int lpt_place(std::vector<std::pair<int, int2>>& items, int nsm, std::vector<int
     return grid;
 }
 
+// LPT weight of an item in half-tiles: a tile on the diagonal (I == J) feeds one product
+// instead of two and costs about half a tile (measured per CTA: 1.47 us per off-diagonal
+// tile, 0.75 per I == J tile on the fp32 path, tools/sm_speed.py; half the DMMAs on the
+// fp64 path), so a diagonal item of n x n blocks weighs n (n + 1) - n = n^2.
+inline int sym_item_cost(bool diag, int nI, int nJ) { return diag ? nI * nI : 2 * nI * nJ; }
+
 int sym_schedule(cimcs_ctx* c, int nb, const cimcs_ctx::SymSched** out, bool s64 = false) {
     if (s64 && c->cmp_active) {  // built per alternation by enqueue_refit_compact64
         *out = &c->cmp_sched;
@@ -211,8 +217,7 @@ int sym_schedule(cimcs_ctx* c, int nb, const cimcs_ctx::SymSched** out, bool s64
         for (int P = P0; P < P1; ++P)
             for (int Q = P; Q < nSB; ++Q) {
                 const int nI = std::min(kS, nRB - P * kS), nJ = std::min(kS, nRB - Q * kS);
-                const int t = P == Q ? nI * (nI + 1) / 2 : nI * nJ;
-                items.push_back({t, make_int2(b, P << 16 | Q)});
+                items.push_back({sym_item_cost(P == Q, nI, nJ), make_int2(b, P << 16 | Q)});
             }
     std::vector<int2> flat;
     std::vector<int> beg;

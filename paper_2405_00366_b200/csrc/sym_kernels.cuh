@@ -197,7 +197,7 @@ struct SymArgs {
     int S;                 // item edge in tiles (kSyS; 2 for the compacted refit)
     const int* rowmap;     // compacted refit: row -> original spin (error reports), or null
     // measurement aid (option "timeline"): %globaltimer stamps of the last launch pair,
-    // 4 per CTA: tile CTA x at [x] = (entry, past the PDL wait, last item stored, -),
+    // 4 per CTA: tile CTA x at [x] = (entry, past the PDL wait, last item stored, SM id << 32 | tiles),
     // update CTA (K, b) at [kTlUpd + b * nRB + K] = (entry, past the PDL wait, exit, -)
     unsigned long long* tlog;
 };
@@ -554,7 +554,12 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
             if (!m.diag)
                 for (int jj = 0; jj < m.nJ; ++jj) put_cs(m.b, m.J0 + jj, m.P, jj);
         }
-        if (sa.tlog && row == 0) sa.tlog[blockIdx.x * 4 + 2] = sy_gtime();
+        if (sa.tlog && row == 0) {
+            sa.tlog[blockIdx.x * 4 + 2] = sy_gtime();
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            sa.tlog[blockIdx.x * 4 + 3] = ((unsigned long long)smid << 32) | (unsigned)tt;  // SM, tiles
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
