@@ -114,6 +114,51 @@ struct GemvArgs {
     StepScalars s;
 };
 
+// Positive-P element update shared by every contraction path (the CUDA-core epilogue and
+// the update kernels of the symmetric-tile paths): pp_step solver_pp.cpp:45-98 with
+// h = (D∘w - G w) + rt*hz (local_field_pp :31-38).  One definition, so every path
+// evaluates the same expressions in the same order (the TU is compiled -fmad=false).
+template <typename T>
+struct PpConsts {
+    T p, dt, rt, tau, nbeta, g2, jj, Kj, m2j, scale, sdt, sjg, thresh, mu_abort, q1;
+    __device__ PpConsts(const StepScalars& sc, const AltParams& alt, double pd)
+        : p((T)pd), dt((T)sc.dt), rt((T)sc.rt), tau((T)sc.tau), nbeta((T)sc.nbeta), g2((T)sc.g2),
+          jj((T)sc.j), Kj((T)sc.Kj), m2j((T)sc.pp_m2j), scale((T)sc.pp_scale), sdt((T)sc.pp_sdt),
+          sjg((T)sc.pp_sjg), thresh((T)alt.thresh_pp), mu_abort((T)sc.mu_abort) {
+        q1 = -((T(1) - p) + jj);  // -(1.0 - p + j)
+    }
+};
+template <typename T>
+struct PpElem {
+    T mu, n, m, e, mt;
+    bool finite;
+};
+template <typename T>
+__device__ __forceinline__ PpElem<T> pp_elem(const PpConsts<T>& c, T w, T Dv, T hzv, T Rv, T gw,
+                                             T mu, T n, T m, T e, T nzk) {
+    const T h = (Dv * w - gw) + c.rt * hzv;
+    const T mu2 = mu * mu;
+    const T mn2 = (m + n) * (m + n);
+    const T inj = (c.Kj * e) * (Rv * h - c.thresh);
+    const T drift = c.q1 * mu - mu * (mu2 + T(2) * c.g2 * n + c.g2 * m) + inj;
+    const T diff = c.sjg * (m + n) * nzk;
+    PpElem<T> o;
+    o.mu = mu + c.dt * drift + c.sdt * diff;
+    o.n = n + c.dt * (c.m2j * n + T(2) * c.p * m - T(2) * mu2 * (T(2) * n + m) - c.jj * mn2);
+    o.m = m + c.dt * (c.m2j * m + T(2) * c.p * n - T(2) * mu2 * (T(2) * m + n) + c.p -
+                      (mu2 + c.g2 * m) - c.jj * mn2);
+    o.mt = mu + c.scale * nzk;
+    o.e = e + c.dt * ((c.nbeta * (o.mt * o.mt - c.tau)) * e);
+    o.finite = isfinite(o.mu) && isfinite(o.n) && isfinite(o.m) && isfinite(o.e);
+    return o;
+}
+// the next contraction input w' = (R*0.5)*(mu~' + rt), mu~' = mu' + scale*w_{k+1}
+template <typename T>
+__device__ __forceinline__ T pp_next_w(const PpConsts<T>& c, T Rv, T mun, T nz_next) {
+    const T mtn = mun + c.scale * nz_next;
+    return (Rv * T(0.5)) * (mtn + c.rt);
+}
+
 // fp32 tensor-core path: a contraction input W is stored as the concatenated
 // UMMA B operand [W | W_lo] (2*NR rows, K-major, canonical no-swizzle layout)
 // where W_lo = W - trunc_tf32(W) is its tf32 residue (see tc_kernels.cuh).
@@ -488,50 +533,33 @@ __global__ void __launch_bounds__(kThreads, Cfg<T>::kMinBlocks) gemv_fused_kerne
         const T* __restrict__ Wp = static_cast<const T*>(a.Win);
         T* __restrict__ Wo = static_cast<T*>(a.Wout);
         const double pd = a.pump ? a.pump[a.step] : a.p_scalar;
-        const T p = (T)pd, dt = (T)sc.dt, rt = (T)sc.rt, tau = (T)sc.tau, nbeta = (T)sc.nbeta;
-        const T g2 = (T)sc.g2, jj = (T)sc.j, Kj = (T)sc.Kj, m2j = (T)sc.pp_m2j;
-        const T scale = (T)sc.pp_scale, sdt = (T)sc.pp_sdt, sjg = (T)sc.pp_sjg;
-        const T thresh = (T)a.alt->thresh_pp, mu_abort = (T)sc.mu_abort;
-        const T q1 = -((T(1) - p) + jj);  // -(1.0 - p + j)
+        const PpConsts<T> pc(sc, *a.alt, pd);
 #pragma unroll
         for (int k = 0; k < OPT; ++k) {
             if (!ok[k]) continue;
             const size_t vi = ((size_t)b * ldN + iv[k]) * NR + q;
             const size_t si = (size_t)b * ldN + iv[k];
-            const T w = Wp[vi], Dv = static_cast<const T*>(a.D)[si];
-            const T hzv = static_cast<const T*>(a.hz)[si], Rv = static_cast<const T*>(a.Rs)[vi];
-            const T h = (Dv * w - gwv[k]) + rt * hzv;
-            const T mu = Mu[vi], n = Np[vi], m = Mp[vi], e = Ep[vi];
-            const T nzk = (T)a.nz[vi];
-            const T mu2 = mu * mu;
-            const T mn2 = (m + n) * (m + n);
-            const T inj = (Kj * e) * (Rv * h - thresh);
-            const T drift = q1 * mu - mu * (mu2 + T(2) * g2 * n + g2 * m) + inj;
-            const T diff = sjg * (m + n) * nzk;
-            const T mun = mu + dt * drift + sdt * diff;
-            const T nn = n + dt * (m2j * n + T(2) * p * m - T(2) * mu2 * (T(2) * n + m) - jj * mn2);
-            const T mm = m + dt * (m2j * m + T(2) * p * n - T(2) * mu2 * (T(2) * m + n) + p -
-                                   (mu2 + g2 * m) - jj * mn2);
-            const T mt = mu + scale * nzk;
-            const T en = e + dt * ((nbeta * (mt * mt - tau)) * e);
+            const T Rv = static_cast<const T*>(a.Rs)[vi];
+            const PpElem<T> o = pp_elem(pc, Wp[vi], static_cast<const T*>(a.D)[si],
+                                        static_cast<const T*>(a.hz)[si], Rv, gwv[k], Mu[vi], Np[vi],
+                                        Mp[vi], Ep[vi], (T)a.nz[vi]);
             const int traj = b * NR + q;
-            if (!finite_(mun) || !finite_(nn) || !finite_(mm) || !finite_(en)) {
+            if (!o.finite) {
                 atomicMin(&a.fail_gstep[traj], a.alt->gstep_base + a.step);
                 atomicMin(&a.fail_idx[traj], iv[k]);  // kind 0: non-finite (pp_step)
                 continue;
             }
-            Mu[vi] = mun;
-            Np[vi] = nn;
-            Mp[vi] = mm;
-            Ep[vi] = en;
-            MTp[vi] = mt;  // the last step's measured amplitude gives sigma (run_pp :128)
-            local_min = en < local_min ? en : local_min;
-            if (fabs((double)mun) > (double)mu_abort) {  // run_pp :119-124, kind 1
+            Mu[vi] = o.mu;
+            Np[vi] = o.n;
+            Mp[vi] = o.m;
+            Ep[vi] = o.e;
+            MTp[vi] = o.mt;  // the last step's measured amplitude gives sigma (run_pp :128)
+            local_min = o.e < local_min ? o.e : local_min;
+            if (fabs((double)o.mu) > (double)pc.mu_abort) {  // run_pp :119-124, kind 1
                 atomicMin(&a.fail_gstep[traj], a.alt->gstep_base + a.step);
                 atomicMin(&a.fail_idx[traj], (1 << 30) + iv[k]);
             }
-            const T mtn = mun + scale * (T)a.nz_next[vi];
-            Wo[vi] = (Rv * T(0.5)) * (mtn + rt);
+            Wo[vi] = pp_next_w(pc, Rv, o.mu, (T)a.nz_next[vi]);
         }
     } else if constexpr (MODE == EPI_JACOBI) {
         // cdp.cpp:60-61: offdiag = G R - D∘R; R = (1-dt_c) R + dt_c (b - offdiag) / D

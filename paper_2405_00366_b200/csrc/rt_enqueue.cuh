@@ -629,14 +629,8 @@ constexpr int kPpChunk = 64;  // steps of unit normals per host -> device chunk
 int ensure_pp(cimcs_ctx* c) {  // outside any capture
     if (c->mri)
         return fail(CIMCS_CONFIG_ERROR, "pp backend: not on matrix-free MRI problems (fp32 MFZ only)");
-    if (c->tc)
-        return fail(CIMCS_CONFIG_ERROR,
-                    "pp backend: use an fp64 context or tensor_cores=0 (the tcgen05 epilogues "
-                    "implement the MFZ update only)");
-    if (c->sym64)
-        return fail(CIMCS_CONFIG_ERROR,
-                    "pp backend: set option sym64=0 before set_problems (the DMMA symmetric "
-                    "path implements the MFZ update only)");
+    if (c->tshard)
+        return fail(CIMCS_CONFIG_ERROR, "pp backend is not supported on tile-sharded contexts");
     if (c->world > 1)
         return fail(CIMCS_CONFIG_ERROR, "pp backend is not supported on row-sharded contexts");
     const size_t n = c->state_elems();
@@ -729,6 +723,7 @@ int run_pp_cim(cimcs_ctx* c, int Rreal, const StepScalars& s, const cimcs_hyper*
     if (!rc)
         rc = c->st64() ? pp_init_T<double>(c, Rreal, c->nzd[0], s)
                                    : pp_init_T<float>(c, Rreal, c->nzd[0], s);
+    if (!rc) rc = sym_sync_w(c, c->W0);  // symmetric-tile paths: the tiles of the first w
     GemvArgs a = base_args(c, s);
     a.pump = c->pump;
     a.Hdbg = nullptr;

@@ -56,6 +56,11 @@ TcArgs tc_args(const cimcs_ctx* c, const GemvArgs& g) {
     a.E = g.E;
     a.Hdbg = g.Hdbg;
     a.Mv = g.Mv;
+    a.Pn = g.Pn;
+    a.Pm = g.Pm;
+    a.MT = g.MT;
+    a.nz = g.nz;
+    a.nz_next = g.nz_next;
     a.sigma = g.sigma;
     a.fail_gstep = g.fail_gstep;
     a.fail_idx = g.fail_idx;
@@ -177,6 +182,7 @@ int launch_sym_grp(cimcs_ctx* c, int mode, const GemvArgs& a, int b0, int nb) {
         case EPI_STEP_CN: return launch_sym_t<NR, EPI_STEP_CN>(c, a, b0, nb);
         case EPI_JACOBI: return launch_sym_t<NR, EPI_JACOBI>(c, a, b0, nb);
         case EPI_MATVEC: return launch_sym_t<NR, EPI_MATVEC>(c, a, b0, nb);
+        case EPI_STEP_PP: return launch_sym_t<NR, EPI_STEP_PP>(c, a, b0, nb);
         default: return launch_sym_t<NR, EPI_SCORE>(c, a, b0, nb);
     }
 }
@@ -275,6 +281,7 @@ int launch_sym64_nc(cimcs_ctx* c, int mode, const GemvArgs& a) {
         case EPI_STEP_CN: return launch_sym64_t<NR, EPI_STEP_CN, NC>(c, a);
         case EPI_JACOBI: return launch_sym64_t<NR, EPI_JACOBI, NC>(c, a);
         case EPI_MATVEC: return launch_sym64_t<NR, EPI_MATVEC, NC>(c, a);
+        case EPI_STEP_PP: return launch_sym64_t<NR, EPI_STEP_PP, NC>(c, a);
         default: return launch_sym64_t<NR, EPI_SCORE, NC>(c, a);
     }
 }

@@ -497,8 +497,9 @@ __global__ void __maxnreg__(80) sym64_update_kernel(Sym64Args sa) {
     const int fga[4] = {fg4.x, fg4.y, fg4.z, fg4.w};
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-        fz[u] = (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) ? fga[u] < a.alt->gstep_base + a.step
-                                                             : fga[u] != kFreeTraj;
+        fz[u] = (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN || MODE == EPI_STEP_PP)
+                    ? fga[u] < a.alt->gstep_base + a.step
+                    : fga[u] != kFreeTraj;
     double wn[4] = {0.0, 0.0, 0.0, 0.0};
     bool emit = false;
     if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
@@ -553,6 +554,74 @@ __global__ void __maxnreg__(80) sym64_update_kernel(Sym64Args sa) {
             sy_st4(Cp + vi0, cn);
             sy_st4(Ep + vi0, en);
             if (sa.keep_w) sy_st4(Wout + vi0, wo);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            double m = lmin[u];
+#pragma unroll
+            for (int off = 16; off >= QG; off >>= 1) {
+                const double o = __shfl_xor_sync(0xffffffffu, m, off);
+                m = o < m ? o : m;
+            }
+            if (lane < QG) s_min[wid][q0 + u] = m;
+        }
+        __syncthreads();
+        if (t < NR) {
+            double mn = INFINITY;
+            for (int w = 0; w < NW; ++w) mn = s_min[w][t] < mn ? s_min[w][t] : mn;
+            if (mn != INFINITY) atomicMin(&a.minE[b * NR + t], ord_key(mn));
+        }
+    } else if constexpr (MODE == EPI_STEP_PP) {
+        // Positive-P step (pp_elem, kernels.cuh): the same element update as the CUDA-core
+        // epilogue on this path's G w; the plain w is read and written as well as its tile
+        emit = true;
+        double lmin[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+        if (valid) {
+            double* __restrict__ Np = static_cast<double*>(a.Pn);
+            double* __restrict__ Mp = static_cast<double*>(a.Pm);
+            double* __restrict__ MTp = static_cast<double*>(a.MT);
+            const double pd = a.pump ? a.pump[a.step] : a.p_scalar;
+            const PpConsts<double> pc(sc, *a.alt, pd);
+            const double Dv = __ldg(Dp + si), hzv = __ldg(Hp + si);
+            double wv[4], Rr[4], mu[4], nn[4], mm[4], ee[4], mt[4] = {0, 0, 0, 0}, z0[4], z1[4];
+            sy_ld4(Win + vi0, wv);
+            sy_ldg4(Rp + vi0, Rr);
+            sy_ld4(Cp + vi0, mu);
+            sy_ld4(Np + vi0, nn);
+            sy_ld4(Mp + vi0, mm);
+            sy_ld4(Ep + vi0, ee);
+            sy_ld4(MTp + vi0, mt);
+            sy_ldg4(a.nz + vi0, z0);
+            sy_ldg4(a.nz_next + vi0, z1);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                wn[u] = wv[u];  // frozen / failing trajectories keep their w
+                if (fz[u]) continue;
+                const PpElem<double> o =
+                    pp_elem(pc, wv[u], Dv, hzv, Rr[u], gw[u], mu[u], nn[u], mm[u], ee[u], z0[u]);
+                if (!o.finite) {
+                    atomicMin(&a.fail_gstep[b * NR + q0 + u], a.alt->gstep_base + a.step);
+                    atomicMin(&a.fail_idx[b * NR + q0 + u], i);  // kind 0: non-finite (pp_step)
+                    continue;
+                }
+                mu[u] = o.mu;
+                nn[u] = o.n;
+                mm[u] = o.m;
+                ee[u] = o.e;
+                mt[u] = o.mt;
+                lmin[u] = o.e;
+                if (fabs(o.mu) > pc.mu_abort) {  // run_pp :119-124, kind 1
+                    atomicMin(&a.fail_gstep[b * NR + q0 + u], a.alt->gstep_base + a.step);
+                    atomicMin(&a.fail_idx[b * NR + q0 + u], (1 << 30) + i);
+                }
+                wn[u] = pp_next_w(pc, Rr[u], o.mu, z1[u]);
+            }
+            sy_st4(Cp + vi0, mu);
+            sy_st4(Np + vi0, nn);
+            sy_st4(Mp + vi0, mm);
+            sy_st4(Ep + vi0, ee);
+            sy_st4(MTp + vi0, mt);
+            sy_st4(Wout + vi0, wn);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {

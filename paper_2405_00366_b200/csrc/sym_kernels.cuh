@@ -699,8 +699,9 @@ __global__ void __launch_bounds__(kSyT * NR / 4, SY_UPD_OCC) sym_update_kernel(S
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const int fg = fga[u];
-        fz[u] = (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) ? fg < a.alt->gstep_base + a.step
-                                                             : fg != kFreeTraj;
+        fz[u] = (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN || MODE == EPI_STEP_PP)
+                    ? fg < a.alt->gstep_base + a.step
+                    : fg != kFreeTraj;
     }
     TS wn[4] = {TS(0), TS(0), TS(0), TS(0)};  // new contraction input (0: frozen / padding)
     if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
@@ -754,6 +755,68 @@ __global__ void __launch_bounds__(kSyT * NR / 4, SY_UPD_OCC) sym_update_kernel(S
             sy_st4(Cp + vi0, cn);
             sy_st4(Ep + vi0, en);
             if (sa.keep_w) sy_st4(Wout + vi0, wo);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // min e: warp, then CTA (one atomic per replica)
+            TS m = lmin[u];
+#pragma unroll
+            for (int off = 16; off >= QG; off >>= 1) {
+                const TS o = __shfl_xor_sync(0xffffffffu, m, off);
+                m = o < m ? o : m;
+            }
+            if (lane < QG) s_min[wid][q0 + u] = m;
+        }
+    } else if constexpr (MODE == EPI_STEP_PP) {
+        // Positive-P step (pp_elem, kernels.cuh): the same element update as the CUDA-core
+        // epilogue on this path's G w; the plain w is read and written as well as its B tile
+        TS lmin[4] = {TS(INFINITY), TS(INFINITY), TS(INFINITY), TS(INFINITY)};
+        if (valid) {
+            TS* __restrict__ Np = static_cast<TS*>(a.Pn);
+            TS* __restrict__ Mp = static_cast<TS*>(a.Pm);
+            TS* __restrict__ MTp = static_cast<TS*>(a.MT);
+            const double pd = a.pump ? a.pump[a.step] : a.p_scalar;
+            const PpConsts<TS> pc(sc, *a.alt, pd);
+            const TS Dv = __ldg(Dp + si), hzv = __ldg(Hp + si);
+            TS wv[4], Rr[4], mu[4], nn[4], mm[4], ee[4], mt[4];
+            double z0[4], z1[4];
+            sy_ld4(Win + vi0, wv);
+            sy_ldg4(Rp + vi0, Rr);
+            sy_ld4(Cp + vi0, mu);
+            sy_ld4(Np + vi0, nn);
+            sy_ld4(Mp + vi0, mm);
+            sy_ld4(Ep + vi0, ee);
+            sy_ld4(MTp + vi0, mt);
+            sy_ldg4(a.nz + vi0, z0);
+            sy_ldg4(a.nz_next + vi0, z1);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                wn[u] = wv[u];  // frozen / failing trajectories keep their w
+                if (fz[u]) continue;
+                const PpElem<TS> o = pp_elem(pc, wv[u], Dv, hzv, Rr[u], gw[u], mu[u], nn[u],
+                                             mm[u], ee[u], (TS)z0[u]);
+                if (!o.finite) {
+                    atomicMin(&a.fail_gstep[b * NR + q0 + u], a.alt->gstep_base + a.step);
+                    atomicMin(&a.fail_idx[b * NR + q0 + u], i);  // kind 0: non-finite (pp_step)
+                    continue;
+                }
+                mu[u] = o.mu;
+                nn[u] = o.n;
+                mm[u] = o.m;
+                ee[u] = o.e;
+                mt[u] = o.mt;
+                lmin[u] = o.e;
+                if (fabs((double)o.mu) > (double)pc.mu_abort) {  // run_pp :119-124, kind 1
+                    atomicMin(&a.fail_gstep[b * NR + q0 + u], a.alt->gstep_base + a.step);
+                    atomicMin(&a.fail_idx[b * NR + q0 + u], (1 << 30) + i);
+                }
+                wn[u] = pp_next_w(pc, Rr[u], o.mu, (TS)z1[u]);
+            }
+            sy_st4(Cp + vi0, mu);
+            sy_st4(Np + vi0, nn);
+            sy_st4(Mp + vi0, mm);
+            sy_st4(Ep + vi0, ee);
+            sy_st4(MTp + vi0, mt);
+            sy_st4(Wout + vi0, wn);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {  // min e: warp, then CTA (one atomic per replica)
@@ -846,7 +909,8 @@ __global__ void __launch_bounds__(kSyT * NR / 4, SY_UPD_OCC) sym_update_kernel(S
             p[2] = C_;
         }
     }
-    if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN || MODE == EPI_JACOBI) {
+    if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN || MODE == EPI_STEP_PP ||
+                  MODE == EPI_JACOBI) {
         // fp16 B tile of the new w of block K: per-replica max over the 128 rows
         // (no tile when the contraction does not read them: transform chains)
         const bool emit = sa.WBout != nullptr;
@@ -859,7 +923,7 @@ __global__ void __launch_bounds__(kSyT * NR / 4, SY_UPD_OCC) sym_update_kernel(S
         }
         __syncthreads();
         if (t < NR) {
-            if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
+            if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN || MODE == EPI_STEP_PP) {
                 TS mn = TS(INFINITY);
                 for (int w = 0; w < NW; ++w) mn = s_min[w][t] < mn ? s_min[w][t] : mn;
                 if (mn != TS(INFINITY)) atomicMin(&a.minE[b * NR + t], ord_key(mn));

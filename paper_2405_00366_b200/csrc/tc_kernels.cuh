@@ -74,6 +74,11 @@ struct TcArgs {
     void* E;
     void* Hdbg;
     double* Mv;            // EPI_MATVEC output [B][ldN][NR]
+    void* Pn;              // Positive-P moments n, m and the measured amplitude [B][ldN][NR]
+    void* Pm;
+    void* MT;
+    const double* nz;      // this step's unit normals [B][ldN][NR] (host stream), the next step's
+    const double* nz_next;
     const int8_t* sigma;   // [B][ldN][NR]
     int* fail_gstep;
     int* fail_idx;
