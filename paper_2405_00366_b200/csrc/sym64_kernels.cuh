@@ -283,8 +283,16 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) sym64_step_kernel(Sym64Args 
         const uint32_t smem0 = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
         const uint32_t full0 = __shfl_sync(0xffffffffu, smem_u32(full), 0);
         const int k0 = __shfl_sync(0xffffffffu, it0, 0), k1 = __shfl_sync(0xffffffffu, it1, 0);
+        // item descriptors one per lane, loaded before the PDL wait (sym_kernels.cuh)
+        const int2 mine = lane < k1 - k0 ? sa.items[k0 + lane] : make_int2(0, 0);
         auto item_u = [&](int k, int& b, int& P, int& Q, int& nI, int& nJ) {
-            const int2 itv = sa.items[k];
+            int2 itv;
+            if (k - k0 < 32) {
+                itv.x = __shfl_sync(0xffffffffu, mine.x, k - k0);
+                itv.y = __shfl_sync(0xffffffffu, mine.y, k - k0);
+            } else {
+                itv = sa.items[k];
+            }
             b = __shfl_sync(0xffffffffu, itv.x, 0);
             const int iy = __shfl_sync(0xffffffffu, itv.y, 0);
             P = iy >> 16;

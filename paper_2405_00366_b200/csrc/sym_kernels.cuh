@@ -356,8 +356,18 @@ __global__ void __launch_bounds__(kSyThreads, 1) sym_step_kernel(SymArgs sa) {
         const uint32_t smem0 = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
         const uint32_t full0 = __shfl_sync(0xffffffffu, smem_u32(full), 0);
         const int k0 = __shfl_sync(0xffffffffu, it0, 0), k1 = __shfl_sync(0xffffffffu, it1, 0);
+        // this CTA's item descriptors, one per lane, loaded BEFORE the PDL wait: right after
+        // it the memory system is busy with the update kernel's write-back and a dependent
+        // global load on the way to the first w copies measured 1 - 2 us
+        const int2 mine = lane < k1 - k0 ? sa.items[k0 + lane] : make_int2(0, 0);
         auto item_u = [&](int k, int& b, int& I0, int& J0, int& nI, int& nJ, bool& diag) {
-            const int2 itv = sa.items[k];
+            int2 itv;
+            if (k - k0 < 32) {
+                itv.x = __shfl_sync(0xffffffffu, mine.x, k - k0);
+                itv.y = __shfl_sync(0xffffffffu, mine.y, k - k0);
+            } else {
+                itv = sa.items[k];
+            }
             b = sa.b0 + __shfl_sync(0xffffffffu, itv.x, 0);
             const int iy = __shfl_sync(0xffffffffu, itv.y, 0);
             const int P = iy >> 16, Q = iy & 0xffff;
