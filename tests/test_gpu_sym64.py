@@ -256,3 +256,35 @@ def test_item_flags_do_not_change_results(gpu, O, backend):
         be, O.baseline_params(velo=2, n_steps=150), O.Rng(int(seeds[5, 7])))
     assert np.array_equal(res[1]["R"][5, 7], ref["R"])
     assert np.array_equal(res[1]["sigma"][5, 7], ref["sigma"])
+
+
+def test_update_runs_under_the_tile_kernel(gpu, O):
+    """The defining property of the item flags, from the per-CTA %globaltimer stamps
+    (option timeline): with the flags on, update CTAs of early instances pass their
+    wait while tile CTAs are still working (48 instances x 16 replicas, N = 1100: 288
+    items on 148 CTAs); with the flags off every update CTA waits for the whole tile
+    grid.  Stamps are ordered entry <= past the wait <= exit either way."""
+    N, B, R = 1100, 48, 16
+    insts = [O.gen_instance(N, 0.5, 0.1, 0.01, 100 + s) for s in range(B)]
+    rng = np.random.default_rng(5)
+    Rs = np.abs(rng.normal(size=(B, R, N))) * 0.1
+    c0 = rng.normal(scale=1e-2, size=(B, R, N))
+    first_pass, last_tile = {}, {}
+    for ov in (0, 1):
+        ctx = gpu.Context(0, "f64")
+        ctx.set_option("timeline", 1)
+        ctx.set_option("overlap_update", ov)
+        ctx.set_problems(insts)
+        ctx.build_coupling()
+        ctx.run_cim(R, "mfz-bn", gpu.baseline_params(velo=1, n_steps=12), 0.5, Rs, c0)
+        tl = ctx.timeline().astype(np.int64)
+        ctx.close()
+        tile = tl[:256]
+        tile = tile[tile[:, 0] > 0]
+        nupd = 2 * B * (-(-N // 64))  # step modes: two 32-row CTAs per 64-row block
+        upd = tl[256:256 + nupd]
+        assert len(tile) == 148 and np.all(upd[:, 0] > 0)
+        assert np.all(upd[:, 0] <= upd[:, 1]) and np.all(upd[:, 1] <= upd[:, 2])
+        first_pass[ov], last_tile[ov] = upd[:, 1].min(), tile[:, 2].max()
+    assert first_pass[0] >= last_tile[0]  # no flags: after the whole tile grid
+    assert first_pass[1] < last_tile[1]   # flags: under the tile kernel
