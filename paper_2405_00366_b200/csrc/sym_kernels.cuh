@@ -687,19 +687,29 @@ __global__ void __launch_bounds__(kSyT * NR / 4, SY_UPD_OCC) sym_update_kernel(S
                             g;
         constexpr size_t kSlot4 = (size_t)kSyT * NR / 4;
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int s0 = 0; s0 < nSB; s0 += 8) {
-            float4 v[8];
+        // groups of 4 slots (config 1 has exactly 4: no predicated-off loads / adds, which
+        // still cost issue slots in this issue-bound kernel); same slot order either way
+        for (int s0 = 0; s0 < nSB; s0 += 4) {
+            float4 v[4];
+            if (s0 + 4 <= nSB) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (s0 + u < nSB) v[u] = __ldcs(src + (s0 + u) * kSlot4);
+                for (int u = 0; u < 4; ++u) v[u] = __ldcs(src + (s0 + u) * kSlot4);
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (s0 + u < nSB) {
+                for (int u = 0; u < 4; ++u) {
                     acc.x = acc.x + v[u].x;
                     acc.y = acc.y + v[u].y;
                     acc.z = acc.z + v[u].z;
                     acc.w = acc.w + v[u].w;
                 }
+            } else {
+                for (int u = 0; s0 + u < nSB; ++u) {
+                    const float4 w1 = __ldcs(src + (s0 + u) * kSlot4);
+                    acc.x = acc.x + w1.x;
+                    acc.y = acc.y + w1.y;
+                    acc.z = acc.z + w1.z;
+                    acc.w = acc.w + w1.w;
+                }
+            }
         }
         gw[0] = (TS)acc.x; gw[1] = (TS)acc.y; gw[2] = (TS)acc.z; gw[3] = (TS)acc.w;
     }
