@@ -83,10 +83,12 @@ def tensor_peak_tf32():
         return 2250.0 / 2  # the profiling recipe's nominal bf16 figure
 
 
-def ncu_traffic():
+def ncu_traffic(dtype="f32"):
     """Per-launch DRAM traffic of the dominant (tile) kernel from the committed ncu
-    --set full capture of the current kernel (profiles/r02e_ncu_sym_step.json)."""
-    p = os.path.join(ROOT, "profiles", "r02e_ncu_sym_step.json")
+    --set full captures (profiles/r02e_ncu_sym_step.json: sym_step_kernel;
+    profiles/r02_ncu_sym64_step.json: sym64_step_kernel)."""
+    p = os.path.join(ROOT, "profiles",
+                     "r02e_ncu_sym_step.json" if dtype == "f32" else "r02_ncu_sym64_step.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
@@ -619,7 +621,7 @@ def measure(args, dtype, insts, R, hp, ws, rank, local, dist, tile_sharded=False
                      {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                       "frac": achieved / peak}),
         "roofline_detail": {
-                     "traffic": ncu_traffic() if Nn == 2000 and dtype == "f32" else None,
+                     "traffic": ncu_traffic(dtype) if Nn == 2000 else None,
                      "kernel": kernel_label(Nn, ctx_nr(R, dtype, Nn), dtype),
                      "bytes_per_launch": step_bytes, "peak_kind": peak_kind,
                      "step_us": step_s * 1e6, "dominant_kernel": dom,
