@@ -621,7 +621,7 @@ def measure(args, dtype, insts, R, hp, ws, rank, local, dist, tile_sharded=False
                      {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                       "frac": achieved / peak}),
         "roofline_detail": {
-                     "traffic": ncu_traffic(dtype) if Nn == 2000 else None,
+                     "traffic": ncu_traffic(dtype) if Nn == 2000 and args.config == 1 else None,
                      "kernel": kernel_label(Nn, ctx_nr(R, dtype, Nn), dtype),
                      "bytes_per_launch": step_bytes, "peak_kind": peak_kind,
                      "step_us": step_s * 1e6, "dominant_kernel": dom,
