@@ -3,6 +3,8 @@ instruction-class counts that prove the Blackwell paths (UTC*MMA = tcgen05.mma,
 LDTM = tcgen05.ld, UBLKCP = cp.async.bulk, DMMA = fp64 mma.sync, SYNCS = mbarrier)
 plus registers / spills.
   python tools/sass_summary.py > profiles/r02_sass_summary.txt
+Also counts BRA.U.ANY: zero means every tcgen05.mma / bulk copy is issued straight from
+uniform registers (no per-instruction ELECT / R2UR / BRA.U.ANY loop).
 """
 import collections
 import os
@@ -45,6 +47,11 @@ def main():
         for m in re.finditer(r"/\*[0-9a-f]{4,}\*/\s+(?:@!?U?P\w+\s+)?([A-Z][A-Z0-9_]*)", f):
             ops[m.group(1)] += 1
         cls = {c: sum(v for k, v in ops.items() if k.startswith(c)) for c in CLASSES}
+        # waterfall loops around uniform-register instructions (an `if (lane == 0)` issue
+        # path makes ptxas emit ELECT / R2UR.BROADCAST / BRA.U.ANY per UTCHMMA / UBLKCP)
+        cls["BRA.U.ANY(waterfall loops)"] = len(re.findall(r"BRA\.U\.ANY", f))
+        cls["ELECT"] = ops.get("ELECT", 0)
+        cls["R2UR"] = ops.get("R2UR", 0)
         demangled = subprocess.run(["c++filt", name], capture_output=True, text=True).stdout.strip()
         print(f"\n{demangled}\n  {usage.get(name, '')}")
         print("  " + "  ".join(f"{c}={n}" for c, n in cls.items() if n))
