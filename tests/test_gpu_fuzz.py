@@ -1,0 +1,22 @@
+"""Randomised shapes (tools/shape_fuzz.py): odd N around the tile and segment edges,
+batches of 1..12, replica counts that pad, MFZ-BN / MFZ-CN / Positive-P, Jacobi and CG
+refits, 2-5 alternations -- fp64 bitwise against the oracle in the context's canonical
+order, fp32 finite on the same problems.  (Two longer runs of 20 + 30 cases are recorded
+in profiles/r02_shape_fuzz.log.)"""
+import importlib.util
+import os
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("seed", [11])
+def test_random_shapes(gpu, O, seed):
+    spec = importlib.util.spec_from_file_location("shape_fuzz",
+                                                  os.path.join(ROOT, "tools", "shape_fuzz.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert mod.run(6, seed, quiet=True) == 0
