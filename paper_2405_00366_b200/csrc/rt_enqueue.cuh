@@ -88,6 +88,11 @@ int enqueue_refit_compact(cimcs_ctx* c, const StepScalars& s, int iters) {
     CK(cudaGetLastError());
     int mx = 0;
     if (int rc = copy_sync(c, &mx, c->cMax, 4, cudaMemcpyDeviceToHost)) return rc;
+    // Dense unions: the compacted problem is padded to 128-row blocks, which can exceed the
+    // state's leading dimension ldN = round_up(N, 32) (N = 577: 5 blocks = 640 > 608; the
+    // union index list and the compacted state are [B][ldN]).  Nothing to gain then: the
+    // full refit.
+    if ((mx + kSyT - 1) / kSyT * kSyT > c->ldN) return enqueue_refit(c, s, iters, false);
     if (mx > 0 && iters > 0) {
         const int nRBc = (mx + kSyT - 1) / kSyT, ntric = nRBc * (nRBc + 1) / 2;
         cmp_gather_tiles_kernel<<<dim3(ntric, c->B), 256, 0, c->stream>>>(

@@ -284,3 +284,24 @@ def test_timeline_stamps(gpu, O):
     n = int((per[:, 1] > 0).sum())
     assert n >= 1
     assert np.all(per[:n, 0] <= per[:n, 1]) and np.all(per[:n, 1] <= per[:n, 2])
+
+
+def test_compacted_refit_dense_unions(gpu, O):
+    """Regression (found by tools/shape_fuzz.py): with dense support unions the compacted
+    problem's 128-row padding exceeds ldN = round_up(N, 32) (N = 577: 5 blocks = 640 > 608)
+    and the union index list was read out of bounds; the refit now falls back to the full
+    sweeps there.  12 instances x 16 replicas, 5 alternations: runs, finite, and close to
+    the uncompacted refit."""
+    N, B, R = 577, 12, 16
+    insts = [O.gen_instance(N, 0.55, 0.25, 0.01, 1000 + s) for s in range(B)]
+    seeds = np.array([[O.mix_seed(i.seed, 1 + 3 * r) for r in range(R)] for i in insts], np.uint64)
+    hp = gpu.baseline_params(velo=4, n_steps=134)
+    res = []
+    for cmp in (1, 0):
+        ctx = _ctx(gpu, insts, refit_compact=cmp)
+        res.append(ctx.solve(R, "mfz-bn", hp, seeds))
+        ctx.close()
+    assert np.all(np.isfinite(res[0]["R"]))
+    same = np.all(res[0]["sigma"] == res[1]["sigma"], axis=2)
+    assert same.mean() >= 0.9
+    assert np.max(np.abs(res[0]["R"][same] - res[1]["R"][same])) < 1e-3
