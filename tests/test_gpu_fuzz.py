@@ -1,8 +1,9 @@
-"""Randomised shapes (tools/shape_fuzz.py): odd N around the tile and segment edges,
-batches of 1..12, replica counts that pad, MFZ-BN / MFZ-CN / Positive-P, Jacobi and CG
-refits, 2-5 alternations -- fp64 bitwise against the oracle in the context's canonical
-order, fp32 finite on the same problems.  (Two longer runs of 20 + 30 cases are recorded
-in profiles/r02_shape_fuzz.log.)"""
+"""Randomised shapes (tools/shape_fuzz.py): N from 33 to 3000 around the cluster, tile and
+segment edges, batches of 1..33, replica counts that pad, MFZ-BN / MFZ-CN / Positive-P,
+Jacobi and CG refits, track_best, world-1 sharded contexts and option toggles, 2-5
+alternations -- fp64 bitwise against the oracle in the context's canonical order, fp32
+finite on the same problems.  (Longer runs, 270 cases, and the two bugs they found are
+recorded in profiles/r02_shape_fuzz.log.)"""
 import importlib.util
 import os
 

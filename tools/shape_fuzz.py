@@ -16,13 +16,18 @@ def run(cases, seed, quiet=False):
     rng = np.random.default_rng(seed)
     bad = 0
     for ci in range(cases):
-        N = int(rng.choice([513, 520, 577, 640, 1025, 1100, 1537, 2000, 2049, 3000]))
-        B = int(rng.choice([1, 2, 5, 12]))
+        N = int(rng.choice([33, 97, 200, 500, 512, 513, 520, 577, 640, 1025, 1100, 1537, 2000, 2049,
+                            3000]))
+        B = int(rng.choice([1, 2, 5, 12, 33]))
         R = int(rng.choice([1, 3, 8, 16]))
         backend = str(rng.choice(["mfz-bn", "mfz-cn", "pp"]))
         cdp = str(rng.choice(["jacobi", "cg"])) if backend != "pp" else "jacobi"
-        alpha, a = float(rng.uniform(0.35, 0.8)), float(rng.uniform(0.05, 0.3))
+        alpha, a = float(rng.uniform(0.25, 0.95)), float(rng.uniform(0.02, 0.6))
         velo, n_steps = int(rng.integers(1, 5)), int(rng.integers(20, 160))
+        track_best = bool(rng.integers(0, 2)) and backend != "pp"
+        # context variants: plain, world-1 sharded (tile sharding in fp32, row sharding in
+        # fp64: same results as plain), option toggles that must not change fp64 bits
+        variant = str(rng.choice(["plain", "plain", "sharded", "no_graphs", "no_cluster", "no_pdl"]))
         insts = [O.gen_instance(N, alpha, a, 0.01, 1000 * ci + s) for s in range(B)]
         be = O.BACKENDS[backend]
         seeds = np.array([[O.mix_seed(i.seed, be + 3 * r) for r in range(R)] for i in insts],
@@ -30,18 +35,30 @@ def run(cases, seed, quiet=False):
         kw = dict(velo=velo, n_steps=n_steps, g2=0.01) if backend == "pp" else dict(velo=velo, n_steps=n_steps)
         ghp = P.HyperParams(**kw) if backend == "pp" else P.baseline_params(**kw)
         ohp = O.HyperParams(**kw) if backend == "pp" else O.baseline_params(**kw)
-        tag = f"case {ci}: N={N} B={B} R={R} {backend} {cdp} velo={velo} steps={n_steps}"
+        tag = (f"case {ci}: N={N} B={B} R={R} {backend} {cdp} velo={velo} steps={n_steps} "
+               f"best={int(track_best)} {variant}")
         t0 = time.time()
         try:
-            with P.Context(0, "f64") as ctx:
+            def make(dt):
+                sharded = variant == "sharded" and backend != "pp"
+                ctx = P.Context(0, dt, shard=(1, 0, P.cimcs.nccl_unique_id()) if sharded else None)
+                if variant == "no_graphs":
+                    ctx.set_option("use_graphs", 0)
+                if variant == "no_cluster":
+                    ctx.set_option("cluster_loop", 0)
+                if variant == "no_pdl":
+                    ctx.set_option("pdl", 0)
+                return ctx
+            with make("f64") as ctx:
                 ctx.set_problems(insts)
                 ctx.build_coupling()
                 order = ctx.canon_order()
-                r64 = ctx.solve(R, backend, ghp, seeds, cdp=cdp)
+                r64 = ctx.solve(R, backend, ghp, seeds, cdp=cdp, track_best=track_best)
             ok = True
             for (b, r) in {(0, 0), (B - 1, R - 1)}:
                 ref = O.Problem(insts[b], O.CANON, *order).alternating_minimize(
-                    be, ohp, O.Rng(int(seeds[b, r])), cdp=(O.CDP_CG if cdp == "cg" else O.CDP_JACOBI))
+                    be, ohp, O.Rng(int(seeds[b, r])), cdp=(O.CDP_CG if cdp == "cg" else O.CDP_JACOBI),
+                    track_best=track_best)
                 if ref.get("failed"):
                     ok &= bool(r64["fail_alt"][b, r] == ref["fail_alternation"])
                 else:
@@ -50,10 +67,10 @@ def run(cases, seed, quiet=False):
             msg = "fp64 bitwise " + ("OK" if ok else "MISMATCH")
             if not ok:
                 bad += 1
-            with P.Context(0, "f32") as ctx:
+            with make("f32") as ctx:
                 ctx.set_problems(insts)
                 ctx.build_coupling()
-                r32 = ctx.solve(R, backend, ghp, seeds, cdp=cdp)
+                r32 = ctx.solve(R, backend, ghp, seeds, cdp=cdp, track_best=track_best)
             fin = bool(np.all(np.isfinite(r32["R"])))
             same = float(np.mean(np.all(r32["sigma"] == r64["sigma"], axis=2)))
             msg += f" | fp32 finite {fin} same-support {same:.2f}"
