@@ -21,3 +21,15 @@ def test_random_shapes(gpu, O, seed):
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
     assert mod.run(6, seed, quiet=True) == 0
+
+
+def test_context_reuse_sequences(gpu, O):
+    """tools/reuse_fuzz.py: one fp64 and one fp32 context driven through random sequences
+    of set_problems / solve calls whose shapes, per-instance M, replica counts, schedules
+    and backends change from call to call (cached graphs, schedules, state and pump
+    buffers must follow): every fp64 solve bitwise equal to the oracle, fp32 finite."""
+    spec = importlib.util.spec_from_file_location("reuse_fuzz",
+                                                  os.path.join(ROOT, "tools", "reuse_fuzz.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert mod.run(3, 5, quiet=True) == 0
