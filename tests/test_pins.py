@@ -110,3 +110,42 @@ def test_parallel_matrix_generator_matches_oracle(O, threads):
     ref = O.gen_instance(*args)
     assert np.array_equal(inst.A, ref.A) and np.array_equal(inst.y, ref.y)
     assert np.array_equal(inst.x_true, ref.x_true) and np.array_equal(inst.xi_true, ref.xi_true)
+
+
+def test_generator_random_parameters_three_way(O):
+    """80 random (N, alpha, a, nu, seed) including the edges (N = 1, alpha = 1 / N or 1,
+    a = 0 or 1, nu = 0): the product's host generator, the oracle and the reference's own
+    datagen.cpp agree bit for bit on A, y, x, xi and M, and reject the same inputs."""
+    from paper_2405_00366_b200 import cimcs as P
+    L = _ref()
+    rng = np.random.default_rng(0)
+    compared = 0
+    for _ in range(80):
+        N = int(rng.choice([1, 2, 3, 7, 12, 33, 100, 257]))
+        alpha = float(rng.choice([rng.uniform(0.01, 1.0), 1.0, 1.0 / N, 0.5]))
+        a = float(rng.choice([rng.uniform(0.0, 1.0), 0.0, 1.0, 1.0 / N]))
+        nu = float(rng.choice([0.0, 0.01, 1.0]))
+        seed = int(rng.integers(0, 2 ** 63))
+        try:
+            pi = P.gen_instance(N, alpha, a, nu, seed)
+        except Exception:  # noqa: BLE001
+            pi = None
+        try:
+            oi = O.gen_instance(N, alpha, a, nu, seed)
+        except Exception:  # noqa: BLE001
+            oi = None
+        assert (pi is None) == (oi is None), (N, alpha, a, nu, seed)
+        if pi is None:
+            continue
+        A = np.zeros((oi.M, N), order="F")
+        y, x = np.zeros(oi.M), np.zeros(N)
+        xi = np.zeros(N, np.int32)
+        M = C.c_int()
+        assert L.ref_gen_instance(N, alpha, a, nu, seed, A.ctypes.data, y.ctypes.data,
+                                  x.ctypes.data, xi.ctypes.data, C.byref(M)) == 0
+        assert M.value == pi.M == oi.M
+        for inst in (pi, oi):
+            assert np.array_equal(inst.A, A) and np.array_equal(inst.y, y)
+            assert np.array_equal(inst.x_true, x) and np.array_equal(inst.xi_true, xi)
+        compared += 1
+    assert compared >= 60
