@@ -119,3 +119,26 @@ def test_cdp_minimize_and_score_bitwise(O, cdp):
     assert obj == p.objective_at(out, sigma, 0.05)
     assert rm == O.rmse(out, sigma, inst.x_true, inst.xi_true)
     assert hm == O.hamming_loss(sigma, inst.xi_true)
+
+
+def test_random_small_problems_bitwise(O):
+    """40 random small problems (N 8-150, random alpha / a / nu, BN / CN / Positive-P,
+    Jacobi / CG, track_best, dt 0.01-0.1, 2-5 alternations of 10-200 steps, divergent
+    ones included): the reference's own alternating_minimize and the oracle's LITERAL
+    restatement agree bit for bit on R, sigma and the failure flag."""
+    rng = np.random.default_rng(3)
+    for _ in range(40):
+        N = int(rng.choice([8, 20, 33, 64, 100, 150]))
+        inst = O.gen_instance(N, float(rng.uniform(0.3, 0.95)), float(rng.uniform(0.05, 0.5)),
+                              float(rng.choice([0.0, 0.01, 0.1])), int(rng.integers(0, 10 ** 6)))
+        be = O.BACKENDS[str(rng.choice(["mfz-bn", "mfz-cn", "pp"]))]
+        cd = int(rng.choice([O.CDP_JACOBI, O.CDP_CG]))
+        hp = O.HyperParams(velo=int(rng.integers(1, 5)), n_steps=int(rng.integers(10, 200)),
+                           dt=float(rng.choice([0.01, 0.02, 0.1])))
+        tb = bool(rng.integers(0, 2))
+        seed = int(rng.integers(0, 2 ** 62))
+        ref = RS.alternating_minimize(inst, be, hp, seed, cdp=cd, track_best=tb)
+        orc = O.Problem(inst, O.LITERAL).alternating_minimize(be, hp, O.Rng(seed), cdp=cd,
+                                                              track_best=tb)
+        assert ref["failed"] == orc["failed"]
+        assert np.array_equal(ref["R"], orc["R"]) and np.array_equal(ref["sigma"], orc["sigma"])
