@@ -33,3 +33,13 @@ def test_context_reuse_sequences(gpu, O):
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
     assert mod.run(3, 5, quiet=True) == 0
+
+
+def test_low_level_abi_random_shapes(gpu, O):
+    """tools/abi_fuzz.py: cimcs_mfz_step, cimcs_run_cim, cimcs_cdp_minimize (Jacobi and CG)
+    and cimcs_score on random shapes of an fp64 context, bitwise against the oracle (scorer
+    scalars 1e-12 relative)."""
+    spec = importlib.util.spec_from_file_location("abi_fuzz", os.path.join(ROOT, "tools", "abi_fuzz.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert mod.run(4, 9, quiet=True) == 0
