@@ -1,4 +1,5 @@
-"""Random shapes through the low-level C-ABI calls of an fp64 context -- one fused step
+"""Random shapes through the low-level C-ABI calls of an fp64 context (and the fp32 unit
+tolerances on the same problems) -- one fused step
 (cimcs_mfz_step), a whole CIM call (cimcs_run_cim), the refit (cimcs_cdp_minimize, Jacobi
 and CG) and the scorer (cimcs_score) -- bitwise against the oracle in the context's
 canonical order (scalars of the scorer 1e-12 relative).  Run on the B200 box."""
@@ -73,6 +74,24 @@ def run(cases, seed, quiet=False):
                       and math.isclose(out["rmse"][b, r], rm, rel_tol=1e-12)
                       and out["hamming"][b, r] == O.hamming_loss(sigma[b, r], insts[b].xi_true))
                 msgs.append("score " + ("OK" if ok else "BAD")); bad += not ok
+            # the fp32 path on the same problem: field within 2e-5 of its scale, one Jacobi
+            # refit within 1e-4, score within 1e-4 (the fp32 unit tolerances)
+            with P.Context(0, "f32") as ctx:
+                ctx.set_problems(insts)
+                ctx.build_coupling()
+                pc = [O.Problem(i, O.CANON) for i in (insts[b],)][0]
+                out = ctx.mfz_step(R, backend, ghp, 0.37, 0.83, Rs, c, e)
+                h = (pc.local_field_bn(Rs[b, r], (c[b, r] > 0).astype(np.int32), hp.tau)
+                     if backend == "mfz-bn" else pc.local_field_cn(Rs[b, r], c[b, r], hp.tau))
+                eh = float(np.max(np.abs(out["h"][b, r] - h)) / np.max(np.abs(h)))
+                got = ctx.refit(R, sigma, Rp, P.HyperParams(), cdp="jacobi")
+                ref = pc.cdp(sigma[b, r], Rp[b, r], O.CDP_JACOBI, O.HyperParams())
+                er = float(np.max(np.abs(got[b, r] - ref)) / max(np.max(np.abs(ref)), 1e-30))
+                sc = ctx.score(R, Rp, sigma, 0.05)
+                es = abs(sc["objective"][b, r] - obj) / max(abs(obj), 1e-30)
+                ok = eh < 2e-5 and er < 1e-4 and es < 1e-4
+                msgs.append(f"f32 h {eh:.1e} refit {er:.1e} obj {es:.1e} " + ("OK" if ok else "BAD"))
+                bad += not ok
         except Exception as ex:  # noqa: BLE001
             msgs.append("ERROR " + str(ex)[:140]); bad += 1
         if not quiet or any("OK" not in m for m in msgs):
