@@ -357,7 +357,16 @@ class Context:
                                             hz.ctypes.data, D.ctypes.data))
         return G, hz, D
 
+    def _need(self, R: int):
+        """The reference raises input_error for an empty problem / replica set (types.hpp:16-33);
+        checked here before any host array is shaped."""
+        if getattr(self, "B", 0) < 1:
+            raise InputError("no problems set (set_problems / set_mri_problem first)")
+        if not 1 <= int(R) <= 16:
+            raise InputError("R must be in [1, 16]")
+
     def mfz_step(self, R: int, backend: str, hp: HyperParams, eta: float, p: float, Rsig, c, e):
+        self._need(R)
         B, N = self.B, self.N
         Rs, cc, ee = (_traj(x, B, R, N) for x in (Rsig, c, e))
         co, eo, ho = (np.zeros((B, R, N)) for _ in range(3))
@@ -372,6 +381,7 @@ class Context:
         return dict(c=co, e=eo, h=ho, fail_index=fi)
 
     def run_cim(self, R: int, backend: str, hp: HyperParams, eta: float, Rsig, c0):
+        self._need(R)
         B, N = self.B, self.N
         Rs, c0 = _traj(Rsig, B, R, N), _traj(c0, B, R, N)
         co, eo = np.zeros((B, R, N)), np.zeros((B, R, N))
@@ -389,6 +399,7 @@ class Context:
 
     def run_pp(self, R: int, hp: HyperParams, eta: float, Rsig, seeds):
         """run_pp (solver_pp.cpp:100-132) for every trajectory from its stream seed."""
+        self._need(R)
         B, N = self.B, self.N
         Rs = _traj(Rsig, B, R, N)
         sd = np.ascontiguousarray(seeds, np.uint64).reshape(B * R)
@@ -411,6 +422,7 @@ class Context:
         if cdp not in ("jacobi", "cg"):
             raise ConfigError("cdp must be 'jacobi' or 'cg'")
         hp = hp or HyperParams()
+        self._need(R)
         B, N = self.B, self.N
         s = _traj(sigma, B, R, N, np.int32)
         rp = _traj(R_prev, B, R, N)
@@ -423,6 +435,7 @@ class Context:
         return (out, its) if return_iterations else out
 
     def score(self, R: int, Rsig, sigma, lam: float):
+        self._need(R)
         B, N = self.B, self.N
         rs = _traj(Rsig, B, R, N)
         s = _traj(sigma, B, R, N, np.int32)
@@ -437,6 +450,7 @@ class Context:
             raise ConfigError(f"unknown backend '{backend}' (use mfz-bn, mfz-cn or pp)")
         if cdp not in ("jacobi", "cg"):
             raise ConfigError("cdp must be 'jacobi' or 'cg'")
+        self._need(R)
         B, N = self.B, self.N
         sd = np.ascontiguousarray(seeds, np.uint64).reshape(B * R)
         ri = None if R_init is None else _traj(R_init, B, R, N)

@@ -71,3 +71,30 @@ def test_no_gpu_context_fails_loudly():
     from paper_2405_00366_b200 import cimcs
     with pytest.raises((cimcs.CudaError, cimcs.ConfigError)):
         cimcs.Context(0, "f64")
+
+
+def test_python_mirror_rejects_empty_problem_and_bad_R():
+    """The Python mirror raises the reference's InputError (types.hpp:16-33) before shaping
+    any host array when no problem is set or R is outside [1, 16] (no GPU call is made)."""
+    import numpy as np
+
+    from paper_2405_00366_b200 import cimcs as P
+
+    class Dummy(P.Context):
+        def __init__(self):  # no device context: only the host-side checks are exercised
+            self.B = self.N = 0
+
+        def close(self):
+            pass
+
+    d = Dummy()
+    hp = P.baseline_params(velo=1, n_steps=10)
+    import pytest
+    with pytest.raises(P.InputError):
+        d.solve(2, "mfz-bn", hp, np.array([[1, 2]], np.uint64))
+    d.B, d.N = 2, 8
+    for R in (0, 17):
+        with pytest.raises(P.InputError):
+            d.solve(R, "mfz-bn", hp, np.zeros((2, max(R, 1)), np.uint64))
+        with pytest.raises(P.InputError):
+            d.score(R, np.zeros((2, 1, 8)), np.zeros((2, 1, 8), np.int32), 0.1)
