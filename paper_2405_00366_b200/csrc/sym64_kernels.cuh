@@ -479,6 +479,7 @@ __global__ void __maxnreg__(80) sym64_update_kernel(Sym64Args sa) {
         sy_pdl_wait();
     }
     if (tl) tl[1] = sy_gtime();
+    sy_pdl_trigger();  // early: dependents launch once every CTA of this grid has started
     double Rv[4] = {0, 0, 0, 0}, cv[4] = {0, 0, 0, 0}, ev[4] = {0, 0, 0, 0};
     double st_D = 0.0, st_hz = 0.0;
     if constexpr (MODE == EPI_STEP_BN || MODE == EPI_STEP_CN) {
