@@ -261,10 +261,13 @@ def test_item_flags_do_not_change_results(gpu, O, backend):
 def test_update_runs_under_the_tile_kernel(gpu, O):
     """The defining property of the item flags, from the per-CTA %globaltimer stamps
     (option timeline): with the flags on, update CTAs of early instances pass their
-    wait while tile CTAs are still working (48 instances x 16 replicas, N = 1100: 288
-    items on 148 CTAs); with the flags off every update CTA waits for the whole tile
-    grid.  Stamps are ordered entry <= past the wait <= exit either way."""
-    N, B, R = 1100, 48, 16
+    wait while tile CTAs are still working (40 instances x 16 replicas, N = 1537: 400
+    items on 148 CTAs, so a CTA's first item -- an early instance's -- ends well before the
+    launch does; with a shape whose largest item spans the whole launch, e.g. N = 1100,
+    every instance completes at the end and there is nothing to overlap); with the flags
+    off every update CTA waits for the whole tile grid.  Stamps are ordered entry <= past
+    the wait <= exit either way."""
+    N, B, R = 1537, 40, 16
     insts = [O.gen_instance(N, 0.5, 0.1, 0.01, 100 + s) for s in range(B)]
     rng = np.random.default_rng(5)
     Rs = np.abs(rng.normal(size=(B, R, N))) * 0.1
@@ -287,4 +290,4 @@ def test_update_runs_under_the_tile_kernel(gpu, O):
         assert np.all(upd[:, 0] <= upd[:, 1]) and np.all(upd[:, 1] <= upd[:, 2])
         first_pass[ov], last_tile[ov] = upd[:, 1].min(), tile[:, 2].max()
     assert first_pass[0] >= last_tile[0]  # no flags: after the whole tile grid
-    assert first_pass[1] < last_tile[1]   # flags: under the tile kernel
+    assert first_pass[1] < last_tile[1] - 5000  # flags: >= 5 us before the last tile item
